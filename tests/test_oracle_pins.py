@@ -1,0 +1,409 @@
+"""Pins of the CPU oracle against things other than itself (runs without a GPU).
+
+Each test names what fixes the expected value: SPEC/PAPER worked examples (tests/golden/),
+brute-force dense convolution (torch CPU fp64, a library routine, and a numpy definition),
+fp64 autograd, finite differences, full Python sorts, closed forms and invariants.
+"""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as ora
+from synth import COO, Filter, uniform_map, sparse_filter, bias_vector, grad_values, mnist_like
+from tests._brute import (coo_to_dense, filter_to_dense, torch_xcorr, shift_xcorr, dense_to_sorted,
+                          brute_topk, masked_conv_grads)
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+U24 = 2.0 ** -24
+
+
+def _coo_from_points(dims, entries, batch=1, channels=1):
+    V = int(np.prod(dims))
+    keys = np.array(sorted(int(np.ravel_multi_index(p, dims)) for p, _ in entries), np.uint64)
+    d = {int(np.ravel_multi_index(p, dims)): v for p, v in entries}
+    vals = np.array([d[int(k)] for k in keys], np.float32)
+    assert V > 0
+    return COO(batch, channels, tuple(dims), keys, vals)
+
+
+# ----------------------------------------------------------------- golden examples
+@pytest.mark.parametrize("ex", GOLD["key_codec"], ids=lambda e: e["source"][:6])
+def test_key_codec_golden(ex):
+    assert ora.encode_key(ex["index"], ex["dims"], ex["channels"]) == ex["key"]
+    assert ora.decode_key(ex["key"], ex["dims"], ex["batch"], ex["channels"]) == tuple(ex["index"])
+
+
+def test_key_codec_roundtrip_vs_numpy():
+    rng = np.random.default_rng(0)
+    dims, B, Cc = (5, 7, 3), 3, 4
+    for _ in range(200):
+        idx = [int(rng.integers(B)), int(rng.integers(Cc))] + [int(rng.integers(d)) for d in dims]
+        key = ora.encode_key(idx, dims, Cc)
+        assert key == int(np.ravel_multi_index(tuple(idx), (B, Cc) + dims))  # library routine
+        assert ora.decode_key(key, dims, B, Cc) == tuple(idx)
+
+
+@pytest.mark.parametrize("ex", GOLD["get_update_id"], ids=lambda e: e["source"][:6])
+def test_get_update_id_golden(ex):
+    got = ora.get_update_id(ex["id"], ex["fid"], ex["dims"], ex["ksize"])
+    assert got == (tuple(ex["uid"]) if ex["uid"] is not None else None)
+
+
+@pytest.mark.parametrize("ex", GOLD["k_select"], ids=lambda e: e["source"][:6])
+def test_kselect_golden(ex):
+    x = COO(1, 1, (len(ex["values"]),), np.arange(len(ex["values"]), dtype=np.uint64),
+            np.array(ex["values"], np.float32))
+    attn = ora.ATTN_RAW if ex["attn"] == "raw" else ora.ATTN_MAGNITUDE
+    _, yv, _ = ora.topk(x, attn, ex["k"])
+    np.testing.assert_array_equal(np.sort(yv), np.sort(np.array(ex["kept"], np.float32)))
+
+
+@pytest.mark.parametrize("ex", GOLD["conv"], ids=lambda e: e["source"][:6])
+def test_conv_golden(ex):
+    dims = tuple(ex["dims"])
+    x = _coo_from_points(dims, [(tuple(int(t) for t in k.split(",")), v) for k, v in ex["x"].items()])
+    K = int(np.prod(ex["ksize"]))
+    w = Filter(1, 1, tuple(ex["ksize"]), np.arange(K, dtype=np.uint64), np.ones(K, np.float32))
+    yk, yv, _, _ = ora.conv_fwd(x, w, None)
+    want = {int(np.ravel_multi_index(tuple(int(t) for t in k.split(",")), dims)): v for k, v in ex["y"].items()}
+    assert yk.tolist() == sorted(want)
+    np.testing.assert_array_equal(yv, np.array([want[k] for k in sorted(want)], np.float32))
+
+
+def test_identity_1x1_conv():
+    """1x1 filter with weight 1.0 on the diagonal ic == oc, zero bias -> output == input."""
+    x = uniform_map(2, 3, (6, 5), 0.3, 11)
+    ks = (1, 1)
+    keys = np.array([(oc * 3 + oc) for oc in range(3)], np.uint64)
+    w = Filter(3, 3, ks, keys, np.ones(3, np.float32))
+    yk, yv, _, _ = ora.conv_fwd(x, w, None)
+    np.testing.assert_array_equal(yk, x.keys)
+    np.testing.assert_array_equal(yv, x.values)
+
+
+@pytest.mark.parametrize("ex", GOLD["maxpool"], ids=lambda e: e["source"][:6])
+def test_maxpool_golden(ex):
+    x = COO(1, 1, tuple(ex["dims"]), np.array([e[0] for e in ex["x"]], np.uint64),
+            np.array([e[1] for e in ex["x"]], np.float32))
+    yk, yv, am = ora.maxpool(x, ex["stride"])
+    assert yk.tolist() == [e[0] for e in ex["y"]]
+    assert yv.tolist() == [e[1] for e in ex["y"]]
+    assert am.tolist() == ex["argmax"]
+
+
+@pytest.mark.parametrize("ex", GOLD["relu"], ids=lambda e: e["source"][:6])
+def test_relu_golden(ex):
+    n = len(ex["values"])
+    x = COO(1, 1, (n,), np.arange(n, dtype=np.uint64), np.array(ex["values"], np.float32))
+    _, yv, _ = ora.relu(x)
+    assert yv.tolist() == ex["kept"]
+
+
+# --------------------------------------------------------- forward vs brute force
+CASES = [
+    # ndim dims, batch, c_in, c_out, ksize, rho_d, rho_f
+    ((9,), 2, 2, 3, (3,), 0.3, 0.7),
+    ((8, 8), 2, 2, 3, (3, 3), 0.2, 0.5),   # S:170 shape
+    ((7, 10), 3, 1, 4, (5, 3), 0.15, 0.8),
+    ((6, 5, 7), 2, 3, 2, (3, 3, 3), 0.1, 0.5),
+    ((5, 6, 4), 1, 2, 2, (1, 3, 5), 0.3, 1.0),
+    ((12, 12, 12), 2, 2, 2, (3, 3, 3), 0.03, 0.5),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "x".join(map(str, c[0])) + f"_k{'x'.join(map(str, c[4]))}")
+@pytest.mark.parametrize("values", ["continuous", "dyadic"])
+def test_fwd_unbounded_vs_dense_xcorr(case, values):
+    """Alg. 1 without attention == dense SAME cross-correlation read on the structural support
+    (brute force: torch conv fp64 and the numpy shift definition)."""
+    dims, B, ci, co, ks, rd, rf = case
+    x = uniform_map(B, ci, dims, rd, 100 + len(dims), values=values)
+    w = sparse_filter(ci, co, ks, rf, 7, values=values)
+    bias = bias_vector(co, 3, values=values)
+    yk, yv, ya, macs = ora.conv_fwd(x, w, bias, with_abs=True)
+    Xd, Xm = coo_to_dense(x)
+    Wd, Wm = filter_to_dense(w)
+    Yd = torch_xcorr(Xd, Wd)
+    np.testing.assert_allclose(shift_xcorr(Xd, Wd), Yd, rtol=1e-12, atol=1e-12)
+    S = torch_xcorr(Xm.astype(np.float64), Wm.astype(np.float64)) > 0.5  # structural support (P1)
+    sk, sv = dense_to_sorted(Yd + bias.astype(np.float64).reshape((1, -1) + (1,) * len(dims)), S)
+    np.testing.assert_array_equal(yk, sk)
+    # one fp64 -> fp32 rounding at most (different summation order in fp64)
+    err = np.abs(yv.astype(np.float64) - sv)
+    assert np.all(err <= U24 * np.abs(sv) + 1e-12 * ya), err.max()
+    if values == "dyadic":
+        np.testing.assert_array_equal(yv, sv.astype(np.float32))
+    # macs = number of in-bounds (input, weight) pairs (Eq. (1) first term)
+    pairs = torch_xcorr(Xm.astype(np.float64), Wm.astype(np.float64)).sum()
+    assert macs == int(round(pairs))
+
+
+def test_fwd_4d_vs_shift_definition():
+    x = uniform_map(1, 2, (4, 3, 5, 4), 0.2, 5)
+    w = sparse_filter(2, 2, (3, 1, 3, 3), 0.6, 5)
+    yk, yv, _, _ = ora.conv_fwd(x, w, None)
+    Xd, Xm = coo_to_dense(x)
+    Wd, Wm = filter_to_dense(w)
+    S = shift_xcorr(Xm.astype(np.float64), Wm.astype(np.float64)) > 0.5
+    sk, sv = dense_to_sorted(shift_xcorr(Xd, Wd), S)
+    np.testing.assert_array_equal(yk, sk)
+    np.testing.assert_allclose(yv, sv, rtol=2 * U24, atol=1e-12)
+
+
+def test_library_special_case_dense():
+    """rho_d = rho_f = 1, no attention, zero bias: equals torch.nn.functional.conv3d (fp64)
+    at every grid point."""
+    x = uniform_map(2, 2, (5, 4, 6), 1.0, 9)
+    w = sparse_filter(2, 3, (3, 3, 3), 1.0, 9)
+    yk, yv, _, _ = ora.conv_fwd(x, w, None)
+    Y = torch_xcorr(*[coo_to_dense(x)[0], filter_to_dense(w)[0]])
+    assert yk.shape[0] == Y.size
+    np.testing.assert_allclose(yv, Y.reshape(-1).astype(np.float32), rtol=2 * U24, atol=1e-7)
+
+
+def test_macs_closed_form_dense():
+    """Dense input, dense filter: in-bounds pairs = b*c_in*c_out*prod_d(s_f*n_d - c_d*(c_d+1))."""
+    dims, ks = (6, 7, 5), (3, 5, 3)
+    B, ci, co = 2, 2, 3
+    x = uniform_map(B, ci, dims, 1.0, 4)
+    w = sparse_filter(ci, co, ks, 1.0, 4)
+    _, _, _, macs = ora.conv_fwd(x, w, None)
+    per = 1
+    for n, s in zip(dims, ks):
+        c = s // 2
+        per *= s * n - c * (c + 1)
+    assert macs == B * ci * co * per
+
+
+def test_macs_linear_in_densities():
+    """Eq. (1): the MAC term is linear in rho_d and rho_f (expected value; interior-dominated grid)."""
+    base = None
+    for rd in (0.02, 0.04):
+        for rf in (0.25, 0.5):
+            x = uniform_map(2, 2, (24, 24, 24), rd, 21)
+            w = sparse_filter(2, 2, (3, 3, 3), rf, 21)
+            _, _, _, macs = ora.conv_fwd(x, w, None)
+            pred = x.nnz * w.nnz / 2  # c_out-average of weights per input channel
+            ratio = macs / pred
+            base = ratio if base is None else base
+            assert abs(ratio - base) < 0.03 * base
+
+
+def test_fill_in_uniform_3d():
+    """Fig. 2: uniform data under a dense 3x3x3 filter fills the interior to
+    1 - (1 - rho)^27 (independent positions)."""
+    rho = 0.02
+    x = uniform_map(1, 1, (40, 40, 40), rho, 31)
+    w = sparse_filter(1, 1, (3, 3, 3), 1.0, 31)
+    yk, _, _, _ = ora.conv_fwd(x, w, None)
+    m = np.zeros(40 ** 3, bool)
+    m[yk.astype(np.int64)] = True
+    interior = m.reshape(40, 40, 40)[1:-1, 1:-1, 1:-1].mean()
+    # sampling without replacement: P(empty neighbourhood) ~ (1 - rho)^27
+    assert abs(interior - (1 - (1 - rho) ** 27)) < 0.01
+
+
+# ------------------------------------------------------------------------ attention
+@pytest.mark.parametrize("attn", ["magnitude", "raw"])
+@pytest.mark.parametrize("values", ["continuous", "dyadic"])
+def test_fused_attention_vs_full_sort(attn, values):
+    """Alg. 1 with attention == brute-force full sort of the exact (unbounded) output per (b, oc),
+    rule (score desc, key asc) (readings R5-R7); plus the paper's invariants."""
+    dims = (10, 9, 8)
+    x = uniform_map(2, 2, dims, 0.05, 41, values=values)
+    w = sparse_filter(2, 3, (3, 3, 3), 0.5, 41, values=values)
+    bias = bias_vector(3, 41, values=values)
+    V = int(np.prod(dims))
+    k = int(0.05 * V)
+    a = ora.ATTN_MAGNITUDE if attn == "magnitude" else ora.ATTN_RAW
+    fk, fv, _, _ = ora.conv_fwd(x, w, bias)
+    yk, yv, _, _ = ora.conv_fwd(x, w, bias, attn=a, k=k)
+    bk, bv = brute_topk(fk, fv, V, k, attn)
+    np.testing.assert_array_equal(yk, bk)
+    np.testing.assert_array_equal(yv, bv)
+    # invariants: nnz(b, oc) <= k (density bound rho_up*V), dominance
+    seg = (yk // np.uint64(V)).astype(np.int64)
+    assert np.bincount(seg).max() <= k
+    sc = (lambda v: np.abs(v)) if attn == "magnitude" else (lambda v: v)
+    fseg = (fk // np.uint64(V)).astype(np.int64)
+    kept = set(yk.tolist())
+    for s in np.unique(fseg):
+        m = fseg == s
+        keep = np.array([kk in kept for kk in fk[m].tolist()])
+        if (~keep).any():
+            assert sc(fv[m][keep]).min() >= sc(fv[m][~keep]).max()
+
+
+def test_attention_k_ge_support_is_identity():
+    x = uniform_map(1, 1, (6, 6), 0.1, 5)
+    w = sparse_filter(1, 2, (3, 3), 1.0, 5)
+    fk, fv, _, _ = ora.conv_fwd(x, w, None)
+    yk, yv, _, _ = ora.conv_fwd(x, w, None, attn=ora.ATTN_MAGNITUDE, k=36)
+    np.testing.assert_array_equal(fk, yk)
+    np.testing.assert_array_equal(fv, yv)
+
+
+@pytest.mark.parametrize("attn", ["magnitude", "raw"])
+def test_topk_standalone_vs_full_sort(attn):
+    x = uniform_map(3, 2, (11, 13), 0.4, 8, values="dyadic")  # many exact ties
+    V = 11 * 13
+    k = 17
+    a = ora.ATTN_MAGNITUDE if attn == "magnitude" else ora.ATTN_RAW
+    yk, yv, src = ora.topk(x, a, k)
+    bk, bv = brute_topk(x.keys, x.values, V, k, attn)
+    np.testing.assert_array_equal(yk, bk)
+    np.testing.assert_array_equal(yv, bv)
+    np.testing.assert_array_equal(x.keys[src], yk)
+
+
+def test_topk_negative_zero_ties():
+    """R7: -0 and +0 are the same score; ties resolved by smaller key."""
+    vals = np.array([0.0, -0.0, 1.0, -0.0, 0.0], np.float32)
+    vals[1] = -0.0
+    x = COO(1, 1, (5,), np.arange(5, dtype=np.uint64), vals)
+    yk, _, _ = ora.topk(x, ora.ATTN_MAGNITUDE, 3)
+    assert yk.tolist() == [0, 1, 2]
+    yk, _, _ = ora.topk(x, ora.ATTN_RAW, 2)
+    assert yk.tolist() == [0, 2]
+
+
+# ------------------------------------------------------------------------ backward
+@pytest.mark.parametrize("dims,ks", [((9, 8), (3, 3)), ((6, 5, 7), (3, 3, 3)), ((11,), (5,))])
+@pytest.mark.parametrize("values", ["continuous", "dyadic"])
+def test_bwd_vs_autograd(dims, ks, values):
+    """Alg. 2 / Eqs. (3)-(4) == fp64 autograd of sum_kept dy*y, read at stored inputs/weights
+    (P5). dbias == sum of dy per channel."""
+    x = uniform_map(2, 2, dims, 0.25, 61, values=values)
+    w = sparse_filter(2, 3, ks, 0.6, 61, values=values)
+    bias = bias_vector(3, 61, values=values)
+    V = int(np.prod(dims))
+    yk, yv, _, _ = ora.conv_fwd(x, w, bias, attn=ora.ATTN_MAGNITUDE, k=max(1, V // 4))
+    dy = grad_values(yk.shape[0], 61, values=values)
+    dx, dw, db, dxa, dwa = ora.conv_bwd(x, w, yk, dy, with_abs=True)
+    gX, gW, gb = masked_conv_grads(x, w, bias, yk, dy)
+    ref_dx = gX.reshape(-1)[x.keys.astype(np.int64)]
+    ref_dw = gW.reshape(-1)[w.keys.astype(np.int64)]
+    assert np.all(np.abs(dx - ref_dx) <= U24 * np.abs(ref_dx) + 1e-12 * dxa)
+    assert np.all(np.abs(dw - ref_dw) <= U24 * np.abs(ref_dw) + 1e-12 * dwa)
+    np.testing.assert_allclose(db, gb, rtol=2 * U24, atol=1e-12)
+    if values == "dyadic":
+        np.testing.assert_array_equal(dx, ref_dx.astype(np.float32))
+        np.testing.assert_array_equal(dw, ref_dw.astype(np.float32))
+    # Eq. (3)/(4) masking: the dense autograd gradient is generally nonzero at non-stored inputs,
+    # the sparse rule assigns it no storage at all (fixed shape, P:135 (i)).
+    assert dx.shape == (x.nnz,) and dw.shape == (w.nnz,)
+
+
+def test_bwd_finite_differences():
+    """Central differences (step 1e-4, rtol 1e-3) of L = sum dy*y (unbounded, so the
+    output set is fixed), perturbing only stored entries."""
+    x = uniform_map(1, 2, (6, 6), 0.3, 71)
+    w = sparse_filter(2, 2, (3, 3), 0.7, 71)
+    bias = bias_vector(2, 71)
+    yk, _, _, _ = ora.conv_fwd(x, w, bias)
+    dy = grad_values(yk.shape[0], 71)
+    dx, dw, db, _, _ = ora.conv_bwd(x, w, yk, dy)
+
+    def L(xv, wv, bv):
+        xx = COO(x.batch, x.channels, x.dims, x.keys, xv.astype(np.float32))
+        ww = Filter(w.c_in, w.c_out, w.ksize, w.keys, wv.astype(np.float32))
+        k2, v2, _, _ = ora.conv_fwd(xx, ww, bv.astype(np.float32))
+        assert np.array_equal(k2, yk)
+        return float(np.dot(v2.astype(np.float64), dy.astype(np.float64)))
+
+    h = 1e-2  # values are O(1); fp32 forward -> use a larger step, relative check below
+    for i in range(0, x.nnz, max(1, x.nnz // 10)):
+        e = np.zeros(x.nnz)
+        e[i] = h
+        fd = (L(x.values + e, w.values, bias) - L(x.values - e, w.values, bias)) / (2 * h)
+        assert abs(fd - dx[i]) <= 1e-3 * max(1.0, abs(dx[i]))
+    for j in range(0, w.nnz, max(1, w.nnz // 10)):
+        e = np.zeros(w.nnz)
+        e[j] = h
+        fd = (L(x.values, w.values + e, bias) - L(x.values, w.values - e, bias)) / (2 * h)
+        assert abs(fd - dw[j]) <= 1e-3 * max(1.0, abs(dw[j]))
+
+
+def test_bwd_zero_dy():
+    x = uniform_map(1, 2, (7, 7), 0.3, 3)
+    w = sparse_filter(2, 2, (3, 3), 0.5, 3)
+    yk, _, _, _ = ora.conv_fwd(x, w, None)
+    dx, dw, db, _, _ = ora.conv_bwd(x, w, yk, np.zeros(yk.shape[0], np.float32))
+    assert not dx.any() and not dw.any() and not db.any()
+
+
+def test_bwd_identity_1x1():
+    """identity 1x1 -> dx = dy restricted to input keys; dw[diag] = sum val*g."""
+    x = uniform_map(2, 2, (5, 5), 0.4, 13)
+    w = Filter(2, 2, (1, 1), np.array([0, 3], np.uint64), np.ones(2, np.float32))
+    yk, _, _, _ = ora.conv_fwd(x, w, None)
+    np.testing.assert_array_equal(yk, x.keys)
+    dy = grad_values(yk.shape[0], 13)
+    dx, dw, _, _, _ = ora.conv_bwd(x, w, yk, dy)
+    np.testing.assert_array_equal(dx, dy)
+    V = 25
+    ch = ((x.keys // np.uint64(V)) % np.uint64(2)).astype(np.int64)
+    for c in range(2):
+        want = np.sum(x.values[ch == c].astype(np.float64) * dy[ch == c].astype(np.float64))
+        assert abs(dw[c] - want) <= 1e-6 * max(1.0, abs(want))
+
+
+# ------------------------------------------------------------------- relu and pooling
+def test_relu_definition_and_idempotence():
+    x = uniform_map(2, 3, (9, 9), 0.3, 17)
+    yk, yv, src = ora.relu(x)
+    m = x.values > 0
+    np.testing.assert_array_equal(yk, x.keys[m])
+    np.testing.assert_array_equal(yv, x.values[m])
+    np.testing.assert_array_equal(src, np.nonzero(m)[0])
+    y = COO(x.batch, x.channels, x.dims, yk, yv)
+    yk2, yv2, _ = ora.relu(y)
+    np.testing.assert_array_equal(yk2, yk)
+
+
+@pytest.mark.parametrize("dims,stride", [((8, 8), (2, 2)), ((7, 9), (2, 3)), ((6, 6, 6), (2, 2, 2)), ((5, 7, 4), (2, 3, 2))])
+def test_maxpool_vs_dense(dims, stride):
+    """§3.3 pooling == dense max-pool (torch, -inf for absent entries, ceil mode) on occupied
+    clusters; argmax == brute-force first maximum in key order."""
+    x = uniform_map(2, 2, dims, 0.3, 23, values="dyadic")  # dyadic: exact ties occur
+    yk, yv, am = ora.maxpool(x, stride)
+    Xd, Xm = coo_to_dense(x)
+    Xi = np.where(Xm, Xd, -np.inf)
+    nd = len(dims)
+    pool = {2: torch.nn.functional.max_pool2d, 3: torch.nn.functional.max_pool3d}[nd]
+    P = pool(torch.from_numpy(Xi), kernel_size=stride, stride=stride, ceil_mode=True).numpy()
+    occ = np.isfinite(P)
+    pk, pv = dense_to_sorted(P, occ)
+    np.testing.assert_array_equal(yk, pk)
+    np.testing.assert_array_equal(yv, pv.astype(np.float32))
+    # argmax: smallest input index attaining the cluster max
+    V = int(np.prod(dims))
+    odims = tuple(-(-d // s) for d, s in zip(dims, stride))
+    best = {}
+    for i, (kk, v) in enumerate(zip(x.keys.tolist(), x.values.tolist())):
+        seg, sp = divmod(kk, V)
+        p = np.unravel_index(sp, dims)
+        q = tuple(pi // si for pi, si in zip(p, stride))
+        pkk = seg * int(np.prod(odims)) + int(np.ravel_multi_index(q, odims))
+        if pkk not in best or v > best[pkk][0]:
+            best[pkk] = (v, i)
+    assert am.tolist() == [best[k][1] for k in yk.tolist()]
+
+
+def test_scatter_grad():
+    src = np.array([4, 0, 2], np.int64)
+    dy = np.array([1.5, -2.0, 3.0], np.float32)
+    dx = ora.scatter_grad(src, dy, 6)
+    assert dx.tolist() == [-2.0, 0.0, 3.0, 0.0, 1.5, 0.0]
+
+
+# --------------------------------------------------------------------------- inputs
+def test_mnist_like_density_matches_paper():
+    """thresholded MNIST has mean density 0.23."""
+    m = mnist_like(400, 5)
+    assert abs(m.nnz / 400 / 784 - 0.23) < 0.02
