@@ -1,0 +1,217 @@
+/*
+ * spconv.h — C-ABI of libspconv.so, the B200 (sm_100a) hot path of
+ * Hackel et al., arXiv 1801.10585, "Inference, Learning and Attention Mechanisms that
+ * Exploit and Preserve Sparsity in Convolutional Networks".
+ *
+ * Citations: "P:n" = PAPER.md line n (the paper text); readings R1..R13 are in DESIGN.md.
+ *
+ * ----------------------------------------------------------------------------------------
+ * Data format (reading R11)
+ *   A sparse feature map is a coordinate list: strictly increasing 64-bit keys and fp32
+ *   values in separate device arrays ("indices ... and the corresponding data entries in
+ *   separate tensors"; "64 bit keys, and 32 bit depth for feature maps").
+ *     key = ((b * channels + c) * V + row_major(p)),   V = prod(dims),
+ *   with the first spatial dimension most significant, so keys sort by batch, then channel
+ *   ("sorted w.r.t. batches and within each batch w.r.t. channels").
+ *   A filter bank is a coordinate list over (oc, ic, delta):
+ *     key = ((oc * c_in + ic) * prod(ksize) + row_major(delta)), strictly increasing
+ *   ("sorted w.r.t. the output channels and within each channel w.r.t. the input channels").
+ *
+ * Conventions (all functions)
+ *   - Every array argument is a DEVICE pointer; the descriptor structs themselves, stride[]
+ *     and k are HOST values. Calls are stream-ordered and asynchronous: they enqueue work on
+ *     `stream` and return without synchronising (except SPC_VALIDATE=1, see Errors).
+ *   - Ownership: every buffer (inputs, outputs, workspace, nnz words) belongs to the caller and
+ *     must stay alive until the enqueued work completes. The library keeps no pointer after
+ *     returning and allocates no device memory; it is re-entrant for distinct workspaces.
+ *   - Sizes: an input map's exact nnz is *nnz_dev when nnz_dev != NULL (a device int64; `nnz`
+ *     is then an upper bound used for grid sizing), else `nnz`. Outputs write their exact
+ *     count to *nnz_dev (device) so chained layers never need a host sync.
+ *   - Spatial rank 1..3 (SPC_MAX_NDIM); odd kernel sizes; prod(ksize) <= 1024.
+ *   - Convolution is cross-correlation with SAME zero padding and stride 1 (readings R1, R2).
+ *   - Workspace: query the byte count with the matching *_query function, pass a device
+ *     buffer of at least that many bytes (256-byte aligned).
+ *
+ * Errors
+ *   Host-checkable problems (NULL pointers, ndim out of range, even ksize, c_in mismatch,
+ *   k < 1 with attention on, capacity or workspace too small) return synchronously with
+ *   nothing enqueued. With the environment variable SPC_VALIDATE=1 every input map is also
+ *   checked on the device (strictly increasing, in range); that check synchronises the
+ *   stream and returns SPC_ERR_UNSORTED on failure. Without it, unsorted or duplicate keys
+ *   give unspecified values but every write stays within the output capacity. CUDA launch
+ *   failures return SPC_ERR_CUDA.
+ * ----------------------------------------------------------------------------------------
+ */
+#ifndef SPCONV_H
+#define SPCONV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* cudaStream_t;
+
+#define SPC_MAX_NDIM 3
+
+typedef enum {
+    SPC_OK = 0,
+    SPC_ERR_INVALID_ARG = 1,
+    SPC_ERR_SHAPE = 2,
+    SPC_ERR_CAPACITY = 3,
+    SPC_ERR_WORKSPACE = 4,
+    SPC_ERR_UNSORTED = 5,
+    SPC_ERR_UNSUPPORTED = 6,
+    SPC_ERR_CUDA = 7
+} spc_status_t;
+
+/* Attention variants: (i) raw responses, (ii) absolute values. */
+typedef enum {
+    SPC_ATTN_NONE = 0,      /* exact convolution, no k-selection                      */
+    SPC_ATTN_MAGNITUDE = 1, /* variant (ii): keep the k largest |y|                    */
+    SPC_ATTN_RAW = 2        /* variant (i):  keep the k largest y                      */
+} spc_attn_t;
+
+/* Input sparse feature map. */
+typedef struct {
+    int32_t ndim;                  /* spatial rank k of Eq. (1), 1..3                    */
+    int64_t batch;                 /* b                                                  */
+    int64_t channels;              /* c                                                  */
+    int64_t dims[SPC_MAX_NDIM];    /* s_d per spatial dim (first = most significant)     */
+    int64_t nnz;                   /* exact count, or upper bound if nnz_dev != NULL     */
+    const int64_t* nnz_dev;        /* device: exact count, or NULL                       */
+    const uint64_t* keys;          /* device [nnz], strictly increasing                  */
+    const float* values;           /* device [nnz]                                       */
+} spc_map_t;
+
+/* Output sparse feature map (shape implied by the operation). */
+typedef struct {
+    int64_t capacity;              /* entries available in keys/values (and index arrays) */
+    uint64_t* keys;                /* device [capacity]                                   */
+    float* values;                 /* device [capacity]                                   */
+    int64_t* nnz_dev;              /* device: receives the exact output count             */
+} spc_map_out_t;
+
+/* Sparse filter bank; nnz entries = the unpruned weights (rho_f of Eq. (1)). */
+typedef struct {
+    int32_t ndim;
+    int64_t c_in, c_out;
+    int64_t ksize[SPC_MAX_NDIM];   /* odd, s_f per spatial dim                            */
+    int64_t nnz;
+    const uint64_t* keys;          /* device [nnz], strictly increasing                   */
+    const float* values;           /* device [nnz]                                        */
+} spc_filter_t;
+
+const char* spc_version(void);
+const char* spc_status_string(spc_status_t s);
+
+/* ------------------------------------------------------------------------------------
+ * sparse_conv_fwd — Direct Sparse Convolution with Attention, Alg. 1 (§3.1-3.2).
+ *   For every (b, oc): accumulate val*fval at uid = id - fid + centre over all stored inputs
+ *   and stored weights; the pre-attention set is the structural support S(b,oc) of
+ *   those updates (reading R3); bias[oc] is added on S only (R4); if attn !=
+ *   NONE and |S| > k, keep the k entries with the largest score (|y| or y), ties by smaller
+ *   spatial key (R5-R7); write keys ((b*c_out + oc)*V + p) in key order.
+ *   x: input map (channels == w->c_in); w: filter; bias: device [c_out] or NULL (zero);
+ *   y: output, capacity >= spc_conv_fwd_query's out_capacity = batch*c_out*min(k, V)
+ *   (attention) or batch*c_out*V (none); output shape (batch, c_out, dims).
+ *   Guarantees nnz(b, oc) <= k, i.e. output density <= k/V per channel.
+ * ------------------------------------------------------------------------------------ */
+spc_status_t spc_conv_fwd_query(const spc_map_t* x, const spc_filter_t* w, spc_attn_t attn, int64_t k,
+                                int64_t* out_capacity, size_t* workspace_bytes);
+spc_status_t sparse_conv_fwd(const spc_map_t* x, const spc_filter_t* w, const float* bias,
+                             spc_attn_t attn, int64_t k, spc_map_out_t* y,
+                             void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * Backward of the convolution, Alg. 2 with the masked rule of Eqs. (3)/(4)
+ * (P:121-129): gradients exist only at stored inputs and stored (unpruned) weights.
+ *   y: the forward OUTPUT map (its keys are the kept entries; values unused);
+ *   dy: device [nnz(y)] gradient aligned with y's keys (attention-dropped outputs carry no
+ *   gradient, reading R10);
+ *   dx: device [nnz(x)] aligned with x's keys (fixed shape, P:135 (i));
+ *   dw: device [w->nnz] aligned with w's keys (pruned weights have no storage and stay 0,
+ *   P:135 (iii)); dbias: device [c_out] = sum of dy per output channel, or NULL.
+ *   dx accumulates in fp32; dw and dbias accumulate in fp64 and are rounded once.
+ * sparse_conv_bwd computes all three in one pass over the (input, weight) pairs as Alg. 2
+ * does; the _input / _weight entry points compute one side each.
+ * ------------------------------------------------------------------------------------ */
+spc_status_t spc_conv_bwd_query(const spc_map_t* x, const spc_filter_t* w, const spc_map_t* y,
+                                size_t* workspace_bytes);
+spc_status_t sparse_conv_bwd(const spc_map_t* x, const spc_filter_t* w, const spc_map_t* y,
+                             const float* dy, float* dx, float* dw, float* dbias,
+                             void* workspace, size_t workspace_bytes, cudaStream_t stream);
+spc_status_t sparse_conv_bwd_input(const spc_map_t* x, const spc_filter_t* w, const spc_map_t* y,
+                                   const float* dy, float* dx,
+                                   void* workspace, size_t workspace_bytes, cudaStream_t stream);
+spc_status_t sparse_conv_bwd_weight(const spc_map_t* x, const spc_filter_t* w, const spc_map_t* y,
+                                    const float* dy, float* dw, float* dbias,
+                                    void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * attention_topk — the attention filter as a standalone layer: per (b, c)
+ * segment of x keep min(k, n_seg) entries with the largest score (|v| for MAGNITUDE, v for
+ * RAW; ties by smaller key, R7); output in key order with x's shape.
+ *   src_index: device [capacity] int64 (input position of each kept entry) or NULL.
+ *   out capacity >= min(nnz(x), batch*channels*min(k, V)).
+ * ------------------------------------------------------------------------------------ */
+spc_status_t spc_topk_query(const spc_map_t* x, spc_attn_t attn, int64_t k,
+                            int64_t* out_capacity, size_t* workspace_bytes);
+spc_status_t attention_topk(const spc_map_t* x, spc_attn_t attn, int64_t k, spc_map_out_t* y,
+                            int64_t* src_index, void* workspace, size_t workspace_bytes,
+                            cudaStream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * sparse_relu — sparse ReLU ("truncates negative activations"): keep entries
+ * with v > 0 (R9), order preserved. src_index: device [capacity] int64 or NULL.
+ * out capacity >= nnz(x).
+ * ------------------------------------------------------------------------------------ */
+spc_status_t spc_relu_query(const spc_map_t* x, int64_t* out_capacity, size_t* workspace_bytes);
+spc_status_t sparse_relu(const spc_map_t* x, spc_map_out_t* y, int64_t* src_index,
+                         void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * sparse_maxpool — sparse max-pooling, §3.3: entries are assigned to the pooled
+ * voxel floor(p / stride) ("dividing ... their index by strides"), and the max is taken per
+ * cluster (R8: window = stride, output dims ceil(d / stride), max over stored entries only,
+ * empty clusters absent). argmax: device [capacity] int64, the input position of the
+ * maximum (ties -> smaller input key), or NULL. stride: HOST [ndim] positive integers.
+ * out capacity >= nnz(x). The algorithm is sort-free, unlike the paper's sort.
+ * ------------------------------------------------------------------------------------ */
+spc_status_t spc_maxpool_query(const spc_map_t* x, const int64_t* stride,
+                               int64_t* out_capacity, size_t* workspace_bytes);
+spc_status_t sparse_maxpool(const spc_map_t* x, const int64_t* stride, spc_map_out_t* y,
+                            int64_t* argmax, void* workspace, size_t workspace_bytes,
+                            cudaStream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * sparse_scatter_grad — backward of ReLU / max-pool / attention_topk (Eq. (5)):
+ *   dx[0..n_in) = 0, then dx[src_index[t]] = dy[t] for t < n_out. src_index must be
+ *   injective (it is for all three layers). n_out = *n_out_dev if non-NULL (bounded by
+ *   n_out_bound), else n_out_bound.
+ * ------------------------------------------------------------------------------------ */
+spc_status_t sparse_scatter_grad(const int64_t* src_index, const float* dy, int64_t n_out_bound,
+                                 const int64_t* n_out_dev, float* dx, int64_t n_in,
+                                 cudaStream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * Instrumentation (measurement only; not part of the method).
+ *   spc_kernel_launches: monotonically increasing count of kernels this library launched
+ *   (process-wide).
+ *   spc_profile_enable(1): every kernel phase is bracketed by CUDA events recorded on the
+ *   call's stream; spc_profile_read synchronises those events and returns, per phase name,
+ *   the accumulated milliseconds and the number of launches (names are written NUL-separated
+ *   into `names`; returns the number of phases). spc_profile_reset clears the totals.
+ * ------------------------------------------------------------------------------------ */
+int64_t spc_kernel_launches(void);
+spc_status_t spc_profile_enable(int on);
+spc_status_t spc_profile_reset(void);
+int spc_profile_read(char* names, size_t names_len, double* ms, int64_t* counts, int max_phases);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPCONV_H */

@@ -276,7 +276,7 @@ int ora_conv_bwd(int ndim, const int64_t* dims, int64_t batch, int64_t c_in, int
                  int64_t nw, const uint64_t* wk, const float* wv,
                  int64_t ny, const uint64_t* yk, const float* dy,
                  float* dx, float* dw, float* dbias,
-                 double* dx_abs, double* dw_abs) {
+                 double* dx_abs, double* dw_abs, int64_t* kept_pairs_out) {
     if (ndim < 1 || ndim > ORA_MAXDIM || batch < 0 || c_in < 1 || c_out < 1) return -1;
     for (int d = 0; d < ndim; ++d) if (dims[d] < 1 || ksize[d] < 1 || ksize[d] % 2 == 0) return -1;
     if (check_sorted(nx, xk) || check_sorted(nw, wk) || check_sorted(ny, yk)) return -2;
@@ -288,12 +288,14 @@ int ora_conv_bwd(int ndim, const int64_t* dims, int64_t batch, int64_t c_in, int
     int64_t* woff = (int64_t*)malloc(sizeof(int64_t) * (size_t)(c_out * c_in + 1));
     int64_t* yoff = (int64_t*)malloc(sizeof(int64_t) * (size_t)(batch * c_out + 1));
     double* G = (double*)malloc(sizeof(double) * (size_t)V);
+    char* K = (char*)malloc((size_t)V);
+    int64_t kept_pairs = 0;
     double* bpd = (double*)calloc((size_t)(nx > 0 ? nx : 1), sizeof(double));
     double* bpf = (double*)calloc((size_t)(nw > 0 ? nw : 1), sizeof(double));
     double* bpd_abs = (double*)calloc((size_t)(nx > 0 ? nx : 1), sizeof(double));
     double* bpf_abs = (double*)calloc((size_t)(nw > 0 ? nw : 1), sizeof(double));
     int rc = 0;
-    if (!xp || !wp || !xoff || !woff || !yoff || !G || !bpd || !bpf || !bpd_abs || !bpf_abs) { rc = -5; goto done; }
+    if (!xp || !wp || !xoff || !woff || !yoff || !G || !K || !bpd || !bpf || !bpd_abs || !bpf_abs) { rc = -5; goto done; }
     for (int64_t i = 0; i < nx; ++i) {
         int64_t b, c;
         if (decode_key(xk[i], ndim, dims, batch, c_in, &b, &c, &xp[i * ndim])) { rc = -3; goto done; }
@@ -319,13 +321,18 @@ int ora_conv_bwd(int ndim, const int64_t* dims, int64_t batch, int64_t c_in, int
         for (int64_t oc = 0; oc < c_out; ++oc) {
             /* initialize dense buffer with gradients(b, oc) */
             memset(G, 0, sizeof(double) * (size_t)V);
-            for (int64_t t = yoff[b * c_out + oc]; t < yoff[b * c_out + oc + 1]; ++t)
+            memset(K, 0, (size_t)V);
+            for (int64_t t = yoff[b * c_out + oc]; t < yoff[b * c_out + oc + 1]; ++t) {
                 G[yk[t] % (uint64_t)V] = (double)dy[t];
+                K[yk[t] % (uint64_t)V] = 1;   /* kept output (for the MAC count only) */
+            }
             for (int64_t ic = 0; ic < c_in; ++ic) {
                 for (int64_t i = xoff[b * c_in + ic]; i < xoff[b * c_in + ic + 1]; ++i) {
                     for (int64_t j = woff[oc * c_in + ic]; j < woff[oc * c_in + ic + 1]; ++j) {
                         if (!get_update_id(ndim, dims, ksize, &xp[i * ndim], &wp[j * ndim], uid)) continue;
-                        double g = G[lin_of(ndim, dims, uid)];     /* gradient at uid */
+                        const int64_t u = lin_of(ndim, dims, uid);
+                        double g = G[u];                             /* gradient at uid */
+                        kept_pairs += K[u];
                         bpd[i] += g * (double)wv[j];                 /* bp_data[id] += g*fval */
                         bpf[j] += g * (double)xv[i];                 /* bp_filter[fid] += g*val */
                         bpd_abs[i] += fabs(g * (double)wv[j]);
@@ -337,8 +344,9 @@ int ora_conv_bwd(int ndim, const int64_t* dims, int64_t batch, int64_t c_in, int
     }
     for (int64_t i = 0; i < nx; ++i) { dx[i] = (float)bpd[i]; if (dx_abs) dx_abs[i] = bpd_abs[i]; }
     for (int64_t j = 0; j < nw; ++j) { dw[j] = (float)bpf[j]; if (dw_abs) dw_abs[j] = bpf_abs[j]; }
+    if (kept_pairs_out) *kept_pairs_out = kept_pairs;
 done:
-    free(xp); free(wp); free(xoff); free(woff); free(yoff); free(G);
+    free(xp); free(wp); free(xoff); free(woff); free(yoff); free(G); free(K);
     free(bpd); free(bpf); free(bpd_abs); free(bpf_abs);
     return rc;
 }

@@ -39,7 +39,7 @@ def _load():
         _lib.ora_conv_fwd.argtypes = [C.c_int, P, I64, I64, I64, P, I64, P, P, I64, P, P, P, C.c_int, I64,
                                       I64, P, P, P, P, P]
         _lib.ora_conv_bwd.argtypes = [C.c_int, P, I64, I64, I64, P, I64, P, P, I64, P, P, I64, P, P,
-                                      P, P, P, P, P]
+                                      P, P, P, P, P, P]
         _lib.ora_topk.argtypes = [C.c_int, P, I64, I64, I64, P, P, C.c_int, I64, I64, P, P, P, P]
         _lib.ora_relu.argtypes = [I64, P, P, P, P, P, P]
         _lib.ora_maxpool.argtypes = [C.c_int, P, I64, I64, P, I64, P, P, I64, P, P, P, P]
@@ -118,8 +118,9 @@ def conv_fwd(x, w, bias, attn: int = ATTN_NONE, k: int = 0, with_abs: bool = Fal
     return yk[:n].copy(), yv[:n].copy(), (ya[:n].copy() if with_abs else None), int(macs[0])
 
 
-def conv_bwd(x, w, y_keys, dy, with_abs: bool = False):
-    """Alg. 2. Returns (dx, dw, dbias, dx_abs, dw_abs)."""
+def conv_bwd(x, w, y_keys, dy, with_abs: bool = False, return_pairs: bool = False):
+    """Alg. 2. Returns (dx, dw, dbias, dx_abs, dw_abs) [+ number of (input, weight) pairs whose
+    target is a kept output, when return_pairs]."""
     dims = _i64(x.dims)
     ks = _i64(w.ksize)
     xk, xv, wk, wv = _u64(x.keys), _f32(x.values), _u64(w.keys), _f32(w.values)
@@ -129,12 +130,14 @@ def conv_bwd(x, w, y_keys, dy, with_abs: bool = False):
     db = np.zeros(w.c_out, np.float32)
     dxa = np.zeros(max(1, x.nnz), np.float64) if with_abs else None
     dwa = np.zeros(max(1, w.nnz), np.float64) if with_abs else None
+    pairs = np.zeros(1, np.int64)
     rc = _load().ora_conv_bwd(x.ndim, _p(dims), x.batch, w.c_in, w.c_out, _p(ks),
                               x.nnz, _p(xk), _p(xv), w.nnz, _p(wk), _p(wv), yk.shape[0], _p(yk), _p(g),
-                              _p(dx), _p(dw), _p(db), _p(dxa), _p(dwa))
+                              _p(dx), _p(dw), _p(db), _p(dxa), _p(dwa), _p(pairs))
     _check(rc, "ora_conv_bwd")
-    return (dx[:x.nnz], dw[:w.nnz], db,
-            dxa[:x.nnz] if with_abs else None, dwa[:w.nnz] if with_abs else None)
+    out = (dx[:x.nnz], dw[:w.nnz], db,
+           dxa[:x.nnz] if with_abs else None, dwa[:w.nnz] if with_abs else None)
+    return out + (int(pairs[0]),) if return_pairs else out
 
 
 def topk(x, attn: int, k: int):

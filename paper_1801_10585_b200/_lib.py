@@ -1,0 +1,101 @@
+"""ctypes declaration of libspconv.so (include/spconv.h). Argument marshalling only."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libspconv.so")
+
+MAX_NDIM = 3
+
+STATUS = {
+    0: "SPC_OK", 1: "SPC_ERR_INVALID_ARG", 2: "SPC_ERR_SHAPE", 3: "SPC_ERR_CAPACITY",
+    4: "SPC_ERR_WORKSPACE", 5: "SPC_ERR_UNSORTED", 6: "SPC_ERR_UNSUPPORTED", 7: "SPC_ERR_CUDA",
+}
+
+ATTN = {"none": 0, "magnitude": 1, "raw": 2}
+
+# every symbol include/spconv.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "spc_version", "spc_status_string",
+    "spc_conv_fwd_query", "sparse_conv_fwd",
+    "spc_conv_bwd_query", "sparse_conv_bwd", "sparse_conv_bwd_input", "sparse_conv_bwd_weight",
+    "spc_topk_query", "attention_topk",
+    "spc_relu_query", "sparse_relu",
+    "spc_maxpool_query", "sparse_maxpool",
+    "sparse_scatter_grad",
+    "spc_kernel_launches", "spc_profile_enable", "spc_profile_reset", "spc_profile_read",
+]
+
+
+class MapT(C.Structure):
+    _fields_ = [("ndim", C.c_int32), ("batch", C.c_int64), ("channels", C.c_int64),
+                ("dims", C.c_int64 * MAX_NDIM), ("nnz", C.c_int64), ("nnz_dev", C.c_void_p),
+                ("keys", C.c_void_p), ("values", C.c_void_p)]
+
+
+class MapOutT(C.Structure):
+    _fields_ = [("capacity", C.c_int64), ("keys", C.c_void_p), ("values", C.c_void_p), ("nnz_dev", C.c_void_p)]
+
+
+class FilterT(C.Structure):
+    _fields_ = [("ndim", C.c_int32), ("c_in", C.c_int64), ("c_out", C.c_int64),
+                ("ksize", C.c_int64 * MAX_NDIM), ("nnz", C.c_int64), ("keys", C.c_void_p), ("values", C.c_void_p)]
+
+
+class SpconvError(RuntimeError):
+    def __init__(self, fn: str, code: int):
+        super().__init__(f"{fn} returned {STATUS.get(code, code)}")
+        self.code = code
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libspconv.so. Fails loudly when the library is missing: there is no fallback."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libspconv.so not found at {path}; run `python -c 'import __graft_entry__ as g; g.build()'`"
+                          " (there is no CPU fallback)")
+    lib = C.CDLL(path)
+    P = C.c_void_p
+    I64 = C.c_int64
+    pM, pO, pF = C.POINTER(MapT), C.POINTER(MapOutT), C.POINTER(FilterT)
+    sz = C.POINTER(C.c_size_t)
+    pi64 = C.POINTER(C.c_int64)
+    sig = {
+        "spc_version": ([], C.c_char_p),
+        "spc_status_string": ([C.c_int], C.c_char_p),
+        "spc_conv_fwd_query": ([pM, pF, C.c_int, I64, pi64, sz], C.c_int),
+        "sparse_conv_fwd": ([pM, pF, P, C.c_int, I64, pO, P, C.c_size_t, P], C.c_int),
+        "spc_conv_bwd_query": ([pM, pF, pM, sz], C.c_int),
+        "sparse_conv_bwd": ([pM, pF, pM, P, P, P, P, P, C.c_size_t, P], C.c_int),
+        "sparse_conv_bwd_input": ([pM, pF, pM, P, P, P, C.c_size_t, P], C.c_int),
+        "sparse_conv_bwd_weight": ([pM, pF, pM, P, P, P, P, C.c_size_t, P], C.c_int),
+        "spc_topk_query": ([pM, C.c_int, I64, pi64, sz], C.c_int),
+        "attention_topk": ([pM, C.c_int, I64, pO, P, P, C.c_size_t, P], C.c_int),
+        "spc_relu_query": ([pM, pi64, sz], C.c_int),
+        "sparse_relu": ([pM, pO, P, P, C.c_size_t, P], C.c_int),
+        "spc_maxpool_query": ([pM, P, pi64, sz], C.c_int),
+        "sparse_maxpool": ([pM, P, pO, P, P, C.c_size_t, P], C.c_int),
+        "sparse_scatter_grad": ([P, P, I64, P, P, I64, P], C.c_int),
+        "spc_kernel_launches": ([], C.c_int64),
+        "spc_profile_enable": ([C.c_int], C.c_int),
+        "spc_profile_reset": ([], C.c_int),
+        "spc_profile_read": ([C.c_char_p, C.c_size_t, P, P, C.c_int], C.c_int),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = lib
+    return lib
+
+
+def check(fn: str, code: int):
+    if code != 0:
+        raise SpconvError(fn, code)

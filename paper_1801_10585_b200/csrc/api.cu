@@ -1,0 +1,520 @@
+// C-ABI entry points of libspconv (include/spconv.h): argument validation, workspace carving
+// and kernel launches. No device memory is allocated here; every buffer is the caller's.
+#include "spc_internal.cuh"
+
+#include <stdlib.h>
+#include <string.h>
+#include <algorithm>
+
+using namespace spc;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+
+// Carves a caller-provided workspace; with base == nullptr it only measures.
+struct Carver {
+    char* base;
+    size_t used = 0;
+    explicit Carver(void* b) : base(static_cast<char*>(b)) {}
+    template <typename T>
+    T* take(size_t count) {
+        used = (used + kAlign - 1) & ~(kAlign - 1);
+        T* p = base ? reinterpret_cast<T*>(base + used) : nullptr;
+        used += sizeof(T) * (count ? count : 1);
+        return p;
+    }
+};
+
+bool validate_env() {
+    const char* v = getenv("SPC_VALIDATE");
+    return v && v[0] == '1';
+}
+
+spc_status_t check_map(const spc_map_t* m, bool need_values = true) {
+    if (!m) return SPC_ERR_INVALID_ARG;
+    if (m->ndim < 1 || m->ndim > SPC_MAX_NDIM) return SPC_ERR_UNSUPPORTED;
+    if (m->batch < 0 || m->channels < 1 || m->nnz < 0) return SPC_ERR_SHAPE;
+    double total = (double)m->batch * (double)m->channels;
+    for (int d = 0; d < m->ndim; ++d) {
+        if (m->dims[d] < 1 || m->dims[d] > (1ll << 30)) return SPC_ERR_SHAPE;
+        total *= (double)m->dims[d];
+    }
+    if (total >= 9.2e18) return SPC_ERR_SHAPE;
+    if (m->nnz >= (1ll << 32) - 1) return SPC_ERR_UNSUPPORTED;   // 32-bit row index
+    if (m->nnz > 0 && (!m->keys || (need_values && !m->values))) return SPC_ERR_INVALID_ARG;
+    return SPC_OK;
+}
+
+Geo geo_of(const spc_map_t* m, int64_t channels) {
+    Geo g{};
+    int64_t d[3] = {1, 1, 1};
+    for (int i = 0; i < m->ndim; ++i) d[3 - m->ndim + i] = m->dims[i];
+    g.B = m->batch;
+    g.C = channels;
+    g.X = (int)d[0];
+    g.Y = (int)d[1];
+    g.Z = (int)d[2];
+    g.V = d[0] * d[1] * d[2];
+    g.R = d[0] * d[1];
+    return g;
+}
+
+spc_status_t check_filter(const spc_filter_t* w, const spc_map_t* x, KGeo* kg) {
+    if (!w) return SPC_ERR_INVALID_ARG;
+    if (w->ndim != x->ndim) return SPC_ERR_SHAPE;
+    if (w->c_in != x->channels || w->c_out < 1 || w->nnz < 0) return SPC_ERR_SHAPE;
+    if (w->c_in * w->c_out > (1ll << 28)) return SPC_ERR_UNSUPPORTED;
+    int64_t k[3] = {1, 1, 1};
+    int64_t kv = 1;
+    for (int i = 0; i < w->ndim; ++i) {
+        if (w->ksize[i] < 1 || w->ksize[i] % 2 == 0) return SPC_ERR_SHAPE;
+        k[3 - w->ndim + i] = w->ksize[i];
+        kv *= w->ksize[i];
+    }
+    if (kv > 1024) return SPC_ERR_UNSUPPORTED;
+    if (w->nnz > w->c_in * w->c_out * kv) return SPC_ERR_SHAPE;
+    if (w->nnz > 0 && (!w->keys || !w->values)) return SPC_ERR_INVALID_ARG;
+    kg->kx = (int)k[0]; kg->ky = (int)k[1]; kg->kz = (int)k[2];
+    kg->hx = kg->kx / 2; kg->hy = kg->ky / 2; kg->hz = kg->kz / 2;
+    kg->KV = (int)kv;
+    return SPC_OK;
+}
+
+spc_status_t check_out(const spc_map_out_t* y, int64_t need) {
+    if (!y) return SPC_ERR_INVALID_ARG;
+    if (!y->nnz_dev) return SPC_ERR_INVALID_ARG;
+    if (y->capacity < need) return SPC_ERR_CAPACITY;
+    if (need > 0 && (!y->keys || !y->values)) return SPC_ERR_INVALID_ARG;
+    return SPC_OK;
+}
+
+spc_status_t cu(cudaError_t e) { return e == cudaSuccess ? SPC_OK : SPC_ERR_CUDA; }
+
+#define SPC_TRY(expr)                          \
+    do {                                       \
+        spc_status_t _s = (expr);              \
+        if (_s != SPC_OK) return _s;           \
+    } while (0)
+
+// SPC_VALIDATE=1: device check of sortedness and range; synchronises the stream.
+spc_status_t maybe_validate(const spc_map_t* m, int* flag, cudaStream_t s) {
+    if (!flag) return SPC_OK;
+    const uint64_t limit = (uint64_t)m->batch * (uint64_t)m->channels *
+                           (uint64_t)(m->ndim >= 1 ? m->dims[0] : 1) * (uint64_t)(m->ndim >= 2 ? m->dims[1] : 1) *
+                           (uint64_t)(m->ndim >= 3 ? m->dims[2] : 1);
+    SPC_TRY(cu(cudaMemsetAsync(flag, 0, sizeof(int), s)));
+    SPC_TRY(cu(launch_validate(m->keys, m->nnz_dev, m->nnz, limit, flag, s)));
+    int h = 0;
+    SPC_TRY(cu(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s)));
+    SPC_TRY(cu(cudaStreamSynchronize(s)));
+    return h ? SPC_ERR_UNSORTED : SPC_OK;
+}
+
+struct FilterWs {
+    int2* meta;
+    float* val;
+    int* off;
+    int* src;
+    int* scratch;
+};
+
+FilterWs carve_filter(Carver& c, const spc_filter_t* w) {
+    FilterWs f{};
+    f.meta = c.take<int2>((size_t)w->nnz);
+    f.val = c.take<float>((size_t)w->nnz);
+    f.off = c.take<int>((size_t)w->c_in * (w->c_out + 1));
+    f.src = c.take<int>((size_t)w->nnz);
+    f.scratch = c.take<int>((size_t)2 * w->c_in * w->c_out);
+    return f;
+}
+
+// ----------------------------------------------------------------------- forward
+struct FwdWs {
+    uint32_t* xrow;
+    FilterWs f;
+    float* pre;
+    unsigned long long* seg_count;
+    SelState* st;
+    uint32_t* hist;
+    ChunkRec* rec;
+    uint64_t* seg_off;
+    int* flag;
+};
+
+spc_status_t fwd_plan(const spc_map_t* x, const spc_filter_t* w, spc_attn_t attn, int64_t k, Geo* gx, Geo* gy,
+                      KGeo* kg, ConvTile* t, int64_t* cap) {
+    SPC_TRY(check_map(x));
+    SPC_TRY(check_filter(w, x, kg));
+    if (attn != SPC_ATTN_NONE && attn != SPC_ATTN_MAGNITUDE && attn != SPC_ATTN_RAW) return SPC_ERR_INVALID_ARG;
+    if (attn != SPC_ATTN_NONE && k < 1) return SPC_ERR_INVALID_ARG;
+    *gx = geo_of(x, x->channels);
+    *gy = geo_of(x, w->c_out);
+    const int64_t per = attn != SPC_ATTN_NONE ? std::min<int64_t>(k, gy->V) : gy->V;
+    *cap = x->batch * w->c_out * per;
+    *t = plan_fwd_tile(*gy, *kg, (int)w->c_out);
+    if (t->smem == 0) return SPC_ERR_UNSUPPORTED;
+    return SPC_OK;
+}
+
+FwdWs carve_fwd(Carver& c, const Geo& gx, const Geo& gy, const spc_filter_t* w) {
+    FwdWs ws{};
+    const int64_t nseg = gy.B * gy.C;
+    const int64_t nchunk = (gy.V + kSelChunk - 1) / kSelChunk;
+    ws.xrow = c.take<uint32_t>((size_t)(gx.B * gx.C * gx.R + 1));
+    ws.f = carve_filter(c, w);
+    ws.pre = c.take<float>((size_t)(nseg * gy.V));
+    ws.seg_count = c.take<unsigned long long>((size_t)nseg);
+    ws.st = c.take<SelState>((size_t)nseg);
+    ws.hist = c.take<uint32_t>((size_t)nseg * kSelBins);
+    ws.rec = c.take<ChunkRec>((size_t)(nseg * nchunk));
+    ws.seg_off = c.take<uint64_t>((size_t)nseg + 1);
+    ws.flag = c.take<int>(1);
+    return ws;
+}
+
+// ---------------------------------------------------------------------- backward
+struct BwdWs {
+    uint32_t* xrow;
+    uint32_t* yrow;
+    FilterWs f;
+    double* dw_acc;
+    double* db_acc;
+    int* flag;
+};
+
+spc_status_t bwd_plan(const spc_map_t* x, const spc_filter_t* w, const spc_map_t* y, Geo* gx, Geo* gy, KGeo* kg,
+                      BwdTile* t) {
+    SPC_TRY(check_map(x));
+    SPC_TRY(check_map(y, false));
+    SPC_TRY(check_filter(w, x, kg));
+    if (y->ndim != x->ndim || y->batch != x->batch || y->channels != w->c_out) return SPC_ERR_SHAPE;
+    for (int d = 0; d < x->ndim; ++d)
+        if (y->dims[d] != x->dims[d]) return SPC_ERR_SHAPE;
+    *gx = geo_of(x, x->channels);
+    *gy = geo_of(y, y->channels);
+    *t = plan_bwd_tile(*gx, *kg, (int)w->c_out, (int)std::min<int64_t>(w->nnz, 1ll << 30));
+    if (t->smem == 0) return SPC_ERR_UNSUPPORTED;
+    return SPC_OK;
+}
+
+BwdWs carve_bwd(Carver& c, const Geo& gx, const Geo& gy, const spc_filter_t* w) {
+    BwdWs ws{};
+    ws.xrow = c.take<uint32_t>((size_t)(gx.B * gx.C * gx.R + 1));
+    ws.yrow = c.take<uint32_t>((size_t)(gy.B * gy.C * gy.R + 1));
+    ws.f = carve_filter(c, w);
+    ws.dw_acc = c.take<double>((size_t)w->nnz);
+    ws.db_acc = c.take<double>((size_t)w->c_out);
+    ws.flag = c.take<int>(1);
+    return ws;
+}
+
+spc_status_t conv_bwd_impl(const spc_map_t* x, const spc_filter_t* w, const spc_map_t* y, const float* dy, float* dx,
+                           float* dw, float* dbias, void* workspace, size_t ws_bytes, cudaStream_t s) {
+    Geo gx, gy;
+    KGeo kg;
+    BwdTile t;
+    SPC_TRY(bwd_plan(x, w, y, &gx, &gy, &kg, &t));
+    const bool want_dx = dx != nullptr, want_dw = dw != nullptr;
+    if (y->nnz > 0 && !dy) return SPC_ERR_INVALID_ARG;
+    if (!want_dx && !want_dw && !dbias) return SPC_OK;
+    if (want_dx && x->nnz > 0 && !dx) return SPC_ERR_INVALID_ARG;
+    Carver m(nullptr);
+    carve_bwd(m, gx, gy, w);
+    if (!workspace || ws_bytes < m.used) return SPC_ERR_WORKSPACE;
+    Carver c(workspace);
+    BwdWs ws = carve_bwd(c, gx, gy, w);
+    if (validate_env()) {
+        SPC_TRY(maybe_validate(x, ws.flag, s));
+        SPC_TRY(maybe_validate(y, ws.flag, s));
+    }
+    if (dbias) {
+        SPC_TRY(cu(cudaMemsetAsync(ws.db_acc, 0, sizeof(double) * (size_t)w->c_out, s)));
+        SPC_TRY(cu(launch_dbias(gy, y->keys, dy, y->nnz_dev, y->nnz, ws.db_acc, s)));
+        SPC_TRY(cu(launch_f64_to_f32(ws.db_acc, dbias, w->c_out, s)));
+    }
+    if (!want_dx && !want_dw) return SPC_OK;
+    SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
+    SPC_TRY(cu(launch_row_index(gy, y->keys, y->nnz_dev, y->nnz, ws.yrow, s)));
+    SPC_TRY(cu(launch_filter_table(kg, (int)w->c_in, (int)w->c_out, w->keys, w->values, w->nnz, ws.f.meta, ws.f.val,
+                                   ws.f.off, ws.f.src, ws.f.scratch, s)));
+    if (want_dx && t.n_ocg > 1 && x->nnz > 0) SPC_TRY(cu(cudaMemsetAsync(dx, 0, sizeof(float) * (size_t)x->nnz, s)));
+    if (want_dw && w->nnz > 0) SPC_TRY(cu(cudaMemsetAsync(ws.dw_acc, 0, sizeof(double) * (size_t)w->nnz, s)));
+    SPC_TRY(cu(launch_conv_bwd(gx, gy, kg, t, x->keys, x->values, ws.xrow, y->keys, dy, ws.yrow, ws.f.meta, ws.f.val,
+                               ws.f.off, ws.f.src, dx, ws.dw_acc, want_dx, want_dw, s)));
+    if (want_dw) SPC_TRY(cu(launch_f64_to_f32(ws.dw_acc, dw, w->nnz, s)));
+    return SPC_OK;
+}
+
+// -------------------------------------------------------------------- selection ws
+struct TopkWs {
+    uint32_t* xrow;
+    SelState* st;
+    uint32_t* hist;
+    ChunkRec* rec;
+    uint64_t* seg_off;
+    int* flag;
+};
+
+int64_t topk_nchunk(const Geo& g, int64_t nnz) {
+    const int64_t maxseg = std::min<int64_t>(g.V, nnz);
+    return std::max<int64_t>(1, (maxseg + kSelChunk - 1) / kSelChunk);
+}
+
+TopkWs carve_topk(Carver& c, const Geo& g, int64_t nnz) {
+    TopkWs ws{};
+    const int64_t nseg = g.B * g.C;
+    ws.xrow = c.take<uint32_t>((size_t)(g.B * g.C * g.R + 1));
+    ws.st = c.take<SelState>((size_t)nseg);
+    ws.hist = c.take<uint32_t>((size_t)nseg * kSelBins);
+    ws.rec = c.take<ChunkRec>((size_t)(nseg * topk_nchunk(g, nnz)));
+    ws.seg_off = c.take<uint64_t>((size_t)nseg + 1);
+    ws.flag = c.take<int>(1);
+    return ws;
+}
+
+struct ReluWs {
+    uint32_t* cnt;
+    uint64_t* off;
+    uint64_t* tmp;
+    int* flag;
+};
+constexpr int kReluChunkHost = 4096;
+
+ReluWs carve_relu(Carver& c, int64_t n) {
+    ReluWs ws{};
+    const int64_t nch = std::max<int64_t>(1, (n + kReluChunkHost - 1) / kReluChunkHost);
+    ws.cnt = c.take<uint32_t>((size_t)nch);
+    ws.off = c.take<uint64_t>((size_t)nch);
+    ws.tmp = c.take<uint64_t>(scan_tmp_words(nch));
+    ws.flag = c.take<int>(1);
+    return ws;
+}
+
+struct PoolWs {
+    uint32_t* xrow;
+    uint32_t* cnt;
+    uint64_t* off;
+    uint64_t* tmp;
+    int* flag;
+};
+
+PoolWs carve_pool(Carver& c, const Geo& g, const PoolPlan& p) {
+    PoolWs ws{};
+    ws.xrow = c.take<uint32_t>((size_t)(g.B * g.C * g.R + 1));
+    ws.cnt = c.take<uint32_t>((size_t)p.items);
+    ws.off = c.take<uint64_t>((size_t)p.items);
+    ws.tmp = c.take<uint64_t>(scan_tmp_words(p.items));
+    ws.flag = c.take<int>(1);
+    return ws;
+}
+
+spc_status_t pool_plan(const spc_map_t* x, const int64_t* stride, Geo* g, PoolPlan* p) {
+    SPC_TRY(check_map(x));
+    if (!stride) return SPC_ERR_INVALID_ARG;
+    int64_t s3[3] = {1, 1, 1};
+    for (int i = 0; i < x->ndim; ++i) {
+        if (stride[i] < 1 || stride[i] > (1 << 20)) return SPC_ERR_SHAPE;
+        s3[3 - x->ndim + i] = stride[i];
+    }
+    *g = geo_of(x, x->channels);
+    *p = plan_pool(*g, (int)s3[0], (int)s3[1], (int)s3[2]);
+    return SPC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* spc_version(void) { return "spconv-b200 0.1 (sm_100a)"; }
+
+const char* spc_status_string(spc_status_t s) {
+    switch (s) {
+        case SPC_OK: return "ok";
+        case SPC_ERR_INVALID_ARG: return "invalid argument";
+        case SPC_ERR_SHAPE: return "shape mismatch";
+        case SPC_ERR_CAPACITY: return "output capacity too small";
+        case SPC_ERR_WORKSPACE: return "workspace too small";
+        case SPC_ERR_UNSORTED: return "keys unsorted, duplicated or out of range";
+        case SPC_ERR_UNSUPPORTED: return "unsupported configuration";
+        case SPC_ERR_CUDA: return "CUDA error";
+    }
+    return "unknown status";
+}
+
+spc_status_t spc_conv_fwd_query(const spc_map_t* x, const spc_filter_t* w, spc_attn_t attn, int64_t k,
+                                int64_t* out_capacity, size_t* workspace_bytes) {
+    Geo gx, gy;
+    KGeo kg;
+    ConvTile t;
+    int64_t cap;
+    SPC_TRY(fwd_plan(x, w, attn, k, &gx, &gy, &kg, &t, &cap));
+    Carver m(nullptr);
+    carve_fwd(m, gx, gy, w);
+    if (out_capacity) *out_capacity = cap;
+    if (workspace_bytes) *workspace_bytes = m.used;
+    return SPC_OK;
+}
+
+spc_status_t sparse_conv_fwd(const spc_map_t* x, const spc_filter_t* w, const float* bias, spc_attn_t attn, int64_t k,
+                             spc_map_out_t* y, void* workspace, size_t workspace_bytes, cudaStream_t s) {
+    Geo gx, gy;
+    KGeo kg;
+    ConvTile t;
+    int64_t cap;
+    SPC_TRY(fwd_plan(x, w, attn, k, &gx, &gy, &kg, &t, &cap));
+    SPC_TRY(check_out(y, cap));
+    Carver m(nullptr);
+    carve_fwd(m, gx, gy, w);
+    if (!workspace || workspace_bytes < m.used) return SPC_ERR_WORKSPACE;
+    Carver c(workspace);
+    FwdWs ws = carve_fwd(c, gx, gy, w);
+    if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
+    const int64_t nseg = gy.B * gy.C;
+    SPC_TRY(cu(cudaMemsetAsync(ws.seg_count, 0, sizeof(unsigned long long) * (size_t)std::max<int64_t>(1, nseg), s)));
+    SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
+    SPC_TRY(cu(launch_filter_table(kg, (int)w->c_in, (int)w->c_out, w->keys, w->values, w->nnz, ws.f.meta, ws.f.val,
+                                   ws.f.off, ws.f.src, ws.f.scratch, s)));
+    SPC_TRY(cu(launch_conv_fwd(gx, gy, kg, t, x->keys, x->values, ws.xrow, ws.f.meta, ws.f.val, ws.f.off, bias,
+                               ws.pre, ws.seg_count, s)));
+    SelSrc src{};
+    src.kind = 0;
+    src.attn = attn;
+    src.nseg = nseg;
+    src.V = gy.V;
+    src.nchunk = (gy.V + kSelChunk - 1) / kSelChunk;
+    src.pre = ws.pre;
+    src.seg_count = ws.seg_count;
+    return cu(launch_select(src, k, ws.st, ws.hist, ws.rec, ws.seg_off, y->keys, y->values, nullptr, y->nnz_dev, s));
+}
+
+spc_status_t spc_conv_bwd_query(const spc_map_t* x, const spc_filter_t* w, const spc_map_t* y,
+                                size_t* workspace_bytes) {
+    Geo gx, gy;
+    KGeo kg;
+    BwdTile t;
+    SPC_TRY(bwd_plan(x, w, y, &gx, &gy, &kg, &t));
+    Carver m(nullptr);
+    carve_bwd(m, gx, gy, w);
+    if (workspace_bytes) *workspace_bytes = m.used;
+    return SPC_OK;
+}
+
+spc_status_t sparse_conv_bwd(const spc_map_t* x, const spc_filter_t* w, const spc_map_t* y, const float* dy, float* dx,
+                             float* dw, float* dbias, void* workspace, size_t workspace_bytes, cudaStream_t s) {
+    if (!dx || !dw) return SPC_ERR_INVALID_ARG;
+    return conv_bwd_impl(x, w, y, dy, dx, dw, dbias, workspace, workspace_bytes, s);
+}
+
+spc_status_t sparse_conv_bwd_input(const spc_map_t* x, const spc_filter_t* w, const spc_map_t* y, const float* dy,
+                                   float* dx, void* workspace, size_t workspace_bytes, cudaStream_t s) {
+    if (!dx) return SPC_ERR_INVALID_ARG;
+    return conv_bwd_impl(x, w, y, dy, dx, nullptr, nullptr, workspace, workspace_bytes, s);
+}
+
+spc_status_t sparse_conv_bwd_weight(const spc_map_t* x, const spc_filter_t* w, const spc_map_t* y, const float* dy,
+                                    float* dw, float* dbias, void* workspace, size_t workspace_bytes, cudaStream_t s) {
+    if (!dw) return SPC_ERR_INVALID_ARG;
+    return conv_bwd_impl(x, w, y, dy, nullptr, dw, dbias, workspace, workspace_bytes, s);
+}
+
+spc_status_t spc_topk_query(const spc_map_t* x, spc_attn_t attn, int64_t k, int64_t* out_capacity,
+                            size_t* workspace_bytes) {
+    SPC_TRY(check_map(x));
+    if (attn != SPC_ATTN_MAGNITUDE && attn != SPC_ATTN_RAW) return SPC_ERR_INVALID_ARG;
+    if (k < 1) return SPC_ERR_INVALID_ARG;
+    const Geo g = geo_of(x, x->channels);
+    Carver m(nullptr);
+    carve_topk(m, g, x->nnz);
+    if (out_capacity) *out_capacity = std::min<int64_t>(x->nnz, g.B * g.C * std::min<int64_t>(k, g.V));
+    if (workspace_bytes) *workspace_bytes = m.used;
+    return SPC_OK;
+}
+
+spc_status_t attention_topk(const spc_map_t* x, spc_attn_t attn, int64_t k, spc_map_out_t* y, int64_t* src_index,
+                            void* workspace, size_t workspace_bytes, cudaStream_t s) {
+    int64_t cap;
+    size_t need;
+    SPC_TRY(spc_topk_query(x, attn, k, &cap, &need));
+    SPC_TRY(check_out(y, cap));
+    if (!workspace || workspace_bytes < need) return SPC_ERR_WORKSPACE;
+    const Geo g = geo_of(x, x->channels);
+    Carver c(workspace);
+    TopkWs ws = carve_topk(c, g, x->nnz);
+    if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
+    SPC_TRY(cu(launch_row_index(g, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
+    SelSrc src{};
+    src.kind = 1;
+    src.attn = attn;
+    src.nseg = g.B * g.C;
+    src.V = g.V;
+    src.nchunk = topk_nchunk(g, x->nnz);
+    src.keys = x->keys;
+    src.vals = x->values;
+    src.row_ptr = ws.xrow;
+    src.R = g.R;
+    return cu(launch_select(src, k, ws.st, ws.hist, ws.rec, ws.seg_off, y->keys, y->values, src_index, y->nnz_dev, s));
+}
+
+spc_status_t spc_relu_query(const spc_map_t* x, int64_t* out_capacity, size_t* workspace_bytes) {
+    SPC_TRY(check_map(x));
+    Carver m(nullptr);
+    carve_relu(m, x->nnz);
+    if (out_capacity) *out_capacity = x->nnz;
+    if (workspace_bytes) *workspace_bytes = m.used;
+    return SPC_OK;
+}
+
+spc_status_t sparse_relu(const spc_map_t* x, spc_map_out_t* y, int64_t* src_index, void* workspace,
+                         size_t workspace_bytes, cudaStream_t s) {
+    int64_t cap;
+    size_t need;
+    SPC_TRY(spc_relu_query(x, &cap, &need));
+    SPC_TRY(check_out(y, cap));
+    if (!workspace || workspace_bytes < need) return SPC_ERR_WORKSPACE;
+    Carver c(workspace);
+    ReluWs ws = carve_relu(c, x->nnz);
+    if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
+    return cu(launch_relu(x->keys, x->values, x->nnz_dev, x->nnz, ws.cnt, ws.off, ws.tmp, y->keys, y->values, src_index,
+                          y->nnz_dev, s));
+}
+
+spc_status_t spc_maxpool_query(const spc_map_t* x, const int64_t* stride, int64_t* out_capacity,
+                               size_t* workspace_bytes) {
+    Geo g;
+    PoolPlan p;
+    SPC_TRY(pool_plan(x, stride, &g, &p));
+    Carver m(nullptr);
+    carve_pool(m, g, p);
+    if (out_capacity) *out_capacity = x->nnz;
+    if (workspace_bytes) *workspace_bytes = m.used;
+    return SPC_OK;
+}
+
+spc_status_t sparse_maxpool(const spc_map_t* x, const int64_t* stride, spc_map_out_t* y, int64_t* argmax,
+                            void* workspace, size_t workspace_bytes, cudaStream_t s) {
+    Geo g;
+    PoolPlan p;
+    SPC_TRY(pool_plan(x, stride, &g, &p));
+    SPC_TRY(check_out(y, x->nnz));
+    Carver m(nullptr);
+    carve_pool(m, g, p);
+    if (!workspace || workspace_bytes < m.used) return SPC_ERR_WORKSPACE;
+    Carver c(workspace);
+    PoolWs ws = carve_pool(c, g, p);
+    if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
+    SPC_TRY(cu(launch_row_index(g, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
+    return cu(launch_maxpool(g, p, x->keys, x->values, ws.xrow, ws.cnt, ws.off, ws.tmp, y->keys, y->values, argmax,
+                             y->nnz_dev, s));
+}
+
+spc_status_t sparse_scatter_grad(const int64_t* src_index, const float* dy, int64_t n_out_bound,
+                                 const int64_t* n_out_dev, float* dx, int64_t n_in, cudaStream_t s) {
+    if (n_out_bound < 0 || n_in < 0) return SPC_ERR_SHAPE;
+    if (n_out_bound > 0 && (!src_index || !dy)) return SPC_ERR_INVALID_ARG;
+    if (n_in > 0 && !dx) return SPC_ERR_INVALID_ARG;
+    if (n_in == 0) return SPC_OK;
+    return cu(launch_scatter_grad(src_index, dy, n_out_bound, n_out_dev, dx, n_in, s));
+}
+
+}  // extern "C"

@@ -1,0 +1,230 @@
+// Index structures (Alg. 1 step 1 "decompress filter and data indices"), device-wide
+// scan, validation and small helpers. Internal to libspconv.
+#include "spc_internal.cuh"
+#include "block_scan.cuh"
+
+namespace spc {
+
+// ---------------------------------------------------------------------------- row index
+// row_ptr[r] = first entry whose key >= r*Z, for r in [0, total_rows]. One thread per entry
+// owns the gap of rows between its predecessor's row and its own row; a warp fills the gaps of
+// its 32 lanes cooperatively so that long empty stretches do not serialise on one thread.
+__global__ void row_index_kernel(int Z, const uint64_t* __restrict__ keys, const int64_t* nnz_dev,
+                                 int64_t nbound, uint32_t* __restrict__ row_ptr, int64_t total_rows) {
+    const int64_t n = load_n(nnz_dev, nbound);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    int64_t lo = 0, hi = -1;
+    if (i < n) {
+        const int64_t r = (int64_t)(keys[i] / (uint64_t)Z);
+        const int64_t rp = (i == 0) ? -1 : (int64_t)(keys[i - 1] / (uint64_t)Z);
+        lo = rp + 1;
+        hi = r < total_rows ? r : total_rows;
+    } else if (i == n) {
+        const int64_t rl = (n == 0) ? -1 : (int64_t)(keys[n - 1] / (uint64_t)Z);
+        lo = rl + 1;
+        hi = total_rows;
+    }
+    unsigned m = __ballot_sync(kFull, hi >= lo);
+    while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const int64_t l = __shfl_sync(kFull, lo, src);
+        const int64_t h = __shfl_sync(kFull, hi, src);
+        const int64_t v = __shfl_sync(kFull, i, src);
+        for (int64_t r = l + lane; r <= h; r += 32) row_ptr[r] = (uint32_t)v;
+    }
+}
+
+cudaError_t launch_row_index(const Geo& g, const uint64_t* keys, const int64_t* nnz_dev, int64_t nbound,
+                             uint32_t* row_ptr, cudaStream_t s) {
+    const int64_t total_rows = g.B * g.C * g.R;
+    const int64_t threads = nbound + 1;
+    const int bs = 256;
+    const int64_t grid = (threads + bs - 1) / bs;
+    { SPC_PHASE("row_index", s, 1); row_index_kernel<<<(unsigned)grid, bs, 0, s>>>(g.Z, keys, nnz_dev, nbound, row_ptr, total_rows); }
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------- filter table
+__device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t n, uint64_t v) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (a[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// One block. Re-lays the (oc, ic, delta)-sorted filter into ic-major order (ic, oc, delta) so
+// that a CTA finds "filter(oc, ic)" of Alg. 1 for a group of oc as one contiguous range.
+__global__ void filter_table_kernel(KGeo kg, int c_in, int c_out, const uint64_t* __restrict__ wk,
+                                    const float* __restrict__ wv, int64_t nw, int2* __restrict__ meta,
+                                    float* __restrict__ val, int* __restrict__ off, int* __restrict__ src,
+                                    int* __restrict__ run_start,
+                                    int* __restrict__ run_len) {
+    __shared__ int sm[32];
+    const int npairs = c_in * c_out;
+    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+        const int64_t lo = lower_bound_u64(wk, nw, (uint64_t)p * (uint64_t)kg.KV);
+        const int64_t hi = lower_bound_u64(wk, nw, (uint64_t)(p + 1) * (uint64_t)kg.KV);
+        run_start[p] = (int)lo;
+        run_len[p] = (int)(hi - lo);
+    }
+    __syncthreads();
+    int carry = 0;
+    for (int base = 0; base < npairs; base += blockDim.x) {
+        const int q = base + threadIdx.x;          // ic-major: q = ic*c_out + oc
+        int len = 0, ic = 0, oc = 0;
+        if (q < npairs) {
+            ic = q / c_out;
+            oc = q - ic * c_out;
+            len = run_len[oc * c_in + ic];
+        }
+        int tot;
+        const int ex = block_excl_scan(len, sm, &tot);
+        if (q < npairs) off[ic * (c_out + 1) + oc] = carry + ex;
+        carry += tot;
+    }
+    __syncthreads();
+    for (int ic = threadIdx.x; ic < c_in; ic += blockDim.x)
+        off[ic * (c_out + 1) + c_out] = (ic + 1 < c_in) ? off[(ic + 1) * (c_out + 1)] : carry;
+    __syncthreads();
+    for (int64_t j = threadIdx.x; j < nw; j += blockDim.x) {
+        const uint64_t key = wk[j];
+        const int p = (int)(key / (uint64_t)kg.KV);
+        const int dlin = (int)(key - (uint64_t)p * (uint64_t)kg.KV);
+        const int oc = p / c_in, ic = p - (p / c_in) * c_in;
+        const int dst = off[ic * (c_out + 1) + oc] + (int)(j - run_start[p]);
+        const int dz = dlin % kg.kz;
+        const int dy = (dlin / kg.kz) % kg.ky;
+        const int dx = dlin / (kg.kz * kg.ky);
+        meta[dst] = make_int2(oc, pack_off(dx - kg.hx, dy - kg.hy, dz - kg.hz));
+        val[dst] = wv[j];
+        src[dst] = (int)j;
+    }
+}
+
+cudaError_t launch_filter_table(const KGeo& kg, int c_in, int c_out, const uint64_t* wkeys, const float* wvals,
+                                int64_t nw, int2* meta, float* val, int* off, int* src, int* scratch, cudaStream_t s) {
+    { SPC_PHASE("filter_table", s, 1); filter_table_kernel<<<1, 1024, 0, s>>>(kg, c_in, c_out, wkeys, wvals, nw, meta, val, off, src, scratch,
+                                           scratch + (size_t)c_in * c_out); }
+    return cudaGetLastError();
+}
+
+// --------------------------------------------------------------------- device-wide scan
+constexpr int kScanBlock = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanBlock * kScanItems;
+
+size_t scan_tmp_words(int64_t n) { return (size_t)((n + kScanTile - 1) / kScanTile) + 2; }
+
+__global__ void scan_reduce_kernel(const uint32_t* __restrict__ in, int64_t n, uint64_t* __restrict__ sums) {
+    __shared__ uint64_t sm[32];
+    const int64_t base = (int64_t)blockIdx.x * kScanTile;
+    uint64_t acc = 0;
+    for (int t = 0; t < kScanItems; ++t) {
+        const int64_t i = base + (int64_t)t * kScanBlock + threadIdx.x;
+        if (i < n) acc += in[i];
+    }
+    const uint64_t tot = block_sum(acc, sm);
+    if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void scan_sums_kernel(uint64_t* sums, int64_t nb, int64_t* total) {
+    __shared__ uint64_t sm[32];
+    uint64_t carry = 0;
+    for (int64_t base = 0; base < nb; base += blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const uint64_t v = i < nb ? sums[i] : 0;
+        uint64_t tot;
+        const uint64_t ex = block_excl_scan(v, sm, &tot);
+        if (i < nb) sums[i] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0 && total) *total = (int64_t)carry;
+}
+
+__global__ void scan_down_kernel(const uint32_t* __restrict__ in, int64_t n, const uint64_t* __restrict__ sums,
+                                 uint64_t* __restrict__ out) {
+    __shared__ uint64_t sm[32];
+    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    uint32_t v[kScanItems];
+    uint64_t acc = 0;
+#pragma unroll
+    for (int t = 0; t < kScanItems; ++t) {
+        const int64_t i = base + t;
+        v[t] = i < n ? in[i] : 0u;
+        acc += v[t];
+    }
+    uint64_t tot;
+    uint64_t ex = block_excl_scan(acc, sm, &tot) + sums[blockIdx.x];
+#pragma unroll
+    for (int t = 0; t < kScanItems; ++t) {
+        const int64_t i = base + t;
+        if (i < n) out[i] = ex;
+        ex += v[t];
+    }
+}
+
+cudaError_t launch_scan_u32(const uint32_t* in, uint64_t* out, int64_t n, int64_t* total, uint64_t* tmp,
+                            cudaStream_t s) {
+    const int64_t nb = (n + kScanTile - 1) / kScanTile;
+    if (nb > 0) { SPC_PHASE("scan_reduce", s, 1); scan_reduce_kernel<<<(unsigned)nb, kScanBlock, 0, s>>>(in, n, tmp); }
+    { SPC_PHASE("scan_sums", s, 1); scan_sums_kernel<<<1, 1024, 0, s>>>(tmp, nb, total); }
+    if (nb > 0) { SPC_PHASE("scan_down", s, 1); scan_down_kernel<<<(unsigned)nb, kScanBlock, 0, s>>>(in, n, tmp, out); }
+    return cudaGetLastError();
+}
+
+// --------------------------------------------------------------------------- validation
+__global__ void validate_kernel(const uint64_t* __restrict__ keys, const int64_t* nnz_dev, int64_t nbound,
+                                uint64_t limit, int* flag) {
+    const int64_t n = load_n(nnz_dev, nbound);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        if (k >= limit || (i > 0 && keys[i - 1] >= k)) atomicOr(flag, 1);
+    }
+}
+
+cudaError_t launch_validate(const uint64_t* keys, const int64_t* nnz_dev, int64_t nbound, uint64_t limit,
+                            int* flag, cudaStream_t s) {
+    { SPC_PHASE("validate", s, 1); validate_kernel<<<592, 256, 0, s>>>(keys, nnz_dev, nbound, limit, flag); }
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------ helpers
+__global__ void f64_to_f32_kernel(const double* __restrict__ a, float* __restrict__ b, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        b[i] = (float)a[i];
+}
+
+cudaError_t launch_f64_to_f32(const double* a, float* b, int64_t n, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    int64_t grid = (n + 255) / 256;
+    if (grid > 1184) grid = 1184;
+    { SPC_PHASE("f64_to_f32", s, 1); f64_to_f32_kernel<<<(unsigned)grid, 256, 0, s>>>(a, b, n); }
+    return cudaGetLastError();
+}
+
+// Eq. (5): the gradient passes where the forward layer kept an entry.
+__global__ void scatter_grad_kernel(const int64_t* __restrict__ src, const float* __restrict__ dy, int64_t nbound,
+                                    const int64_t* n_dev, float* __restrict__ dx, int64_t n_in) {
+    const int64_t n = load_n(n_dev, nbound);
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = src[t];
+        if (i >= 0 && i < n_in) dx[i] = dy[t];
+    }
+}
+
+cudaError_t launch_scatter_grad(const int64_t* src, const float* dy, int64_t n_out_bound, const int64_t* n_out_dev,
+                                float* dx, int64_t n_in, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(dx, 0, sizeof(float) * (size_t)n_in, s);
+    if (e != cudaSuccess) return e;
+    if (n_out_bound <= 0) return cudaSuccess;
+    int64_t grid = (n_out_bound + 255) / 256;
+    if (grid > 148 * 16) grid = 148 * 16;
+    { SPC_PHASE("scatter_grad", s, 1); scatter_grad_kernel<<<(unsigned)grid, 256, 0, s>>>(src, dy, n_out_bound, n_out_dev, dx, n_in); }
+    return cudaGetLastError();
+}
+
+}  // namespace spc

@@ -1,0 +1,191 @@
+// Sparse ReLU and sparse max-pooling (§3.3) as compacting kernels.
+#include "spc_internal.cuh"
+#include "block_scan.cuh"
+
+namespace spc {
+
+// ------------------------------------------------------------------------------- ReLU
+// Keep v > 0 (reading R9); order preserved; ordered stream compaction in two passes over
+// 4096-entry chunks (count, device scan, write).
+constexpr int kReluThreads = 256;
+constexpr int kReluItems = 16;
+constexpr int kReluChunk = kReluThreads * kReluItems;
+
+__global__ void __launch_bounds__(kReluThreads) relu_count_kernel(const float* __restrict__ vals, const int64_t* nnz_dev,
+                                                                  int64_t nbound, uint32_t* __restrict__ cnt) {
+    const int64_t n = load_n(nnz_dev, nbound);
+    const int64_t base = (int64_t)blockIdx.x * kReluChunk;
+    uint32_t c = 0;
+#pragma unroll
+    for (int u = 0; u < kReluItems; ++u) {
+        const int64_t i = base + (int64_t)u * kReluThreads + threadIdx.x;
+        if (i < n) c += vals[i] > 0.0f;
+    }
+    __shared__ uint32_t sm[32];
+    const uint32_t tot = block_sum(c, sm);
+    if (threadIdx.x == 0) cnt[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kReluThreads) relu_write_kernel(const uint64_t* __restrict__ keys,
+                                                                  const float* __restrict__ vals, const int64_t* nnz_dev,
+                                                                  int64_t nbound, const uint64_t* __restrict__ off,
+                                                                  uint64_t* __restrict__ ok, float* __restrict__ ov,
+                                                                  int64_t* __restrict__ osrc) {
+    const int64_t n = load_n(nnz_dev, nbound);
+    const int64_t base = (int64_t)blockIdx.x * kReluChunk;
+    if (base >= n) return;
+    const int64_t my = base + (int64_t)threadIdx.x * kReluItems;
+    float v[kReluItems];
+    uint32_t c = 0;
+#pragma unroll
+    for (int u = 0; u < kReluItems; ++u) {
+        v[u] = (my + u < n) ? vals[my + u] : 0.0f;
+        c += v[u] > 0.0f;
+    }
+    __shared__ uint32_t sm[32];
+    uint32_t tot;
+    uint64_t pos = off[blockIdx.x] + block_excl_scan(c, sm, &tot);
+#pragma unroll
+    for (int u = 0; u < kReluItems; ++u) {
+        if (v[u] > 0.0f) {
+            ok[pos] = keys[my + u];
+            ov[pos] = v[u];
+            if (osrc) osrc[pos] = my + u;
+            ++pos;
+        }
+    }
+}
+
+cudaError_t launch_relu(const uint64_t* keys, const float* vals, const int64_t* nnz_dev, int64_t nbound,
+                        uint32_t* chunk_cnt, uint64_t* chunk_off, uint64_t* scan_tmp,
+                        uint64_t* out_keys, float* out_vals, int64_t* out_src, int64_t* out_nnz, cudaStream_t s) {
+    const int64_t nch = (nbound + kReluChunk - 1) / kReluChunk;
+    if (nch == 0) return cudaMemsetAsync(out_nnz, 0, sizeof(int64_t), s);
+    { SPC_PHASE("relu_count", s, 1); relu_count_kernel<<<(unsigned)nch, kReluThreads, 0, s>>>(vals, nnz_dev, nbound, chunk_cnt); }
+    cudaError_t e = launch_scan_u32(chunk_cnt, chunk_off, nch, out_nnz, scan_tmp, s);
+    if (e != cudaSuccess) return e;
+    { SPC_PHASE("relu_write", s, 1); relu_write_kernel<<<(unsigned)nch, kReluThreads, 0, s>>>(keys, vals, nnz_dev, nbound, chunk_off, out_keys,
+                                                             out_vals, out_src); }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------- max-pool
+// §3.3: "features are assigned to an output (hyper-) voxel, by dividing ... their index by
+// strides", then the max is taken per cluster. The paper sorts by voxel (Eq. (2),
+// O(n log n)); here every pooled row segment (b, c, X', Y', z-chunk) is one warp work item:
+// its clusters receive the members from the sx*sy contributing input rows through native
+// shared-memory integer atomics (max on an order-preserving u32 of the value, then min of
+// the entry index among the maxima = smaller key wins, reading R8), and the occupied
+// clusters are compacted in pooled-key order. No sort.
+constexpr int kPoolThreads = 256;
+constexpr int kPoolWarps = kPoolThreads / 32;
+constexpr int kPoolZChunk = 512;
+
+PoolPlan plan_pool(const Geo& g, int sx, int sy, int sz) {
+    PoolPlan p{};
+    p.sx = sx; p.sy = sy; p.sz = sz;
+    p.PX = (g.X + sx - 1) / sx;
+    p.PY = (g.Y + sy - 1) / sy;
+    p.PZ = (g.Z + sz - 1) / sz;
+    p.zchunk = p.PZ < kPoolZChunk ? p.PZ : kPoolZChunk;
+    p.nzc = (p.PZ + p.zchunk - 1) / p.zchunk;
+    p.items = g.B * g.C * (int64_t)p.PX * p.PY * p.nzc;
+    return p;
+}
+
+template <bool WRITE>
+__global__ void __launch_bounds__(kPoolThreads)
+pool_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, const float* __restrict__ vals,
+            const uint32_t* __restrict__ row_ptr, uint32_t* __restrict__ item_cnt,
+            const uint64_t* __restrict__ item_off, uint64_t* __restrict__ ok, float* __restrict__ ov,
+            int64_t* __restrict__ oarg) {
+    __shared__ uint32_t s_best[kPoolWarps][kPoolZChunk];
+    __shared__ uint32_t s_arg[kPoolWarps][kPoolZChunk];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t item = (int64_t)blockIdx.x * kPoolWarps + warp;
+    if (item >= p.items) return;
+    uint32_t* best = s_best[warp];
+    uint32_t* arg = s_arg[warp];
+    const int zc = (int)(item % p.nzc);
+    int64_t r = item / p.nzc;
+    const int py = (int)(r % p.PY);
+    r /= p.PY;
+    const int px = (int)(r % p.PX);
+    const int64_t seg = r / p.PX;
+    const int z0 = zc * p.zchunk;
+    const int nz = min(p.zchunk, p.PZ - z0);
+    for (int i = lane; i < nz; i += 32) {
+        best[i] = 0u;
+        arg[i] = 0xffffffffu;
+    }
+    __syncwarp();
+    const int xa = px * p.sx, xb = min(xa + p.sx, g.X);
+    const int ya = py * p.sy, yb = min(ya + p.sy, g.Y);
+    // pass 1: max per cluster (or occupancy only when counting)
+    for (int x = xa; x < xb; ++x) {
+        for (int y = ya; y < yb; ++y) {
+            const int64_t row = (seg * g.X + x) * (int64_t)g.Y + y;
+            const uint32_t e0 = row_ptr[row], e1 = row_ptr[row + 1];
+            const uint64_t rowbase = (uint64_t)row * (uint64_t)g.Z;
+            for (uint32_t e = e0 + lane; e < e1; e += 32) {
+                const int pz = (int)(keys[e] - rowbase) / p.sz - z0;
+                if (pz < 0 || pz >= nz) continue;
+                if (WRITE) atomicMax(&best[pz], orderable(vals[e]));
+                else best[pz] = 1u;
+            }
+        }
+    }
+    __syncwarp();
+    if (!WRITE) {
+        uint32_t c = 0;
+        for (int i = lane; i < nz; i += 32) c += best[i] != 0u;
+        c = warp_sum(c);
+        if (lane == 0) item_cnt[item] = c;
+        return;
+    }
+    // pass 2: smallest entry index among the maxima (argmax, ties -> smaller key)
+    for (int x = xa; x < xb; ++x) {
+        for (int y = ya; y < yb; ++y) {
+            const int64_t row = (seg * g.X + x) * (int64_t)g.Y + y;
+            const uint32_t e0 = row_ptr[row], e1 = row_ptr[row + 1];
+            const uint64_t rowbase = (uint64_t)row * (uint64_t)g.Z;
+            for (uint32_t e = e0 + lane; e < e1; e += 32) {
+                const int pz = (int)(keys[e] - rowbase) / p.sz - z0;
+                if (pz < 0 || pz >= nz) continue;
+                if (orderable(vals[e]) == best[pz]) atomicMin(&arg[pz], e);
+            }
+        }
+    }
+    __syncwarp();
+    uint64_t pos = item_off[item];
+    const uint64_t pbase = ((uint64_t)(seg * p.PX + px) * p.PY + py) * (uint64_t)p.PZ + z0;
+    for (int i0 = 0; i0 < nz; i0 += 32) {
+        const int i = i0 + lane;
+        const bool occ = i < nz && best[i] != 0u;
+        const unsigned m = __ballot_sync(kFull, occ);
+        if (occ) {
+            const uint64_t o = pos + __popc(m & ((1u << lane) - 1u));
+            const uint32_t a = arg[i];
+            ok[o] = pbase + i;
+            ov[o] = vals[a];
+            if (oarg) oarg[o] = a;
+        }
+        pos += __popc(m);
+    }
+}
+
+cudaError_t launch_maxpool(const Geo& g, const PoolPlan& p, const uint64_t* keys, const float* vals,
+                           const uint32_t* row_ptr, uint32_t* item_cnt, uint64_t* item_off, uint64_t* scan_tmp,
+                           uint64_t* out_keys, float* out_vals, int64_t* out_arg, int64_t* out_nnz, cudaStream_t s) {
+    if (p.items == 0) return cudaMemsetAsync(out_nnz, 0, sizeof(int64_t), s);
+    const unsigned grid = (unsigned)((p.items + kPoolWarps - 1) / kPoolWarps);
+    { SPC_PHASE("pool_count", s, 1); pool_kernel<false><<<grid, kPoolThreads, 0, s>>>(g, p, keys, vals, row_ptr, item_cnt, nullptr, nullptr, nullptr,
+                                                     nullptr); }
+    cudaError_t e = launch_scan_u32(item_cnt, item_off, p.items, out_nnz, scan_tmp, s);
+    if (e != cudaSuccess) return e;
+    { SPC_PHASE("pool_write", s, 1); pool_kernel<true><<<grid, kPoolThreads, 0, s>>>(g, p, keys, vals, row_ptr, item_cnt, item_off, out_keys, out_vals,
+                                                    out_arg); }
+    return cudaGetLastError();
+}
+
+}  // namespace spc

@@ -1,0 +1,189 @@
+// Internal declarations of libspconv (not part of the ABI). sm_100a only.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#include "../../include/spconv.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libspconv is written for sm_100a (B200) only"
+#endif
+
+namespace spc {
+
+// Absent marker for the dense pre-attention buffer: a NaN pattern. Finite inputs never
+// produce it (NaN/Inf inputs are outside the contract).
+constexpr uint32_t kAbsent = 0x7fffffffu;
+
+// Geometry of a feature map with its spatial dims padded to rank 3 (leading 1s):
+// key = seg*V + (x*Y + y)*Z + z, seg = b*C + c. A "row" is (seg, x, y): the Z consecutive
+// keys of the last spatial dimension.
+struct Geo {
+    int64_t B, C;
+    int X, Y, Z;
+    int64_t V;   // X*Y*Z
+    int64_t R;   // rows per segment = X*Y
+};
+
+// Filter geometry padded to rank 3; h = ksize/2 (centre).
+struct KGeo {
+    int kx, ky, kz;
+    int hx, hy, hz;
+    int KV;
+};
+
+// Packed signed offset o = delta - centre per dim, 10 bits each (|o| < 512).
+__host__ __device__ inline int pack_off(int ox, int oy, int oz) {
+    return (ox + 512) | ((oy + 512) << 10) | ((oz + 512) << 20);
+}
+__device__ __forceinline__ int off_x(int p) { return (p & 1023) - 512; }
+__device__ __forceinline__ int off_y(int p) { return ((p >> 10) & 1023) - 512; }
+__device__ __forceinline__ int off_z(int p) { return ((p >> 20) & 1023) - 512; }
+
+// Order-preserving u32 scores of fp32 values (reading R7: -0 == +0, larger = stronger).
+__device__ __forceinline__ uint32_t score_bits(uint32_t bits, int attn) {
+    if (attn == SPC_ATTN_MAGNITUDE) return bits & 0x7fffffffu;
+    if (bits == 0x80000000u) bits = 0u;                       // -0 -> +0
+    return (bits & 0x80000000u) ? ~bits : (bits | 0x80000000u);
+}
+
+// Order-preserving u32 of a float for max-pooling; never 0 for non-NaN inputs (0 = empty).
+__device__ __forceinline__ uint32_t orderable(float v) {
+    uint32_t b = __float_as_uint(v);
+    if (b == 0x80000000u) b = 0u;
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float from_orderable(uint32_t o) {
+    uint32_t b = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+    return __uint_as_float(b);
+}
+
+__device__ __forceinline__ int64_t load_n(const int64_t* nnz_dev, int64_t bound) {
+    if (!nnz_dev) return bound;
+    int64_t n = *nnz_dev;
+    return n < bound ? n : bound;
+}
+
+// ------------------------------------------------------------- launch accounting (prof.cu)
+void note_launch(int n = 1);
+struct PhaseScope {
+    PhaseScope(const char* name, cudaStream_t s);
+    ~PhaseScope();
+    const char* name_;
+    cudaStream_t s_;
+    cudaEvent_t a_, b_;
+};
+#define SPC_CAT2(a, b) a##b
+#define SPC_CAT(a, b) SPC_CAT2(a, b)
+// Brackets the kernel launches of the enclosing scope (one kernel = one note_launch).
+#define SPC_PHASE(name, stream, nk) \
+    ::spc::note_launch(nk);         \
+    ::spc::PhaseScope SPC_CAT(_spc_phase_, __LINE__)(name, stream)
+
+// ------------------------------------------------------------------ launchers (host)
+// Row index: row_ptr[r] = first entry with key >= r*Z, r in [0, B*C*R]; workspace
+// (B*C*R + 1) uint32 words. Requires nnz < 2^32.
+cudaError_t launch_row_index(const Geo& g, const uint64_t* keys, const int64_t* nnz_dev, int64_t nnz_bound,
+                             uint32_t* row_ptr, cudaStream_t s);
+
+// Filter table in ic-major order. meta[j] = {oc, packed offset}; val[j]; off[ic*(c_out+1)+oc]
+// = first table entry of (ic, oc) (off[ic*(c_out+1)+c_out] = end); src[j] = original filter
+// position of table entry j. scratch: 2*c_in*c_out ints.
+cudaError_t launch_filter_table(const KGeo& kg, int c_in, int c_out, const uint64_t* wkeys, const float* wvals,
+                                int64_t nw, int2* meta, float* val, int* off, int* src, int* scratch, cudaStream_t s);
+
+struct ConvTile {
+    int TX, TY;       // output rows per tile
+    int ocg;          // output channels per CTA
+    int ntx, nty;     // tiles along x, y
+    int n_ocg;        // groups of output channels
+    size_t smem;      // dynamic shared memory bytes
+};
+ConvTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out);
+cudaError_t launch_conv_fwd(const Geo& gx, const Geo& gy, const KGeo& kg, const ConvTile& t,
+                            const uint64_t* xkeys, const float* xvals, const uint32_t* xrow,
+                            const int2* wmeta, const float* wval, const int* woff, const float* bias,
+                            float* pre, unsigned long long* seg_count, cudaStream_t s);
+
+struct BwdTile {
+    int TX, TY, ocg, ntx, nty, n_ocg, grid;
+    size_t smem;
+};
+BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int n_w_max_group);
+cudaError_t launch_conv_bwd(const Geo& gx, const Geo& gy, const KGeo& kg, const BwdTile& t,
+                            const uint64_t* xkeys, const float* xvals, const uint32_t* xrow,
+                            const uint64_t* ykeys, const float* dy, const uint32_t* yrow,
+                            const int2* wmeta, const float* wval, const int* woff, const int* wsrc,
+                            float* dx, double* dw_acc, bool want_dx, bool want_dw, cudaStream_t s);
+cudaError_t launch_dbias(const Geo& gy, const uint64_t* ykeys, const float* dy, const int64_t* ny_dev,
+                         int64_t ny_bound, double* db_acc, cudaStream_t s);
+cudaError_t launch_f64_to_f32(const double* a, float* b, int64_t n, cudaStream_t s);
+
+// ---------------------------------------------------------------- selection (attention)
+struct SelState {
+    uint32_t prefix;   // known high bits of the threshold score T
+    uint32_t pmask;    // which bits of prefix are known
+    int64_t need;      // entries with score == T to keep (after the last pass)
+    int64_t kept;      // min(k, n) for the segment
+    int32_t keep_all;  // 1: keep every present entry (n <= k or no attention)
+    int32_t pad;
+};
+struct ChunkRec {
+    uint32_t gt, eq;          // entries with score > T / == T in the chunk
+    uint64_t out_off;         // output offset of the chunk within its segment
+    uint64_t tie_before;      // entries == T in earlier chunks of the segment
+};
+constexpr int kSelChunk = 4096;   // elements per chunk (256 threads x 16)
+constexpr int kSelBins = 2048;    // 11-bit digits
+
+// Source of a selection: dense pre-attention buffer (kind 0) or compact COO (kind 1).
+struct SelSrc {
+    int kind;
+    int attn;
+    int64_t nseg;
+    int64_t V;
+    int64_t nchunk;             // chunks per segment (grid.x)
+    // dense
+    const float* pre;           // [nseg*V]
+    const unsigned long long* seg_count;  // support counts per segment (dense)
+    // compact
+    const uint64_t* keys;
+    const float* vals;
+    const uint32_t* row_ptr;    // segment s starts at row_ptr[s*R]
+    int64_t R;
+};
+cudaError_t launch_select(const SelSrc& src, int64_t k, SelState* st, uint32_t* hist, ChunkRec* rec,
+                          uint64_t* seg_off, uint64_t* out_keys, float* out_vals, int64_t* out_src,
+                          int64_t* out_nnz, cudaStream_t s);
+
+// --------------------------------------------------------------------- relu / pool / misc
+cudaError_t launch_relu(const uint64_t* keys, const float* vals, const int64_t* nnz_dev, int64_t nbound,
+                        uint32_t* chunk_cnt, uint64_t* chunk_off, uint64_t* scan_tmp,
+                        uint64_t* out_keys, float* out_vals, int64_t* out_src, int64_t* out_nnz, cudaStream_t s);
+struct PoolPlan {
+    int sx, sy, sz;
+    int PX, PY, PZ;       // pooled dims
+    int zchunk;           // pooled z positions per work item
+    int nzc;              // z chunks per pooled row
+    int64_t items;        // B*C*PX*PY*nzc
+};
+PoolPlan plan_pool(const Geo& g, int sx, int sy, int sz);
+cudaError_t launch_maxpool(const Geo& g, const PoolPlan& p, const uint64_t* keys, const float* vals,
+                           const uint32_t* row_ptr, uint32_t* item_cnt, uint64_t* item_off, uint64_t* scan_tmp,
+                           uint64_t* out_keys, float* out_vals, int64_t* out_arg, int64_t* out_nnz, cudaStream_t s);
+cudaError_t launch_scatter_grad(const int64_t* src, const float* dy, int64_t n_out_bound, const int64_t* n_out_dev,
+                                float* dx, int64_t n_in, cudaStream_t s);
+
+// Device-wide exclusive scan of uint32 counts into uint64 offsets; total -> *total (int64,
+// may be NULL). tmp: scan_tmp_words(n) uint64 words.
+size_t scan_tmp_words(int64_t n);
+cudaError_t launch_scan_u32(const uint32_t* in, uint64_t* out, int64_t n, int64_t* total, uint64_t* tmp,
+                            cudaStream_t s);
+
+// Validation (SPC_VALIDATE=1): flag = 1 if keys are not strictly increasing or out of range.
+cudaError_t launch_validate(const uint64_t* keys, const int64_t* nnz_dev, int64_t nbound, uint64_t limit,
+                            int* flag, cudaStream_t s);
+
+}  // namespace spc

@@ -1,0 +1,315 @@
+"""Python binding of the C-ABI (same names as include/spconv.h). Marshalling only: every step
+of the hot path runs in libspconv's CUDA kernels. PyTorch provides device memory and streams.
+
+Sparse maps live on the device as (keys int64 [capacity], values float32 [capacity]) plus a
+device nnz word; nothing here synchronises unless `.nnz()` / `.trimmed()` is called.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence, Tuple
+
+import torch
+
+from . import _lib
+from ._lib import ATTN, FilterT, MapOutT, MapT, check
+
+
+def _stream(stream: Optional[torch.cuda.Stream]):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+@dataclass
+class SparseMap:
+    """Device COO feature map: key = ((b*C + c)*V + row_major(p)) (include/spconv.h)."""
+
+    keys: torch.Tensor          # int64 (bit pattern of the uint64 keys), [capacity]
+    values: torch.Tensor        # float32 [capacity]
+    batch: int
+    channels: int
+    dims: Tuple[int, ...]
+    nnz_bound: int              # host upper bound (exact when nnz_dev is None)
+    nnz_dev: Optional[torch.Tensor] = None   # int64 [1] exact count on the device
+
+    @property
+    def ndim(self) -> int:
+        return len(self.dims)
+
+    @property
+    def volume(self) -> int:
+        v = 1
+        for d in self.dims:
+            v *= int(d)
+        return v
+
+    def nnz(self) -> int:
+        """Exact count (synchronises when it lives on the device)."""
+        return int(self.nnz_dev.item()) if self.nnz_dev is not None else int(self.nnz_bound)
+
+    def trimmed(self) -> Tuple[torch.Tensor, torch.Tensor]:
+        n = self.nnz()
+        return self.keys[:n], self.values[:n]
+
+    def exact(self) -> "SparseMap":
+        """Same map with a host-exact nnz (synchronises once)."""
+        n = self.nnz()
+        return SparseMap(self.keys[:n], self.values[:n], self.batch, self.channels, self.dims, n, None)
+
+    def c_struct(self) -> MapT:
+        m = MapT()
+        m.ndim = self.ndim
+        m.batch = self.batch
+        m.channels = self.channels
+        for i, d in enumerate(self.dims):
+            m.dims[i] = int(d)
+        m.nnz = int(self.nnz_bound)
+        m.nnz_dev = None if self.nnz_dev is None else self.nnz_dev.data_ptr()
+        m.keys = self.keys.data_ptr() if self.keys.numel() else None
+        m.values = self.values.data_ptr() if self.values.numel() else None
+        return m
+
+    @staticmethod
+    def from_arrays(keys, values, batch: int, channels: int, dims: Sequence[int], device="cuda") -> "SparseMap":
+        """Upload host arrays (numpy uint64 keys / float32 values, or tensors)."""
+        if not isinstance(keys, torch.Tensor):
+            import numpy as np
+
+            keys = torch.from_numpy(np.ascontiguousarray(keys).view(np.int64))
+        if not isinstance(values, torch.Tensor):
+            values = torch.from_numpy(values)
+        k = keys.to(device=device, dtype=torch.int64).contiguous()
+        v = values.to(device=device, dtype=torch.float32).contiguous()
+        return SparseMap(k, v, int(batch), int(channels), tuple(int(d) for d in dims), int(k.numel()), None)
+
+
+@dataclass
+class SparseFilter:
+    """Device filter bank: key = ((oc*c_in + ic)*prod(ksize) + row_major(delta))."""
+
+    keys: torch.Tensor
+    values: torch.Tensor
+    c_in: int
+    c_out: int
+    ksize: Tuple[int, ...]
+
+    def c_struct(self) -> FilterT:
+        f = FilterT()
+        f.ndim = len(self.ksize)
+        f.c_in = self.c_in
+        f.c_out = self.c_out
+        for i, k in enumerate(self.ksize):
+            f.ksize[i] = int(k)
+        f.nnz = int(self.keys.numel())
+        f.keys = self.keys.data_ptr() if self.keys.numel() else None
+        f.values = self.values.data_ptr() if self.values.numel() else None
+        return f
+
+    @staticmethod
+    def from_arrays(keys, values, c_in: int, c_out: int, ksize: Sequence[int], device="cuda") -> "SparseFilter":
+        if not isinstance(keys, torch.Tensor):
+            import numpy as np
+
+            keys = torch.from_numpy(np.ascontiguousarray(keys).view(np.int64))
+        if not isinstance(values, torch.Tensor):
+            values = torch.from_numpy(values)
+        return SparseFilter(keys.to(device=device, dtype=torch.int64).contiguous(),
+                            values.to(device=device, dtype=torch.float32).contiguous(),
+                            int(c_in), int(c_out), tuple(int(k) for k in ksize))
+
+
+def load():
+    return _lib.load()
+
+
+def version() -> str:
+    return load().spc_version().decode()
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def _out(cap: int, device) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor, MapOutT]:
+    keys = torch.empty(max(cap, 1), dtype=torch.int64, device=device)
+    vals = torch.empty(max(cap, 1), dtype=torch.float32, device=device)
+    nnz = torch.zeros(1, dtype=torch.int64, device=device)
+    o = MapOutT()
+    o.capacity = int(cap)
+    o.keys = keys.data_ptr()
+    o.values = vals.data_ptr()
+    o.nnz_dev = nnz.data_ptr()
+    return keys, vals, nnz, o
+
+
+class FwdPlan:
+    """Queries once, then reuses output and workspace buffers across calls with the same
+    shapes (for timing loops and CUDA-graph capture)."""
+
+    def __init__(self, x: SparseMap, w: SparseFilter, attn: str = "magnitude", k: int = 0):
+        lib = load()
+        self.attn = ATTN[attn]
+        self.k = int(k)
+        cap = C.c_int64()
+        ws = C.c_size_t()
+        xs, fs = x.c_struct(), w.c_struct()
+        check("spc_conv_fwd_query", lib.spc_conv_fwd_query(C.byref(xs), C.byref(fs), self.attn, self.k,
+                                                           C.byref(cap), C.byref(ws)))
+        dev = x.values.device
+        self.capacity = int(cap.value)
+        self.ws = _workspace(ws.value, dev)
+        self.keys, self.vals, self.nnz, self.out = _out(self.capacity, dev)
+        self.c_out = w.c_out
+        self.batch, self.dims = x.batch, x.dims
+
+    def __call__(self, x: SparseMap, w: SparseFilter, bias: Optional[torch.Tensor] = None,
+                 stream: Optional[torch.cuda.Stream] = None) -> SparseMap:
+        xs, fs = x.c_struct(), w.c_struct()
+        rc = load().sparse_conv_fwd(C.byref(xs), C.byref(fs), _ptr(bias), self.attn, self.k, C.byref(self.out),
+                                    _ptr(self.ws), self.ws.numel(), _stream(stream))
+        check("sparse_conv_fwd", rc)
+        return SparseMap(self.keys, self.vals, self.batch, self.c_out, self.dims, self.capacity, self.nnz)
+
+
+def sparse_conv_fwd(x: SparseMap, w: SparseFilter, bias: Optional[torch.Tensor] = None, attn: str = "magnitude",
+                    k: int = 0, stream=None) -> SparseMap:
+    """Alg. 1. attn in {"none", "magnitude", "raw"}; k entries kept per (b, oc)."""
+    return FwdPlan(x, w, attn, k)(x, w, bias, stream)
+
+
+class BwdPlan:
+    def __init__(self, x: SparseMap, w: SparseFilter, y: SparseMap):
+        lib = load()
+        ws = C.c_size_t()
+        xs, fs, ys = x.c_struct(), w.c_struct(), y.c_struct()
+        check("spc_conv_bwd_query", lib.spc_conv_bwd_query(C.byref(xs), C.byref(fs), C.byref(ys), C.byref(ws)))
+        self.ws = _workspace(ws.value, x.values.device)
+
+    def __call__(self, x, w, y, dy, dx=None, dw=None, dbias=None, stream=None):
+        xs, fs, ys = x.c_struct(), w.c_struct(), y.c_struct()
+        lib = load()
+        st = _stream(stream)
+        if dx is not None and dw is not None:
+            rc = lib.sparse_conv_bwd(C.byref(xs), C.byref(fs), C.byref(ys), _ptr(dy), _ptr(dx), _ptr(dw), _ptr(dbias),
+                                     _ptr(self.ws), self.ws.numel(), st)
+            check("sparse_conv_bwd", rc)
+        elif dx is not None:
+            rc = lib.sparse_conv_bwd_input(C.byref(xs), C.byref(fs), C.byref(ys), _ptr(dy), _ptr(dx),
+                                           _ptr(self.ws), self.ws.numel(), st)
+            check("sparse_conv_bwd_input", rc)
+        elif dw is not None:
+            rc = lib.sparse_conv_bwd_weight(C.byref(xs), C.byref(fs), C.byref(ys), _ptr(dy), _ptr(dw), _ptr(dbias),
+                                            _ptr(self.ws), self.ws.numel(), st)
+            check("sparse_conv_bwd_weight", rc)
+        return dx, dw, dbias
+
+
+def sparse_conv_bwd(x: SparseMap, w: SparseFilter, y: SparseMap, dy: torch.Tensor, need_dx=True, need_dw=True,
+                    need_dbias=True, stream=None):
+    """Alg. 2, Eqs. (3)/(4). Returns (dx [nnz_x], dw [nnz_w], dbias [c_out])."""
+    dev = x.values.device
+    dx = torch.empty(max(x.nnz_bound, 1), dtype=torch.float32, device=dev) if need_dx else None
+    dw = torch.empty(max(w.keys.numel(), 1), dtype=torch.float32, device=dev) if need_dw else None
+    db = torch.empty(w.c_out, dtype=torch.float32, device=dev) if need_dbias else None
+    BwdPlan(x, w, y)(x, w, y, dy, dx, dw, db, stream)
+    return (dx[:x.nnz_bound] if dx is not None else None, dw[:w.keys.numel()] if dw is not None else None, db)
+
+
+def sparse_conv_bwd_input(x, w, y, dy, stream=None):
+    return sparse_conv_bwd(x, w, y, dy, True, False, False, stream)[0]
+
+
+def sparse_conv_bwd_weight(x, w, y, dy, stream=None):
+    _, dw, db = sparse_conv_bwd(x, w, y, dy, False, True, True, stream)
+    return dw, db
+
+
+def attention_topk(x: SparseMap, attn: str, k: int, stream=None) -> Tuple[SparseMap, torch.Tensor]:
+    """Attention as a standalone layer. Returns (kept map, src index)."""
+    lib = load()
+    cap = C.c_int64()
+    ws = C.c_size_t()
+    xs = x.c_struct()
+    a = ATTN[attn]
+    check("spc_topk_query", lib.spc_topk_query(C.byref(xs), a, int(k), C.byref(cap), C.byref(ws)))
+    dev = x.values.device
+    keys, vals, nnz, o = _out(int(cap.value), dev)
+    src = torch.empty(max(int(cap.value), 1), dtype=torch.int64, device=dev)
+    w = _workspace(ws.value, dev)
+    check("attention_topk", lib.attention_topk(C.byref(xs), a, int(k), C.byref(o), _ptr(src), _ptr(w), w.numel(),
+                                               _stream(stream)))
+    return SparseMap(keys, vals, x.batch, x.channels, x.dims, int(cap.value), nnz), src
+
+
+def sparse_relu(x: SparseMap, stream=None) -> Tuple[SparseMap, torch.Tensor]:
+    """Sparse ReLU. Returns (kept map, src index)."""
+    lib = load()
+    cap = C.c_int64()
+    ws = C.c_size_t()
+    xs = x.c_struct()
+    check("spc_relu_query", lib.spc_relu_query(C.byref(xs), C.byref(cap), C.byref(ws)))
+    dev = x.values.device
+    keys, vals, nnz, o = _out(int(cap.value), dev)
+    src = torch.empty(max(int(cap.value), 1), dtype=torch.int64, device=dev)
+    w = _workspace(ws.value, dev)
+    check("sparse_relu", lib.sparse_relu(C.byref(xs), C.byref(o), _ptr(src), _ptr(w), w.numel(), _stream(stream)))
+    return SparseMap(keys, vals, x.batch, x.channels, x.dims, int(cap.value), nnz), src
+
+
+def sparse_maxpool(x: SparseMap, stride: Sequence[int], stream=None) -> Tuple[SparseMap, torch.Tensor]:
+    """Sparse max-pooling (§3.3). Returns (pooled map with dims ceil(d/s), argmax index)."""
+    lib = load()
+    cap = C.c_int64()
+    ws = C.c_size_t()
+    xs = x.c_struct()
+    st = (C.c_int64 * len(stride))(*[int(s) for s in stride])
+    check("spc_maxpool_query", lib.spc_maxpool_query(C.byref(xs), C.cast(st, C.c_void_p), C.byref(cap), C.byref(ws)))
+    dev = x.values.device
+    keys, vals, nnz, o = _out(int(cap.value), dev)
+    arg = torch.empty(max(int(cap.value), 1), dtype=torch.int64, device=dev)
+    w = _workspace(ws.value, dev)
+    check("sparse_maxpool", lib.sparse_maxpool(C.byref(xs), C.cast(st, C.c_void_p), C.byref(o), _ptr(arg), _ptr(w),
+                                               w.numel(), _stream(stream)))
+    pdims = tuple(-(-int(d) // int(s)) for d, s in zip(x.dims, stride))
+    return SparseMap(keys, vals, x.batch, x.channels, pdims, int(cap.value), nnz), arg
+
+
+def sparse_scatter_grad(src: torch.Tensor, dy: torch.Tensor, n_out_bound: int, n_in: int,
+                        n_out_dev: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Backward of ReLU / pool / top-k (Eq. (5)): dx[src[t]] = dy[t], zeros elsewhere."""
+    dx = torch.empty(max(n_in, 1), dtype=torch.float32, device=dy.device)
+    check("sparse_scatter_grad", load().sparse_scatter_grad(_ptr(src), _ptr(dy), int(n_out_bound), _ptr(n_out_dev),
+                                                            _ptr(dx), int(n_in), _stream(stream)))
+    return dx[:n_in]
+
+
+# ------------------------------------------------------------------ instrumentation
+def kernel_launches() -> int:
+    """Kernels launched by libspconv so far in this process."""
+    return int(load().spc_kernel_launches())
+
+
+def profile_enable(on: bool = True):
+    load().spc_profile_enable(1 if on else 0)
+
+
+def profile_reset():
+    load().spc_profile_reset()
+
+
+def profile_read():
+    """{phase: (total_ms, launches)} of the CUDA-event brackets recorded while enabled."""
+    import numpy as np
+
+    n = 64
+    names = C.create_string_buffer(8192)
+    ms = np.zeros(n, np.float64)
+    cnt = np.zeros(n, np.int64)
+    k = load().spc_profile_read(names, 8192, ms.ctypes.data_as(C.c_void_p), cnt.ctypes.data_as(C.c_void_p), n)
+    labels = names.raw.split(b"\0")[:k]
+    return {lab.decode(): (float(ms[i]), int(cnt[i])) for i, lab in enumerate(labels)}

@@ -14,7 +14,8 @@ can generate only its shard and obtain exactly the rows of the full batch.
 
 Value modes:
 * "continuous": U[-1, 1] without 0;
-* "dyadic": j/64 with j in [-64, 64] \\ {0}. Products of two such values are multiples of
+* "dyadic": j/64 with j in [-64, 64] \\ {0}; "dyadic4": j/4 with j in [-4, 4] \\ {0} (coarse grid
+  for deeper layers of a chain, so that exactness survives several layers). Products of two such values are multiples of
   2^-12; sums of fewer than 2^12 such products are exact in fp32 in any order, which makes the
   GPU and the oracle agree bit for bit.
 """
@@ -82,6 +83,9 @@ def _draw_values(rng: np.random.Generator, n: int, mode: str) -> np.ndarray:
     if mode == "dyadic":
         j = rng.integers(1, 65, size=n) * rng.choice(np.array([-1, 1]), size=n)
         return (j.astype(np.float32) / np.float32(64.0)).astype(np.float32)
+    if mode == "dyadic4":
+        j = rng.integers(1, 5, size=n) * rng.choice(np.array([-1, 1]), size=n)
+        return (j.astype(np.float32) / np.float32(4.0)).astype(np.float32)
     if mode == "positive":
         return rng.uniform(0.05, 1.0, size=n).astype(np.float32)
     raise ValueError(f"unknown value mode {mode!r}")

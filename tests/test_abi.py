@@ -1,0 +1,117 @@
+"""The C-ABI library loads and exports every symbol include/spconv.h declares; host-side
+argument validation (no device work) returns the documented codes. Runs without a GPU."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+import pytest
+
+import paper_1801_10585_b200 as spc
+from paper_1801_10585_b200 import _lib
+from paper_1801_10585_b200._lib import FilterT, MapT
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "spconv.h")
+
+
+def header_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\*?\s+\**([a-z_0-9]+)\s*\(", src, flags=re.M)))
+
+
+def test_header_declares_the_north_star_calls():
+    fns = header_functions()
+    for name in ["sparse_conv_fwd", "sparse_conv_bwd_input", "sparse_conv_bwd_weight", "sparse_relu",
+                 "sparse_maxpool", "attention_topk"]:
+        assert name in fns
+    assert sorted(_lib.EXPORTS) == fns
+
+
+def test_library_exports_every_declared_symbol():
+    lib = spc.load()
+    for name in header_functions():
+        assert hasattr(lib, name), name
+    out = os.popen(f"nm -D {_lib.LIB_PATH}").read()
+    for name in header_functions():
+        assert re.search(rf" T {name}$", out, flags=re.M), name
+
+
+def test_version_and_status_strings():
+    lib = spc.load()
+    assert b"sm_100a" in lib.spc_version()
+    assert lib.spc_status_string(3) == b"output capacity too small"
+
+
+def _c4_structs(ks=(3, 3, 3), c_in=8, ndim=3):
+    m = MapT()
+    m.ndim, m.batch, m.channels = ndim, 64, 8
+    for i in range(ndim):
+        m.dims[i] = 128
+    m.nnz, m.keys, m.values = 53687296, 64, 64   # dummy non-null device pointers (never read)
+    f = FilterT()
+    f.ndim, f.c_in, f.c_out = ndim, c_in, 8
+    for i in range(ndim):
+        f.ksize[i] = ks[i]
+    f.nnz, f.keys, f.values = 864, 64, 64
+    return m, f
+
+
+def _query(m, f, attn=1, k=104857):
+    cap, ws = C.c_int64(), C.c_size_t()
+    rc = spc.load().spc_conv_fwd_query(C.byref(m), C.byref(f), attn, k, C.byref(cap), C.byref(ws))
+    return rc, cap.value, ws.value
+
+
+def test_fwd_query_capacity_is_the_density_bound():
+    m, f = _c4_structs()
+    rc, cap, ws = _query(m, f)
+    assert rc == 0
+    assert cap == 64 * 8 * 104857        # b * c_out * min(k, V): the rho_up guarantee
+    assert ws > 64 * 8 * 128 ** 3 * 4    # dense pre-attention buffer
+    rc, cap, _ = _query(m, f, attn=0)
+    assert rc == 0 and cap == 64 * 8 * 128 ** 3
+
+
+@pytest.mark.parametrize("mut,code", [
+    (lambda m, f: setattr(f, "c_in", 4), 2),                 # c_in mismatch -> SPC_ERR_SHAPE
+    (lambda m, f: f.ksize.__setitem__(0, 2), 2),             # even kernel -> SPC_ERR_SHAPE
+    (lambda m, f: setattr(m, "ndim", 4), 6),                 # rank 4 -> SPC_ERR_UNSUPPORTED
+    (lambda m, f: setattr(m, "keys", None), 1),              # NULL keys -> SPC_ERR_INVALID_ARG
+    (lambda m, f: setattr(m, "channels", 0), 2),
+])
+def test_fwd_query_rejects_bad_arguments(mut, code):
+    m, f = _c4_structs()
+    mut(m, f)
+    assert _query(m, f)[0] == code
+
+
+def test_fwd_query_rejects_k_below_one():
+    m, f = _c4_structs()
+    assert _query(m, f, attn=1, k=0)[0] == 1
+    assert _query(m, f, attn=0, k=0)[0] == 0    # no attention: k unused
+
+
+def test_bwd_and_pool_queries():
+    m, f = _c4_structs()
+    ws = C.c_size_t()
+    assert spc.load().spc_conv_bwd_query(C.byref(m), C.byref(f), C.byref(m), C.byref(ws)) == 0
+    st = (C.c_int64 * 3)(2, 2, 2)
+    cap = C.c_int64()
+    assert spc.load().spc_maxpool_query(C.byref(m), C.cast(st, C.c_void_p), C.byref(cap), C.byref(ws)) == 0
+    assert cap.value == m.nnz
+    bad = (C.c_int64 * 3)(2, 0, 2)
+    assert spc.load().spc_maxpool_query(C.byref(m), C.cast(bad, C.c_void_p), C.byref(cap), C.byref(ws)) == 2
+
+
+def test_product_package_does_not_import_oracle():
+    import sys
+
+    for mod in list(sys.modules):
+        if mod.startswith("paper_1801_10585_b200"):
+            src = getattr(sys.modules[mod], "__file__", None)
+            if src and src.endswith(".py"):
+                text = open(src).read()
+                assert "import oracle" not in text and "from oracle" not in text

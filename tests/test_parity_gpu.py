@@ -1,0 +1,401 @@
+"""Parity of the CUDA path (through the C-ABI) with the CPU oracle on identical seeded inputs.
+
+Bar: keys, masks, argmax and src indices bit-exact; with dyadic
+inputs every value and gradient bit-exact too (all fp32 sums exact in any order); with
+continuous inputs |gpu - ora| <= 1e-5 |ora| + 1e-6 sum|terms| and attention sets equal up to
+near-threshold swaps.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle as ora
+from synth import (COO, Filter, uniform_map, mnist_like, surface_occupancy, sparse_filter, bias_vector, grad_values,
+                   select_samples, SEED_BASE)
+from tests._compare import assert_values_close, assert_topk_sets_match
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ATTN_ORA = {"none": ora.ATTN_NONE, "magnitude": ora.ATTN_MAGNITUDE, "raw": ora.ATTN_RAW}
+
+
+def dev_map(spc, x: COO):
+    return spc.SparseMap.from_arrays(x.keys, x.values, x.batch, x.channels, x.dims)
+
+
+def dev_filter(spc, w: Filter):
+    return spc.SparseFilter.from_arrays(w.keys, w.values, w.c_in, w.c_out, w.ksize)
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def host_keys(t):
+    return host(t).view(np.uint64)
+
+
+def run_fwd(spc, x, w, bias, attn, k):
+    y = spc.sparse_conv_fwd(dev_map(spc, x), dev_filter(spc, w),
+                            None if bias is None else torch.from_numpy(bias).cuda(), attn, k)
+    yk, yv = y.trimmed()
+    return host_keys(yk), host(yv), y
+
+
+FWD_CASES = [
+    # name, dims, batch, c_in, c_out, ksize, rho_d, rho_f
+    ("1d", (37,), 3, 2, 3, (3,), 0.2, 0.7),
+    ("2d_8x8", (8, 8), 2, 2, 3, (3, 3), 0.2, 0.5),
+    ("2d_5x3k", (13, 17), 2, 3, 5, (5, 3), 0.1, 0.8),
+    ("3d_small", (9, 7, 11), 2, 3, 4, (3, 3, 3), 0.08, 0.5),
+    ("3d_tiles", (24, 20, 40), 2, 8, 8, (3, 3, 3), 0.03, 0.5),   # several tiles + ragged tail
+    ("3d_k1", (6, 6, 6), 2, 4, 6, (1, 1, 1), 0.3, 1.0),
+    ("3d_wide_oc", (10, 12, 14), 1, 2, 40, (3, 3, 3), 0.05, 0.3),  # several oc groups
+    ("3d_long_z", (3, 3, 700), 2, 2, 3, (3, 3, 3), 0.05, 0.5),
+]
+
+
+@pytest.mark.parametrize("case", FWD_CASES, ids=lambda c: c[0])
+@pytest.mark.parametrize("attn", ["none", "magnitude", "raw"])
+def test_fwd_dyadic_bit_exact(cuda_lib, case, attn):
+    spc = cuda_lib
+    _, dims, B, ci, co, ks, rd, rf = case
+    x = uniform_map(B, ci, dims, rd, 1000 + len(dims), values="dyadic")
+    w = sparse_filter(ci, co, ks, rf, 1001, values="dyadic")
+    bias = bias_vector(co, 1002, values="dyadic")
+    V = int(np.prod(dims))
+    k = max(1, V // 20)
+    ok_, ov, _, _ = ora.conv_fwd(x, w, bias, attn=ATTN_ORA[attn], k=k)
+    gk, gv, _ = run_fwd(spc, x, w, bias, attn, k)
+    np.testing.assert_array_equal(gk, ok_)
+    np.testing.assert_array_equal(gv, ov)
+
+
+@pytest.mark.parametrize("case", FWD_CASES, ids=lambda c: c[0])
+@pytest.mark.parametrize("attn", ["none", "magnitude", "raw"])
+def test_fwd_continuous_tolerance(cuda_lib, case, attn):
+    spc = cuda_lib
+    _, dims, B, ci, co, ks, rd, rf = case
+    x = uniform_map(B, ci, dims, rd, 2000 + len(dims))
+    w = sparse_filter(ci, co, ks, rf, 2001)
+    bias = bias_vector(co, 2002)
+    V = int(np.prod(dims))
+    k = max(1, V // 20)
+    fk, fv, fa, _ = ora.conv_fwd(x, w, bias, with_abs=True)           # exact support + scales
+    gk, gv, _ = run_fwd(spc, x, w, bias, attn, k)
+    if attn == "none":
+        np.testing.assert_array_equal(gk, fk)                           # structural support: exact
+        assert_values_close(gv, fv, fa)
+        return
+    ok_, ov, _, _ = ora.conv_fwd(x, w, bias, attn=ATTN_ORA[attn], k=k)
+    assert_topk_sets_match(gk, gv, ok_, ov, fk, fv, fa, V, k, attn)
+    # values at common keys
+    common, gi, oi = np.intersect1d(gk, ok_, return_indices=True)
+    idx = np.searchsorted(fk, common)
+    assert_values_close(gv[gi], ov[oi], fa[idx])
+
+
+def test_fwd_mnist_like_c1(cuda_lib):
+    """BASELINE configs[0]: 2D 28x28, 1->8, 3x3, rho_up 15%, batch 4 (k = floor(0.15*784))."""
+    spc = cuda_lib
+    x = mnist_like(4, SEED_BASE, values="dyadic")
+    w = sparse_filter(1, 8, (3, 3), 1.0, SEED_BASE, values="dyadic")
+    bias = bias_vector(8, SEED_BASE, values="dyadic")
+    k = int(0.15 * 784)
+    ok_, ov, _, _ = ora.conv_fwd(x, w, bias, attn=ora.ATTN_MAGNITUDE, k=k)
+    gk, gv, _ = run_fwd(spc, x, w, bias, "magnitude", k)
+    np.testing.assert_array_equal(gk, ok_)
+    np.testing.assert_array_equal(gv, ov)
+
+
+def test_fwd_binary_surface_ties(cuda_lib):
+    """Binary occupancy (value 1.0): massive exact ties at the threshold (reading R7)."""
+    spc = cuda_lib
+    x = surface_occupancy(2, 24, 0.05, 77)
+    w = sparse_filter(1, 4, (3, 3, 3), 1.0, 77, values="dyadic")
+    k = int(0.05 * 24 ** 3)
+    for attn in ("magnitude", "raw"):
+        ok_, ov, _, _ = ora.conv_fwd(x, w, None, attn=ATTN_ORA[attn], k=k)
+        gk, gv, _ = run_fwd(spc, x, w, None, attn, k)
+        np.testing.assert_array_equal(gk, ok_)
+        np.testing.assert_array_equal(gv, ov)
+
+
+def test_fwd_empty_and_degenerate(cuda_lib):
+    spc = cuda_lib
+    x = COO(2, 2, (5, 6), np.zeros(0, np.uint64), np.zeros(0, np.float32))
+    w = sparse_filter(2, 3, (3, 3), 0.5, 3)
+    gk, gv, y = run_fwd(spc, x, w, None, "magnitude", 4)
+    assert gk.size == 0
+    # empty filter
+    x = uniform_map(2, 2, (5, 6), 0.3, 4)
+    w0 = Filter(2, 3, (3, 3), np.zeros(0, np.uint64), np.zeros(0, np.float32))
+    gk, _, _ = run_fwd(spc, x, w0, None, "none", 0)
+    assert gk.size == 0
+    # k >= V: identity on the support
+    w = sparse_filter(2, 3, (3, 3), 0.5, 3)
+    fk, fv, _, _ = ora.conv_fwd(x, w, None)
+    gk, gv, _ = run_fwd(spc, x, w, None, "magnitude", 10 ** 6)
+    np.testing.assert_array_equal(gk, fk)
+    # a stored 0.0 input stays structurally present (reading R3)
+    xz = COO(1, 1, (5,), np.array([2], np.uint64), np.array([0.0], np.float32))
+    wz = Filter(1, 1, (3,), np.arange(3, dtype=np.uint64), np.ones(3, np.float32))
+    gk, gv, _ = run_fwd(spc, xz, wz, None, "none", 0)
+    assert gk.tolist() == [1, 2, 3] and not gv.any()
+
+
+def test_fwd_device_nnz_input(cuda_lib):
+    """Input with a device nnz word and a larger host bound (chained layers, no host sync)."""
+    spc = cuda_lib
+    x = uniform_map(2, 2, (9, 10, 11), 0.1, 5, values="dyadic")
+    w = sparse_filter(2, 3, (3, 3, 3), 0.5, 5, values="dyadic")
+    d = dev_map(spc, x)
+    pad = 1000
+    keys = torch.cat([d.keys, torch.full((pad,), 2 ** 62, dtype=torch.int64, device="cuda")])
+    vals = torch.cat([d.values, torch.ones(pad, device="cuda")])
+    nnz = torch.tensor([x.nnz], dtype=torch.int64, device="cuda")
+    dd = spc.SparseMap(keys, vals, d.batch, d.channels, d.dims, x.nnz + pad, nnz)
+    y = spc.sparse_conv_fwd(dd, dev_filter(spc, w), None, "magnitude", 50)
+    yk, yv = y.trimmed()
+    ok_, ov, _, _ = ora.conv_fwd(x, w, None, attn=ora.ATTN_MAGNITUDE, k=50)
+    np.testing.assert_array_equal(host_keys(yk), ok_)
+    np.testing.assert_array_equal(host(yv), ov)
+
+
+# ----------------------------------------------------------------------------- backward
+BWD_CASES = [
+    ("2d", (12, 11), 2, 2, 3, (3, 3), 0.2, 0.6),
+    ("3d", (10, 9, 12), 2, 3, 4, (3, 3, 3), 0.06, 0.5),
+    ("3d_tiles", (20, 24, 36), 2, 8, 8, (3, 3, 3), 0.03, 0.5),
+    ("3d_wide_oc", (8, 9, 10), 1, 2, 40, (3, 3, 3), 0.06, 0.4),
+    ("1d_k5", (50,), 3, 2, 2, (5,), 0.2, 0.8),
+]
+
+
+@pytest.mark.parametrize("case", BWD_CASES, ids=lambda c: c[0])
+@pytest.mark.parametrize("values", ["dyadic", "continuous"])
+def test_bwd_parity(cuda_lib, case, values):
+    spc = cuda_lib
+    _, dims, B, ci, co, ks, rd, rf = case
+    x = uniform_map(B, ci, dims, rd, 3000, values=values)
+    w = sparse_filter(ci, co, ks, rf, 3001, values=values)
+    bias = bias_vector(co, 3002, values=values)
+    V = int(np.prod(dims))
+    k = max(1, V // 10)
+    yk, yv, _, _ = ora.conv_fwd(x, w, bias, attn=ora.ATTN_MAGNITUDE, k=k)   # kept keys (oracle)
+    dy = grad_values(yk.shape[0], 3003, values=values)
+    dx, dw, db, dxa, dwa = ora.conv_bwd(x, w, yk, dy, with_abs=True)
+    X, W = dev_map(spc, x), dev_filter(spc, w)
+    Y = spc.SparseMap.from_arrays(yk, yv, B, co, dims)
+    gdx, gdw, gdb = spc.sparse_conv_bwd(X, W, Y, torch.from_numpy(dy).cuda())
+    gdx, gdw, gdb = host(gdx), host(gdw), host(gdb)
+    if values == "dyadic":
+        np.testing.assert_array_equal(gdx, dx)
+        np.testing.assert_array_equal(gdw, dw)
+        np.testing.assert_array_equal(gdb, db)
+    else:
+        assert_values_close(gdx, dx, dxa, "dx")
+        assert_values_close(gdw, dw, dwa, "dw")
+        assert_values_close(gdb, db, np.full(co, np.abs(dy).sum()), "dbias")
+    # separate entry points agree with the oracle too (dx sums over several output-channel
+    # groups with fp32 atomics when c_out > 16, so run-to-run bits may differ there)
+    gdx2 = host(spc.sparse_conv_bwd_input(X, W, Y, torch.from_numpy(dy).cuda()))
+    gdw2, gdb2 = spc.sparse_conv_bwd_weight(X, W, Y, torch.from_numpy(dy).cuda())
+    assert_values_close(gdx2, dx, dxa, "dx (bwd_input)")
+    assert_values_close(host(gdw2), dw, dwa, "dw (bwd_weight)")
+    if values == "dyadic" or co <= 16:
+        np.testing.assert_array_equal(gdx2, gdx)
+    np.testing.assert_array_equal(host(gdb2), gdb)
+
+
+def test_bwd_zero_dy_and_empty(cuda_lib):
+    spc = cuda_lib
+    x = uniform_map(2, 2, (7, 8), 0.3, 9)
+    w = sparse_filter(2, 2, (3, 3), 0.5, 9)
+    yk, yv, _, _ = ora.conv_fwd(x, w, None)
+    Y = spc.SparseMap.from_arrays(yk, yv, 2, 2, (7, 8))
+    gdx, gdw, gdb = spc.sparse_conv_bwd(dev_map(spc, x), dev_filter(spc, w), Y,
+                                        torch.zeros(yk.shape[0], device="cuda"))
+    assert not host(gdx).any() and not host(gdw).any() and not host(gdb).any()
+    Ye = spc.SparseMap.from_arrays(np.zeros(0, np.uint64), np.zeros(0, np.float32), 2, 2, (7, 8))
+    gdx, gdw, gdb = spc.sparse_conv_bwd(dev_map(spc, x), dev_filter(spc, w), Ye, torch.zeros(1, device="cuda"))
+    assert not host(gdx).any() and not host(gdw).any() and not host(gdb).any()
+
+
+# ----------------------------------------------------------------------- other layers
+@pytest.mark.parametrize("attn", ["magnitude", "raw"])
+def test_topk_parity(cuda_lib, attn):
+    spc = cuda_lib
+    x = uniform_map(3, 4, (11, 13, 9), 0.3, 41, values="dyadic")   # many exact ties
+    k = 37
+    ok_, ov, osrc = ora.topk(x, ATTN_ORA[attn], k)
+    y, src = spc.attention_topk(dev_map(spc, x), attn, k)
+    yk, yv = y.trimmed()
+    n = yk.shape[0]
+    np.testing.assert_array_equal(host_keys(yk), ok_)
+    np.testing.assert_array_equal(host(yv), ov)
+    np.testing.assert_array_equal(host(src[:n]), osrc)
+
+
+def test_topk_large_segments(cuda_lib):
+    spc = cuda_lib
+    x = uniform_map(2, 2, (64, 64, 16), 0.2, 43)   # segments of 13k entries, several chunks
+    k = 2000
+    ok_, ov, osrc = ora.topk(x, ora.ATTN_MAGNITUDE, k)
+    y, src = spc.attention_topk(dev_map(spc, x), "magnitude", k)
+    yk, yv = y.trimmed()
+    np.testing.assert_array_equal(host_keys(yk), ok_)
+    np.testing.assert_array_equal(host(yv), ov)
+    np.testing.assert_array_equal(host(src[:yk.shape[0]]), osrc)
+
+
+def test_relu_parity(cuda_lib):
+    spc = cuda_lib
+    for x in [uniform_map(3, 5, (17, 19), 0.3, 51), uniform_map(1, 1, (10,), 0.0, 1),
+              uniform_map(2, 3, (40, 40, 10), 0.2, 52)]:
+        ok_, ov, osrc = ora.relu(x)
+        y, src = spc.sparse_relu(dev_map(spc, x))
+        yk, yv = y.trimmed()
+        np.testing.assert_array_equal(host_keys(yk), ok_)
+        np.testing.assert_array_equal(host(yv), ov)
+        np.testing.assert_array_equal(host(src[:yk.shape[0]]), osrc)
+
+
+@pytest.mark.parametrize("dims,stride", [((28, 28), (2, 2)), ((7, 9), (2, 3)), ((16, 16, 16), (2, 2, 2)),
+                                         ((5, 7, 1100), (2, 3, 2)), ((30,), (4,))])
+def test_maxpool_parity(cuda_lib, dims, stride):
+    spc = cuda_lib
+    x = uniform_map(2, 3, dims, 0.3, 61, values="dyadic")   # exact ties exercise the argmax rule
+    ok_, ov, oarg = ora.maxpool(x, stride)
+    y, arg = spc.sparse_maxpool(dev_map(spc, x), stride)
+    yk, yv = y.trimmed()
+    np.testing.assert_array_equal(host_keys(yk), ok_)
+    np.testing.assert_array_equal(host(yv), ov)
+    np.testing.assert_array_equal(host(arg[:yk.shape[0]]), oarg)
+
+
+def test_scatter_grad_parity(cuda_lib):
+    spc = cuda_lib
+    x = uniform_map(2, 3, (9, 9), 0.4, 71)
+    _, _, src = ora.relu(x)
+    dy = grad_values(src.shape[0], 71)
+    want = ora.scatter_grad(src, dy, x.nnz)
+    got = spc.sparse_scatter_grad(torch.from_numpy(src).cuda(), torch.from_numpy(dy).cuda(), src.shape[0], x.nnz)
+    np.testing.assert_array_equal(host(got), want)
+
+
+def test_chain_c2_like_device_nnz(cuda_lib):
+    """BASELINE configs[1] shape (smaller batch): 3 x [conv+attention -> ReLU -> maxpool2],
+    1->8->16->32, chained on the device with no host sync between layers. Dyadic values on
+    coarsening grids; the oracle certifies (sum|terms| * 2^e < 2^24) that blocks 1-2 are
+    exact in fp32 in any order, so they must match bit for bit; block 3 is compared with the
+    tolerance rule."""
+    spc = cuda_lib
+    x = mnist_like(16, SEED_BASE + 1, values="dyadic")
+    chans = [1, 8, 16, 32]
+    ks = [117, 29, 7]
+    ws = [sparse_filter(1, 8, (3, 3), 1.0, 80, values="dyadic", scale=0.25),
+          sparse_filter(8, 16, (3, 3), 1.0, 81, values="dyadic4", scale=0.125),
+          sparse_filter(16, 32, (3, 3), 1.0, 82, values="dyadic4", scale=0.125)]
+    bs = [bias_vector(chans[i + 1], 90 + i, values="dyadic") for i in range(3)]
+    grid_e = [14, 19, 24]
+    g = dev_map(spc, x)
+    cur = x
+    for i in range(3):
+        yk, yv, ya, _ = ora.conv_fwd(cur, ws[i], bs[i], attn=ora.ATTN_MAGNITUDE, k=ks[i], with_abs=True)
+        g = spc.sparse_conv_fwd(g, dev_filter(spc, ws[i]), torch.from_numpy(bs[i]).cuda(), "magnitude", ks[i])
+        gk, gv = g.trimmed()
+        if i < 2:
+            assert np.all(ya * 2.0 ** grid_e[i] < 2.0 ** 24)     # exactness certificate
+            np.testing.assert_array_equal(host_keys(gk), yk)
+            np.testing.assert_array_equal(host(gv), yv)
+        else:
+            fk, fv, fa, _ = ora.conv_fwd(cur, ws[i], bs[i], with_abs=True)
+            assert_topk_sets_match(host_keys(gk), host(gv), yk, yv, fk, fv, fa, 49, ks[i], "magnitude")
+            return
+        cur = COO(cur.batch, chans[i + 1], cur.dims, yk, yv)
+        rk, rv, _ = ora.relu(cur)
+        cur = COO(cur.batch, chans[i + 1], cur.dims, rk, rv)
+        pk, pv, _ = ora.maxpool(cur, (2, 2))
+        cur = COO(cur.batch, chans[i + 1], tuple(-(-d // 2) for d in cur.dims), pk, pv)
+        g, _ = spc.sparse_relu(g)
+        g, _ = spc.sparse_maxpool(g, (2, 2))
+        gk, gv = g.trimmed()
+        np.testing.assert_array_equal(host_keys(gk), cur.keys)
+        np.testing.assert_array_equal(host(gv), cur.values)
+
+
+# ------------------------------------------------------------------------------ errors
+def test_error_codes(cuda_lib):
+    spc = cuda_lib
+    from paper_1801_10585_b200._lib import SpconvError
+    import ctypes as C
+
+    x = uniform_map(1, 2, (6, 6), 0.3, 3)
+    w = sparse_filter(2, 2, (3, 3), 0.5, 3)
+    X, W = dev_map(spc, x), dev_filter(spc, w)
+    plan = spc.FwdPlan(X, W, "magnitude", 5)
+    plan.out.capacity = 3
+    with pytest.raises(SpconvError) as e:
+        plan(X, W)
+    assert e.value.code == 3
+    plan.out.capacity = plan.capacity
+    small = plan.ws[:16]
+    plan.ws = small
+    with pytest.raises(SpconvError) as e:
+        plan(X, W)
+    assert e.value.code == 4
+
+
+def test_validate_env_detects_unsorted(cuda_lib, monkeypatch):
+    spc = cuda_lib
+    from paper_1801_10585_b200._lib import SpconvError
+
+    x = uniform_map(1, 2, (6, 6), 0.5, 3)
+    keys = x.keys.copy()
+    keys[[1, 2]] = keys[[2, 1]]
+    bad = COO(1, 2, (6, 6), keys, x.values)
+    monkeypatch.setenv("SPC_VALIDATE", "1")
+    with pytest.raises(SpconvError) as e:
+        spc.sparse_relu(dev_map(spc, bad))
+    assert e.value.code == 5
+    spc.sparse_relu(dev_map(spc, x))   # sorted input passes validation
+
+
+# ------------------------------------------------------------- full size (bench config)
+@pytest.mark.slow
+def test_c4_full_size_sampled(cuda_lib):
+    """BASELINE configs[3] at full size in the bench launch configuration: 128^3, b=64, 8->8,
+    rho_d 2%, rho_f 0.5, rho_up 5%. The GPU runs the whole batch; the oracle recomputes two
+    sampled samples (forward and dx are per-sample) on dyadic inputs -> bit-exact; nnz bound
+    holds for every (b, oc)."""
+    spc = cuda_lib
+    import bench
+
+    cfg = bench.c4_inputs(density=0.02, values="dyadic")
+    x, w, bias, k = cfg["x"], cfg["w"], cfg["bias"], cfg["k"]
+    X, W = dev_map(spc, x), dev_filter(spc, w)
+    y = spc.sparse_conv_fwd(X, W, torch.from_numpy(bias).cuda(), "magnitude", k)
+    yk, yv = y.trimmed()
+    gk, gv = host_keys(yk), host(yv)
+    V = 128 ** 3
+    seg = (gk // np.uint64(V)).astype(np.int64)
+    assert np.bincount(seg, minlength=64 * 8).max() <= k
+    dy = grad_values(gk.shape[0], SEED_BASE + 7, values="dyadic")
+    gdx, gdw, gdb = spc.sparse_conv_bwd(X, W, spc.SparseMap.from_arrays(gk, gv, 64, 8, (128,) * 3),
+                                        torch.from_numpy(dy).cuda())
+    gdx = host(gdx)
+    span = np.uint64(8 * V)
+    for b in (0, 37):
+        xs = select_samples(x, [b])
+        ok_, ov, _, _ = ora.conv_fwd(xs, w, bias, attn=ora.ATTN_MAGNITUDE, k=k)
+        lo, hi = np.searchsorted(gk, np.uint64(b) * span), np.searchsorted(gk, np.uint64(b + 1) * span)
+        np.testing.assert_array_equal(gk[lo:hi] - np.uint64(b) * span, ok_)
+        np.testing.assert_array_equal(gv[lo:hi], ov)
+        odx, _, _, _, _ = ora.conv_bwd(xs, w, ok_, dy[lo:hi])
+        xlo, xhi = np.searchsorted(x.keys, np.uint64(b) * span), np.searchsorted(x.keys, np.uint64(b + 1) * span)
+        np.testing.assert_array_equal(gdx[xlo:xhi], odx)
