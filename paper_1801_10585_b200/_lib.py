@@ -54,10 +54,12 @@ _lib = None
 
 
 def load(path: str = LIB_PATH):
-    """Load libspconv.so. Fails loudly when the library is missing: there is no fallback."""
+    """Load libspconv.so. Fails loudly when the library is missing: there is no fallback.
+    SPC_LIB=<path> selects another build of the same library (e.g. libspconv_debug.so)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("SPC_LIB", path)
     if not os.path.exists(path):
         raise ImportError(f"libspconv.so not found at {path}; run `python -c 'import __graft_entry__ as g; g.build()'`"
                           " (there is no CPU fallback)")

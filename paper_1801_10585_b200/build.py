@@ -40,16 +40,19 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, debug: bool = False) -> str:
+    """debug=True builds libspconv_debug.so with -DSPC_DEBUG (device-side bounds reports)."""
+    lib = LIB if not debug else os.path.join(HERE, "libspconv_debug.so")
+    if not force and not debug and not needs_build():
         return LIB
     objs = []
-    bdir = os.path.join(HERE, "build")
+    bdir = os.path.join(HERE, "build" if not debug else "build_debug")
     os.makedirs(bdir, exist_ok=True)
     procs = []
     for src in sources():
         obj = os.path.join(bdir, os.path.basename(src)[:-3] + ".o")
-        cmd = [_nvcc(), "-c", src, "-o", obj] + NVCC_FLAGS + (["-Xptxas", "-v"] if ptxas_v else [])
+        cmd = [_nvcc(), "-c", src, "-o", obj] + NVCC_FLAGS + (["-Xptxas", "-v"] if ptxas_v else []) + \
+              (["-DSPC_DEBUG"] if debug else [])
         if verbose:
             print(" ".join(cmd), flush=True)
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -63,12 +66,13 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
             failed.append(src)
     if failed:
         raise RuntimeError(f"nvcc failed for {failed}")
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     subprocess.check_call([_nvcc(), "-shared", "-o", tmp] + objs +
                           ["-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, ptxas_v="--ptxas" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, ptxas_v="--ptxas" in sys.argv,
+                debug="--debug" in sys.argv))

@@ -132,18 +132,16 @@ FilterWs carve_filter(Carver& c, const spc_filter_t* w) {
 // ----------------------------------------------------------------------- forward
 struct FwdWs {
     uint32_t* xrow;
-    FilterWs f;
-    float* pre;
-    unsigned long long* seg_count;
-    SelState* st;
-    uint32_t* hist;
-    ChunkRec* rec;
-    uint64_t* seg_off;
+    int2* meta2;
+    float* val2;
+    int* off2;
+    int* scratch2;
+    FwdArgs a;
     int* flag;
 };
 
 spc_status_t fwd_plan(const spc_map_t* x, const spc_filter_t* w, spc_attn_t attn, int64_t k, Geo* gx, Geo* gy,
-                      KGeo* kg, ConvTile* t, int64_t* cap) {
+                      KGeo* kg, FwdTile* t, int64_t* cap) {
     SPC_TRY(check_map(x));
     SPC_TRY(check_filter(w, x, kg));
     if (attn != SPC_ATTN_NONE && attn != SPC_ATTN_MAGNITUDE && attn != SPC_ATTN_RAW) return SPC_ERR_INVALID_ARG;
@@ -152,23 +150,36 @@ spc_status_t fwd_plan(const spc_map_t* x, const spc_filter_t* w, spc_attn_t attn
     *gy = geo_of(x, w->c_out);
     const int64_t per = attn != SPC_ATTN_NONE ? std::min<int64_t>(k, gy->V) : gy->V;
     *cap = x->batch * w->c_out * per;
-    *t = plan_fwd_tile(*gy, *kg, (int)w->c_out);
+    *t = plan_fwd_tile(*gy, *kg, (int)w->c_out, (int)w->c_in, w->nnz);
     if (t->smem == 0) return SPC_ERR_UNSUPPORTED;
     return SPC_OK;
 }
 
-FwdWs carve_fwd(Carver& c, const Geo& gx, const Geo& gy, const spc_filter_t* w) {
+// Candidate capacity: the threshold bucket of a segment holds at most its whole support, so the
+// worst case is nseg*V entries (binary data with massive ties); typical use is ~1-2% of that.
+FwdWs carve_fwd(Carver& c, const Geo& gx, const Geo& gy, const KGeo& kg, const FwdTile& t, const spc_filter_t* w,
+                spc_attn_t attn) {
     FwdWs ws{};
     const int64_t nseg = gy.B * gy.C;
-    const int64_t nchunk = (gy.V + kSelChunk - 1) / kSelChunk;
+    const size_t KXY = (size_t)kg.kx * kg.ky;
     ws.xrow = c.take<uint32_t>((size_t)(gx.B * gx.C * gx.R + 1));
-    ws.f = carve_filter(c, w);
-    ws.pre = c.take<float>((size_t)(nseg * gy.V));
-    ws.seg_count = c.take<unsigned long long>((size_t)nseg);
-    ws.st = c.take<SelState>((size_t)nseg);
-    ws.hist = c.take<uint32_t>((size_t)nseg * kSelBins);
-    ws.rec = c.take<ChunkRec>((size_t)(nseg * nchunk));
-    ws.seg_off = c.take<uint64_t>((size_t)nseg + 1);
+    ws.meta2 = c.take<int2>((size_t)w->nnz);
+    ws.val2 = c.take<float>((size_t)w->nnz);
+    ws.off2 = c.take<int>((size_t)w->c_in * KXY * (w->c_out + 1));
+    ws.scratch2 = c.take<int>((size_t)2 * w->c_in * KXY * w->c_out);
+    FwdArgs& a = ws.a;
+    a.seg_count = c.take<unsigned long long>((size_t)nseg);
+    a.hist = c.take<uint32_t>((size_t)nseg * kSelBins);
+    a.seg = c.take<FwdSeg>((size_t)nseg);
+    a.tile_cnt = c.take<uint32_t>((size_t)nseg * t.NT);
+    a.tile_def = c.take<uint32_t>((size_t)nseg * t.NT);
+    a.tile_sel = c.take<uint32_t>((size_t)nseg * t.NT);
+    a.tile_off = c.take<uint64_t>((size_t)nseg * t.NT);
+    a.cand_off = c.take<uint64_t>((size_t)nseg + 1);
+    a.cand_cnt = c.take<uint64_t>((size_t)nseg + 1);
+    a.cand_cur = c.take<unsigned long long>((size_t)nseg);
+    a.cand = c.take<uint2>(attn == SPC_ATTN_NONE ? 1 : (size_t)(nseg * gy.V));
+    a.seg_off = c.take<uint64_t>((size_t)nseg + 1);
     ws.flag = c.take<int>(1);
     return ws;
 }
@@ -346,11 +357,11 @@ spc_status_t spc_conv_fwd_query(const spc_map_t* x, const spc_filter_t* w, spc_a
                                 int64_t* out_capacity, size_t* workspace_bytes) {
     Geo gx, gy;
     KGeo kg;
-    ConvTile t;
+    FwdTile t;
     int64_t cap;
     SPC_TRY(fwd_plan(x, w, attn, k, &gx, &gy, &kg, &t, &cap));
     Carver m(nullptr);
-    carve_fwd(m, gx, gy, w);
+    carve_fwd(m, gx, gy, kg, t, w, attn);
     if (out_capacity) *out_capacity = cap;
     if (workspace_bytes) *workspace_bytes = m.used;
     return SPC_OK;
@@ -360,32 +371,33 @@ spc_status_t sparse_conv_fwd(const spc_map_t* x, const spc_filter_t* w, const fl
                              spc_map_out_t* y, void* workspace, size_t workspace_bytes, cudaStream_t s) {
     Geo gx, gy;
     KGeo kg;
-    ConvTile t;
+    FwdTile t;
     int64_t cap;
     SPC_TRY(fwd_plan(x, w, attn, k, &gx, &gy, &kg, &t, &cap));
     SPC_TRY(check_out(y, cap));
     Carver m(nullptr);
-    carve_fwd(m, gx, gy, w);
+    carve_fwd(m, gx, gy, kg, t, w, attn);
     if (!workspace || workspace_bytes < m.used) return SPC_ERR_WORKSPACE;
     Carver c(workspace);
-    FwdWs ws = carve_fwd(c, gx, gy, w);
+    FwdWs ws = carve_fwd(c, gx, gy, kg, t, w, attn);
     if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
-    const int64_t nseg = gy.B * gy.C;
-    SPC_TRY(cu(cudaMemsetAsync(ws.seg_count, 0, sizeof(unsigned long long) * (size_t)std::max<int64_t>(1, nseg), s)));
     SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
-    SPC_TRY(cu(launch_filter_table(kg, (int)w->c_in, (int)w->c_out, w->keys, w->values, w->nnz, ws.f.meta, ws.f.val,
-                                   ws.f.off, ws.f.src, ws.f.scratch, s)));
-    SPC_TRY(cu(launch_conv_fwd(gx, gy, kg, t, x->keys, x->values, ws.xrow, ws.f.meta, ws.f.val, ws.f.off, bias,
-                               ws.pre, ws.seg_count, s)));
-    SelSrc src{};
-    src.kind = 0;
-    src.attn = attn;
-    src.nseg = nseg;
-    src.V = gy.V;
-    src.nchunk = (gy.V + kSelChunk - 1) / kSelChunk;
-    src.pre = ws.pre;
-    src.seg_count = ws.seg_count;
-    return cu(launch_select(src, k, ws.st, ws.hist, ws.rec, ws.seg_off, y->keys, y->values, nullptr, y->nnz_dev, s));
+    SPC_TRY(cu(launch_filter_table_fwd(kg, (int)w->c_in, (int)w->c_out, w->keys, w->values, w->nnz, ws.meta2, ws.val2,
+                                       ws.off2, ws.scratch2, s)));
+    FwdArgs a = ws.a;
+    a.xkeys = x->keys;
+    a.xvals = x->values;
+    a.xrow = ws.xrow;
+    a.meta2 = ws.meta2;
+    a.val2 = ws.val2;
+    a.off2 = ws.off2;
+    a.bias = bias;
+    a.attn = attn;
+    a.k = attn == SPC_ATTN_NONE ? gy.V : k;
+    a.out_keys = y->keys;
+    a.out_vals = y->values;
+    a.out_nnz = y->nnz_dev;
+    return cu(launch_conv_fwd_pipeline(gx, gy, kg, t, a, s));
 }
 
 spc_status_t spc_conv_bwd_query(const spc_map_t* x, const spc_filter_t* w, const spc_map_t* y,

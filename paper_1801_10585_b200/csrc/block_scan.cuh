@@ -25,7 +25,8 @@ __device__ __forceinline__ T warp_sum(T v) {
     return v;
 }
 
-// Block exclusive scan; every thread of the block must call it. `sm` needs 32 T.
+// Block exclusive scan; every thread of the block must call it. `sm` needs 33 T (one slot per
+// warp plus the block total, kept apart so that 32-warp blocks do not overwrite warp 31's prefix).
 // Returns the exclusive prefix of v; *total receives the block sum (all threads).
 template <typename T>
 __device__ __forceinline__ T block_excl_scan(T v, T* sm, T* total) {
@@ -37,11 +38,11 @@ __device__ __forceinline__ T block_excl_scan(T v, T* sm, T* total) {
         T s = lane < nw ? sm[lane] : T(0);
         T si = warp_incl_scan(s);
         if (lane < nw) sm[lane] = si - s;
-        if (lane == nw - 1) sm[31] = si;
+        if (lane == nw - 1) sm[32] = si;
     }
     __syncthreads();
     T res = inc - v + sm[wid];
-    *total = sm[31];
+    *total = sm[32];
     __syncthreads();
     return res;
 }

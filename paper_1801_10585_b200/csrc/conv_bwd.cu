@@ -1,16 +1,17 @@
 // Backward of the sparse convolution, Alg. 2 with the masked rule of Eqs. (3)/(4)
 // (P:121-129): gradients only at stored inputs (dx) and stored weights (dw).
 //
-// B200 mapping: Alg. 2 initialises a dense buffer with the gradients of
-// (b, oc) and, for every (input, weight) pair, reads g at uid and atomically adds
-// g*fval to bp_data and g*val to bp_filter. Here a persistent CTA owns a group of
-// output channels and walks (b, spatial tile) work items: the gradients of the tile plus its
-// halo are scattered into a dense shared-memory buffer (zeros elsewhere = attention-dropped or
-// non-existent outputs, reading R10), each lane owns one stored input entry and accumulates
-// its dx in a register over all stored weights (no atomics on bp_data), and the dw
-// contributions go to a per-CTA fp64 shared array that is flushed once per CTA. Lanes visit
-// the weights in a lane-rotated order so that the 32 shared-memory updates of one step hit 32
-// different weights.
+// B200 mapping: Alg. 2 initialises a dense buffer with the
+// gradients of (b, oc) and for every (input, weight) pair reads g at uid and atomically
+// adds g*fval to bp_data and g*val to bp_filter. Here a persistent CTA owns a group
+// of output channels and walks (b, spatial tile) items. The gradients of the tile plus halo are
+// scattered into a zero shared-memory buffer G with margins (attention-dropped and absent
+// outputs read 0, reading R10; out-of-grid targets land in the margin). The stored entries of
+// the tile are processed in warp-level 32x32 blocks: lane L owns weight j0+L, the warp walks 32
+// staged entries; g = G[ebase(e) - wdel(j)] is one shared load; lane L accumulates g*x into its
+// dw register and the 32x32 products g*w are reduced across lanes with a shuffle
+// reduce-scatter that leaves dx(e) in lane e. No atomics on dx inside a group; dw goes to a
+// per-CTA fp64 shared array once per block and to global fp64 once per CTA.
 #include "spc_internal.cuh"
 #include "block_scan.cuh"
 
@@ -18,74 +19,109 @@
 
 namespace spc {
 
-constexpr int kBwdThreads = 256;
+constexpr int kBwdThreads = 512;
 constexpr size_t kBwdBudget = 200 * 1024;
+
+static size_t bwd_smem(const KGeo& kg, int c_in, int TX, int TY, int ZR, int ocg, int64_t nwg) {
+    const size_t g = (size_t)ocg * (TX + 2 * kg.hx) * (TY + 2 * kg.hy) * ZR * sizeof(float);
+    const size_t w = (size_t)nwg * (sizeof(int) + sizeof(float) + sizeof(double));
+    const size_t idx = (size_t)(c_in + 1) * sizeof(int) * 2 + (size_t)c_in * TX * 2 * sizeof(uint32_t);
+    const size_t stage = (size_t)(kBwdThreads / 32) * 32 * (sizeof(int) + sizeof(float));
+    return g + w + idx + stage + 256;
+}
 
 BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int nw_total) {
     BwdTile t{};
     const int c_in = (int)gx.C;
-    const int zr = gx.Z + 2 * kg.hz;
-    int ocg = c_out < 16 ? c_out : 16;
-    for (;;) {
-        const int64_t nwg = std::min<int64_t>((int64_t)nw_total, (int64_t)ocg * c_in * kg.KV);
-        const size_t dwb = (size_t)nwg * sizeof(double) + (size_t)(c_in + 1) * sizeof(int) + 64;
-        const size_t rowb = (size_t)zr * ocg * sizeof(float);
-        if (dwb + rowb * (1 + 2 * kg.hx) * (1 + 2 * kg.hy) <= kBwdBudget || ocg == 1) {
-            const int64_t hrows = dwb >= kBwdBudget ? 0 : (int64_t)((kBwdBudget - dwb) / rowb);
-            double best = -1.0;
-            int bx = 1, by = 1;
-            for (int tx = 1; tx <= gx.X; ++tx) {
-                if ((int64_t)(tx + 2 * kg.hx) * (1 + 2 * kg.hy) > hrows) break;
-                int ty = (int)(hrows / (tx + 2 * kg.hx)) - 2 * kg.hy;
-                if (ty > gx.Y) ty = gx.Y;
-                if (ty < 1) break;
-                const double score = (double)tx * ty / ((double)(tx + 2 * kg.hx) * (ty + 2 * kg.hy)) + 1e-6 * tx * ty;
-                if (score > best) { best = score; bx = tx; by = ty; }
+    const int ZR = gx.Z + 2 * kg.hz;
+    int ocg = std::min(c_out, 8);
+    for (; ocg >= 1; ocg = ocg > 1 ? (ocg + 1) / 2 : 0) {
+        const int64_t nwg = std::min<int64_t>(nw_total, (int64_t)ocg * c_in * kg.KV);
+        double best = -1.0;
+        int bx = 0, by = 0;
+        for (int tx = 1; tx <= gx.X && tx <= 64; ++tx) {
+            int lo = 1, hi = gx.Y, ty = 0;
+            while (lo <= hi) {   // largest ty that fits
+                const int mid = (lo + hi) / 2;
+                if (bwd_smem(kg, c_in, tx, mid, ZR, ocg, nwg) <= kBwdBudget) { ty = mid; lo = mid + 1; }
+                else hi = mid - 1;
             }
-            if (best < 0) { t.smem = 0; return t; }   // does not fit: unsupported
-            t.TX = bx;
-            t.TY = by;
-            t.ocg = ocg;
-            t.n_ocg = (c_out + ocg - 1) / ocg;
-            t.ntx = (gx.X + bx - 1) / bx;
-            t.nty = (gx.Y + by - 1) / by;
-            const size_t gb = (size_t)(bx + 2 * kg.hx) * (by + 2 * kg.hy) * rowb;
-            t.smem = gb + dwb;
-            const int per_sm = (int)std::max<size_t>(1, (228 * 1024) / (t.smem + 1024));
-            const int64_t items = gx.B * t.ntx * t.nty;
-            int64_t grid = (int64_t)148 * std::min(per_sm, 8) / t.n_ocg;
-            if (grid < 1) grid = 1;
-            if (grid > items) grid = items;
-            t.grid = (int)grid;
-            return t;
+            if (ty < 1) break;
+            ty = std::min(ty, 64);
+            const double score = (double)tx * ty / ((double)(tx + 2 * kg.hx) * (ty + 2 * kg.hy)) + 1e-9 * tx * ty;
+            if (score > best) { best = score; bx = tx; by = ty; }
         }
-        ocg = (ocg + 1) / 2;
+        if (best < 0) { if (ocg == 1) break; continue; }
+        t.TX = bx;
+        t.TY = by;
+        t.ocg = ocg;
+        t.n_ocg = (c_out + ocg - 1) / ocg;
+        t.ntx = (gx.X + bx - 1) / bx;
+        t.nty = (gx.Y + by - 1) / by;
+        t.nwg_max = (int)nwg;
+        t.smem = bwd_smem(kg, c_in, bx, by, ZR, ocg, nwg);
+        const int64_t items = gx.B * (int64_t)t.ntx * t.nty;
+        int64_t grid = (148 + t.n_ocg - 1) / t.n_ocg;
+        grid = std::max<int64_t>(1, std::min<int64_t>(grid, items));
+        t.grid = (int)grid;
+        return t;
     }
+    t.smem = 0;
+    return t;
 }
 
-__global__ void __launch_bounds__(kBwdThreads)
+// 32 values per lane -> lane L receives the sum over lanes of v[L] (butterfly reduce-scatter).
+__device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
+#pragma unroll
+    for (int half = 16; half >= 1; half >>= 1) {
+        const bool up = (lane & half) != 0;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+            const float send = up ? v[i] : v[i + half];
+            const float keep = up ? v[i + half] : v[i];
+            v[i] = keep + __shfl_xor_sync(kFull, send, half);
+        }
+    }
+    return v[0];
+}
+
+template <bool DX, bool DW>
+__global__ void __launch_bounds__(kBwdThreads, 1)
 conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__ xkeys,
                 const float* __restrict__ xvals, const uint32_t* __restrict__ xrow,
                 const uint64_t* __restrict__ ykeys, const float* __restrict__ dy, const uint32_t* __restrict__ yrow,
                 const int2* __restrict__ wmeta, const float* __restrict__ wval, const int* __restrict__ woff,
-                const int* __restrict__ wsrc, float* __restrict__ dx, double* __restrict__ dw_acc,
-                int want_dx, int want_dw) {
+                const int* __restrict__ wsrc, float* __restrict__ dx, double* __restrict__ dw_acc) {
     extern __shared__ __align__(16) unsigned char smraw[];
     const int c_in = (int)gx.C, c_out = (int)gy.C;
     const int oc0 = blockIdx.y * t.ocg;
     const int nocl = min(t.ocg, c_out - oc0);
     const int HX = t.TX + 2 * kg.hx, HY = t.TY + 2 * kg.hy;
     const int ZR = gx.Z + 2 * kg.hz;
-    const int hrows = HX * HY;
-    const int gsize = t.ocg * hrows * ZR;
-    // layout: dwp (double) | lbase (int c_in+1) | G (float)
-    double* dwp = reinterpret_cast<double*>(smraw);
-    // local weight bases per ic for this oc group (every thread computes nwg: c_in reads)
-    int nwg = 0;
-    for (int ic = 0; ic < c_in; ++ic)
-        nwg += woff[ic * (c_out + 1) + oc0 + nocl] - woff[ic * (c_out + 1) + oc0];
-    int* lbase = reinterpret_cast<int*>(smraw + (size_t)nwg * sizeof(double));
-    float* G = reinterpret_cast<float*>(smraw + (((size_t)nwg * sizeof(double) + (size_t)(c_in + 1) * sizeof(int) + 15) & ~(size_t)15));
+    const int HXY = HX * HY;
+    const int gsize = t.ocg * HXY * ZR;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+
+    // ---- shared layout: G | dwp | wdel | wv | lbase | cpre | rng | stage
+    float* G = reinterpret_cast<float*>(smraw);
+    unsigned char* p = smraw + (((size_t)gsize * sizeof(float) + 15) & ~(size_t)15);
+    double* dwp = reinterpret_cast<double*>(p);
+    p += (size_t)t.nwg_max * sizeof(double);
+    int* wdel = reinterpret_cast<int*>(p);
+    p += (size_t)t.nwg_max * sizeof(int);
+    float* wv = reinterpret_cast<float*>(p);
+    p += (size_t)t.nwg_max * sizeof(float);
+    int* lbase = reinterpret_cast<int*>(p);
+    p += (size_t)(c_in + 1) * sizeof(int);
+    int* cpre = reinterpret_cast<int*>(p);
+    p += (size_t)(c_in + 1) * sizeof(int);
+    uint32_t* rng = reinterpret_cast<uint32_t*>(p);
+    p += (size_t)c_in * t.TX * 2 * sizeof(uint32_t);
+    p = reinterpret_cast<unsigned char*>(((uintptr_t)p + 15) & ~(uintptr_t)15);
+    int* st_eb = reinterpret_cast<int*>(p) + warp * 64;   // per warp: 32 ebase + 32 values
+    float* st_v = reinterpret_cast<float*>(st_eb + 32);
+
+    // ---- one-time setup: group weights with their G-offsets, zero G and dw partials
     if (threadIdx.x == 0) {
         int acc = 0;
         for (int ic = 0; ic < c_in; ++ic) {
@@ -94,79 +130,158 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
         }
         lbase[c_in] = acc;
     }
+    __syncthreads();
+    const int nwg = lbase[c_in];
+    for (int ic = 0; ic < c_in; ++ic) {
+        const int t0 = woff[ic * (c_out + 1) + oc0];
+        const int n = lbase[ic + 1] - lbase[ic];
+        for (int j = threadIdx.x; j < n; j += blockDim.x) {
+            const int2 m = wmeta[t0 + j];
+            // g at uid = id - (fid - centre): G index = ebase - wdel
+            wdel[lbase[ic] + j] = (off_x(m.y) * HY + off_y(m.y)) * ZR + off_z(m.y) - (m.x - oc0) * HXY * ZR;
+            wv[lbase[ic] + j] = wval[t0 + j];
+        }
+    }
     for (int i = threadIdx.x; i < nwg; i += blockDim.x) dwp[i] = 0.0;
+    for (int i = threadIdx.x; i < gsize; i += blockDim.x) G[i] = 0.0f;
+    const int eb_safe = (kg.hx * HY + kg.hy) * ZR + kg.hz;   // an in-range G index for idle lanes
 
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int64_t items = gx.B * (int64_t)t.ntx * t.nty;
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
         const int64_t b = item / ((int64_t)t.ntx * t.nty);
         const int tile = (int)(item - b * (int64_t)t.ntx * t.nty);
         const int x0 = (tile % t.ntx) * t.TX, y0 = (tile / t.ntx) * t.TY;
+        const int xe = min(x0 + t.TX, gx.X), ye = min(y0 + t.TY, gx.Y);
         __syncthreads();
-        for (int i = threadIdx.x; i < gsize; i += blockDim.x) G[i] = 0.0f;
-        __syncthreads();
-        // "initialize dense buffer with gradients(b, oc)", restricted to tile + halo
-        for (int r = warp; r < nocl * hrows; r += nwarps) {
-            const int ocl = r / hrows, hr = r - ocl * hrows;
+        // "initialize dense buffer with gradients(b, oc)", tile + halo, this oc group
+        for (int r = warp; r < nocl * HXY; r += nwarps) {
+            const int ocl = r / HXY, hr = r - ocl * HXY;
             const int xs = x0 - kg.hx + hr / HY, ys = y0 - kg.hy + hr % HY;
             if (xs < 0 || xs >= gy.X || ys < 0 || ys >= gy.Y) continue;
             const int64_t row = ((b * c_out + oc0 + ocl) * gy.X + xs) * (int64_t)gy.Y + ys;
             const uint32_t e0 = yrow[row], e1 = yrow[row + 1];
             const uint64_t rowbase = (uint64_t)row * (uint64_t)gy.Z;
             for (uint32_t e = e0 + lane; e < e1; e += 32)
-                G[(ocl * hrows + hr) * ZR + (int)(ykeys[e] - rowbase) + kg.hz] = dy[e];
+                G[(ocl * HXY + hr) * ZR + (int)(ykeys[e] - rowbase) + kg.hz] = dy[e];
+        }
+        // entry ranges: per (ic, x) the stored entries of rows y0..ye-1 are contiguous
+        for (int q = threadIdx.x; q < c_in * t.TX; q += blockDim.x) {
+            const int ic = q / t.TX, xi = q - (q / t.TX) * t.TX;
+            uint32_t lo = 0, hi = 0;
+            if (x0 + xi < xe) {
+                const int64_t r0 = ((b * c_in + ic) * gx.X + x0 + xi) * (int64_t)gx.Y + y0;
+                lo = xrow[r0];
+                hi = xrow[r0 + (ye - y0)];
+            }
+            rng[2 * q] = lo;
+            rng[2 * q + 1] = hi;
         }
         __syncthreads();
-        const int xe = min(x0 + t.TX, gx.X), ye = min(y0 + t.TY, gx.Y);
-        const int nrow = (xe - x0) * (ye - y0);
-        for (int ic = 0; ic < c_in; ++ic) {
-            const int wlo = woff[ic * (c_out + 1) + oc0];
-            const int nwi = woff[ic * (c_out + 1) + oc0 + nocl] - wlo;
-            if (nwi == 0) continue;
-            const int lb = lbase[ic];
-            for (int rr = warp; rr < nrow; rr += nwarps) {
-                const int x = x0 + rr / (ye - y0), y = y0 + rr % (ye - y0);
-                const int64_t row = ((b * c_in + ic) * gx.X + x) * (int64_t)gx.Y + y;
-                const uint32_t e0 = xrow[row], e1 = xrow[row + 1];
-                const uint64_t rowbase = (uint64_t)row * (uint64_t)gx.Z;
-                const int hxr = x - x0 + kg.hx, hyr = y - y0 + kg.hy;
-                for (uint32_t e = e0 + lane; e < e1; e += 32) {
-                    const int z = (int)(xkeys[e] - rowbase);
-                    const float v = xvals[e];
-                    float dxa = 0.0f;
-                    int j = lane % nwi;
-                    for (int jj = 0; jj < nwi; ++jj) {
-                        const int2 m = wmeta[wlo + j];
-                        // g at uid = id - (fid - centre)
-                        const int gi = ((m.x - oc0) * hrows + (hxr - off_x(m.y)) * HY + (hyr - off_y(m.y))) * ZR +
-                                       z - off_z(m.y) + kg.hz;
-                        const float g = G[gi];
-                        if (g != 0.0f) {
-                            const float w = wval[wlo + j];
-                            dxa = fmaf(g, w, dxa);                                   // bp_data += g*fval
-                            if (want_dw) atomicAdd(&dwp[lb + j], (double)g * (double)v);  // bp_filter += g*val
-                        }
-                        j = (j + 1 == nwi) ? 0 : j + 1;
+        if (threadIdx.x == 0) {
+            int acc = 0;
+            for (int ic = 0; ic < c_in; ++ic) {
+                cpre[ic] = acc;
+                int cnt = 0;
+                for (int xi = 0; xi < t.TX; ++xi) cnt += (int)(rng[2 * (ic * t.TX + xi) + 1] - rng[2 * (ic * t.TX + xi)]);
+                acc += (cnt + 31) >> 5;
+            }
+            cpre[c_in] = acc;
+        }
+        __syncthreads();
+        const int nchunks = cpre[c_in];
+        for (int f = warp; f < nchunks; f += nwarps) {
+            int ic = 0;
+            while (cpre[ic + 1] <= f) ++ic;
+            const int s = ((f - cpre[ic]) << 5) + lane;
+            // locate the entry: walk the TX ranges of this ic
+            int eb = eb_safe;
+            float v = 0.0f;
+            int64_t e = -1;
+            {
+                int pre = 0;
+                for (int xi = 0; xi < t.TX; ++xi) {
+                    const uint32_t lo = rng[2 * (ic * t.TX + xi)], hi = rng[2 * (ic * t.TX + xi) + 1];
+                    const int n = (int)(hi - lo);
+                    if (s >= pre && s < pre + n) {
+                        e = (int64_t)lo + (s - pre);
+                        const int64_t r0 = ((b * c_in + ic) * gx.X + x0 + xi) * (int64_t)gx.Y + y0;
+                        const uint32_t L = (uint32_t)(xkeys[e] - (uint64_t)r0 * (uint64_t)gx.Z);
+                        const uint32_t yl = L / (uint32_t)gx.Z;
+                        const int z = (int)(L - yl * (uint32_t)gx.Z);
+                        eb = ((xi + kg.hx) * HY + (int)yl + kg.hy) * ZR + z + kg.hz;
+                        v = xvals[e];
                     }
-                    if (want_dx) {
-                        if (t.n_ocg == 1) dx[e] = dxa;
-                        else atomicAdd(&dx[e], dxa);
-                    }
+                    pre += n;
                 }
             }
+            __syncwarp();
+            st_eb[lane] = eb;
+            st_v[lane] = v;
+            __syncwarp();
+            const int n = lbase[ic + 1] - lbase[ic];
+            const int lb = lbase[ic];
+            float dxa = 0.0f;
+            for (int wb = 0; wb < n; wb += 32) {
+                const int j = wb + lane;
+                const bool wok = j < n;
+                const int wd = wok ? wdel[lb + j] : wdel[lb];
+                const float wl = wok ? wv[lb + j] : 0.0f;
+                float prod[32];
+                float dwl = 0.0f;
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    const float g = G[st_eb[q] - wd];
+                    prod[q] = g * wl;                       // bp_data contribution
+                    dwl = fmaf(g, st_v[q], dwl);            // bp_filter contribution
+                }
+                if (DX) dxa += reduce_scatter32(prod, lane);
+                if (DW && wok && dwl != 0.0f) atomicAdd(&dwp[lb + j], (double)dwl);
+            }
+            if (DX && e >= 0) {
+                if (t.n_ocg == 1) dx[e] = dxa;
+                else atomicAdd(&dx[e], dxa);
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        // restore G to zero where this item wrote gradients
+        for (int r = warp; r < nocl * HXY; r += nwarps) {
+            const int ocl = r / HXY, hr = r - ocl * HXY;
+            const int xs = x0 - kg.hx + hr / HY, ys = y0 - kg.hy + hr % HY;
+            if (xs < 0 || xs >= gy.X || ys < 0 || ys >= gy.Y) continue;
+            const int64_t row = ((b * c_out + oc0 + ocl) * gy.X + xs) * (int64_t)gy.Y + ys;
+            const uint32_t e0 = yrow[row], e1 = yrow[row + 1];
+            const uint64_t rowbase = (uint64_t)row * (uint64_t)gy.Z;
+            for (uint32_t e = e0 + lane; e < e1; e += 32)
+                G[(ocl * HXY + hr) * ZR + (int)(ykeys[e] - rowbase) + kg.hz] = 0.0f;
         }
     }
     __syncthreads();
-    if (want_dw) {
+    if (DW) {
         for (int ic = 0; ic < c_in; ++ic) {
-            const int wlo = woff[ic * (c_out + 1) + oc0];
+            const int t0 = woff[ic * (c_out + 1) + oc0];
             const int n = lbase[ic + 1] - lbase[ic];
             for (int j = threadIdx.x; j < n; j += blockDim.x) {
                 const double v = dwp[lbase[ic] + j];
-                if (v != 0.0) atomicAdd(&dw_acc[wsrc[wlo + j]], v);
+                if (v != 0.0) atomicAdd(&dw_acc[wsrc[t0 + j]], v);
             }
         }
     }
+}
+
+template <bool DX, bool DW>
+static cudaError_t launch_bwd_t(const Geo& gx, const Geo& gy, const KGeo& kg, const BwdTile& t,
+                                const uint64_t* xkeys, const float* xvals, const uint32_t* xrow,
+                                const uint64_t* ykeys, const float* dy, const uint32_t* yrow,
+                                const int2* wmeta, const float* wval, const int* woff, const int* wsrc,
+                                float* dx, double* dw_acc, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(conv_bwd_kernel<DX, DW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)t.smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)t.grid, (unsigned)t.n_ocg);
+    { SPC_PHASE("conv_bwd", s, 1); conv_bwd_kernel<DX, DW><<<grid, kBwdThreads, t.smem, s>>>(
+          gx, gy, kg, t, xkeys, xvals, xrow, ykeys, dy, yrow, wmeta, wval, woff, wsrc, dx, dw_acc); }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_conv_bwd(const Geo& gx, const Geo& gy, const KGeo& kg, const BwdTile& t,
@@ -174,17 +289,20 @@ cudaError_t launch_conv_bwd(const Geo& gx, const Geo& gy, const KGeo& kg, const 
                             const uint64_t* ykeys, const float* dy, const uint32_t* yrow,
                             const int2* wmeta, const float* wval, const int* woff, const int* wsrc,
                             float* dx, double* dw_acc, bool want_dx, bool want_dw, cudaStream_t s) {
-    cudaError_t e = cudaFuncSetAttribute(conv_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem);
-    if (e != cudaSuccess) return e;
     if (gx.B == 0) return cudaSuccess;
-    dim3 grid((unsigned)t.grid, (unsigned)t.n_ocg);
-    { SPC_PHASE("conv_bwd", s, 1); conv_bwd_kernel<<<grid, kBwdThreads, t.smem, s>>>(gx, gy, kg, t, xkeys, xvals, xrow, ykeys, dy, yrow, wmeta,
-                                                      wval, woff, wsrc, dx, dw_acc, want_dx ? 1 : 0,
-                                                      want_dw ? 1 : 0); }
-    return cudaGetLastError();
+    if (want_dx && want_dw)
+        return launch_bwd_t<true, true>(gx, gy, kg, t, xkeys, xvals, xrow, ykeys, dy, yrow, wmeta, wval, woff, wsrc,
+                                        dx, dw_acc, s);
+    if (want_dx)
+        return launch_bwd_t<true, false>(gx, gy, kg, t, xkeys, xvals, xrow, ykeys, dy, yrow, wmeta, wval, woff,
+                                         wsrc, dx, dw_acc, s);
+    return launch_bwd_t<false, true>(gx, gy, kg, t, xkeys, xvals, xrow, ykeys, dy, yrow, wmeta, wval, woff, wsrc,
+                                     dx, dw_acc, s);
 }
 
-// dbias[oc] = sum of dy over the kept outputs of oc (fp64 accumulation).
+// dbias[oc] = sum of dy over the kept outputs of oc (fp64). Keys are sorted, so a thread's
+// run of consecutive entries mostly shares one (b, oc) segment: accumulate locally and flush
+// on segment change.
 __global__ void dbias_kernel(Geo gy, const uint64_t* __restrict__ ykeys, const float* __restrict__ dy,
                              const int64_t* ny_dev, int64_t nbound, double* __restrict__ db) {
     extern __shared__ double sdb[];
@@ -192,9 +310,22 @@ __global__ void dbias_kernel(Geo gy, const uint64_t* __restrict__ ykeys, const f
     for (int i = threadIdx.x; i < c_out; i += blockDim.x) sdb[i] = 0.0;
     __syncthreads();
     const int64_t n = load_n(ny_dev, nbound);
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        const int oc = (int)((ykeys[t] / (uint64_t)gy.V) % (uint64_t)c_out);
-        atomicAdd(&sdb[oc], (double)dy[t]);
+    constexpr int RUN = 64;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * RUN; t0 < n; t0 += nthreads * RUN) {
+        const int64_t t1 = min(t0 + RUN, n);
+        int64_t seg = (int64_t)(ykeys[t0] / (uint64_t)gy.V);
+        double acc = 0.0;
+        for (int64_t t = t0; t < t1; ++t) {
+            const int64_t s2 = (int64_t)(ykeys[t] / (uint64_t)gy.V);
+            if (s2 != seg) {
+                atomicAdd(&sdb[seg % c_out], acc);
+                acc = 0.0;
+                seg = s2;
+            }
+            acc += (double)dy[t];
+        }
+        atomicAdd(&sdb[seg % c_out], acc);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < c_out; i += blockDim.x)
@@ -204,7 +335,7 @@ __global__ void dbias_kernel(Geo gy, const uint64_t* __restrict__ ykeys, const f
 cudaError_t launch_dbias(const Geo& gy, const uint64_t* ykeys, const float* dy, const int64_t* ny_dev,
                          int64_t ny_bound, double* db_acc, cudaStream_t s) {
     if (ny_bound <= 0) return cudaSuccess;
-    int64_t grid = (ny_bound + 255) / 256;
+    int64_t grid = (ny_bound + 256 * 64 - 1) / (256 * 64);
     if (grid > 592) grid = 592;
     const size_t sm = (size_t)gy.C * sizeof(double);
     if (sm > 48 * 1024) {

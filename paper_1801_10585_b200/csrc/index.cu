@@ -63,7 +63,7 @@ __global__ void filter_table_kernel(KGeo kg, int c_in, int c_out, const uint64_t
                                     float* __restrict__ val, int* __restrict__ off, int* __restrict__ src,
                                     int* __restrict__ run_start,
                                     int* __restrict__ run_len) {
-    __shared__ int sm[32];
+    __shared__ int sm[33];
     const int npairs = c_in * c_out;
     for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
         const int64_t lo = lower_bound_u64(wk, nw, (uint64_t)p * (uint64_t)kg.KV);
@@ -112,6 +112,59 @@ cudaError_t launch_filter_table(const KGeo& kg, int c_in, int c_out, const uint6
     return cudaGetLastError();
 }
 
+// Second order of the filter for the forward kernel: (ic, (dx,dy), oc, dz). For a fixed input
+// channel and in-plane offset the weights of a group of output channels are then one
+// contiguous range. meta2[j] = {oc, oz}, off2[(ic*KXY + dxdy)*(c_out+1) + oc] = first entry.
+// scratch: 2 * c_in*KXY*c_out ints. One block.
+__global__ void filter_table_fwd_kernel(KGeo kg, int c_in, int c_out, const uint64_t* __restrict__ wk,
+                                        const float* __restrict__ wv, int64_t nw, int2* __restrict__ meta2,
+                                        float* __restrict__ val2, int* __restrict__ off2, int* __restrict__ run_start,
+                                        int* __restrict__ run_len) {
+    __shared__ int sm[33];
+    const int KXY = kg.kx * kg.ky;
+    const int nq = c_in * KXY * c_out;   // q = (ic*KXY + dxdy)*c_out + oc
+    for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+        const int oc = q % c_out, rest = q / c_out;
+        const int dxdy = rest % KXY, ic = rest / KXY;
+        const uint64_t k0 = ((uint64_t)oc * c_in + ic) * (uint64_t)kg.KV + (uint64_t)dxdy * kg.kz;
+        const int64_t lo = lower_bound_u64(wk, nw, k0);
+        const int64_t hi = lower_bound_u64(wk, nw, k0 + (uint64_t)kg.kz);
+        run_start[q] = (int)lo;
+        run_len[q] = (int)(hi - lo);
+    }
+    __syncthreads();
+    int carry = 0;
+    for (int base = 0; base < nq; base += blockDim.x) {
+        const int q = base + threadIdx.x;
+        const int len = q < nq ? run_len[q] : 0;
+        int tot;
+        const int ex = block_excl_scan(len, sm, &tot);
+        if (q < nq) off2[(q / c_out) * (c_out + 1) + q % c_out] = carry + ex;
+        carry += tot;
+    }
+    __syncthreads();
+    for (int g = threadIdx.x; g < c_in * KXY; g += blockDim.x)
+        off2[g * (c_out + 1) + c_out] = (g + 1 < c_in * KXY) ? off2[(g + 1) * (c_out + 1)] : carry;
+    __syncthreads();
+    for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+        const int oc = q % c_out, g = q / c_out;
+        const int dst = off2[g * (c_out + 1) + oc];
+        for (int i = 0; i < run_len[q]; ++i) {
+            const int j = run_start[q] + i;
+            const int dz = (int)(wk[j] % (uint64_t)kg.kz);
+            meta2[dst + i] = make_int2(oc, dz - kg.hz);
+            val2[dst + i] = wv[j];
+        }
+    }
+}
+
+cudaError_t launch_filter_table_fwd(const KGeo& kg, int c_in, int c_out, const uint64_t* wkeys, const float* wvals,
+                                    int64_t nw, int2* meta2, float* val2, int* off2, int* scratch, cudaStream_t s) {
+    const size_t nq = (size_t)c_in * kg.kx * kg.ky * c_out;
+    { SPC_PHASE("filter_table", s, 1); filter_table_fwd_kernel<<<1, 1024, 0, s>>>(kg, c_in, c_out, wkeys, wvals, nw, meta2, val2, off2, scratch, scratch + nq); }
+    return cudaGetLastError();
+}
+
 // --------------------------------------------------------------------- device-wide scan
 constexpr int kScanBlock = 256;
 constexpr int kScanItems = 16;
@@ -120,7 +173,7 @@ constexpr int kScanTile = kScanBlock * kScanItems;
 size_t scan_tmp_words(int64_t n) { return (size_t)((n + kScanTile - 1) / kScanTile) + 2; }
 
 __global__ void scan_reduce_kernel(const uint32_t* __restrict__ in, int64_t n, uint64_t* __restrict__ sums) {
-    __shared__ uint64_t sm[32];
+    __shared__ uint64_t sm[33];
     const int64_t base = (int64_t)blockIdx.x * kScanTile;
     uint64_t acc = 0;
     for (int t = 0; t < kScanItems; ++t) {
@@ -132,7 +185,7 @@ __global__ void scan_reduce_kernel(const uint32_t* __restrict__ in, int64_t n, u
 }
 
 __global__ void scan_sums_kernel(uint64_t* sums, int64_t nb, int64_t* total) {
-    __shared__ uint64_t sm[32];
+    __shared__ uint64_t sm[33];
     uint64_t carry = 0;
     for (int64_t base = 0; base < nb; base += blockDim.x) {
         const int64_t i = base + threadIdx.x;
@@ -147,7 +200,7 @@ __global__ void scan_sums_kernel(uint64_t* sums, int64_t nb, int64_t* total) {
 
 __global__ void scan_down_kernel(const uint32_t* __restrict__ in, int64_t n, const uint64_t* __restrict__ sums,
                                  uint64_t* __restrict__ out) {
-    __shared__ uint64_t sm[32];
+    __shared__ uint64_t sm[33];
     const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
     uint32_t v[kScanItems];
     uint64_t acc = 0;

@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(kReluThreads) relu_count_kernel(const float* _
         const int64_t i = base + (int64_t)u * kReluThreads + threadIdx.x;
         if (i < n) c += vals[i] > 0.0f;
     }
-    __shared__ uint32_t sm[32];
+    __shared__ uint32_t sm[33];
     const uint32_t tot = block_sum(c, sm);
     if (threadIdx.x == 0) cnt[blockIdx.x] = tot;
 }
@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(kReluThreads) relu_write_kernel(const uint64_t
         v[u] = (my + u < n) ? vals[my + u] : 0.0f;
         c += v[u] > 0.0f;
     }
-    __shared__ uint32_t sm[32];
+    __shared__ uint32_t sm[33];
     uint32_t tot;
     uint64_t pos = off[blockIdx.x] + block_excl_scan(c, sm, &tot);
 #pragma unroll

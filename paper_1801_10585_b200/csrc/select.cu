@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kSelThreads) sel_hist_kernel(SelSrc S, const S
 // Per segment: walk the bins from the top until the running count reaches `need`.
 __global__ void __launch_bounds__(kSelThreads) sel_find_kernel(SelState* st, uint32_t* hist, int sh, int nbits) {
     const int64_t s = blockIdx.x;
-    __shared__ uint64_t sm[32];
+    __shared__ uint64_t sm[33];
     __shared__ int found;
     SelState x = st[s];
     if (x.keep_all) return;
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kSelThreads) sel_count_kernel(SelSrc S, const 
             }
         }
     }
-    __shared__ uint32_t sm[32];
+    __shared__ uint32_t sm[33];
     const uint32_t g = block_sum(gt, sm);
     const uint32_t e = block_sum(eq, sm);
     if (threadIdx.x == 0) {
@@ -167,7 +167,7 @@ __global__ void sel_chunk_scan_kernel(int64_t nchunk, const SelState* __restrict
                                       uint64_t* __restrict__ seg_kept) {
     const int64_t s = blockIdx.x;
     const SelState x = st[s];
-    __shared__ uint64_t sm[32];
+    __shared__ uint64_t sm[33];
     uint64_t tie_carry = 0, keep_carry = 0;
     for (int64_t base = 0; base < nchunk; base += blockDim.x) {
         const int64_t c = base + threadIdx.x;
@@ -194,7 +194,7 @@ __global__ void sel_chunk_scan_kernel(int64_t nchunk, const SelState* __restrict
 }
 
 __global__ void seg_scan_kernel(uint64_t* seg, int64_t nseg, int64_t* total) {
-    __shared__ uint64_t sm[32];
+    __shared__ uint64_t sm[33];
     uint64_t carry = 0;
     for (int64_t base = 0; base < nseg; base += blockDim.x) {
         const int64_t i = base + threadIdx.x;
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kSelThreads) sel_write_kernel(SelSrc S, const 
             }
         }
     }
-    __shared__ uint32_t sm[32];
+    __shared__ uint32_t sm[33];
     uint32_t t_eq;
     uint64_t tie = r.tie_before + block_excl_scan(neq, sm, &t_eq);
     uint32_t nkeep = 0;

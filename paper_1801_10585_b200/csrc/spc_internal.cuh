@@ -94,21 +94,60 @@ cudaError_t launch_row_index(const Geo& g, const uint64_t* keys, const int64_t* 
 cudaError_t launch_filter_table(const KGeo& kg, int c_in, int c_out, const uint64_t* wkeys, const float* wvals,
                                 int64_t nw, int2* meta, float* val, int* off, int* src, int* scratch, cudaStream_t s);
 
-struct ConvTile {
-    int TX, TY;       // output rows per tile
-    int ocg;          // output channels per CTA
-    int ntx, nty;     // tiles along x, y
-    int n_ocg;        // groups of output channels
-    size_t smem;      // dynamic shared memory bytes
+// Second filter order for the forward kernel: (ic, dxdy, oc, dz); meta2 = {oc, oz}.
+// scratch: 2 * c_in * kx*ky * c_out ints.
+cudaError_t launch_filter_table_fwd(const KGeo& kg, int c_in, int c_out, const uint64_t* wkeys, const float* wvals,
+                                    int64_t nw, int2* meta2, float* val2, int* off2, int* scratch, cudaStream_t s);
+
+// Forward tile: one x-plane, rows [y0, y0+TY) (full Z), a group of ocg output channels. Warp w
+// owns rows [y0 + w*RW, y0 + (w+1)*RW). Tiles of a segment are in key order: ti = x*nty + ty.
+struct FwdTile {
+    int TY, RW, nty, ocg, n_ocg, ZR, NT;
+    int pad;           // leading float pad of the accumulator (z margin of row 0)
+    int nwg_max;       // stored weights of one output-channel group (upper bound)
+    size_t smem;
 };
-ConvTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out);
-cudaError_t launch_conv_fwd(const Geo& gx, const Geo& gy, const KGeo& kg, const ConvTile& t,
-                            const uint64_t* xkeys, const float* xvals, const uint32_t* xrow,
-                            const int2* wmeta, const float* wval, const int* woff, const float* bias,
-                            float* pre, unsigned long long* seg_count, cudaStream_t s);
+FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_t nw_total);
+
+// Per-segment selection state of the forward (attention) pipeline.
+struct FwdSeg {
+    uint64_t kstar;      // keep an entry iff composite(score, p) >= kstar
+    int64_t need;        // candidates to select
+    uint32_t b1;         // threshold digit (11 bits)
+    int32_t keep_all;    // 1: keep every support entry
+};
+struct FwdArgs {
+    const uint64_t* xkeys;
+    const float* xvals;
+    const uint32_t* xrow;
+    const int2* meta2;
+    const float* val2;
+    const int* off2;
+    const float* bias;
+    int attn;
+    int64_t k;
+    unsigned long long* seg_count;   // [nseg] support size
+    uint32_t* hist;                  // [nseg * kSelBins]
+    FwdSeg* seg;                     // [nseg]
+    uint32_t* tile_cnt;              // [nseg * NT] support per tile
+    uint32_t* tile_def;              // [nseg * NT] definite keeps per tile
+    uint32_t* tile_sel;              // [nseg * NT] selected candidates per tile
+    uint64_t* tile_off;              // [nseg * NT] output offset of a tile within its segment
+    uint64_t* cand_off;              // [nseg + 1] candidate list offsets
+    uint64_t* cand_cnt;              // [nseg] candidates per segment
+    unsigned long long* cand_cur;    // [nseg] append cursors
+    uint2* cand;                     // candidate list {p, value bits}
+    uint64_t* seg_off;               // [nseg + 1] output offsets
+    uint64_t* out_keys;
+    float* out_vals;
+    int64_t* out_nnz;
+};
+cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& kg, const FwdTile& t,
+                                     const FwdArgs& a, cudaStream_t s);
 
 struct BwdTile {
     int TX, TY, ocg, ntx, nty, n_ocg, grid;
+    int nwg_max;      // upper bound of stored weights in one output-channel group
     size_t smem;
 };
 BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int n_w_max_group);
