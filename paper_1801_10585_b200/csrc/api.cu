@@ -171,10 +171,11 @@ FwdWs carve_fwd(Carver& c, const Geo& gx, const Geo& gy, const KGeo& kg, const F
     a.seg_count = c.take<unsigned long long>((size_t)nseg);
     a.hist = c.take<uint32_t>((size_t)nseg * kSelBins);
     a.seg = c.take<FwdSeg>((size_t)nseg);
-    a.tile_cnt = c.take<uint32_t>((size_t)nseg * t.NT);
-    a.tile_def = c.take<uint32_t>((size_t)nseg * t.NT);
-    a.tile_sel = c.take<uint32_t>((size_t)nseg * t.NT);
-    a.tile_off = c.take<uint64_t>((size_t)nseg * t.NT);
+    a.nchunk = (gy.V + 4095) / 4096;
+    a.pre = c.take<float>((size_t)(nseg * gy.V));
+    a.tile_def = c.take<uint32_t>((size_t)(nseg * a.nchunk));
+    a.tile_sel = c.take<uint32_t>((size_t)(nseg * a.nchunk));
+    a.tile_off = c.take<uint64_t>((size_t)(nseg * a.nchunk));
     a.cand_off = c.take<uint64_t>((size_t)nseg + 1);
     a.cand_cnt = c.take<uint64_t>((size_t)nseg + 1);
     a.cand_cur = c.take<unsigned long long>((size_t)nseg);

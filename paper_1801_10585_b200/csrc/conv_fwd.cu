@@ -40,9 +40,10 @@ constexpr int kStageCap = 2048;             // staged input entries per input ch
 
 // shared-memory bytes beyond the accumulator
 static size_t fwd_fixed_smem(const KGeo& kg, int c_in, int TY, int64_t nwg) {
-    const size_t nrp = (size_t)c_in * kg.kx * (TY + 2 * kg.hy + 1);
-    return (size_t)kSelBins * 4 + 256 * 4 + (size_t)nwg * 8 + (size_t)(c_in * kg.kx * kg.ky + 1) * 4 + nrp * 4 +
-           (size_t)(c_in * kg.kx + 1) * 4 + 16 + (size_t)kStageCap * 8 + 64;
+    auto r4 = [](size_t n) { return (n + 3) & ~(size_t)3; };
+    const size_t PK = (size_t)c_in * kg.kx, G = (size_t)c_in * kg.kx * kg.ky;
+    return 4 * ((size_t)kSelBins + 256 + 4 * r4((size_t)nwg) + r4(G + 1) + r4(PK * (TY + 2 * kg.hy + 1)) +
+                r4(PK + 1) + 2 * (size_t)kStageCap) + 64;
 }
 
 FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_t nw_total) {
@@ -61,7 +62,7 @@ FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_
     while (TY > 1 && need(ocg, TY) > kFwdBudget) --TY;          // ocg == 1: shorter tiles
     if (need(ocg, TY) > kFwdBudget) { t.smem = 0; return t; }
     while (TY < gy.Y && need(ocg, TY + kFwdWarps) <= kFwdBudget) TY += kFwdWarps;   // spare room
-    TY = std::min(TY, gy.Y);
+    TY = std::min(TY, std::min(gy.Y, 240));   // staged rows are packed in 8 bits (TY + 2*hy < 256)
     t.TY = TY;
     t.RW = (TY + kFwdWarps - 1) / kFwdWarps;
     t.nty = (gy.Y + TY - 1) / TY;
@@ -87,7 +88,6 @@ __device__ __forceinline__ uint64_t composite(uint32_t sc, uint32_t p) {
     return ((uint64_t)sc << 32) | (uint64_t)(0xffffffffu - p);
 }
 
-template <int MODE>
 __global__ void __launch_bounds__(kFwdThreads, 2)
 conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     extern __shared__ __align__(16) float smf[];
@@ -100,32 +100,36 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     const int oc0 = blockIdx.y * t.ocg;
     const int nocl = min(t.ocg, c_out - oc0);
     const int y0 = ty * t.TY, ye = min(y0 + t.TY, gy.Y);
-    const int ti = x * t.nty + ty;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int TYZR = t.TY * ZR;
 
-    // layout: [pad][acc ocg*TY*ZR][pad] | hist | misc(256) | swd | sww | swoff | rp | sbase | stage
+    // shared layout (float offsets, 16-byte aligned pieces):
+    // [pad][acc ocg*TY*ZR][pad] | hist | misc(256) | swd | sww | swoy | swoff | rp | sbase | stage
     const int KXY = kg.kx * kg.ky;
-    const int G = c_in * KXY;
+    const int G = c_in * KXY;                        // (ic, dx, dy) weight groups
+    const int PK = c_in * kg.kx;                     // (ic, input plane) work items
     const int ylo = max(0, y0 - kg.hy), yhi = min(gy.Y, ye + kg.hy);
     const int nr = yhi - ylo;                        // input rows read per plane
+    const int NRP = nr + 1;
+    const int nw4 = (t.nwg_max + 3) & ~3;
     float* acc = smf + t.pad;
     uint32_t* hist = reinterpret_cast<uint32_t*>(smf + 2 * t.pad + t.ocg * TYZR);
     uint32_t* misc = hist + kSelBins;
-    int* swd = reinterpret_cast<int*>(misc + 256);   // group weights: acc offset (ocl*TY*ZR - oz)
-    float* sww = reinterpret_cast<float*>(swd + t.nwg_max);
-    int* swoff = reinterpret_cast<int*>(sww + t.nwg_max);
-    uint32_t* rp = reinterpret_cast<uint32_t*>(swoff + G + 1);
-    const int PK = c_in * kg.kx;                     // (input channel, input plane) pairs
-    int* sbase = reinterpret_cast<int*>(rp + PK * (t.TY + 2 * kg.hy + 1));
-    uint2* stage = reinterpret_cast<uint2*>((reinterpret_cast<uintptr_t>(sbase + PK + 1) + 15) & ~(uintptr_t)15);
+    // per weight {acc offset of its target, value bits, row offset oy, 0}
+    int4* sw4 = reinterpret_cast<int4*>(misc + 256);
+    int* swoff = reinterpret_cast<int*>(sw4 + nw4);   // [G + 1] first weight of each (ic, dx, dy)
+    uint32_t* rp = reinterpret_cast<uint32_t*>(swoff + ((G + 1 + 3) & ~3));
+    int* sbase = reinterpret_cast<int*>(rp + ((PK * (t.TY + 2 * kg.hy + 1) + 3) & ~3));
+    uint2* stage = reinterpret_cast<uint2*>(sbase + ((PK + 1 + 3) & ~3));
 
     {
         const int n4 = (2 * t.pad + t.ocg * TYZR) / 4;
         uint4 ab = make_uint4(kAbsent, kAbsent, kAbsent, kAbsent);
         for (int i = threadIdx.x; i < n4; i += blockDim.x) reinterpret_cast<uint4*>(smf)[i] = ab;
     }
-    // this group's weights, grouped by (ic, dx, dy): "filter(oc, ic)" of Alg. 1
+    // this group's weights, ordered by (ic, dx, dy): "filter(oc, ic)" of Alg. 1. Each
+    // carries the accumulator offset of its target relative to the input's staged position:
+    // uid = id - (fid - centre) -> row y - oy, column z - oz, slice of channel oc.
     {
         int carry = 0;
         for (int g0 = 0; g0 < G; g0 += blockDim.x) {
@@ -142,18 +146,19 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
         for (int g = warp; g < G; g += kFwdWarps) {
             const int lo = a.off2[g * (c_out + 1) + oc0];
             const int n = swoff[g + 1] - swoff[g];
+            const int oy = g % kg.ky - kg.hy;
             for (int j = lane; j < n; j += 32) {
                 const int2 m = a.meta2[lo + j];
-                swd[swoff[g] + j] = (m.x - oc0) * TYZR - m.y;
-                sww[swoff[g] + j] = a.val2[lo + j];
+                sw4[swoff[g] + j] = make_int4((m.x - oc0) * TYZR - m.y + (ylo - y0 - oy) * ZR,
+                                              __float_as_int(a.val2[lo + j]), oy, 0);
             }
         }
     }
 
     // ------------------------------------------------------------ accumulate (Alg. 1 inner loops)
     const int yw0 = y0 + warp * t.RW, yw1 = min(yw0 + t.RW, ye);
+    const uint32_t nrw = (uint32_t)max(0, yw1 - yw0);
     const float invZ = 1.0f / (float)Z;
-    const int NRP = nr + 1;
     // row pointers of every (ic, input plane), rows ylo..yhi, in one burst
     for (int q = threadIdx.x; q < PK * NRP; q += blockDim.x) {
         const int pk = q / NRP, r = q - pk * NRP;
@@ -183,70 +188,71 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
         const int nst = sbase[ic1 * kg.kx] - sb0;
         const bool staged = nst <= kStageCap;        // false only for one over-full channel
         if (staged) {
-            for (int i = threadIdx.x; i < nst; i += blockDim.x) {
-                const int gi = sb0 + i;
-                int lo = ic0 * kg.kx, hi = ic1 * kg.kx - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (sbase[mid] <= gi) lo = mid; else hi = mid - 1;
-                }
-                const int ic = lo / kg.kx, pl = lo - ic * kg.kx;
-                const uint32_t ge = rp[lo * NRP] + (uint32_t)(gi - sbase[lo]);
-                const int xs = x + pl - kg.hx;
+            // one warp per (ic, plane) run: coalesced loads, no per-entry search
+            for (int pk = ic0 * kg.kx + warp; pk < ic1 * kg.kx; pk += kFwdWarps) {
+                const int ic = pk / kg.kx, xs = x + (pk - ic * kg.kx) - kg.hx;
+                const uint32_t g0 = rp[pk * NRP];
+                const int n = sbase[pk + 1] - sbase[pk];
+                uint2* dst = stage + (sbase[pk] - sb0);
                 const uint64_t rowbase = (uint64_t)(((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo) * (uint64_t)Z;
-                const uint32_t L = (uint32_t)(a.xkeys[ge] - rowbase);
-                const uint32_t yrel = div_small(L, (uint32_t)Z, invZ);
-                stage[i] = make_uint2(yrel * (uint32_t)ZR + (L - yrel * (uint32_t)Z), __float_as_uint(a.xvals[ge]));
+                for (int i = lane; i < n; i += 32) {
+                    const uint32_t L = (uint32_t)(a.xkeys[g0 + i] - rowbase);
+                    const uint32_t yrel = div_small(L, (uint32_t)Z, invZ);
+                    // {row (8 bits) | offset in the stage window (24 bits), value}
+                    dst[i] = make_uint2((yrel << 24) | (yrel * (uint32_t)ZR + (L - yrel * (uint32_t)Z)),
+                                        __float_as_uint(a.xvals[g0 + i]));
+                }
             }
         }
         __syncthreads();
-        for (int ic = ic0; ic < ic1 && yw0 < yw1; ++ic)
-        for (int dxy = 0; dxy < KXY; ++dxy) {
-            const int pl = dxy / kg.ky, oy = dxy - pl * kg.ky - kg.hy;
-            const int xs = x + pl - kg.hx;                   // input plane of uid_x = x
-            if (xs < 0 || xs >= gx.X) continue;
-            const int g = ic * KXY + dxy;
-            const int w0 = swoff[g], nwt = swoff[g + 1] - w0;
-            if (nwt == 0) continue;
-            const int yr0 = max(ylo, yw0 + oy), yr1 = min(yhi, yw1 + oy);
-            if (yr0 >= yr1) continue;
-            const int pk = ic * kg.kx + pl;
+        // work items (ic, input plane): the inputs of rows yw0-hy .. yw1+hy against all weights of
+        // (ic, dx) whose target row falls in this warp's rows
+        const int pk1 = (yw0 < yw1) ? ic1 * kg.kx : 0;
+        for (int pk = ic0 * kg.kx; pk < pk1; ++pk) {
             const uint32_t* RP = rp + pk * NRP;
-            const uint32_t e0 = RP[yr0 - ylo], e1 = RP[yr1 - ylo];
+            const int r0 = max(ylo, yw0 - kg.hy) - ylo, r1 = min(yhi, yw1 + kg.hy) - ylo;
+            const uint32_t e0 = RP[r0], e1 = RP[r1];
             if (e0 == e1) continue;
-            const int shift = (ylo - y0 - oy) * ZR;           // input row offset -> target row offset
+            const int wlo = swoff[pk * kg.ky], whi = swoff[(pk + 1) * kg.ky];
+            if (wlo == whi) continue;
             const int n = (int)(e1 - e0);
             const int s0 = staged ? sbase[pk] - sb0 + (int)(e0 - RP[0]) : 0;
-            const uint64_t rowbase = (uint64_t)(((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo) * (uint64_t)Z;
+            uint64_t rowbase = 0;
+            if (!staged) {
+                const int ic = pk / kg.kx, xs = x + (pk - ic * kg.kx) - kg.hx;
+                rowbase = (uint64_t)(((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo) * (uint64_t)Z;
+            }
             for (int c = 0; c < n; c += 32) {
                 const bool valid = c + lane < n;
-                int pos = 0;
+                int pos = 0, rel = -1000;                     // rel: input row - yw0
                 float v = 0.0f;
                 if (valid) {
+                    uint32_t yrel;
                     if (staged) {
                         const uint2 en = stage[s0 + c + lane];
-                        pos = (int)en.x;
+                        pos = (int)(en.x & 0xffffffu);
                         v = __uint_as_float(en.y);
+                        yrel = en.x >> 24;
                     } else {
                         const uint32_t L = (uint32_t)(a.xkeys[e0 + c + lane] - rowbase);
-                        const uint32_t yrel = div_small(L, (uint32_t)Z, invZ);
+                        yrel = div_small(L, (uint32_t)Z, invZ);
                         pos = (int)(yrel * (uint32_t)ZR + (L - yrel * (uint32_t)Z));
                         v = a.xvals[e0 + c + lane];
                     }
-                    pos += shift;
+                    rel = ylo + (int)yrel - yw0;
                 }
-                for (int j = 0; j < nwt; ++j) {
-                    const int wd = swd[w0 + j];
-                    const float w = sww[w0 + j];
+                for (int j = wlo; j < whi; ++j) {
+                    const int4 q = sw4[j];
+                    const int wd = q.x;
+                    const float w = __int_as_float(q.y);
+                    // target row (input row - oy) must be one of this warp's rows
+                    if ((uint32_t)(rel - q.z) < nrw) {
 #ifdef SPC_DEBUG
-                    if (valid && (pos + wd < -t.pad || pos + wd >= t.ocg * TYZR + t.pad))
-                        printf("OOB b=%lld x=%d ty=%d oc0=%d warp=%d lane=%d ic=%d dxy=%d pos=%d wd=%d j=%d w0=%d "
-                               "nwt=%d shift=%d s0=%d c=%d yr0=%d yr1=%d e0=%u e1=%u staged=%d swoffG=%d\n",
-                               (long long)b, x, ty, oc0, warp, lane, ic, dxy, pos, wd, j, w0, nwt, shift, s0, c, yr0,
-                               yr1, e0, e1, (int)staged, swoff[G]);
+                        if (pos + wd < -t.pad || pos + wd >= t.ocg * TYZR + t.pad)
+                            printf("OOB b=%lld x=%d ty=%d oc0=%d warp=%d lane=%d pk=%d pos=%d wd=%d j=%d\n",
+                                   (long long)b, x, ty, oc0, warp, lane, pk, pos, wd, j);
 #endif
-                    if (valid) {
-                        // "add val*fval to buffer at uid", uid = id - (fid - centre)
+                        // "add val*fval to buffer at uid"
                         float* p = acc + pos + wd;
                         const float old = *p;
                         const float base = __float_as_uint(old) == kAbsent ? 0.0f : old;
@@ -260,112 +266,40 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
         ic0 = ic1;
     }
 
-    // ------------------------------------------------------------------------ epilogues
+    // ------------------------------------------------------------------------ epilogue
+    // "get non-zero entries" and "add bias to non-zero entries": the tile's slice
+    // of the pre-attention responses goes to the (b, oc) buffers -- the paper's temporary dense
+    // buffer, absent marker where there is no support -- while the support size and a
+    // histogram of the top score digit are accumulated for the attention threshold.
     const int nyr = ye - y0;
-    const int nvox = nyr * Z;
+    const bool do_hist = a.attn != SPC_ATTN_NONE;
     for (int ocl = 0; ocl < nocl; ++ocl) {
         const int oc = oc0 + ocl;
         const int64_t s = b * c_out + oc;
         const float bv = a.bias ? a.bias[oc] : 0.0f;
         const float* A = acc + ocl * TYZR;
-        if (MODE == 0) {
-            // support count + histogram of the top score digit ("get non-zero entries",
-            // "add bias")
-            const bool do_hist = a.attn != SPC_ATTN_NONE;
-            if (do_hist)
-                for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) hist[i] = 0;
-            __syncthreads();
-            uint32_t cnt = 0;
-            for (int r = warp; r < nyr; r += kFwdWarps) {
-                for (int z = lane; z < Z; z += 32) {
-                    const float v = A[r * ZR + z];
-                    if (__float_as_uint(v) == kAbsent) continue;
+        if (do_hist)
+            for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        uint32_t cnt = 0;
+        float* P = a.pre + s * gy.V + ((int64_t)x * gy.Y + y0) * Z;
+        for (int r = warp; r < nyr; r += kFwdWarps) {
+            for (int z = lane; z < Z; z += 32) {
+                float v = A[r * ZR + z];
+                if (__float_as_uint(v) != kAbsent) {
+                    v += bv;
                     ++cnt;
-                    if (do_hist) atomicAdd(&hist[score_bits(__float_as_uint(v + bv), a.attn) >> 21], 1u);
+                    if (do_hist) atomicAdd(&hist[score_bits(__float_as_uint(v), a.attn) >> 21], 1u);
                 }
-            }
-            const uint32_t tot = block_sum(cnt, misc);
-            if (threadIdx.x == 0) {
-                a.tile_cnt[s * t.NT + ti] = tot;
-                if (tot) atomicAdd(&a.seg_count[s], (unsigned long long)tot);
-            }
-            if (do_hist)
-                for (int i = threadIdx.x; i < kSelBins; i += blockDim.x)
-                    if (hist[i]) atomicAdd(&a.hist[s * kSelBins + i], hist[i]);
-            __syncthreads();
-        } else if (MODE == 1) {
-            const FwdSeg st = a.seg[s];
-            if (st.keep_all) continue;                   // uniform over the block
-            uint32_t ndef = 0, ncand = 0;
-            for (int r = warp; r < nyr; r += kFwdWarps) {
-                for (int z = lane; z < Z; z += 32) {
-                    const float v = A[r * ZR + z];
-                    if (__float_as_uint(v) == kAbsent) continue;
-                    const uint32_t d = score_bits(__float_as_uint(v + bv), a.attn) >> 21;
-                    ndef += d > st.b1;
-                    ncand += d == st.b1;
-                }
-            }
-            const uint32_t tdef = block_sum(ndef, misc);
-            const uint32_t tcand = block_sum(ncand, misc);
-            if (threadIdx.x == 0) {
-                a.tile_def[s * t.NT + ti] = tdef;
-                misc[40] = tcand ? (uint32_t)atomicAdd(&a.cand_cur[s], (unsigned long long)tcand) : 0u;
-                misc[41] = 0;
-            }
-            __syncthreads();
-            if (tcand) {
-                const uint64_t base = a.cand_off[s] + misc[40];
-                for (int r = warp; r < nyr; r += kFwdWarps) {
-                    for (int z = lane; z < Z; z += 32) {
-                        const float v = A[r * ZR + z];
-                        if (__float_as_uint(v) == kAbsent) continue;
-                        const float val = v + bv;
-                        if ((score_bits(__float_as_uint(val), a.attn) >> 21) != st.b1) continue;
-                        const uint32_t slot = atomicAdd(&misc[41], 1u);
-                        const uint32_t p = (uint32_t)(((int64_t)x * gy.Y + (y0 + r)) * Z + z);
-                        a.cand[base + slot] = make_uint2(p, __float_as_uint(val));
-                    }
-                }
-            }
-            __syncthreads();
-        } else {
-            // keep iff composite(score, p) >= kstar; ordered compaction in key order
-            const FwdSeg st = a.seg[s];
-            const int per = (nvox + kFwdThreads - 1) / kFwdThreads;
-            const int l0 = threadIdx.x * per, l1 = min(l0 + per, nvox);
-            const uint32_t pbase = (uint32_t)(((int64_t)x * gy.Y + y0) * Z);
-            uint32_t nk = 0;
-            {
-                int r = l0 / Z, z = l0 - (l0 / Z) * Z;
-                for (int l = l0; l < l1; ++l) {
-                    const float v = A[r * ZR + z];
-                    if (__float_as_uint(v) != kAbsent) {
-                        const uint32_t sc = score_bits(__float_as_uint(v + bv), a.attn);
-                        nk += st.keep_all || composite(sc, pbase + (uint32_t)l) >= st.kstar;
-                    }
-                    if (++z == Z) { z = 0; ++r; }
-                }
-            }
-            uint32_t tot;
-            uint64_t pos = a.seg_off[s] + a.tile_off[s * t.NT + ti] + block_excl_scan(nk, misc, &tot);
-            if (nk) {
-                int r = l0 / Z, z = l0 - (l0 / Z) * Z;
-                for (int l = l0; l < l1; ++l) {
-                    const float v = A[r * ZR + z];
-                    if (__float_as_uint(v) != kAbsent) {
-                        const float val = v + bv;
-                        const uint32_t sc = score_bits(__float_as_uint(val), a.attn);
-                        if (st.keep_all || composite(sc, pbase + (uint32_t)l) >= st.kstar) {
-                            a.out_keys[pos] = (uint64_t)s * (uint64_t)gy.V + pbase + (uint32_t)l;
-                            a.out_vals[pos] = val;
-                            ++pos;
-                        }
-                    }
-                    if (++z == Z) { z = 0; ++r; }
-                }
+                __stcs(P + (int64_t)r * Z + z, v);
             }
         }
+        const uint32_t tot = block_sum(cnt, misc);
+        if (threadIdx.x == 0 && tot) atomicAdd(&a.seg_count[s], (unsigned long long)tot);
+        if (do_hist)
+            for (int i = threadIdx.x; i < kSelBins; i += blockDim.x)
+                if (hist[i]) atomicAdd(&a.hist[s * kSelBins + i], hist[i]);
+        __syncthreads();
     }
 }
 
@@ -429,9 +363,53 @@ __global__ void seg_scan_u64_kernel(const uint64_t* in, uint64_t* out, int64_t n
     }
 }
 
+constexpr int kChunkThreads = 256;
+constexpr int kChunkItems = 16;
+constexpr int kChunk = kChunkThreads * kChunkItems;   // voxels per chunk of a (b, oc) buffer
+
+// classify (HBM stream over the buffers): per chunk the entries kept outright (digit > B1, or
+// every support entry when the segment keeps all) and the candidates (digit == B1), which are
+// appended to the segment's candidate list.
+__global__ void __launch_bounds__(kChunkThreads) fwd_classify_kernel(FwdArgs a, int64_t V) {
+    const int64_t s = blockIdx.x / a.nchunk, c = blockIdx.x % a.nchunk;
+    const FwdSeg st = a.seg[s];
+    const int64_t lo = c * kChunk;
+    const float* P = a.pre + s * V;
+    __shared__ uint32_t sm[33];
+    __shared__ uint32_t sh_base, sh_slot;
+    uint32_t bits[kChunkItems];
+    uint32_t ndef = 0, ncand = 0;
+#pragma unroll
+    for (int u = 0; u < kChunkItems; ++u) {
+        const int64_t i = lo + (int64_t)u * kChunkThreads + threadIdx.x;
+        bits[u] = i < V ? __float_as_uint(__ldcs(P + i)) : kAbsent;
+        if (bits[u] == kAbsent) continue;
+        if (st.keep_all) { ++ndef; continue; }
+        const uint32_t d = score_bits(bits[u], a.attn) >> 21;
+        ndef += d > st.b1;
+        ncand += d == st.b1;
+    }
+    const uint32_t tdef = block_sum(ndef, sm);
+    const uint32_t tcand = block_sum(ncand, sm);
+    if (threadIdx.x == 0) {
+        a.tile_def[s * a.nchunk + c] = tdef;
+        sh_base = tcand ? (uint32_t)atomicAdd(&a.cand_cur[s], (unsigned long long)tcand) : 0u;
+        sh_slot = 0;
+    }
+    __syncthreads();
+    if (tcand == 0) return;
+    const uint64_t base = a.cand_off[s] + sh_base;
+#pragma unroll
+    for (int u = 0; u < kChunkItems; ++u) {
+        if (bits[u] == kAbsent || (score_bits(bits[u], a.attn) >> 21) != st.b1) continue;
+        const uint32_t slot = atomicAdd(&sh_slot, 1u);
+        a.cand[base + slot] = make_uint2((uint32_t)(lo + (int64_t)u * kChunkThreads + threadIdx.x), bits[u]);
+    }
+}
+
 // resolve: the `need` largest composite keys among the candidates of a segment (8-bit radix
-// select over 64 bits, all keys distinct) -> kstar; then count selected candidates per tile.
-__global__ void __launch_bounds__(512) fwd_resolve_kernel(FwdArgs a, Geo gy, FwdTile t) {
+// select over 64 bits, all keys distinct) -> kstar; then count selected candidates per chunk.
+__global__ void __launch_bounds__(512) fwd_resolve_kernel(FwdArgs a) {
     const int64_t s = blockIdx.x;
     FwdSeg st = a.seg[s];
     if (st.keep_all) return;
@@ -475,63 +453,98 @@ __global__ void __launch_bounds__(512) fwd_resolve_kernel(FwdArgs a, Geo gy, Fwd
         st.kstar = kstar;
         a.seg[s] = st;
     }
-    const uint32_t YZ = (uint32_t)gy.Y * (uint32_t)gy.Z;
     for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
         const uint2 e = c[i];
-        if (composite(score_bits(e.y, a.attn), e.x) >= kstar) {
-            const uint32_t px = e.x / YZ, py = (e.x / (uint32_t)gy.Z) % (uint32_t)gy.Y;
-            atomicAdd(&a.tile_sel[s * t.NT + px * t.nty + py / t.TY], 1u);
-        }
+        if (composite(score_bits(e.y, a.attn), e.x) >= kstar) atomicAdd(&a.tile_sel[s * a.nchunk + e.x / kChunk], 1u);
     }
 }
 
-// per segment: kept count per tile -> exclusive offsets; segment total -> kept[s]
-__global__ void fwd_tile_scan_kernel(FwdArgs a, FwdTile t, uint64_t* kept) {
+// per segment: kept count per chunk -> exclusive offsets; segment total -> kept[s]
+__global__ void fwd_chunk_scan_kernel(FwdArgs a, uint64_t* kept) {
     const int64_t s = blockIdx.x;
-    const FwdSeg st = a.seg[s];
     __shared__ uint64_t sm[33];
     uint64_t carry = 0;
-    for (int base = 0; base < t.NT; base += blockDim.x) {
-        const int ti = base + threadIdx.x;
+    for (int64_t base = 0; base < a.nchunk; base += blockDim.x) {
+        const int64_t c = base + threadIdx.x;
         uint64_t v = 0;
-        if (ti < t.NT)
-            v = st.keep_all ? a.tile_cnt[s * t.NT + ti] : (uint64_t)a.tile_def[s * t.NT + ti] + a.tile_sel[s * t.NT + ti];
+        if (c < a.nchunk) v = (uint64_t)a.tile_def[s * a.nchunk + c] + a.tile_sel[s * a.nchunk + c];
         uint64_t tot;
         const uint64_t ex = block_excl_scan(v, sm, &tot);
-        if (ti < t.NT) a.tile_off[s * t.NT + ti] = carry + ex;
+        if (c < a.nchunk) a.tile_off[s * a.nchunk + c] = carry + ex;
         carry += tot;
     }
     if (threadIdx.x == 0) kept[s] = carry;
+}
+
+// write (HBM stream): keep iff composite(score, p) >= kstar (all support when keep-all);
+// ordered compaction in key order ("compress ids ... write k largest features").
+__global__ void __launch_bounds__(kChunkThreads) fwd_write_kernel(FwdArgs a, int64_t V) {
+    const int64_t s = blockIdx.x / a.nchunk, c = blockIdx.x % a.nchunk;
+    const FwdSeg st = a.seg[s];
+    const int64_t lo = c * kChunk + (int64_t)threadIdx.x * kChunkItems;
+    const float* P = a.pre + s * V;
+    __shared__ uint64_t sm[33];
+    uint32_t bits[kChunkItems];
+    uint32_t keep = 0;
+    if (lo + kChunkItems <= V && (V & 3) == 0) {
+#pragma unroll
+        for (int u = 0; u < kChunkItems; u += 4) {
+            const float4 q = __ldcs(reinterpret_cast<const float4*>(P + lo + u));
+            bits[u] = __float_as_uint(q.x);
+            bits[u + 1] = __float_as_uint(q.y);
+            bits[u + 2] = __float_as_uint(q.z);
+            bits[u + 3] = __float_as_uint(q.w);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < kChunkItems; ++u) bits[u] = lo + u < V ? __float_as_uint(P[lo + u]) : kAbsent;
+    }
+#pragma unroll
+    for (int u = 0; u < kChunkItems; ++u) {
+        bool k = bits[u] != kAbsent;
+        if (k && !st.keep_all) k = composite(score_bits(bits[u], a.attn), (uint32_t)(lo + u)) >= st.kstar;
+        keep |= (uint32_t)k << u;
+    }
+    uint64_t tot;
+    uint64_t pos = a.seg_off[s] + a.tile_off[s * a.nchunk + c] + block_excl_scan((uint64_t)__popc(keep), sm, &tot);
+#pragma unroll
+    for (int u = 0; u < kChunkItems; ++u) {
+        if (keep & (1u << u)) {
+            a.out_keys[pos] = (uint64_t)s * (uint64_t)V + (uint64_t)(lo + u);
+            a.out_vals[pos] = __uint_as_float(bits[u]);
+            ++pos;
+        }
+    }
 }
 
 cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& kg, const FwdTile& t,
                                      const FwdArgs& a, cudaStream_t s) {
     const int64_t nseg = gy.B * gy.C;
     if (nseg == 0) return cudaMemsetAsync(a.out_nnz, 0, sizeof(int64_t), s);
-    cudaError_t e;
-    e = cudaFuncSetAttribute(conv_fwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(conv_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(conv_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem);
+    cudaError_t e = cudaFuncSetAttribute(conv_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem);
     if (e != cudaSuccess) return e;
     const size_t segb = sizeof(uint64_t) * (size_t)nseg;
     cudaMemsetAsync(a.seg_count, 0, segb, s);
     cudaMemsetAsync(a.cand_cur, 0, segb, s);
-    cudaMemsetAsync(a.tile_sel, 0, sizeof(uint32_t) * (size_t)nseg * t.NT, s);
+    cudaMemsetAsync(a.tile_sel, 0, sizeof(uint32_t) * (size_t)(nseg * a.nchunk), s);
     if (a.attn != SPC_ATTN_NONE) cudaMemsetAsync(a.hist, 0, sizeof(uint32_t) * kSelBins * (size_t)nseg, s);
     const dim3 grid((unsigned)(gy.B * gy.X * t.nty), (unsigned)t.n_ocg);
-    { SPC_PHASE("conv_fwd_hist", s, 1); conv_fwd_kernel<0><<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a); }
+    const unsigned sgrid = (unsigned)(nseg * a.nchunk);
+    { SPC_PHASE("conv_fwd", s, 1); conv_fwd_kernel<<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a); }
     { SPC_PHASE("fwd_find", s, 1); fwd_find_kernel<<<(unsigned)nseg, 256, 0, s>>>(a, nseg); }
     if (a.attn != SPC_ATTN_NONE) {
-        { SPC_PHASE("seg_scan", s, 1); seg_scan_u64_kernel<<<1, 1024, 0, s>>>(a.cand_cnt, a.cand_off, nseg, nullptr); }
-        { SPC_PHASE("conv_fwd_classify", s, 1); conv_fwd_kernel<1><<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a); }
-        { SPC_PHASE("fwd_resolve", s, 1); fwd_resolve_kernel<<<(unsigned)nseg, 512, 0, s>>>(a, gy, t); }
+        SPC_PHASE("seg_scan", s, 1);
+        seg_scan_u64_kernel<<<1, 1024, 0, s>>>(a.cand_cnt, a.cand_off, nseg, nullptr);
+    }
+    { SPC_PHASE("fwd_classify", s, 1); fwd_classify_kernel<<<sgrid, kChunkThreads, 0, s>>>(a, gy.V); }
+    if (a.attn != SPC_ATTN_NONE) {
+        SPC_PHASE("fwd_resolve", s, 1);
+        fwd_resolve_kernel<<<(unsigned)nseg, 512, 0, s>>>(a);
     }
     // kept per segment goes to cand_cnt (reused as scratch), then segment offsets
-    { SPC_PHASE("fwd_tile_scan", s, 1); fwd_tile_scan_kernel<<<(unsigned)nseg, 256, 0, s>>>(a, t, a.cand_cnt); }
+    { SPC_PHASE("fwd_chunk_scan", s, 1); fwd_chunk_scan_kernel<<<(unsigned)nseg, 256, 0, s>>>(a, a.cand_cnt); }
     { SPC_PHASE("seg_scan", s, 1); seg_scan_u64_kernel<<<1, 1024, 0, s>>>(a.cand_cnt, a.seg_off, nseg, a.out_nnz); }
-    { SPC_PHASE("conv_fwd_write", s, 1); conv_fwd_kernel<2><<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a); }
+    { SPC_PHASE("fwd_write", s, 1); fwd_write_kernel<<<sgrid, kChunkThreads, 0, s>>>(a, gy.V); }
     return cudaGetLastError();
 }
 

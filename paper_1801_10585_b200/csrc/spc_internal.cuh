@@ -126,13 +126,14 @@ struct FwdArgs {
     const float* bias;
     int attn;
     int64_t k;
+    float* pre;                      // [nseg * V] pre-attention responses (absent marker off support)
+    int64_t nchunk;                  // chunks of 4096 voxels per (b, oc) buffer
     unsigned long long* seg_count;   // [nseg] support size
     uint32_t* hist;                  // [nseg * kSelBins]
     FwdSeg* seg;                     // [nseg]
-    uint32_t* tile_cnt;              // [nseg * NT] support per tile
-    uint32_t* tile_def;              // [nseg * NT] definite keeps per tile
-    uint32_t* tile_sel;              // [nseg * NT] selected candidates per tile
-    uint64_t* tile_off;              // [nseg * NT] output offset of a tile within its segment
+    uint32_t* tile_def;              // [nseg * nchunk] entries kept outright per chunk
+    uint32_t* tile_sel;              // [nseg * nchunk] selected candidates per chunk
+    uint64_t* tile_off;              // [nseg * nchunk] output offset of a chunk within its segment
     uint64_t* cand_off;              // [nseg + 1] candidate list offsets
     uint64_t* cand_cnt;              // [nseg] candidates per segment
     unsigned long long* cand_cur;    // [nseg] append cursors
