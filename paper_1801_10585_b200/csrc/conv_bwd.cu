@@ -153,16 +153,25 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
         const int x0 = (tile % t.ntx) * t.TX, y0 = (tile / t.ntx) * t.TY;
         const int xe = min(x0 + t.TX, gx.X), ye = min(y0 + t.TY, gx.Y);
         __syncthreads();
-        // "initialize dense buffer with gradients(b, oc)", tile + halo, this oc group
-        for (int r = warp; r < nocl * HXY; r += nwarps) {
-            const int ocl = r / HXY, hr = r - ocl * HXY;
-            const int xs = x0 - kg.hx + hr / HY, ys = y0 - kg.hy + hr % HY;
-            if (xs < 0 || xs >= gy.X || ys < 0 || ys >= gy.Y) continue;
-            const int64_t row = ((b * c_out + oc0 + ocl) * gy.X + xs) * (int64_t)gy.Y + ys;
-            const uint32_t e0 = yrow[row], e1 = yrow[row + 1];
+        // "initialize dense buffer with gradients(b, oc)", tile + halo, this oc group:
+        // per (oc, halo x-row) the kept outputs of the halo y-range are one contiguous key run
+        const int hylo = max(0, y0 - kg.hy), hyhi = min(gy.Y, y0 + t.TY + kg.hy);
+        const float invZ = 1.0f / (float)gy.Z;
+        for (int r = warp; r < nocl * HX; r += nwarps) {
+            const int ocl = r / HX, hxr = r - ocl * HX;
+            const int xs = x0 - kg.hx + hxr;
+            if (xs < 0 || xs >= gy.X || hylo >= hyhi) continue;
+            const int64_t row = ((b * c_out + oc0 + ocl) * gy.X + xs) * (int64_t)gy.Y + hylo;
+            const uint32_t e0 = yrow[row], e1 = yrow[row + (hyhi - hylo)];
             const uint64_t rowbase = (uint64_t)row * (uint64_t)gy.Z;
-            for (uint32_t e = e0 + lane; e < e1; e += 32)
-                G[(ocl * HXY + hr) * ZR + (int)(ykeys[e] - rowbase) + kg.hz] = dy[e];
+            const int gbase = (ocl * HXY + hxr * HY + (hylo - (y0 - kg.hy))) * ZR + kg.hz;
+            for (uint32_t e = e0 + lane; e < e1; e += 32) {
+                const uint32_t L = (uint32_t)(ykeys[e] - rowbase);
+                uint32_t yr = __float2uint_rz(__uint2float_rz(L) * invZ);
+                if (yr * (uint32_t)gy.Z > L) --yr;
+                if ((yr + 1) * (uint32_t)gy.Z <= L) ++yr;
+                G[gbase + (int)yr * ZR + (int)(L - yr * (uint32_t)gy.Z)] = dy[e];
+            }
         }
         // entry ranges: per (ic, x) the stored entries of rows y0..ye-1 are contiguous
         for (int q = threadIdx.x; q < c_in * t.TX; q += blockDim.x) {
@@ -245,15 +254,21 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
         }
         __syncthreads();
         // restore G to zero where this item wrote gradients
-        for (int r = warp; r < nocl * HXY; r += nwarps) {
-            const int ocl = r / HXY, hr = r - ocl * HXY;
-            const int xs = x0 - kg.hx + hr / HY, ys = y0 - kg.hy + hr % HY;
-            if (xs < 0 || xs >= gy.X || ys < 0 || ys >= gy.Y) continue;
-            const int64_t row = ((b * c_out + oc0 + ocl) * gy.X + xs) * (int64_t)gy.Y + ys;
-            const uint32_t e0 = yrow[row], e1 = yrow[row + 1];
+        for (int r = warp; r < nocl * HX; r += nwarps) {
+            const int ocl = r / HX, hxr = r - ocl * HX;
+            const int xs = x0 - kg.hx + hxr;
+            if (xs < 0 || xs >= gy.X || hylo >= hyhi) continue;
+            const int64_t row = ((b * c_out + oc0 + ocl) * gy.X + xs) * (int64_t)gy.Y + hylo;
+            const uint32_t e0 = yrow[row], e1 = yrow[row + (hyhi - hylo)];
             const uint64_t rowbase = (uint64_t)row * (uint64_t)gy.Z;
-            for (uint32_t e = e0 + lane; e < e1; e += 32)
-                G[(ocl * HXY + hr) * ZR + (int)(ykeys[e] - rowbase) + kg.hz] = 0.0f;
+            const int gbase = (ocl * HXY + hxr * HY + (hylo - (y0 - kg.hy))) * ZR + kg.hz;
+            for (uint32_t e = e0 + lane; e < e1; e += 32) {
+                const uint32_t L = (uint32_t)(ykeys[e] - rowbase);
+                uint32_t yr = __float2uint_rz(__uint2float_rz(L) * invZ);
+                if (yr * (uint32_t)gy.Z > L) --yr;
+                if ((yr + 1) * (uint32_t)gy.Z <= L) ++yr;
+                G[gbase + (int)yr * ZR + (int)(L - yr * (uint32_t)gy.Z)] = 0.0f;
+            }
         }
     }
     __syncthreads();
@@ -312,20 +327,37 @@ __global__ void dbias_kernel(Geo gy, const uint64_t* __restrict__ ykeys, const f
     const int64_t n = load_n(ny_dev, nbound);
     constexpr int RUN = 64;
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t t0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * RUN; t0 < n; t0 += nthreads * RUN) {
-        const int64_t t1 = min(t0 + RUN, n);
-        int64_t seg = (int64_t)(ykeys[t0] / (uint64_t)gy.V);
+    const int lane = threadIdx.x & 31;
+    constexpr uint64_t kNone = ~0ull;
+    // warp-uniform loop: lane L of a warp takes the run starting at wb + L*RUN
+    for (int64_t wb = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * RUN; wb < n; wb += nthreads * RUN) {
+        const int64_t t0 = wb + (int64_t)lane * RUN;
+        uint64_t seg = kNone;
         double acc = 0.0;
-        for (int64_t t = t0; t < t1; ++t) {
-            const int64_t s2 = (int64_t)(ykeys[t] / (uint64_t)gy.V);
-            if (s2 != seg) {
-                atomicAdd(&sdb[seg % c_out], acc);
-                acc = 0.0;
-                seg = s2;
+        if (t0 < n) {
+            const int64_t t1 = min(t0 + RUN, n);
+            // keys are sorted, so most runs lie in one segment
+            seg = ykeys[t0] / (uint64_t)gy.V;
+            uint64_t seg_end = (seg + 1) * (uint64_t)gy.V;    // first key of the next segment
+            for (int64_t t = t0; t < t1; ++t) {
+                const uint64_t k = ykeys[t];
+                if (k >= seg_end) {
+                    atomicAdd(&sdb[seg % c_out], acc);
+                    acc = 0.0;
+                    seg = k / (uint64_t)gy.V;
+                    seg_end = (seg + 1) * (uint64_t)gy.V;
+                }
+                acc += (double)dy[t];
             }
-            acc += (double)dy[t];
         }
-        atomicAdd(&sdb[seg % c_out], acc);
+        // the usual case: the warp's runs end in one segment -> one atomic per warp
+        const uint64_t seg0 = __shfl_sync(kFull, seg, 0);
+        if (__all_sync(kFull, seg == seg0 || seg == kNone)) {
+            acc = warp_sum(acc);
+            if (lane == 0 && seg0 != kNone) atomicAdd(&sdb[seg0 % c_out], acc);
+        } else if (seg != kNone) {
+            atomicAdd(&sdb[seg % c_out], acc);
+        }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < c_out; i += blockDim.x)

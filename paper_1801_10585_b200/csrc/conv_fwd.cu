@@ -35,15 +35,16 @@ namespace spc {
 
 constexpr int kFwdThreads = 256;
 constexpr int kFwdWarps = kFwdThreads / 32;
-constexpr size_t kFwdBudget = 110 * 1024;   // two CTAs per SM
-constexpr int kStageCap = 2048;             // staged input entries per input channel
+constexpr size_t kFwdBudget = 108 * 1024;   // two CTAs (16 warps) per SM
+constexpr int kStageCap = 2048;             // staged input entries per chunk of input channels
+static_assert(2 * kStageCap >= kSelBins, "the epilogue histogram reuses the stage buffer");
 
 // shared-memory bytes beyond the accumulator
 static size_t fwd_fixed_smem(const KGeo& kg, int c_in, int TY, int64_t nwg) {
     auto r4 = [](size_t n) { return (n + 3) & ~(size_t)3; };
     const size_t PK = (size_t)c_in * kg.kx, G = (size_t)c_in * kg.kx * kg.ky;
-    return 4 * ((size_t)kSelBins + 256 + 4 * r4((size_t)nwg) + r4(G + 1) + r4(PK * (TY + 2 * kg.hy + 1)) +
-                r4(PK + 1) + 2 * (size_t)kStageCap) + 64;
+    return 4 * (256 + 4 * r4((size_t)nwg) + r4(G + 1) + r4(PK * (TY + 2 * kg.hy + 1)) + r4(PK + 1) +
+                2 * (size_t)kStageCap) + 64;
 }
 
 FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_t nw_total) {
@@ -104,7 +105,7 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     const int TYZR = t.TY * ZR;
 
     // shared layout (float offsets, 16-byte aligned pieces):
-    // [pad][acc ocg*TY*ZR][pad] | hist | misc(256) | swd | sww | swoy | swoff | rp | sbase | stage
+    // [pad][acc ocg*TY*ZR][pad] | misc(256) | sw4 | swoff | rp | sbase | stage (= hist in the epilogue)
     const int KXY = kg.kx * kg.ky;
     const int G = c_in * KXY;                        // (ic, dx, dy) weight groups
     const int PK = c_in * kg.kx;                     // (ic, input plane) work items
@@ -113,14 +114,14 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     const int NRP = nr + 1;
     const int nw4 = (t.nwg_max + 3) & ~3;
     float* acc = smf + t.pad;
-    uint32_t* hist = reinterpret_cast<uint32_t*>(smf + 2 * t.pad + t.ocg * TYZR);
-    uint32_t* misc = hist + kSelBins;
+    uint32_t* misc = reinterpret_cast<uint32_t*>(smf + 2 * t.pad + t.ocg * TYZR);
     // per weight {acc offset of its target, value bits, row offset oy, 0}
     int4* sw4 = reinterpret_cast<int4*>(misc + 256);
     int* swoff = reinterpret_cast<int*>(sw4 + nw4);   // [G + 1] first weight of each (ic, dx, dy)
     uint32_t* rp = reinterpret_cast<uint32_t*>(swoff + ((G + 1 + 3) & ~3));
     int* sbase = reinterpret_cast<int*>(rp + ((PK * (t.TY + 2 * kg.hy + 1) + 3) & ~3));
     uint2* stage = reinterpret_cast<uint2*>(sbase + ((PK + 1 + 3) & ~3));
+    uint32_t* hist = reinterpret_cast<uint32_t*>(stage);   // epilogue only
 
     {
         const int n4 = (2 * t.pad + t.ocg * TYZR) / 4;
@@ -283,15 +284,32 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
         __syncthreads();
         uint32_t cnt = 0;
         float* P = a.pre + s * gy.V + ((int64_t)x * gy.Y + y0) * Z;
+        const bool vec = (Z & 3) == 0;
         for (int r = warp; r < nyr; r += kFwdWarps) {
-            for (int z = lane; z < Z; z += 32) {
-                float v = A[r * ZR + z];
-                if (__float_as_uint(v) != kAbsent) {
-                    v += bv;
-                    ++cnt;
-                    if (do_hist) atomicAdd(&hist[score_bits(__float_as_uint(v), a.attn) >> 21], 1u);
+            for (int z0 = 4 * lane; z0 < Z; z0 += 128) {
+                float v[4];
+                if (vec) {
+                    const float4 q = *reinterpret_cast<const float4*>(A + r * ZR + z0);
+                    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) v[u] = z0 + u < Z ? A[r * ZR + z0 + u] : __uint_as_float(kAbsent);
                 }
-                __stcs(P + (int64_t)r * Z + z, v);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (__float_as_uint(v[u]) != kAbsent) {
+                        v[u] += bv;
+                        ++cnt;
+                        if (do_hist) atomicAdd(&hist[score_bits(__float_as_uint(v[u]), a.attn) >> 21], 1u);
+                    }
+                }
+                if (vec) {
+                    __stcs(reinterpret_cast<float4*>(P + (int64_t)r * Z + z0), make_float4(v[0], v[1], v[2], v[3]));
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (z0 + u < Z) __stcs(P + (int64_t)r * Z + z0 + u, v[u]);
+                }
             }
         }
         const uint32_t tot = block_sum(cnt, misc);
@@ -375,35 +393,59 @@ __global__ void __launch_bounds__(kChunkThreads) fwd_classify_kernel(FwdArgs a, 
     const FwdSeg st = a.seg[s];
     const int64_t lo = c * kChunk;
     const float* P = a.pre + s * V;
-    __shared__ uint32_t sm[33];
-    __shared__ uint32_t sh_base, sh_slot;
+    __shared__ uint32_t sh_cnt, sh_base, sh_slot;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) { sh_cnt = 0; sh_slot = 0; }
+    // element u of this thread: lo + 4*(v*256 + tid) + w, u = 4v + w (float4 loads, coalesced)
     uint32_t bits[kChunkItems];
-    uint32_t ndef = 0, ncand = 0;
+    const bool vec = (V & 3) == 0;
+#pragma unroll
+    for (int v = 0; v < kChunkItems / 4; ++v) {
+        const int64_t i = lo + 4 * ((int64_t)v * kChunkThreads + threadIdx.x);
+        if (vec && i + 4 <= V) {
+            const float4 q = __ldcs(reinterpret_cast<const float4*>(P + i));
+            bits[4 * v] = __float_as_uint(q.x);
+            bits[4 * v + 1] = __float_as_uint(q.y);
+            bits[4 * v + 2] = __float_as_uint(q.z);
+            bits[4 * v + 3] = __float_as_uint(q.w);
+        } else {
+#pragma unroll
+            for (int w = 0; w < 4; ++w) bits[4 * v + w] = i + w < V ? __float_as_uint(P[i + w]) : kAbsent;
+        }
+    }
+    uint32_t packed = 0;   // kept outright (low 16 bits) | candidates (high 16 bits)
 #pragma unroll
     for (int u = 0; u < kChunkItems; ++u) {
-        const int64_t i = lo + (int64_t)u * kChunkThreads + threadIdx.x;
-        bits[u] = i < V ? __float_as_uint(__ldcs(P + i)) : kAbsent;
         if (bits[u] == kAbsent) continue;
-        if (st.keep_all) { ++ndef; continue; }
+        if (st.keep_all) { ++packed; continue; }
         const uint32_t d = score_bits(bits[u], a.attn) >> 21;
-        ndef += d > st.b1;
-        ncand += d == st.b1;
+        packed += (d > st.b1) + ((uint32_t)(d == st.b1) << 16);
     }
-    const uint32_t tdef = block_sum(ndef, sm);
-    const uint32_t tcand = block_sum(ncand, sm);
+    packed = warp_sum(packed);
+    __syncthreads();
+    if (lane == 0 && packed) atomicAdd(&sh_cnt, packed);
+    __syncthreads();
+    const uint32_t tot = sh_cnt;
+    const uint32_t tcand = tot >> 16;
     if (threadIdx.x == 0) {
-        a.tile_def[s * a.nchunk + c] = tdef;
+        a.tile_def[s * a.nchunk + c] = tot & 0xffffu;
         sh_base = tcand ? (uint32_t)atomicAdd(&a.cand_cur[s], (unsigned long long)tcand) : 0u;
-        sh_slot = 0;
     }
     __syncthreads();
     if (tcand == 0) return;
     const uint64_t base = a.cand_off[s] + sh_base;
 #pragma unroll
     for (int u = 0; u < kChunkItems; ++u) {
-        if (bits[u] == kAbsent || (score_bits(bits[u], a.attn) >> 21) != st.b1) continue;
-        const uint32_t slot = atomicAdd(&sh_slot, 1u);
-        a.cand[base + slot] = make_uint2((uint32_t)(lo + (int64_t)u * kChunkThreads + threadIdx.x), bits[u]);
+        const bool is_c = bits[u] != kAbsent && (score_bits(bits[u], a.attn) >> 21) == st.b1;
+        const unsigned m = __ballot_sync(kFull, is_c);
+        if (!m) continue;
+        uint32_t slot0 = 0;
+        if (lane == 0) slot0 = atomicAdd(&sh_slot, (uint32_t)__popc(m));
+        slot0 = __shfl_sync(kFull, slot0, 0);
+        if (is_c) {
+            const uint32_t p = (uint32_t)(lo + 4 * ((int64_t)(u >> 2) * kChunkThreads + threadIdx.x) + (u & 3));
+            a.cand[base + slot0 + __popc(m & ((1u << lane) - 1u))] = make_uint2(p, bits[u]);
+        }
     }
 }
 
@@ -434,16 +476,26 @@ __global__ void __launch_bounds__(512) fwd_resolve_kernel(FwdArgs a) {
             if ((k & mask) == prefix) atomicAdd(&h[(k >> sh) & 255], 1u);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            int64_t need = sh_need, cum = 0;
-            for (int bin = 255; bin >= 0; --bin) {
-                if (cum + (int64_t)h[bin] >= need) {
-                    sh_need = need - cum;
-                    sh_prefix = prefix | ((uint64_t)bin << sh);
-                    sh_mask = mask | ((uint64_t)255 << sh);
-                    break;
+        if (threadIdx.x < 32) {
+            // warp scan of the 256 bins from the top: lane l owns bins 255-8l .. 248-8l
+            const int l = threadIdx.x;
+            uint32_t own = 0;
+            for (int q = 0; q < 8; ++q) own += h[255 - 8 * l - q];
+            const uint32_t incl = warp_incl_scan(own);
+            const int64_t need = sh_need;
+            const int64_t before = (int64_t)(incl - own);
+            if (before < need && before + (int64_t)own >= need) {
+                int64_t cum = before;
+                for (int q = 0; q < 8; ++q) {
+                    const int bin = 255 - 8 * l - q;
+                    if (cum + (int64_t)h[bin] >= need) {
+                        sh_need = need - cum;
+                        sh_prefix = prefix | ((uint64_t)bin << sh);
+                        sh_mask = mask | ((uint64_t)255 << sh);
+                        break;
+                    }
+                    cum += h[bin];
                 }
-                cum += h[bin];
             }
         }
         __syncthreads();

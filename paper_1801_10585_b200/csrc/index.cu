@@ -9,23 +9,37 @@ namespace spc {
 // row_ptr[r] = first entry whose key >= r*Z, for r in [0, total_rows]. One thread per entry
 // owns the gap of rows between its predecessor's row and its own row; a warp fills the gaps of
 // its 32 lanes cooperatively so that long empty stretches do not serialise on one thread.
+// key / Z for keys < 2^52: double reciprocal, then an exact integer correction
+__device__ __forceinline__ int64_t row_of(uint64_t key, int64_t Z, double invZ) {
+    int64_t q = (int64_t)((double)key * invZ);
+    int64_t r = (int64_t)key - q * Z;
+    while (r < 0) { --q; r += Z; }
+    while (r >= Z) { ++q; r -= Z; }
+    return q;
+}
+
 __global__ void row_index_kernel(int Z, const uint64_t* __restrict__ keys, const int64_t* nnz_dev,
                                  int64_t nbound, uint32_t* __restrict__ row_ptr, int64_t total_rows) {
     const int64_t n = load_n(nnz_dev, nbound);
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
+    const double invZ = 1.0 / (double)Z;
     int64_t lo = 0, hi = -1;
     if (i < n) {
-        const int64_t r = (int64_t)(keys[i] / (uint64_t)Z);
-        const int64_t rp = (i == 0) ? -1 : (int64_t)(keys[i - 1] / (uint64_t)Z);
+        const int64_t r = row_of(keys[i], Z, invZ);
+        const int64_t rp = (i == 0) ? -1 : row_of(keys[i - 1], Z, invZ);
         lo = rp + 1;
         hi = r < total_rows ? r : total_rows;
     } else if (i == n) {
-        const int64_t rl = (n == 0) ? -1 : (int64_t)(keys[n - 1] / (uint64_t)Z);
+        const int64_t rl = (n == 0) ? -1 : row_of(keys[n - 1], Z, invZ);
         lo = rl + 1;
         hi = total_rows;
     }
-    unsigned m = __ballot_sync(kFull, hi >= lo);
+    // short gaps (the common case): the owning thread fills them; long ones: the whole warp
+    const bool longgap = hi - lo >= 16;
+    if (!longgap)
+        for (int64_t r = lo; r <= hi; ++r) row_ptr[r] = (uint32_t)i;
+    unsigned m = __ballot_sync(kFull, longgap);
     while (m) {
         const int src = __ffs(m) - 1;
         m &= m - 1;
