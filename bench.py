@@ -17,6 +17,7 @@ kept outputs (dx and dw). HBM GB/s is reported alongside from compulsory bytes (
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import statistics
@@ -182,18 +183,13 @@ def run_ours(args):
     dx_t = torch.empty(max(X.nnz_bound, 1), device="cuda")
     dw_t = torch.empty(W.keys.numel(), device="cuda")
     db_t = torch.empty(C_OUT, device="cuda")
-    red = torch.empty(W.keys.numel() + C_OUT, dtype=torch.float64, device="cuda")
+    allreduce = spc.dp.GradAllReduce(W.keys.numel(), C_OUT, "cuda")   # SUM of dw||dbias (R13)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # 512 MB > L2
 
     def step():
         Y = fwd(X, W, bias_t)
         bwd(X, W, Y, dy_t, dx_t, dw_t, db_t)
-        if world > 1:
-            red[:dw_t.numel()].copy_(dw_t)
-            red[dw_t.numel():].copy_(db_t)
-            dist.all_reduce(red)            # SUM over ranks (reading R13)
-            dw_t.copy_(red[:dw_t.numel()])
-            db_t.copy_(red[dw_t.numel():])
+        allreduce(dw_t, db_t)               # no-op on one GPU
         return Y
 
     for _ in range(args.warmup):
@@ -322,26 +318,40 @@ def roofline_for(name, ph, ny, nnz_x, nnz_w, B_local, fwd_macs, bwd_macs, pk, sr
     if name == "conv_fwd":
         return {"kernel": name, "bound": "alu", "achieved": round(fwd_macs / t / 1e12, 4), "unit": "TMAC/s",
                 "peak": round(fma_peak, 2), "frac": round(fwd_macs / t / 1e12 / fma_peak, 5),
-                "traffic": None, "peak_source": f"derived: 148 SM x 128 FFMA/clk x {sm_mhz:.0f} MHz",
+                "traffic": ncu_traffic(name), "peak_source": f"derived: 148 SM x 128 FFMA/clk x {sm_mhz:.0f} MHz",
                 "algorithmic": f"{fwd_macs} MACs per launch (Eq. (1) pairs)"}
     if name == "conv_bwd":
         return {"kernel": name, "bound": "alu", "achieved": round(bwd_macs / t / 1e12, 4), "unit": "TMAC/s",
-                "peak": round(fma_peak, 2), "frac": round(bwd_macs / t / 1e12 / fma_peak, 5), "traffic": None,
+                "peak": round(fma_peak, 2), "frac": round(bwd_macs / t / 1e12 / fma_peak, 5),
+                "traffic": ncu_traffic(name),
                 "peak_source": f"derived: 148 SM x 128 FFMA/clk x {sm_mhz:.0f} MHz",
                 "algorithmic": f"{bwd_macs} MACs per launch (2 x pairs on kept outputs)"}
     per_launch_bytes = {
-        "sel_hist": 4 * nseg * V,
-        "sel_count": 4 * nseg * V,
-        "sel_write": 4 * nseg * V + 12 * ny,
+        "fwd_classify": 4 * nseg * V,
+        "fwd_write": 4 * nseg * V + 12 * ny,
         "row_index": 8 * nnz_x + 4 * (B_local * C_IN * RES * RES + 1),
+        "dbias": 12 * ny,
     }.get(name)
     if per_launch_bytes is None:
         return {"kernel": name, "bound": "unknown", "achieved": None, "peak": None, "unit": None, "frac": None,
                 "traffic": None}
     gbs = per_launch_bytes / t / 1e9
     return {"kernel": name, "bound": "hbm", "achieved": round(gbs, 1), "unit": "GB/s", "peak": hbm,
-            "frac": round(gbs / hbm, 4), "traffic": None, "peak_source": f"{src} (MEASURED_PEAKS.json hbm_gbs)",
+            "frac": round(gbs / hbm, 4), "traffic": ncu_traffic(name),
+            "peak_source": f"{src} (MEASURED_PEAKS.json hbm_gbs)",
             "algorithmic": f"{per_launch_bytes} bytes per launch"}
+
+
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture, or None."""
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_traffic.json")), reverse=True):
+        try:
+            d = json.load(open(path))
+        except Exception:
+            continue
+        if kernel in d:
+            return {"bytes": d[kernel]["traffic"], "source": os.path.relpath(path, ROOT) + ":" + d[kernel]["report"]}
+    return None
 
 
 def run_e2e(torch, spc, x, w, bias, k, cap, dy_dev, args, world, dist):
@@ -367,7 +377,7 @@ def run_e2e(torch, spc, x, w, bias, k, cap, dy_dev, args, world, dist):
     out_dw = torch.empty(W.keys.numel()).pin_memory()
     out_db = torch.empty(C_OUT).pin_memory()
     out_n = torch.empty(1, dtype=torch.int64).pin_memory()
-    red = torch.empty(W.keys.numel() + C_OUT, dtype=torch.float64, device="cuda")
+    allreduce = spc.dp.GradAllReduce(W.keys.numel(), C_OUT, "cuda")
 
     def step():
         dk.copy_(hk, non_blocking=True)
@@ -375,12 +385,7 @@ def run_e2e(torch, spc, x, w, bias, k, cap, dy_dev, args, world, dist):
         ddy.copy_(hdy, non_blocking=True)
         Y = fwd(X, W, bias_t)
         bwd(X, W, Y, ddy, dx, dw, db)
-        if dist is not None:
-            red[:dw.numel()].copy_(dw)
-            red[dw.numel():].copy_(db)
-            dist.all_reduce(red)
-            dw.copy_(red[:dw.numel()])
-            db.copy_(red[dw.numel():])
+        allreduce(dw, db)
         out_dw.copy_(dw, non_blocking=True)
         out_db.copy_(db, non_blocking=True)
         out_n.copy_(Y.nnz_dev, non_blocking=True)
