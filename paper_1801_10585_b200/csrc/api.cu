@@ -181,6 +181,11 @@ FwdWs carve_fwd(Carver& c, const Geo& gx, const Geo& gy, const KGeo& kg, const F
     a.cand_cur = c.take<unsigned long long>((size_t)nseg);
     a.cand = c.take<uint2>(attn == SPC_ATTN_NONE ? 1 : (size_t)(nseg * gy.V));
     a.seg_off = c.take<uint64_t>((size_t)nseg + 1);
+    const size_t PK = (size_t)w->c_in * kg.kx;
+    a.rec = c.take<int4>((size_t)t.n_ocg * t.nwg_max + 1);
+    a.pkoff = c.take<int>((size_t)t.n_ocg * (PK + 1));
+    a.pkfull = c.take<int>((size_t)t.n_ocg * PK);
+    a.guard = c.take<int>(1);
     ws.flag = c.take<int>(1);
     return ws;
 }
@@ -240,14 +245,14 @@ spc_status_t conv_bwd_impl(const spc_map_t* x, const spc_filter_t* w, const spc_
         SPC_TRY(maybe_validate(x, ws.flag, s));
         SPC_TRY(maybe_validate(y, ws.flag, s));
     }
+    SPC_TRY(cu(launch_row_index(gy, y->keys, y->nnz_dev, y->nnz, ws.yrow, s)));
     if (dbias) {
         SPC_TRY(cu(cudaMemsetAsync(ws.db_acc, 0, sizeof(double) * (size_t)w->c_out, s)));
-        SPC_TRY(cu(launch_dbias(gy, y->keys, dy, y->nnz_dev, y->nnz, ws.db_acc, s)));
+        SPC_TRY(cu(launch_dbias(gy, ws.yrow, dy, ws.db_acc, s)));
         SPC_TRY(cu(launch_f64_to_f32(ws.db_acc, dbias, w->c_out, s)));
     }
     if (!want_dx && !want_dw) return SPC_OK;
     SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
-    SPC_TRY(cu(launch_row_index(gy, y->keys, y->nnz_dev, y->nnz, ws.yrow, s)));
     SPC_TRY(cu(launch_filter_table(kg, (int)w->c_in, (int)w->c_out, w->keys, w->values, w->nnz, ws.f.meta, ws.f.val,
                                    ws.f.off, ws.f.src, ws.f.scratch, s)));
     if (want_dx && t.n_ocg > 1 && x->nnz > 0) SPC_TRY(cu(cudaMemsetAsync(dx, 0, sizeof(float) * (size_t)x->nnz, s)));
@@ -387,6 +392,8 @@ spc_status_t sparse_conv_fwd(const spc_map_t* x, const spc_filter_t* w, const fl
                                        ws.off2, ws.scratch2, s)));
     FwdArgs a = ws.a;
     a.xkeys = x->keys;
+    a.x_nnz_dev = x->nnz_dev;
+    a.x_nnz = x->nnz;
     a.xvals = x->values;
     a.xrow = ws.xrow;
     a.meta2 = ws.meta2;

@@ -117,7 +117,8 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
     p += (size_t)(c_in + 1) * sizeof(int);
     uint32_t* rng = reinterpret_cast<uint32_t*>(p);
     p += (size_t)c_in * t.TX * 2 * sizeof(uint32_t);
-    p = reinterpret_cast<unsigned char*>(((uintptr_t)p + 15) & ~(uintptr_t)15);
+    // align from the __shared__ base with integer offsets (keeps the shared address space)
+    p = smraw + ((size_t)(p - smraw + 15) & ~(size_t)15);
     int* st_eb = reinterpret_cast<int*>(p) + warp * 64;   // per warp: 32 ebase + 32 values
     float* st_v = reinterpret_cast<float*>(st_eb + 32);
 
@@ -186,15 +187,20 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
             rng[2 * q + 1] = hi;
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            int acc = 0;
-            for (int ic = 0; ic < c_in; ++ic) {
-                cpre[ic] = acc;
+        if (warp == 0) {   // chunks per ic (32 entries each), exclusive prefix over ic
+            int carry = 0;
+            for (int ic0 = 0; ic0 < c_in; ic0 += 32) {
+                const int ic = ic0 + lane;
                 int cnt = 0;
-                for (int xi = 0; xi < t.TX; ++xi) cnt += (int)(rng[2 * (ic * t.TX + xi) + 1] - rng[2 * (ic * t.TX + xi)]);
-                acc += (cnt + 31) >> 5;
+                if (ic < c_in)
+                    for (int xi = 0; xi < t.TX; ++xi)
+                        cnt += (int)(rng[2 * (ic * t.TX + xi) + 1] - rng[2 * (ic * t.TX + xi)]);
+                const int nch = (cnt + 31) >> 5;
+                const int incl = warp_incl_scan(nch);
+                if (ic < c_in) cpre[ic] = carry + incl - nch;
+                carry += __shfl_sync(kFull, incl, 31);
             }
-            cpre[c_in] = acc;
+            if (lane == 0) cpre[c_in] = carry;
         }
         __syncthreads();
         const int nchunks = cpre[c_in];
@@ -224,28 +230,31 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
                 }
             }
             __syncwarp();
-            st_eb[lane] = eb;
+            st_eb[lane] = eb * (int)sizeof(float);   // byte offsets into G
             st_v[lane] = v;
             __syncwarp();
             const int n = lbase[ic + 1] - lbase[ic];
             const int lb = lbase[ic];
-            float dxa = 0.0f;
+            const char* Gb = reinterpret_cast<const char*>(G);
+            float prod[32];
+#pragma unroll
+            for (int q = 0; q < 32; ++q) prod[q] = 0.0f;
             for (int wb = 0; wb < n; wb += 32) {
                 const int j = wb + lane;
                 const bool wok = j < n;
-                const int wd = wok ? wdel[lb + j] : wdel[lb];
+                const int wd = (wok ? wdel[lb + j] : wdel[lb]) * (int)sizeof(float);
                 const float wl = wok ? wv[lb + j] : 0.0f;
-                float prod[32];
                 float dwl = 0.0f;
 #pragma unroll
                 for (int q = 0; q < 32; ++q) {
-                    const float g = G[st_eb[q] - wd];
-                    prod[q] = g * wl;                       // bp_data contribution
+                    const float g = *reinterpret_cast<const float*>(Gb + (st_eb[q] - wd));
+                    prod[q] = fmaf(g, wl, prod[q]);         // bp_data contribution
                     dwl = fmaf(g, st_v[q], dwl);            // bp_filter contribution
                 }
-                if (DX) dxa += reduce_scatter32(prod, lane);
                 if (DW && wok && dwl != 0.0f) atomicAdd(&dwp[lb + j], (double)dwl);
             }
+            float dxa = 0.0f;
+            if (DX) dxa = reduce_scatter32(prod, lane);   // lane e: sum over this ic's weights
             if (DX && e >= 0) {
                 if (t.n_ocg == 1) dx[e] = dxa;
                 else atomicAdd(&dx[e], dxa);
@@ -315,66 +324,29 @@ cudaError_t launch_conv_bwd(const Geo& gx, const Geo& gy, const KGeo& kg, const 
                                      dx, dw_acc, s);
 }
 
-// dbias[oc] = sum of dy over the kept outputs of oc (fp64). Keys are sorted, so a thread's
-// run of consecutive entries mostly shares one (b, oc) segment: accumulate locally and flush
-// on segment change.
-__global__ void dbias_kernel(Geo gy, const uint64_t* __restrict__ ykeys, const float* __restrict__ dy,
-                             const int64_t* ny_dev, int64_t nbound, double* __restrict__ db) {
-    extern __shared__ double sdb[];
-    const int c_out = (int)gy.C;
-    for (int i = threadIdx.x; i < c_out; i += blockDim.x) sdb[i] = 0.0;
-    __syncthreads();
-    const int64_t n = load_n(ny_dev, nbound);
-    constexpr int RUN = 64;
-    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-    const int lane = threadIdx.x & 31;
-    constexpr uint64_t kNone = ~0ull;
-    // warp-uniform loop: lane L of a warp takes the run starting at wb + L*RUN
-    for (int64_t wb = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * RUN; wb < n; wb += nthreads * RUN) {
-        const int64_t t0 = wb + (int64_t)lane * RUN;
-        uint64_t seg = kNone;
-        double acc = 0.0;
-        if (t0 < n) {
-            const int64_t t1 = min(t0 + RUN, n);
-            // keys are sorted, so most runs lie in one segment
-            seg = ykeys[t0] / (uint64_t)gy.V;
-            uint64_t seg_end = (seg + 1) * (uint64_t)gy.V;    // first key of the next segment
-            for (int64_t t = t0; t < t1; ++t) {
-                const uint64_t k = ykeys[t];
-                if (k >= seg_end) {
-                    atomicAdd(&sdb[seg % c_out], acc);
-                    acc = 0.0;
-                    seg = k / (uint64_t)gy.V;
-                    seg_end = (seg + 1) * (uint64_t)gy.V;
-                }
-                acc += (double)dy[t];
-            }
-        }
-        // the usual case: the warp's runs end in one segment -> one atomic per warp
-        const uint64_t seg0 = __shfl_sync(kFull, seg, 0);
-        if (__all_sync(kFull, seg == seg0 || seg == kNone)) {
-            acc = warp_sum(acc);
-            if (lane == 0 && seg0 != kNone) atomicAdd(&sdb[seg0 % c_out], acc);
-        } else if (seg != kNone) {
-            atomicAdd(&sdb[seg % c_out], acc);
-        }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < c_out; i += blockDim.x)
-        if (sdb[i] != 0.0) atomicAdd(&db[i], sdb[i]);
+// dbias[oc] = sum of dy over the kept outputs of oc (fp64), reading R13. Segment (b, oc) owns
+// the contiguous entry range yrow[s*R] .. yrow[(s+1)*R] of the row index, so a block sums a
+// slice of one segment with coalesced loads and adds it to dbias[oc] once.
+__global__ void __launch_bounds__(256) dbias_kernel(Geo gy, const uint32_t* __restrict__ yrow,
+                                                    const float* __restrict__ dy, int splits,
+                                                    double* __restrict__ db) {
+    __shared__ double sm[33];
+    const int64_t s = blockIdx.x / splits;
+    const int j = blockIdx.x - (int)(s * splits);
+    const int64_t e0 = yrow[s * gy.R], e1 = yrow[(s + 1) * gy.R];
+    const int64_t len = e1 - e0, per = (len + splits - 1) / splits;
+    const int64_t lo = e0 + j * per, hi = min(e1, lo + per);
+    double acc = 0.0;
+    for (int64_t t = lo + threadIdx.x; t < hi; t += blockDim.x) acc += (double)dy[t];
+    acc = block_sum(acc, sm);
+    if (threadIdx.x == 0 && acc != 0.0) atomicAdd(&db[s % gy.C], acc);
 }
 
-cudaError_t launch_dbias(const Geo& gy, const uint64_t* ykeys, const float* dy, const int64_t* ny_dev,
-                         int64_t ny_bound, double* db_acc, cudaStream_t s) {
-    if (ny_bound <= 0) return cudaSuccess;
-    int64_t grid = (ny_bound + 256 * 64 - 1) / (256 * 64);
-    if (grid > 592) grid = 592;
-    const size_t sm = (size_t)gy.C * sizeof(double);
-    if (sm > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(dbias_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        if (e != cudaSuccess) return e;
-    }
-    { SPC_PHASE("dbias", s, 1); dbias_kernel<<<(unsigned)grid, 256, sm, s>>>(gy, ykeys, dy, ny_dev, ny_bound, db_acc); }
+cudaError_t launch_dbias(const Geo& gy, const uint32_t* yrow, const float* dy, double* db_acc, cudaStream_t s) {
+    const int64_t nseg = gy.B * gy.C;
+    if (nseg <= 0) return cudaSuccess;
+    const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(64, (4 * 148 + nseg - 1) / nseg));
+    { SPC_PHASE("dbias", s, 1); dbias_kernel<<<(unsigned)(nseg * splits), 256, 0, s>>>(gy, yrow, dy, splits, db_acc); }
     return cudaGetLastError();
 }
 

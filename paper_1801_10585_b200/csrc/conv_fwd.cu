@@ -35,15 +35,16 @@ namespace spc {
 
 constexpr int kFwdThreads = 256;
 constexpr int kFwdWarps = kFwdThreads / 32;
-constexpr size_t kFwdBudget = 108 * 1024;   // two CTAs (16 warps) per SM
-constexpr int kStageCap = 2048;             // staged input entries per chunk of input channels
-static_assert(2 * kStageCap >= kSelBins, "the epilogue histogram reuses the stage buffer");
+constexpr size_t kFwdBudget = 113 * 1024;   // two CTAs (16 warps) per SM
+constexpr int kStageCap = 1088;             // staged input entries per chunk of input channels
+static_assert(2 * kStageCap >= kSelBins + 32, "the epilogue histogram (+ 32 dummy bins) reuses the stage buffer");
+
+static size_t r4(size_t n) { return (n + 3) & ~(size_t)3; }
 
 // shared-memory bytes beyond the accumulator
 static size_t fwd_fixed_smem(const KGeo& kg, int c_in, int TY, int64_t nwg) {
-    auto r4 = [](size_t n) { return (n + 3) & ~(size_t)3; };
-    const size_t PK = (size_t)c_in * kg.kx, G = (size_t)c_in * kg.kx * kg.ky;
-    return 4 * (256 + 4 * r4((size_t)nwg) + r4(G + 1) + r4(PK * (TY + 2 * kg.hy + 1)) + r4(PK + 1) +
+    const size_t PK = (size_t)c_in * kg.kx;
+    return 4 * (256 + 4 * (size_t)nwg + 2 * r4(PK + 1) + r4(PK * (TY + 2 * kg.hy + 1)) + r4(PK + 1) +
                 2 * (size_t)kStageCap) + 64;
 }
 
@@ -52,11 +53,12 @@ FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_
     const int ZR = ((gy.Z + 2 * kg.hz + 3) / 4) * 4;
     const int pad = ((kg.hz + 3) / 4) * 4;
     const size_t row_b = (size_t)ZR * sizeof(float);
+    auto rows = [&](int TY) { return TY + 2 * kg.hy + 2 * kg.hy * kFwdWarps; };
     auto need = [&](int ocg, int TY) {
         const int64_t nwg = std::min<int64_t>(nw_total, (int64_t)ocg * c_in * kg.KV);
-        return fwd_fixed_smem(kg, c_in, TY, nwg) + (size_t)ocg * TY * row_b + (size_t)pad * 8;
+        return fwd_fixed_smem(kg, c_in, TY, nwg) + (size_t)ocg * rows(TY) * row_b + (size_t)pad * 8;
     };
-    // prefer >= 8 rows per warp (lane utilisation), then the largest group of channels
+    // prefer >= 8 input rows per warp (lane utilisation), then the largest group of channels
     int TY = std::min(gy.Y, 8 * kFwdWarps);
     int ocg = std::min(c_out, 16);
     while (ocg > 1 && need(ocg, TY) > kFwdBudget) --ocg;
@@ -66,6 +68,7 @@ FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_
     TY = std::min(TY, std::min(gy.Y, 240));   // staged rows are packed in 8 bits (TY + 2*hy < 256)
     t.TY = TY;
     t.RW = (TY + kFwdWarps - 1) / kFwdWarps;
+    t.RT = rows(TY);
     t.nty = (gy.Y + TY - 1) / TY;
     t.ocg = ocg;
     t.n_ocg = (c_out + ocg - 1) / ocg;
@@ -75,6 +78,106 @@ FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_
     t.nwg_max = (int)std::min<int64_t>(nw_total, (int64_t)ocg * c_in * kg.KV);
     t.smem = need(ocg, TY);
     return t;
+}
+
+// The -0 accumulation mode of conv_fwd is exact iff every product of an input value and a weight
+// is a nonzero multiple of 2^-149: true when all |x|, |w| >= 2^-50 (then no update can round to
+// -0, the marker). This pass flags inputs that break it (weights: fwd_rounds_kernel).
+__global__ void value_guard_kernel(const float* __restrict__ v, const int64_t* nnz_dev, int64_t bound,
+                                   int* __restrict__ guard) {
+    const int64_t n = load_n(nnz_dev, bound);
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float a = v[i];
+        bad |= !(fabsf(a) >= 0x1p-50f) && !isnan(a);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) *guard = 1;
+}
+
+// Weight rounds of one output-channel group (one block per group). Alg. 1 walks "for {fid,
+// fval} in filter(oc, ic)"; the kernel below walks, per (ic, input plane dx), rounds that
+// pair a weight of channel 2p with one of channel 2p+1: the two targets lie in different channel
+// slices of the accumulator, so both read-modify-writes of a round can be in flight together.
+// Round record {wdA, wA, wdB, wB}: wd = byte offset from an input's accumulator position to its
+// target uid = id - (fid - centre) = slice(oc) - oy rows - oz columns. Per (ic, dx): first
+// the two-channel rounds of every pair, then the leftovers of the longer list (wdB unused).
+__global__ void fwd_rounds_kernel(KGeo kg, int c_in, int c_out, FwdTile t, const int2* __restrict__ meta2,
+                                  const float* __restrict__ val2, const int* __restrict__ off2, int4* __restrict__ rec,
+                                  int* __restrict__ pkoff, int* __restrict__ pkfull, int* __restrict__ guard) {
+    __shared__ int sm[33];
+    const int grp = blockIdx.x, oc0 = grp * t.ocg, nocl = min(t.ocg, c_out - oc0);
+    const int PK = c_in * kg.kx, npair = (nocl + 1) / 2;
+    const int SLb = t.RT * t.ZR * (int)sizeof(float);
+    int4* R = rec + (int64_t)grp * t.nwg_max;
+    int* PO = pkoff + (int64_t)grp * (PK + 1);
+    int* PF = pkfull + (int64_t)grp * PK;
+    auto count = [&](int pk, int oc) {
+        int n = 0;
+        if (oc < oc0 + nocl)
+            for (int dyi = 0; dyi < kg.ky; ++dyi) {
+                const int g = pk * kg.ky + dyi;
+                n += off2[g * (c_out + 1) + oc + 1] - off2[g * (c_out + 1) + oc];
+            }
+        return n;
+    };
+    // the r-th weight of channel oc in (ic, dx), ordered (dy, dz)
+    auto weight = [&](int pk, int oc, int r, int& wd, float& wv) {
+        for (int dyi = 0; dyi < kg.ky; ++dyi) {
+            const int g = pk * kg.ky + dyi;
+            const int lo = off2[g * (c_out + 1) + oc], n = off2[g * (c_out + 1) + oc + 1] - lo;
+            if (r < n) {
+                const int2 m = meta2[lo + r];
+                wd = (oc - oc0) * SLb - ((dyi - kg.hy) * t.ZR + m.y) * (int)sizeof(float);
+                wv = val2[lo + r];
+                if (!(fabsf(wv) >= 0x1p-50f) && !isnan(wv)) *guard = 1;
+                return;
+            }
+            r -= n;
+        }
+    };
+    int carry = 0;
+    for (int p0 = 0; p0 < PK; p0 += blockDim.x) {
+        const int pk = p0 + threadIdx.x;
+        int tot = 0, full = 0;
+        if (pk < PK)
+            for (int p = 0; p < npair; ++p) {
+                const int na = count(pk, oc0 + 2 * p), nb = count(pk, oc0 + 2 * p + 1);
+                tot += max(na, nb);
+                full += min(na, nb);
+            }
+        int all;
+        const int ex = block_excl_scan(tot, sm, &all);
+        if (pk < PK) {
+            const int base = carry + ex;
+            PO[pk] = base;
+            PF[pk] = full;
+            int f = base, sgl = base + full;
+            for (int p = 0; p < npair; ++p) {
+                const int oa = oc0 + 2 * p, ob = oa + 1;
+                const int na = count(pk, oa), nb = count(pk, ob);
+                const int m = min(na, nb);
+                for (int r = 0; r < m; ++r) {
+                    int4 q;
+                    float wa, wb;
+                    weight(pk, oa, r, q.x, wa);
+                    weight(pk, ob, r, q.z, wb);
+                    q.y = __float_as_int(wa);
+                    q.w = __float_as_int(wb);
+                    R[f++] = q;
+                }
+                const int ol = na > nb ? oa : ob;
+                for (int r = m; r < max(na, nb); ++r) {
+                    int4 q{0, 0, 0, 0};
+                    float wa;
+                    weight(pk, ol, r, q.x, wa);
+                    q.y = __float_as_int(wa);
+                    R[sgl++] = q;
+                }
+            }
+        }
+        carry += all;
+    }
+    if (threadIdx.x == 0) PO[PK] = carry;
 }
 
 // fast y = L / Z for L < 2^24 (float reciprocal + one correction each way)
@@ -87,6 +190,147 @@ __device__ __forceinline__ uint32_t div_small(uint32_t L, uint32_t Z, float invZ
 
 __device__ __forceinline__ uint64_t composite(uint32_t sc, uint32_t p) {
     return ((uint64_t)sc << 32) | (uint64_t)(0xffffffffu - p);
+}
+
+__device__ __forceinline__ float absent_add(float a, float b, uint32_t marker) {
+    if (__float_as_uint(a) == marker) return b;
+    if (__float_as_uint(b) == marker) return a;
+    return a + b;
+}
+
+// Epilogue rows of one output channel: merge the warps' copies of each row (fixed warp order),
+// bias on the support, streaming store of the slice, support count and (with attention) the
+// score-digit histogram. Branch-free: lanes off the support increment a private dummy bin past
+// the histogram instead of branching around the atomic.
+template <int MODE>
+__device__ __forceinline__ void epi_rows(const float* S, float* P, float bv, int nyr, int Z, int ZR, int warp,
+                                         int lane, uint32_t hist_s, uint32_t& cnt, int yoff, int nr, int hy,
+                                         uint32_t marker) {
+    const bool vec = (Z & 3) == 0;
+    const uint32_t dummy = hist_s + (uint32_t)(kSelBins + lane) * 4u;
+    for (int r = warp; r < nyr; r += kFwdWarps) {
+        // row yrel = r + yoff (relative to the first input row) has a copy in the region of every
+        // warp owning an input row in [yrel - hy, yrel + hy], at region row yrel + hy*(2w + 1)
+        const int yrel = r + yoff;
+        const int wlo = (8 * max(0, yrel - hy) + 7) / nr, whi = (8 * min(nr - 1, yrel + hy) + 7) / nr;
+        for (int z0 = 4 * lane; z0 < Z; z0 += 128) {
+            float v[4];
+            for (int w = wlo; w <= whi; ++w) {
+                const float* A = S + (yrel + hy * (2 * w + 1)) * ZR + z0;
+                float u[4];
+                if (vec) {
+                    const float4 q = *reinterpret_cast<const float4*>(A);
+                    u[0] = q.x; u[1] = q.y; u[2] = q.z; u[3] = q.w;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) u[e] = z0 + e < Z ? A[e] : __uint_as_float(marker);
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) v[e] = w == wlo ? u[e] : absent_add(v[e], u[e], marker);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool pres = __float_as_uint(v[u]) != marker;
+                v[u] = pres ? v[u] + bv : __uint_as_float(kAbsent);
+                cnt += pres ? 1u : 0u;
+                if (MODE != SPC_ATTN_NONE) {
+                    const uint32_t addr = pres ? hist_s + ((score_bits(__float_as_uint(v[u]), MODE) >> 21) << 2) : dummy;
+                    asm volatile("red.shared.add.u32 [%0], 1;" :: "r"(addr) : "memory");
+                }
+            }
+            if (vec) {
+                __stcs(reinterpret_cast<float4*>(P + (int64_t)r * Z + z0), make_float4(v[0], v[1], v[2], v[3]));
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (z0 + u < Z) __stcs(P + (int64_t)r * Z + z0 + u, v[u]);
+            }
+        }
+    }
+}
+
+// "add val*fval to buffer at uid" on the shared accumulator; the first update of a voxel
+// replaces the absent marker (structural support, reading R3)
+// shared-memory load (idle lanes read a harmless in-range word) / predicated store: no branch
+// around the read-modify-write
+__device__ __forceinline__ float lds_u(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_p(uint32_t addr, float v, bool p) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.f32 [%0], %1;\n\t}"
+                 :: "r"(addr), "f"(v), "r"((int)p) : "memory");
+}
+
+// (-0 mode: the marker is -0.0, which the first fma replaces by the product itself)
+template <bool NEG0>
+__device__ __forceinline__ float upd(float old, float v, float w) {
+    if (NEG0) return fmaf(v, w, old);
+    return fmaf(v, w, __float_as_uint(old) == kAbsent ? 0.0f : old);
+}
+
+// The accumulate loop of one staged chunk of input channels for one warp: every (ic, input
+// plane) run of the warp's input rows, 32 inputs per step (lanes), against the weight rounds.
+template <bool NEG0>
+__device__ __forceinline__ void fwd_items(const Geo& gx, const KGeo& kg, const FwdArgs& a, int64_t b, int x, int ic0,
+                                          int ic1, bool staged, int sb0, int A_w, int B_w, int NRP, int ylo, int Z,
+                                          int ZR, float invZ, int lane, const uint32_t* rp, const int* pko,
+                                          const int* pkf, const int4* rec, const int* sbase, const uint2* stage,
+                                          const char* accw) {
+    const int c_in = (int)gx.C;
+    const uint32_t accs = (uint32_t)__cvta_generic_to_shared(accw);
+    for (int pk = ic0 * kg.kx; pk < ic1 * kg.kx; ++pk) {
+        const uint32_t* RP = rp + pk * NRP;
+        const uint32_t e0 = RP[A_w], e1 = RP[B_w];
+        if (e0 == e1) continue;
+        const int rb = pko[pk], re = pko[pk + 1], rf = rb + pkf[pk];
+        if (rb == re) continue;
+        const int n = (int)(e1 - e0);
+        const int s0 = staged ? sbase[pk] - sb0 + (int)(e0 - RP[0]) : 0;
+        uint64_t rowbase = 0;
+        if (!staged) {
+            const int ic = pk / kg.kx, xs = x + (pk - ic * kg.kx) - kg.hx;
+            rowbase = (uint64_t)(((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo) * (uint64_t)Z;
+        }
+        for (int c = 0; c < n; c += 32) {
+            const bool valid = c + lane < n;
+            int pos = 0;   // idle lanes: position 0 of the warp's region (reads stay in range)
+            float v = 0.0f;
+            if (valid) {
+                if (staged) {
+                    const uint2 en = stage[s0 + c + lane];
+                    pos = (int)(en.x & 0xffffffu);
+                    v = __uint_as_float(en.y);
+                } else {
+                    const uint32_t L = (uint32_t)(a.xkeys[e0 + c + lane] - rowbase);
+                    const uint32_t yrel = div_small(L, (uint32_t)Z, invZ);
+                    pos = (int)(yrel * (uint32_t)ZR + (L - yrel * (uint32_t)Z));
+                    v = a.xvals[e0 + c + lane];
+                }
+            }
+            const uint32_t base = accs + (uint32_t)pos * 4u;
+            // two-channel rounds: both read-modify-writes in flight (distinct slices); predicated
+            // shared loads/stores (no branch), the next round's record prefetched
+            int4 q = rec[rb];
+            for (int r = rb; r < rf; ++r) {
+                const int4 qn = rec[r + 1];   // rec[re] stays inside shared memory (pko follows)
+                const uint32_t pa = base + (uint32_t)q.x, pb = base + (uint32_t)q.z;
+                const float oa = lds_u(pa), ob = lds_u(pb);
+                sts_p(pa, upd<NEG0>(oa, v, __int_as_float(q.y)), valid);
+                sts_p(pb, upd<NEG0>(ob, v, __int_as_float(q.w)), valid);
+                __syncwarp();   // the next round's lanes may read what this one wrote
+                q = qn;
+            }
+            for (int r = rf; r < re; ++r) {
+                const int4 qn = rec[r + 1];   // rec[re] stays inside shared memory (pko follows)
+                const uint32_t pa = base + (uint32_t)q.x;
+                sts_p(pa, upd<NEG0>(lds_u(pa), v, __int_as_float(q.y)), valid);
+                q = qn;
+                __syncwarp();
+            }
+        }
+    }
 }
 
 __global__ void __launch_bounds__(kFwdThreads, 2)
@@ -102,63 +346,41 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     const int nocl = min(t.ocg, c_out - oc0);
     const int y0 = ty * t.TY, ye = min(y0 + t.TY, gy.Y);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int TYZR = t.TY * ZR;
+    const int SL = t.RT * ZR;                        // floats per output-channel slice
 
     // shared layout (float offsets, 16-byte aligned pieces):
-    // [pad][acc ocg*TY*ZR][pad] | misc(256) | sw4 | swoff | rp | sbase | stage (= hist in the epilogue)
-    const int KXY = kg.kx * kg.ky;
-    const int G = c_in * KXY;                        // (ic, dx, dy) weight groups
+    // [pad][acc ocg*RT*ZR][pad] | misc(256) | rounds | pko | pkf | rp | sbase | stage (= hist in the epilogue)
     const int PK = c_in * kg.kx;                     // (ic, input plane) work items
     const int ylo = max(0, y0 - kg.hy), yhi = min(gy.Y, ye + kg.hy);
     const int nr = yhi - ylo;                        // input rows read per plane
     const int NRP = nr + 1;
-    const int nw4 = (t.nwg_max + 3) & ~3;
     float* acc = smf + t.pad;
-    uint32_t* misc = reinterpret_cast<uint32_t*>(smf + 2 * t.pad + t.ocg * TYZR);
-    // per weight {acc offset of its target, value bits, row offset oy, 0}
-    int4* sw4 = reinterpret_cast<int4*>(misc + 256);
-    int* swoff = reinterpret_cast<int*>(sw4 + nw4);   // [G + 1] first weight of each (ic, dx, dy)
-    uint32_t* rp = reinterpret_cast<uint32_t*>(swoff + ((G + 1 + 3) & ~3));
+    uint32_t* misc = reinterpret_cast<uint32_t*>(smf + 2 * t.pad + t.ocg * SL);
+    int4* rec = reinterpret_cast<int4*>(misc + 256);
+    int* pko = reinterpret_cast<int*>(rec + t.nwg_max);
+    int* pkf = pko + ((PK + 1 + 3) & ~3);
+    uint32_t* rp = reinterpret_cast<uint32_t*>(pkf + ((PK + 1 + 3) & ~3));
     int* sbase = reinterpret_cast<int*>(rp + ((PK * (t.TY + 2 * kg.hy + 1) + 3) & ~3));
     uint2* stage = reinterpret_cast<uint2*>(sbase + ((PK + 1 + 3) & ~3));
     uint32_t* hist = reinterpret_cast<uint32_t*>(stage);   // epilogue only
 
+    const bool neg0 = *a.guard == 0;                 // -0 accumulation mode (value_guard_kernel)
+    const uint32_t marker = neg0 ? kNegZero : kAbsent;
     {
-        const int n4 = (2 * t.pad + t.ocg * TYZR) / 4;
-        uint4 ab = make_uint4(kAbsent, kAbsent, kAbsent, kAbsent);
+        const int n4 = (2 * t.pad + t.ocg * SL) / 4;
+        uint4 ab = make_uint4(marker, marker, marker, marker);
         for (int i = threadIdx.x; i < n4; i += blockDim.x) reinterpret_cast<uint4*>(smf)[i] = ab;
     }
-    // this group's weights, ordered by (ic, dx, dy): "filter(oc, ic)" of Alg. 1. Each
-    // carries the accumulator offset of its target relative to the input's staged position:
-    // uid = id - (fid - centre) -> row y - oy, column z - oz, slice of channel oc.
-    {
-        int carry = 0;
-        for (int g0 = 0; g0 < G; g0 += blockDim.x) {
-            const int g = g0 + threadIdx.x;
-            int cnt = 0;
-            if (g < G) cnt = a.off2[g * (c_out + 1) + oc0 + nocl] - a.off2[g * (c_out + 1) + oc0];
-            int tot;
-            const int ex = block_excl_scan(cnt, reinterpret_cast<int*>(misc), &tot);
-            if (g < G) swoff[g] = carry + ex;
-            carry += tot;
-        }
-        if (threadIdx.x == 0) swoff[G] = carry;
-        __syncthreads();
-        for (int g = warp; g < G; g += kFwdWarps) {
-            const int lo = a.off2[g * (c_out + 1) + oc0];
-            const int n = swoff[g + 1] - swoff[g];
-            const int oy = g % kg.ky - kg.hy;
-            for (int j = lane; j < n; j += 32) {
-                const int2 m = a.meta2[lo + j];
-                sw4[swoff[g] + j] = make_int4((m.x - oc0) * TYZR - m.y + (ylo - y0 - oy) * ZR,
-                                              __float_as_int(a.val2[lo + j]), oy, 0);
-            }
-        }
-    }
+    const int* gpko = a.pkoff + (int64_t)blockIdx.y * (PK + 1);
+    for (int i = threadIdx.x; i <= PK; i += blockDim.x) pko[i] = gpko[i];
+    for (int i = threadIdx.x; i < PK; i += blockDim.x) pkf[i] = a.pkfull[(int64_t)blockIdx.y * PK + i];
 
     // ------------------------------------------------------------ accumulate (Alg. 1 inner loops)
-    const int yw0 = y0 + warp * t.RW, yw1 = min(yw0 + t.RW, ye);
-    const uint32_t nrw = (uint32_t)max(0, yw1 - yw0);
+    // Warp w owns input rows [A_w, B_w) (relative to ylo) and writes into a private region of the
+    // accumulator: input row yrel lands at region row yrel + hy*(2w + 1), so targets (rows
+    // yrel - oy, |oy| <= hy) of different warps never meet; the epilogue merges the copies.
+    const int A_w = (warp * nr) / kFwdWarps, B_w = ((warp + 1) * nr) / kFwdWarps;
+    const int cw = kg.hy * (2 * warp + 1) * ZR;
     const float invZ = 1.0f / (float)Z;
     // row pointers of every (ic, input plane), rows ylo..yhi, in one burst
     for (int q = threadIdx.x; q < PK * NRP; q += blockDim.x) {
@@ -168,6 +390,11 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
         rp[q] = (xs >= 0 && xs < gx.X) ? a.xrow[((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo + r] : 0u;
     }
     __syncthreads();
+    {   // this group's weight rounds (fwd_rounds_kernel), one coalesced copy
+        const int4* grec = a.rec + (int64_t)blockIdx.y * t.nwg_max;
+        const int nrec = pko[PK];
+        for (int i = threadIdx.x; i < nrec; i += blockDim.x) rec[i] = grec[i];
+    }
     {   // stage offsets of every (ic, plane) run
         int carry = 0;
         for (int p0 = 0; p0 < PK; p0 += blockDim.x) {
@@ -181,6 +408,7 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
         if (threadIdx.x == 0) sbase[PK] = carry;
         __syncthreads();
     }
+    const char* accw = reinterpret_cast<const char*>(acc + cw);
     // chunks of input channels whose stored inputs fit the stage (one coalesced burst each)
     for (int ic0 = 0; ic0 < c_in;) {
         int ic1 = ic0 + 1;
@@ -206,62 +434,14 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
             }
         }
         __syncthreads();
-        // work items (ic, input plane): the inputs of rows yw0-hy .. yw1+hy against all weights of
-        // (ic, dx) whose target row falls in this warp's rows
-        const int pk1 = (yw0 < yw1) ? ic1 * kg.kx : 0;
-        for (int pk = ic0 * kg.kx; pk < pk1; ++pk) {
-            const uint32_t* RP = rp + pk * NRP;
-            const int r0 = max(ylo, yw0 - kg.hy) - ylo, r1 = min(yhi, yw1 + kg.hy) - ylo;
-            const uint32_t e0 = RP[r0], e1 = RP[r1];
-            if (e0 == e1) continue;
-            const int wlo = swoff[pk * kg.ky], whi = swoff[(pk + 1) * kg.ky];
-            if (wlo == whi) continue;
-            const int n = (int)(e1 - e0);
-            const int s0 = staged ? sbase[pk] - sb0 + (int)(e0 - RP[0]) : 0;
-            uint64_t rowbase = 0;
-            if (!staged) {
-                const int ic = pk / kg.kx, xs = x + (pk - ic * kg.kx) - kg.hx;
-                rowbase = (uint64_t)(((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo) * (uint64_t)Z;
-            }
-            for (int c = 0; c < n; c += 32) {
-                const bool valid = c + lane < n;
-                int pos = 0, rel = -1000;                     // rel: input row - yw0
-                float v = 0.0f;
-                if (valid) {
-                    uint32_t yrel;
-                    if (staged) {
-                        const uint2 en = stage[s0 + c + lane];
-                        pos = (int)(en.x & 0xffffffu);
-                        v = __uint_as_float(en.y);
-                        yrel = en.x >> 24;
-                    } else {
-                        const uint32_t L = (uint32_t)(a.xkeys[e0 + c + lane] - rowbase);
-                        yrel = div_small(L, (uint32_t)Z, invZ);
-                        pos = (int)(yrel * (uint32_t)ZR + (L - yrel * (uint32_t)Z));
-                        v = a.xvals[e0 + c + lane];
-                    }
-                    rel = ylo + (int)yrel - yw0;
-                }
-                for (int j = wlo; j < whi; ++j) {
-                    const int4 q = sw4[j];
-                    const int wd = q.x;
-                    const float w = __int_as_float(q.y);
-                    // target row (input row - oy) must be one of this warp's rows
-                    if ((uint32_t)(rel - q.z) < nrw) {
-#ifdef SPC_DEBUG
-                        if (pos + wd < -t.pad || pos + wd >= t.ocg * TYZR + t.pad)
-                            printf("OOB b=%lld x=%d ty=%d oc0=%d warp=%d lane=%d pk=%d pos=%d wd=%d j=%d\n",
-                                   (long long)b, x, ty, oc0, warp, lane, pk, pos, wd, j);
-#endif
-                        // "add val*fval to buffer at uid"
-                        float* p = acc + pos + wd;
-                        const float old = *p;
-                        const float base = __float_as_uint(old) == kAbsent ? 0.0f : old;
-                        *p = fmaf(v, w, base);
-                    }
-                    __syncwarp();   // the next weight's lanes may read what this step wrote
-                }
-            }
+        // work items (ic, input plane): this warp's input rows against all weight rounds of (ic, dx)
+        if (A_w < B_w) {
+            if (neg0)
+                fwd_items<true>(gx, kg, a, b, x, ic0, ic1, staged, sb0, A_w, B_w, NRP, ylo, Z, ZR, invZ, lane, rp, pko,
+                                pkf, rec, sbase, stage, accw);
+            else
+                fwd_items<false>(gx, kg, a, b, x, ic0, ic1, staged, sb0, A_w, B_w, NRP, ylo, Z, ZR, invZ, lane, rp, pko,
+                                 pkf, rec, sbase, stage, accw);
         }
         __syncthreads();                                 // stage consumed
         ic0 = ic1;
@@ -274,44 +454,24 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     // histogram of the top score digit are accumulated for the attention threshold.
     const int nyr = ye - y0;
     const bool do_hist = a.attn != SPC_ATTN_NONE;
+    const uint32_t hist_s = (uint32_t)__cvta_generic_to_shared(hist);
     for (int ocl = 0; ocl < nocl; ++ocl) {
         const int oc = oc0 + ocl;
         const int64_t s = b * c_out + oc;
         const float bv = a.bias ? a.bias[oc] : 0.0f;
-        const float* A = acc + ocl * TYZR;
+        const float* S = acc + ocl * SL;
         if (do_hist)
             for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) hist[i] = 0;
         __syncthreads();
         uint32_t cnt = 0;
         float* P = a.pre + s * gy.V + ((int64_t)x * gy.Y + y0) * Z;
-        const bool vec = (Z & 3) == 0;
-        for (int r = warp; r < nyr; r += kFwdWarps) {
-            for (int z0 = 4 * lane; z0 < Z; z0 += 128) {
-                float v[4];
-                if (vec) {
-                    const float4 q = *reinterpret_cast<const float4*>(A + r * ZR + z0);
-                    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
-                } else {
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) v[u] = z0 + u < Z ? A[r * ZR + z0 + u] : __uint_as_float(kAbsent);
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (__float_as_uint(v[u]) != kAbsent) {
-                        v[u] += bv;
-                        ++cnt;
-                        if (do_hist) atomicAdd(&hist[score_bits(__float_as_uint(v[u]), a.attn) >> 21], 1u);
-                    }
-                }
-                if (vec) {
-                    __stcs(reinterpret_cast<float4*>(P + (int64_t)r * Z + z0), make_float4(v[0], v[1], v[2], v[3]));
-                } else {
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if (z0 + u < Z) __stcs(P + (int64_t)r * Z + z0 + u, v[u]);
-                }
-            }
-        }
+        const int yoff = y0 - ylo;
+        if (a.attn == SPC_ATTN_MAGNITUDE)
+            epi_rows<SPC_ATTN_MAGNITUDE>(S, P, bv, nyr, Z, ZR, warp, lane, hist_s, cnt, yoff, nr, kg.hy, marker);
+        else if (a.attn == SPC_ATTN_RAW)
+            epi_rows<SPC_ATTN_RAW>(S, P, bv, nyr, Z, ZR, warp, lane, hist_s, cnt, yoff, nr, kg.hy, marker);
+        else
+            epi_rows<SPC_ATTN_NONE>(S, P, bv, nyr, Z, ZR, warp, lane, hist_s, cnt, yoff, nr, kg.hy, marker);
         const uint32_t tot = block_sum(cnt, misc);
         if (threadIdx.x == 0 && tot) atomicAdd(&a.seg_count[s], (unsigned long long)tot);
         if (do_hist)
@@ -449,49 +609,71 @@ __global__ void __launch_bounds__(kChunkThreads) fwd_classify_kernel(FwdArgs a, 
     }
 }
 
-// resolve: the `need` largest composite keys among the candidates of a segment (8-bit radix
-// select over 64 bits, all keys distinct) -> kstar; then count selected candidates per chunk.
-__global__ void __launch_bounds__(512) fwd_resolve_kernel(FwdArgs a) {
+// resolve: the `need` largest composite keys among the candidates of a segment -> kstar; then
+// count selected candidates per chunk. All candidates share the top 11 bits (digit B1), so the
+// radix select starts below them: an 11-bit digit over the candidate list in HBM, after which
+// the survivors (about n/2048) are copied to shared memory and the remaining digits (8, 8, 8,
+// 8, 8, 2 bits) run there. All composite keys are distinct (p is unique), so kstar is exact.
+constexpr int kResThreads = 512;
+constexpr int kResCap = 2048;   // survivors kept in shared memory
+__global__ void __launch_bounds__(kResThreads) fwd_resolve_kernel(FwdArgs a) {
     const int64_t s = blockIdx.x;
     FwdSeg st = a.seg[s];
     if (st.keep_all) return;
     const uint64_t n = a.cand_cnt[s];
     const uint2* c = a.cand + a.cand_off[s];
-    __shared__ uint32_t h[256];
+    __shared__ uint32_t h[kSelBins];
+    __shared__ uint64_t sc[kResCap];
     __shared__ uint64_t sh_prefix, sh_mask;
     __shared__ int64_t sh_need;
+    __shared__ uint32_t sh_bin_cnt, sh_ns;
     if (threadIdx.x == 0) {
-        sh_prefix = 0;
-        sh_mask = 0;
+        sh_prefix = (uint64_t)st.b1 << 53;
+        sh_mask = (uint64_t)(kSelBins - 1) << 53;
         sh_need = st.need;
+        sh_ns = 0;
     }
-    __syncthreads();
-    for (int sh = 56; sh >= 0; sh -= 8) {
-        for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+    bool in_smem = false;
+    uint32_t ns = 0;
+#pragma unroll 1
+    for (int pass = 0; pass < 7; ++pass) {
+        const int sh = pass < 6 ? 42 - 8 * pass : 0;            // bits 52..42, 41..34, ..., 9..2, 1..0
+        const int nb = pass == 0 ? kSelBins : (pass < 6 ? 256 : 4);
+        for (int i = threadIdx.x; i < nb; i += blockDim.x) h[i] = 0;
         __syncthreads();
         const uint64_t prefix = sh_prefix, mask = sh_mask;
-        for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
-            const uint2 e = c[i];
-            const uint64_t k = composite(score_bits(e.y, a.attn), e.x);
-            if ((k & mask) == prefix) atomicAdd(&h[(k >> sh) & 255], 1u);
+        const uint32_t dmask = (uint32_t)nb - 1u;
+        if (!in_smem) {
+            for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+                const uint2 e = c[i];
+                const uint64_t k = composite(score_bits(e.y, a.attn), e.x);
+                if ((k & mask) == prefix) atomicAdd(&h[(uint32_t)(k >> sh) & dmask], 1u);
+            }
+        } else {
+            for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) {
+                const uint64_t k = sc[i];
+                if ((k & mask) == prefix) atomicAdd(&h[(uint32_t)(k >> sh) & dmask], 1u);
+            }
         }
         __syncthreads();
         if (threadIdx.x < 32) {
-            // warp scan of the 256 bins from the top: lane l owns bins 255-8l .. 248-8l
-            const int l = threadIdx.x;
+            // warp scan of the bins from the top: lane l owns bins nb-1-per*l .. nb-per*(l+1)
+            const int l = threadIdx.x, per = nb >= 32 ? nb / 32 : 1;
             uint32_t own = 0;
-            for (int q = 0; q < 8; ++q) own += h[255 - 8 * l - q];
+            if (l * per < nb)
+                for (int q = 0; q < per; ++q) own += h[nb - 1 - per * l - q];
             const uint32_t incl = warp_incl_scan(own);
             const int64_t need = sh_need;
             const int64_t before = (int64_t)(incl - own);
-            if (before < need && before + (int64_t)own >= need) {
+            if (own && before < need && before + (int64_t)own >= need) {
                 int64_t cum = before;
-                for (int q = 0; q < 8; ++q) {
-                    const int bin = 255 - 8 * l - q;
+                for (int q = 0; q < per; ++q) {
+                    const int bin = nb - 1 - per * l - q;
                     if (cum + (int64_t)h[bin] >= need) {
                         sh_need = need - cum;
                         sh_prefix = prefix | ((uint64_t)bin << sh);
-                        sh_mask = mask | ((uint64_t)255 << sh);
+                        sh_mask = mask | ((uint64_t)dmask << sh);
+                        sh_bin_cnt = h[bin];
                         break;
                     }
                     cum += h[bin];
@@ -499,6 +681,18 @@ __global__ void __launch_bounds__(512) fwd_resolve_kernel(FwdArgs a) {
             }
         }
         __syncthreads();
+        if (!in_smem && pass + 1 < 7 && sh_bin_cnt <= (uint32_t)kResCap) {
+            // survivors of the chosen prefix -> shared memory (order irrelevant: keys distinct)
+            const uint64_t p2 = sh_prefix, m2 = sh_mask;
+            for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+                const uint2 e = c[i];
+                const uint64_t k = composite(score_bits(e.y, a.attn), e.x);
+                if ((k & m2) == p2) sc[atomicAdd(&sh_ns, 1u)] = k;
+            }
+            __syncthreads();
+            ns = sh_ns;
+            in_smem = true;
+        }
     }
     const uint64_t kstar = sh_prefix;
     if (threadIdx.x == 0) {
@@ -582,6 +776,16 @@ cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& k
     if (a.attn != SPC_ATTN_NONE) cudaMemsetAsync(a.hist, 0, sizeof(uint32_t) * kSelBins * (size_t)nseg, s);
     const dim3 grid((unsigned)(gy.B * gy.X * t.nty), (unsigned)t.n_ocg);
     const unsigned sgrid = (unsigned)(nseg * a.nchunk);
+    cudaMemsetAsync(a.guard, 0, sizeof(int), s);
+    {
+        SPC_PHASE("value_guard", s, 1);
+        value_guard_kernel<<<148 * 4, 256, 0, s>>>(a.xvals, a.x_nnz_dev, a.x_nnz, a.guard);
+    }
+    {
+        SPC_PHASE("fwd_rounds", s, 1);
+        fwd_rounds_kernel<<<(unsigned)t.n_ocg, 128, 0, s>>>(kg, (int)gx.C, (int)gy.C, t, a.meta2, a.val2, a.off2,
+                                                          a.rec, a.pkoff, a.pkfull, a.guard);
+    }
     { SPC_PHASE("conv_fwd", s, 1); conv_fwd_kernel<<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a); }
     { SPC_PHASE("fwd_find", s, 1); fwd_find_kernel<<<(unsigned)nseg, 256, 0, s>>>(a, nseg); }
     if (a.attn != SPC_ATTN_NONE) {
@@ -591,7 +795,7 @@ cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& k
     { SPC_PHASE("fwd_classify", s, 1); fwd_classify_kernel<<<sgrid, kChunkThreads, 0, s>>>(a, gy.V); }
     if (a.attn != SPC_ATTN_NONE) {
         SPC_PHASE("fwd_resolve", s, 1);
-        fwd_resolve_kernel<<<(unsigned)nseg, 512, 0, s>>>(a);
+        fwd_resolve_kernel<<<(unsigned)nseg, kResThreads, 0, s>>>(a);
     }
     // kept per segment goes to cand_cnt (reused as scratch), then segment offsets
     { SPC_PHASE("fwd_chunk_scan", s, 1); fwd_chunk_scan_kernel<<<(unsigned)nseg, 256, 0, s>>>(a, a.cand_cnt); }

@@ -16,6 +16,7 @@ namespace spc {
 // Absent marker for the dense pre-attention buffer: a NaN pattern. Finite inputs never
 // produce it (NaN/Inf inputs are outside the contract).
 constexpr uint32_t kAbsent = 0x7fffffffu;
+constexpr uint32_t kNegZero = 0x80000000u;   // accumulator marker of the -0 mode (conv_fwd)
 
 // Geometry of a feature map with its spatial dims padded to rank 3 (leading 1s):
 // key = seg*V + (x*Y + y)*Z + z, seg = b*C + c. A "row" is (seg, x, y): the Z consecutive
@@ -103,8 +104,9 @@ cudaError_t launch_filter_table_fwd(const KGeo& kg, int c_in, int c_out, const u
 // owns rows [y0 + w*RW, y0 + (w+1)*RW). Tiles of a segment are in key order: ti = x*nty + ty.
 struct FwdTile {
     int TY, RW, nty, ocg, n_ocg, ZR, NT;
+    int RT;            // accumulator rows per output channel: TY + 2*hy input rows + 2*hy halo per warp
     int pad;           // leading float pad of the accumulator (z margin of row 0)
-    int nwg_max;       // stored weights of one output-channel group (upper bound)
+    int nwg_max;       // stored weights of one output-channel group (upper bound = round records)
     size_t smem;
 };
 FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_t nw_total);
@@ -118,11 +120,17 @@ struct FwdSeg {
 };
 struct FwdArgs {
     const uint64_t* xkeys;
+    const int64_t* x_nnz_dev;        // device-side input count (or null: x_nnz)
+    int64_t x_nnz;
     const float* xvals;
     const uint32_t* xrow;
     const int2* meta2;
     const float* val2;
     const int* off2;
+    int4* rec;                       // [n_ocg * nwg_max] weight rounds {wdA, wA, wdB, wB} (fwd_rounds)
+    int* pkoff;                      // [n_ocg * (PK + 1)] first round of each (ic, input plane)
+    int* pkfull;                     // [n_ocg * PK] rounds with two channels
+    int* guard;                      // set when some |x| or |w| < 2^-50: NaN-marker accumulation
     const float* bias;
     int attn;
     int64_t k;
@@ -157,8 +165,7 @@ cudaError_t launch_conv_bwd(const Geo& gx, const Geo& gy, const KGeo& kg, const 
                             const uint64_t* ykeys, const float* dy, const uint32_t* yrow,
                             const int2* wmeta, const float* wval, const int* woff, const int* wsrc,
                             float* dx, double* dw_acc, bool want_dx, bool want_dw, cudaStream_t s);
-cudaError_t launch_dbias(const Geo& gy, const uint64_t* ykeys, const float* dy, const int64_t* ny_dev,
-                         int64_t ny_bound, double* db_acc, cudaStream_t s);
+cudaError_t launch_dbias(const Geo& gy, const uint32_t* yrow, const float* dy, double* db_acc, cudaStream_t s);
 cudaError_t launch_f64_to_f32(const double* a, float* b, int64_t n, cudaStream_t s);
 
 // ---------------------------------------------------------------- selection (attention)
