@@ -215,7 +215,17 @@ __device__ __forceinline__ void epi_rows(const float* S, float* P, float bv, int
         const int wlo = (8 * max(0, yrel - hy) + 7) / nr, whi = (8 * min(nr - 1, yrel + hy) + 7) / nr;
         for (int z0 = 4 * lane; z0 < Z; z0 += 128) {
             float v[4];
-            for (int w = wlo; w <= whi; ++w) {
+            {
+                const float* A = S + (yrel + hy * (2 * wlo + 1)) * ZR + z0;
+                if (vec) {
+                    const float4 q = *reinterpret_cast<const float4*>(A);
+                    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) v[e] = z0 + e < Z ? A[e] : __uint_as_float(marker);
+                }
+            }
+            for (int w = wlo + 1; w <= whi; ++w) {   // rows next to a warp boundary: merge copies
                 const float* A = S + (yrel + hy * (2 * w + 1)) * ZR + z0;
                 float u[4];
                 if (vec) {
@@ -226,13 +236,13 @@ __device__ __forceinline__ void epi_rows(const float* S, float* P, float bv, int
                     for (int e = 0; e < 4; ++e) u[e] = z0 + e < Z ? A[e] : __uint_as_float(marker);
                 }
 #pragma unroll
-                for (int e = 0; e < 4; ++e) v[e] = w == wlo ? u[e] : absent_add(v[e], u[e], marker);
+                for (int e = 0; e < 4; ++e) v[e] = absent_add(v[e], u[e], marker);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const bool pres = __float_as_uint(v[u]) != marker;
                 v[u] = pres ? v[u] + bv : __uint_as_float(kAbsent);
-                cnt += pres ? 1u : 0u;
+                if (MODE == SPC_ATTN_NONE) cnt += pres ? 1u : 0u;   // else: the histogram total
                 if (MODE != SPC_ATTN_NONE) {
                     const uint32_t addr = pres ? hist_s + ((score_bits(__float_as_uint(v[u]), MODE) >> 21) << 2) : dummy;
                     asm volatile("red.shared.add.u32 [%0], 1;" :: "r"(addr) : "memory");
@@ -293,6 +303,7 @@ __device__ __forceinline__ void fwd_items(const Geo& gx, const KGeo& kg, const F
             const int ic = pk / kg.kx, xs = x + (pk - ic * kg.kx) - kg.hx;
             rowbase = (uint64_t)(((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo) * (uint64_t)Z;
         }
+#pragma unroll 1
         for (int c = 0; c < n; c += 32) {
             const bool valid = c + lane < n;
             int pos = 0;   // idle lanes: position 0 of the warp's region (reads stay in range)
@@ -313,6 +324,7 @@ __device__ __forceinline__ void fwd_items(const Geo& gx, const KGeo& kg, const F
             // two-channel rounds: both read-modify-writes in flight (distinct slices); predicated
             // shared loads/stores (no branch), the next round's record prefetched
             int4 q = rec[rb];
+#pragma unroll 2
             for (int r = rb; r < rf; ++r) {
                 const int4 qn = rec[r + 1];   // rec[re] stays inside shared memory (pko follows)
                 const uint32_t pa = base + (uint32_t)q.x, pb = base + (uint32_t)q.z;
@@ -322,6 +334,7 @@ __device__ __forceinline__ void fwd_items(const Geo& gx, const KGeo& kg, const F
                 __syncwarp();   // the next round's lanes may read what this one wrote
                 q = qn;
             }
+#pragma unroll 1
             for (int r = rf; r < re; ++r) {
                 const int4 qn = rec[r + 1];   // rec[re] stays inside shared memory (pko follows)
                 const uint32_t pa = base + (uint32_t)q.x;
@@ -424,6 +437,7 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
                 const int n = sbase[pk + 1] - sbase[pk];
                 uint2* dst = stage + (sbase[pk] - sb0);
                 const uint64_t rowbase = (uint64_t)(((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo) * (uint64_t)Z;
+#pragma unroll 4
                 for (int i = lane; i < n; i += 32) {
                     const uint32_t L = (uint32_t)(a.xkeys[g0 + i] - rowbase);
                     const uint32_t yrel = div_small(L, (uint32_t)Z, invZ);
@@ -472,11 +486,16 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
             epi_rows<SPC_ATTN_RAW>(S, P, bv, nyr, Z, ZR, warp, lane, hist_s, cnt, yoff, nr, kg.hy, marker);
         else
             epi_rows<SPC_ATTN_NONE>(S, P, bv, nyr, Z, ZR, warp, lane, hist_s, cnt, yoff, nr, kg.hy, marker);
+        if (do_hist) {   // merge the tile histogram; support size = its total
+            __syncthreads();
+            for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) {
+                const uint32_t h = hist[i];
+                cnt += h;
+                if (h) atomicAdd(&a.hist[s * kSelBins + i], h);
+            }
+        }
         const uint32_t tot = block_sum(cnt, misc);
         if (threadIdx.x == 0 && tot) atomicAdd(&a.seg_count[s], (unsigned long long)tot);
-        if (do_hist)
-            for (int i = threadIdx.x; i < kSelBins; i += blockDim.x)
-                if (hist[i]) atomicAdd(&a.hist[s * kSelBins + i], hist[i]);
         __syncthreads();
     }
 }
@@ -548,14 +567,49 @@ constexpr int kChunk = kChunkThreads * kChunkItems;   // voxels per chunk of a (
 // classify (HBM stream over the buffers): per chunk the entries kept outright (digit > B1, or
 // every support entry when the segment keeps all) and the candidates (digit == B1), which are
 // appended to the segment's candidate list.
+template <int MODE>
+__device__ __forceinline__ void classify_chunk(const FwdArgs& a, const FwdSeg& st, int64_t s, int64_t c, int64_t V,
+                                               const uint32_t (&bits)[kChunkItems], int64_t lo,
+                                               unsigned long long* sm) {
+    // digit of each value, -1 off the support: kept outright iff d > B1, candidate iff d == B1
+    int d[kChunkItems];
+    uint32_t def = 0, cand = 0;
+#pragma unroll
+    for (int u = 0; u < kChunkItems; ++u) {
+        const bool pres = bits[u] != kAbsent;
+        d[u] = pres ? (int)(score_bits(bits[u], MODE) >> 21) : -1;
+        if (st.keep_all) d[u] = pres ? (int)st.b1 + 1 : -1;   // keep-all: every support entry is "definite"
+        def += d[u] > (int)st.b1 ? 1u : 0u;
+        cand += d[u] == (int)st.b1 ? 1u : 0u;
+    }
+    // one scan of (definite << 32 | candidates) gives the tile total and each thread's slot
+    unsigned long long tot;
+    const unsigned long long ex = block_excl_scan(((unsigned long long)def << 32) | cand, sm, &tot);
+    __shared__ uint64_t sh_base;
+    const uint32_t tcand = (uint32_t)tot;
+    if (threadIdx.x == 0) {
+        a.tile_def[s * a.nchunk + c] = (uint32_t)(tot >> 32);
+        sh_base = tcand ? a.cand_off[s] + atomicAdd(&a.cand_cur[s], (unsigned long long)tcand) : 0ull;
+    }
+    __syncthreads();
+    if (tcand == 0 || cand == 0) return;
+    uint2* out = a.cand + sh_base + (uint32_t)ex;
+    uint32_t k = 0;
+#pragma unroll
+    for (int u = 0; u < kChunkItems; ++u) {
+        if (d[u] == (int)st.b1) {
+            const uint32_t p = (uint32_t)(lo + 4 * ((int64_t)(u >> 2) * kChunkThreads + threadIdx.x) + (u & 3));
+            out[k++] = make_uint2(p, bits[u]);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kChunkThreads) fwd_classify_kernel(FwdArgs a, int64_t V) {
     const int64_t s = blockIdx.x / a.nchunk, c = blockIdx.x % a.nchunk;
     const FwdSeg st = a.seg[s];
     const int64_t lo = c * kChunk;
     const float* P = a.pre + s * V;
-    __shared__ uint32_t sh_cnt, sh_base, sh_slot;
-    const int lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) { sh_cnt = 0; sh_slot = 0; }
+    __shared__ unsigned long long sm[33];
     // element u of this thread: lo + 4*(v*256 + tid) + w, u = 4v + w (float4 loads, coalesced)
     uint32_t bits[kChunkItems];
     const bool vec = (V & 3) == 0;
@@ -573,40 +627,8 @@ __global__ void __launch_bounds__(kChunkThreads) fwd_classify_kernel(FwdArgs a, 
             for (int w = 0; w < 4; ++w) bits[4 * v + w] = i + w < V ? __float_as_uint(P[i + w]) : kAbsent;
         }
     }
-    uint32_t packed = 0;   // kept outright (low 16 bits) | candidates (high 16 bits)
-#pragma unroll
-    for (int u = 0; u < kChunkItems; ++u) {
-        if (bits[u] == kAbsent) continue;
-        if (st.keep_all) { ++packed; continue; }
-        const uint32_t d = score_bits(bits[u], a.attn) >> 21;
-        packed += (d > st.b1) + ((uint32_t)(d == st.b1) << 16);
-    }
-    packed = warp_sum(packed);
-    __syncthreads();
-    if (lane == 0 && packed) atomicAdd(&sh_cnt, packed);
-    __syncthreads();
-    const uint32_t tot = sh_cnt;
-    const uint32_t tcand = tot >> 16;
-    if (threadIdx.x == 0) {
-        a.tile_def[s * a.nchunk + c] = tot & 0xffffu;
-        sh_base = tcand ? (uint32_t)atomicAdd(&a.cand_cur[s], (unsigned long long)tcand) : 0u;
-    }
-    __syncthreads();
-    if (tcand == 0) return;
-    const uint64_t base = a.cand_off[s] + sh_base;
-#pragma unroll
-    for (int u = 0; u < kChunkItems; ++u) {
-        const bool is_c = bits[u] != kAbsent && (score_bits(bits[u], a.attn) >> 21) == st.b1;
-        const unsigned m = __ballot_sync(kFull, is_c);
-        if (!m) continue;
-        uint32_t slot0 = 0;
-        if (lane == 0) slot0 = atomicAdd(&sh_slot, (uint32_t)__popc(m));
-        slot0 = __shfl_sync(kFull, slot0, 0);
-        if (is_c) {
-            const uint32_t p = (uint32_t)(lo + 4 * ((int64_t)(u >> 2) * kChunkThreads + threadIdx.x) + (u & 3));
-            a.cand[base + slot0 + __popc(m & ((1u << lane) - 1u))] = make_uint2(p, bits[u]);
-        }
-    }
+    if (a.attn == SPC_ATTN_RAW) classify_chunk<SPC_ATTN_RAW>(a, st, s, c, V, bits, lo, sm);
+    else classify_chunk<SPC_ATTN_MAGNITUDE>(a, st, s, c, V, bits, lo, sm);   // NONE: keep_all
 }
 
 // resolve: the `need` largest composite keys among the candidates of a segment -> kstar; then
@@ -722,45 +744,69 @@ __global__ void fwd_chunk_scan_kernel(FwdArgs a, uint64_t* kept) {
     if (threadIdx.x == 0) kept[s] = carry;
 }
 
+// Elements are loaded as in classify (slab v = 0..3 of 256 float4, thread t holds voxels
+// lo + 4*(v*256 + t) + w): coalesced. Key order within the chunk is (v, t, w), so one scan of
+// four packed 16-bit per-slab counts gives every thread the output slot of each of its slabs.
+template <int MODE>
+__device__ __forceinline__ void write_chunk(const FwdArgs& a, const FwdSeg& st, int64_t s, int64_t c, int64_t V,
+                                            const uint32_t (&bits)[kChunkItems], int64_t lo,
+                                            unsigned long long* sm) {
+    uint32_t keep = 0;
+    unsigned long long packed = 0;
+#pragma unroll
+    for (int u = 0; u < kChunkItems; ++u) {
+        const uint32_t p = (uint32_t)(lo + 4 * ((int64_t)(u >> 2) * kChunkThreads + threadIdx.x) + (u & 3));
+        bool k = bits[u] != kAbsent;
+        if (!st.keep_all) k = k && composite(score_bits(bits[u], MODE), p) >= st.kstar;
+        keep |= (uint32_t)k << u;
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) packed |= (unsigned long long)__popc((keep >> (4 * v)) & 15u) << (16 * v);
+    unsigned long long tot;
+    const unsigned long long ex = block_excl_scan(packed, sm, &tot);
+    uint64_t pos = a.seg_off[s] + a.tile_off[s * a.nchunk + c];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+        uint64_t q = pos + ((ex >> (16 * v)) & 0xffffu);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const int u = 4 * v + w;
+            if (keep & (1u << u)) {
+                a.out_keys[q] = (uint64_t)s * (uint64_t)V + (uint64_t)(lo + 4 * ((int64_t)v * kChunkThreads + threadIdx.x) + w);
+                a.out_vals[q] = __uint_as_float(bits[u]);
+                ++q;
+            }
+        }
+        pos += (tot >> (16 * v)) & 0xffffu;
+    }
+}
+
 // write (HBM stream): keep iff composite(score, p) >= kstar (all support when keep-all);
 // ordered compaction in key order ("compress ids ... write k largest features").
 __global__ void __launch_bounds__(kChunkThreads) fwd_write_kernel(FwdArgs a, int64_t V) {
     const int64_t s = blockIdx.x / a.nchunk, c = blockIdx.x % a.nchunk;
     const FwdSeg st = a.seg[s];
-    const int64_t lo = c * kChunk + (int64_t)threadIdx.x * kChunkItems;
+    const int64_t lo = c * kChunk;
     const float* P = a.pre + s * V;
-    __shared__ uint64_t sm[33];
+    __shared__ unsigned long long sm[33];
     uint32_t bits[kChunkItems];
-    uint32_t keep = 0;
-    if (lo + kChunkItems <= V && (V & 3) == 0) {
+    const bool vec = (V & 3) == 0;
 #pragma unroll
-        for (int u = 0; u < kChunkItems; u += 4) {
-            const float4 q = __ldcs(reinterpret_cast<const float4*>(P + lo + u));
-            bits[u] = __float_as_uint(q.x);
-            bits[u + 1] = __float_as_uint(q.y);
-            bits[u + 2] = __float_as_uint(q.z);
-            bits[u + 3] = __float_as_uint(q.w);
-        }
-    } else {
+    for (int v = 0; v < kChunkItems / 4; ++v) {
+        const int64_t i = lo + 4 * ((int64_t)v * kChunkThreads + threadIdx.x);
+        if (vec && i + 4 <= V) {
+            const float4 q = __ldcs(reinterpret_cast<const float4*>(P + i));
+            bits[4 * v] = __float_as_uint(q.x);
+            bits[4 * v + 1] = __float_as_uint(q.y);
+            bits[4 * v + 2] = __float_as_uint(q.z);
+            bits[4 * v + 3] = __float_as_uint(q.w);
+        } else {
 #pragma unroll
-        for (int u = 0; u < kChunkItems; ++u) bits[u] = lo + u < V ? __float_as_uint(P[lo + u]) : kAbsent;
-    }
-#pragma unroll
-    for (int u = 0; u < kChunkItems; ++u) {
-        bool k = bits[u] != kAbsent;
-        if (k && !st.keep_all) k = composite(score_bits(bits[u], a.attn), (uint32_t)(lo + u)) >= st.kstar;
-        keep |= (uint32_t)k << u;
-    }
-    uint64_t tot;
-    uint64_t pos = a.seg_off[s] + a.tile_off[s * a.nchunk + c] + block_excl_scan((uint64_t)__popc(keep), sm, &tot);
-#pragma unroll
-    for (int u = 0; u < kChunkItems; ++u) {
-        if (keep & (1u << u)) {
-            a.out_keys[pos] = (uint64_t)s * (uint64_t)V + (uint64_t)(lo + u);
-            a.out_vals[pos] = __uint_as_float(bits[u]);
-            ++pos;
+            for (int w = 0; w < 4; ++w) bits[4 * v + w] = i + w < V ? __float_as_uint(P[i + w]) : kAbsent;
         }
     }
+    if (a.attn == SPC_ATTN_RAW) write_chunk<SPC_ATTN_RAW>(a, st, s, c, V, bits, lo, sm);
+    else write_chunk<SPC_ATTN_MAGNITUDE>(a, st, s, c, V, bits, lo, sm);   // NONE: keep_all
 }
 
 cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& kg, const FwdTile& t,
