@@ -158,8 +158,10 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
         // per (oc, halo x-row) the kept outputs of the halo y-range are one contiguous key run
         const int hylo = max(0, y0 - kg.hy), hyhi = min(gy.Y, y0 + t.TY + kg.hy);
         const float invZ = 1.0f / (float)gy.Z;
+        const float invHX = 1.0f / (float)HX;
         for (int r = warp; r < nocl * HX; r += nwarps) {
-            const int ocl = r / HX, hxr = r - ocl * HX;
+            int ocl = __float2int_rz(((float)r + 0.5f) * invHX);   // r / HX (small integers)
+            const int hxr = r - ocl * HX;
             const int xs = x0 - kg.hx + hxr;
             if (xs < 0 || xs >= gy.X || hylo >= hyhi) continue;
             const int64_t row = ((b * c_out + oc0 + ocl) * gy.X + xs) * (int64_t)gy.Y + hylo;
@@ -262,22 +264,13 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
             __syncwarp();
         }
         __syncthreads();
-        // restore G to zero where this item wrote gradients
-        for (int r = warp; r < nocl * HX; r += nwarps) {
-            const int ocl = r / HX, hxr = r - ocl * HX;
-            const int xs = x0 - kg.hx + hxr;
-            if (xs < 0 || xs >= gy.X || hylo >= hyhi) continue;
-            const int64_t row = ((b * c_out + oc0 + ocl) * gy.X + xs) * (int64_t)gy.Y + hylo;
-            const uint32_t e0 = yrow[row], e1 = yrow[row + (hyhi - hylo)];
-            const uint64_t rowbase = (uint64_t)row * (uint64_t)gy.Z;
-            const int gbase = (ocl * HXY + hxr * HY + (hylo - (y0 - kg.hy))) * ZR + kg.hz;
-            for (uint32_t e = e0 + lane; e < e1; e += 32) {
-                const uint32_t L = (uint32_t)(ykeys[e] - rowbase);
-                uint32_t yr = __float2uint_rz(__uint2float_rz(L) * invZ);
-                if (yr * (uint32_t)gy.Z > L) --yr;
-                if ((yr + 1) * (uint32_t)gy.Z <= L) ++yr;
-                G[gbase + (int)yr * ZR + (int)(L - yr * (uint32_t)gy.Z)] = 0.0f;
-            }
+        // zero G for the next item: one vectorized sweep of the slab (a few hundred warp
+        // instructions) instead of revisiting every scattered gradient
+        {
+            float4* G4 = reinterpret_cast<float4*>(G);
+            const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int i = threadIdx.x; i < (gsize >> 2); i += blockDim.x) G4[i] = z4;
+            for (int i = (gsize & ~3) + threadIdx.x; i < gsize; i += blockDim.x) G[i] = 0.0f;
         }
     }
     __syncthreads();

@@ -570,17 +570,18 @@ constexpr int kChunk = kChunkThreads * kChunkItems;   // voxels per chunk of a (
 template <int MODE>
 __device__ __forceinline__ void classify_chunk(const FwdArgs& a, const FwdSeg& st, int64_t s, int64_t c, int64_t V,
                                                const uint32_t (&bits)[kChunkItems], int64_t lo,
-                                               unsigned long long* sm) {
+                                               unsigned long long* sm, uint2* sbuf) {
     // digit of each value, -1 off the support: kept outright iff d > B1, candidate iff d == B1
     int d[kChunkItems];
     uint32_t def = 0, cand = 0;
 #pragma unroll
     for (int u = 0; u < kChunkItems; ++u) {
         const bool pres = bits[u] != kAbsent;
-        d[u] = pres ? (int)(score_bits(bits[u], MODE) >> 21) : -1;
-        if (st.keep_all) d[u] = pres ? (int)st.b1 + 1 : -1;   // keep-all: every support entry is "definite"
-        def += d[u] > (int)st.b1 ? 1u : 0u;
-        cand += d[u] == (int)st.b1 ? 1u : 0u;
+        // keep-all: every support entry is "definite" (digit forced above B1)
+        const int dig = st.keep_all ? (int)st.b1 + 1 : (int)(score_bits(bits[u], MODE) >> 21);
+        d[u] = pres ? dig : -1;
+        def += (uint32_t)(d[u] > (int)st.b1);
+        cand += (uint32_t)(d[u] == (int)st.b1);
     }
     // one scan of (definite << 32 | candidates) gives the tile total and each thread's slot
     unsigned long long tot;
@@ -591,17 +592,20 @@ __device__ __forceinline__ void classify_chunk(const FwdArgs& a, const FwdSeg& s
         a.tile_def[s * a.nchunk + c] = (uint32_t)(tot >> 32);
         sh_base = tcand ? a.cand_off[s] + atomicAdd(&a.cand_cur[s], (unsigned long long)tcand) : 0ull;
     }
-    __syncthreads();
-    if (tcand == 0 || cand == 0) return;
-    uint2* out = a.cand + sh_base + (uint32_t)ex;
-    uint32_t k = 0;
+    if (tcand == 0) return;   // block-uniform
+    // stage this thread's candidates at its scanned slots (predicated stores, no branches),
+    // then the block writes the chunk's candidates out coalesced
+    uint32_t k = (uint32_t)ex;
 #pragma unroll
     for (int u = 0; u < kChunkItems; ++u) {
-        if (d[u] == (int)st.b1) {
-            const uint32_t p = (uint32_t)(lo + 4 * ((int64_t)(u >> 2) * kChunkThreads + threadIdx.x) + (u & 3));
-            out[k++] = make_uint2(p, bits[u]);
-        }
+        const bool is_c = d[u] == (int)st.b1;
+        const uint32_t p = (uint32_t)(lo + 4 * ((int64_t)(u >> 2) * kChunkThreads + threadIdx.x) + (u & 3));
+        if (is_c) sbuf[k] = make_uint2(p, bits[u]);
+        k += is_c ? 1u : 0u;
     }
+    __syncthreads();
+    uint2* out = a.cand + sh_base;
+    for (uint32_t i = threadIdx.x; i < tcand; i += kChunkThreads) out[i] = sbuf[i];
 }
 
 __global__ void __launch_bounds__(kChunkThreads) fwd_classify_kernel(FwdArgs a, int64_t V) {
@@ -610,6 +614,7 @@ __global__ void __launch_bounds__(kChunkThreads) fwd_classify_kernel(FwdArgs a, 
     const int64_t lo = c * kChunk;
     const float* P = a.pre + s * V;
     __shared__ unsigned long long sm[33];
+    __shared__ uint2 sbuf[kChunk];   // the chunk's candidates, staged for a coalesced write
     // element u of this thread: lo + 4*(v*256 + tid) + w, u = 4v + w (float4 loads, coalesced)
     uint32_t bits[kChunkItems];
     const bool vec = (V & 3) == 0;
@@ -627,8 +632,8 @@ __global__ void __launch_bounds__(kChunkThreads) fwd_classify_kernel(FwdArgs a, 
             for (int w = 0; w < 4; ++w) bits[4 * v + w] = i + w < V ? __float_as_uint(P[i + w]) : kAbsent;
         }
     }
-    if (a.attn == SPC_ATTN_RAW) classify_chunk<SPC_ATTN_RAW>(a, st, s, c, V, bits, lo, sm);
-    else classify_chunk<SPC_ATTN_MAGNITUDE>(a, st, s, c, V, bits, lo, sm);   // NONE: keep_all
+    if (a.attn == SPC_ATTN_RAW) classify_chunk<SPC_ATTN_RAW>(a, st, s, c, V, bits, lo, sm, sbuf);
+    else classify_chunk<SPC_ATTN_MAGNITUDE>(a, st, s, c, V, bits, lo, sm, sbuf);   // NONE: keep_all
 }
 
 // resolve: the `need` largest composite keys among the candidates of a segment -> kstar; then
@@ -750,34 +755,47 @@ __global__ void fwd_chunk_scan_kernel(FwdArgs a, uint64_t* kept) {
 template <int MODE>
 __device__ __forceinline__ void write_chunk(const FwdArgs& a, const FwdSeg& st, int64_t s, int64_t c, int64_t V,
                                             const uint32_t (&bits)[kChunkItems], int64_t lo,
-                                            unsigned long long* sm) {
+                                            unsigned long long* sm, uint2* sbuf) {
+    // keep iff composite(score, p) = (score << 32 | ~p) >= kstar, as two 32-bit compares
+    const uint32_t ks = (uint32_t)(st.kstar >> 32), kp = (uint32_t)st.kstar;
     uint32_t keep = 0;
-    unsigned long long packed = 0;
 #pragma unroll
     for (int u = 0; u < kChunkItems; ++u) {
-        const uint32_t p = (uint32_t)(lo + 4 * ((int64_t)(u >> 2) * kChunkThreads + threadIdx.x) + (u & 3));
-        bool k = bits[u] != kAbsent;
-        if (!st.keep_all) k = k && composite(score_bits(bits[u], MODE), p) >= st.kstar;
-        keep |= (uint32_t)k << u;
+        const uint32_t p = (uint32_t)lo + 4u * ((uint32_t)(u >> 2) * kChunkThreads + threadIdx.x) + (uint32_t)(u & 3);
+        const uint32_t sc = score_bits(bits[u], MODE);
+        // bitwise (no short-circuit branches)
+        const uint32_t k = (uint32_t)(bits[u] != kAbsent) &
+                           ((uint32_t)(st.keep_all != 0) | (uint32_t)(sc > ks) | ((uint32_t)(sc == ks) & (uint32_t)(~p >= kp)));
+        keep |= k << u;
     }
+    unsigned long long packed = 0;
 #pragma unroll
     for (int v = 0; v < 4; ++v) packed |= (unsigned long long)__popc((keep >> (4 * v)) & 15u) << (16 * v);
     unsigned long long tot;
     const unsigned long long ex = block_excl_scan(packed, sm, &tot);
-    uint64_t pos = a.seg_off[s] + a.tile_off[s * a.nchunk + c];
+    // chunk-local slot of slab v, thread t: sum of the earlier slabs' totals + this thread's prefix
+    uint32_t slab0 = 0;
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-        uint64_t q = pos + ((ex >> (16 * v)) & 0xffffu);
+        uint32_t q = slab0 + (uint32_t)((ex >> (16 * v)) & 0xffffu);
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
             const int u = 4 * v + w;
-            if (keep & (1u << u)) {
-                a.out_keys[q] = (uint64_t)s * (uint64_t)V + (uint64_t)(lo + 4 * ((int64_t)v * kChunkThreads + threadIdx.x) + w);
-                a.out_vals[q] = __uint_as_float(bits[u]);
-                ++q;
-            }
+            const bool k = (keep >> u) & 1u;
+            const uint32_t p = (uint32_t)lo + 4u * ((uint32_t)v * kChunkThreads + threadIdx.x) + (uint32_t)w;
+            if (k) sbuf[q] = make_uint2(p, bits[u]);
+            q += k ? 1u : 0u;
         }
-        pos += (tot >> (16 * v)) & 0xffffu;
+        slab0 += (uint32_t)((tot >> (16 * v)) & 0xffffu);
+    }
+    __syncthreads();
+    // coalesced output of the chunk's kept entries (key order)
+    const uint64_t pos = a.seg_off[s] + a.tile_off[s * a.nchunk + c];
+    const uint64_t kb = (uint64_t)s * (uint64_t)V;
+    for (uint32_t i = threadIdx.x; i < slab0; i += kChunkThreads) {
+        const uint2 e = sbuf[i];
+        a.out_keys[pos + i] = kb + e.x;
+        a.out_vals[pos + i] = __uint_as_float(e.y);
     }
 }
 
@@ -789,6 +807,7 @@ __global__ void __launch_bounds__(kChunkThreads) fwd_write_kernel(FwdArgs a, int
     const int64_t lo = c * kChunk;
     const float* P = a.pre + s * V;
     __shared__ unsigned long long sm[33];
+    __shared__ uint2 sbuf[kChunk];   // the chunk's kept entries, staged for a coalesced write
     uint32_t bits[kChunkItems];
     const bool vec = (V & 3) == 0;
 #pragma unroll
@@ -805,8 +824,8 @@ __global__ void __launch_bounds__(kChunkThreads) fwd_write_kernel(FwdArgs a, int
             for (int w = 0; w < 4; ++w) bits[4 * v + w] = i + w < V ? __float_as_uint(P[i + w]) : kAbsent;
         }
     }
-    if (a.attn == SPC_ATTN_RAW) write_chunk<SPC_ATTN_RAW>(a, st, s, c, V, bits, lo, sm);
-    else write_chunk<SPC_ATTN_MAGNITUDE>(a, st, s, c, V, bits, lo, sm);   // NONE: keep_all
+    if (a.attn == SPC_ATTN_RAW) write_chunk<SPC_ATTN_RAW>(a, st, s, c, V, bits, lo, sm, sbuf);
+    else write_chunk<SPC_ATTN_MAGNITUDE>(a, st, s, c, V, bits, lo, sm, sbuf);   // NONE: keep_all
 }
 
 cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& kg, const FwdTile& t,
