@@ -172,6 +172,7 @@ FwdWs carve_fwd(Carver& c, const Geo& gx, const Geo& gy, const KGeo& kg, const F
     a.hist = c.take<uint32_t>((size_t)nseg * kSelBins);
     a.seg = c.take<FwdSeg>((size_t)nseg);
     a.nchunk = (gy.V + 4095) / 4096;
+    a.nseg = nseg;
     a.pre = c.take<float>((size_t)(nseg * gy.V));
     a.tile_def = c.take<uint32_t>((size_t)(nseg * a.nchunk));
     a.tile_sel = c.take<uint32_t>((size_t)(nseg * a.nchunk));
@@ -181,6 +182,12 @@ FwdWs carve_fwd(Carver& c, const Geo& gx, const Geo& gy, const KGeo& kg, const F
     a.cand_cur = c.take<unsigned long long>((size_t)nseg);
     a.cand = c.take<uint2>(attn == SPC_ATTN_NONE ? 1 : (size_t)(nseg * gy.V));
     a.seg_off = c.take<uint64_t>((size_t)nseg + 1);
+    a.stg = c.take<uint2>((size_t)(nseg * gy.V));
+    a.stg_cnt = c.take<uint64_t>((size_t)nseg + 1);
+    a.stg_off = c.take<uint64_t>((size_t)nseg + 1);
+    a.stg_cur = c.take<unsigned long long>((size_t)nseg);
+    a.chunk_stg = c.take<uint64_t>((size_t)(nseg * a.nchunk));
+    a.chunk_ge = c.take<uint32_t>((size_t)(nseg * a.nchunk));
     const size_t PK = (size_t)w->c_in * kg.kx;
     a.rec = c.take<int4>((size_t)t.n_ocg * t.nwg_max + 1);
     a.pkoff = c.take<int>((size_t)t.n_ocg * (PK + 1));

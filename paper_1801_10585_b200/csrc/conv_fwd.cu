@@ -514,6 +514,7 @@ __global__ void fwd_find_kernel(FwdArgs a, int64_t nseg) {
             st.kstar = 0;
             a.seg[s] = st;
             a.cand_cnt[s] = 0;
+            a.stg_cnt[s] = (uint64_t)n;
         }
         return;
     }
@@ -535,6 +536,7 @@ __global__ void fwd_find_kernel(FwdArgs a, int64_t nseg) {
                 st.kstar = 0;
                 a.seg[s] = st;
                 a.cand_cnt[s] = h[bin];
+                a.stg_cnt[s] = cum + h[bin];   // digits >= B1
                 break;
             }
             cum += h[bin];
@@ -571,41 +573,74 @@ template <int MODE>
 __device__ __forceinline__ void classify_chunk(const FwdArgs& a, const FwdSeg& st, int64_t s, int64_t c, int64_t V,
                                                const uint32_t (&bits)[kChunkItems], int64_t lo,
                                                unsigned long long* sm, uint2* sbuf) {
-    // digit of each value, -1 off the support: kept outright iff d > B1, candidate iff d == B1
-    int d[kChunkItems];
-    uint32_t def = 0, cand = 0;
+    // digit of each value, -1 off the support: kept outright iff d > B1, candidate iff d == B1;
+    // staged iff d >= B1 (the write pass then never touches the dense buffer again)
+    uint32_t ge = 0, cand = 0;
 #pragma unroll
     for (int u = 0; u < kChunkItems; ++u) {
         const bool pres = bits[u] != kAbsent;
         // keep-all: every support entry is "definite" (digit forced above B1)
         const int dig = st.keep_all ? (int)st.b1 + 1 : (int)(score_bits(bits[u], MODE) >> 21);
-        d[u] = pres ? dig : -1;
-        def += (uint32_t)(d[u] > (int)st.b1);
-        cand += (uint32_t)(d[u] == (int)st.b1);
+        const int d = pres ? dig : -1;
+        ge |= (uint32_t)(d >= (int)st.b1) << u;
+        cand += (uint32_t)(d == (int)st.b1);
     }
-    // one scan of (definite << 32 | candidates) gives the tile total and each thread's slot
-    unsigned long long tot;
-    const unsigned long long ex = block_excl_scan(((unsigned long long)def << 32) | cand, sm, &tot);
-    __shared__ uint64_t sh_base;
-    const uint32_t tcand = (uint32_t)tot;
-    if (threadIdx.x == 0) {
-        a.tile_def[s * a.nchunk + c] = (uint32_t)(tot >> 32);
-        sh_base = tcand ? a.cand_off[s] + atomicAdd(&a.cand_cur[s], (unsigned long long)tcand) : 0ull;
-    }
-    if (tcand == 0) return;   // block-uniform
-    // stage this thread's candidates at its scanned slots (predicated stores, no branches),
-    // then the block writes the chunk's candidates out coalesced
-    uint32_t k = (uint32_t)ex;
+    // one scan of 4 x 12-bit per-slab staged counts | 16-bit candidate count: key-ordered slots
+    unsigned long long packed = (unsigned long long)cand << 48;
 #pragma unroll
-    for (int u = 0; u < kChunkItems; ++u) {
-        const bool is_c = d[u] == (int)st.b1;
-        const uint32_t p = (uint32_t)(lo + 4 * ((int64_t)(u >> 2) * kChunkThreads + threadIdx.x) + (u & 3));
-        if (is_c) sbuf[k] = make_uint2(p, bits[u]);
-        k += is_c ? 1u : 0u;
+    for (int v = 0; v < 4; ++v) packed |= (unsigned long long)__popc((ge >> (4 * v)) & 15u) << (12 * v);
+    unsigned long long tot;
+    const unsigned long long ex = block_excl_scan(packed, sm, &tot);
+    uint32_t nge = 0;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) nge += (uint32_t)((tot >> (12 * v)) & 0xfffu);
+    const uint32_t tcand = (uint32_t)(tot >> 48);
+    __shared__ uint64_t sh_base, sh_cbase;
+    __shared__ uint32_t sh_ccur;
+    const int64_t it = s * a.nchunk + c;
+    if (threadIdx.x == 0) {
+        a.tile_def[it] = nge - tcand;
+        a.chunk_ge[it] = nge;
+        const uint64_t b0 = nge ? a.stg_off[s] + atomicAdd(&a.stg_cur[s], (unsigned long long)nge) : 0ull;
+        a.chunk_stg[it] = b0;
+        sh_base = b0;
+        sh_cbase = tcand ? a.cand_off[s] + atomicAdd(&a.cand_cur[s], (unsigned long long)tcand) : 0ull;
+        sh_ccur = 0;
+    }
+    if (nge == 0) return;   // block-uniform
+    // stage this thread's entries at their key-ordered slots (predicated shared stores)
+    uint32_t slab0 = 0;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+        uint32_t q = slab0 + (uint32_t)((ex >> (12 * v)) & 0xfffu);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const int u = 4 * v + w;
+            const bool k = (ge >> u) & 1u;
+            const uint32_t p = (uint32_t)lo + 4u * ((uint32_t)v * kChunkThreads + threadIdx.x) + (uint32_t)w;
+            if (k) sbuf[q] = make_uint2(p, bits[u]);
+            q += k ? 1u : 0u;
+        }
+        slab0 += (uint32_t)((tot >> (12 * v)) & 0xfffu);
     }
     __syncthreads();
-    uint2* out = a.cand + sh_base;
-    for (uint32_t i = threadIdx.x; i < tcand; i += kChunkThreads) out[i] = sbuf[i];
+    // coalesced copy to the staging list; candidates (digit == B1) also appended, any order
+    uint2* out = a.stg + sh_base;
+    const int lane = threadIdx.x & 31;
+    for (uint32_t i0 = threadIdx.x & ~31u; i0 < nge; i0 += kChunkThreads) {
+        const uint32_t i = i0 + lane;
+        const bool ok = i < nge;
+        const uint2 e = ok ? sbuf[i] : make_uint2(0u, kAbsent);
+        if (ok) out[i] = e;
+        const bool is_c = ok && !st.keep_all && (score_bits(e.y, MODE) >> 21) == st.b1;
+        const unsigned m = __ballot_sync(kFull, is_c);
+        if (m) {
+            uint32_t slot = 0;
+            if (lane == 0) slot = atomicAdd(&sh_ccur, (uint32_t)__popc(m));
+            slot = __shfl_sync(kFull, slot, 0);
+            if (is_c) a.cand[sh_cbase + slot + __popc(m & ((1u << lane) - 1u))] = e;
+        }
+    }
 }
 
 __global__ void __launch_bounds__(kChunkThreads) fwd_classify_kernel(FwdArgs a, int64_t V) {
@@ -752,80 +787,37 @@ __global__ void fwd_chunk_scan_kernel(FwdArgs a, uint64_t* kept) {
 // Elements are loaded as in classify (slab v = 0..3 of 256 float4, thread t holds voxels
 // lo + 4*(v*256 + t) + w): coalesced. Key order within the chunk is (v, t, w), so one scan of
 // four packed 16-bit per-slab counts gives every thread the output slot of each of its slabs.
-template <int MODE>
-__device__ __forceinline__ void write_chunk(const FwdArgs& a, const FwdSeg& st, int64_t s, int64_t c, int64_t V,
-                                            const uint32_t (&bits)[kChunkItems], int64_t lo,
-                                            unsigned long long* sm, uint2* sbuf) {
-    // keep iff composite(score, p) = (score << 32 | ~p) >= kstar, as two 32-bit compares
-    const uint32_t ks = (uint32_t)(st.kstar >> 32), kp = (uint32_t)st.kstar;
-    uint32_t keep = 0;
-#pragma unroll
-    for (int u = 0; u < kChunkItems; ++u) {
-        const uint32_t p = (uint32_t)lo + 4u * ((uint32_t)(u >> 2) * kChunkThreads + threadIdx.x) + (uint32_t)(u & 3);
-        const uint32_t sc = score_bits(bits[u], MODE);
-        // bitwise (no short-circuit branches)
-        const uint32_t k = (uint32_t)(bits[u] != kAbsent) &
-                           ((uint32_t)(st.keep_all != 0) | (uint32_t)(sc > ks) | ((uint32_t)(sc == ks) & (uint32_t)(~p >= kp)));
-        keep |= k << u;
-    }
-    unsigned long long packed = 0;
-#pragma unroll
-    for (int v = 0; v < 4; ++v) packed |= (unsigned long long)__popc((keep >> (4 * v)) & 15u) << (16 * v);
-    unsigned long long tot;
-    const unsigned long long ex = block_excl_scan(packed, sm, &tot);
-    // chunk-local slot of slab v, thread t: sum of the earlier slabs' totals + this thread's prefix
-    uint32_t slab0 = 0;
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-        uint32_t q = slab0 + (uint32_t)((ex >> (16 * v)) & 0xffffu);
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-            const int u = 4 * v + w;
-            const bool k = (keep >> u) & 1u;
-            const uint32_t p = (uint32_t)lo + 4u * ((uint32_t)v * kChunkThreads + threadIdx.x) + (uint32_t)w;
-            if (k) sbuf[q] = make_uint2(p, bits[u]);
-            q += k ? 1u : 0u;
-        }
-        slab0 += (uint32_t)((tot >> (16 * v)) & 0xffffu);
-    }
-    __syncthreads();
-    // coalesced output of the chunk's kept entries (key order)
-    const uint64_t pos = a.seg_off[s] + a.tile_off[s * a.nchunk + c];
-    const uint64_t kb = (uint64_t)s * (uint64_t)V;
-    for (uint32_t i = threadIdx.x; i < slab0; i += kChunkThreads) {
-        const uint2 e = sbuf[i];
-        a.out_keys[pos + i] = kb + e.x;
-        a.out_vals[pos + i] = __uint_as_float(e.y);
-    }
-}
-
-// write (HBM stream): keep iff composite(score, p) >= kstar (all support when keep-all);
-// ordered compaction in key order ("compress ids ... write k largest features").
-__global__ void __launch_bounds__(kChunkThreads) fwd_write_kernel(FwdArgs a, int64_t V) {
-    const int64_t s = blockIdx.x / a.nchunk, c = blockIdx.x % a.nchunk;
+// write: keep iff composite(score, p) >= kstar (every staged entry when keep-all); ordered
+// compaction in key order ("compress ids ... write k largest features"). One warp per
+// chunk over its staged run (entries with digit >= B1, already in key order).
+constexpr int kWriteWarps = 8;
+__global__ void __launch_bounds__(32 * kWriteWarps) fwd_write_kernel(FwdArgs a, int64_t V) {
+    const int lane = threadIdx.x & 31;
+    const int64_t it = (int64_t)blockIdx.x * kWriteWarps + (threadIdx.x >> 5);
+    if (it >= a.nseg * a.nchunk) return;
+    const int64_t s = it / a.nchunk;
     const FwdSeg st = a.seg[s];
-    const int64_t lo = c * kChunk;
-    const float* P = a.pre + s * V;
-    __shared__ unsigned long long sm[33];
-    __shared__ uint2 sbuf[kChunk];   // the chunk's kept entries, staged for a coalesced write
-    uint32_t bits[kChunkItems];
-    const bool vec = (V & 3) == 0;
-#pragma unroll
-    for (int v = 0; v < kChunkItems / 4; ++v) {
-        const int64_t i = lo + 4 * ((int64_t)v * kChunkThreads + threadIdx.x);
-        if (vec && i + 4 <= V) {
-            const float4 q = __ldcs(reinterpret_cast<const float4*>(P + i));
-            bits[4 * v] = __float_as_uint(q.x);
-            bits[4 * v + 1] = __float_as_uint(q.y);
-            bits[4 * v + 2] = __float_as_uint(q.z);
-            bits[4 * v + 3] = __float_as_uint(q.w);
-        } else {
-#pragma unroll
-            for (int w = 0; w < 4; ++w) bits[4 * v + w] = i + w < V ? __float_as_uint(P[i + w]) : kAbsent;
+    const uint32_t n = a.chunk_ge[it];
+    if (n == 0) return;
+    const uint2* in = a.stg + a.chunk_stg[it];
+    uint64_t out = a.seg_off[s] + a.tile_off[it];
+    const uint64_t kb = (uint64_t)s * (uint64_t)V;
+    // composite(score, p) = (score << 32 | ~p) >= kstar, as two 32-bit compares
+    const uint32_t ks = (uint32_t)(st.kstar >> 32), kp = (uint32_t)st.kstar;
+    for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        const bool ok = i < n;
+        const uint2 e = ok ? in[i] : make_uint2(0u, kAbsent);
+        const uint32_t sc = score_bits(e.y, a.attn);
+        const bool keep = ok && (st.keep_all || sc > ks || (sc == ks && ~e.x >= kp));
+        const unsigned m = __ballot_sync(kFull, keep);
+        if (keep) {
+            const uint64_t q = out + __popc(m & ((1u << lane) - 1u));
+            a.out_keys[q] = kb + e.x;
+            a.out_vals[q] = __uint_as_float(e.y);
         }
+        out += __popc(m);
     }
-    if (a.attn == SPC_ATTN_RAW) write_chunk<SPC_ATTN_RAW>(a, st, s, c, V, bits, lo, sm, sbuf);
-    else write_chunk<SPC_ATTN_MAGNITUDE>(a, st, s, c, V, bits, lo, sm, sbuf);   // NONE: keep_all
 }
 
 cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& kg, const FwdTile& t,
@@ -837,6 +829,7 @@ cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& k
     const size_t segb = sizeof(uint64_t) * (size_t)nseg;
     cudaMemsetAsync(a.seg_count, 0, segb, s);
     cudaMemsetAsync(a.cand_cur, 0, segb, s);
+    cudaMemsetAsync(a.stg_cur, 0, segb, s);
     cudaMemsetAsync(a.tile_sel, 0, sizeof(uint32_t) * (size_t)(nseg * a.nchunk), s);
     if (a.attn != SPC_ATTN_NONE) cudaMemsetAsync(a.hist, 0, sizeof(uint32_t) * kSelBins * (size_t)nseg, s);
     const dim3 grid((unsigned)(gy.B * gy.X * t.nty), (unsigned)t.n_ocg);
@@ -853,9 +846,10 @@ cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& k
     }
     { SPC_PHASE("conv_fwd", s, 1); conv_fwd_kernel<<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a); }
     { SPC_PHASE("fwd_find", s, 1); fwd_find_kernel<<<(unsigned)nseg, 256, 0, s>>>(a, nseg); }
-    if (a.attn != SPC_ATTN_NONE) {
-        SPC_PHASE("seg_scan", s, 1);
-        seg_scan_u64_kernel<<<1, 1024, 0, s>>>(a.cand_cnt, a.cand_off, nseg, nullptr);
+    {
+        SPC_PHASE("seg_scan", s, a.attn != SPC_ATTN_NONE ? 2 : 1);
+        if (a.attn != SPC_ATTN_NONE) seg_scan_u64_kernel<<<1, 1024, 0, s>>>(a.cand_cnt, a.cand_off, nseg, nullptr);
+        seg_scan_u64_kernel<<<1, 1024, 0, s>>>(a.stg_cnt, a.stg_off, nseg, nullptr);
     }
     { SPC_PHASE("fwd_classify", s, 1); fwd_classify_kernel<<<sgrid, kChunkThreads, 0, s>>>(a, gy.V); }
     if (a.attn != SPC_ATTN_NONE) {
@@ -865,7 +859,7 @@ cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& k
     // kept per segment goes to cand_cnt (reused as scratch), then segment offsets
     { SPC_PHASE("fwd_chunk_scan", s, 1); fwd_chunk_scan_kernel<<<(unsigned)nseg, 256, 0, s>>>(a, a.cand_cnt); }
     { SPC_PHASE("seg_scan", s, 1); seg_scan_u64_kernel<<<1, 1024, 0, s>>>(a.cand_cnt, a.seg_off, nseg, a.out_nnz); }
-    { SPC_PHASE("fwd_write", s, 1); fwd_write_kernel<<<sgrid, kChunkThreads, 0, s>>>(a, gy.V); }
+    { SPC_PHASE("fwd_write", s, 1); fwd_write_kernel<<<(unsigned)((nseg * a.nchunk + kWriteWarps - 1) / kWriteWarps), 32 * kWriteWarps, 0, s>>>(a, gy.V); }
     return cudaGetLastError();
 }
 

@@ -136,6 +136,7 @@ struct FwdArgs {
     int64_t k;
     float* pre;                      // [nseg * V] pre-attention responses (absent marker off support)
     int64_t nchunk;                  // chunks of 4096 voxels per (b, oc) buffer
+    int64_t nseg;                    // (b, oc) segments
     unsigned long long* seg_count;   // [nseg] support size
     uint32_t* hist;                  // [nseg * kSelBins]
     FwdSeg* seg;                     // [nseg]
@@ -146,6 +147,12 @@ struct FwdArgs {
     uint64_t* cand_cnt;              // [nseg] candidates per segment
     unsigned long long* cand_cur;    // [nseg] append cursors
     uint2* cand;                     // candidate list {p, value bits}
+    uint2* stg;                      // staged entries with digit >= B1 {p, value bits}, per chunk in key order
+    uint64_t* stg_cnt;               // [nseg] staged entries per segment (histogram count of digits >= B1)
+    uint64_t* stg_off;               // [nseg + 1] staging offsets
+    unsigned long long* stg_cur;     // [nseg] chunk placement cursors
+    uint64_t* chunk_stg;             // [nseg * nchunk] first staged entry of each chunk
+    uint32_t* chunk_ge;              // [nseg * nchunk] staged entries of each chunk
     uint64_t* seg_off;               // [nseg + 1] output offsets
     uint64_t* out_keys;
     float* out_vals;
