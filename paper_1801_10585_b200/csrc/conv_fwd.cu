@@ -198,6 +198,16 @@ __device__ __forceinline__ float absent_add(float a, float b, uint32_t marker) {
     return a + b;
 }
 
+// warp owning input row i (rows split as A_w = floor(w*nr/8)): floor((8i + 7) / nr), by a float
+// reciprocal and one correction each way (8i + 7 < 2^11)
+__device__ __forceinline__ int owner_of(int i, int nr, float inv_nr) {
+    const int num = 8 * i + 7;
+    int q = __float2int_rz((float)num * inv_nr);
+    if (q * nr > num) --q;
+    if ((q + 1) * nr <= num) ++q;
+    return q;
+}
+
 // Epilogue rows of one output channel: merge the warps' copies of each row (fixed warp order),
 // bias on the support, streaming store of the slice, support count and (with attention) the
 // score-digit histogram. Branch-free: lanes off the support increment a private dummy bin past
@@ -208,11 +218,12 @@ __device__ __forceinline__ void epi_rows(const float* S, float* P, float bv, int
                                          uint32_t marker) {
     const bool vec = (Z & 3) == 0;
     const uint32_t dummy = hist_s + (uint32_t)(kSelBins + lane) * 4u;
+    const float inv_nr = 1.0f / (float)nr;
     for (int r = warp; r < nyr; r += kFwdWarps) {
         // row yrel = r + yoff (relative to the first input row) has a copy in the region of every
         // warp owning an input row in [yrel - hy, yrel + hy], at region row yrel + hy*(2w + 1)
         const int yrel = r + yoff;
-        const int wlo = (8 * max(0, yrel - hy) + 7) / nr, whi = (8 * min(nr - 1, yrel + hy) + 7) / nr;
+        const int wlo = owner_of(max(0, yrel - hy), nr, inv_nr), whi = owner_of(min(nr - 1, yrel + hy), nr, inv_nr);
         for (int z0 = 4 * lane; z0 < Z; z0 += 128) {
             float v[4];
             {
@@ -290,57 +301,76 @@ __device__ __forceinline__ void fwd_items(const Geo& gx, const KGeo& kg, const F
                                           const char* accw) {
     const int c_in = (int)gx.C;
     const uint32_t accs = (uint32_t)__cvta_generic_to_shared(accw);
-    for (int pk = ic0 * kg.kx; pk < ic1 * kg.kx; ++pk) {
-        const uint32_t* RP = rp + pk * NRP;
-        const uint32_t e0 = RP[A_w], e1 = RP[B_w];
-        if (e0 == e1) continue;
-        const int rb = pko[pk], re = pko[pk + 1], rf = rb + pkf[pk];
-        if (rb == re) continue;
-        const int n = (int)(e1 - e0);
-        const int s0 = staged ? sbase[pk] - sb0 + (int)(e0 - RP[0]) : 0;
-        uint64_t rowbase = 0;
-        if (!staged) {
-            const int ic = pk / kg.kx, xs = x + (pk - ic * kg.kx) - kg.hx;
-            rowbase = (uint64_t)(((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo) * (uint64_t)Z;
+    // lane j gathers the metadata of work item ic0*kx + pg + j in parallel; the warp then walks
+    // the non-empty items via ballot + shuffles (no serial chain of shared loads per item)
+    const int pk0 = ic0 * kg.kx, npk = (ic1 - ic0) * kg.kx;
+    for (int pg = 0; pg < npk; pg += 32) {
+        int m_n = 0, m_rb = 0, m_re = 0, m_rf = 0, m_s0 = 0;
+        uint32_t m_e0 = 0;
+        if (pg + lane < npk) {
+            const int pk = pk0 + pg + lane;
+            const uint32_t* RP = rp + pk * NRP;
+            m_e0 = RP[A_w];
+            m_n = (int)(RP[B_w] - m_e0);
+            m_rb = pko[pk];
+            m_re = pko[pk + 1];
+            m_rf = m_rb + pkf[pk];
+            if (m_rb == m_re) m_n = 0;
+            m_s0 = staged ? sbase[pk] - sb0 + (int)(m_e0 - RP[0]) : 0;
         }
+        unsigned todo = __ballot_sync(kFull, m_n > 0);
+        while (todo) {
+            const int jl = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int pk = pk0 + pg + jl;
+            const int n = __shfl_sync(kFull, m_n, jl);
+            const int rb = __shfl_sync(kFull, m_rb, jl), re = __shfl_sync(kFull, m_re, jl);
+            const int rf = __shfl_sync(kFull, m_rf, jl), s0 = __shfl_sync(kFull, m_s0, jl);
+            const uint32_t e0 = __shfl_sync(kFull, m_e0, jl);
+            uint64_t rowbase = 0;
+            if (!staged) {
+                const int ic = pk / kg.kx, xs = x + (pk - ic * kg.kx) - kg.hx;
+                rowbase = (uint64_t)(((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo) * (uint64_t)Z;
+            }
 #pragma unroll 1
-        for (int c = 0; c < n; c += 32) {
-            const bool valid = c + lane < n;
-            int pos = 0;   // idle lanes: position 0 of the warp's region (reads stay in range)
-            float v = 0.0f;
-            if (valid) {
-                if (staged) {
-                    const uint2 en = stage[s0 + c + lane];
-                    pos = (int)(en.x & 0xffffffu);
-                    v = __uint_as_float(en.y);
-                } else {
-                    const uint32_t L = (uint32_t)(a.xkeys[e0 + c + lane] - rowbase);
-                    const uint32_t yrel = div_small(L, (uint32_t)Z, invZ);
-                    pos = (int)(yrel * (uint32_t)ZR + (L - yrel * (uint32_t)Z));
-                    v = a.xvals[e0 + c + lane];
+            for (int c = 0; c < n; c += 32) {
+                const bool valid = c + lane < n;
+                int pos = 0;   // idle lanes: position 0 of the warp's region (reads stay in range)
+                float v = 0.0f;
+                if (valid) {
+                    if (staged) {
+                        const uint2 en = stage[s0 + c + lane];
+                        pos = (int)(en.x & 0xffffffu);
+                        v = __uint_as_float(en.y);
+                    } else {
+                        const uint32_t L = (uint32_t)(a.xkeys[e0 + c + lane] - rowbase);
+                        const uint32_t yrel = div_small(L, (uint32_t)Z, invZ);
+                        pos = (int)(yrel * (uint32_t)ZR + (L - yrel * (uint32_t)Z));
+                        v = a.xvals[e0 + c + lane];
+                    }
                 }
-            }
-            const uint32_t base = accs + (uint32_t)pos * 4u;
-            // two-channel rounds: both read-modify-writes in flight (distinct slices); predicated
-            // shared loads/stores (no branch), the next round's record prefetched
-            int4 q = rec[rb];
+                const uint32_t base = accs + (uint32_t)pos * 4u;
+                // two-channel rounds: both read-modify-writes in flight (distinct slices); predicated
+                // shared loads/stores (no branch), the next round's record prefetched
+                int4 q = rec[rb];
 #pragma unroll 2
-            for (int r = rb; r < rf; ++r) {
-                const int4 qn = rec[r + 1];   // rec[re] stays inside shared memory (pko follows)
-                const uint32_t pa = base + (uint32_t)q.x, pb = base + (uint32_t)q.z;
-                const float oa = lds_u(pa), ob = lds_u(pb);
-                sts_p(pa, upd<NEG0>(oa, v, __int_as_float(q.y)), valid);
-                sts_p(pb, upd<NEG0>(ob, v, __int_as_float(q.w)), valid);
-                __syncwarp();   // the next round's lanes may read what this one wrote
-                q = qn;
-            }
+                for (int r = rb; r < rf; ++r) {
+                    const int4 qn = rec[r + 1];   // rec[re] stays inside shared memory (pko follows)
+                    const uint32_t pa = base + (uint32_t)q.x, pb = base + (uint32_t)q.z;
+                    const float oa = lds_u(pa), ob = lds_u(pb);
+                    sts_p(pa, upd<NEG0>(oa, v, __int_as_float(q.y)), valid);
+                    sts_p(pb, upd<NEG0>(ob, v, __int_as_float(q.w)), valid);
+                    __syncwarp();   // the next round's lanes may read what this one wrote
+                    q = qn;
+                }
 #pragma unroll 1
-            for (int r = rf; r < re; ++r) {
-                const int4 qn = rec[r + 1];   // rec[re] stays inside shared memory (pko follows)
-                const uint32_t pa = base + (uint32_t)q.x;
-                sts_p(pa, upd<NEG0>(lds_u(pa), v, __int_as_float(q.y)), valid);
-                q = qn;
-                __syncwarp();
+                for (int r = rf; r < re; ++r) {
+                    const int4 qn = rec[r + 1];   // rec[re] stays inside shared memory (pko follows)
+                    const uint32_t pa = base + (uint32_t)q.x;
+                    sts_p(pa, upd<NEG0>(lds_u(pa), v, __int_as_float(q.y)), valid);
+                    q = qn;
+                    __syncwarp();
+                }
             }
         }
     }
