@@ -36,16 +36,17 @@ namespace spc {
 constexpr int kFwdThreads = 256;
 constexpr int kFwdWarps = kFwdThreads / 32;
 constexpr size_t kFwdBudget = 113 * 1024;   // two CTAs (16 warps) per SM
-constexpr int kStageCap = 1088;             // staged input entries per chunk of input channels
-static_assert(2 * kStageCap >= kSelBins + 32, "the epilogue histogram (+ 32 dummy bins) reuses the stage buffer");
+constexpr int kRing = 4;                    // per-warp cp.async ring: jobs in flight
+constexpr int kRingSlotB = 32 * 12;         // one job: 32 keys (8 B) + 32 values (4 B)
+constexpr int kRingWords = kFwdWarps * kRing * kRingSlotB / 4;
+static_assert(kRingWords >= kSelBins + 32, "the epilogue histogram (+ 32 dummy bins) reuses the ring");
 
 static size_t r4(size_t n) { return (n + 3) & ~(size_t)3; }
 
 // shared-memory bytes beyond the accumulator
 static size_t fwd_fixed_smem(const KGeo& kg, int c_in, int TY, int64_t nwg) {
     const size_t PK = (size_t)c_in * kg.kx;
-    return 4 * (256 + 4 * (size_t)nwg + 2 * r4(PK + 1) + r4(PK * (TY + 2 * kg.hy + 1)) + r4(PK + 1) +
-                2 * (size_t)kStageCap) + 64;
+    return 4 * (512 + 4 * (size_t)nwg + 2 * r4(PK + 1) + r4(PK * (TY + 2 * kg.hy + 1)) + (size_t)kRingWords) + 64;
 }
 
 FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_t nw_total) {
@@ -65,7 +66,7 @@ FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_
     while (TY > 1 && need(ocg, TY) > kFwdBudget) --TY;          // ocg == 1: shorter tiles
     if (need(ocg, TY) > kFwdBudget) { t.smem = 0; return t; }
     while (TY < gy.Y && need(ocg, TY + kFwdWarps) <= kFwdBudget) TY += kFwdWarps;   // spare room
-    TY = std::min(TY, std::min(gy.Y, 240));   // staged rows are packed in 8 bits (TY + 2*hy < 256)
+    TY = std::min(TY, std::min(gy.Y, 240));   // staged rows are packed in 8 bits (TY + 2*hy < 256); TY <= 448 (row owners)
     t.TY = TY;
     t.RW = (TY + kFwdWarps - 1) / kFwdWarps;
     t.RT = rows(TY);
@@ -214,16 +215,16 @@ __device__ __forceinline__ int owner_of(int i, int nr, float inv_nr) {
 // the histogram instead of branching around the atomic.
 template <int MODE>
 __device__ __forceinline__ void epi_rows(const float* S, float* P, float bv, int nyr, int Z, int ZR, int warp,
-                                         int lane, uint32_t hist_s, uint32_t& cnt, int yoff, int nr, int hy,
-                                         uint32_t marker) {
+                                         int lane, uint32_t hist_s, uint32_t& cnt, int yoff, int hy,
+                                         uint32_t marker, const uint32_t* rowsrc) {
     const bool vec = (Z & 3) == 0;
     const uint32_t dummy = hist_s + (uint32_t)(kSelBins + lane) * 4u;
-    const float inv_nr = 1.0f / (float)nr;
     for (int r = warp; r < nyr; r += kFwdWarps) {
         // row yrel = r + yoff (relative to the first input row) has a copy in the region of every
         // warp owning an input row in [yrel - hy, yrel + hy], at region row yrel + hy*(2w + 1)
         const int yrel = r + yoff;
-        const int wlo = owner_of(max(0, yrel - hy), nr, inv_nr), whi = owner_of(min(nr - 1, yrel + hy), nr, inv_nr);
+        const uint32_t ow = rowsrc[r];   // source warps of this row (owner table of the tile)
+        const int wlo = (int)(ow & 0xffu), whi = (int)(ow >> 8);
         for (int z0 = 4 * lane; z0 < Z; z0 += 128) {
             float v[4];
             {
@@ -291,24 +292,49 @@ __device__ __forceinline__ float upd(float old, float v, float w) {
     return fmaf(v, w, __float_as_uint(old) == kAbsent ? 0.0f : old);
 }
 
-// The accumulate loop of one staged chunk of input channels for one warp: every (ic, input
-// plane) run of the warp's input rows, 32 inputs per step (lanes), against the weight rounds.
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+
+// Work-item cursor of a warp: the non-empty (ic, input plane) items of a group of 32 (metadata in
+// lanes, jl = owning lane), each split into jobs of up to 32 stored inputs (chunk c).
+struct JobCur {
+    unsigned todo;
+    int jl, c, n;
+};
+__device__ __forceinline__ void job_next(JobCur& j, int m_n) {
+    if (j.jl >= 0 && j.c + 32 < j.n) { j.c += 32; return; }
+    if (!j.todo) { j.jl = -1; return; }
+    j.jl = __ffs(j.todo) - 1;
+    j.todo &= j.todo - 1;
+    j.c = 0;
+    j.n = __shfl_sync(kFull, m_n, j.jl);
+}
+
+// The accumulate loop of one warp: its input rows of every (ic, input plane) item against the
+// item's weight rounds. Inputs stream straight from global memory into a private shared ring
+// with cp.async, kRing - 1 jobs ahead of the one being processed (no block-wide staging).
 template <bool NEG0>
-__device__ __forceinline__ void fwd_items(const Geo& gx, const KGeo& kg, const FwdArgs& a, int64_t b, int x, int ic0,
-                                          int ic1, bool staged, int sb0, int A_w, int B_w, int NRP, int ylo, int Z,
-                                          int ZR, float invZ, int lane, const uint32_t* rp, const int* pko,
-                                          const int* pkf, const int4* rec, const int* sbase, const uint2* stage,
-                                          const char* accw) {
+__device__ __forceinline__ void fwd_items(const Geo& gx, const KGeo& kg, const FwdArgs& a, int64_t b, int x,
+                                          int A_w, int B_w, int NRP, int ylo, int Z, int ZR, float invZ,
+                                          int lane, const uint32_t* rp, const int* pko, const int* pkf,
+                                          const int4* rec, unsigned char* ring, const char* accw) {
     const int c_in = (int)gx.C;
+    const int PK = c_in * kg.kx;
     const uint32_t accs = (uint32_t)__cvta_generic_to_shared(accw);
-    // lane j gathers the metadata of work item ic0*kx + pg + j in parallel; the warp then walks
-    // the non-empty items via ballot + shuffles (no serial chain of shared loads per item)
-    const int pk0 = ic0 * kg.kx, npk = (ic1 - ic0) * kg.kx;
-    for (int pg = 0; pg < npk; pg += 32) {
-        int m_n = 0, m_rb = 0, m_re = 0, m_rf = 0, m_s0 = 0;
+    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+    for (int pg = 0; pg < PK; pg += 32) {
+        // lane j gathers the metadata of item pg + j
+        int m_n = 0, m_rb = 0, m_re = 0, m_rf = 0;
         uint32_t m_e0 = 0;
-        if (pg + lane < npk) {
-            const int pk = pk0 + pg + lane;
+        if (pg + lane < PK) {
+            const int pk = pg + lane;
             const uint32_t* RP = rp + pk * NRP;
             m_e0 = RP[A_w];
             m_n = (int)(RP[B_w] - m_e0);
@@ -316,63 +342,79 @@ __device__ __forceinline__ void fwd_items(const Geo& gx, const KGeo& kg, const F
             m_re = pko[pk + 1];
             m_rf = m_rb + pkf[pk];
             if (m_rb == m_re) m_n = 0;
-            m_s0 = staged ? sbase[pk] - sb0 + (int)(m_e0 - RP[0]) : 0;
         }
-        unsigned todo = __ballot_sync(kFull, m_n > 0);
-        while (todo) {
-            const int jl = __ffs(todo) - 1;
-            todo &= todo - 1;
-            const int pk = pk0 + pg + jl;
-            const int n = __shfl_sync(kFull, m_n, jl);
-            const int rb = __shfl_sync(kFull, m_rb, jl), re = __shfl_sync(kFull, m_re, jl);
-            const int rf = __shfl_sync(kFull, m_rf, jl), s0 = __shfl_sync(kFull, m_s0, jl);
-            const uint32_t e0 = __shfl_sync(kFull, m_e0, jl);
-            uint64_t rowbase = 0;
-            if (!staged) {
+        const unsigned todo = __ballot_sync(kFull, m_n > 0);
+        JobCur iss{todo, -1, 0, 0}, pro{todo, -1, 0, 0};
+        // prologue: kRing - 1 jobs in flight
+#pragma unroll
+        for (int k = 0; k < kRing - 1; ++k) {
+            job_next(iss, m_n);
+            if (iss.jl >= 0) {
+                const uint32_t e = __shfl_sync(kFull, m_e0, iss.jl) + (uint32_t)iss.c;
+                if (iss.c + lane < iss.n) {
+                    const uint32_t slot = ring_s + (uint32_t)(k * kRingSlotB);
+                    cp_async8(slot + lane * 8u, a.xkeys + e + lane);
+                    cp_async4(slot + 256u + lane * 4u, a.xvals + e + lane);
+                }
+            }
+            cp_async_commit();
+        }
+        for (int k = 0;; ++k) {
+            job_next(pro, m_n);
+            if (pro.jl < 0) break;
+            // issue job k + kRing - 1 into the slot freed by job k - 1
+            job_next(iss, m_n);
+            if (iss.jl >= 0) {
+                const uint32_t e = __shfl_sync(kFull, m_e0, iss.jl) + (uint32_t)iss.c;
+                if (iss.c + lane < iss.n) {
+                    const uint32_t slot = ring_s + (uint32_t)(((k + kRing - 1) % kRing) * kRingSlotB);
+                    cp_async8(slot + lane * 8u, a.xkeys + e + lane);
+                    cp_async4(slot + 256u + lane * 4u, a.xvals + e + lane);
+                }
+            }
+            cp_async_commit();
+            cp_async_wait<kRing - 1>();   // job k has landed (this lane's copies)
+            const int pk = pg + pro.jl;
+            const int rb = __shfl_sync(kFull, m_rb, pro.jl), re = __shfl_sync(kFull, m_re, pro.jl);
+            const int rf = __shfl_sync(kFull, m_rf, pro.jl);
+            const bool valid = pro.c + lane < pro.n;
+            int pos = 0;   // idle lanes: position 0 of the warp's region (reads stay in range)
+            float v = 0.0f;
+            if (valid) {
+                const unsigned char* slot = ring + (k % kRing) * kRingSlotB;
+                const uint64_t key = reinterpret_cast<const uint64_t*>(slot)[lane];
+                v = reinterpret_cast<const float*>(slot + 256)[lane];
                 const int ic = pk / kg.kx, xs = x + (pk - ic * kg.kx) - kg.hx;
-                rowbase = (uint64_t)(((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo) * (uint64_t)Z;
+                const uint64_t rowbase = (uint64_t)(((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo) * (uint64_t)Z;
+                const uint32_t L = (uint32_t)(key - rowbase);
+                const uint32_t yrel = div_small(L, (uint32_t)Z, invZ);
+                pos = (int)(yrel * (uint32_t)ZR + (L - yrel * (uint32_t)Z));
+            }
+            const uint32_t base = accs + (uint32_t)pos * 4u;
+            // two-channel rounds: both read-modify-writes in flight (distinct slices); predicated
+            // shared loads/stores (no branch), the next round's record prefetched
+            int4 q = rec[rb];
+#pragma unroll 2
+            for (int r = rb; r < rf; ++r) {
+                const int4 qn = rec[r + 1];   // rec[re] stays inside shared memory (pko follows)
+                const uint32_t pa = base + (uint32_t)q.x, pb = base + (uint32_t)q.z;
+                const float oa = lds_u(pa), ob = lds_u(pb);
+                sts_p(pa, upd<NEG0>(oa, v, __int_as_float(q.y)), valid);
+                sts_p(pb, upd<NEG0>(ob, v, __int_as_float(q.w)), valid);
+                __syncwarp();   // the next round's lanes may read what this one wrote
+                q = qn;
             }
 #pragma unroll 1
-            for (int c = 0; c < n; c += 32) {
-                const bool valid = c + lane < n;
-                int pos = 0;   // idle lanes: position 0 of the warp's region (reads stay in range)
-                float v = 0.0f;
-                if (valid) {
-                    if (staged) {
-                        const uint2 en = stage[s0 + c + lane];
-                        pos = (int)(en.x & 0xffffffu);
-                        v = __uint_as_float(en.y);
-                    } else {
-                        const uint32_t L = (uint32_t)(a.xkeys[e0 + c + lane] - rowbase);
-                        const uint32_t yrel = div_small(L, (uint32_t)Z, invZ);
-                        pos = (int)(yrel * (uint32_t)ZR + (L - yrel * (uint32_t)Z));
-                        v = a.xvals[e0 + c + lane];
-                    }
-                }
-                const uint32_t base = accs + (uint32_t)pos * 4u;
-                // two-channel rounds: both read-modify-writes in flight (distinct slices); predicated
-                // shared loads/stores (no branch), the next round's record prefetched
-                int4 q = rec[rb];
-#pragma unroll 2
-                for (int r = rb; r < rf; ++r) {
-                    const int4 qn = rec[r + 1];   // rec[re] stays inside shared memory (pko follows)
-                    const uint32_t pa = base + (uint32_t)q.x, pb = base + (uint32_t)q.z;
-                    const float oa = lds_u(pa), ob = lds_u(pb);
-                    sts_p(pa, upd<NEG0>(oa, v, __int_as_float(q.y)), valid);
-                    sts_p(pb, upd<NEG0>(ob, v, __int_as_float(q.w)), valid);
-                    __syncwarp();   // the next round's lanes may read what this one wrote
-                    q = qn;
-                }
-#pragma unroll 1
-                for (int r = rf; r < re; ++r) {
-                    const int4 qn = rec[r + 1];   // rec[re] stays inside shared memory (pko follows)
-                    const uint32_t pa = base + (uint32_t)q.x;
-                    sts_p(pa, upd<NEG0>(lds_u(pa), v, __int_as_float(q.y)), valid);
-                    q = qn;
-                    __syncwarp();
-                }
+            for (int r = rf; r < re; ++r) {
+                const int4 qn = rec[r + 1];
+                const uint32_t pa = base + (uint32_t)q.x;
+                sts_p(pa, upd<NEG0>(lds_u(pa), v, __int_as_float(q.y)), valid);
+                q = qn;
+                __syncwarp();
             }
         }
+        cp_async_wait<0>();
+        __syncwarp();
     }
 }
 
@@ -392,20 +434,19 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     const int SL = t.RT * ZR;                        // floats per output-channel slice
 
     // shared layout (float offsets, 16-byte aligned pieces):
-    // [pad][acc ocg*RT*ZR][pad] | misc(256) | rounds | pko | pkf | rp | sbase | stage (= hist in the epilogue)
+    // [pad][acc ocg*RT*ZR][pad] | misc(512) | rounds | pko | pkf | rp | cp.async rings (= hist in the epilogue)
     const int PK = c_in * kg.kx;                     // (ic, input plane) work items
     const int ylo = max(0, y0 - kg.hy), yhi = min(gy.Y, ye + kg.hy);
     const int nr = yhi - ylo;                        // input rows read per plane
     const int NRP = nr + 1;
     float* acc = smf + t.pad;
     uint32_t* misc = reinterpret_cast<uint32_t*>(smf + 2 * t.pad + t.ocg * SL);
-    int4* rec = reinterpret_cast<int4*>(misc + 256);
+    int4* rec = reinterpret_cast<int4*>(misc + 512);   // misc: scan scratch [0, 64), row owners [64, 64 + TY)
     int* pko = reinterpret_cast<int*>(rec + t.nwg_max);
     int* pkf = pko + ((PK + 1 + 3) & ~3);
     uint32_t* rp = reinterpret_cast<uint32_t*>(pkf + ((PK + 1 + 3) & ~3));
-    int* sbase = reinterpret_cast<int*>(rp + ((PK * (t.TY + 2 * kg.hy + 1) + 3) & ~3));
-    uint2* stage = reinterpret_cast<uint2*>(sbase + ((PK + 1 + 3) & ~3));
-    uint32_t* hist = reinterpret_cast<uint32_t*>(stage);   // epilogue only
+    unsigned char* ring = reinterpret_cast<unsigned char*>(rp + ((PK * (t.TY + 2 * kg.hy + 1) + 3) & ~3));
+    uint32_t* hist = reinterpret_cast<uint32_t*>(ring);   // epilogue only
 
     const bool neg0 = *a.guard == 0;                 // -0 accumulation mode (value_guard_kernel)
     const uint32_t marker = neg0 ? kNegZero : kAbsent;
@@ -418,7 +459,6 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     for (int i = threadIdx.x; i <= PK; i += blockDim.x) pko[i] = gpko[i];
     for (int i = threadIdx.x; i < PK; i += blockDim.x) pkf[i] = a.pkfull[(int64_t)blockIdx.y * PK + i];
 
-    // ------------------------------------------------------------ accumulate (Alg. 1 inner loops)
     // Warp w owns input rows [A_w, B_w) (relative to ylo) and writes into a private region of the
     // accumulator: input row yrel lands at region row yrel + hy*(2w + 1), so targets (rows
     // yrel - oy, |oy| <= hy) of different warps never meet; the epilogue merges the copies.
@@ -432,64 +472,22 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
         const int xs = x + pl - kg.hx;
         rp[q] = (xs >= 0 && xs < gx.X) ? a.xrow[((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo + r] : 0u;
     }
-    __syncthreads();
     {   // this group's weight rounds (fwd_rounds_kernel), one coalesced copy
         const int4* grec = a.rec + (int64_t)blockIdx.y * t.nwg_max;
-        const int nrec = pko[PK];
+        const int nrec = gpko[PK];
         for (int i = threadIdx.x; i < nrec; i += blockDim.x) rec[i] = grec[i];
     }
-    {   // stage offsets of every (ic, plane) run
-        int carry = 0;
-        for (int p0 = 0; p0 < PK; p0 += blockDim.x) {
-            const int pk = p0 + threadIdx.x;
-            const int cnt = pk < PK ? (int)(rp[pk * NRP + nr] - rp[pk * NRP]) : 0;
-            int tot;
-            const int ex = block_excl_scan(cnt, reinterpret_cast<int*>(misc), &tot);
-            if (pk < PK) sbase[pk] = carry + ex;
-            carry += tot;
-        }
-        if (threadIdx.x == 0) sbase[PK] = carry;
-        __syncthreads();
+    __syncthreads();   // row pointers, tables and rounds in shared memory
+    // ------------------------------------------------------------ accumulate (Alg. 1 inner loops)
+    if (A_w < B_w) {
+        const char* accw = reinterpret_cast<const char*>(acc + cw);
+        unsigned char* ring_w = ring + warp * (kRing * kRingSlotB);
+        if (neg0)
+            fwd_items<true>(gx, kg, a, b, x, A_w, B_w, NRP, ylo, Z, ZR, invZ, lane, rp, pko, pkf, rec, ring_w, accw);
+        else
+            fwd_items<false>(gx, kg, a, b, x, A_w, B_w, NRP, ylo, Z, ZR, invZ, lane, rp, pko, pkf, rec, ring_w, accw);
     }
-    const char* accw = reinterpret_cast<const char*>(acc + cw);
-    // chunks of input channels whose stored inputs fit the stage (one coalesced burst each)
-    for (int ic0 = 0; ic0 < c_in;) {
-        int ic1 = ic0 + 1;
-        while (ic1 < c_in && sbase[(ic1 + 1) * kg.kx] - sbase[ic0 * kg.kx] <= kStageCap) ++ic1;
-        const int sb0 = sbase[ic0 * kg.kx];
-        const int nst = sbase[ic1 * kg.kx] - sb0;
-        const bool staged = nst <= kStageCap;        // false only for one over-full channel
-        if (staged) {
-            // one warp per (ic, plane) run: coalesced loads, no per-entry search
-            for (int pk = ic0 * kg.kx + warp; pk < ic1 * kg.kx; pk += kFwdWarps) {
-                const int ic = pk / kg.kx, xs = x + (pk - ic * kg.kx) - kg.hx;
-                const uint32_t g0 = rp[pk * NRP];
-                const int n = sbase[pk + 1] - sbase[pk];
-                uint2* dst = stage + (sbase[pk] - sb0);
-                const uint64_t rowbase = (uint64_t)(((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo) * (uint64_t)Z;
-#pragma unroll 4
-                for (int i = lane; i < n; i += 32) {
-                    const uint32_t L = (uint32_t)(a.xkeys[g0 + i] - rowbase);
-                    const uint32_t yrel = div_small(L, (uint32_t)Z, invZ);
-                    // {row (8 bits) | offset in the stage window (24 bits), value}
-                    dst[i] = make_uint2((yrel << 24) | (yrel * (uint32_t)ZR + (L - yrel * (uint32_t)Z)),
-                                        __float_as_uint(a.xvals[g0 + i]));
-                }
-            }
-        }
-        __syncthreads();
-        // work items (ic, input plane): this warp's input rows against all weight rounds of (ic, dx)
-        if (A_w < B_w) {
-            if (neg0)
-                fwd_items<true>(gx, kg, a, b, x, ic0, ic1, staged, sb0, A_w, B_w, NRP, ylo, Z, ZR, invZ, lane, rp, pko,
-                                pkf, rec, sbase, stage, accw);
-            else
-                fwd_items<false>(gx, kg, a, b, x, ic0, ic1, staged, sb0, A_w, B_w, NRP, ylo, Z, ZR, invZ, lane, rp, pko,
-                                 pkf, rec, sbase, stage, accw);
-        }
-        __syncthreads();                                 // stage consumed
-        ic0 = ic1;
-    }
+    __syncthreads();   // accumulator complete; rings free for the histogram
 
     // ------------------------------------------------------------------------ epilogue
     // "get non-zero entries" and "add bias to non-zero entries": the tile's slice
@@ -498,6 +496,16 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     // histogram of the top score digit are accumulated for the attention threshold.
     const int nyr = ye - y0;
     const bool do_hist = a.attn != SPC_ATTN_NONE;
+    // output row r has copies in the regions of the warps owning input rows yrel-hy..yrel+hy
+    uint32_t* rowsrc = misc + 64;
+    {
+        const float inv_nr = 1.0f / (float)nr;
+        for (int r = threadIdx.x; r < nyr; r += blockDim.x) {
+            const int yrel = r + (y0 - ylo);
+            const int wlo = owner_of(max(0, yrel - kg.hy), nr, inv_nr), whi = owner_of(min(nr - 1, yrel + kg.hy), nr, inv_nr);
+            rowsrc[r] = (uint32_t)wlo | ((uint32_t)whi << 8);
+        }
+    }
     const uint32_t hist_s = (uint32_t)__cvta_generic_to_shared(hist);
     for (int ocl = 0; ocl < nocl; ++ocl) {
         const int oc = oc0 + ocl;
@@ -511,11 +519,11 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
         float* P = a.pre + s * gy.V + ((int64_t)x * gy.Y + y0) * Z;
         const int yoff = y0 - ylo;
         if (a.attn == SPC_ATTN_MAGNITUDE)
-            epi_rows<SPC_ATTN_MAGNITUDE>(S, P, bv, nyr, Z, ZR, warp, lane, hist_s, cnt, yoff, nr, kg.hy, marker);
+            epi_rows<SPC_ATTN_MAGNITUDE>(S, P, bv, nyr, Z, ZR, warp, lane, hist_s, cnt, yoff, kg.hy, marker, rowsrc);
         else if (a.attn == SPC_ATTN_RAW)
-            epi_rows<SPC_ATTN_RAW>(S, P, bv, nyr, Z, ZR, warp, lane, hist_s, cnt, yoff, nr, kg.hy, marker);
+            epi_rows<SPC_ATTN_RAW>(S, P, bv, nyr, Z, ZR, warp, lane, hist_s, cnt, yoff, kg.hy, marker, rowsrc);
         else
-            epi_rows<SPC_ATTN_NONE>(S, P, bv, nyr, Z, ZR, warp, lane, hist_s, cnt, yoff, nr, kg.hy, marker);
+            epi_rows<SPC_ATTN_NONE>(S, P, bv, nyr, Z, ZR, warp, lane, hist_s, cnt, yoff, kg.hy, marker, rowsrc);
         if (do_hist) {   // merge the tile histogram; support size = its total
             __syncthreads();
             for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) {
