@@ -37,8 +37,9 @@ constexpr int kFwdThreads = 256;
 constexpr int kFwdWarps = kFwdThreads / 32;
 constexpr size_t kFwdBudget = 113 * 1024;   // two CTAs (16 warps) per SM
 constexpr int kRing = 4;                    // per-warp cp.async ring: jobs in flight
-constexpr int kRingSlotB = 32 * 12;         // one job: 32 keys (8 B) + 32 values (4 B)
-constexpr int kRingWords = kFwdWarps * kRing * kRingSlotB / 4;
+constexpr int kRingSlotB = 32 * 8;          // one item: 32 key low words + 32 values
+constexpr int kRingWords = kFwdWarps * kRing * kRingSlotB / 4 > kSelBins + 32 ? kFwdWarps * kRing * kRingSlotB / 4
+                                                                              : kSelBins + 32;
 static_assert(kRingWords >= kSelBins + 32, "the epilogue histogram (+ 32 dummy bins) reuses the ring");
 
 static size_t r4(size_t n) { return (n + 3) & ~(size_t)3; }
@@ -292,9 +293,6 @@ __device__ __forceinline__ float upd(float old, float v, float w) {
     return fmaf(v, w, __float_as_uint(old) == kAbsent ? 0.0f : old);
 }
 
-__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(dst), "l"(src) : "memory");
-}
 __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dst), "l"(src) : "memory");
 }
@@ -302,24 +300,18 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
 
-// Work-item cursor of a warp: the non-empty (ic, input plane) items of a group of 32 (metadata in
-// lanes, jl = owning lane), each split into jobs of up to 32 stored inputs (chunk c).
-struct JobCur {
-    unsigned todo;
-    int jl, c, n;
-};
-__device__ __forceinline__ void job_next(JobCur& j, int m_n) {
-    if (j.jl >= 0 && j.c + 32 < j.n) { j.c += 32; return; }
-    if (!j.todo) { j.jl = -1; return; }
-    j.jl = __ffs(j.todo) - 1;
-    j.todo &= j.todo - 1;
-    j.c = 0;
-    j.n = __shfl_sync(kFull, m_n, j.jl);
+__device__ __forceinline__ int pop_lane(unsigned& m) {
+    if (!m) return -1;
+    const int j = __ffs(m) - 1;
+    m &= m - 1;
+    return j;
 }
 
 // The accumulate loop of one warp: its input rows of every (ic, input plane) item against the
-// item's weight rounds. Inputs stream straight from global memory into a private shared ring
-// with cp.async, kRing - 1 jobs ahead of the one being processed (no block-wide staging).
+// item's weight rounds. Each item's first 32 stored inputs stream from global memory into a
+// private shared ring with cp.async, kRing - 1 items ahead of the one being processed (no
+// block-wide staging); the rare longer runs load their remainder directly. Only the low 32 bits
+// of a key are needed: L = key - rowbase < 2^32, so L = key_lo - rowbase_lo (mod 2^32).
 template <bool NEG0>
 __device__ __forceinline__ void fwd_items(const Geo& gx, const KGeo& kg, const FwdArgs& a, int64_t b, int x,
                                           int A_w, int B_w, int NRP, int ylo, int Z, int ZR, float invZ,
@@ -329,10 +321,11 @@ __device__ __forceinline__ void fwd_items(const Geo& gx, const KGeo& kg, const F
     const int PK = c_in * kg.kx;
     const uint32_t accs = (uint32_t)__cvta_generic_to_shared(accw);
     const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+    const uint32_t* xk32 = reinterpret_cast<const uint32_t*>(a.xkeys);   // little-endian low words
     for (int pg = 0; pg < PK; pg += 32) {
         // lane j gathers the metadata of item pg + j
         int m_n = 0, m_rb = 0, m_re = 0, m_rf = 0;
-        uint32_t m_e0 = 0;
+        uint32_t m_e0 = 0, m_base = 0;
         if (pg + lane < PK) {
             const int pk = pg + lane;
             const uint32_t* RP = rp + pk * NRP;
@@ -342,75 +335,77 @@ __device__ __forceinline__ void fwd_items(const Geo& gx, const KGeo& kg, const F
             m_re = pko[pk + 1];
             m_rf = m_rb + pkf[pk];
             if (m_rb == m_re) m_n = 0;
+            const int ic = pk / kg.kx, xs = x + (pk - ic * kg.kx) - kg.hx;
+            m_base = (uint32_t)((uint64_t)(((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo) * (uint64_t)Z);
         }
-        const unsigned todo = __ballot_sync(kFull, m_n > 0);
-        JobCur iss{todo, -1, 0, 0}, pro{todo, -1, 0, 0};
-        // prologue: kRing - 1 jobs in flight
+        unsigned iss = __ballot_sync(kFull, m_n > 0), pro = iss;
+        auto issue = [&](int jl, int slotk) {
+            const uint32_t e = __shfl_sync(kFull, m_e0, jl);
+            const int n = __shfl_sync(kFull, m_n, jl);
+            if (lane < n) {
+                const uint32_t slot = ring_s + (uint32_t)(slotk * kRingSlotB);
+                cp_async4(slot + lane * 4u, xk32 + 2 * (size_t)(e + lane));
+                cp_async4(slot + 128u + lane * 4u, a.xvals + e + lane);
+            }
+        };
 #pragma unroll
-        for (int k = 0; k < kRing - 1; ++k) {
-            job_next(iss, m_n);
-            if (iss.jl >= 0) {
-                const uint32_t e = __shfl_sync(kFull, m_e0, iss.jl) + (uint32_t)iss.c;
-                if (iss.c + lane < iss.n) {
-                    const uint32_t slot = ring_s + (uint32_t)(k * kRingSlotB);
-                    cp_async8(slot + lane * 8u, a.xkeys + e + lane);
-                    cp_async4(slot + 256u + lane * 4u, a.xvals + e + lane);
-                }
-            }
+        for (int k = 0; k < kRing - 1; ++k) {   // prologue: kRing - 1 items in flight
+            const int jl = pop_lane(iss);
+            if (jl >= 0) issue(jl, k);
             cp_async_commit();
         }
-        for (int k = 0;; ++k) {
-            job_next(pro, m_n);
-            if (pro.jl < 0) break;
-            // issue job k + kRing - 1 into the slot freed by job k - 1
-            job_next(iss, m_n);
-            if (iss.jl >= 0) {
-                const uint32_t e = __shfl_sync(kFull, m_e0, iss.jl) + (uint32_t)iss.c;
-                if (iss.c + lane < iss.n) {
-                    const uint32_t slot = ring_s + (uint32_t)(((k + kRing - 1) % kRing) * kRingSlotB);
-                    cp_async8(slot + lane * 8u, a.xkeys + e + lane);
-                    cp_async4(slot + 256u + lane * 4u, a.xvals + e + lane);
-                }
-            }
+        for (int k = 0; pro; ++k) {
+            const int jl = pop_lane(pro);
+            const int ji = pop_lane(iss);
+            if (ji >= 0) issue(ji, (k + kRing - 1) % kRing);   // into the slot freed by item k - 1
             cp_async_commit();
-            cp_async_wait<kRing - 1>();   // job k has landed (this lane's copies)
-            const int pk = pg + pro.jl;
-            const int rb = __shfl_sync(kFull, m_rb, pro.jl), re = __shfl_sync(kFull, m_re, pro.jl);
-            const int rf = __shfl_sync(kFull, m_rf, pro.jl);
-            const bool valid = pro.c + lane < pro.n;
-            int pos = 0;   // idle lanes: position 0 of the warp's region (reads stay in range)
-            float v = 0.0f;
-            if (valid) {
-                const unsigned char* slot = ring + (k % kRing) * kRingSlotB;
-                const uint64_t key = reinterpret_cast<const uint64_t*>(slot)[lane];
-                v = reinterpret_cast<const float*>(slot + 256)[lane];
-                const int ic = pk / kg.kx, xs = x + (pk - ic * kg.kx) - kg.hx;
-                const uint64_t rowbase = (uint64_t)(((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo) * (uint64_t)Z;
-                const uint32_t L = (uint32_t)(key - rowbase);
-                const uint32_t yrel = div_small(L, (uint32_t)Z, invZ);
-                pos = (int)(yrel * (uint32_t)ZR + (L - yrel * (uint32_t)Z));
-            }
-            const uint32_t base = accs + (uint32_t)pos * 4u;
-            // two-channel rounds: both read-modify-writes in flight (distinct slices); predicated
-            // shared loads/stores (no branch), the next round's record prefetched
-            int4 q = rec[rb];
+            cp_async_wait<kRing - 1>();   // item k has landed (this lane's copies)
+            const int n = __shfl_sync(kFull, m_n, jl);
+            const int rb = __shfl_sync(kFull, m_rb, jl), re = __shfl_sync(kFull, m_re, jl);
+            const int rf = __shfl_sync(kFull, m_rf, jl);
+            const uint32_t rbase = __shfl_sync(kFull, m_base, jl);
+            const uint32_t e0 = __shfl_sync(kFull, m_e0, jl);
+            const unsigned char* slot = ring + (k % kRing) * kRingSlotB;
+            for (int c = 0; c < n; c += 32) {
+                const bool valid = c + lane < n;
+                int pos = 0;   // idle lanes: position 0 of the warp's region (reads stay in range)
+                float v = 0.0f;
+                if (valid) {
+                    uint32_t klo;
+                    if (c == 0) {
+                        klo = reinterpret_cast<const uint32_t*>(slot)[lane];
+                        v = reinterpret_cast<const float*>(slot + 128)[lane];
+                    } else {   // remainder of a long run: direct loads
+                        const uint32_t e = e0 + (uint32_t)(c + lane);
+                        klo = xk32[2 * (size_t)e];
+                        v = a.xvals[e];
+                    }
+                    const uint32_t L = klo - rbase;
+                    const uint32_t yrel = div_small(L, (uint32_t)Z, invZ);
+                    pos = (int)(yrel * (uint32_t)ZR + (L - yrel * (uint32_t)Z));
+                }
+                const uint32_t base = accs + (uint32_t)pos * 4u;
+                // two-channel rounds: both read-modify-writes in flight (distinct slices);
+                // predicated shared loads/stores (no branch), the next round's record prefetched
+                int4 q = rec[rb];
 #pragma unroll 2
-            for (int r = rb; r < rf; ++r) {
-                const int4 qn = rec[r + 1];   // rec[re] stays inside shared memory (pko follows)
-                const uint32_t pa = base + (uint32_t)q.x, pb = base + (uint32_t)q.z;
-                const float oa = lds_u(pa), ob = lds_u(pb);
-                sts_p(pa, upd<NEG0>(oa, v, __int_as_float(q.y)), valid);
-                sts_p(pb, upd<NEG0>(ob, v, __int_as_float(q.w)), valid);
-                __syncwarp();   // the next round's lanes may read what this one wrote
-                q = qn;
-            }
+                for (int r = rb; r < rf; ++r) {
+                    const int4 qn = rec[r + 1];   // rec[re] stays inside shared memory (pko follows)
+                    const uint32_t pa = base + (uint32_t)q.x, pb = base + (uint32_t)q.z;
+                    const float oa = lds_u(pa), ob = lds_u(pb);
+                    sts_p(pa, upd<NEG0>(oa, v, __int_as_float(q.y)), valid);
+                    sts_p(pb, upd<NEG0>(ob, v, __int_as_float(q.w)), valid);
+                    __syncwarp();   // the next round's lanes may read what this one wrote
+                    q = qn;
+                }
 #pragma unroll 1
-            for (int r = rf; r < re; ++r) {
-                const int4 qn = rec[r + 1];
-                const uint32_t pa = base + (uint32_t)q.x;
-                sts_p(pa, upd<NEG0>(lds_u(pa), v, __int_as_float(q.y)), valid);
-                q = qn;
-                __syncwarp();
+                for (int r = rf; r < re; ++r) {
+                    const int4 qn = rec[r + 1];
+                    const uint32_t pa = base + (uint32_t)q.x;
+                    sts_p(pa, upd<NEG0>(lds_u(pa), v, __int_as_float(q.y)), valid);
+                    q = qn;
+                    __syncwarp();
+                }
             }
         }
         cp_async_wait<0>();
