@@ -16,17 +16,22 @@
 #include "block_scan.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace spc {
 
-constexpr int kBwdThreads = 512;
-constexpr size_t kBwdBudget = 200 * 1024;
+// CTA shapes: one 512-thread CTA per SM (largest G slab), or two 256-thread CTAs per SM that
+// hide each other's per-item global-memory latency (SPC_BWD_CTAS=1|2 overrides the default)
+static int bwd_ctas_per_sm() {
+    const char* v = getenv("SPC_BWD_CTAS");
+    return (v && v[0] == '2') ? 2 : 1;
+}
 
-static size_t bwd_smem(const KGeo& kg, int c_in, int TX, int TY, int ZR, int ocg, int64_t nwg) {
+static size_t bwd_smem(const KGeo& kg, int c_in, int TX, int TY, int ZR, int ocg, int64_t nwg, int threads) {
     const size_t g = (size_t)ocg * (TX + 2 * kg.hx) * (TY + 2 * kg.hy) * ZR * sizeof(float);
     const size_t w = (size_t)nwg * (sizeof(int) + sizeof(float) + sizeof(double));
     const size_t idx = (size_t)(c_in + 1) * sizeof(int) * 2 + (size_t)c_in * TX * 2 * sizeof(uint32_t);
-    const size_t stage = (size_t)(kBwdThreads / 32) * 32 * (sizeof(int) + sizeof(float));
+    const size_t stage = (size_t)(threads / 32) * 32 * (sizeof(int) + sizeof(float));
     return g + w + idx + stage + 256;
 }
 
@@ -34,7 +39,10 @@ BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int nw_total) {
     BwdTile t{};
     const int c_in = (int)gx.C;
     const int ZR = gx.Z + 2 * kg.hz;
-    int ocg = std::min(c_out, 8);
+    const int cps = bwd_ctas_per_sm();
+    const int threads = cps == 2 ? 256 : 512;
+    const size_t budget = cps == 2 ? 110 * 1024 : 200 * 1024;
+    int ocg = std::min(c_out, cps == 2 ? 4 : 8);
     for (; ocg >= 1; ocg = ocg > 1 ? (ocg + 1) / 2 : 0) {
         const int64_t nwg = std::min<int64_t>(nw_total, (int64_t)ocg * c_in * kg.KV);
         double best = -1.0;
@@ -43,7 +51,7 @@ BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int nw_total) {
             int lo = 1, hi = gx.Y, ty = 0;
             while (lo <= hi) {   // largest ty that fits
                 const int mid = (lo + hi) / 2;
-                if (bwd_smem(kg, c_in, tx, mid, ZR, ocg, nwg) <= kBwdBudget) { ty = mid; lo = mid + 1; }
+                if (bwd_smem(kg, c_in, tx, mid, ZR, ocg, nwg, threads) <= budget) { ty = mid; lo = mid + 1; }
                 else hi = mid - 1;
             }
             if (ty < 1) break;
@@ -59,9 +67,10 @@ BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int nw_total) {
         t.ntx = (gx.X + bx - 1) / bx;
         t.nty = (gx.Y + by - 1) / by;
         t.nwg_max = (int)nwg;
-        t.smem = bwd_smem(kg, c_in, bx, by, ZR, ocg, nwg);
+        t.smem = bwd_smem(kg, c_in, bx, by, ZR, ocg, nwg, threads);
+        t.threads = threads;
         const int64_t items = gx.B * (int64_t)t.ntx * t.nty;
-        int64_t grid = (148 + t.n_ocg - 1) / t.n_ocg;
+        int64_t grid = (148 * cps + t.n_ocg - 1) / t.n_ocg;
         grid = std::max<int64_t>(1, std::min<int64_t>(grid, items));
         t.grid = (int)grid;
         return t;
@@ -85,8 +94,8 @@ __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
     return v[0];
 }
 
-template <bool DX, bool DW>
-__global__ void __launch_bounds__(kBwdThreads, 1)
+template <bool DX, bool DW, int THREADS>
+__global__ void __launch_bounds__(THREADS, 512 / THREADS)
 conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__ xkeys,
                 const float* __restrict__ xvals, const uint32_t* __restrict__ xrow,
                 const uint64_t* __restrict__ ykeys, const float* __restrict__ dy, const uint32_t* __restrict__ yrow,
@@ -286,19 +295,32 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
     }
 }
 
+template <bool DX, bool DW, int THREADS>
+static cudaError_t launch_bwd_tt(const Geo& gx, const Geo& gy, const KGeo& kg, const BwdTile& t,
+                                const uint64_t* xkeys, const float* xvals, const uint32_t* xrow,
+                                const uint64_t* ykeys, const float* dy, const uint32_t* yrow,
+                                const int2* wmeta, const float* wval, const int* woff, const int* wsrc,
+                                float* dx, double* dw_acc, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(conv_bwd_kernel<DX, DW, THREADS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)t.grid, (unsigned)t.n_ocg);
+    { SPC_PHASE("conv_bwd", s, 1); conv_bwd_kernel<DX, DW, THREADS><<<grid, THREADS, t.smem, s>>>(
+          gx, gy, kg, t, xkeys, xvals, xrow, ykeys, dy, yrow, wmeta, wval, woff, wsrc, dx, dw_acc); }
+    return cudaGetLastError();
+}
+
 template <bool DX, bool DW>
 static cudaError_t launch_bwd_t(const Geo& gx, const Geo& gy, const KGeo& kg, const BwdTile& t,
                                 const uint64_t* xkeys, const float* xvals, const uint32_t* xrow,
                                 const uint64_t* ykeys, const float* dy, const uint32_t* yrow,
                                 const int2* wmeta, const float* wval, const int* woff, const int* wsrc,
                                 float* dx, double* dw_acc, cudaStream_t s) {
-    cudaError_t e = cudaFuncSetAttribute(conv_bwd_kernel<DX, DW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)t.smem);
-    if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)t.grid, (unsigned)t.n_ocg);
-    { SPC_PHASE("conv_bwd", s, 1); conv_bwd_kernel<DX, DW><<<grid, kBwdThreads, t.smem, s>>>(
-          gx, gy, kg, t, xkeys, xvals, xrow, ykeys, dy, yrow, wmeta, wval, woff, wsrc, dx, dw_acc); }
-    return cudaGetLastError();
+    if (t.threads == 256)
+        return launch_bwd_tt<DX, DW, 256>(gx, gy, kg, t, xkeys, xvals, xrow, ykeys, dy, yrow, wmeta, wval, woff, wsrc,
+                                          dx, dw_acc, s);
+    return launch_bwd_tt<DX, DW, 512>(gx, gy, kg, t, xkeys, xvals, xrow, ykeys, dy, yrow, wmeta, wval, woff, wsrc,
+                                      dx, dw_acc, s);
 }
 
 cudaError_t launch_conv_bwd(const Geo& gx, const Geo& gy, const KGeo& kg, const BwdTile& t,

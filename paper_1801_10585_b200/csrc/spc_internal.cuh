@@ -163,6 +163,7 @@ cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& k
 
 struct BwdTile {
     int TX, TY, ocg, ntx, nty, n_ocg, grid;
+    int threads;      // CTA size (512: one CTA per SM, 256: two)
     int nwg_max;      // upper bound of stored weights in one output-channel group
     size_t smem;
 };

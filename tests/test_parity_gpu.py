@@ -56,6 +56,7 @@ FWD_CASES = [
     ("3d_k1", (6, 6, 6), 2, 4, 6, (1, 1, 1), 0.3, 1.0),
     ("3d_wide_oc", (10, 12, 14), 1, 2, 40, (3, 3, 3), 0.05, 0.3),  # several oc groups
     ("3d_long_z", (3, 3, 700), 2, 2, 3, (3, 3, 3), 0.05, 0.5),
+    ("3d_dense", (12, 16, 64), 1, 3, 4, (3, 3, 3), 0.4, 0.5),     # > 32 inputs per warp item
 ]
 
 
