@@ -189,9 +189,8 @@ FwdWs carve_fwd(Carver& c, const Geo& gx, const Geo& gy, const KGeo& kg, const F
     a.chunk_stg = c.take<uint64_t>((size_t)(nseg * a.nchunk));
     a.chunk_ge = c.take<uint32_t>((size_t)(nseg * a.nchunk));
     const size_t PK = (size_t)w->c_in * kg.kx;
-    a.rec = c.take<int4>((size_t)t.n_ocg * t.nwg_max + 1);
-    a.pkoff = c.take<int>((size_t)t.n_ocg * (PK + 1));
-    a.pkfull = c.take<int>((size_t)t.n_ocg * PK);
+    a.rnd = c.take<int2>((size_t)t.n_ocg * t.nwg_max + 1);
+    a.roff = c.take<int>((size_t)t.n_ocg * (t.ocg * PK + 1));
     a.guard = c.take<int>(1);
     ws.flag = c.take<int>(1);
     return ws;

@@ -27,6 +27,7 @@
 #include "block_scan.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #ifdef SPC_DEBUG
 #include <cstdio>
 #endif
@@ -34,51 +35,47 @@
 namespace spc {
 
 constexpr int kFwdThreads = 256;
-constexpr int kFwdWarps = kFwdThreads / 32;
-constexpr size_t kFwdBudget = 113 * 1024;   // two CTAs (16 warps) per SM
-constexpr int kRing = 4;                    // per-warp cp.async ring: jobs in flight
-constexpr int kRingSlotB = 32 * 8;          // one item: 32 key low words + 32 values
-constexpr int kRingWords = kFwdWarps * kRing * kRingSlotB / 4 > kSelBins + 32 ? kFwdWarps * kRing * kRingSlotB / 4
-                                                                              : kSelBins + 32;
-static_assert(kRingWords >= kSelBins + 32, "the epilogue histogram (+ 32 dummy bins) reuses the ring");
+constexpr int kFwdWarps = kFwdThreads / 32;   // warp w accumulates output channel oc0 + w
+constexpr size_t kFwdBudget = 113 * 1024;     // two CTAs (16 warps) per SM
+constexpr int kStageCap = 1536;               // staged input entries per chunk (byte position + value)
+static_assert(kStageCap * 8 >= (kSelBins + 32) * 4, "the epilogue histogram (+ 32 dummy bins) reuses the staging area");
 
-static size_t r4(size_t n) { return (n + 3) & ~(size_t)3; }
+__host__ __device__ inline size_t r4(size_t n) { return (n + 3) & ~(size_t)3; }
 
-// shared-memory bytes beyond the accumulator
-static size_t fwd_fixed_smem(const KGeo& kg, int c_in, int TY, int64_t nwg) {
-    const size_t PK = (size_t)c_in * kg.kx;
-    return 4 * (512 + 4 * (size_t)nwg + 2 * r4(PK + 1) + r4(PK * (TY + 2 * kg.hy + 1)) + (size_t)kRingWords) + 64;
+// shared-memory bytes beyond the accumulator: staging, item tables (flat offset, first global
+// entry, row base), round offsets and round records of the group, scratch
+static size_t fwd_fixed_smem(int PK, int ocg, int64_t nwg) {
+    return (size_t)kStageCap * 8 + 4 * (3 * r4(PK + 1) + r4(kStageCap / 64 + PK + 1) + 64) +
+           8 * ((size_t)ocg * PK + (size_t)nwg) + 64;
 }
 
 FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_t nw_total) {
     FwdTile t{};
-    const int ZR = ((gy.Z + 2 * kg.hz + 3) / 4) * 4;
-    const int pad = ((kg.hz + 3) / 4) * 4;
-    const size_t row_b = (size_t)ZR * sizeof(float);
-    auto rows = [&](int TY) { return TY + 2 * kg.hy + 2 * kg.hy * kFwdWarps; };
+    const int cz = ((kg.hz + 3) / 4) * 4;                         // column of z = 0 (16-byte aligned rows)
+    const int ZR = (int)r4((size_t)cz + gy.Z + kg.hz);
+    const int PK = c_in * kg.kx;
+    auto nwg = [&](int ocg) { return std::min<int64_t>(nw_total, (int64_t)ocg * c_in * kg.KV); };
     auto need = [&](int ocg, int TY) {
-        const int64_t nwg = std::min<int64_t>(nw_total, (int64_t)ocg * c_in * kg.KV);
-        return fwd_fixed_smem(kg, c_in, TY, nwg) + (size_t)ocg * rows(TY) * row_b + (size_t)pad * 8;
+        return fwd_fixed_smem(PK, ocg, nwg(ocg)) + (size_t)ocg * (TY + 4 * kg.hy) * ZR * sizeof(float);
     };
-    // prefer >= 8 input rows per warp (lane utilisation), then the largest group of channels
-    int TY = std::min(gy.Y, 8 * kFwdWarps);
-    int ocg = std::min(c_out, 16);
-    while (ocg > 1 && need(ocg, TY) > kFwdBudget) --ocg;
-    while (TY > 1 && need(ocg, TY) > kFwdBudget) --TY;          // ocg == 1: shorter tiles
-    if (need(ocg, TY) > kFwdBudget) { t.smem = 0; return t; }
-    while (TY < gy.Y && need(ocg, TY + kFwdWarps) <= kFwdBudget) TY += kFwdWarps;   // spare room
-    TY = std::min(TY, std::min(gy.Y, 240));   // staged rows are packed in 8 bits (TY + 2*hy < 256); TY <= 448 (row owners)
-    t.TY = TY;
-    t.RW = (TY + kFwdWarps - 1) / kFwdWarps;
-    t.RT = rows(TY);
-    t.nty = (gy.Y + TY - 1) / TY;
+    if (PK >= (1 << 13)) { t.smem = 0; return t; }                 // work descriptors hold 13-bit items
+    int ocg = std::min(c_out, kFwdWarps);
+    while (ocg > 1 && need(ocg, 1) > kFwdBudget) --ocg;
+    if (need(ocg, 1) > kFwdBudget) { t.smem = 0; return t; }
+    int TYmax = 1;
+    while (TYmax < gy.Y && need(ocg, TYmax + 1) <= kFwdBudget) ++TYmax;
+    if (const char* e = getenv("SPC_FWD_TY")) TYmax = std::max(1, std::min(TYmax, atoi(e)));
+    const int nty = (gy.Y + TYmax - 1) / TYmax;
+    t.TY = (gy.Y + nty - 1) / nty;                                   // balanced bands
+    t.nty = nty;
     t.ocg = ocg;
     t.n_ocg = (c_out + ocg - 1) / ocg;
     t.ZR = ZR;
-    t.pad = pad;
-    t.NT = gy.X * t.nty;
-    t.nwg_max = (int)std::min<int64_t>(nw_total, (int64_t)ocg * c_in * kg.KV);
-    t.smem = need(ocg, TY);
+    t.cz = cz;
+    t.RA = t.TY + 4 * kg.hy;
+    t.PK = PK;
+    t.nwg_max = (int)nwg(ocg);
+    t.smem = need(ocg, t.TY);
     return t;
 }
 
@@ -97,89 +94,51 @@ __global__ void value_guard_kernel(const float* __restrict__ v, const int64_t* n
 }
 
 // Weight rounds of one output-channel group (one block per group). Alg. 1 walks "for {fid,
-// fval} in filter(oc, ic)"; the kernel below walks, per (ic, input plane dx), rounds that
-// pair a weight of channel 2p with one of channel 2p+1: the two targets lie in different channel
-// slices of the accumulator, so both read-modify-writes of a round can be in flight together.
-// Round record {wdA, wA, wdB, wB}: wd = byte offset from an input's accumulator position to its
-// target uid = id - (fid - centre) = slice(oc) - oy rows - oz columns. Per (ic, dx): first
-// the two-channel rounds of every pair, then the leftovers of the longer list (wdB unused).
+// fval} in filter(oc, ic)"; here the stored weights of (oc, ic, input plane dx) form the
+// rounds of work item (ic, dx) for the warp of oc, ordered (dy, dz). Round record {wd, w}: wd =
+// byte offset from an input's accumulator position to its target uid = id - (fid - centre)
+// = -(dy - hy) rows - (dz - hz) columns, plus the channel slice of oc.
 __global__ void fwd_rounds_kernel(KGeo kg, int c_in, int c_out, FwdTile t, const int2* __restrict__ meta2,
-                                  const float* __restrict__ val2, const int* __restrict__ off2, int4* __restrict__ rec,
-                                  int* __restrict__ pkoff, int* __restrict__ pkfull, int* __restrict__ guard) {
+                                  const float* __restrict__ val2, const int* __restrict__ off2, int2* __restrict__ rnd,
+                                  int* __restrict__ roff, int* __restrict__ guard) {
     __shared__ int sm[33];
     const int grp = blockIdx.x, oc0 = grp * t.ocg, nocl = min(t.ocg, c_out - oc0);
-    const int PK = c_in * kg.kx, npair = (nocl + 1) / 2;
-    const int SLb = t.RT * t.ZR * (int)sizeof(float);
-    int4* R = rec + (int64_t)grp * t.nwg_max;
-    int* PO = pkoff + (int64_t)grp * (PK + 1);
-    int* PF = pkfull + (int64_t)grp * PK;
-    auto count = [&](int pk, int oc) {
+    const int PK = t.PK, NQ = t.ocg * PK;
+    const int SLb = t.RA * t.ZR * (int)sizeof(float);
+    int2* R = rnd + (int64_t)grp * t.nwg_max;
+    int* RO = roff + (int64_t)grp * (NQ + 1);
+    int carry = 0;
+    for (int q0 = 0; q0 < NQ; q0 += blockDim.x) {
+        const int q = q0 + threadIdx.x;            // q = ocl*PK + pk
+        const int ocl = q / PK, pk = q - (q / PK) * PK;
+        const int ic = pk / kg.kx, dx = pk - (pk / kg.kx) * kg.kx;
+        const int oc = oc0 + ocl;
         int n = 0;
-        if (oc < oc0 + nocl)
-            for (int dyi = 0; dyi < kg.ky; ++dyi) {
-                const int g = pk * kg.ky + dyi;
+        if (q < NQ && ocl < nocl)
+            for (int dy = 0; dy < kg.ky; ++dy) {
+                const int g = (ic * kg.kx + dx) * kg.ky + dy;
                 n += off2[g * (c_out + 1) + oc + 1] - off2[g * (c_out + 1) + oc];
             }
-        return n;
-    };
-    // the r-th weight of channel oc in (ic, dx), ordered (dy, dz)
-    auto weight = [&](int pk, int oc, int r, int& wd, float& wv) {
-        for (int dyi = 0; dyi < kg.ky; ++dyi) {
-            const int g = pk * kg.ky + dyi;
-            const int lo = off2[g * (c_out + 1) + oc], n = off2[g * (c_out + 1) + oc + 1] - lo;
-            if (r < n) {
-                const int2 m = meta2[lo + r];
-                wd = (oc - oc0) * SLb - ((dyi - kg.hy) * t.ZR + m.y) * (int)sizeof(float);
-                wv = val2[lo + r];
-                if (!(fabsf(wv) >= 0x1p-50f) && !isnan(wv)) *guard = 1;
-                return;
-            }
-            r -= n;
-        }
-    };
-    int carry = 0;
-    for (int p0 = 0; p0 < PK; p0 += blockDim.x) {
-        const int pk = p0 + threadIdx.x;
-        int tot = 0, full = 0;
-        if (pk < PK)
-            for (int p = 0; p < npair; ++p) {
-                const int na = count(pk, oc0 + 2 * p), nb = count(pk, oc0 + 2 * p + 1);
-                tot += max(na, nb);
-                full += min(na, nb);
-            }
         int all;
-        const int ex = block_excl_scan(tot, sm, &all);
-        if (pk < PK) {
-            const int base = carry + ex;
-            PO[pk] = base;
-            PF[pk] = full;
-            int f = base, sgl = base + full;
-            for (int p = 0; p < npair; ++p) {
-                const int oa = oc0 + 2 * p, ob = oa + 1;
-                const int na = count(pk, oa), nb = count(pk, ob);
-                const int m = min(na, nb);
-                for (int r = 0; r < m; ++r) {
-                    int4 q;
-                    float wa, wb;
-                    weight(pk, oa, r, q.x, wa);
-                    weight(pk, ob, r, q.z, wb);
-                    q.y = __float_as_int(wa);
-                    q.w = __float_as_int(wb);
-                    R[f++] = q;
+        const int ex = block_excl_scan(n, sm, &all);
+        if (q < NQ) {
+            int f = carry + ex;
+            RO[q] = f;
+            if (ocl < nocl)
+                for (int dy = 0; dy < kg.ky; ++dy) {
+                    const int g = (ic * kg.kx + dx) * kg.ky + dy;
+                    const int lo = off2[g * (c_out + 1) + oc], hi = off2[g * (c_out + 1) + oc + 1];
+                    for (int j = lo; j < hi; ++j) {
+                        const float wv = val2[j];
+                        if (!(fabsf(wv) >= 0x1p-50f) && !isnan(wv)) *guard = 1;
+                        const int wd = ocl * SLb - ((dy - kg.hy) * t.ZR + meta2[j].y) * (int)sizeof(float);
+                        R[f++] = make_int2(wd, __float_as_int(wv));
+                    }
                 }
-                const int ol = na > nb ? oa : ob;
-                for (int r = m; r < max(na, nb); ++r) {
-                    int4 q{0, 0, 0, 0};
-                    float wa;
-                    weight(pk, ol, r, q.x, wa);
-                    q.y = __float_as_int(wa);
-                    R[sgl++] = q;
-                }
-            }
         }
         carry += all;
     }
-    if (threadIdx.x == 0) PO[PK] = carry;
+    if (threadIdx.x == 0) RO[NQ] = carry;
 }
 
 // fast y = L / Z for L < 2^24 (float reciprocal + one correction each way)
@@ -194,62 +153,26 @@ __device__ __forceinline__ uint64_t composite(uint32_t sc, uint32_t p) {
     return ((uint64_t)sc << 32) | (uint64_t)(0xffffffffu - p);
 }
 
-__device__ __forceinline__ float absent_add(float a, float b, uint32_t marker) {
-    if (__float_as_uint(a) == marker) return b;
-    if (__float_as_uint(b) == marker) return a;
-    return a + b;
-}
-
-// warp owning input row i (rows split as A_w = floor(w*nr/8)): floor((8i + 7) / nr), by a float
-// reciprocal and one correction each way (8i + 7 < 2^11)
-__device__ __forceinline__ int owner_of(int i, int nr, float inv_nr) {
-    const int num = 8 * i + 7;
-    int q = __float2int_rz((float)num * inv_nr);
-    if (q * nr > num) --q;
-    if ((q + 1) * nr <= num) ++q;
-    return q;
-}
-
-// Epilogue rows of one output channel: merge the warps' copies of each row (fixed warp order),
-// bias on the support, streaming store of the slice, support count and (with attention) the
-// score-digit histogram. Branch-free: lanes off the support increment a private dummy bin past
-// the histogram instead of branching around the atomic.
+// Epilogue rows of one output channel: bias on the support, streaming store of the slice,
+// support count and (with attention) the score-digit histogram. Branch-free: lanes off the
+// support increment a private dummy bin past the histogram instead of branching around the
+// atomic.
 template <int MODE>
-__device__ __forceinline__ void epi_rows(const float* S, float* P, float bv, int nyr, int Z, int ZR, int warp,
-                                         int lane, uint32_t hist_s, uint32_t& cnt, int yoff, int hy,
-                                         uint32_t marker, const uint32_t* rowsrc) {
+__device__ __forceinline__ void epi_rows(const float* S, float* P, float bv, int nyr, int Z, int ZR, uint32_t hist_s,
+                                         uint32_t& cnt, uint32_t marker) {
     const bool vec = (Z & 3) == 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t dummy = hist_s + (uint32_t)(kSelBins + lane) * 4u;
     for (int r = warp; r < nyr; r += kFwdWarps) {
-        // row yrel = r + yoff (relative to the first input row) has a copy in the region of every
-        // warp owning an input row in [yrel - hy, yrel + hy], at region row yrel + hy*(2w + 1)
-        const int yrel = r + yoff;
-        const uint32_t ow = rowsrc[r];   // source warps of this row (owner table of the tile)
-        const int wlo = (int)(ow & 0xffu), whi = (int)(ow >> 8);
         for (int z0 = 4 * lane; z0 < Z; z0 += 128) {
+            const float* A = S + r * ZR + z0;
             float v[4];
-            {
-                const float* A = S + (yrel + hy * (2 * wlo + 1)) * ZR + z0;
-                if (vec) {
-                    const float4 q = *reinterpret_cast<const float4*>(A);
-                    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
-                } else {
+            if (vec) {
+                const float4 q = *reinterpret_cast<const float4*>(A);
+                v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+            } else {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) v[e] = z0 + e < Z ? A[e] : __uint_as_float(marker);
-                }
-            }
-            for (int w = wlo + 1; w <= whi; ++w) {   // rows next to a warp boundary: merge copies
-                const float* A = S + (yrel + hy * (2 * w + 1)) * ZR + z0;
-                float u[4];
-                if (vec) {
-                    const float4 q = *reinterpret_cast<const float4*>(A);
-                    u[0] = q.x; u[1] = q.y; u[2] = q.z; u[3] = q.w;
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) u[e] = z0 + e < Z ? A[e] : __uint_as_float(marker);
-                }
-#pragma unroll
-                for (int e = 0; e < 4; ++e) v[e] = absent_add(v[e], u[e], marker);
+                for (int e = 0; e < 4; ++e) v[e] = z0 + e < Z ? A[e] : __uint_as_float(marker);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -293,126 +216,58 @@ __device__ __forceinline__ float upd(float old, float v, float w) {
     return fmaf(v, w, __float_as_uint(old) == kAbsent ? 0.0f : old);
 }
 
-__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
-
-__device__ __forceinline__ int pop_lane(unsigned& m) {
-    if (!m) return -1;
-    const int j = __ffs(m) - 1;
-    m &= m - 1;
-    return j;
-}
-
-// The accumulate loop of one warp: its input rows of every (ic, input plane) item against the
-// item's weight rounds. Each item's first 32 stored inputs stream from global memory into a
-// private shared ring with cp.async, kRing - 1 items ahead of the one being processed (no
-// block-wide staging); the rare longer runs load their remainder directly. Only the low 32 bits
-// of a key are needed: L = key - rowbase < 2^32, so L = key_lo - rowbase_lo (mod 2^32).
+// The accumulate loop of one warp (output channel slice fixed by the round records): every
+// work item (ic, input plane) of the staged chunk against the item's rounds {byte offset,
+// weight}, read from shared memory by broadcast. Entries go 64 at a time, two per lane, so that
+// two independent read-modify-writes are in flight per round. Entries of one item have distinct
+// positions, so the 64 targets of a round are distinct; rounds are separated by __syncwarp (a
+// later round may read what an earlier one wrote). Idle lanes address a safe interior word
+// (every round offset keeps it inside the slice) and do not store.
 template <bool NEG0>
-__device__ __forceinline__ void fwd_items(const Geo& gx, const KGeo& kg, const FwdArgs& a, int64_t b, int x,
-                                          int A_w, int B_w, int NRP, int ylo, int Z, int ZR, float invZ,
-                                          int lane, const uint32_t* rp, const int* pko, const int* pkf,
-                                          const int4* rec, unsigned char* ring, const char* accw) {
-    const int c_in = (int)gx.C;
-    const int PK = c_in * kg.kx;
-    const uint32_t accs = (uint32_t)__cvta_generic_to_shared(accw);
-    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
-    const uint32_t* xk32 = reinterpret_cast<const uint32_t*>(a.xkeys);   // little-endian low words
-    for (int pg = 0; pg < PK; pg += 32) {
-        // lane j gathers the metadata of item pg + j
-        int m_n = 0, m_rb = 0, m_re = 0, m_rf = 0;
-        uint32_t m_e0 = 0, m_base = 0;
-        if (pg + lane < PK) {
-            const int pk = pg + lane;
-            const uint32_t* RP = rp + pk * NRP;
-            m_e0 = RP[A_w];
-            m_n = (int)(RP[B_w] - m_e0);
-            m_rb = pko[pk];
-            m_re = pko[pk + 1];
-            m_rf = m_rb + pkf[pk];
-            if (m_rb == m_re) m_n = 0;
-            const int ic = pk / kg.kx, xs = x + (pk - ic * kg.kx) - kg.hx;
-            m_base = (uint32_t)((uint64_t)(((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo) * (uint64_t)Z);
-        }
-        unsigned iss = __ballot_sync(kFull, m_n > 0), pro = iss;
-        auto issue = [&](int jl, int slotk) {
-            const uint32_t e = __shfl_sync(kFull, m_e0, jl);
-            const int n = __shfl_sync(kFull, m_n, jl);
-            if (lane < n) {
-                const uint32_t slot = ring_s + (uint32_t)(slotk * kRingSlotB);
-                cp_async4(slot + lane * 4u, xk32 + 2 * (size_t)(e + lane));
-                cp_async4(slot + 128u + lane * 4u, a.xvals + e + lane);
-            }
-        };
-#pragma unroll
-        for (int k = 0; k < kRing - 1; ++k) {   // prologue: kRing - 1 items in flight
-            const int jl = pop_lane(iss);
-            if (jl >= 0) issue(jl, k);
-            cp_async_commit();
-        }
-        for (int k = 0; pro; ++k) {
-            const int jl = pop_lane(pro);
-            const int ji = pop_lane(iss);
-            if (ji >= 0) issue(ji, (k + kRing - 1) % kRing);   // into the slot freed by item k - 1
-            cp_async_commit();
-            cp_async_wait<kRing - 1>();   // item k has landed (this lane's copies)
-            const int n = __shfl_sync(kFull, m_n, jl);
-            const int rb = __shfl_sync(kFull, m_rb, jl), re = __shfl_sync(kFull, m_re, jl);
-            const int rf = __shfl_sync(kFull, m_rf, jl);
-            const uint32_t rbase = __shfl_sync(kFull, m_base, jl);
-            const uint32_t e0 = __shfl_sync(kFull, m_e0, jl);
-            const unsigned char* slot = ring + (k % kRing) * kRingSlotB;
-            for (int c = 0; c < n; c += 32) {
-                const bool valid = c + lane < n;
-                int pos = 0;   // idle lanes: position 0 of the warp's region (reads stay in range)
-                float v = 0.0f;
-                if (valid) {
-                    uint32_t klo;
-                    if (c == 0) {
-                        klo = reinterpret_cast<const uint32_t*>(slot)[lane];
-                        v = reinterpret_cast<const float*>(slot + 128)[lane];
-                    } else {   // remainder of a long run: direct loads
-                        const uint32_t e = e0 + (uint32_t)(c + lane);
-                        klo = xk32[2 * (size_t)e];
-                        v = a.xvals[e];
-                    }
-                    const uint32_t L = klo - rbase;
-                    const uint32_t yrel = div_small(L, (uint32_t)Z, invZ);
-                    pos = (int)(yrel * (uint32_t)ZR + (L - yrel * (uint32_t)Z));
-                }
-                const uint32_t base = accs + (uint32_t)pos * 4u;
-                // two-channel rounds: both read-modify-writes in flight (distinct slices);
-                // predicated shared loads/stores (no branch), the next round's record prefetched
-                int4 q = rec[rb];
-#pragma unroll 2
-                for (int r = rb; r < rf; ++r) {
-                    const int4 qn = rec[r + 1];   // rec[re] stays inside shared memory (pko follows)
-                    const uint32_t pa = base + (uint32_t)q.x, pb = base + (uint32_t)q.z;
-                    const float oa = lds_u(pa), ob = lds_u(pb);
-                    sts_p(pa, upd<NEG0>(oa, v, __int_as_float(q.y)), valid);
-                    sts_p(pb, upd<NEG0>(ob, v, __int_as_float(q.w)), valid);
-                    __syncwarp();   // the next round's lanes may read what this one wrote
-                    q = qn;
-                }
+__device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, uint32_t safe, const uint32_t* work,
+                                          const int2* rpair, const int2* rec, const uint32_t* spos,
+                                          const float* sval) {
 #pragma unroll 1
-                for (int r = rf; r < re; ++r) {
-                    const int4 qn = rec[r + 1];
-                    const uint32_t pa = base + (uint32_t)q.x;
-                    sts_p(pa, upd<NEG0>(lds_u(pa), v, __int_as_float(q.y)), valid);
-                    q = qn;
-                    __syncwarp();
-                }
+    for (int g = 0; g < nwork; ++g) {
+        const uint32_t wdsc = work[g];                 // {chunk-relative start, count <= 64, item}
+        const int2 rr = rpair[wdsc >> 19];
+        if (rr.x == rr.y) continue;
+        const int s = (int)(wdsc & 0xfffu), n = (int)((wdsc >> 12) & 0x7fu);
+        const bool okA = lane < n, okB = lane + 32 < n;
+        const uint32_t aA = accs + (okA ? spos[s + lane] : safe);
+        const float vA = okA ? sval[s + lane] : 0.0f;
+        if (n > 32) {
+            const uint32_t aB = accs + (okB ? spos[s + 32 + lane] : safe);
+            const float vB = okB ? sval[s + 32 + lane] : 0.0f;
+#pragma unroll 2
+            for (int r = rr.x; r < rr.y; ++r) {
+                const int2 q = rec[r];
+                const uint32_t qa = aA + (uint32_t)q.x, qb = aB + (uint32_t)q.x;
+                const float w = __int_as_float(q.y);
+                const float oa = lds_u(qa), ob = lds_u(qb);
+                sts_p(qa, upd<NEG0>(oa, vA, w), okA);
+                sts_p(qb, upd<NEG0>(ob, vB, w), okB);
+                __syncwarp();
+            }
+        } else {
+#pragma unroll 2
+            for (int r = rr.x; r < rr.y; ++r) {
+                const int2 q = rec[r];
+                const uint32_t qa = aA + (uint32_t)q.x;
+                sts_p(qa, upd<NEG0>(lds_u(qa), vA, __int_as_float(q.y)), okA);
+                __syncwarp();
             }
         }
-        cp_async_wait<0>();
-        __syncwarp();
     }
 }
 
+// One CTA = (b, output x-plane, band of TY rows, group of ocg output channels); its slice of the
+// paper's temporary dense buffer lives in shared memory as [ocg][TY + 4hy rows][ZR
+// columns] (2hy margin rows on each side catch the targets of halo inputs that fall outside the
+// band). The stored inputs of every work item (ic, input plane x + dx - hx), rows of the band
+// plus halo, are contiguous key runs (row index); they are staged once per CTA as (byte position,
+// value) and shared by all warps. Warp w owns output channel oc0 + w: no two warps write the
+// same word, no atomics, and a fixed order makes the result deterministic.
 __global__ void __launch_bounds__(kFwdThreads, 2)
 conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     extern __shared__ __align__(16) float smf[];
@@ -426,63 +281,118 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     const int nocl = min(t.ocg, c_out - oc0);
     const int y0 = ty * t.TY, ye = min(y0 + t.TY, gy.Y);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int SL = t.RT * ZR;                        // floats per output-channel slice
+    const int SL = t.RA * ZR;                        // floats per output-channel slice
+    const int PK = t.PK;
 
-    // shared layout (float offsets, 16-byte aligned pieces):
-    // [pad][acc ocg*RT*ZR][pad] | misc(512) | rounds | pko | pkf | rp | cp.async rings (= hist in the epilogue)
-    const int PK = c_in * kg.kx;                     // (ic, input plane) work items
-    const int ylo = max(0, y0 - kg.hy), yhi = min(gy.Y, ye + kg.hy);
-    const int nr = yhi - ylo;                        // input rows read per plane
-    const int NRP = nr + 1;
-    float* acc = smf + t.pad;
-    uint32_t* misc = reinterpret_cast<uint32_t*>(smf + 2 * t.pad + t.ocg * SL);
-    int4* rec = reinterpret_cast<int4*>(misc + 512);   // misc: scan scratch [0, 64), row owners [64, 64 + TY)
-    int* pko = reinterpret_cast<int*>(rec + t.nwg_max);
-    int* pkf = pko + ((PK + 1 + 3) & ~3);
-    uint32_t* rp = reinterpret_cast<uint32_t*>(pkf + ((PK + 1 + 3) & ~3));
-    unsigned char* ring = reinterpret_cast<unsigned char*>(rp + ((PK * (t.TY + 2 * kg.hy + 1) + 3) & ~3));
-    uint32_t* hist = reinterpret_cast<uint32_t*>(ring);   // epilogue only
+    // shared layout: acc [ocg*SL] | spos [cap] | sval [cap] | ioff | iglob | ibase | work | misc |
+    // rpair [ocg*PK] | rec [nwg]
+    float* acc = smf;
+    uint32_t* spos = reinterpret_cast<uint32_t*>(smf + (size_t)t.ocg * SL);
+    float* sval = reinterpret_cast<float*>(spos + kStageCap);
+    int* ioff = reinterpret_cast<int*>(sval + kStageCap);
+    uint32_t* iglob = reinterpret_cast<uint32_t*>(ioff + r4(PK + 1));
+    uint32_t* ibase = iglob + r4(PK + 1);
+    uint32_t* work = ibase + r4(PK + 1);
+    uint32_t* misc = work + r4(kStageCap / 64 + PK + 1);
+    int2* rpair = reinterpret_cast<int2*>(misc + 64);
+    int2* rec = rpair + (size_t)t.ocg * PK;
+    uint32_t* hist = spos;                           // epilogue only
 
     const bool neg0 = *a.guard == 0;                 // -0 accumulation mode (value_guard_kernel)
     const uint32_t marker = neg0 ? kNegZero : kAbsent;
     {
-        const int n4 = (2 * t.pad + t.ocg * SL) / 4;
-        uint4 ab = make_uint4(marker, marker, marker, marker);
+        const int n4 = t.ocg * SL / 4;
+        const uint4 ab = make_uint4(marker, marker, marker, marker);
         for (int i = threadIdx.x; i < n4; i += blockDim.x) reinterpret_cast<uint4*>(smf)[i] = ab;
     }
-    const int* gpko = a.pkoff + (int64_t)blockIdx.y * (PK + 1);
-    for (int i = threadIdx.x; i <= PK; i += blockDim.x) pko[i] = gpko[i];
-    for (int i = threadIdx.x; i < PK; i += blockDim.x) pkf[i] = a.pkfull[(int64_t)blockIdx.y * PK + i];
-
-    // Warp w owns input rows [A_w, B_w) (relative to ylo) and writes into a private region of the
-    // accumulator: input row yrel lands at region row yrel + hy*(2w + 1), so targets (rows
-    // yrel - oy, |oy| <= hy) of different warps never meet; the epilogue merges the copies.
-    const int A_w = (warp * nr) / kFwdWarps, B_w = ((warp + 1) * nr) / kFwdWarps;
-    const int cw = kg.hy * (2 * warp + 1) * ZR;
-    const float invZ = 1.0f / (float)Z;
-    // row pointers of every (ic, input plane), rows ylo..yhi, in one burst
-    for (int q = threadIdx.x; q < PK * NRP; q += blockDim.x) {
-        const int pk = q / NRP, r = q - pk * NRP;
-        const int ic = pk / kg.kx, pl = pk - ic * kg.kx;
-        const int xs = x + pl - kg.hx;
-        rp[q] = (xs >= 0 && xs < gx.X) ? a.xrow[((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo + r] : 0u;
-    }
-    {   // this group's weight rounds (fwd_rounds_kernel), one coalesced copy
-        const int4* grec = a.rec + (int64_t)blockIdx.y * t.nwg_max;
-        const int nrec = gpko[PK];
+    {
+        const int* groff = a.roff + (int64_t)blockIdx.y * (t.ocg * PK + 1);
+        for (int i = threadIdx.x; i < t.ocg * PK; i += blockDim.x) rpair[i] = make_int2(groff[i], groff[i + 1]);
+        const int2* grec = a.rnd + (int64_t)blockIdx.y * t.nwg_max;
+        const int nrec = groff[t.ocg * PK];
         for (int i = threadIdx.x; i < nrec; i += blockDim.x) rec[i] = grec[i];
     }
-    __syncthreads();   // row pointers, tables and rounds in shared memory
-    // ------------------------------------------------------------ accumulate (Alg. 1 inner loops)
-    if (A_w < B_w) {
-        const char* accw = reinterpret_cast<const char*>(acc + cw);
-        unsigned char* ring_w = ring + warp * (kRing * kRingSlotB);
-        if (neg0)
-            fwd_items<true>(gx, kg, a, b, x, A_w, B_w, NRP, ylo, Z, ZR, invZ, lane, rp, pko, pkf, rec, ring_w, accw);
-        else
-            fwd_items<false>(gx, kg, a, b, x, A_w, B_w, NRP, ylo, Z, ZR, invZ, lane, rp, pko, pkf, rec, ring_w, accw);
+    // work items: stored inputs of (ic, plane xs), rows ylo..yhi-1 -> one contiguous key run
+    const int ylo = max(0, y0 - kg.hy), yhi = min(gy.Y, ye + kg.hy);
+    int carry = 0;
+    for (int q0 = 0; q0 < PK; q0 += blockDim.x) {
+        const int q = q0 + threadIdx.x;
+        uint32_t e0 = 0, n = 0, rb = 0;
+        if (q < PK) {
+            const int ic = q / kg.kx, xs = x + (q - ic * kg.kx) - kg.hx;
+            if (xs >= 0 && xs < gx.X) {
+                const int64_t row = ((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo;
+                e0 = a.xrow[row];
+                n = a.xrow[row + (yhi - ylo)] - e0;
+                rb = (uint32_t)((uint64_t)row * (uint64_t)Z);   // low word of the row's first key
+            }
+        }
+        int tot;
+        const int ex = block_excl_scan((int)n, reinterpret_cast<int*>(misc), &tot);
+        if (q < PK) {
+            ioff[q] = carry + ex;
+            iglob[q] = e0;
+            ibase[q] = rb;
+        }
+        carry += tot;
     }
-    __syncthreads();   // accumulator complete; rings free for the histogram
+    if (threadIdx.x == 0) ioff[PK] = carry;
+    const int total = carry;
+    __syncthreads();
+
+    const uint32_t accs = (uint32_t)__cvta_generic_to_shared(acc);
+    const uint32_t safe = (uint32_t)(2 * kg.hy * ZR + t.cz) * 4u;   // interior word of slice 0
+    const float invZ = 1.0f / (float)Z;
+    const uint32_t* xk32 = reinterpret_cast<const uint32_t*>(a.xkeys);   // little-endian low words
+    // accumulator row of input row ylo (input row yi -> row yi - (y0 - 2hy))
+    const int arow0 = ylo - y0 + 2 * kg.hy;
+    for (int f0 = 0; f0 < total; f0 += kStageCap) {
+        const int f1 = min(total, f0 + kStageCap);
+        // ---- stage the chunk: (byte position in a channel slice, value); one warp per item,
+        // coalesced reads of the item's key run
+        for (int pk = warp; pk < PK; pk += kFwdWarps) {
+            const int s0 = max(ioff[pk], f0), s1 = min(ioff[pk + 1], f1);
+            const uint32_t eb = iglob[pk] - (uint32_t)ioff[pk], rb = ibase[pk];
+            for (int f = s0 + lane; f < s1; f += 32) {
+                const uint32_t e = eb + (uint32_t)f;
+                const uint32_t L = xk32[2 * (size_t)e] - rb;   // < 2^32: offset within the run
+                const uint32_t yrel = div_small(L, (uint32_t)Z, invZ);
+                const uint32_t z = L - yrel * (uint32_t)Z;
+                spos[f - f0] = ((yrel + (uint32_t)arow0) * (uint32_t)ZR + z + (uint32_t)t.cz) * 4u;
+                sval[f - f0] = a.xvals[e];
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {   // work list of the chunk: groups of <= 64 entries of one item
+            int wcar = 0;
+            for (int p0 = 0; p0 < PK; p0 += 32) {
+                const int pk = p0 + lane;
+                int s0 = 0, s1 = 0;
+                if (pk < PK) {
+                    s0 = max(ioff[pk], f0) - f0;
+                    s1 = min(ioff[pk + 1], f1) - f0;
+                }
+                const int ng = s1 > s0 ? (s1 - s0 + 63) >> 6 : 0;
+                const int inc = warp_incl_scan(ng);
+                for (int gi = 0; gi < ng; ++gi) {
+                    const int st = s0 + 64 * gi;
+                    work[wcar + inc - ng + gi] = (uint32_t)st | ((uint32_t)min(64, s1 - st) << 12) | ((uint32_t)pk << 19);
+                }
+                wcar += __shfl_sync(kFull, inc, 31);
+            }
+            if (lane == 0) misc[0] = (uint32_t)wcar;
+        }
+        __syncthreads();
+        // ---- accumulate (Alg. 1 inner loops)
+        const int nwork = (int)misc[0];
+        if (warp < nocl) {
+            if (neg0)
+                fwd_items<true>(nwork, lane, accs, safe, work, rpair + warp * PK, rec, spos, sval);
+            else
+                fwd_items<false>(nwork, lane, accs, safe, work, rpair + warp * PK, rec, spos, sval);
+        }
+        __syncthreads();
+    }
 
     // ------------------------------------------------------------------------ epilogue
     // "get non-zero entries" and "add bias to non-zero entries": the tile's slice
@@ -491,45 +401,45 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     // histogram of the top score digit are accumulated for the attention threshold.
     const int nyr = ye - y0;
     const bool do_hist = a.attn != SPC_ATTN_NONE;
-    // output row r has copies in the regions of the warps owning input rows yrel-hy..yrel+hy
-    uint32_t* rowsrc = misc + 64;
-    {
-        const float inv_nr = 1.0f / (float)nr;
-        for (int r = threadIdx.x; r < nyr; r += blockDim.x) {
-            const int yrel = r + (y0 - ylo);
-            const int wlo = owner_of(max(0, yrel - kg.hy), nr, inv_nr), whi = owner_of(min(nr - 1, yrel + kg.hy), nr, inv_nr);
-            rowsrc[r] = (uint32_t)wlo | ((uint32_t)whi << 8);
-        }
-    }
     const uint32_t hist_s = (uint32_t)__cvta_generic_to_shared(hist);
+    uint4* hist4 = reinterpret_cast<uint4*>(hist);
+    constexpr int kHist4 = (kSelBins + 32) / 4;      // bins + one dummy bin per lane
+    if (do_hist)
+        for (int i = threadIdx.x; i < kHist4; i += blockDim.x) hist4[i] = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();
     for (int ocl = 0; ocl < nocl; ++ocl) {
         const int oc = oc0 + ocl;
         const int64_t s = b * c_out + oc;
-        const float bv = a.bias ? a.bias[oc] : 0.0f;
-        const float* S = acc + ocl * SL;
-        if (do_hist)
-            for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) hist[i] = 0;
-        __syncthreads();
+        const float bv = a.bias ? __ldg(&a.bias[oc]) : 0.0f;
+        const float* S = acc + ocl * SL + 2 * kg.hy * ZR + t.cz;
         uint32_t cnt = 0;
         float* P = a.pre + s * gy.V + ((int64_t)x * gy.Y + y0) * Z;
-        const int yoff = y0 - ylo;
         if (a.attn == SPC_ATTN_MAGNITUDE)
-            epi_rows<SPC_ATTN_MAGNITUDE>(S, P, bv, nyr, Z, ZR, warp, lane, hist_s, cnt, yoff, kg.hy, marker, rowsrc);
+            epi_rows<SPC_ATTN_MAGNITUDE>(S, P, bv, nyr, Z, ZR, hist_s, cnt, marker);
         else if (a.attn == SPC_ATTN_RAW)
-            epi_rows<SPC_ATTN_RAW>(S, P, bv, nyr, Z, ZR, warp, lane, hist_s, cnt, yoff, kg.hy, marker, rowsrc);
+            epi_rows<SPC_ATTN_RAW>(S, P, bv, nyr, Z, ZR, hist_s, cnt, marker);
         else
-            epi_rows<SPC_ATTN_NONE>(S, P, bv, nyr, Z, ZR, warp, lane, hist_s, cnt, yoff, kg.hy, marker, rowsrc);
-        if (do_hist) {   // merge the tile histogram; support size = its total
+            epi_rows<SPC_ATTN_NONE>(S, P, bv, nyr, Z, ZR, hist_s, cnt, marker);
+        if (do_hist) {   // merge the tile histogram (support size = its total) and clear it
             __syncthreads();
-            for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) {
-                const uint32_t h = hist[i];
-                cnt += h;
-                if (h) atomicAdd(&a.hist[s * kSelBins + i], h);
+            uint32_t* gh = a.hist + s * kSelBins;
+            for (int i = threadIdx.x; i < kHist4; i += blockDim.x) {
+                const uint4 h = hist4[i];
+                if (h.x | h.y | h.z | h.w) {
+                    hist4[i] = make_uint4(0u, 0u, 0u, 0u);
+                    if (4 * i < kSelBins) {
+                        cnt += h.x + h.y + h.z + h.w;
+                        if (h.x) atomicAdd(gh + 4 * i, h.x);
+                        if (h.y) atomicAdd(gh + 4 * i + 1, h.y);
+                        if (h.z) atomicAdd(gh + 4 * i + 2, h.z);
+                        if (h.w) atomicAdd(gh + 4 * i + 3, h.w);
+                    }
+                }
             }
         }
-        const uint32_t tot = block_sum(cnt, misc);
-        if (threadIdx.x == 0 && tot) atomicAdd(&a.seg_count[s], (unsigned long long)tot);
-        __syncthreads();
+        cnt = warp_sum(cnt);
+        if (lane == 0 && cnt) atomicAdd(&a.seg_count[s], (unsigned long long)cnt);
+        if (do_hist) __syncthreads();
     }
 }
 
@@ -874,8 +784,8 @@ cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& k
     }
     {
         SPC_PHASE("fwd_rounds", s, 1);
-        fwd_rounds_kernel<<<(unsigned)t.n_ocg, 128, 0, s>>>(kg, (int)gx.C, (int)gy.C, t, a.meta2, a.val2, a.off2,
-                                                          a.rec, a.pkoff, a.pkfull, a.guard);
+        fwd_rounds_kernel<<<(unsigned)t.n_ocg, 256, 0, s>>>(kg, (int)gx.C, (int)gy.C, t, a.meta2, a.val2, a.off2,
+                                                          a.rnd, a.roff, a.guard);
     }
     { SPC_PHASE("conv_fwd", s, 1); conv_fwd_kernel<<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a); }
     { SPC_PHASE("fwd_find", s, 1); fwd_find_kernel<<<(unsigned)nseg, 256, 0, s>>>(a, nseg); }

@@ -100,12 +100,14 @@ cudaError_t launch_filter_table(const KGeo& kg, int c_in, int c_out, const uint6
 cudaError_t launch_filter_table_fwd(const KGeo& kg, int c_in, int c_out, const uint64_t* wkeys, const float* wvals,
                                     int64_t nw, int2* meta2, float* val2, int* off2, int* scratch, cudaStream_t s);
 
-// Forward tile: one x-plane, rows [y0, y0+TY) (full Z), a group of ocg output channels. Warp w
-// owns rows [y0 + w*RW, y0 + (w+1)*RW). Tiles of a segment are in key order: ti = x*nty + ty.
+// Forward tile: one x-plane, rows [y0, y0+TY) (full Z), a group of ocg output channels (warp w
+// accumulates channel oc0 + w). Tiles of a segment are in key order: ti = x*nty + ty.
 struct FwdTile {
-    int TY, RW, nty, ocg, n_ocg, ZR, NT;
-    int RT;            // accumulator rows per output channel: TY + 2*hy input rows + 2*hy halo per warp
-    int pad;           // leading float pad of the accumulator (z margin of row 0)
+    int TY, nty, ocg, n_ocg;
+    int ZR;            // accumulator row pitch (floats)
+    int cz;            // accumulator column of z = 0 (>= hz, multiple of 4)
+    int RA;            // accumulator rows per output channel: TY + 4*hy (2*hy margin rows each side)
+    int PK;            // work items (ic, input plane) = c_in * kx
     int nwg_max;       // stored weights of one output-channel group (upper bound = round records)
     size_t smem;
 };
@@ -127,9 +129,8 @@ struct FwdArgs {
     const int2* meta2;
     const float* val2;
     const int* off2;
-    int4* rec;                       // [n_ocg * nwg_max] weight rounds {wdA, wA, wdB, wB} (fwd_rounds)
-    int* pkoff;                      // [n_ocg * (PK + 1)] first round of each (ic, input plane)
-    int* pkfull;                     // [n_ocg * PK] rounds with two channels
+    int2* rnd;                       // [n_ocg * nwg_max] weight rounds {byte offset, w} (fwd_rounds)
+    int* roff;                       // [n_ocg * (ocg * PK + 1)] first round of each (oc, ic, input plane)
     int* guard;                      // set when some |x| or |w| < 2^-50: NaN-marker accumulation
     const float* bias;
     int attn;
