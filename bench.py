@@ -322,18 +322,26 @@ def roofline_for(name, ph, ny, nnz_x, nnz_w, B_local, fwd_macs, bwd_macs, pk, sr
     nseg = B_local * C_OUT
     hbm = float(pk.get("hbm_gbs", 6650.0))
     sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
-    fma_peak = 148 * 128 * sm_mhz * 1e6 / 1e12        # TMAC/s: 148 SMs x 128 FP32 lanes
+    # The scatter convolutions are bound by shared-memory read-modify-writes, not by FFMA issue:
+    # every MAC of Alg. 1 (fwd) reads and writes one 4-byte accumulator word (8 B through the
+    # 128 B/clk/SM shared-memory crossbar, B300_MICROARCH "LDS/STS"), so the peak is 16 MAC/clk/SM.
+    # The backward reads one 4-byte gradient word per (entry, weight) pair it visits (every pair
+    # is visited; 2 MACs are algorithmic only on kept outputs): 32 pair visits/clk/SM on the same
+    # crossbar. DESIGN.md section 7 derives both.
+    lsu_fwd = 148 * 16 * sm_mhz * 1e6 / 1e12
     if name == "conv_fwd":
         return {"kernel": name, "bound": "alu", "achieved": round(fwd_macs / t / 1e12, 4), "unit": "TMAC/s",
-                "peak": round(fma_peak, 2), "frac": round(fwd_macs / t / 1e12 / fma_peak, 5),
-                "traffic": ncu_traffic(name), "peak_source": f"derived: 148 SM x 128 FFMA/clk x {sm_mhz:.0f} MHz",
+                "peak": round(lsu_fwd, 3), "frac": round(fwd_macs / t / 1e12 / lsu_fwd, 4),
+                "traffic": ncu_traffic(name),
+                "peak_source": f"derived: shared-memory RMW rate 148 SM x 128 B/clk / 8 B per MAC x {sm_mhz:.0f} MHz",
                 "algorithmic": f"{fwd_macs} MACs per launch (Eq. (1) pairs)"}
     if name == "conv_bwd":
-        return {"kernel": name, "bound": "alu", "achieved": round(bwd_macs / t / 1e12, 4), "unit": "TMAC/s",
-                "peak": round(fma_peak, 2), "frac": round(bwd_macs / t / 1e12 / fma_peak, 5),
+        lsu_bwd = 148 * 32 * sm_mhz * 1e6 / 1e12   # pair visits/s: one 4-byte G load each
+        return {"kernel": name, "bound": "alu", "achieved": round(fwd_macs / t / 1e12, 4), "unit": "Tpair/s",
+                "peak": round(lsu_bwd, 3), "frac": round(fwd_macs / t / 1e12 / lsu_bwd, 4),
                 "traffic": ncu_traffic(name),
-                "peak_source": f"derived: 148 SM x 128 FFMA/clk x {sm_mhz:.0f} MHz",
-                "algorithmic": f"{bwd_macs} MACs per launch (2 x pairs on kept outputs)"}
+                "peak_source": f"derived: one 4-byte shared gradient load per (entry, weight) pair, 148 SM x 32 lanes/clk x {sm_mhz:.0f} MHz",
+                "algorithmic": f"{fwd_macs} (entry, weight) pairs visited per launch ({bwd_macs} MACs on kept outputs)"}
     per_launch_bytes = {
         "fwd_classify": 4 * nseg * V,
         "fwd_write": 4 * nseg * V + 12 * ny,
