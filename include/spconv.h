@@ -125,6 +125,27 @@ spc_status_t sparse_conv_fwd(const spc_map_t* x, const spc_filter_t* w, const fl
                              spc_attn_t attn, int64_t k, spc_map_out_t* y,
                              void* workspace, size_t workspace_bytes, cudaStream_t stream);
 
+/* Accumulate variants of the forward. Both compute the sum of Alg. 1
+ * and the same structural support, then share the attention stage.
+ *   SCATTER: each stored input times each stored weight, read-modify-write into a shared-memory
+ *            slice of the dense buffer -- work proportional to Eq. (1)'s pairs.
+ *   GEMM:    output-stationary contraction over (filter offset, c_in) on the tensor cores
+ *            (tcgen05 kind::tf32, 3xTF32 split for fp32 accuracy) -- work proportional to the grid;
+ *            for layers whose rows are dense (c_in <= 32, c_out <= 64; more workspace: a dense
+ *            copy of the input, 8*c_in bytes + 4 per voxel).
+ *   AUTO:    the cheaper one by a cost model (sparse_conv_fwd); the Python layer replaces the model
+ *            by a measurement per layer.
+ * Unsupported explicit choices return SPC_ERR_UNSUPPORTED. spc_conv_fwd_variant() reports which
+ * variant a call would run (SPC_VARIANT_SCATTER or SPC_VARIANT_GEMM; 0 on invalid arguments). */
+typedef enum { SPC_VARIANT_AUTO = 0, SPC_VARIANT_SCATTER = 1, SPC_VARIANT_GEMM = 2 } spc_variant_t;
+spc_status_t spc_conv_fwd_query_ex(const spc_map_t* x, const spc_filter_t* w, spc_attn_t attn, int64_t k,
+                                   spc_variant_t variant, int64_t* out_capacity, size_t* workspace_bytes);
+spc_status_t sparse_conv_fwd_ex(const spc_map_t* x, const spc_filter_t* w, const float* bias,
+                                spc_attn_t attn, int64_t k, spc_variant_t variant, spc_map_out_t* y,
+                                void* workspace, size_t workspace_bytes, cudaStream_t stream);
+int spc_conv_fwd_variant(const spc_map_t* x, const spc_filter_t* w, spc_attn_t attn, int64_t k,
+                         spc_variant_t variant);
+
 /* ------------------------------------------------------------------------------------
  * Backward of the convolution, Alg. 2 with the masked rule of Eqs. (3)/(4)
  * (P:121-129): gradients exist only at stored inputs and stored (unpruned) weights.

@@ -15,11 +15,13 @@ STATUS = {
 }
 
 ATTN = {"none": 0, "magnitude": 1, "raw": 2}
+VARIANT = {"auto": 0, "scatter": 1, "gemm": 2}
 
 # every symbol include/spconv.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "spc_version", "spc_status_string",
     "spc_conv_fwd_query", "sparse_conv_fwd",
+    "spc_conv_fwd_query_ex", "sparse_conv_fwd_ex", "spc_conv_fwd_variant",
     "spc_conv_bwd_query", "sparse_conv_bwd", "sparse_conv_bwd_input", "sparse_conv_bwd_weight",
     "spc_topk_query", "attention_topk",
     "spc_relu_query", "sparse_relu",
@@ -74,6 +76,9 @@ def load(path: str = LIB_PATH):
         "spc_status_string": ([C.c_int], C.c_char_p),
         "spc_conv_fwd_query": ([pM, pF, C.c_int, I64, pi64, sz], C.c_int),
         "sparse_conv_fwd": ([pM, pF, P, C.c_int, I64, pO, P, C.c_size_t, P], C.c_int),
+        "spc_conv_fwd_query_ex": ([pM, pF, C.c_int, I64, C.c_int, pi64, sz], C.c_int),
+        "sparse_conv_fwd_ex": ([pM, pF, P, C.c_int, I64, C.c_int, pO, P, C.c_size_t, P], C.c_int),
+        "spc_conv_fwd_variant": ([pM, pF, C.c_int, I64, C.c_int], C.c_int),
         "spc_conv_bwd_query": ([pM, pF, pM, sz], C.c_int),
         "sparse_conv_bwd": ([pM, pF, pM, P, P, P, P, P, C.c_size_t, P], C.c_int),
         "sparse_conv_bwd_input": ([pM, pF, pM, P, P, P, C.c_size_t, P], C.c_int),

@@ -131,6 +131,7 @@ FilterWs carve_filter(Carver& c, const spc_filter_t* w) {
 
 // ----------------------------------------------------------------------- forward
 struct FwdWs {
+    GemmArgs g;        // variant G buffers (null unless the variant is G)
     uint32_t* xrow;
     int2* meta2;
     float* val2;
@@ -140,26 +141,57 @@ struct FwdWs {
     int* flag;
 };
 
-spc_status_t fwd_plan(const spc_map_t* x, const spc_filter_t* w, spc_attn_t attn, int64_t k, Geo* gx, Geo* gy,
-                      KGeo* kg, FwdTile* t, int64_t* cap) {
+// Estimated seconds of the two accumulate variants (AUTO's choice; the Python layer's per-layer
+// autotuner replaces it with a measurement). S: Eq. (1) pairs at the measured scatter rate. G:
+// per 128-voxel tile and filter offset, the larger of the operand gather (shared-memory bytes at
+// 128 B/clk) and the 3xTF32 MMAs (128*N/256 clk per K step), plus the densify traffic.
+double est_scatter_s(const spc_map_t* x, const spc_filter_t* w) {
+    const double pairs = (double)x->nnz * (double)w->nnz / (double)std::max<int64_t>(1, w->c_in);
+    return pairs / 4e11;
+}
+double est_gemm_s(const Geo& gx, const GemmPlan& g) {
+    const double gather = (2.0 * 128 * g.Kp * 4 + 2.0 * g.Np * g.Kp * 4) / 128.0;
+    const double mma = 3.0 * (g.Kp / 8) * (128.0 * g.Np / 256.0);
+    const double tiles = (double)gx.B * (double)g.ntile;
+    return tiles * g.KV * std::max(gather, mma) / (148.0 * 1.9e9) + (double)gx.B * gx.V * g.Kp * 16.0 / 3e12;
+}
+
+spc_status_t fwd_plan(const spc_map_t* x, const spc_filter_t* w, spc_attn_t attn, int64_t k, spc_variant_t variant,
+                      Geo* gx, Geo* gy, KGeo* kg, FwdTile* t, GemmPlan* gp, int64_t* cap, int* use_gemm) {
     SPC_TRY(check_map(x));
     SPC_TRY(check_filter(w, x, kg));
     if (attn != SPC_ATTN_NONE && attn != SPC_ATTN_MAGNITUDE && attn != SPC_ATTN_RAW) return SPC_ERR_INVALID_ARG;
     if (attn != SPC_ATTN_NONE && k < 1) return SPC_ERR_INVALID_ARG;
+    if (variant != SPC_VARIANT_AUTO && variant != SPC_VARIANT_SCATTER && variant != SPC_VARIANT_GEMM)
+        return SPC_ERR_INVALID_ARG;
     *gx = geo_of(x, x->channels);
     *gy = geo_of(x, w->c_out);
     const int64_t per = attn != SPC_ATTN_NONE ? std::min<int64_t>(k, gy->V) : gy->V;
     *cap = x->batch * w->c_out * per;
     *t = plan_fwd_tile(*gy, *kg, (int)w->c_out, (int)w->c_in, w->nnz);
-    if (t->smem == 0) return SPC_ERR_UNSUPPORTED;
+    *gp = plan_gemm(*gx, *gy, *kg);
+    const bool s_ok = t->smem != 0, g_ok = gp->ok != 0;
+    if (variant == SPC_VARIANT_SCATTER) *use_gemm = 0;
+    else if (variant == SPC_VARIANT_GEMM) *use_gemm = 1;
+    else *use_gemm = g_ok && (!s_ok || est_gemm_s(*gx, *gp) < est_scatter_s(x, w));
+    if (*use_gemm ? !g_ok : !s_ok) return SPC_ERR_UNSUPPORTED;
     return SPC_OK;
 }
 
 // Candidate capacity: the threshold bucket of a segment holds at most its whole support, so the
 // worst case is nseg*V entries (binary data with massive ties); typical use is ~1-2% of that.
 FwdWs carve_fwd(Carver& c, const Geo& gx, const Geo& gy, const KGeo& kg, const FwdTile& t, const spc_filter_t* w,
-                spc_attn_t attn) {
+                spc_attn_t attn, const GemmPlan* gp = nullptr) {
     FwdWs ws{};
+    if (gp) {
+        const size_t nvox = (size_t)(gx.B * gx.V);
+        ws.g.xhi = c.take<float>(nvox * gp->Kp);
+        ws.g.xlo = c.take<float>(nvox * gp->Kp);
+        ws.g.occ = c.take<uint32_t>(nvox);
+        ws.g.bhi = c.take<float>((size_t)gp->KV * gp->Np * gp->Kp);
+        ws.g.blo = c.take<float>((size_t)gp->KV * gp->Np * gp->Kp);
+        ws.g.wmask = c.take<uint32_t>((size_t)gp->KV * gp->Np);
+    }
     const int64_t nseg = gy.B * gy.C;
     const size_t KXY = (size_t)kg.kx * kg.ky;
     ws.xrow = c.take<uint32_t>((size_t)(gx.B * gx.C * gx.R + 1));
@@ -365,37 +397,61 @@ const char* spc_status_string(spc_status_t s) {
     return "unknown status";
 }
 
-spc_status_t spc_conv_fwd_query(const spc_map_t* x, const spc_filter_t* w, spc_attn_t attn, int64_t k,
-                                int64_t* out_capacity, size_t* workspace_bytes) {
+spc_status_t spc_conv_fwd_query_ex(const spc_map_t* x, const spc_filter_t* w, spc_attn_t attn, int64_t k,
+                                   spc_variant_t variant, int64_t* out_capacity, size_t* workspace_bytes) {
     Geo gx, gy;
     KGeo kg;
     FwdTile t;
+    GemmPlan gp;
     int64_t cap;
-    SPC_TRY(fwd_plan(x, w, attn, k, &gx, &gy, &kg, &t, &cap));
+    int use_gemm;
+    SPC_TRY(fwd_plan(x, w, attn, k, variant, &gx, &gy, &kg, &t, &gp, &cap, &use_gemm));
     Carver m(nullptr);
-    carve_fwd(m, gx, gy, kg, t, w, attn);
+    carve_fwd(m, gx, gy, kg, t, w, attn, use_gemm ? &gp : nullptr);
     if (out_capacity) *out_capacity = cap;
     if (workspace_bytes) *workspace_bytes = m.used;
     return SPC_OK;
 }
 
-spc_status_t sparse_conv_fwd(const spc_map_t* x, const spc_filter_t* w, const float* bias, spc_attn_t attn, int64_t k,
-                             spc_map_out_t* y, void* workspace, size_t workspace_bytes, cudaStream_t s) {
+spc_status_t spc_conv_fwd_query(const spc_map_t* x, const spc_filter_t* w, spc_attn_t attn, int64_t k,
+                                int64_t* out_capacity, size_t* workspace_bytes) {
+    return spc_conv_fwd_query_ex(x, w, attn, k, SPC_VARIANT_AUTO, out_capacity, workspace_bytes);
+}
+
+int spc_conv_fwd_variant(const spc_map_t* x, const spc_filter_t* w, spc_attn_t attn, int64_t k, spc_variant_t variant) {
     Geo gx, gy;
     KGeo kg;
     FwdTile t;
+    GemmPlan gp;
     int64_t cap;
-    SPC_TRY(fwd_plan(x, w, attn, k, &gx, &gy, &kg, &t, &cap));
+    int use_gemm;
+    if (fwd_plan(x, w, attn, k, variant, &gx, &gy, &kg, &t, &gp, &cap, &use_gemm) != SPC_OK) return 0;
+    return use_gemm ? SPC_VARIANT_GEMM : SPC_VARIANT_SCATTER;
+}
+
+spc_status_t sparse_conv_fwd_ex(const spc_map_t* x, const spc_filter_t* w, const float* bias, spc_attn_t attn,
+                                int64_t k, spc_variant_t variant, spc_map_out_t* y, void* workspace,
+                                size_t workspace_bytes, cudaStream_t s) {
+    Geo gx, gy;
+    KGeo kg;
+    FwdTile t;
+    GemmPlan gp;
+    int64_t cap;
+    int use_gemm;
+    SPC_TRY(fwd_plan(x, w, attn, k, variant, &gx, &gy, &kg, &t, &gp, &cap, &use_gemm));
     SPC_TRY(check_out(y, cap));
+    const GemmPlan* gpp = use_gemm ? &gp : nullptr;
     Carver m(nullptr);
-    carve_fwd(m, gx, gy, kg, t, w, attn);
+    carve_fwd(m, gx, gy, kg, t, w, attn, gpp);
     if (!workspace || workspace_bytes < m.used) return SPC_ERR_WORKSPACE;
     Carver c(workspace);
-    FwdWs ws = carve_fwd(c, gx, gy, kg, t, w, attn);
+    FwdWs ws = carve_fwd(c, gx, gy, kg, t, w, attn, gpp);
     if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
-    SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
-    SPC_TRY(cu(launch_filter_table_fwd(kg, (int)w->c_in, (int)w->c_out, w->keys, w->values, w->nnz, ws.meta2, ws.val2,
-                                       ws.off2, ws.scratch2, s)));
+    if (!use_gemm) {
+        SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
+        SPC_TRY(cu(launch_filter_table_fwd(kg, (int)w->c_in, (int)w->c_out, w->keys, w->values, w->nnz, ws.meta2,
+                                           ws.val2, ws.off2, ws.scratch2, s)));
+    }
     FwdArgs a = ws.a;
     a.xkeys = x->keys;
     a.x_nnz_dev = x->nnz_dev;
@@ -411,7 +467,23 @@ spc_status_t sparse_conv_fwd(const spc_map_t* x, const spc_filter_t* w, const fl
     a.out_keys = y->keys;
     a.out_vals = y->values;
     a.out_nnz = y->nnz_dev;
+    if (use_gemm) {
+        GemmArgs g = ws.g;
+        g.xkeys = x->keys;
+        g.xvals = x->values;
+        g.x_nnz_dev = x->nnz_dev;
+        g.x_nnz = x->nnz;
+        g.wkeys = w->keys;
+        g.wvals = w->values;
+        g.nw = w->nnz;
+        return cu(launch_conv_fwd_pipeline(gx, gy, kg, t, a, s, &gp, &g));
+    }
     return cu(launch_conv_fwd_pipeline(gx, gy, kg, t, a, s));
+}
+
+spc_status_t sparse_conv_fwd(const spc_map_t* x, const spc_filter_t* w, const float* bias, spc_attn_t attn, int64_t k,
+                             spc_map_out_t* y, void* workspace, size_t workspace_bytes, cudaStream_t s) {
+    return sparse_conv_fwd_ex(x, w, bias, attn, k, SPC_VARIANT_AUTO, y, workspace, workspace_bytes, s);
 }
 
 spc_status_t spc_conv_bwd_query(const spc_map_t* x, const spc_filter_t* w, const spc_map_t* y,

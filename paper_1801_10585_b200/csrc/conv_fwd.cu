@@ -764,11 +764,13 @@ __global__ void __launch_bounds__(32 * kWriteWarps) fwd_write_kernel(FwdArgs a, 
 }
 
 cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& kg, const FwdTile& t,
-                                     const FwdArgs& a, cudaStream_t s) {
+                                     const FwdArgs& a, cudaStream_t s, const GemmPlan* gp, const GemmArgs* ga) {
     const int64_t nseg = gy.B * gy.C;
     if (nseg == 0) return cudaMemsetAsync(a.out_nnz, 0, sizeof(int64_t), s);
-    cudaError_t e = cudaFuncSetAttribute(conv_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem);
-    if (e != cudaSuccess) return e;
+    if (!gp) {
+        cudaError_t e = cudaFuncSetAttribute(conv_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem);
+        if (e != cudaSuccess) return e;
+    }
     const size_t segb = sizeof(uint64_t) * (size_t)nseg;
     cudaMemsetAsync(a.seg_count, 0, segb, s);
     cudaMemsetAsync(a.cand_cur, 0, segb, s);
@@ -777,17 +779,22 @@ cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& k
     if (a.attn != SPC_ATTN_NONE) cudaMemsetAsync(a.hist, 0, sizeof(uint32_t) * kSelBins * (size_t)nseg, s);
     const dim3 grid((unsigned)(gy.B * gy.X * t.nty), (unsigned)t.n_ocg);
     const unsigned sgrid = (unsigned)(nseg * a.nchunk);
-    cudaMemsetAsync(a.guard, 0, sizeof(int), s);
-    {
-        SPC_PHASE("value_guard", s, 1);
-        value_guard_kernel<<<148 * 4, 256, 0, s>>>(a.xvals, a.x_nnz_dev, a.x_nnz, a.guard);
+    if (gp) {
+        cudaError_t eg = launch_conv_gemm(gx, gy, kg, *gp, *ga, a, s);
+        if (eg != cudaSuccess) return eg;
+    } else {
+        cudaMemsetAsync(a.guard, 0, sizeof(int), s);
+        {
+            SPC_PHASE("value_guard", s, 1);
+            value_guard_kernel<<<148 * 4, 256, 0, s>>>(a.xvals, a.x_nnz_dev, a.x_nnz, a.guard);
+        }
+        {
+            SPC_PHASE("fwd_rounds", s, 1);
+            fwd_rounds_kernel<<<(unsigned)t.n_ocg, 256, 0, s>>>(kg, (int)gx.C, (int)gy.C, t, a.meta2, a.val2, a.off2,
+                                                              a.rnd, a.roff, a.guard);
+        }
+        { SPC_PHASE("conv_fwd", s, 1); conv_fwd_kernel<<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a); }
     }
-    {
-        SPC_PHASE("fwd_rounds", s, 1);
-        fwd_rounds_kernel<<<(unsigned)t.n_ocg, 256, 0, s>>>(kg, (int)gx.C, (int)gy.C, t, a.meta2, a.val2, a.off2,
-                                                          a.rnd, a.roff, a.guard);
-    }
-    { SPC_PHASE("conv_fwd", s, 1); conv_fwd_kernel<<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a); }
     { SPC_PHASE("fwd_find", s, 1); fwd_find_kernel<<<(unsigned)nseg, 256, 0, s>>>(a, nseg); }
     {
         SPC_PHASE("seg_scan", s, a.attn != SPC_ATTN_NONE ? 2 : 1);

@@ -1,0 +1,346 @@
+// Variant G of the forward accumulate (north star (b)): the same sum as Alg. 1
+// (P:60-67), y[b, oc, p] = sum_{delta, ic} x[b, ic, p + delta - c] * w[oc, ic, delta] (reading R1),
+// computed output-stationary on the 5th-generation tensor cores for layers whose rows are dense
+// enough that a contraction over (delta, ic) is genuine (C3/C5-like channel widths, high density).
+//
+// Per CTA: one tile of 128 consecutive output voxels of one sample (UMMA M = 128, one TMEM lane
+// per voxel) and all output channels (UMMA N = c_out padded to 16). For every filter offset delta
+// with a stored weight, the 128 rows of A = x[b, :, p + delta - c] (K = c_in padded to 8) are
+// gathered with cp.async from a dense, zero-padded copy of the input into shared memory in the
+// canonical K-major layout, B = W_delta is copied likewise, and one elected thread issues
+// tcgen05.mma.kind::tf32 into the TMEM accumulator; the gather of delta + 1 overlaps the MMAs of
+// delta (two stages, released by tcgen05.commit -> mbarrier). fp32 accuracy from TF32 units:
+// every operand is split a = hi + lo (hi = a with the low 13 mantissa bits cleared, exact) and
+// D += A_hi B_hi + A_hi B_lo + A_lo B_hi (3xTF32; the dropped lo*lo term is < 2^-22 relative).
+//
+// The epilogue reads the accumulator with tcgen05.ld, applies the structural support of reading
+// R3 (a voxel is present for oc iff some stored input meets some stored weight of oc: an OR over
+// delta of the input-occupancy masks AND the weight masks), adds the bias on the support
+// and writes the same dense pre-attention buffer as the scatter variant (absent marker off the
+// support), so the attention pipeline that follows is shared. Support and values therefore match
+// variant S exactly in coordinates and within fp32 rounding in value.
+#include "spc_internal.cuh"
+#include "block_scan.cuh"
+
+#include <algorithm>
+
+namespace spc {
+
+constexpr int kGM = 128;        // output voxels per tile = UMMA M = TMEM lanes
+constexpr int kGThreads = 128;  // thread t gathers A row t and owns TMEM lane t in the epilogue
+
+GemmPlan plan_gemm(const Geo& gx, const Geo& gy, const KGeo& kg) {
+    GemmPlan g{};
+    const int c_in = (int)gx.C, c_out = (int)gy.C;
+    if (c_in < 1 || c_in > 32 || c_out < 1 || c_out > 64) return g;   // masks are u32 over ic; N <= 64
+    g.Kp = (c_in + 7) & ~7;
+    g.Np = (c_out + 15) & ~15;
+    g.KV = kg.KV;
+    g.ntile = (gy.V + kGM - 1) / kGM;
+    g.stage_bytes = (size_t)2 * kGM * g.Kp * 4 + (size_t)2 * g.Np * g.Kp * 4;
+    g.smem = 2 * g.stage_bytes + (size_t)g.KV * g.Np * 4 + (size_t)g.KV * 4 + 64;
+    g.tcols = g.Np <= 32 ? 32 : 64;
+    g.ok = g.smem <= 200 * 1024;
+    return g;
+}
+
+// Dense zero-padded copy of the input, split into TF32 hi/lo halves, plus per-voxel occupancy
+// masks over ic (a stored 0.0 is occupied: structural support, reading R3).
+__global__ void gemm_densify_kernel(Geo gx, int Kp, const uint64_t* __restrict__ keys, const float* __restrict__ vals,
+                                    const int64_t* nnz_dev, int64_t bound, float* __restrict__ xhi,
+                                    float* __restrict__ xlo, uint32_t* __restrict__ occ) {
+    const int64_t n = load_n(nnz_dev, bound);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t key = keys[e];
+        const uint64_t seg = key / (uint64_t)gx.V, p = key - seg * (uint64_t)gx.V;
+        const uint64_t b = seg / (uint64_t)gx.C, ic = seg - b * (uint64_t)gx.C;
+        const float v = vals[e];
+        const float hi = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
+        const size_t o = (size_t)(b * (uint64_t)gx.V + p) * (size_t)Kp + (size_t)ic;
+        xhi[o] = hi;
+        xlo[o] = v - hi;
+        atomicOr(&occ[b * (uint64_t)gx.V + p], 1u << ic);
+    }
+}
+
+// element offset of (row, k) in the canonical K-major, no-swizzle UMMA layout of an R-row operand:
+// K steps of 8 (32 B per row), 8-row core-matrix groups of 256 B, two 16-byte K halves 128 B apart
+__host__ __device__ inline int canon(int row, int k, int R) {
+    return (k >> 3) * R * 8 + (row >> 3) * 64 + ((k & 7) >> 2) * 32 + (row & 7) * 4 + (k & 3);
+}
+
+// Filter -> per-offset B_delta (hi/lo, canonical layout, N = oc, K = ic) and weight masks over ic.
+__global__ void gemm_wprep_kernel(KGeo kg, int c_in, int Kp, int Np, const uint64_t* __restrict__ wk,
+                                  const float* __restrict__ wv, int64_t nw, float* __restrict__ bhi,
+                                  float* __restrict__ blo, uint32_t* __restrict__ wmask) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nw; j += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t key = wk[j];
+        const int d = (int)(key % (uint64_t)kg.KV);
+        const uint64_t r = key / (uint64_t)kg.KV;
+        const int ic = (int)(r % (uint64_t)c_in), oc = (int)(r / (uint64_t)c_in);
+        const float v = wv[j];
+        const float hi = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
+        const size_t o = (size_t)d * Np * Kp + canon(oc, ic, Np);
+        bhi[o] = hi;
+        blo[o] = v - hi;
+        atomicOr(&wmask[d * Np + oc], 1u << ic);
+    }
+}
+
+// ------------------------------------------------------------------ tcgen05 / mbarrier helpers
+__device__ __forceinline__ uint64_t umma_sdesc(uint32_t saddr) {
+    // start address >> 4 | LBO (K-half stride 128 B) >> 4 << 16 | SBO (8-row group 256 B) >> 4 << 32 |
+    // version 1 (sm_100) << 46 | layout SWIZZLE_NONE (0) << 61
+    return (uint64_t)((saddr >> 4) & 0x3fffu) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
+           (1ull << 46);
+}
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
+        :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint32_t mbar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT%=;\n\t}\n"
+        :: "r"(mbar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool ok) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__global__ void __launch_bounds__(kGThreads) conv_gemm_kernel(Geo gx, Geo gy, KGeo kg, GemmPlan g, GemmArgs a) {
+    extern __shared__ __align__(1024) unsigned char gsm[];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int64_t b = blockIdx.x / g.ntile;
+    const int64_t p0 = (blockIdx.x - b * g.ntile) * (int64_t)kGM;
+    const int Kp = g.Kp, Np = g.Np, KV = g.KV;
+    const int c_out = (int)gy.C;
+    const size_t A_B = (size_t)kGM * Kp * 4, B_B = (size_t)Np * Kp * 4;
+    uint32_t* wmask = reinterpret_cast<uint32_t*>(gsm + 2 * g.stage_bytes);
+    int* dlist = reinterpret_cast<int*>(wmask + KV * Np);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(gsm + ((2 * g.stage_bytes + (size_t)KV * Np * 4 + (size_t)KV * 4 + 7) & ~(size_t)7));
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 2);
+    __shared__ int s_nd;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(gsm);
+    const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(mbar);
+
+    for (int i = tid; i < KV * Np; i += kGThreads) wmask[i] = a.wmask[i];
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"((uint32_t)__cvta_generic_to_shared(tslot)), "r"((uint32_t)g.tcols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        mbar_init(mb0, 1);
+        mbar_init(mb0 + 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {   // offsets with at least one stored weight (the others contribute nothing)
+        int nd = 0;
+        for (int d = 0; d < KV; ++d) {
+            uint32_t any = 0;
+            for (int oc = 0; oc < Np; ++oc) any |= wmask[d * Np + oc];
+            if (any) dlist[nd++] = d;
+        }
+        s_nd = nd;
+    }
+    const uint32_t tmem = *tslot;
+
+    // this thread's output voxel and its coordinates
+    const int64_t p = p0 + tid;
+    const bool pin = p < gy.V;
+    const int pz = (int)(p % gy.Z), py = (int)((p / gy.Z) % gy.Y), px = (int)(p / ((int64_t)gy.Z * gy.Y));
+    __syncthreads();
+    const int nd = s_nd;
+
+    auto load_stage = [&](int st, int d) {
+        const uint32_t base = sbase + (uint32_t)(st * g.stage_bytes);
+        const int dz = d % kg.kz, dy = (d / kg.kz) % kg.ky, dx = d / (kg.kz * kg.ky);
+        const int qx = px + dx - kg.hx, qy = py + dy - kg.hy, qz = pz + dz - kg.hz;
+        const bool ok = pin && qx >= 0 && qx < gx.X && qy >= 0 && qy < gx.Y && qz >= 0 && qz < gx.Z;
+        const size_t q = ok ? ((size_t)b * gx.V + ((size_t)qx * gx.Y + qy) * gx.Z + qz) * Kp : 0;
+        const uint32_t rowoff = (uint32_t)((tid >> 3) * 256 + (tid & 7) * 16);
+        for (int c = 0; c < Kp / 4; ++c) {   // 16-byte chunks of the row: K step c/2, half c%2
+            const uint32_t off = (uint32_t)((c >> 1) * kGM * 32 + (c & 1) * 128) + rowoff;
+            cp16(base + off, a.xhi + q + 4 * c, ok);
+            cp16(base + (uint32_t)A_B + off, a.xlo + q + 4 * c, ok);
+        }
+        const float* bh = a.bhi + (size_t)d * Np * Kp;
+        const float* bl = a.blo + (size_t)d * Np * Kp;
+        for (int c = tid; c < Np * Kp / 4; c += kGThreads) {
+            cp16(base + (uint32_t)(2 * A_B) + 16u * c, bh + 4 * c, true);
+            cp16(base + (uint32_t)(2 * A_B + B_B) + 16u * c, bl + 4 * c, true);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(Np >> 3) << 17) | ((uint32_t)(kGM >> 4) << 24);
+
+    if (nd > 0) {
+        load_stage(0, dlist[0]);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        for (int it = 0; it < nd; ++it) {
+            const int st = it & 1;
+            if (tid == 0) {
+                tc_fence_after();
+                const uint32_t base = sbase + (uint32_t)(st * g.stage_bytes);
+                const uint32_t Ah = base, Al = base + (uint32_t)A_B;
+                const uint32_t Bh = base + (uint32_t)(2 * A_B), Bl = Bh + (uint32_t)B_B;
+#pragma unroll 1
+                for (int sp = 0; sp < 3; ++sp) {   // hi*hi, hi*lo, lo*hi
+                    const uint32_t A = sp == 2 ? Al : Ah, B = sp == 1 ? Bl : Bh;
+                    for (int ks = 0; ks < Kp / 8; ++ks)
+                        umma_tf32(tmem, umma_sdesc(A + (uint32_t)(ks * kGM * 32)), umma_sdesc(B + (uint32_t)(ks * Np * 32)),
+                                  idesc, (it | sp | ks) != 0);
+                }
+                umma_commit(mb0 + 8u * st);
+            }
+            if (it + 1 < nd) {
+                if (it >= 1) mbar_wait(mb0 + 8u * (st ^ 1), (uint32_t)(((it - 1) >> 1) & 1));   // stage free
+                load_stage(st ^ 1, dlist[it + 1]);
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
+            __syncthreads();
+        }
+        mbar_wait(mb0 + 8u * ((nd - 1) & 1), (uint32_t)(((nd - 1) >> 1) & 1));
+        tc_fence_after();
+    }
+
+    // ---- epilogue: structural support, bias, dense pre-attention buffer
+    uint32_t nbr[27];
+    const bool small = KV <= 27;
+    if (small) {
+        for (int d = 0; d < KV; ++d) {
+            const int dz = d % kg.kz, dy = (d / kg.kz) % kg.ky, dx = d / (kg.kz * kg.ky);
+            const int qx = px + dx - kg.hx, qy = py + dy - kg.hy, qz = pz + dz - kg.hz;
+            const bool ok = pin && qx >= 0 && qx < gx.X && qy >= 0 && qy < gx.Y && qz >= 0 && qz < gx.Z;
+            nbr[d] = ok ? a.occ[(size_t)b * gx.V + ((size_t)qx * gx.Y + qy) * gx.Z + qz] : 0u;
+        }
+    }
+    for (int c0 = 0; c0 < Np; c0 += 16) {
+        float v[16];
+        if (nd > 0) tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+        else
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+        if (!pin) continue;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int oc = c0 + i;
+            if (oc >= c_out) break;
+            uint32_t sup = 0;
+            for (int d = 0; d < KV; ++d) {
+                uint32_t nb;
+                if (small) nb = nbr[d];
+                else {
+                    const int dz = d % kg.kz, dy = (d / kg.kz) % kg.ky, dx = d / (kg.kz * kg.ky);
+                    const int qx = px + dx - kg.hx, qy = py + dy - kg.hy, qz = pz + dz - kg.hz;
+                    const bool ok = qx >= 0 && qx < gx.X && qy >= 0 && qy < gx.Y && qz >= 0 && qz < gx.Z;
+                    nb = ok ? a.occ[(size_t)b * gx.V + ((size_t)qx * gx.Y + qy) * gx.Z + qz] : 0u;
+                }
+                sup |= nb & wmask[d * Np + oc];
+            }
+            const float bv = a.bias ? __ldg(&a.bias[oc]) : 0.0f;
+            a.pre[((size_t)b * c_out + oc) * gy.V + p] = sup ? v[i] + bv : __uint_as_float(kAbsent);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"((uint32_t)g.tcols));
+}
+
+// Support size and score-digit histogram of each (b, oc) buffer (the scatter variant fuses this
+// into its epilogue): one block per slice of a segment, shared-memory histogram.
+__global__ void __launch_bounds__(256) pre_hist_kernel(FwdArgs a, int64_t V, int splits) {
+    __shared__ uint32_t h[kSelBins];
+    __shared__ uint32_t sm[33];
+    const int64_t s = blockIdx.x / splits;
+    const int j = (int)(blockIdx.x - s * splits);
+    const int64_t per = (V + splits - 1) / splits;
+    const int64_t lo = j * per, hi = min(V, lo + per);
+    for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const float* P = a.pre + s * V;
+    uint32_t cnt = 0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const uint32_t bits = __float_as_uint(P[i]);
+        if (bits == kAbsent) continue;
+        ++cnt;
+        if (a.attn != SPC_ATTN_NONE) atomicAdd(&h[score_bits(bits, a.attn) >> 21], 1u);
+    }
+    __syncthreads();
+    if (a.attn != SPC_ATTN_NONE)
+        for (int i = threadIdx.x; i < kSelBins; i += blockDim.x)
+            if (h[i]) atomicAdd(&a.hist[s * kSelBins + i], h[i]);
+    const uint32_t tot = block_sum(cnt, sm);
+    if (threadIdx.x == 0 && tot) atomicAdd(&a.seg_count[s], (unsigned long long)tot);
+}
+
+cudaError_t launch_conv_gemm(const Geo& gx, const Geo& gy, const KGeo& kg, const GemmPlan& g, const GemmArgs& ga,
+                             const FwdArgs& a, cudaStream_t s) {
+    const size_t nvox = (size_t)gx.B * gx.V;
+    cudaMemsetAsync(ga.xhi, 0, nvox * g.Kp * sizeof(float), s);
+    cudaMemsetAsync(ga.xlo, 0, nvox * g.Kp * sizeof(float), s);
+    cudaMemsetAsync(ga.occ, 0, nvox * sizeof(uint32_t), s);
+    cudaMemsetAsync(ga.bhi, 0, (size_t)g.KV * g.Np * g.Kp * sizeof(float), s);
+    cudaMemsetAsync(ga.blo, 0, (size_t)g.KV * g.Np * g.Kp * sizeof(float), s);
+    cudaMemsetAsync(ga.wmask, 0, (size_t)g.KV * g.Np * sizeof(uint32_t), s);
+    {
+        SPC_PHASE("gemm_densify", s, 1);
+        gemm_densify_kernel<<<148 * 8, 256, 0, s>>>(gx, g.Kp, ga.xkeys, ga.xvals, ga.x_nnz_dev, ga.x_nnz, ga.xhi, ga.xlo,
+                                                  ga.occ);
+    }
+    {
+        SPC_PHASE("gemm_wprep", s, 1);
+        gemm_wprep_kernel<<<32, 256, 0, s>>>(kg, (int)gx.C, g.Kp, g.Np, ga.wkeys, ga.wvals, ga.nw, ga.bhi, ga.blo,
+                                             ga.wmask);
+    }
+    cudaError_t e = cudaFuncSetAttribute(conv_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+    if (e != cudaSuccess) return e;
+    {
+        SPC_PHASE("conv_gemm", s, 1);
+        GemmArgs gg = ga;
+        gg.pre = a.pre;
+        gg.bias = a.bias;
+        conv_gemm_kernel<<<(unsigned)(gx.B * g.ntile), kGThreads, g.smem, s>>>(gx, gy, kg, g, gg);
+    }
+    {
+        const int64_t nseg = gy.B * gy.C;
+        const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(256, (4 * 148 + nseg - 1) / nseg));
+        SPC_PHASE("pre_hist", s, 1);
+        pre_hist_kernel<<<(unsigned)(nseg * splits), 256, 0, s>>>(a, gy.V, splits);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace spc

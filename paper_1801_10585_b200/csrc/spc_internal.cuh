@@ -159,8 +159,41 @@ struct FwdArgs {
     float* out_vals;
     int64_t* out_nnz;
 };
+// Variant G of the forward accumulate (conv_gemm.cu): tcgen05 TF32 (3xTF32) implicit GEMM over
+// filter offsets, writing the same dense pre-attention buffer as the scatter kernel.
+struct GemmPlan {
+    int ok;            // 1 if the layer fits the variant (c_in <= 32, c_out <= 64)
+    int Kp, Np, KV;    // K = c_in padded to 8, N = c_out padded to 16, filter offsets
+    int64_t ntile;     // 128-voxel tiles per sample
+    int tcols;         // TMEM columns allocated per CTA
+    size_t stage_bytes, smem;
+};
+struct GemmArgs {
+    const uint64_t* xkeys;
+    const float* xvals;
+    const int64_t* x_nnz_dev;
+    int64_t x_nnz;
+    const uint64_t* wkeys;
+    const float* wvals;
+    int64_t nw;
+    float* xhi;        // [B*V*Kp] dense input, TF32 high part (zero off the support)
+    float* xlo;        // [B*V*Kp] low part
+    uint32_t* occ;     // [B*V] occupancy mask over ic
+    float* bhi;        // [KV*Np*Kp] per-offset B (canonical K-major layout), high part
+    float* blo;        // low part
+    uint32_t* wmask;   // [KV*Np] stored-weight mask over ic
+    const float* bias;
+    float* pre;
+};
+GemmPlan plan_gemm(const Geo& gx, const Geo& gy, const KGeo& kg);
+cudaError_t launch_conv_gemm(const Geo& gx, const Geo& gy, const KGeo& kg, const GemmPlan& g, const GemmArgs& ga,
+                             const FwdArgs& a, cudaStream_t s);
+
+// Forward pipeline: the accumulate stage (scatter variant S, or variant G when `gemm` is given)
+// followed by the shared attention/selection stage.
 cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& kg, const FwdTile& t,
-                                     const FwdArgs& a, cudaStream_t s);
+                                     const FwdArgs& a, cudaStream_t s, const GemmPlan* gp = nullptr,
+                                     const GemmArgs* ga = nullptr);
 
 struct BwdTile {
     int TX, TY, ocg, ntx, nty, n_ocg, grid;

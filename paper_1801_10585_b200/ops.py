@@ -13,7 +13,7 @@ from typing import Optional, Sequence, Tuple
 import torch
 
 from . import _lib
-from ._lib import ATTN, FilterT, MapOutT, MapT, check
+from ._lib import ATTN, VARIANT, FilterT, MapOutT, MapT, check
 
 
 def _stream(stream: Optional[torch.cuda.Stream]):
@@ -149,17 +149,27 @@ def _out(cap: int, device) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor, Ma
 
 class FwdPlan:
     """Queries once, then reuses output and workspace buffers across calls with the same
-    shapes (for timing loops and CUDA-graph capture)."""
+    shapes (for timing loops and CUDA-graph capture).
 
-    def __init__(self, x: SparseMap, w: SparseFilter, attn: str = "magnitude", k: int = 0):
+    variant: "scatter" (S), "gemm" (G, tensor cores), "auto" (the library's cost model) or
+    "measure" (time both once per layer shape and keep the faster: SURVEY §8 a3 "the faster
+    variant is picked per layer from measurement")."""
+
+    def __init__(self, x: SparseMap, w: SparseFilter, attn: str = "magnitude", k: int = 0, variant: str = "auto",
+                 bias: Optional[torch.Tensor] = None):
         lib = load()
         self.attn = ATTN[attn]
         self.k = int(k)
+        if variant == "measure":
+            variant = select_variant(x, w, bias, attn, k)
+        self.variant = VARIANT[variant]
         cap = C.c_int64()
         ws = C.c_size_t()
         xs, fs = x.c_struct(), w.c_struct()
-        check("spc_conv_fwd_query", lib.spc_conv_fwd_query(C.byref(xs), C.byref(fs), self.attn, self.k,
-                                                           C.byref(cap), C.byref(ws)))
+        check("spc_conv_fwd_query_ex", lib.spc_conv_fwd_query_ex(C.byref(xs), C.byref(fs), self.attn, self.k,
+                                                                 self.variant, C.byref(cap), C.byref(ws)))
+        self.resolved = {1: "scatter", 2: "gemm"}.get(
+            lib.spc_conv_fwd_variant(C.byref(xs), C.byref(fs), self.attn, self.k, self.variant), "?")
         dev = x.values.device
         self.capacity = int(cap.value)
         self.ws = _workspace(ws.value, dev)
@@ -170,16 +180,54 @@ class FwdPlan:
     def __call__(self, x: SparseMap, w: SparseFilter, bias: Optional[torch.Tensor] = None,
                  stream: Optional[torch.cuda.Stream] = None) -> SparseMap:
         xs, fs = x.c_struct(), w.c_struct()
-        rc = load().sparse_conv_fwd(C.byref(xs), C.byref(fs), _ptr(bias), self.attn, self.k, C.byref(self.out),
-                                    _ptr(self.ws), self.ws.numel(), _stream(stream))
-        check("sparse_conv_fwd", rc)
+        rc = load().sparse_conv_fwd_ex(C.byref(xs), C.byref(fs), _ptr(bias), self.attn, self.k, self.variant,
+                                       C.byref(self.out), _ptr(self.ws), self.ws.numel(), _stream(stream))
+        check("sparse_conv_fwd_ex", rc)
         return SparseMap(self.keys, self.vals, self.batch, self.c_out, self.dims, self.capacity, self.nnz)
 
 
+_MEASURED = {}
+
+
+def _layer_key(x: SparseMap, w: SparseFilter, attn: str, k: int):
+    return (x.batch, x.channels, tuple(x.dims), w.c_out, tuple(w.ksize), int(w.keys.numel()),
+            int(max(1, x.nnz_bound)).bit_length(), attn, int(k))
+
+
+def select_variant(x: SparseMap, w: SparseFilter, bias=None, attn: str = "magnitude", k: int = 0, reps: int = 3) -> str:
+    """Time the supported accumulate variants on this layer (CUDA events, after one warm-up call)
+    and return the faster; cached per layer shape and input-size bucket."""
+    key = _layer_key(x, w, attn, k)
+    if key in _MEASURED:
+        return _MEASURED[key]
+    lib = load()
+    xs, fs = x.c_struct(), w.c_struct()
+    times = {}
+    for name in ("scatter", "gemm"):
+        cap, wsb = C.c_int64(), C.c_size_t()
+        if lib.spc_conv_fwd_query_ex(C.byref(xs), C.byref(fs), ATTN[attn], int(k), VARIANT[name],
+                                     C.byref(cap), C.byref(wsb)) != 0:
+            continue
+        plan = FwdPlan(x, w, attn, k, name)
+        plan(x, w, bias)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            plan(x, w, bias)
+        b.record()
+        b.synchronize()
+        times[name] = a.elapsed_time(b) / reps
+        del plan
+    choice = min(times, key=times.get) if times else "scatter"
+    _MEASURED[key] = choice
+    return choice
+
+
 def sparse_conv_fwd(x: SparseMap, w: SparseFilter, bias: Optional[torch.Tensor] = None, attn: str = "magnitude",
-                    k: int = 0, stream=None) -> SparseMap:
-    """Alg. 1. attn in {"none", "magnitude", "raw"}; k entries kept per (b, oc)."""
-    return FwdPlan(x, w, attn, k)(x, w, bias, stream)
+                    k: int = 0, stream=None, variant: str = "auto") -> SparseMap:
+    """Alg. 1 (P:51-90). attn in {"none", "magnitude", "raw"}; k entries kept per (b, oc);
+    variant in {"auto", "scatter", "gemm", "measure"} (FwdPlan)."""
+    return FwdPlan(x, w, attn, k, variant, bias)(x, w, bias, stream)
 
 
 class BwdPlan:

@@ -39,9 +39,9 @@ def host_keys(t):
     return host(t).view(np.uint64)
 
 
-def run_fwd(spc, x, w, bias, attn, k):
+def run_fwd(spc, x, w, bias, attn, k, variant="scatter"):
     y = spc.sparse_conv_fwd(dev_map(spc, x), dev_filter(spc, w),
-                            None if bias is None else torch.from_numpy(bias).cuda(), attn, k)
+                            None if bias is None else torch.from_numpy(bias).cuda(), attn, k, variant=variant)
     yk, yv = y.trimmed()
     return host_keys(yk), host(yv), y
 
@@ -98,6 +98,85 @@ def test_fwd_continuous_tolerance(cuda_lib, case, attn):
     common, gi, oi = np.intersect1d(gk, ok_, return_indices=True)
     idx = np.searchsorted(fk, common)
     assert_values_close(gv[gi], ov[oi], fa[idx])
+
+
+# ---------------------------------------------------------------- variant G (tcgen05, 3xTF32)
+GEMM_CASES = FWD_CASES + [
+    # C5-like: 32 -> 32 channels, dense filter, several densities (SURVEY §8 d, C5)
+    ("c5_like_5pct", (10, 12, 32), 2, 32, 32, (3, 3, 3), 0.05, 1.0),
+    ("c5_like_30pct", (6, 8, 32), 1, 32, 32, (3, 3, 3), 0.3, 1.0),
+    ("c3_like_32_64", (8, 8, 24), 1, 32, 64, (3, 3, 3), 0.1, 0.6),
+]
+
+
+@pytest.mark.parametrize("case", GEMM_CASES, ids=lambda c: c[0])
+@pytest.mark.parametrize("attn", ["none", "magnitude"])
+def test_fwd_gemm_dyadic_bit_exact(cuda_lib, case, attn):
+    """Variant G must reproduce the oracle bit for bit on dyadic data (TF32 holds the 7-bit
+    dyadic operands exactly, every partial sum is exact) -- same support, same selection."""
+    spc = cuda_lib
+    _, dims, B, ci, co, ks, rd, rf = case
+    x = uniform_map(B, ci, dims, rd, 3000 + len(dims), values="dyadic")
+    w = sparse_filter(ci, co, ks, rf, 3001, values="dyadic4" if ci >= 16 else "dyadic")
+    bias = bias_vector(co, 3002, values="dyadic")
+    V = int(np.prod(dims))
+    k = max(1, V // 20)
+    ok_, ov, _, _ = ora.conv_fwd(x, w, bias, attn=ATTN_ORA[attn], k=k)
+    gk, gv, _ = run_fwd(spc, x, w, bias, attn, k, variant="gemm")
+    np.testing.assert_array_equal(gk, ok_)
+    np.testing.assert_array_equal(gv, ov)
+
+
+@pytest.mark.parametrize("case", GEMM_CASES, ids=lambda c: c[0])
+def test_fwd_gemm_continuous_tolerance(cuda_lib, case):
+    """Continuous values: 3xTF32 keeps every element within the fp32 tolerance rule."""
+    spc = cuda_lib
+    _, dims, B, ci, co, ks, rd, rf = case
+    x = uniform_map(B, ci, dims, rd, 4000 + len(dims))
+    w = sparse_filter(ci, co, ks, rf, 4001)
+    bias = bias_vector(co, 4002)
+    V = int(np.prod(dims))
+    k = max(1, V // 20)
+    fk, fv, fa, _ = ora.conv_fwd(x, w, bias, with_abs=True)
+    gk, gv, _ = run_fwd(spc, x, w, bias, "none", k, variant="gemm")
+    np.testing.assert_array_equal(gk, fk)
+    assert_values_close(gv, fv, fa)
+    ok_, ov, _, _ = ora.conv_fwd(x, w, bias, attn=ora.ATTN_MAGNITUDE, k=k)
+    gk, gv, _ = run_fwd(spc, x, w, bias, "magnitude", k, variant="gemm")
+    assert_topk_sets_match(gk, gv, ok_, ov, fk, fv, fa, V, k, "magnitude")
+
+
+def test_fwd_variant_measure_and_auto(cuda_lib):
+    """Per-layer variant choice by measurement agrees with both variants' results."""
+    spc = cuda_lib
+    x = uniform_map(1, 16, (8, 8, 32), 0.2, 55, values="dyadic")
+    w = sparse_filter(16, 16, (3, 3, 3), 1.0, 56, values="dyadic4")
+    X, W = dev_map(spc, x), dev_filter(spc, w)
+    k = 100
+    ys = {v: spc.sparse_conv_fwd(X, W, None, "magnitude", k, variant=v).trimmed() for v in ("scatter", "gemm", "auto")}
+    choice = spc.ops.select_variant(X, W, None, "magnitude", k)
+    assert choice in ("scatter", "gemm")
+    ym = spc.sparse_conv_fwd(X, W, None, "magnitude", k, variant="measure").trimmed()
+    for v in list(ys.values()) + [ym]:
+        assert torch.equal(v[0], ys["scatter"][0]) and torch.equal(v[1], ys["scatter"][1])
+
+
+def test_fwd_gemm_empty_and_unsupported(cuda_lib):
+    spc = cuda_lib
+    x = COO(2, 2, (5, 6), np.zeros(0, np.uint64), np.zeros(0, np.float32))
+    w = sparse_filter(2, 3, (3, 3), 0.5, 3)
+    gk, _, _ = run_fwd(spc, x, w, None, "magnitude", 4, variant="gemm")
+    assert gk.size == 0
+    x = uniform_map(2, 2, (5, 6), 0.3, 4)
+    w0 = Filter(2, 3, (3, 3), np.zeros(0, np.uint64), np.zeros(0, np.float32))
+    gk, _, _ = run_fwd(spc, x, w0, None, "none", 0, variant="gemm")
+    assert gk.size == 0
+    x = uniform_map(1, 40, (4, 4, 4), 0.2, 5)          # c_in > 32: G unsupported, explicit request fails
+    w = sparse_filter(40, 4, (3, 3, 3), 0.5, 6)
+    with pytest.raises(spc.SpconvError):
+        run_fwd(spc, x, w, None, "none", 0, variant="gemm")
+    gk, _, _ = run_fwd(spc, x, w, None, "none", 0, variant="auto")   # AUTO falls back to S
+    assert gk.size > 0
 
 
 def test_fwd_mnist_like_c1(cuda_lib):
