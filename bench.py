@@ -183,7 +183,8 @@ def run_ours(args):
     X = spc.SparseMap.from_arrays(x.keys, x.values, x.batch, x.channels, x.dims)
     W = spc.SparseFilter.from_arrays(w.keys, w.values, w.c_in, w.c_out, w.ksize)
     bias_t = torch.from_numpy(bias).cuda()
-    fwd = spc.FwdPlan(X, W, "magnitude", k)
+    fwd = spc.FwdPlan(X, W, "magnitude", k, args.variant, bias_t)
+    args.resolved_variant = fwd.resolved
     cap = fwd.capacity
     dy_t = torch.from_numpy(grad_values(cap, SEED_BASE + 7 + rank)).cuda()
     Y0 = fwd(X, W, bias_t)
@@ -289,6 +290,7 @@ def run_ours(args):
                             f"fwd + bwd(dx,dw,dbias)",
                 "global_batch": BATCH,
                 "density": args.density,
+                "fwd_variant": f"{args.variant} -> {args.resolved_variant}",
                 "parallelism": f"dp{world}",
                 "l2": "flushed between timed steps (512 MB write); inputs also exceed L2",
             },
@@ -382,7 +384,7 @@ def run_e2e(torch, spc, x, w, bias, k, cap, dy_dev, args, world, dist):
     W = spc.SparseFilter.from_arrays(w.keys, w.values, w.c_in, w.c_out, w.ksize)
     bias_t = torch.from_numpy(bias).cuda()
     X = spc.SparseMap(dk, dv, x.batch, x.channels, x.dims, x.nnz, None)
-    fwd = spc.FwdPlan(X, W, "magnitude", k)
+    fwd = spc.FwdPlan(X, W, "magnitude", k, args.resolved_variant)
     dk.copy_(hk)
     dv.copy_(hv)
     Y0 = fwd(X, W, bias_t)
@@ -501,6 +503,8 @@ def main(argv=None):
     ap.add_argument("--values", default="continuous", choices=["continuous", "dyadic"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--variant", default="measure", choices=["auto", "scatter", "gemm", "measure"],
+                    help="forward accumulate variant (SURVEY §8 a3); 'measure' times both once and keeps the faster")
     args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference(args)
