@@ -55,8 +55,11 @@ FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_
     const int ZR = (int)r4((size_t)cz + gy.Z + kg.hz);
     const int PK = c_in * kg.kx;
     auto nwg = [&](int ocg) { return std::min<int64_t>(nw_total, (int64_t)ocg * c_in * kg.KV); };
+    // round records live in shared memory when small; large filter banks (e.g. 32 x 32 x 27) are
+    // read through L1 instead of being copied into every CTA
+    auto rec_sm = [&](int ocg) { return nwg(ocg) * 8 <= 16 * 1024; };
     auto need = [&](int ocg, int TY) {
-        return fwd_fixed_smem(PK, ocg, nwg(ocg)) + (size_t)ocg * (TY + 4 * kg.hy) * ZR * sizeof(float);
+        return fwd_fixed_smem(PK, ocg, rec_sm(ocg) ? nwg(ocg) : 0) + (size_t)ocg * (TY + 4 * kg.hy) * ZR * sizeof(float);
     };
     if (PK >= (1 << 13)) { t.smem = 0; return t; }                 // work descriptors hold 13-bit items
     int ocg = std::min(c_out, kFwdWarps);
@@ -75,6 +78,7 @@ FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_
     t.RA = t.TY + 4 * kg.hy;
     t.PK = PK;
     t.nwg_max = (int)nwg(ocg);
+    t.rec_smem = rec_sm(ocg) ? 1 : 0;
     t.smem = need(ocg, t.TY);
     return t;
 }
@@ -268,6 +272,7 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
 // plus halo, are contiguous key runs (row index); they are staged once per CTA as (byte position,
 // value) and shared by all warps. Warp w owns output channel oc0 + w: no two warps write the
 // same word, no atomics, and a fixed order makes the result deterministic.
+template <bool REC_SMEM>
 __global__ void __launch_bounds__(kFwdThreads, 2)
 conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     extern __shared__ __align__(16) float smf[];
@@ -296,6 +301,7 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     uint32_t* misc = work + r4(kStageCap / 64 + PK + 1);
     int2* rpair = reinterpret_cast<int2*>(misc + 64);
     int2* rec = rpair + (size_t)t.ocg * PK;
+    const int2* recp = REC_SMEM ? rec : a.rnd + (int64_t)blockIdx.y * t.nwg_max;
     uint32_t* hist = spos;                           // epilogue only
 
     const bool neg0 = *a.guard == 0;                 // -0 accumulation mode (value_guard_kernel)
@@ -310,7 +316,8 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
         for (int i = threadIdx.x; i < t.ocg * PK; i += blockDim.x) rpair[i] = make_int2(groff[i], groff[i + 1]);
         const int2* grec = a.rnd + (int64_t)blockIdx.y * t.nwg_max;
         const int nrec = groff[t.ocg * PK];
-        for (int i = threadIdx.x; i < nrec; i += blockDim.x) rec[i] = grec[i];
+        if (REC_SMEM)
+            for (int i = threadIdx.x; i < nrec; i += blockDim.x) rec[i] = grec[i];
     }
     // work items: stored inputs of (ic, plane xs), rows ylo..yhi-1 -> one contiguous key run
     const int ylo = max(0, y0 - kg.hy), yhi = min(gy.Y, ye + kg.hy);
@@ -387,9 +394,9 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
         const int nwork = (int)misc[0];
         if (warp < nocl) {
             if (neg0)
-                fwd_items<true>(nwork, lane, accs, safe, work, rpair + warp * PK, rec, spos, sval);
+                fwd_items<true>(nwork, lane, accs, safe, work, rpair + warp * PK, recp, spos, sval);
             else
-                fwd_items<false>(nwork, lane, accs, safe, work, rpair + warp * PK, rec, spos, sval);
+                fwd_items<false>(nwork, lane, accs, safe, work, rpair + warp * PK, recp, spos, sval);
         }
         __syncthreads();
     }
@@ -768,7 +775,9 @@ cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& k
     const int64_t nseg = gy.B * gy.C;
     if (nseg == 0) return cudaMemsetAsync(a.out_nnz, 0, sizeof(int64_t), s);
     if (!gp) {
-        cudaError_t e = cudaFuncSetAttribute(conv_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem);
+        cudaError_t e = t.rec_smem
+            ? cudaFuncSetAttribute(conv_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem)
+            : cudaFuncSetAttribute(conv_fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem);
         if (e != cudaSuccess) return e;
     }
     const size_t segb = sizeof(uint64_t) * (size_t)nseg;
@@ -793,7 +802,11 @@ cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& k
             fwd_rounds_kernel<<<(unsigned)t.n_ocg, 256, 0, s>>>(kg, (int)gx.C, (int)gy.C, t, a.meta2, a.val2, a.off2,
                                                               a.rnd, a.roff, a.guard);
         }
-        { SPC_PHASE("conv_fwd", s, 1); conv_fwd_kernel<<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a); }
+        {
+            SPC_PHASE("conv_fwd", s, 1);
+            if (t.rec_smem) conv_fwd_kernel<true><<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a);
+            else conv_fwd_kernel<false><<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a);
+        }
     }
     { SPC_PHASE("fwd_find", s, 1); fwd_find_kernel<<<(unsigned)nseg, 256, 0, s>>>(a, nseg); }
     {

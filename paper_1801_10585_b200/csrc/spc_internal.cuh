@@ -109,6 +109,7 @@ struct FwdTile {
     int RA;            // accumulator rows per output channel: TY + 4*hy (2*hy margin rows each side)
     int PK;            // work items (ic, input plane) = c_in * kx
     int nwg_max;       // stored weights of one output-channel group (upper bound = round records)
+    int rec_smem;      // 1: round records copied to shared memory; 0: read through L1
     size_t smem;
 };
 FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_t nw_total);
