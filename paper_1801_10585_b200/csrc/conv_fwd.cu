@@ -46,7 +46,7 @@ __host__ __device__ inline size_t r4(size_t n) { return (n + 3) & ~(size_t)3; }
 // entry, row base), round offsets and round records of the group, scratch
 static size_t fwd_fixed_smem(int PK, int ocg, int64_t nwg) {
     return (size_t)kStageCap * 8 + 4 * (3 * r4(PK + 1) + r4(kStageCap / 64 + PK + 1) + 64) +
-           8 * ((size_t)ocg * PK + (size_t)nwg) + 64;
+           8 * ((size_t)ocg * PK + (size_t)nwg + 1) + 64;
 }
 
 FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_t nw_total) {
@@ -243,23 +243,27 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
         if (n > 32) {
             const uint32_t aB = accs + (okB ? spos[s + 32 + lane] : safe);
             const float vB = okB ? sval[s + 32 + lane] : 0.0f;
+            int2 q = rec[rr.x];
 #pragma unroll 2
             for (int r = rr.x; r < rr.y; ++r) {
-                const int2 q = rec[r];
+                const int2 qn = rec[r + 1];   // next record in flight during this round (rec has a spare slot)
                 const uint32_t qa = aA + (uint32_t)q.x, qb = aB + (uint32_t)q.x;
                 const float w = __int_as_float(q.y);
                 const float oa = lds_u(qa), ob = lds_u(qb);
                 sts_p(qa, upd<NEG0>(oa, vA, w), okA);
                 sts_p(qb, upd<NEG0>(ob, vB, w), okB);
                 __syncwarp();
+                q = qn;
             }
         } else {
+            int2 q = rec[rr.x];
 #pragma unroll 2
             for (int r = rr.x; r < rr.y; ++r) {
-                const int2 q = rec[r];
+                const int2 qn = rec[r + 1];
                 const uint32_t qa = aA + (uint32_t)q.x;
                 sts_p(qa, upd<NEG0>(lds_u(qa), vA, __int_as_float(q.y)), okA);
                 __syncwarp();
+                q = qn;
             }
         }
     }

@@ -8,8 +8,8 @@
 // with a stored weight, the 128 rows of A = x[b, :, p + delta - c] (K = c_in padded to 8) are
 // gathered with cp.async from a dense, zero-padded copy of the input into shared memory in the
 // canonical K-major layout, B = W_delta is copied likewise, and one elected thread issues
-// tcgen05.mma.kind::tf32 into the TMEM accumulator; the gather of delta + 1 overlaps the MMAs of
-// delta (two stages, released by tcgen05.commit -> mbarrier). fp32 accuracy from TF32 units:
+// tcgen05.mma.kind::tf32 into the TMEM accumulator; the gathers of the next offsets overlap the
+// MMAs of delta (up to 4 shared-memory stages; full/empty mbarriers, released by tcgen05.commit). fp32 accuracy from TF32 units:
 // every operand is split a = hi + lo (hi = a with the low 13 mantissa bits cleared, exact) and
 // D += A_hi B_hi + A_hi B_lo + A_lo B_hi (3xTF32; the dropped lo*lo term is < 2^-22 relative).
 //
@@ -23,11 +23,13 @@
 #include "block_scan.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace spc {
 
 constexpr int kGM = 128;        // output voxels per tile = UMMA M = TMEM lanes
 constexpr int kGThreads = 128;  // thread t gathers A row t and owns TMEM lane t in the epilogue
+constexpr int kGMaxStages = 4;  // operand stages in flight (gathers run kGMaxStages - 1 offsets ahead)
 
 GemmPlan plan_gemm(const Geo& gx, const Geo& gy, const KGeo& kg) {
     GemmPlan g{};
@@ -38,9 +40,13 @@ GemmPlan plan_gemm(const Geo& gx, const Geo& gy, const KGeo& kg) {
     g.KV = kg.KV;
     g.ntile = (gy.V + kGM - 1) / kGM;
     g.stage_bytes = (size_t)2 * kGM * g.Kp * 4 + (size_t)2 * g.Np * g.Kp * 4;
-    g.smem = 2 * g.stage_bytes + (size_t)g.KV * g.Np * 4 + (size_t)g.KV * 4 + 64;
+    const size_t extra = (size_t)g.KV * g.Np * 4 + (size_t)g.KV * 8 + 128;
+    int want = 2;   // two stages keep two CTAs (8 warps of gatherers) per SM for the 32-channel layers
+    if (const char* e = getenv("SPC_GEMM_STAGES")) want = std::max(2, std::min(kGMaxStages, atoi(e)));
+    g.stages = (int)std::min<size_t>((size_t)want, (200 * 1024 - extra) / g.stage_bytes);
+    g.smem = g.stages * g.stage_bytes + extra;
     g.tcols = g.Np <= 32 ? 32 : 64;
-    g.ok = g.smem <= 200 * 1024;
+    g.ok = g.stages >= 2;
     return g;
 }
 
@@ -50,10 +56,16 @@ __global__ void gemm_densify_kernel(Geo gx, int Kp, const uint64_t* __restrict__
                                     const int64_t* nnz_dev, int64_t bound, float* __restrict__ xhi,
                                     float* __restrict__ xlo, uint32_t* __restrict__ occ) {
     const int64_t n = load_n(nnz_dev, bound);
+    const double invV = 1.0 / (double)gx.V;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t key = keys[e];
-        const uint64_t seg = key / (uint64_t)gx.V, p = key - seg * (uint64_t)gx.V;
-        const uint64_t b = seg / (uint64_t)gx.C, ic = seg - b * (uint64_t)gx.C;
+        // key / V through a double reciprocal (exact after one correction each way; keys < 2^53)
+        uint64_t seg = (uint64_t)((double)key * invV);
+        if (seg * (uint64_t)gx.V > key) --seg;
+        if ((seg + 1) * (uint64_t)gx.V <= key) ++seg;
+        const uint64_t p = key - seg * (uint64_t)gx.V;
+        const uint32_t s32 = (uint32_t)seg, C32 = (uint32_t)gx.C;   // b*C + ic < 2^32 (checked by the API)
+        const uint64_t b = s32 / C32, ic = s32 - (uint32_t)b * C32;
         const float v = vals[e];
         const float hi = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
         const size_t o = (size_t)(b * (uint64_t)gx.V + p) * (size_t)Kp + (size_t)ic;
@@ -115,6 +127,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
         "@!P1 bra WAIT%=;\n\t}\n"
         :: "r"(mbar), "r"(parity) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(mbar) : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool ok) {
@@ -140,10 +155,12 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_kernel(Geo gx, Geo gy, KG
     const int Kp = g.Kp, Np = g.Np, KV = g.KV;
     const int c_out = (int)gy.C;
     const size_t A_B = (size_t)kGM * Kp * 4, B_B = (size_t)Np * Kp * 4;
-    uint32_t* wmask = reinterpret_cast<uint32_t*>(gsm + 2 * g.stage_bytes);
+    const int S = g.stages;
+    uint32_t* wmask = reinterpret_cast<uint32_t*>(gsm + S * g.stage_bytes);
     int* dlist = reinterpret_cast<int*>(wmask + KV * Np);
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(gsm + ((2 * g.stage_bytes + (size_t)KV * Np * 4 + (size_t)KV * 4 + 7) & ~(size_t)7));
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 2);
+    // mbarriers: full[S] (all gatherers arrived) then empty[S] (MMAs of the stage retired)
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(gsm + ((S * g.stage_bytes + (size_t)KV * Np * 4 + (size_t)KV * 8 + 7) & ~(size_t)7));
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 2 * kGMaxStages);
     __shared__ int s_nd;
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(gsm);
     const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(mbar);
@@ -155,8 +172,10 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_kernel(Geo gx, Geo gy, KG
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
-        mbar_init(mb0, 1);
-        mbar_init(mb0 + 8, 1);
+        for (int i = 0; i < S; ++i) {
+            mbar_init(mb0 + 8u * i, kGThreads);            // full[i]
+            mbar_init(mb0 + 8u * (S + i), 1);              // empty[i]
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tc_fence_before();
@@ -165,9 +184,13 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_kernel(Geo gx, Geo gy, KG
     if (tid == 0) {   // offsets with at least one stored weight (the others contribute nothing)
         int nd = 0;
         for (int d = 0; d < KV; ++d) {
-            uint32_t any = 0;
-            for (int oc = 0; oc < Np; ++oc) any |= wmask[d * Np + oc];
+            uint32_t any = 0, uni = 1;
+            for (int oc = 0; oc < c_out; ++oc) {
+                any |= wmask[d * Np + oc];
+                uni &= (uint32_t)(wmask[d * Np + oc] == wmask[d * Np]);
+            }
             if (any) dlist[nd++] = d;
+            dlist[KV + d] = (int)uni;   // same ic mask for every oc at this offset
         }
         s_nd = nd;
     }
@@ -202,14 +225,26 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_kernel(Geo gx, Geo gy, KG
     };
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(Np >> 3) << 17) | ((uint32_t)(kGM >> 4) << 24);
 
+    // Pipeline over the offsets: every thread gathers its A rows (and a share of B) for offset
+    // it + S - 1 while the tensor cores work on offset it. full[st] completes when all 128
+    // gatherers' cp.async groups for the stage have landed (each waits for its own group, makes
+    // it visible to the async proxy, then arrives); empty[st] completes when tcgen05.commit
+    // retires the stage's MMAs, after which the stage may be overwritten.
     if (nd > 0) {
-        load_stage(0, dlist[0]);
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
+        for (int j = 0; j < S - 1; ++j) {
+            if (j < nd) load_stage(j, dlist[j]);
+            else asm volatile("cp.async.commit_group;" ::: "memory");
+        }
         for (int it = 0; it < nd; ++it) {
-            const int st = it & 1;
+            const int st = it % S;
+            // this thread's group for offset it has landed (younger groups may stay in flight)
+            if (S >= 4) asm volatile("cp.async.wait_group 2;" ::: "memory");
+            else if (S == 3) asm volatile("cp.async.wait_group 1;" ::: "memory");
+            else asm volatile("cp.async.wait_group 0;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(mb0 + 8u * st);
             if (tid == 0) {
+                mbar_wait(mb0 + 8u * st, (uint32_t)((it / S) & 1));
                 tc_fence_after();
                 const uint32_t base = sbase + (uint32_t)(st * g.stage_bytes);
                 const uint32_t Ah = base, Al = base + (uint32_t)A_B;
@@ -221,31 +256,43 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_kernel(Geo gx, Geo gy, KG
                         umma_tf32(tmem, umma_sdesc(A + (uint32_t)(ks * kGM * 32)), umma_sdesc(B + (uint32_t)(ks * Np * 32)),
                                   idesc, (it | sp | ks) != 0);
                 }
-                umma_commit(mb0 + 8u * st);
+                umma_commit(mb0 + 8u * (S + st));
             }
-            if (it + 1 < nd) {
-                if (it >= 1) mbar_wait(mb0 + 8u * (st ^ 1), (uint32_t)(((it - 1) >> 1) & 1));   // stage free
-                load_stage(st ^ 1, dlist[it + 1]);
-                asm volatile("cp.async.wait_all;" ::: "memory");
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            // gather offset it + S - 1 into the slot of offset it - 1 once its MMAs retired
+            const int nx = it + S - 1;
+            if (nx < nd) {
+                if (it >= 1) mbar_wait(mb0 + 8u * (S + (it - 1) % S), (uint32_t)(((it - 1) / S) & 1));
+                load_stage(nx % S, dlist[nx]);
+            } else {
+                asm volatile("cp.async.commit_group;" ::: "memory");
             }
-            __syncthreads();
         }
-        mbar_wait(mb0 + 8u * ((nd - 1) & 1), (uint32_t)(((nd - 1) >> 1) & 1));
+        mbar_wait(mb0 + 8u * (S + (nd - 1) % S), (uint32_t)(((nd - 1) / S) & 1));
         tc_fence_after();
     }
 
     // ---- epilogue: structural support, bias, dense pre-attention buffer
-    uint32_t nbr[27];
-    const bool small = KV <= 27;
-    if (small) {
+    // supm bit oc <=> some stored input at p + delta - c meets a stored weight (oc, ic, delta):
+    // offsets whose weight masks agree for every oc (dense or uniformly pruned filters) need one
+    // test for all channels
+    uint64_t supm = 0;
+    const uint64_t allm = c_out >= 64 ? ~0ull : ((1ull << c_out) - 1ull);
+    if (pin)
         for (int d = 0; d < KV; ++d) {
             const int dz = d % kg.kz, dy = (d / kg.kz) % kg.ky, dx = d / (kg.kz * kg.ky);
             const int qx = px + dx - kg.hx, qy = py + dy - kg.hy, qz = pz + dz - kg.hz;
-            const bool ok = pin && qx >= 0 && qx < gx.X && qy >= 0 && qy < gx.Y && qz >= 0 && qz < gx.Z;
-            nbr[d] = ok ? a.occ[(size_t)b * gx.V + ((size_t)qx * gx.Y + qy) * gx.Z + qz] : 0u;
+            if (qx < 0 || qx >= gx.X || qy < 0 || qy >= gx.Y || qz < 0 || qz >= gx.Z) continue;
+            const uint32_t nb = a.occ[(size_t)b * gx.V + ((size_t)qx * gx.Y + qy) * gx.Z + qz];
+            if (!nb) continue;
+            const uint32_t m0 = wmask[d * Np];
+            if (dlist[KV + d]) {
+                if (nb & m0) supm = allm;
+            } else {
+                for (int oc = 0; oc < c_out; ++oc)
+                    if (nb & wmask[d * Np + oc]) supm |= 1ull << oc;
+            }
+            if (supm == allm) break;
         }
-    }
     for (int c0 = 0; c0 < Np; c0 += 16) {
         float v[16];
         if (nd > 0) tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
@@ -257,18 +304,7 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_kernel(Geo gx, Geo gy, KG
         for (int i = 0; i < 16; ++i) {
             const int oc = c0 + i;
             if (oc >= c_out) break;
-            uint32_t sup = 0;
-            for (int d = 0; d < KV; ++d) {
-                uint32_t nb;
-                if (small) nb = nbr[d];
-                else {
-                    const int dz = d % kg.kz, dy = (d / kg.kz) % kg.ky, dx = d / (kg.kz * kg.ky);
-                    const int qx = px + dx - kg.hx, qy = py + dy - kg.hy, qz = pz + dz - kg.hz;
-                    const bool ok = qx >= 0 && qx < gx.X && qy >= 0 && qy < gx.Y && qz >= 0 && qz < gx.Z;
-                    nb = ok ? a.occ[(size_t)b * gx.V + ((size_t)qx * gx.Y + qy) * gx.Z + qz] : 0u;
-                }
-                sup |= nb & wmask[d * Np + oc];
-            }
+            const bool sup = (supm >> oc) & 1ull;
             const float bv = a.bias ? __ldg(&a.bias[oc]) : 0.0f;
             a.pre[((size_t)b * c_out + oc) * gy.V + p] = sup ? v[i] + bv : __uint_as_float(kAbsent);
         }

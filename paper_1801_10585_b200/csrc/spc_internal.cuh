@@ -167,6 +167,7 @@ struct GemmPlan {
     int Kp, Np, KV;    // K = c_in padded to 8, N = c_out padded to 16, filter offsets
     int64_t ntile;     // 128-voxel tiles per sample
     int tcols;         // TMEM columns allocated per CTA
+    int stages;        // operand stages in shared memory
     size_t stage_bytes, smem;
 };
 struct GemmArgs {
