@@ -14,6 +14,9 @@ from .oracle import (  # noqa: F401
     decode_key,
     encode_key,
     get_update_id,
+    density_bias,
+    adagrad_step,
+    prune,
     ATTN_NONE,
     ATTN_MAGNITUDE,
     ATTN_RAW,

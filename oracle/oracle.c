@@ -472,3 +472,53 @@ int ora_scatter_grad(int64_t ny, const int64_t* src, const float* dy, int64_t nx
     }
     return 0;
 }
+
+/* ----------------------------------------------------------- training-loop steps
+ * Adaptive density regularisation, §3.5, Eq. (6): the regulariser becomes
+ * sum (w + b)^2 with b = o + b1*(rho - rho_up) when rho > rho_up ("exceeds available
+ * resources"), and b = -b2*(rho_up - rho) when rho <= rho_up ("not using available resources"). */
+double ora_density_bias(double rho, double rho_up, double o, double b1, double b2) {
+    if (rho > rho_up) return o + b1 * (rho - rho_up);
+    return -b2 * (rho_up - rho);
+}
+
+/* One optimiser step over the stored weights (§4: "stochastic gradient descent with the adagrad
+ * optimizer"), with the regulariser's gradient lambda * d/dw (w + b)^2 = 2 lambda (w + b) added to
+ * the data gradient (§3.5). Per weight, in double precision:
+ *   g   = dw + 2 lambda (w + b)
+ *   a   = acc + g^2                 (accumulator += grad^2)
+ *   w' = w - lr g / (sqrt(a) + eps)
+ * then w' and a are stored as fp32. Pruned weights are not stored, so they never move. */
+int ora_adagrad_step(int64_t n, float* w, const float* dw, float* acc, double b, double lambda, double lr,
+                     double eps) {
+    if (n < 0) return -1;
+    for (int64_t i = 0; i < n; ++i) {
+        double g = (double)dw[i] + 2.0 * lambda * ((double)w[i] + b);
+        double a = (double)acc[i] + g * g;
+        double wn = (double)w[i] - lr * g / (sqrt(a) + eps);
+        acc[i] = (float)a;
+        w[i] = (float)wn;
+    }
+    return 0;
+}
+
+/* One-warning-shot pruning at the end of an epoch, §3.6: a stored weight with
+ * |w| < eps that was already flagged at the previous epoch end is pruned -- removed from the
+ * filter ("zero" = not stored), so it never reappears; |w| < eps without the flag sets
+ * the flag (the warning shot); |w| >= eps clears it. Keys, values, accumulators and flags are
+ * compacted together in key order. Returns the new count (>= 0) or -1. */
+int64_t ora_prune(int64_t n, const uint64_t* keys, const float* w, const float* acc, const uint8_t* warn,
+                  double eps, uint64_t* okeys, float* ow, float* oacc, uint8_t* owarn) {
+    if (n < 0) return -1;
+    int64_t m = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int small = fabs((double)w[i]) < eps;
+        if (small && warn[i]) continue;           /* second consecutive low observation: prune */
+        okeys[m] = keys[i];
+        ow[m] = w[i];
+        oacc[m] = acc[i];
+        owarn[m] = (uint8_t)(small ? 1 : 0);       /* warning shot set, or cleared */
+        ++m;
+    }
+    return m;
+}

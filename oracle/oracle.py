@@ -48,6 +48,12 @@ def _load():
         _lib.ora_encode_key.argtypes = [C.c_int, P, I64, P]
         _lib.ora_encode_key.restype = C.c_uint64
         _lib.ora_get_update_id.argtypes = [C.c_int, P, P, P, P, P]
+        _lib.ora_density_bias.argtypes = [C.c_double] * 5
+        _lib.ora_density_bias.restype = C.c_double
+        _lib.ora_adagrad_step.argtypes = [I64, P, P, P, C.c_double, C.c_double, C.c_double, C.c_double]
+        _lib.ora_adagrad_step.restype = C.c_int
+        _lib.ora_prune.argtypes = [I64, P, P, P, P, C.c_double, P, P, P, P]
+        _lib.ora_prune.restype = C.c_int64
         for f in ("ora_conv_fwd", "ora_conv_bwd", "ora_topk", "ora_relu", "ora_maxpool",
                   "ora_scatter_grad", "ora_decode_key", "ora_get_update_id"):
             getattr(_lib, f).restype = C.c_int
@@ -192,3 +198,36 @@ def scatter_grad(src, dy, nx: int):
     dx = np.zeros(max(1, nx), np.float32)
     _check(_load().ora_scatter_grad(s.shape[0], _p(s), _p(g), nx, _p(dx)), "ora_scatter_grad")
     return dx[:nx]
+
+
+# ------------------------------------------------------------------ training-loop steps (f1)
+def density_bias(rho: float, rho_up: float, o: float = 0.1, b1: float = 0.1, b2: float = 0.1) -> float:
+    """Eq. (6) (P:177-181)."""
+    return float(_load().ora_density_bias(rho, rho_up, o, b1, b2))
+
+
+def adagrad_step(w, dw, acc, b: float, lam: float, lr: float, eps: float):
+    """One Adagrad step with the density regulariser (§3.5, §4); returns new (w, acc) as fp32."""
+    w = np.ascontiguousarray(w, np.float32).copy()
+    acc = np.ascontiguousarray(acc, np.float32).copy()
+    dw = np.ascontiguousarray(dw, np.float32)
+    rc = _load().ora_adagrad_step(w.size, w.ctypes.data, dw.ctypes.data, acc.ctypes.data, b, lam, lr, eps)
+    if rc != 0:
+        raise OracleError(f"ora_adagrad_step rc={rc}")
+    return w, acc
+
+
+def prune(keys, w, acc, warn, eps: float = 0.01):
+    """One-warning-shot pruning (§3.6); returns compacted (keys, w, acc, warn)."""
+    keys = np.ascontiguousarray(keys, np.uint64)
+    w = np.ascontiguousarray(w, np.float32)
+    acc = np.ascontiguousarray(acc, np.float32)
+    warn = np.ascontiguousarray(warn, np.uint8)
+    n = keys.size
+    ok, ow, oa, owr = (np.zeros(max(n, 1), np.uint64), np.zeros(max(n, 1), np.float32),
+                       np.zeros(max(n, 1), np.float32), np.zeros(max(n, 1), np.uint8))
+    m = _load().ora_prune(n, keys.ctypes.data, w.ctypes.data, acc.ctypes.data, warn.ctypes.data, eps,
+                          ok.ctypes.data, ow.ctypes.data, oa.ctypes.data, owr.ctypes.data)
+    if m < 0:
+        raise OracleError("ora_prune failed")
+    return ok[:m], ow[:m], oa[:m], owr[:m]

@@ -407,3 +407,98 @@ def test_mnist_like_density_matches_paper():
     """thresholded MNIST has mean density 0.23."""
     m = mnist_like(400, 5)
     assert abs(m.nnz / 400 / 784 - 0.23) < 0.02
+
+
+# ------------------------------------------------------------ training-loop steps (SURVEY §8 f1)
+@pytest.mark.parametrize("ex", GOLD["density_bias"], ids=lambda e: e["cite"][:24])
+def test_density_bias_golden(ex):
+    b = ora.density_bias(ex["rho"], ex["rho_up"], ex["o"], ex["b1"], ex["b2"])
+    assert abs(b - ex["b"]) < 1e-12
+
+
+def test_density_bias_eq6_shape():
+    """Eq. (6): continuous from below at rho_up (b -> 0), a jump of o just above it, slopes b1
+    above and b2 below (finite differences), positive iff rho > rho_up."""
+    o, b1, b2, up = 0.1, 0.3, 0.2, 0.15
+    eps = 1e-7
+    assert abs(ora.density_bias(up, up, o, b1, b2)) < 1e-15
+    assert abs(ora.density_bias(up + eps, up, o, b1, b2) - o) < 1e-6
+    for r in (0.3, 0.6):
+        assert abs((ora.density_bias(r + 1e-4, up, o, b1, b2) - ora.density_bias(r, up, o, b1, b2)) / 1e-4 - b1) < 1e-9
+    for r in (0.01, 0.1):
+        assert abs((ora.density_bias(r + 1e-4, up, o, b1, b2) - ora.density_bias(r, up, o, b1, b2)) / 1e-4 - b2) < 1e-9
+    assert ora.density_bias(0.2, up, o, b1, b2) > 0 > ora.density_bias(0.1, up, o, b1, b2)
+
+
+@pytest.mark.parametrize("ex", GOLD["regularizer_grad"], ids=lambda e: e["cite"][:24])
+def test_regularizer_grad_golden(ex):
+    """From a zero accumulator with no data gradient, one step stores acc = g^2 with g the
+    regulariser gradient 2*lambda*(w + b), and moves w against its sign."""
+    w0 = np.array([ex["w"]], np.float32)
+    w1, acc = ora.adagrad_step(w0, np.zeros(1, np.float32), np.zeros(1, np.float32), ex["b"], ex["lambda"],
+                               0.01, 1e-8)
+    assert abs(float(acc[0]) - np.float32(ex["grad"]) ** 2) <= 2e-7 * max(ex["grad"] ** 2, 1e-30)
+    if ex["grad"] == 0.0:
+        assert acc[0] == 0.0 and w1[0] == w0[0]
+    else:
+        assert np.sign(w0[0] - w1[0]) == np.sign(ex["grad"])
+
+
+def test_adagrad_constant_gradient_closed_form():
+    """Constant gradient g for T steps: acc_T = T g^2 and w_T = w_0 - lr * sum_t g / (sqrt(t)|g| + eps)
+    (the Adagrad recurrence solved in closed form), per weight; zero gradient leaves both alone."""
+    rng = np.random.default_rng(7)
+    n, T, lr, eps = 64, 40, 0.05, 1e-6
+    w0 = rng.uniform(-1, 1, n).astype(np.float32)
+    g = rng.uniform(-2, 2, n).astype(np.float32)
+    g[:4] = 0.0
+    w, acc = w0.copy(), np.zeros(n, np.float32)
+    for _ in range(T):
+        w, acc = ora.adagrad_step(w, g, acc, 0.0, 0.0, lr, eps)
+    gd = g.astype(np.float64)
+    t = np.arange(1, T + 1, dtype=np.float64)[:, None]
+    w_closed = w0.astype(np.float64) - lr * np.sum(gd[None, :] / (np.sqrt(t) * np.abs(gd)[None, :] + eps), axis=0)
+    np.testing.assert_allclose(acc, T * gd * gd, rtol=T * 1.2e-7, atol=0)
+    np.testing.assert_allclose(w, w_closed, rtol=0, atol=T * 2e-7)
+    assert np.array_equal(w[:4], w0[:4]) and np.all(acc[:4] == 0)
+
+
+def _run_epochs(values, eps):
+    """One weight observed at successive epoch ends; returns the epoch (1-based) it got pruned."""
+    keys = np.array([5], np.uint64)
+    acc = np.zeros(1, np.float32)
+    warn = np.zeros(1, np.uint8)
+    for ep, v in enumerate(values, start=1):
+        keys, w, acc, warn = ora.prune(keys, np.array([v], np.float32)[: keys.size], acc, warn, eps)
+        if keys.size == 0:
+            return ep
+    return None
+
+
+@pytest.mark.parametrize("ex", GOLD["prune"], ids=lambda e: e["cite"][:24])
+def test_prune_golden(ex):
+    assert _run_epochs(ex["epochs"], ex["eps"]) == ex["pruned_after_epoch"]
+
+
+def test_prune_monotone_and_ordered():
+    """Pruning only removes (the count never grows: 'every pruning reduces the number of non-zero
+    weights'), keeps key order, and a weight is never removed at its first low observation."""
+    rng = np.random.default_rng(3)
+    n = 500
+    keys = np.sort(rng.choice(10_000, n, replace=False)).astype(np.uint64)
+    acc = rng.uniform(0, 1, n).astype(np.float32)
+    warn = np.zeros(n, np.uint8)
+    first_low = {}
+    prev = n
+    for ep in range(6):
+        w = rng.normal(0, 0.02, keys.size).astype(np.float32)
+        for k, v in zip(keys.tolist(), w.tolist()):
+            if abs(v) < 0.01:
+                first_low.setdefault(k, ep)
+        nk, nw, na, nwr = ora.prune(keys, w, acc, warn, 0.01)
+        assert nk.size <= prev and np.all(np.diff(nk.astype(np.int64)) > 0)
+        assert np.isin(nk, keys).all()
+        removed = np.setdiff1d(keys, nk)
+        for k in removed.tolist():
+            assert first_low[k] < ep
+        prev, keys, acc, warn = nk.size, nk, na, nwr
