@@ -218,6 +218,43 @@ spc_status_t sparse_scatter_grad(const int64_t* src_index, const float* dy, int6
                                  cudaStream_t stream);
 
 /* ------------------------------------------------------------------------------------
+ * Training-loop steps over a sparse filter bank. Elementwise over the STORED
+ * weights only: pruned weights are absent and therefore never move or reappear.
+ *
+ * sparse_adagrad_step — §4 "stochastic gradient descent with the adagrad optimizer" with the
+ *   adaptive density regulariser of §3.5: the regulariser sum (w + b)^2 adds
+ *   2*lambda*(w + b) to the data gradient, with Eq. (6)
+ *     b = o + b1*(rho - rho_up)   if rho > rho_up   ("exceeds available resources")
+ *     b = -b2*(rho_up - rho)      otherwise          ("not using available resources")
+ *   and rho = *y_nnz_dev / y_cells, the measured density of the layer's output (device word of
+ *   the forward, so no host synchronisation). Per parameter, in double precision:
+ *     g = grad + 2 lambda (w + b);  a = accum + g^2;  w -= lr g / (sqrt(a) + eps);  accum = a.
+ *   params/grad/accum: device float [n] (params and accum updated in place); reg: host struct or
+ *   NULL (no regulariser; then y_nnz_dev may be NULL). Errors: n < 0, null arrays with n > 0,
+ *   reg given without y_nnz_dev or y_cells <= 0 -> SPC_ERR_INVALID_ARG.
+ *
+ * sparse_filter_prune — one-warning-shot pruning at an epoch end, §3.6: a stored
+ *   weight with |w| < eps whose warning flag is set is removed; |w| < eps otherwise sets the flag
+ *   (the warning shot); |w| >= eps clears it. keys/values/accum/warn (device, [n]; accum may be
+ *   NULL) are compacted together in key order into the out_* arrays (capacity n); the new count
+ *   goes to *out_nnz_dev. The paper's eps is 0.01 (Appendix B). Workspace: spc_prune_query.
+ * ------------------------------------------------------------------------------------ */
+typedef struct {
+    double lambda;   /* regularisation scale (the paper sweeps 0 .. 0.3, §4.3)            */
+    double rho_up;   /* upper density bound implied by the k-selection                    */
+    double o, b1, b2;/* Eq. (6) control parameters (>= 0; the paper uses 0.1 each)        */
+} spc_density_reg_t;
+spc_status_t sparse_adagrad_step(float* params, const float* grad, float* accum, int64_t n,
+                                 const int64_t* y_nnz_dev, double y_cells, const spc_density_reg_t* reg,
+                                 double lr, double eps, cudaStream_t stream);
+spc_status_t spc_prune_query(int64_t n, size_t* workspace_bytes);
+spc_status_t sparse_filter_prune(const uint64_t* keys, const float* values, const float* accum,
+                                 const uint8_t* warn, int64_t n, double eps, uint64_t* out_keys,
+                                 float* out_values, float* out_accum, uint8_t* out_warn,
+                                 int64_t* out_nnz_dev, void* workspace, size_t workspace_bytes,
+                                 cudaStream_t stream);
+
+/* ------------------------------------------------------------------------------------
  * Instrumentation (measurement only; not part of the method).
  *   spc_kernel_launches: monotonically increasing count of kernels this library launched
  *   (process-wide).

@@ -22,6 +22,10 @@ from .ops import (  # noqa: F401
     sparse_relu,
     sparse_maxpool,
     sparse_scatter_grad,
+    select_variant,
+    DensityReg,
+    adagrad_step,
+    filter_prune,
     kernel_launches,
     profile_enable,
     profile_reset,

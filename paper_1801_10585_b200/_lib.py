@@ -27,6 +27,7 @@ EXPORTS = [
     "spc_relu_query", "sparse_relu",
     "spc_maxpool_query", "sparse_maxpool",
     "sparse_scatter_grad",
+    "sparse_adagrad_step", "spc_prune_query", "sparse_filter_prune",
     "spc_kernel_launches", "spc_profile_enable", "spc_profile_reset", "spc_profile_read",
 ]
 
@@ -44,6 +45,11 @@ class MapOutT(C.Structure):
 class FilterT(C.Structure):
     _fields_ = [("ndim", C.c_int32), ("c_in", C.c_int64), ("c_out", C.c_int64),
                 ("ksize", C.c_int64 * MAX_NDIM), ("nnz", C.c_int64), ("keys", C.c_void_p), ("values", C.c_void_p)]
+
+
+class DensityRegT(C.Structure):
+    _fields_ = [("lambda_", C.c_double), ("rho_up", C.c_double), ("o", C.c_double), ("b1", C.c_double),
+                ("b2", C.c_double)]
 
 
 class SpconvError(RuntimeError):
@@ -90,6 +96,10 @@ def load(path: str = LIB_PATH):
         "spc_maxpool_query": ([pM, P, pi64, sz], C.c_int),
         "sparse_maxpool": ([pM, P, pO, P, P, C.c_size_t, P], C.c_int),
         "sparse_scatter_grad": ([P, P, I64, P, P, I64, P], C.c_int),
+        "sparse_adagrad_step": ([P, P, P, I64, P, C.c_double, C.POINTER(DensityRegT), C.c_double, C.c_double, P],
+                                C.c_int),
+        "spc_prune_query": ([I64, sz], C.c_int),
+        "sparse_filter_prune": ([P, P, P, P, I64, C.c_double, P, P, P, P, P, P, C.c_size_t, P], C.c_int),
         "spc_kernel_launches": ([], C.c_int64),
         "spc_profile_enable": ([C.c_int], C.c_int),
         "spc_profile_reset": ([], C.c_int),

@@ -616,3 +616,30 @@ spc_status_t sparse_scatter_grad(const int64_t* src_index, const float* dy, int6
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ training-loop steps (f1)
+spc_status_t sparse_adagrad_step(float* params, const float* grad, float* accum, int64_t n, const int64_t* y_nnz_dev,
+                                 double y_cells, const spc_density_reg_t* reg, double lr, double eps, cudaStream_t s) {
+    if (n < 0 || (n > 0 && (!params || !grad || !accum))) return SPC_ERR_INVALID_ARG;
+    if (reg && (!y_nnz_dev || !(y_cells > 0.0))) return SPC_ERR_INVALID_ARG;
+    DensityReg r{};
+    if (reg) r = DensityReg{reg->lambda, reg->rho_up, reg->o, reg->b1, reg->b2};
+    return cu(launch_adagrad(params, grad, accum, n, y_nnz_dev, y_cells, r, reg != nullptr, lr, eps, s));
+}
+
+spc_status_t spc_prune_query(int64_t n, size_t* workspace_bytes) {
+    if (n < 0) return SPC_ERR_INVALID_ARG;
+    if (workspace_bytes) *workspace_bytes = prune_ws_words(n) * sizeof(uint64_t);
+    return SPC_OK;
+}
+
+spc_status_t sparse_filter_prune(const uint64_t* keys, const float* values, const float* accum, const uint8_t* warn,
+                                 int64_t n, double eps, uint64_t* out_keys, float* out_values, float* out_accum,
+                                 uint8_t* out_warn, int64_t* out_nnz_dev, void* ws, size_t ws_bytes, cudaStream_t s) {
+    if (n < 0 || !out_nnz_dev) return SPC_ERR_INVALID_ARG;
+    if (n > 0 && (!keys || !values || !warn || !out_keys || !out_values || !out_warn)) return SPC_ERR_INVALID_ARG;
+    if ((accum == nullptr) != (out_accum == nullptr)) return SPC_ERR_INVALID_ARG;
+    if (!ws || ws_bytes < prune_ws_words(n) * sizeof(uint64_t)) return SPC_ERR_WORKSPACE;
+    return cu(launch_prune(keys, values, accum, warn, n, eps, out_keys, out_values, out_accum, out_warn, out_nnz_dev,
+                           static_cast<uint64_t*>(ws), s));
+}

@@ -273,6 +273,17 @@ size_t scan_tmp_words(int64_t n);
 cudaError_t launch_scan_u32(const uint32_t* in, uint64_t* out, int64_t n, int64_t* total, uint64_t* tmp,
                             cudaStream_t s);
 
+// ------------------------------------------------------------- training-loop steps (train.cu)
+struct DensityReg {
+    double lambda, rho_up, o, b1, b2;
+};
+cudaError_t launch_adagrad(float* w, const float* g, float* acc, int64_t n, const int64_t* y_nnz_dev, double y_cells,
+                           const DensityReg& reg, bool has_reg, double lr, double eps, cudaStream_t s);
+size_t prune_ws_words(int64_t n);
+cudaError_t launch_prune(const uint64_t* keys, const float* w, const float* acc, const uint8_t* warn, int64_t n,
+                         double eps, uint64_t* ok, float* ow, float* oacc, uint8_t* owarn, int64_t* out_nnz,
+                         uint64_t* ws, cudaStream_t s);
+
 // Validation (SPC_VALIDATE=1): flag = 1 if keys are not strictly increasing or out of range.
 cudaError_t launch_validate(const uint64_t* keys, const int64_t* nnz_dev, int64_t nbound, uint64_t limit,
                             int* flag, cudaStream_t s);

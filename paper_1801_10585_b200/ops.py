@@ -13,7 +13,7 @@ from typing import Optional, Sequence, Tuple
 import torch
 
 from . import _lib
-from ._lib import ATTN, VARIANT, FilterT, MapOutT, MapT, check
+from ._lib import ATTN, VARIANT, DensityRegT, FilterT, MapOutT, MapT, check
 
 
 def _stream(stream: Optional[torch.cuda.Stream]):
@@ -361,3 +361,55 @@ def profile_read():
     k = load().spc_profile_read(names, 8192, ms.ctypes.data_as(C.c_void_p), cnt.ctypes.data_as(C.c_void_p), n)
     labels = names.raw.split(b"\0")[:k]
     return {lab.decode(): (float(ms[i]), int(cnt[i])) for i, lab in enumerate(labels)}
+
+
+# ------------------------------------------------------------------ training-loop steps (f1)
+@dataclass
+class DensityReg:
+    """Eq. (6) parameters of the adaptive density regulariser (§3.5); the paper uses 0.1 each."""
+
+    lam: float
+    rho_up: float
+    o: float = 0.1
+    b1: float = 0.1
+    b2: float = 0.1
+
+
+def adagrad_step(params: torch.Tensor, grad: torch.Tensor, accum: torch.Tensor, lr: float, eps: float = 1e-8,
+                 reg: Optional[DensityReg] = None, y: Optional[SparseMap] = None, stream=None) -> None:
+    """In-place Adagrad step over stored parameters (§4) with the density regulariser (§3.5); the
+    layer density is y's device count over its cells (no host sync). sparse_adagrad_step."""
+    n = int(params.numel())
+    r = None
+    ynnz, cells = None, 0.0
+    if reg is not None:
+        if y is None or y.nnz_dev is None:
+            raise ValueError("the density regulariser needs the layer output y with a device count")
+        r = DensityRegT(reg.lam, reg.rho_up, reg.o, reg.b1, reg.b2)
+        ynnz, cells = C.c_void_p(y.nnz_dev.data_ptr()), float(y.batch * y.channels * y.volume)
+    rc = load().sparse_adagrad_step(_ptr(params), _ptr(grad), _ptr(accum), n, ynnz, cells,
+                                    C.byref(r) if r is not None else None, float(lr), float(eps), _stream(stream))
+    check("sparse_adagrad_step", rc)
+
+
+def filter_prune(w: SparseFilter, accum: Optional[torch.Tensor], warn: torch.Tensor, eps: float = 0.01,
+                 stream=None) -> Tuple[SparseFilter, Optional[torch.Tensor], torch.Tensor]:
+    """One-warning-shot pruning at an epoch end (§3.6): returns the compacted filter, its
+    Adagrad accumulators and warning flags (synchronises once to learn the new count)."""
+    lib = load()
+    n = int(w.keys.numel())
+    wsb = C.c_size_t()
+    check("spc_prune_query", lib.spc_prune_query(n, C.byref(wsb)))
+    dev = w.values.device
+    ws = _workspace(wsb.value, dev)
+    ok = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    ov = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+    oa = torch.empty(max(n, 1), dtype=torch.float32, device=dev) if accum is not None else None
+    ow = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    nnz = torch.zeros(1, dtype=torch.int64, device=dev)
+    rc = lib.sparse_filter_prune(_ptr(w.keys), _ptr(w.values), _ptr(accum), _ptr(warn), n, float(eps), _ptr(ok),
+                                 _ptr(ov), _ptr(oa), _ptr(ow), _ptr(nnz), _ptr(ws), ws.numel(), _stream(stream))
+    check("sparse_filter_prune", rc)
+    m = int(nnz.item())
+    wf = SparseFilter(ok[:m].clone(), ov[:m].clone(), w.c_in, w.c_out, w.ksize)
+    return wf, (oa[:m].clone() if oa is not None else None), ow[:m].clone()

@@ -479,3 +479,58 @@ def test_c4_full_size_sampled(cuda_lib):
         odx, _, _, _, _ = ora.conv_bwd(xs, w, ok_, dy[lo:hi])
         xlo, xhi = np.searchsorted(x.keys, np.uint64(b) * span), np.searchsorted(x.keys, np.uint64(b + 1) * span)
         np.testing.assert_array_equal(gdx[xlo:xhi], odx)
+
+
+# ------------------------------------------------------------ training-loop steps
+def test_adagrad_step_bit_exact(cuda_lib):
+    """The GPU step performs the oracle's sequence of IEEE double operations: bit-identical, with
+    and without the density regulariser (rho from the forward output's device count)."""
+    spc = cuda_lib
+    x = uniform_map(2, 3, (12, 12, 12), 0.05, 901)
+    w = sparse_filter(3, 4, (3, 3, 3), 0.5, 902)
+    X, W = dev_map(spc, x), dev_filter(spc, w)
+    k = 40
+    Y = spc.sparse_conv_fwd(X, W, None, "magnitude", k)
+    nnz_y = Y.nnz()
+    rng = np.random.default_rng(903)
+    n = w.values.size
+    dw = rng.normal(0, 0.3, n).astype(np.float32)
+    acc0 = rng.uniform(0, 0.5, n).astype(np.float32)
+    cells = 2 * 4 * 12 ** 3
+    for reg in (None, spc.DensityReg(lam=0.2, rho_up=0.01), spc.DensityReg(lam=0.1, rho_up=0.5, o=0.1, b1=0.3, b2=0.2)):
+        p = W.values.clone()
+        a = torch.from_numpy(acc0).cuda()
+        spc.adagrad_step(p, torch.from_numpy(dw).cuda(), a, lr=0.05, eps=1e-8, reg=reg, y=Y)
+        b = 0.0 if reg is None else ora.density_bias(nnz_y / cells, reg.rho_up, reg.o, reg.b1, reg.b2)
+        ow, oa = ora.adagrad_step(w.values, dw, acc0, b, 0.0 if reg is None else reg.lam, 0.05, 1e-8)
+        np.testing.assert_array_equal(host(p), ow)
+        np.testing.assert_array_equal(host(a), oa)
+
+
+def test_filter_prune_bit_exact_over_epochs(cuda_lib):
+    """Pruning over several epoch ends (weights shrinking towards 0) matches the oracle exactly,
+    and the pruned filter still convolves like the oracle (pruned weights are simply absent)."""
+    spc = cuda_lib
+    w = sparse_filter(4, 4, (3, 3, 3), 1.0, 911)
+    W = dev_filter(spc, w)
+    keys, vals = w.keys.copy(), w.values.copy()
+    acc = np.random.default_rng(912).uniform(0, 1, vals.size).astype(np.float32)
+    warn = np.zeros(vals.size, np.uint8)
+    A, WR = torch.from_numpy(acc).cuda(), torch.zeros(vals.size, dtype=torch.uint8, device="cuda")
+    rng = np.random.default_rng(913)
+    for ep in range(5):
+        vals = (vals * rng.uniform(0.2, 1.2, vals.size)).astype(np.float32)
+        W = spc.SparseFilter(W.keys, torch.from_numpy(vals).cuda(), W.c_in, W.c_out, W.ksize)
+        W, A, WR = spc.filter_prune(W, A, WR, 0.05)
+        keys, vals, acc, warn = ora.prune(keys, vals, acc, warn, 0.05)
+        np.testing.assert_array_equal(host_keys(W.keys), keys)
+        np.testing.assert_array_equal(host(W.values), vals)
+        np.testing.assert_array_equal(host(A), acc)
+        np.testing.assert_array_equal(host(WR), warn)
+    assert keys.size < w.keys.size
+    x = uniform_map(1, 4, (10, 10, 10), 0.1, 914)
+    wp = Filter(4, 4, (3, 3, 3), keys, vals)
+    fk, fv, fa, _ = ora.conv_fwd(x, wp, None, with_abs=True)
+    gk, gv, _ = run_fwd(spc, x, wp, None, "none", 0)
+    np.testing.assert_array_equal(gk, fk)
+    assert_values_close(gv, fv, fa)
