@@ -6,57 +6,62 @@
 namespace spc {
 
 // ---------------------------------------------------------------------------- row index
-// row_ptr[r] = first entry whose key >= r*Z, for r in [0, total_rows]. One thread per entry
-// owns the gap of rows between its predecessor's row and its own row; a warp fills the gaps of
-// its 32 lanes cooperatively so that long empty stretches do not serialise on one thread.
-// key / Z for keys < 2^52: double reciprocal, then an exact integer correction
-__device__ __forceinline__ int64_t row_of(uint64_t key, int64_t Z, double invZ) {
-    int64_t q = (int64_t)((double)key * invZ);
-    int64_t r = (int64_t)key - q * Z;
-    while (r < 0) { --q; r += Z; }
-    while (r >= Z) { ++q; r -= Z; }
-    return q;
+// row_ptr[r] = first entry whose key >= r*Z, for r in [0, total_rows]. Each thread takes 8
+// consecutive entries and fills, for each, the gap of rows between its predecessor's row and its
+// own; long empty stretches are filled by the whole warp so they do not serialise on one thread.
+// key / Z by a 64-bit multiply-high with a host-computed reciprocal and one exact correction.
+constexpr int kRiItems = 8;
+
+__device__ __forceinline__ int64_t row_of(uint64_t key, uint64_t Z, uint64_t magic) {
+    uint64_t q = __umul64hi(key, magic);   // floor(key / Z) or one less
+    if ((q + 1) * Z <= key) ++q;
+    return (int64_t)q;
 }
 
-__global__ void row_index_kernel(int Z, const uint64_t* __restrict__ keys, const int64_t* nnz_dev,
-                                 int64_t nbound, uint32_t* __restrict__ row_ptr, int64_t total_rows) {
+__global__ void __launch_bounds__(256) row_index_kernel(uint64_t Z, uint64_t magic, const uint64_t* __restrict__ keys,
+                                                        const int64_t* nnz_dev, int64_t nbound,
+                                                        uint32_t* __restrict__ row_ptr, int64_t total_rows) {
     const int64_t n = load_n(nnz_dev, nbound);
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRiItems;
     const int lane = threadIdx.x & 31;
-    const double invZ = 1.0 / (double)Z;
-    int64_t lo = 0, hi = -1;
-    if (i < n) {
-        const int64_t r = row_of(keys[i], Z, invZ);
-        const int64_t rp = (i == 0) ? -1 : row_of(keys[i - 1], Z, invZ);
-        lo = rp + 1;
-        hi = r < total_rows ? r : total_rows;
-    } else if (i == n) {
-        const int64_t rl = (n == 0) ? -1 : row_of(keys[n - 1], Z, invZ);
-        lo = rl + 1;
-        hi = total_rows;
-    }
-    // short gaps (the common case): the owning thread fills them; long ones: the whole warp
-    const bool longgap = hi - lo >= 16;
-    if (!longgap)
-        for (int64_t r = lo; r <= hi; ++r) row_ptr[r] = (uint32_t)i;
-    unsigned m = __ballot_sync(kFull, longgap);
-    while (m) {
-        const int src = __ffs(m) - 1;
-        m &= m - 1;
-        const int64_t l = __shfl_sync(kFull, lo, src);
-        const int64_t h = __shfl_sync(kFull, hi, src);
-        const int64_t v = __shfl_sync(kFull, i, src);
-        for (int64_t r = l + lane; r <= h; r += 32) row_ptr[r] = (uint32_t)v;
+    int64_t prev = (i0 == 0 || i0 > n) ? -1 : row_of(keys[i0 - 1], Z, magic);
+#pragma unroll
+    for (int u = 0; u < kRiItems; ++u) {
+        const int64_t i = i0 + u;
+        int64_t lo = 0, hi = -1;
+        if (i < n) {
+            const int64_t r = row_of(keys[i], Z, magic);
+            lo = prev + 1;
+            hi = r < total_rows ? r : total_rows;
+            prev = r;
+        } else if (i == n) {
+            lo = prev + 1;
+            hi = total_rows;
+        }
+        const bool longgap = hi - lo >= 16;
+        if (!longgap)
+            for (int64_t r = lo; r <= hi; ++r) row_ptr[r] = (uint32_t)i;
+        unsigned m = __ballot_sync(kFull, longgap);
+        while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const int64_t l = __shfl_sync(kFull, lo, src);
+            const int64_t h = __shfl_sync(kFull, hi, src);
+            const int64_t v = __shfl_sync(kFull, i, src);
+            for (int64_t r = l + lane; r <= h; r += 32) row_ptr[r] = (uint32_t)v;
+        }
     }
 }
 
 cudaError_t launch_row_index(const Geo& g, const uint64_t* keys, const int64_t* nnz_dev, int64_t nbound,
                              uint32_t* row_ptr, cudaStream_t s) {
     const int64_t total_rows = g.B * g.C * g.R;
-    const int64_t threads = nbound + 1;
+    const int64_t threads = (nbound + 1 + kRiItems - 1) / kRiItems;
     const int bs = 256;
     const int64_t grid = (threads + bs - 1) / bs;
-    { SPC_PHASE("row_index", s, 1); row_index_kernel<<<(unsigned)grid, bs, 0, s>>>(g.Z, keys, nnz_dev, nbound, row_ptr, total_rows); }
+    const uint64_t Z = (uint64_t)g.Z;
+    const uint64_t magic = Z == 1 ? ~0ull : ~0ull / Z;   // floor((2^64 - 1) / Z)
+    { SPC_PHASE("row_index", s, 1); row_index_kernel<<<(unsigned)grid, bs, 0, s>>>(Z, magic, keys, nnz_dev, nbound, row_ptr, total_rows); }
     return cudaGetLastError();
 }
 
