@@ -563,19 +563,21 @@ __device__ __forceinline__ void classify_chunk(const FwdArgs& a, const FwdSeg& s
     }
     if (nge == 0) return;   // block-uniform
     // stage this thread's entries at their key-ordered slots (predicated shared stores)
-    uint32_t slab0 = 0;
+    {
+        uint32_t slab0 = 0;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-        uint32_t q = slab0 + (uint32_t)((ex >> (12 * v)) & 0xfffu);
+        for (int v = 0; v < 4; ++v) {
+            uint32_t q = slab0 + (uint32_t)((ex >> (12 * v)) & 0xfffu);
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
-            const int u = 4 * v + w;
-            const bool k = (ge >> u) & 1u;
-            const uint32_t p = (uint32_t)lo + 4u * ((uint32_t)v * kChunkThreads + threadIdx.x) + (uint32_t)w;
-            if (k) sbuf[q] = make_uint2(p, bits[u]);
-            q += k ? 1u : 0u;
+            for (int w = 0; w < 4; ++w) {
+                const int u = 4 * v + w;
+                const bool k = (ge >> u) & 1u;
+                const uint32_t p = (uint32_t)lo + 4u * ((uint32_t)v * kChunkThreads + threadIdx.x) + (uint32_t)w;
+                if (k) sbuf[q] = make_uint2(p, bits[u]);
+                q += k ? 1u : 0u;
+            }
+            slab0 += (uint32_t)((tot >> (12 * v)) & 0xfffu);
         }
-        slab0 += (uint32_t)((tot >> (12 * v)) & 0xfffu);
     }
     __syncthreads();
     // coalesced copy to the staging list; candidates (digit == B1) also appended, any order
@@ -631,6 +633,20 @@ __global__ void __launch_bounds__(kChunkThreads) fwd_classify_kernel(FwdArgs a, 
 // the survivors (about n/2048) are copied to shared memory and the remaining digits (8, 8, 8,
 // 8, 8, 2 bits) run there. All composite keys are distinct (p is unique), so kstar is exact.
 constexpr int kResThreads = 512;
+
+// f(e) for every candidate e of a segment's list, four independent loads in flight per thread
+template <typename F>
+__device__ __forceinline__ void for_cands(const uint2* __restrict__ c, uint64_t n, F f) {
+    uint64_t i = threadIdx.x;
+    for (; i + 3 * kResThreads < n; i += 4 * kResThreads) {
+        const uint2 e0 = c[i], e1 = c[i + kResThreads], e2 = c[i + 2 * kResThreads], e3 = c[i + 3 * kResThreads];
+        f(e0);
+        f(e1);
+        f(e2);
+        f(e3);
+    }
+    for (; i < n; i += kResThreads) f(c[i]);
+}
 constexpr int kResCap = 2048;   // survivors kept in shared memory
 __global__ void __launch_bounds__(kResThreads) fwd_resolve_kernel(FwdArgs a) {
     const int64_t s = blockIdx.x;
@@ -660,11 +676,10 @@ __global__ void __launch_bounds__(kResThreads) fwd_resolve_kernel(FwdArgs a) {
         const uint64_t prefix = sh_prefix, mask = sh_mask;
         const uint32_t dmask = (uint32_t)nb - 1u;
         if (!in_smem) {
-            for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
-                const uint2 e = c[i];
+            for_cands(c, n, [&](uint2 e) {
                 const uint64_t k = composite(score_bits(e.y, a.attn), e.x);
                 if ((k & mask) == prefix) atomicAdd(&h[(uint32_t)(k >> sh) & dmask], 1u);
-            }
+            });
         } else {
             for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) {
                 const uint64_t k = sc[i];
@@ -700,11 +715,10 @@ __global__ void __launch_bounds__(kResThreads) fwd_resolve_kernel(FwdArgs a) {
         if (!in_smem && pass + 1 < 7 && sh_bin_cnt <= (uint32_t)kResCap) {
             // survivors of the chosen prefix -> shared memory (order irrelevant: keys distinct)
             const uint64_t p2 = sh_prefix, m2 = sh_mask;
-            for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
-                const uint2 e = c[i];
+            for_cands(c, n, [&](uint2 e) {
                 const uint64_t k = composite(score_bits(e.y, a.attn), e.x);
                 if ((k & m2) == p2) sc[atomicAdd(&sh_ns, 1u)] = k;
-            }
+            });
             __syncthreads();
             ns = sh_ns;
             in_smem = true;
@@ -715,10 +729,9 @@ __global__ void __launch_bounds__(kResThreads) fwd_resolve_kernel(FwdArgs a) {
         st.kstar = kstar;
         a.seg[s] = st;
     }
-    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const uint2 e = c[i];
+    for_cands(c, n, [&](uint2 e) {
         if (composite(score_bits(e.y, a.attn), e.x) >= kstar) atomicAdd(&a.tile_sel[s * a.nchunk + e.x / kChunk], 1u);
-    }
+    });
 }
 
 // per segment: kept count per chunk -> exclusive offsets; segment total -> kept[s]
