@@ -191,6 +191,7 @@ FwdWs carve_fwd(Carver& c, const Geo& gx, const Geo& gy, const KGeo& kg, const F
         ws.g.bhi = c.take<float>((size_t)gp->KV * gp->Np * gp->Kp);
         ws.g.blo = c.take<float>((size_t)gp->KV * gp->Np * gp->Kp);
         ws.g.wmask = c.take<uint32_t>((size_t)gp->KV * gp->Np);
+        ws.g.dinfo = c.take<int>((size_t)3 * gp->KV + 1);
     }
     const int64_t nseg = gy.B * gy.C;
     const size_t KXY = (size_t)kg.kx * kg.ky;

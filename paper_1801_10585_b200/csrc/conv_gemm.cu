@@ -30,6 +30,9 @@ namespace spc {
 constexpr int kGM = 128;        // output voxels per tile = UMMA M = TMEM lanes
 constexpr int kGThreads = 128;  // thread t gathers A row t and owns TMEM lane t in the epilogue
 constexpr int kGMaxStages = 4;  // operand stages in flight (gathers run kGMaxStages - 1 offsets ahead)
+constexpr int kSlabTY = 16;     // slab form: M tile = 16 rows x 8 z (a core-matrix group = 8 z of one row)
+constexpr int kSlabTZ = 8;
+constexpr int kSlabMaxStages = 8;
 
 GemmPlan plan_gemm(const Geo& gx, const Geo& gy, const KGeo& kg) {
     GemmPlan g{};
@@ -41,13 +44,31 @@ GemmPlan plan_gemm(const Geo& gx, const Geo& gy, const KGeo& kg) {
     g.KV = kg.KV;
     g.ntile = (gy.V + kGM - 1) / kGM;
     g.stage_bytes = (size_t)2 * kGM * g.Kp * 4 + (size_t)2 * g.Np * g.Kp * 4;
-    const size_t extra = (size_t)g.KV * g.Np * 4 + (size_t)g.KV * 8 + 128;
+    const size_t extra = (size_t)g.KV * g.Np * 4 + (size_t)(3 * g.KV + 1) * 4 + 2 * 8 * 8 + 64 + 16;
     int want = 2;   // two stages keep two CTAs (8 warps of gatherers) per SM for the 32-channel layers
     if (const char* e = getenv("SPC_GEMM_STAGES")) want = std::max(2, std::min(kGMaxStages, atoi(e)));
     g.stages = (int)std::min<size_t>((size_t)want, (200 * 1024 - extra) / g.stage_bytes);
     g.smem = g.stages * g.stage_bytes + extra;
     g.tcols = g.Np <= 32 ? 32 : 64;
     g.ok = g.stages >= 2;
+    // slab form: M tile = 16 rows (y) x 8 z of one x-plane; the tile's input neighbourhood is
+    // staged once and every A_delta is a strided window of it (no per-offset re-gather)
+    g.SX = 1 + 2 * kg.hx;
+    g.SY = kSlabTY + 2 * kg.hy;
+    g.SZ = kSlabTZ + 2 * kg.hz;
+    g.NV = g.SX * g.SY * g.SZ;
+    g.nty = (gy.Y + kSlabTY - 1) / kSlabTY;
+    g.ntz = (gy.Z + kSlabTZ - 1) / kSlabTZ;
+    g.slab_bytes = (size_t)2 * g.NV * g.Kp * 4 + (size_t)g.NV * 4;
+    g.bstage_bytes = (size_t)2 * g.Np * g.Kp * 4;
+    // as many B stages as fit next to the slab (they hide the L2 latency of B_delta, 2..8)
+    {
+        const size_t room = 200 * 1024 > g.slab_bytes + extra ? 200 * 1024 - g.slab_bytes - extra : 0;
+        g.bstages = (int)std::max<size_t>(2, std::min<size_t>(kSlabMaxStages, room / g.bstage_bytes));
+    }
+    g.slab_smem = g.slab_bytes + g.bstages * g.bstage_bytes + extra;
+    g.slab = (g.slab_smem <= 200 * 1024 && g.NV * 16 < (1 << 18) && g.SZ * 16 < (1 << 18)) ? 1 : 0;
+    if (const char* e = getenv("SPC_GEMM_SLAB")) g.slab = g.slab && e[0] != '0';
     return g;
 }
 
@@ -100,12 +121,34 @@ __global__ void gemm_wprep_kernel(KGeo kg, int c_in, int Kp, int Np, const uint6
     }
 }
 
+// Offsets with at least one stored weight (the others contribute nothing) and whether every
+// output channel shares the offset's ic mask: dinfo = [nd, dlist[KV], uniform[KV], slab offset[KV]].
+__global__ void gemm_dinfo_kernel(KGeo kg, int c_out, int Np, int SY, int SZ, const uint32_t* __restrict__ wmask,
+                                  int* __restrict__ dinfo) {
+    const int KV = kg.KV;
+    if (threadIdx.x == 0) {
+        int nd = 0;
+        for (int d = 0; d < KV; ++d) {
+            uint32_t any = 0, uni = 1;
+            for (int oc = 0; oc < c_out; ++oc) {
+                any |= wmask[d * Np + oc];
+                uni &= (uint32_t)(wmask[d * Np + oc] == wmask[d * Np]);
+            }
+            if (any) dinfo[1 + nd++] = d;
+            dinfo[1 + KV + d] = (int)uni;
+            const int dz = d % kg.kz, dy = (d / kg.kz) % kg.ky, dx = d / (kg.kz * kg.ky);
+            dinfo[1 + 2 * KV + d] = (dx * SY + dy) * SZ + dz;
+        }
+        dinfo[0] = nd;
+    }
+}
+
 // ------------------------------------------------------------------ tcgen05 / mbarrier helpers
-__device__ __forceinline__ uint64_t umma_sdesc(uint32_t saddr) {
-    // start address >> 4 | LBO (K-half stride 128 B) >> 4 << 16 | SBO (8-row group 256 B) >> 4 << 32 |
-    // version 1 (sm_100) << 46 | layout SWIZZLE_NONE (0) << 61
-    return (uint64_t)((saddr >> 4) & 0x3fffu) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
-           (1ull << 46);
+__device__ __forceinline__ uint64_t umma_sdesc(uint32_t saddr, uint32_t lbo = 128, uint32_t sbo = 256) {
+    // start address >> 4 | LBO (stride between the two 16-byte K halves) >> 4 << 16 | SBO (stride
+    // between 8-row core-matrix groups) >> 4 << 32 | version 1 (sm_100) << 46 | SWIZZLE_NONE (0) << 61
+    return (uint64_t)((saddr >> 4) & 0x3fffu) | ((uint64_t)((lbo >> 4) & 0x3fffu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3fffu) << 32) | (1ull << 46);
 }
 __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                           uint32_t accumulate) {
@@ -131,8 +174,23 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
 __device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(mbar) : "memory");
 }
+// cp.async.wait_group with a runtime bound (the immediate must be a constant)
+__device__ __forceinline__ void cp_async_wait_upto(int n) {
+    switch (n) {
+        case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+        case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+        case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+        case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+        case 4: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
+        case 5: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
+        default: asm volatile("cp.async.wait_group 6;" ::: "memory"); break;
+    }
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void cp4(uint32_t dst, const void* src, bool ok) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" :: "r"(dst), "l"(src), "r"(ok ? 4 : 0) : "memory");
+}
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool ok) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
 }
@@ -316,6 +374,194 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_kernel(Geo gx, Geo gy, KG
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"((uint32_t)g.tcols));
 }
 
+// Slab form of variant G. CTA = (b, x, 16 rows from y0, 8 z from z0) = 128 output voxels; M row m
+// <-> (y0 + m/8, z0 + m%8), so an 8-row core-matrix group is 8 consecutive z of one row. The
+// input neighbourhood (x-hx..x+hx, y0-hy..y0+15+hy, z0-hz..z0+7+hz) is staged ONCE per tile in
+// shared memory as [K step][K half][voxel][16 B] (hi and lo copies, plus occupancy masks), and
+// A_delta for offset (dx, dy, dz) is the window starting at slab voxel (dx, dy, dz): row group
+// stride SBO = SZ*16 B, K-half stride LBO = NV*16 B -- a plain UMMA descriptor, no copy. Only
+// B_delta streams per offset (double-buffered, full/empty mbarriers as in the gather form).
+__global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo gy, KGeo kg, GemmPlan g, GemmArgs a) {
+    extern __shared__ __align__(1024) unsigned char gsm[];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int Kp = g.Kp, Np = g.Np, KV = g.KV, NV = g.NV, SY = g.SY, SZ = g.SZ;
+    const int c_out = (int)gy.C;
+    int64_t t = blockIdx.x;
+    const int tz = (int)(t % g.ntz); t /= g.ntz;
+    const int ty = (int)(t % g.nty); t /= g.nty;
+    const int x = (int)(t % gy.X);
+    const int64_t b = t / gy.X;
+    const int y0 = ty * kSlabTY, z0 = tz * kSlabTZ;
+    const int S = g.bstages;
+    // shared layout: slab hi | slab lo | occ | B stages | wmask | dlist | mbarriers | tmem slot
+    const size_t half_plane = (size_t)NV * 16;             // one K half of one K step, all voxels
+    const size_t slab_one = (size_t)NV * Kp * 4;           // hi or lo
+    uint32_t* occs = reinterpret_cast<uint32_t*>(gsm + 2 * slab_one);
+    unsigned char* bst = gsm + g.slab_bytes;
+    uint32_t* wmask = reinterpret_cast<uint32_t*>(bst + S * g.bstage_bytes);
+    int* dlist = reinterpret_cast<int*>(wmask + KV * Np);   // [nd][dlist KV][uniform KV][slab offset KV]
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(dlist) +
+                                                 (((size_t)(3 * KV + 1) * 4 + 7) & ~(size_t)7));
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 2 * kSlabMaxStages);
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(gsm);
+    const uint32_t bbase = sbase + (uint32_t)g.slab_bytes;
+    const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(mbar);
+    const size_t B_B = (size_t)Np * Kp * 4;
+
+    for (int i = tid; i < KV * Np; i += kGThreads) wmask[i] = a.wmask[i];
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"((uint32_t)__cvta_generic_to_shared(tslot)), "r"((uint32_t)g.tcols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(mb0 + 8u * i, kGThreads);
+            mbar_init(mb0 + 8u * (S + i), 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = tid; i < 3 * KV + 1; i += kGThreads) dlist[i] = a.dinfo[i];
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const int nd = dlist[0];
+    const int* dl = dlist + 1;
+    const int* duni = dlist + 1 + KV;
+    const int* dsoff = dlist + 1 + 2 * KV;
+
+    // ---- stage the neighbourhood (joins cp.async group 0 together with B of the first offset):
+    // one slab row (sx, sy) per warp iteration, lanes over its SZ voxels x 16-byte chunks
+    {
+        const int cpv = Kp / 4, lg = __ffs(cpv) - 1;        // chunks per voxel (power of 2)
+        const int xs0 = x - kg.hx, ys0 = y0 - kg.hy, zs0 = z0 - kg.hz;
+        const int lane = tid & 31;
+        for (int r = warp; r < g.SX * SY; r += kGThreads / 32) {
+            const int sx = r / SY, sy = r - (r / SY) * SY;
+            const int qx = xs0 + sx, qy = ys0 + sy;
+            const bool rok = qx >= 0 && qx < gx.X && qy >= 0 && qy < gx.Y;
+            const size_t rowv = (size_t)b * gx.V + ((size_t)(rok ? qx : 0) * gx.Y + (rok ? qy : 0)) * gx.Z;
+            const size_t rowq = rowv * Kp;
+            for (int j = lane; j < SZ * cpv; j += 32) {
+                const int sz = j >> lg, c = j & (cpv - 1);
+                const int qz = zs0 + sz;
+                const bool ok = rok && qz >= 0 && qz < gx.Z;
+                const size_t q = ok ? rowq + (size_t)qz * Kp + 4 * c : 0;
+                const int v = r * SZ + sz;
+                const uint32_t off = (uint32_t)(((c >> 1) * 2 + (c & 1)) * half_plane + (size_t)v * 16);
+                cp16(sbase + off, a.xhi + q, ok);
+                cp16(sbase + (uint32_t)slab_one + off, a.xlo + q, ok);
+            }
+            for (int sz = lane; sz < SZ; sz += 32) {   // occupancy masks, same async group
+                const int qz = zs0 + sz;
+                const bool ok = rok && qz >= 0 && qz < gx.Z;
+                cp4(sbase + (uint32_t)(2 * slab_one) + 4u * (uint32_t)(r * SZ + sz), a.occ + (ok ? rowv + qz : 0), ok);
+            }
+        }
+    }
+    auto load_b = [&](int st, int d) {
+        const uint32_t base = bbase + (uint32_t)(st * g.bstage_bytes);
+        const float* bh = a.bhi + (size_t)d * Np * Kp;
+        const float* bl = a.blo + (size_t)d * Np * Kp;
+        for (int c = tid; c < Np * Kp / 4; c += kGThreads) {
+            cp16(base + 16u * c, bh + 4 * c, true);
+            cp16(base + (uint32_t)B_B + 16u * c, bl + 4 * c, true);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(Np >> 3) << 17) | ((uint32_t)(kGM >> 4) << 24);
+    const uint32_t lbo_a = (uint32_t)half_plane, sbo_a = (uint32_t)(SZ * 16);
+    const uint64_t dA0 = umma_sdesc(sbase, lbo_a, sbo_a), dB0 = umma_sdesc(bbase);
+
+    if (nd > 0) {
+        // groups 0 .. S-2 in flight up front; group 0 also carries the slab
+        for (int j = 0; j < S - 1; ++j) {
+            if (j < nd) load_b(j, dl[j]);
+            else asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        for (int it = 0; it < nd; ++it) {
+            const int st = it % S;
+            cp_async_wait_upto(S - 2);   // this thread's group for offset it has landed
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(mb0 + 8u * st);
+            if (tid == 0) {
+                mbar_wait(mb0 + 8u * st, (uint32_t)((it / S) & 1));
+                tc_fence_after();
+                // descriptors differ only in the start-address field (bits 0..13, 16-byte units):
+                // offsets are added to precomputed base descriptors
+                const uint64_t dAh = dA0 + (uint64_t)((uint32_t)(dsoff[dl[it]] * 16) >> 4);
+                const uint64_t dBh = dB0 + (uint64_t)((uint32_t)(st * g.bstage_bytes) >> 4);
+                const uint64_t dAl = dAh + (uint64_t)(slab_one >> 4), dBl = dBh + (uint64_t)(B_B >> 4);
+                const uint64_t kA = (uint64_t)(2 * half_plane >> 4), kB = (uint64_t)(Np * 32 >> 4);
+#pragma unroll 1
+                for (int ks = 0; ks < Kp / 8; ++ks) {   // hi*hi, hi*lo, lo*hi per K step
+                    const uint32_t acc = (it | ks) != 0;
+                    umma_tf32(tmem, dAh + ks * kA, dBh + ks * kB, idesc, acc);
+                    umma_tf32(tmem, dAh + ks * kA, dBl + ks * kB, idesc, 1u);
+                    umma_tf32(tmem, dAl + ks * kA, dBh + ks * kB, idesc, 1u);
+                }
+                umma_commit(mb0 + 8u * (S + st));
+            }
+            // B of offset it + S - 1 into the slot of offset it - 1 once its MMAs retired
+            const int nx = it + S - 1;
+            if (nx < nd) {
+                if (it >= 1) mbar_wait(mb0 + 8u * (S + (it - 1) % S), (uint32_t)(((it - 1) / S) & 1));
+                load_b(nx % S, dl[nx]);
+            } else {
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
+        }
+        mbar_wait(mb0 + 8u * (S + (nd - 1) % S), (uint32_t)(((nd - 1) / S) & 1));
+        tc_fence_after();
+    } else {
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();   // occupancy slab visible
+    }
+
+    // ---- epilogue: TMEM lane m = this thread's M row = (y0 + m/8, z0 + m%8)
+    const int yy = tid >> 3, zz = tid & 7;
+    const int py = y0 + yy, pz = z0 + zz;
+    const bool pin = py < gy.Y && pz < gy.Z;
+    if (nd > 0) __syncthreads();   // every thread's occupancy slab writes are visible
+    uint64_t supm = 0;
+    const uint64_t allm = c_out >= 64 ? ~0ull : ((1ull << c_out) - 1ull);
+    if (pin)
+        for (int d = 0; d < KV; ++d) {
+            const uint32_t nb = occs[dsoff[d] + yy * SZ + zz];
+            if (!nb) continue;
+            if (duni[d]) {
+                if (nb & wmask[d * Np]) supm = allm;
+            } else {
+                for (int oc = 0; oc < c_out; ++oc)
+                    if (nb & wmask[d * Np + oc]) supm |= 1ull << oc;
+            }
+            if (supm == allm) break;
+        }
+    const int64_t p = ((int64_t)x * gy.Y + py) * gy.Z + pz;
+    for (int c0 = 0; c0 < Np; c0 += 16) {
+        float v[16];
+        if (nd > 0) tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+        else
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+        if (!pin) continue;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int oc = c0 + i;
+            if (oc >= c_out) break;
+            const bool sup = (supm >> oc) & 1ull;
+            const float bv = a.bias ? __ldg(&a.bias[oc]) : 0.0f;
+            a.pre[((size_t)b * c_out + oc) * gy.V + p] = sup ? v[i] + bv : __uint_as_float(kAbsent);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"((uint32_t)g.tcols));
+}
+
 // Support size and score-digit histogram of each (b, oc) buffer (the scatter variant fuses this
 // into its epilogue): one block per slice of a segment, shared-memory histogram.
 __global__ void __launch_bounds__(256) pre_hist_kernel(FwdArgs a, int64_t V, int splits) {
@@ -362,14 +608,25 @@ cudaError_t launch_conv_gemm(const Geo& gx, const Geo& gy, const KGeo& kg, const
         gemm_wprep_kernel<<<32, 256, 0, s>>>(kg, (int)gx.C, g.Kp, g.Np, ga.wkeys, ga.wvals, ga.nw, ga.bhi, ga.blo,
                                              ga.wmask);
     }
-    cudaError_t e = cudaFuncSetAttribute(conv_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
-    if (e != cudaSuccess) return e;
+    {
+        SPC_PHASE("gemm_dinfo", s, 1);
+        gemm_dinfo_kernel<<<1, 32, 0, s>>>(kg, (int)gy.C, g.Np, g.SY, g.SZ, ga.wmask, ga.dinfo);
+    }
+    cudaError_t e;
     {
         SPC_PHASE("conv_gemm", s, 1);
         GemmArgs gg = ga;
         gg.pre = a.pre;
         gg.bias = a.bias;
-        conv_gemm_kernel<<<(unsigned)(gx.B * g.ntile), kGThreads, g.smem, s>>>(gx, gy, kg, g, gg);
+        if (g.slab) {
+            e = cudaFuncSetAttribute(conv_gemm_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.slab_smem);
+            if (e != cudaSuccess) return e;
+            conv_gemm_slab_kernel<<<(unsigned)(gx.B * gy.X * g.nty * g.ntz), kGThreads, g.slab_smem, s>>>(gx, gy, kg, g, gg);
+        } else {
+            e = cudaFuncSetAttribute(conv_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+            if (e != cudaSuccess) return e;
+            conv_gemm_kernel<<<(unsigned)(gx.B * g.ntile), kGThreads, g.smem, s>>>(gx, gy, kg, g, gg);
+        }
     }
     {
         const int64_t nseg = gy.B * gy.C;

@@ -169,6 +169,9 @@ struct GemmPlan {
     int tcols;         // TMEM columns allocated per CTA
     int stages;        // operand stages in shared memory
     size_t stage_bytes, smem;
+    // slab form (conv_gemm_slab_kernel): tile 16 rows x 8 z, neighbourhood SX x SY x SZ voxels
+    int slab, SX, SY, SZ, NV, nty, ntz, bstages;
+    size_t slab_bytes, bstage_bytes, slab_smem;
 };
 struct GemmArgs {
     const uint64_t* xkeys;
@@ -184,6 +187,7 @@ struct GemmArgs {
     float* bhi;        // [KV*Np*Kp] per-offset B (canonical K-major layout), high part
     float* blo;        // low part
     uint32_t* wmask;   // [KV*Np] stored-weight mask over ic
+    int* dinfo;        // [3*KV + 1] offsets with weights, uniform-mask flags, slab offsets
     const float* bias;
     float* pre;
 };
