@@ -44,7 +44,7 @@ GemmPlan plan_gemm(const Geo& gx, const Geo& gy, const KGeo& kg) {
     g.KV = kg.KV;
     g.ntile = (gy.V + kGM - 1) / kGM;
     g.stage_bytes = (size_t)2 * kGM * g.Kp * 4 + (size_t)2 * g.Np * g.Kp * 4;
-    const size_t extra = (size_t)g.KV * g.Np * 4 + (size_t)(3 * g.KV + 1) * 4 + 2 * 8 * 8 + 64 + 16;
+    const size_t extra = (size_t)g.KV * g.Np * 4 + (size_t)(3 * g.KV + 1) * 4 + 2 * 8 * std::max(8, g.KV) + 64 + 16;
     int want = 2;   // two stages keep two CTAs (8 warps of gatherers) per SM for the 32-channel layers
     if (const char* e = getenv("SPC_GEMM_STAGES")) want = std::max(2, std::min(kGMaxStages, atoi(e)));
     g.stages = (int)std::min<size_t>((size_t)want, (200 * 1024 - extra) / g.stage_bytes);
@@ -65,6 +65,9 @@ GemmPlan plan_gemm(const Geo& gx, const Geo& gy, const KGeo& kg) {
     {
         const size_t room = 200 * 1024 > g.slab_bytes + extra ? 200 * 1024 - g.slab_bytes - extra : 0;
         g.bstages = (int)std::max<size_t>(2, std::min<size_t>(kSlabMaxStages, room / g.bstage_bytes));
+        // every B_delta resident (small filter banks): one load, then all MMAs back to back
+        g.ball = (size_t)g.KV * g.bstage_bytes <= std::min<size_t>(room, 96 * 1024) ? 1 : 0;
+        if (g.ball) g.bstages = g.KV;
     }
     g.slab_smem = g.slab_bytes + g.bstages * g.bstage_bytes + extra;
     g.slab = (g.slab_smem <= 200 * 1024 && g.NV * 16 < (1 << 18) && g.SZ * 16 < (1 << 18)) ? 1 : 0;
@@ -402,7 +405,7 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
     int* dlist = reinterpret_cast<int*>(wmask + KV * Np);   // [nd][dlist KV][uniform KV][slab offset KV]
     uint64_t* mbar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(dlist) +
                                                  (((size_t)(3 * KV + 1) * 4 + 7) & ~(size_t)7));
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 2 * kSlabMaxStages);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 2 * S);
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(gsm);
     const uint32_t bbase = sbase + (uint32_t)g.slab_bytes;
     const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(mbar);
@@ -474,7 +477,41 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
     const uint32_t lbo_a = (uint32_t)half_plane, sbo_a = (uint32_t)(SZ * 16);
     const uint64_t dA0 = umma_sdesc(sbase, lbo_a, sbo_a), dB0 = umma_sdesc(bbase);
 
-    if (nd > 0) {
+    if (nd > 0 && g.ball) {
+        // all B_delta resident: one async group (slab + every B), then every MMA back to back and
+        // a single commit -- no per-offset synchronisation
+        for (int j = 0; j < nd; ++j) {
+            const uint32_t base = bbase + (uint32_t)(j * g.bstage_bytes);
+            const float* bh = a.bhi + (size_t)dl[j] * Np * Kp;
+            const float* bl = a.blo + (size_t)dl[j] * Np * Kp;
+            for (int c = tid; c < Np * Kp / 4; c += kGThreads) {
+                cp16(base + 16u * c, bh + 4 * c, true);
+                cp16(base + (uint32_t)B_B + 16u * c, bl + 4 * c, true);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            const uint64_t kA = (uint64_t)(2 * half_plane >> 4), kB = (uint64_t)(Np * 32 >> 4);
+            for (int it = 0; it < nd; ++it) {
+                const uint64_t dAh = dA0 + (uint64_t)((uint32_t)(dsoff[dl[it]] * 16) >> 4);
+                const uint64_t dBh = dB0 + (uint64_t)((uint32_t)(it * g.bstage_bytes) >> 4);
+                const uint64_t dAl = dAh + (uint64_t)(slab_one >> 4), dBl = dBh + (uint64_t)(B_B >> 4);
+                for (int ks = 0; ks < Kp / 8; ++ks) {
+                    umma_tf32(tmem, dAh + ks * kA, dBh + ks * kB, idesc, (it | ks) != 0);
+                    umma_tf32(tmem, dAh + ks * kA, dBl + ks * kB, idesc, 1u);
+                    umma_tf32(tmem, dAl + ks * kA, dBh + ks * kB, idesc, 1u);
+                }
+            }
+            umma_commit(mb0 + 8u * S);
+        }
+        mbar_wait(mb0 + 8u * S, 0u);
+        tc_fence_after();
+    } else if (nd > 0) {
         // groups 0 .. S-2 in flight up front; group 0 also carries the slab
         for (int j = 0; j < S - 1; ++j) {
             if (j < nd) load_b(j, dl[j]);
