@@ -665,6 +665,31 @@ __global__ void __launch_bounds__(kResThreads) fwd_resolve_kernel(FwdArgs a) {
         sh_need = st.need;
         sh_ns = 0;
     }
+    if (n <= (uint64_t)kResThreads) {
+        // small candidate sets (e.g. the 784-voxel MNIST-like segments): the `need`-th largest
+        // composite key directly by ranking -- each key counts the keys above it (all distinct)
+        for (uint32_t i = threadIdx.x; i < (uint32_t)n; i += blockDim.x) {
+            const uint2 e = c[i];
+            sc[i] = composite(score_bits(e.y, a.attn), e.x);
+        }
+        __syncthreads();
+        const uint64_t want = (uint64_t)st.need - 1;   // rank (0 = largest) of kstar
+        for (uint32_t i = threadIdx.x; i < (uint32_t)n; i += blockDim.x) {
+            const uint64_t k = sc[i];
+            uint32_t above = 0;
+            for (uint32_t j = 0; j < (uint32_t)n; ++j) above += sc[j] > k ? 1u : 0u;
+            if (above == want) sh_prefix = k;
+        }
+        __syncthreads();
+        const uint64_t kstar = sh_prefix;
+        if (threadIdx.x == 0) {
+            st.kstar = kstar;
+            a.seg[s] = st;
+        }
+        for (uint32_t i = threadIdx.x; i < (uint32_t)n; i += blockDim.x)
+            if (sc[i] >= kstar) atomicAdd(&a.tile_sel[s * a.nchunk + (uint32_t)(~sc[i]) / kChunk], 1u);
+        return;
+    }
     bool in_smem = false;
     uint32_t ns = 0;
 #pragma unroll 1
