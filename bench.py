@@ -373,22 +373,26 @@ def ncu_traffic(kernel):
 
 
 def run_e2e(torch, spc, x, w, bias, k, cap, dy_dev, args, world, dist):
-    """Same step through the public API with HOST inputs: pinned H2D of the step's inputs (x
-    keys/values, dy) inside the timed region and D2H of the result (dw, dbias, output nnz)."""
+    """Same step through the public API with HOST inputs: every step's inputs (x keys/values, dy)
+    are copied H2D from pinned memory inside the timed region and its result (dw, dbias, output
+    nnz) is read back D2H. Like a data loader, the upload of step i+1 runs on a copy stream into
+    the second of two device input buffers while step i computes (the buffer is reused only after
+    the step that read it has finished)."""
     hk = torch.from_numpy(x.keys.view(np.int64)).pin_memory()
     hv = torch.from_numpy(x.values).pin_memory()
     hdy = dy_dev.cpu().pin_memory()
-    dk = torch.empty_like(hk, device="cuda")
-    dv = torch.empty_like(hv, device="cuda")
-    ddy = torch.empty_like(hdy, device="cuda")
+    bufs = [(torch.empty_like(hk, device="cuda"), torch.empty_like(hv, device="cuda"),
+             torch.empty_like(hdy, device="cuda")) for _ in range(2)]
     W = spc.SparseFilter.from_arrays(w.keys, w.values, w.c_in, w.c_out, w.ksize)
     bias_t = torch.from_numpy(bias).cuda()
-    X = spc.SparseMap(dk, dv, x.batch, x.channels, x.dims, x.nnz, None)
-    fwd = spc.FwdPlan(X, W, "magnitude", k, args.resolved_variant)
-    dk.copy_(hk)
-    dv.copy_(hv)
-    Y0 = fwd(X, W, bias_t)
-    bwd = spc.BwdPlan(X, W, Y0)
+    Xs = [spc.SparseMap(bk, bv, x.batch, x.channels, x.dims, x.nnz, None) for bk, bv, _ in bufs]
+    fwd = spc.FwdPlan(Xs[0], W, "magnitude", k, args.resolved_variant)
+    for bk, bv, bd in bufs:
+        bk.copy_(hk)
+        bv.copy_(hv)
+        bd.copy_(hdy)
+    Y0 = fwd(Xs[0], W, bias_t)
+    bwd = spc.BwdPlan(Xs[0], W, Y0)
     dx = torch.empty(max(x.nnz, 1), device="cuda")
     dw = torch.empty(W.keys.numel(), device="cuda")
     db = torch.empty(C_OUT, device="cuda")
@@ -396,28 +400,49 @@ def run_e2e(torch, spc, x, w, bias, k, cap, dy_dev, args, world, dist):
     out_db = torch.empty(C_OUT).pin_memory()
     out_n = torch.empty(1, dtype=torch.int64).pin_memory()
     allreduce = spc.dp.GradAllReduce(W.keys.numel(), C_OUT, "cuda")
+    comp = torch.cuda.current_stream()
+    copy = torch.cuda.Stream()
+    loaded = [torch.cuda.Event(), torch.cuda.Event()]
+    consumed = [torch.cuda.Event(), torch.cuda.Event()]
 
-    def step():
-        dk.copy_(hk, non_blocking=True)
-        dv.copy_(hv, non_blocking=True)
-        ddy.copy_(hdy, non_blocking=True)
-        Y = fwd(X, W, bias_t)
-        bwd(X, W, Y, ddy, dx, dw, db)
+    def upload(i):
+        j = i % 2
+        with torch.cuda.stream(copy):
+            copy.wait_event(consumed[j])         # the step that last read buffer j is done
+            bk, bv, bd = bufs[j]
+            bk.copy_(hk, non_blocking=True)
+            bv.copy_(hv, non_blocking=True)
+            bd.copy_(hdy, non_blocking=True)
+            loaded[j].record(copy)
+
+    def step(i, last):
+        j = i % 2
+        if not last:
+            upload(i + 1)
+        comp.wait_event(loaded[j])
+        Y = fwd(Xs[j], W, bias_t)
+        bwd(Xs[j], W, Y, bufs[j][2], dx, dw, db)
+        consumed[j].record(comp)
         allreduce(dw, db)
         out_dw.copy_(dw, non_blocking=True)
         out_db.copy_(db, non_blocking=True)
         out_n.copy_(Y.nnz_dev, non_blocking=True)
 
-    for _ in range(max(1, args.warmup)):
-        step()
+    def run(n):
+        for e in consumed:
+            e.record(comp)
+        upload(0)
+        for i in range(n):
+            step(i, i == n - 1)
+
+    run(max(1, args.warmup))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n = max(1, args.steps)
     if dist is not None:
         dist.barrier()
     e0.record()
-    for _ in range(n):
-        step()
+    run(n)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n

@@ -481,6 +481,26 @@ def test_c4_full_size_sampled(cuda_lib):
         np.testing.assert_array_equal(gdx[xlo:xhi], odx)
 
 
+@pytest.mark.slow
+def test_c5_full_size_gemm_sampled(cuda_lib):
+    """BASELINE configs[4] at full size for variant G (the tensor-core path the per-layer choice
+    takes there): 64^3, b=8, 32->32, rho_d 20%, exact layer. Two sampled samples against the
+    oracle: identical support, values within the tolerance rule."""
+    spc = cuda_lib
+    x = uniform_map(8, 32, (64, 64, 64), 0.2, SEED_BASE * 1000 + 520)
+    w = sparse_filter(32, 32, (3, 3, 3), 1.0, SEED_BASE + 5)
+    bias = bias_vector(32, SEED_BASE + 5)
+    gk, gv, _ = run_fwd(spc, x, w, bias, "none", 0, variant="gemm")
+    V = 64 ** 3
+    span = np.uint64(32 * V)
+    for b in (0, 5):
+        xs = select_samples(x, [b])
+        fk, fv, fa, _ = ora.conv_fwd(xs, w, bias, with_abs=True)
+        lo, hi = np.searchsorted(gk, np.uint64(b) * span), np.searchsorted(gk, np.uint64(b + 1) * span)
+        np.testing.assert_array_equal(gk[lo:hi] - np.uint64(b) * span, fk)
+        assert_values_close(gv[lo:hi], fv, fa)
+
+
 # ------------------------------------------------------------ training-loop steps (SURVEY §8 f1)
 def test_adagrad_step_bit_exact(cuda_lib):
     """The GPU step performs the oracle's sequence of IEEE double operations: bit-identical, with
