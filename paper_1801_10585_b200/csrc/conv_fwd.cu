@@ -45,7 +45,7 @@ __host__ __device__ inline size_t r4(size_t n) { return (n + 3) & ~(size_t)3; }
 // shared-memory bytes beyond the accumulator: staging, item tables (flat offset, first global
 // entry, row base), round offsets and round records of the group, scratch
 static size_t fwd_fixed_smem(int PK, int ocg, int64_t nwg) {
-    return (size_t)kStageCap * 8 + 4 * (3 * r4(PK + 1) + r4(kStageCap / 64 + PK + 1) + 64) +
+    return (size_t)kStageCap * 8 + 4 * (4 * r4(PK + 1) + r4(kStageCap / 64 + PK + 1) + 80) +
            8 * ((size_t)ocg * PK + (size_t)nwg + 1) + 64;
 }
 
@@ -229,12 +229,12 @@ __device__ __forceinline__ float upd(float old, float v, float w) {
 // (every round offset keeps it inside the slice) and do not store.
 template <bool NEG0>
 __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, uint32_t safe, const uint32_t* work,
-                                          const int2* rpair, const int2* rec, const uint32_t* spos,
+                                          const int* roffw, const int2* rec, const uint32_t* spos,
                                           const float* sval) {
 #pragma unroll 1
     for (int g = 0; g < nwork; ++g) {
         const uint32_t wdsc = work[g];                 // {chunk-relative start, count <= 64, item}
-        const int2 rr = rpair[wdsc >> 19];
+        const int2 rr = make_int2(roffw[wdsc >> 19], roffw[(wdsc >> 19) + 1]);
         if (rr.x == rr.y) continue;
         const int s = (int)(wdsc & 0xfffu), n = (int)((wdsc >> 12) & 0x7fu);
         const bool okA = lane < n, okB = lane + 32 < n;
@@ -301,54 +301,74 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     int* ioff = reinterpret_cast<int*>(sval + kStageCap);
     uint32_t* iglob = reinterpret_cast<uint32_t*>(ioff + r4(PK + 1));
     uint32_t* ibase = iglob + r4(PK + 1);
-    uint32_t* work = ibase + r4(PK + 1);
+    int* wpre = reinterpret_cast<int*>(ibase + r4(PK + 1));   // first work descriptor of each item
+    uint32_t* work = reinterpret_cast<uint32_t*>(wpre + r4(PK + 1));
     uint32_t* misc = work + r4(kStageCap / 64 + PK + 1);
-    int2* rpair = reinterpret_cast<int2*>(misc + 64);
+    int2* rpair = reinterpret_cast<int2*>(misc + 80);   // misc: 80 words (u64 block-scan scratch)
     int2* rec = rpair + (size_t)t.ocg * PK;
     const int2* recp = REC_SMEM ? rec : a.rnd + (int64_t)blockIdx.y * t.nwg_max;
     uint32_t* hist = spos;                           // epilogue only
 
     const bool neg0 = *a.guard == 0;                 // -0 accumulation mode (value_guard_kernel)
     const uint32_t marker = neg0 ? kNegZero : kAbsent;
+    // ---- prologue. The global loads go out first (round offsets / records by cp.async, item
+    // bounds into registers) so that their latency overlaps the accumulator fill.
+    int* roffs = reinterpret_cast<int*>(rpair);      // raw round offsets of the group [ocg*PK + 1]
+    {
+        const int* groff = a.roff + (int64_t)blockIdx.y * (t.ocg * PK + 1);
+        const uint32_t rs = (uint32_t)__cvta_generic_to_shared(roffs);
+        for (int i = threadIdx.x; i <= t.ocg * PK; i += blockDim.x)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(rs + 4u * i), "l"(groff + i) : "memory");
+        if (REC_SMEM) {
+            const int2* grec = a.rnd + (int64_t)blockIdx.y * t.nwg_max;
+            const uint32_t rcs = (uint32_t)__cvta_generic_to_shared(rec);
+            for (int i = threadIdx.x; i < t.nwg_max; i += blockDim.x)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(rcs + 8u * i), "l"(grec + i) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    // work items: stored inputs of (ic, plane xs), rows ylo..yhi-1 -> one contiguous key run
+    const int ylo = max(0, y0 - kg.hy), yhi = min(gy.Y, ye + kg.hy);
+    auto item_bounds = [&](int q, uint32_t& e0, uint32_t& n, uint32_t& rb) {
+        e0 = n = rb = 0u;
+        if (q >= PK) return;
+        const int ic = q / kg.kx, xs = x + (q - ic * kg.kx) - kg.hx;
+        if (xs >= 0 && xs < gx.X) {
+            const int64_t row = ((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo;
+            e0 = a.xrow[row];
+            n = a.xrow[row + (yhi - ylo)] - e0;
+            rb = (uint32_t)((uint64_t)row * (uint64_t)Z);   // low word of the row's first key
+        }
+    };
+    uint32_t pe0 = 0, pn = 0, prb = 0;
+    item_bounds(threadIdx.x, pe0, pn, prb);          // first batch of items, loads in flight
     {
         const int n4 = t.ocg * SL / 4;
         const uint4 ab = make_uint4(marker, marker, marker, marker);
         for (int i = threadIdx.x; i < n4; i += blockDim.x) reinterpret_cast<uint4*>(smf)[i] = ab;
     }
-    {
-        const int* groff = a.roff + (int64_t)blockIdx.y * (t.ocg * PK + 1);
-        for (int i = threadIdx.x; i < t.ocg * PK; i += blockDim.x) rpair[i] = make_int2(groff[i], groff[i + 1]);
-        const int2* grec = a.rnd + (int64_t)blockIdx.y * t.nwg_max;
-        const int nrec = groff[t.ocg * PK];
-        if (REC_SMEM)
-            for (int i = threadIdx.x; i < nrec; i += blockDim.x) rec[i] = grec[i];
-    }
-    // work items: stored inputs of (ic, plane xs), rows ylo..yhi-1 -> one contiguous key run
-    const int ylo = max(0, y0 - kg.hy), yhi = min(gy.Y, ye + kg.hy);
-    int carry = 0;
+    // item entry offsets and work-descriptor offsets (groups of <= 64 entries) by one scan of
+    // (count << 32 | groups)
+    uint64_t carry = 0;
     for (int q0 = 0; q0 < PK; q0 += blockDim.x) {
         const int q = q0 + threadIdx.x;
-        uint32_t e0 = 0, n = 0, rb = 0;
+        uint32_t e0 = pe0, n = pn, rb = prb;
+        if (q0 > 0) item_bounds(q, e0, n, rb);
+        const uint64_t packed = ((uint64_t)n << 32) | (uint64_t)((n + 63) >> 6);
+        uint64_t tot;
+        const uint64_t ex = block_excl_scan(packed, reinterpret_cast<uint64_t*>(misc), &tot);
         if (q < PK) {
-            const int ic = q / kg.kx, xs = x + (q - ic * kg.kx) - kg.hx;
-            if (xs >= 0 && xs < gx.X) {
-                const int64_t row = ((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo;
-                e0 = a.xrow[row];
-                n = a.xrow[row + (yhi - ylo)] - e0;
-                rb = (uint32_t)((uint64_t)row * (uint64_t)Z);   // low word of the row's first key
-            }
-        }
-        int tot;
-        const int ex = block_excl_scan((int)n, reinterpret_cast<int*>(misc), &tot);
-        if (q < PK) {
-            ioff[q] = carry + ex;
+            ioff[q] = (int)((carry + ex) >> 32);
+            wpre[q] = (int)((carry + ex) & 0xffffffffu);
             iglob[q] = e0;
             ibase[q] = rb;
         }
         carry += tot;
     }
-    if (threadIdx.x == 0) ioff[PK] = carry;
-    const int total = carry;
+    if (threadIdx.x == 0) ioff[PK] = (int)(carry >> 32);
+    const int total = (int)(carry >> 32);
+    const int wtotal = (int)(carry & 0xffffffffu);
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
 
     const uint32_t accs = (uint32_t)__cvta_generic_to_shared(acc);
@@ -357,10 +377,12 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     const uint32_t* xk32 = reinterpret_cast<const uint32_t*>(a.xkeys);   // little-endian low words
     // accumulator row of input row ylo (input row yi -> row yi - (y0 - 2hy))
     const int arow0 = ylo - y0 + 2 * kg.hy;
+    const bool single = total <= kStageCap;          // the usual case: one chunk, descriptors known
     for (int f0 = 0; f0 < total; f0 += kStageCap) {
         const int f1 = min(total, f0 + kStageCap);
         // ---- stage the chunk: (byte position in a channel slice, value); one warp per item,
-        // coalesced reads of the item's key run
+        // coalesced reads of the item's key run; in the single-chunk case the same warp writes
+        // the item's work descriptors
         for (int pk = warp; pk < PK; pk += kFwdWarps) {
             const int s0 = max(ioff[pk], f0), s1 = min(ioff[pk + 1], f1);
             const uint32_t eb = iglob[pk] - (uint32_t)ioff[pk], rb = ibase[pk];
@@ -372,35 +394,42 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
                 spos[f - f0] = ((yrel + (uint32_t)arow0) * (uint32_t)ZR + z + (uint32_t)t.cz) * 4u;
                 sval[f - f0] = a.xvals[e];
             }
-        }
-        __syncthreads();
-        if (warp == 0) {   // work list of the chunk: groups of <= 64 entries of one item
-            int wcar = 0;
-            for (int p0 = 0; p0 < PK; p0 += 32) {
-                const int pk = p0 + lane;
-                int s0 = 0, s1 = 0;
-                if (pk < PK) {
-                    s0 = max(ioff[pk], f0) - f0;
-                    s1 = min(ioff[pk + 1], f1) - f0;
-                }
-                const int ng = s1 > s0 ? (s1 - s0 + 63) >> 6 : 0;
-                const int inc = warp_incl_scan(ng);
-                for (int gi = 0; gi < ng; ++gi) {
+            if (single)
+                for (int gi = lane; 64 * gi < s1 - s0; gi += 32) {
                     const int st = s0 + 64 * gi;
-                    work[wcar + inc - ng + gi] = (uint32_t)st | ((uint32_t)min(64, s1 - st) << 12) | ((uint32_t)pk << 19);
+                    work[wpre[pk] + gi] = (uint32_t)st | ((uint32_t)min(64, s1 - st) << 12) | ((uint32_t)pk << 19);
                 }
-                wcar += __shfl_sync(kFull, inc, 31);
-            }
-            if (lane == 0) misc[0] = (uint32_t)wcar;
         }
         __syncthreads();
+        if (!single) {
+            if (warp == 0) {   // work list of the chunk: groups of <= 64 entries of one item
+                int wcar = 0;
+                for (int p0 = 0; p0 < PK; p0 += 32) {
+                    const int pk = p0 + lane;
+                    int s0 = 0, s1 = 0;
+                    if (pk < PK) {
+                        s0 = max(ioff[pk], f0) - f0;
+                        s1 = min(ioff[pk + 1], f1) - f0;
+                    }
+                    const int ng = s1 > s0 ? (s1 - s0 + 63) >> 6 : 0;
+                    const int inc = warp_incl_scan(ng);
+                    for (int gi = 0; gi < ng; ++gi) {
+                        const int st = s0 + 64 * gi;
+                        work[wcar + inc - ng + gi] = (uint32_t)st | ((uint32_t)min(64, s1 - st) << 12) | ((uint32_t)pk << 19);
+                    }
+                    wcar += __shfl_sync(kFull, inc, 31);
+                }
+                if (lane == 0) misc[0] = (uint32_t)wcar;
+            }
+            __syncthreads();
+        }
         // ---- accumulate (Alg. 1 inner loops)
-        const int nwork = (int)misc[0];
+        const int nwork = single ? wtotal : (int)misc[0];
         if (warp < nocl) {
             if (neg0)
-                fwd_items<true>(nwork, lane, accs, safe, work, rpair + warp * PK, recp, spos, sval);
+                fwd_items<true>(nwork, lane, accs, safe, work, roffs + warp * PK, recp, spos, sval);
             else
-                fwd_items<false>(nwork, lane, accs, safe, work, rpair + warp * PK, recp, spos, sval);
+                fwd_items<false>(nwork, lane, accs, safe, work, roffs + warp * PK, recp, spos, sval);
         }
         __syncthreads();
     }
