@@ -218,6 +218,16 @@ spc_status_t sparse_scatter_grad(const int64_t* src_index, const float* dy, int6
                                  cudaStream_t stream);
 
 /* ------------------------------------------------------------------------------------
+ * sparse_to_dense — the sparseToDense() bridge of the OctNet3 stacks (Appendix B, Table 2,
+ *   P:332): dense[key] = value for every stored entry, 0 elsewhere. dense: device float
+ *   [batch*channels*prod(dims)] in [b][c][dims] order (the key layout makes the key the linear
+ *   index, reading R11). sparse_to_dense_bwd: dvalues[i] = ddense[key_i] (the gradient flows only
+ *   to stored entries). Errors: null pointers, bad shape -> SPC_ERR_INVALID_ARG/SHAPE.
+ * ------------------------------------------------------------------------------------ */
+spc_status_t sparse_to_dense(const spc_map_t* x, float* dense, cudaStream_t stream);
+spc_status_t sparse_to_dense_bwd(const spc_map_t* x, const float* ddense, float* dvalues, cudaStream_t stream);
+
+/* ------------------------------------------------------------------------------------
  * Training-loop steps over a sparse filter bank. Elementwise over the STORED
  * weights only: pruned weights are absent and therefore never move or reappear.
  *

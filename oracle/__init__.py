@@ -17,6 +17,7 @@ from .oracle import (  # noqa: F401
     density_bias,
     adagrad_step,
     prune,
+    to_dense,
     ATTN_NONE,
     ATTN_MAGNITUDE,
     ATTN_RAW,

@@ -522,3 +522,18 @@ int64_t ora_prune(int64_t n, const uint64_t* keys, const float* w, const float* 
     }
     return m;
 }
+
+/* sparseToDense() bridge, Appendix B Table 2: dense[b][c][p] = value of the stored entry
+ * with key (b, c, p), 0 elsewhere. The dense array is written through decode_key (the key codec of
+ * P:43), cell by cell. */
+int ora_to_dense(int ndim, const int64_t* dims, int64_t batch, int64_t channels, int64_t n, const uint64_t* keys,
+                 const float* vals, float* dense) {
+    int64_t V = volume_of(ndim, dims);
+    memset(dense, 0, sizeof(float) * (size_t)(batch * channels * V));
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t b, c, p[ORA_MAXDIM];
+        if (decode_key(keys[i], ndim, dims, batch, channels, &b, &c, p) != 0) return -3;
+        dense[(b * channels + c) * V + lin_of(ndim, dims, p)] = vals[i];
+    }
+    return 0;
+}

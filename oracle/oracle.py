@@ -54,6 +54,8 @@ def _load():
         _lib.ora_adagrad_step.restype = C.c_int
         _lib.ora_prune.argtypes = [I64, P, P, P, P, C.c_double, P, P, P, P]
         _lib.ora_prune.restype = C.c_int64
+        _lib.ora_to_dense.argtypes = [C.c_int, P, I64, I64, I64, P, P, P]
+        _lib.ora_to_dense.restype = C.c_int
         for f in ("ora_conv_fwd", "ora_conv_bwd", "ora_topk", "ora_relu", "ora_maxpool",
                   "ora_scatter_grad", "ora_decode_key", "ora_get_update_id"):
             getattr(_lib, f).restype = C.c_int
@@ -231,3 +233,16 @@ def prune(keys, w, acc, warn, eps: float = 0.01):
     if m < 0:
         raise OracleError("ora_prune failed")
     return ok[:m], ow[:m], oa[:m], owr[:m]
+
+
+def to_dense(x):
+    """sparseToDense() (Table 2): dense [batch, channels, *dims] float32 array."""
+    dims = np.asarray(x.dims, np.int64)
+    out = np.zeros((x.batch, x.channels) + tuple(x.dims), np.float32)
+    keys = np.ascontiguousarray(x.keys, np.uint64)
+    vals = np.ascontiguousarray(x.values, np.float32)
+    rc = _load().ora_to_dense(len(x.dims), dims.ctypes.data, x.batch, x.channels, keys.size, keys.ctypes.data,
+                              vals.ctypes.data, out.ctypes.data)
+    if rc != 0:
+        raise OracleError(f"ora_to_dense rc={rc}")
+    return out

@@ -26,6 +26,8 @@ from .ops import (  # noqa: F401
     DensityReg,
     adagrad_step,
     filter_prune,
+    sparse_to_dense,
+    sparse_to_dense_bwd,
     kernel_launches,
     profile_enable,
     profile_reset,

@@ -27,6 +27,7 @@ EXPORTS = [
     "spc_relu_query", "sparse_relu",
     "spc_maxpool_query", "sparse_maxpool",
     "sparse_scatter_grad",
+    "sparse_to_dense", "sparse_to_dense_bwd",
     "sparse_adagrad_step", "spc_prune_query", "sparse_filter_prune",
     "spc_kernel_launches", "spc_profile_enable", "spc_profile_reset", "spc_profile_read",
 ]
@@ -99,6 +100,8 @@ def load(path: str = LIB_PATH):
         "sparse_adagrad_step": ([P, P, P, I64, P, C.c_double, C.POINTER(DensityRegT), C.c_double, C.c_double, P],
                                 C.c_int),
         "spc_prune_query": ([I64, sz], C.c_int),
+        "sparse_to_dense": ([pM, P, P], C.c_int),
+        "sparse_to_dense_bwd": ([pM, P, P, P], C.c_int),
         "sparse_filter_prune": ([P, P, P, P, I64, C.c_double, P, P, P, P, P, P, C.c_size_t, P], C.c_int),
         "spc_kernel_launches": ([], C.c_int64),
         "spc_profile_enable": ([C.c_int], C.c_int),

@@ -644,3 +644,17 @@ spc_status_t sparse_filter_prune(const uint64_t* keys, const float* values, cons
     return cu(launch_prune(keys, values, accum, warn, n, eps, out_keys, out_values, out_accum, out_warn, out_nnz_dev,
                            static_cast<uint64_t*>(ws), s));
 }
+
+// ------------------------------------------------------------------ sparseToDense bridge (f3)
+spc_status_t sparse_to_dense(const spc_map_t* x, float* dense, cudaStream_t s) {
+    SPC_TRY(check_map(x));
+    if (!dense) return SPC_ERR_INVALID_ARG;
+    const Geo g = geo_of(x, x->channels);
+    return cu(launch_to_dense(x->keys, x->values, x->nnz_dev, x->nnz, dense, g.B * g.C * g.V, s));
+}
+
+spc_status_t sparse_to_dense_bwd(const spc_map_t* x, const float* ddense, float* dvalues, cudaStream_t s) {
+    SPC_TRY(check_map(x, false));
+    if (!ddense || (x->nnz > 0 && !dvalues)) return SPC_ERR_INVALID_ARG;
+    return cu(launch_gather_dense(x->keys, x->nnz_dev, x->nnz, ddense, dvalues, s));
+}

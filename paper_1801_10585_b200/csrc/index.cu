@@ -3,6 +3,8 @@
 #include "spc_internal.cuh"
 #include "block_scan.cuh"
 
+#include <algorithm>
+
 namespace spc {
 
 // ---------------------------------------------------------------------------- row index
@@ -296,6 +298,41 @@ cudaError_t launch_scatter_grad(const int64_t* src, const float* dy, int64_t n_o
     int64_t grid = (n_out_bound + 255) / 256;
     if (grid > 148 * 16) grid = 148 * 16;
     { SPC_PHASE("scatter_grad", s, 1); scatter_grad_kernel<<<(unsigned)grid, 256, 0, s>>>(src, dy, n_out_bound, n_out_dev, dx, n_in); }
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------- sparseToDense bridge
+// Table 2 "sparseToDense()": the key layout ((b*C + c)*V + row_major(p)) (reading R11)
+// is the linear index of the dense [B, C, dims] tensor, so the bridge is a zero fill plus a
+// scatter of the stored values; its backward gathers the dense gradient at the stored keys.
+__global__ void to_dense_kernel(const uint64_t* __restrict__ keys, const float* __restrict__ vals,
+                                const int64_t* nnz_dev, int64_t bound, float* __restrict__ dense) {
+    const int64_t n = load_n(nnz_dev, bound);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dense[keys[i]] = vals[i];
+}
+
+__global__ void gather_dense_kernel(const uint64_t* __restrict__ keys, const int64_t* nnz_dev, int64_t bound,
+                                    const float* __restrict__ ddense, float* __restrict__ dvals) {
+    const int64_t n = load_n(nnz_dev, bound);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dvals[i] = ddense[keys[i]];
+}
+
+cudaError_t launch_to_dense(const uint64_t* keys, const float* vals, const int64_t* nnz_dev, int64_t bound,
+                            float* dense, int64_t cells, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(dense, 0, (size_t)cells * sizeof(float), s);
+    if (e != cudaSuccess || bound == 0) return e;
+    const unsigned grid = (unsigned)std::min<int64_t>((bound + 255) / 256, 148 * 16);
+    { SPC_PHASE("to_dense", s, 1); to_dense_kernel<<<grid, 256, 0, s>>>(keys, vals, nnz_dev, bound, dense); }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_dense(const uint64_t* keys, const int64_t* nnz_dev, int64_t bound, const float* ddense,
+                                float* dvals, cudaStream_t s) {
+    if (bound == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)std::min<int64_t>((bound + 255) / 256, 148 * 16);
+    { SPC_PHASE("gather_dense", s, 1); gather_dense_kernel<<<grid, 256, 0, s>>>(keys, nnz_dev, bound, ddense, dvals); }
     return cudaGetLastError();
 }
 

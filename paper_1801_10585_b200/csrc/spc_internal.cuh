@@ -288,6 +288,12 @@ cudaError_t launch_prune(const uint64_t* keys, const float* w, const float* acc,
                          double eps, uint64_t* ok, float* ow, float* oacc, uint8_t* owarn, int64_t* out_nnz,
                          uint64_t* ws, cudaStream_t s);
 
+// sparseToDense bridge (index.cu)
+cudaError_t launch_to_dense(const uint64_t* keys, const float* vals, const int64_t* nnz_dev, int64_t bound,
+                            float* dense, int64_t cells, cudaStream_t s);
+cudaError_t launch_gather_dense(const uint64_t* keys, const int64_t* nnz_dev, int64_t bound, const float* ddense,
+                                float* dvals, cudaStream_t s);
+
 // Validation (SPC_VALIDATE=1): flag = 1 if keys are not strictly increasing or out of range.
 cudaError_t launch_validate(const uint64_t* keys, const int64_t* nnz_dev, int64_t nbound, uint64_t limit,
                             int* flag, cudaStream_t s);

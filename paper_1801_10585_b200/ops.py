@@ -413,3 +413,21 @@ def filter_prune(w: SparseFilter, accum: Optional[torch.Tensor], warn: torch.Ten
     m = int(nnz.item())
     wf = SparseFilter(ok[:m].clone(), ov[:m].clone(), w.c_in, w.c_out, w.ksize)
     return wf, (oa[:m].clone() if oa is not None else None), ow[:m].clone()
+
+
+# ------------------------------------------------------------------ sparseToDense bridge (f3)
+def sparse_to_dense(x: SparseMap, stream=None) -> torch.Tensor:
+    """Table 2 sparseToDense(): dense [batch, channels, *dims] tensor, zeros off the map."""
+    dense = torch.empty((x.batch, x.channels) + tuple(x.dims), dtype=torch.float32, device=x.values.device)
+    xs = x.c_struct()
+    check("sparse_to_dense", load().sparse_to_dense(C.byref(xs), _ptr(dense), _stream(stream)))
+    return dense
+
+
+def sparse_to_dense_bwd(x: SparseMap, ddense: torch.Tensor, stream=None) -> torch.Tensor:
+    """Gradient of sparse_to_dense w.r.t. the stored values: ddense at the stored keys."""
+    dv = torch.empty(max(x.nnz_bound, 1), dtype=torch.float32, device=ddense.device)
+    xs = x.c_struct()
+    check("sparse_to_dense_bwd", load().sparse_to_dense_bwd(C.byref(xs), _ptr(ddense.contiguous()), _ptr(dv),
+                                                            _stream(stream)))
+    return dv[:x.nnz_bound]

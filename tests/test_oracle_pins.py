@@ -502,3 +502,29 @@ def test_prune_monotone_and_ordered():
         for k in removed.tolist():
             assert first_low[k] < ep
         prev, keys, acc, warn = nk.size, nk, na, nwr
+
+
+def test_to_dense_pins():
+    """sparseToDense (Table 2): every stored entry lands at the cell its decoded index
+    (b, c, p) names -- numpy's row-major ravel of the decoded tuple -- and all other cells are 0;
+    the dense conv of the bridge equals the bridge of the exact sparse conv (dense xcorr at the
+    support, zero elsewhere)."""
+    x = uniform_map(2, 3, (5, 6, 7), 0.2, 61)
+    d = ora.to_dense(x)
+    idx = np.zeros((x.keys.size, 5), np.int64)
+    for i, k in enumerate(x.keys.tolist()):
+        idx[i] = ora.decode_key(k, x.dims, x.batch, x.channels)
+    ref = np.zeros_like(d)
+    ref[tuple(idx.T)] = x.values
+    np.testing.assert_array_equal(d, ref)
+    import torch
+    w = sparse_filter(3, 2, (3, 3, 3), 1.0, 62)
+    yk, yv, _, _ = ora.conv_fwd(x, w, None)
+    yd = ora.to_dense(COO(2, 2, x.dims, yk, yv))
+    wd = np.zeros((2, 3, 27), np.float64)
+    for k, v in zip(w.keys.tolist(), w.values.tolist()):
+        wd[k // (3 * 27), (k // 27) % 3, k % 27] = v
+    dense = torch.nn.functional.conv3d(torch.from_numpy(d.astype(np.float64)), torch.from_numpy(wd.reshape(2, 3, 3, 3, 3)),
+                                       padding=1).numpy()
+    sup = yd != 0
+    np.testing.assert_allclose(yd[sup], dense[sup], rtol=1e-6, atol=1e-6)

@@ -554,3 +554,16 @@ def test_filter_prune_bit_exact_over_epochs(cuda_lib):
     gk, gv, _ = run_fwd(spc, x, wp, None, "none", 0)
     np.testing.assert_array_equal(gk, fk)
     assert_values_close(gv, fv, fa)
+
+
+# ------------------------------------------------------------ sparseToDense bridge
+def test_sparse_to_dense_and_backward(cuda_lib):
+    spc = cuda_lib
+    for x in (uniform_map(2, 3, (9, 10, 11), 0.1, 71), uniform_map(3, 2, (28, 28), 0.25, 72),
+              COO(1, 2, (4, 4), np.zeros(0, np.uint64), np.zeros(0, np.float32))):
+        X = dev_map(spc, x)
+        d = spc.sparse_to_dense(X)
+        np.testing.assert_array_equal(host(d), ora.to_dense(x))
+        g = torch.randn_like(d)
+        dv = spc.sparse_to_dense_bwd(X, g)
+        np.testing.assert_array_equal(host(dv), host(g).reshape(-1)[x.keys.astype(np.int64)])
