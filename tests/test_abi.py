@@ -115,3 +115,55 @@ def test_product_package_does_not_import_oracle():
             if src and src.endswith(".py"):
                 text = open(src).read()
                 assert "import oracle" not in text and "from oracle" not in text
+
+
+def _map(ndim, batch, ch, dims, nnz):
+    m = MapT()
+    m.ndim, m.batch, m.channels = ndim, batch, ch
+    for i in range(ndim):
+        m.dims[i] = dims[i]
+    m.nnz, m.keys, m.values = nnz, 64, 64   # dummy pointers: host-only calls never read them
+    return m
+
+
+def _filt(ndim, ci, co, ks, nnz):
+    f = FilterT()
+    f.ndim, f.c_in, f.c_out = ndim, ci, co
+    for i in range(ndim):
+        f.ksize[i] = ks[i]
+    f.nnz, f.keys, f.values = nnz, 64, 64
+    return f
+
+
+def test_accumulate_variant_selection_host():
+    """AUTO resolves to the scatter variant on sparse layers (C4: 2 % density, 8 channels) and to
+    the tensor-core variant on dense-row layers (C5 at 50 %); explicit choices are honoured or
+    rejected (G needs c_in <= 32); the G workspace carries the dense input copy."""
+    lib = spc.load()
+    c4m, c4f = _map(3, 64, 8, (128,) * 3, 21474816), _filt(3, 8, 8, (3, 3, 3), 864)
+    assert lib.spc_conv_fwd_variant(C.byref(c4m), C.byref(c4f), 1, 104857, 0) == 1          # S
+    assert lib.spc_conv_fwd_variant(C.byref(c4m), C.byref(c4f), 1, 104857, 2) == 2          # forced G
+    c5m, c5f = _map(3, 8, 32, (64,) * 3, 33554432), _filt(3, 32, 32, (3, 3, 3), 27648)
+    assert lib.spc_conv_fwd_variant(C.byref(c5m), C.byref(c5f), 0, 0, 0) == 2               # G
+    wide_m, wide_f = _map(3, 1, 40, (8, 8, 8), 100), _filt(3, 40, 4, (3, 3, 3), 500)
+    assert lib.spc_conv_fwd_variant(C.byref(wide_m), C.byref(wide_f), 0, 0, 2) == 0          # invalid
+    assert lib.spc_conv_fwd_variant(C.byref(wide_m), C.byref(wide_f), 0, 0, 0) == 1
+    cap, ws_s, ws_g = C.c_int64(), C.c_size_t(), C.c_size_t()
+    assert lib.spc_conv_fwd_query_ex(C.byref(c5m), C.byref(c5f), 0, 0, 1, C.byref(cap), C.byref(ws_s)) == 0
+    assert lib.spc_conv_fwd_query_ex(C.byref(c5m), C.byref(c5f), 0, 0, 2, C.byref(cap), C.byref(ws_g)) == 0
+    assert ws_g.value - ws_s.value >= 8 * 64 ** 3 * 32 * 8          # hi + lo dense copy of the input
+    assert lib.spc_conv_fwd_query_ex(C.byref(wide_m), C.byref(wide_f), 0, 0, 2, C.byref(cap), C.byref(ws_g)) == 6
+
+
+def test_training_and_bridge_argument_checks():
+    lib = spc.load()
+    assert lib.sparse_adagrad_step(None, None, None, -1, None, 1.0, None, 0.1, 1e-8, None) == 1
+    reg = _lib.DensityRegT(0.1, 0.05, 0.1, 0.1, 0.1)
+    assert lib.sparse_adagrad_step(C.c_void_p(64), C.c_void_p(64), C.c_void_p(64), 10, None, 1.0, C.byref(reg),
+                                   0.1, 1e-8, None) == 1                                    # reg without density
+    ws = C.c_size_t()
+    assert lib.spc_prune_query(1000, C.byref(ws)) == 0 and ws.value > 0
+    assert lib.sparse_filter_prune(None, None, None, None, 10, 0.01, None, None, None, None, None, None, 0,
+                                   None) == 1
+    m = _map(2, 1, 1, (4, 4), 3)
+    assert lib.sparse_to_dense(C.byref(m), None, None) == 1
