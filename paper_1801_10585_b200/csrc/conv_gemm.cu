@@ -64,12 +64,18 @@ GemmPlan plan_gemm(const Geo& gx, const Geo& gy, const KGeo& kg) {
     // as many B stages as fit next to the slab (they hide the L2 latency of B_delta, 2..8)
     {
         const size_t room = 200 * 1024 > g.slab_bytes + extra ? 200 * 1024 - g.slab_bytes - extra : 0;
-        g.bstages = (int)std::max<size_t>(2, std::min<size_t>(kSlabMaxStages, room / g.bstage_bytes));
-        // every B_delta resident (small filter banks): one load, then all MMAs back to back
+        // every B_delta resident (small filter banks): one load, then all MMAs back to back;
+        // otherwise two stages of `bgroup` offsets each (one handshake per group, not per offset)
         g.ball = (size_t)g.KV * g.bstage_bytes <= std::min<size_t>(room, 96 * 1024) ? 1 : 0;
-        if (g.ball) g.bstages = g.KV;
+        g.bgroup = (int)std::max<size_t>(1, std::min<size_t>(8, room / (2 * g.bstage_bytes)));
+        g.bstages = g.ball ? g.KV : 2;
     }
-    g.slab_smem = g.slab_bytes + g.bstages * g.bstage_bytes + extra;
+    g.slab_smem = g.slab_bytes + (g.ball ? (size_t)g.KV : (size_t)2 * g.bgroup) * g.bstage_bytes + extra;
+    // several TMEM accumulators, offsets dealt round-robin: consecutive MMAs do not depend on
+    // each other's result (summed in the epilogue)
+    g.nacc = std::max(1, std::min(4, 256 / g.Np));
+    g.tcols_slab = 32;
+    while (g.tcols_slab < g.nacc * g.Np) g.tcols_slab *= 2;
     g.slab = (g.slab_smem <= 200 * 1024 && g.NV * 16 < (1 << 18) && g.SZ * 16 < (1 << 18)) ? 1 : 0;
     if (const char* e = getenv("SPC_GEMM_SLAB")) g.slab = g.slab && e[0] != '0';
     return g;
@@ -401,7 +407,8 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
     const size_t slab_one = (size_t)NV * Kp * 4;           // hi or lo
     uint32_t* occs = reinterpret_cast<uint32_t*>(gsm + 2 * slab_one);
     unsigned char* bst = gsm + g.slab_bytes;
-    uint32_t* wmask = reinterpret_cast<uint32_t*>(bst + S * g.bstage_bytes);
+    uint32_t* wmask = reinterpret_cast<uint32_t*>(
+        bst + (g.ball ? (size_t)KV : (size_t)2 * g.bgroup) * g.bstage_bytes);   // after the B region
     int* dlist = reinterpret_cast<int*>(wmask + KV * Np);   // [nd][dlist KV][uniform KV][slab offset KV]
     uint64_t* mbar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(dlist) +
                                                  (((size_t)(3 * KV + 1) * 4 + 7) & ~(size_t)7));
@@ -414,7 +421,7 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
     for (int i = tid; i < KV * Np; i += kGThreads) wmask[i] = a.wmask[i];
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                     :: "r"((uint32_t)__cvta_generic_to_shared(tslot)), "r"((uint32_t)g.tcols));
+                     :: "r"((uint32_t)__cvta_generic_to_shared(tslot)), "r"((uint32_t)g.tcols_slab));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
@@ -501,10 +508,11 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
                 const uint64_t dAh = dA0 + (uint64_t)((uint32_t)(dsoff[dl[it]] * 16) >> 4);
                 const uint64_t dBh = dB0 + (uint64_t)((uint32_t)(it * g.bstage_bytes) >> 4);
                 const uint64_t dAl = dAh + (uint64_t)(slab_one >> 4), dBl = dBh + (uint64_t)(B_B >> 4);
+                const uint32_t td = tmem + (uint32_t)((it % g.nacc) * Np);
                 for (int ks = 0; ks < Kp / 8; ++ks) {
-                    umma_tf32(tmem, dAh + ks * kA, dBh + ks * kB, idesc, (it | ks) != 0);
-                    umma_tf32(tmem, dAh + ks * kA, dBl + ks * kB, idesc, 1u);
-                    umma_tf32(tmem, dAl + ks * kA, dBh + ks * kB, idesc, 1u);
+                    umma_tf32(td, dAh + ks * kA, dBh + ks * kB, idesc, (it >= g.nacc || ks != 0) ? 1u : 0u);
+                    umma_tf32(td, dAh + ks * kA, dBl + ks * kB, idesc, 1u);
+                    umma_tf32(td, dAl + ks * kA, dBh + ks * kB, idesc, 1u);
                 }
             }
             umma_commit(mb0 + 8u * S);
@@ -512,44 +520,58 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
         mbar_wait(mb0 + 8u * S, 0u);
         tc_fence_after();
     } else if (nd > 0) {
-        // groups 0 .. S-2 in flight up front; group 0 also carries the slab
-        for (int j = 0; j < S - 1; ++j) {
-            if (j < nd) load_b(j, dl[j]);
-            else asm volatile("cp.async.commit_group;" ::: "memory");
-        }
-        for (int it = 0; it < nd; ++it) {
-            const int st = it % S;
-            cp_async_wait_upto(S - 2);   // this thread's group for offset it has landed
+        // two stages, each holding the B of GD consecutive offsets: group j+1 streams in while the
+        // MMAs of group j run; group 0 also carries the slab
+        const int GD = g.bgroup;
+        const int ngrp = (nd + GD - 1) / GD;
+        const size_t gstage = (size_t)GD * g.bstage_bytes;
+        auto load_grp = [&](int st, int grp) {
+            const uint32_t base = bbase + (uint32_t)(st * gstage);
+            for (int j = 0; j < GD && grp * GD + j < nd; ++j) {
+                const int d = dl[grp * GD + j];
+                const float* bh = a.bhi + (size_t)d * Np * Kp;
+                const float* bl = a.blo + (size_t)d * Np * Kp;
+                const uint32_t sb = base + (uint32_t)(j * g.bstage_bytes);
+                for (int c = tid; c < Np * Kp / 4; c += kGThreads) {
+                    cp16(sb + 16u * c, bh + 4 * c, true);
+                    cp16(sb + (uint32_t)B_B + 16u * c, bl + 4 * c, true);
+                }
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        load_grp(0, 0);
+        const uint64_t kA = (uint64_t)(2 * half_plane >> 4), kB = (uint64_t)(Np * 32 >> 4);
+        for (int it = 0; it < ngrp; ++it) {
+            const int st = it & 1;
+            asm volatile("cp.async.wait_group 0;" ::: "memory");   // this thread's share of group it
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(mb0 + 8u * st);
             if (tid == 0) {
-                mbar_wait(mb0 + 8u * st, (uint32_t)((it / S) & 1));
+                mbar_wait(mb0 + 8u * st, (uint32_t)((it >> 1) & 1));
                 tc_fence_after();
-                // descriptors differ only in the start-address field (bits 0..13, 16-byte units):
-                // offsets are added to precomputed base descriptors
-                const uint64_t dAh = dA0 + (uint64_t)((uint32_t)(dsoff[dl[it]] * 16) >> 4);
-                const uint64_t dBh = dB0 + (uint64_t)((uint32_t)(st * g.bstage_bytes) >> 4);
-                const uint64_t dAl = dAh + (uint64_t)(slab_one >> 4), dBl = dBh + (uint64_t)(B_B >> 4);
-                const uint64_t kA = (uint64_t)(2 * half_plane >> 4), kB = (uint64_t)(Np * 32 >> 4);
-#pragma unroll 1
-                for (int ks = 0; ks < Kp / 8; ++ks) {   // hi*hi, hi*lo, lo*hi per K step
-                    const uint32_t acc = (it | ks) != 0;
-                    umma_tf32(tmem, dAh + ks * kA, dBh + ks * kB, idesc, acc);
-                    umma_tf32(tmem, dAh + ks * kA, dBl + ks * kB, idesc, 1u);
-                    umma_tf32(tmem, dAl + ks * kA, dBh + ks * kB, idesc, 1u);
+                for (int j = 0; j < GD && it * GD + j < nd; ++j) {
+                    const int di = it * GD + j;
+                    // descriptors differ only in the start-address field (16-byte units)
+                    const uint64_t dAh = dA0 + (uint64_t)((uint32_t)(dsoff[dl[di]] * 16) >> 4);
+                    const uint64_t dBh = dB0 + (uint64_t)((uint32_t)(st * gstage + (size_t)j * g.bstage_bytes) >> 4);
+                    const uint64_t dAl = dAh + (uint64_t)(slab_one >> 4), dBl = dBh + (uint64_t)(B_B >> 4);
+                    const uint32_t td = tmem + (uint32_t)((di % g.nacc) * Np);
+                    for (int ks = 0; ks < Kp / 8; ++ks) {   // hi*hi, hi*lo, lo*hi per K step
+                        const uint32_t acc = (di >= g.nacc || ks != 0) ? 1u : 0u;
+                        umma_tf32(td, dAh + ks * kA, dBh + ks * kB, idesc, acc);
+                        umma_tf32(td, dAh + ks * kA, dBl + ks * kB, idesc, 1u);
+                        umma_tf32(td, dAl + ks * kA, dBh + ks * kB, idesc, 1u);
+                    }
                 }
                 umma_commit(mb0 + 8u * (S + st));
             }
-            // B of offset it + S - 1 into the slot of offset it - 1 once its MMAs retired
-            const int nx = it + S - 1;
-            if (nx < nd) {
-                if (it >= 1) mbar_wait(mb0 + 8u * (S + (it - 1) % S), (uint32_t)(((it - 1) / S) & 1));
-                load_b(nx % S, dl[nx]);
-            } else {
-                asm volatile("cp.async.commit_group;" ::: "memory");
+            // group it + 1 into the other stage once the MMAs of group it - 1 retired
+            if (it + 1 < ngrp) {
+                if (it >= 1) mbar_wait(mb0 + 8u * (S + (st ^ 1)), (uint32_t)(((it - 1) >> 1) & 1));
+                load_grp(st ^ 1, it + 1);
             }
         }
-        mbar_wait(mb0 + 8u * (S + (nd - 1) % S), (uint32_t)(((nd - 1) / S) & 1));
+        mbar_wait(mb0 + 8u * (S + ((ngrp - 1) & 1)), (uint32_t)(((ngrp - 1) >> 1) & 1));
         tc_fence_after();
     } else {
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -579,10 +601,14 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
     const int64_t p = ((int64_t)x * gy.Y + py) * gy.Z + pz;
     for (int c0 = 0; c0 < Np; c0 += 16) {
         float v[16];
-        if (nd > 0) tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-        else
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+        for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+        for (int ai = 0; ai < min(g.nacc, nd); ++ai) {   // sum the accumulators
+            float u[16];
+            tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(ai * Np + c0), u);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += u[i];
+        }
         if (!pin) continue;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -596,7 +622,7 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
     tc_fence_before();
     __syncthreads();
     if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"((uint32_t)g.tcols));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"((uint32_t)g.tcols_slab));
 }
 
 // Support size and score-digit histogram of each (b, oc) buffer (the scatter variant fuses this

@@ -170,7 +170,7 @@ struct GemmPlan {
     int stages;        // operand stages in shared memory
     size_t stage_bytes, smem;
     // slab form (conv_gemm_slab_kernel): tile 16 rows x 8 z, neighbourhood SX x SY x SZ voxels
-    int slab, SX, SY, SZ, NV, nty, ntz, bstages, ball;
+    int slab, SX, SY, SZ, NV, nty, ntz, bstages, ball, bgroup, nacc, tcols_slab;
     size_t slab_bytes, bstage_bytes, slab_smem;
 };
 struct GemmArgs {
