@@ -159,15 +159,19 @@ __device__ __forceinline__ uint64_t umma_sdesc(uint32_t saddr, uint32_t lbo = 12
     return (uint64_t)((saddr >> 4) & 0x3fffu) | ((uint64_t)((lbo >> 4) & 0x3fffu) << 16) |
            ((uint64_t)((sbo >> 4) & 0x3fffu) << 32) | (1ull << 46);
 }
+// Issued by a whole converged warp; elect.sync picks the lane that issues. (Issuing from one
+// thread of a divergent warp costs ~150 cycles per MMA -- tools/micro/mma_rate.cu -- against
+// 40 cycles for m128n32k8 and 128 for m128n256k8 from a converged warp.)
 __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                           uint32_t accumulate) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
+        "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
         :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ void umma_commit(uint32_t mbar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(mbar) : "memory");
+    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" :: "r"(mbar) : "memory");
 }
 __device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(mbar), "r"(count) : "memory");
@@ -311,7 +315,7 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_kernel(Geo gx, Geo gy, KG
             else asm volatile("cp.async.wait_group 0;" ::: "memory");
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(mb0 + 8u * st);
-            if (tid == 0) {
+            if (warp == 0) {   // converged warp: MMAs issued through elect.sync
                 mbar_wait(mb0 + 8u * st, (uint32_t)((it / S) & 1));
                 tc_fence_after();
                 const uint32_t base = sbase + (uint32_t)(st * g.stage_bytes);
@@ -501,7 +505,7 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         __syncthreads();
-        if (tid == 0) {
+        if (warp == 0) {   // converged warp: MMAs issued through elect.sync
             tc_fence_after();
             const uint64_t kA = (uint64_t)(2 * half_plane >> 4), kB = (uint64_t)(Np * 32 >> 4);
             for (int it = 0; it < nd; ++it) {
@@ -546,7 +550,7 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
             asm volatile("cp.async.wait_group 0;" ::: "memory");   // this thread's share of group it
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(mb0 + 8u * st);
-            if (tid == 0) {
+            if (warp == 0) {   // converged warp: MMAs issued through elect.sync
                 mbar_wait(mb0 + 8u * st, (uint32_t)((it >> 1) & 1));
                 tc_fence_after();
                 for (int j = 0; j < GD && it * GD + j < nd; ++j) {
