@@ -188,8 +188,8 @@ FwdWs carve_fwd(Carver& c, const Geo& gx, const Geo& gy, const KGeo& kg, const F
         ws.g.xhi = c.take<float>(nvox * gp->Kp);
         ws.g.xlo = c.take<float>(nvox * gp->Kp);
         ws.g.occ = c.take<uint32_t>(nvox);
-        ws.g.bhi = c.take<float>((size_t)gp->KV * gp->Np * gp->Kp);
-        ws.g.blo = c.take<float>((size_t)gp->KV * gp->Np * gp->Kp);
+        ws.g.bhi = c.take<float>((size_t)2 * gp->KV * gp->Np * gp->Kp);   // [W_hi ; W_lo] per offset
+        ws.g.blo = nullptr;
         ws.g.wmask = c.take<uint32_t>((size_t)gp->KV * gp->Np);
         ws.g.dinfo = c.take<int>((size_t)3 * gp->KV + 1);
     }

@@ -49,7 +49,8 @@ GemmPlan plan_gemm(const Geo& gx, const Geo& gy, const KGeo& kg) {
     if (const char* e = getenv("SPC_GEMM_STAGES")) want = std::max(2, std::min(kGMaxStages, atoi(e)));
     g.stages = (int)std::min<size_t>((size_t)want, (200 * 1024 - extra) / g.stage_bytes);
     g.smem = g.stages * g.stage_bytes + extra;
-    g.tcols = g.Np <= 32 ? 32 : 64;
+    g.tcols = 32;                                        // D = [A.B_hi | A_hi.B_lo]: 2*Np columns
+    while (g.tcols < 2 * g.Np) g.tcols *= 2;
     g.ok = g.stages >= 2;
     // slab form: M tile = 16 rows (y) x 8 z of one x-plane; the tile's input neighbourhood is
     // staged once and every A_delta is a strided window of it (no per-offset re-gather)
@@ -73,9 +74,9 @@ GemmPlan plan_gemm(const Geo& gx, const Geo& gy, const KGeo& kg) {
     g.slab_smem = g.slab_bytes + (g.ball ? (size_t)g.KV : (size_t)2 * g.bgroup) * g.bstage_bytes + extra;
     // several TMEM accumulators, offsets dealt round-robin: consecutive MMAs do not depend on
     // each other's result (summed in the epilogue)
-    g.nacc = std::max(1, std::min(4, 256 / g.Np));
+    g.nacc = std::max(1, std::min(4, 256 / (2 * g.Np)));
     g.tcols_slab = 32;
-    while (g.tcols_slab < g.nacc * g.Np) g.tcols_slab *= 2;
+    while (g.tcols_slab < g.nacc * 2 * g.Np) g.tcols_slab *= 2;
     g.slab = (g.slab_smem <= 200 * 1024 && g.NV * 16 < (1 << 18) && g.SZ * 16 < (1 << 18)) ? 1 : 0;
     if (const char* e = getenv("SPC_GEMM_SLAB")) g.slab = g.slab && e[0] != '0';
     return g;
@@ -112,10 +113,11 @@ __host__ __device__ inline int canon(int row, int k, int R) {
     return (k >> 3) * R * 8 + (row >> 3) * 64 + ((k & 7) >> 2) * 32 + (row & 7) * 4 + (k & 3);
 }
 
-// Filter -> per-offset B_delta (hi/lo, canonical layout, N = oc, K = ic) and weight masks over ic.
+// Filter -> per-offset B_delta = [W_hi ; W_lo] (canonical layout, N = 2*c_out rows, K = ic) and
+// weight masks over ic. One MMA with the whole operand gives A.W_hi and A.W_lo side by side.
 __global__ void gemm_wprep_kernel(KGeo kg, int c_in, int Kp, int Np, const uint64_t* __restrict__ wk,
                                   const float* __restrict__ wv, int64_t nw, float* __restrict__ bhi,
-                                  float* __restrict__ blo, uint32_t* __restrict__ wmask) {
+                                  uint32_t* __restrict__ wmask) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nw; j += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t key = wk[j];
         const int d = (int)(key % (uint64_t)kg.KV);
@@ -123,9 +125,10 @@ __global__ void gemm_wprep_kernel(KGeo kg, int c_in, int Kp, int Np, const uint6
         const int ic = (int)(r % (uint64_t)c_in), oc = (int)(r / (uint64_t)c_in);
         const float v = wv[j];
         const float hi = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
-        const size_t o = (size_t)d * Np * Kp + canon(oc, ic, Np);
-        bhi[o] = hi;
-        blo[o] = v - hi;
+        // one N = 2*Np operand per offset: rows [0, Np) the high parts, rows [Np, 2Np) the low parts
+        const size_t base = (size_t)d * 2 * Np * Kp;
+        bhi[base + canon(oc, ic, 2 * Np)] = hi;
+        bhi[base + canon(Np + oc, ic, 2 * Np)] = v - hi;
         atomicOr(&wmask[d * Np + oc], 1u << ic);
     }
 }
@@ -287,15 +290,13 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_kernel(Geo gx, Geo gy, KG
             cp16(base + off, a.xhi + q + 4 * c, ok);
             cp16(base + (uint32_t)A_B + off, a.xlo + q + 4 * c, ok);
         }
-        const float* bh = a.bhi + (size_t)d * Np * Kp;
-        const float* bl = a.blo + (size_t)d * Np * Kp;
-        for (int c = tid; c < Np * Kp / 4; c += kGThreads) {
+        const float* bh = a.bhi + (size_t)d * 2 * Np * Kp;
+        for (int c = tid; c < 2 * Np * Kp / 4; c += kGThreads)
             cp16(base + (uint32_t)(2 * A_B) + 16u * c, bh + 4 * c, true);
-            cp16(base + (uint32_t)(2 * A_B + B_B) + 16u * c, bl + 4 * c, true);
-        }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(Np >> 3) << 17) | ((uint32_t)(kGM >> 4) << 24);
+    const uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)((2 * Np) >> 3) << 17) | ((uint32_t)(kGM >> 4) << 24);
 
     // Pipeline over the offsets: every thread gathers its A rows (and a share of B) for offset
     // it + S - 1 while the tensor cores work on offset it. full[st] completes when all 128
@@ -319,14 +320,11 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_kernel(Geo gx, Geo gy, KG
                 mbar_wait(mb0 + 8u * st, (uint32_t)((it / S) & 1));
                 tc_fence_after();
                 const uint32_t base = sbase + (uint32_t)(st * g.stage_bytes);
-                const uint32_t Ah = base, Al = base + (uint32_t)A_B;
-                const uint32_t Bh = base + (uint32_t)(2 * A_B), Bl = Bh + (uint32_t)B_B;
-#pragma unroll 1
-                for (int sp = 0; sp < 3; ++sp) {   // hi*hi, hi*lo, lo*hi
-                    const uint32_t A = sp == 2 ? Al : Ah, B = sp == 1 ? Bl : Bh;
-                    for (int ks = 0; ks < Kp / 8; ++ks)
-                        umma_tf32(tmem, umma_sdesc(A + (uint32_t)(ks * kGM * 32)), umma_sdesc(B + (uint32_t)(ks * Np * 32)),
-                                  idesc, (it | sp | ks) != 0);
+                const uint32_t Ah = base, Al = base + (uint32_t)A_B, Bc = base + (uint32_t)(2 * A_B);
+                for (int ks = 0; ks < Kp / 8; ++ks) {   // A_hi.[W_hi|W_lo] -> D[:, 0:2Np), A_lo.W_hi -> D[:, 0:Np)
+                    const uint64_t db = umma_sdesc(Bc + (uint32_t)(ks * 2 * Np * 32));
+                    umma_tf32(tmem, umma_sdesc(Ah + (uint32_t)(ks * kGM * 32)), db, idesc2, (it | ks) != 0);
+                    umma_tf32(tmem, umma_sdesc(Al + (uint32_t)(ks * kGM * 32)), db, idesc, 1u);
                 }
                 umma_commit(mb0 + 8u * (S + st));
             }
@@ -367,10 +365,16 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_kernel(Geo gx, Geo gy, KG
         }
     for (int c0 = 0; c0 < Np; c0 += 16) {
         float v[16];
-        if (nd > 0) tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-        else
+        if (nd > 0) {
+            float u[16];
+            tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+            tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(Np + c0), u);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += u[i];
+        } else {
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+        }
         if (!pin) continue;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -474,17 +478,8 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
             }
         }
     }
-    auto load_b = [&](int st, int d) {
-        const uint32_t base = bbase + (uint32_t)(st * g.bstage_bytes);
-        const float* bh = a.bhi + (size_t)d * Np * Kp;
-        const float* bl = a.blo + (size_t)d * Np * Kp;
-        for (int c = tid; c < Np * Kp / 4; c += kGThreads) {
-            cp16(base + 16u * c, bh + 4 * c, true);
-            cp16(base + (uint32_t)B_B + 16u * c, bl + 4 * c, true);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(Np >> 3) << 17) | ((uint32_t)(kGM >> 4) << 24);
+    const uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)((2 * Np) >> 3) << 17) | ((uint32_t)(kGM >> 4) << 24);
     const uint32_t lbo_a = (uint32_t)half_plane, sbo_a = (uint32_t)(SZ * 16);
     const uint64_t dA0 = umma_sdesc(sbase, lbo_a, sbo_a), dB0 = umma_sdesc(bbase);
 
@@ -493,12 +488,8 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
         // a single commit -- no per-offset synchronisation
         for (int j = 0; j < nd; ++j) {
             const uint32_t base = bbase + (uint32_t)(j * g.bstage_bytes);
-            const float* bh = a.bhi + (size_t)dl[j] * Np * Kp;
-            const float* bl = a.blo + (size_t)dl[j] * Np * Kp;
-            for (int c = tid; c < Np * Kp / 4; c += kGThreads) {
-                cp16(base + 16u * c, bh + 4 * c, true);
-                cp16(base + (uint32_t)B_B + 16u * c, bl + 4 * c, true);
-            }
+            const float* bh = a.bhi + (size_t)dl[j] * 2 * Np * Kp;
+            for (int c = tid; c < 2 * Np * Kp / 4; c += kGThreads) cp16(base + 16u * c, bh + 4 * c, true);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
         asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -507,16 +498,15 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
         __syncthreads();
         if (warp == 0) {   // converged warp: MMAs issued through elect.sync
             tc_fence_after();
-            const uint64_t kA = (uint64_t)(2 * half_plane >> 4), kB = (uint64_t)(Np * 32 >> 4);
+            const uint64_t kA = (uint64_t)(2 * half_plane >> 4), kB = (uint64_t)(2 * Np * 32 >> 4);
             for (int it = 0; it < nd; ++it) {
                 const uint64_t dAh = dA0 + (uint64_t)((uint32_t)(dsoff[dl[it]] * 16) >> 4);
-                const uint64_t dBh = dB0 + (uint64_t)((uint32_t)(it * g.bstage_bytes) >> 4);
-                const uint64_t dAl = dAh + (uint64_t)(slab_one >> 4), dBl = dBh + (uint64_t)(B_B >> 4);
-                const uint32_t td = tmem + (uint32_t)((it % g.nacc) * Np);
-                for (int ks = 0; ks < Kp / 8; ++ks) {
-                    umma_tf32(td, dAh + ks * kA, dBh + ks * kB, idesc, (it >= g.nacc || ks != 0) ? 1u : 0u);
-                    umma_tf32(td, dAh + ks * kA, dBl + ks * kB, idesc, 1u);
-                    umma_tf32(td, dAl + ks * kA, dBh + ks * kB, idesc, 1u);
+                const uint64_t dBc = dB0 + (uint64_t)((uint32_t)(it * g.bstage_bytes) >> 4);
+                const uint64_t dAl = dAh + (uint64_t)(slab_one >> 4);
+                const uint32_t td = tmem + (uint32_t)((it % g.nacc) * 2 * Np);
+                for (int ks = 0; ks < Kp / 8; ++ks) {   // A_hi.[W_hi|W_lo], then A_lo.W_hi
+                    umma_tf32(td, dAh + ks * kA, dBc + ks * kB, idesc2, (it >= g.nacc || ks != 0) ? 1u : 0u);
+                    umma_tf32(td, dAl + ks * kA, dBc + ks * kB, idesc, 1u);
                 }
             }
             umma_commit(mb0 + 8u * S);
@@ -533,18 +523,14 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
             const uint32_t base = bbase + (uint32_t)(st * gstage);
             for (int j = 0; j < GD && grp * GD + j < nd; ++j) {
                 const int d = dl[grp * GD + j];
-                const float* bh = a.bhi + (size_t)d * Np * Kp;
-                const float* bl = a.blo + (size_t)d * Np * Kp;
+                const float* bh = a.bhi + (size_t)d * 2 * Np * Kp;
                 const uint32_t sb = base + (uint32_t)(j * g.bstage_bytes);
-                for (int c = tid; c < Np * Kp / 4; c += kGThreads) {
-                    cp16(sb + 16u * c, bh + 4 * c, true);
-                    cp16(sb + (uint32_t)B_B + 16u * c, bl + 4 * c, true);
-                }
+                for (int c = tid; c < 2 * Np * Kp / 4; c += kGThreads) cp16(sb + 16u * c, bh + 4 * c, true);
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
         load_grp(0, 0);
-        const uint64_t kA = (uint64_t)(2 * half_plane >> 4), kB = (uint64_t)(Np * 32 >> 4);
+        const uint64_t kA = (uint64_t)(2 * half_plane >> 4), kB = (uint64_t)(2 * Np * 32 >> 4);
         for (int it = 0; it < ngrp; ++it) {
             const int st = it & 1;
             asm volatile("cp.async.wait_group 0;" ::: "memory");   // this thread's share of group it
@@ -557,14 +543,13 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
                     const int di = it * GD + j;
                     // descriptors differ only in the start-address field (16-byte units)
                     const uint64_t dAh = dA0 + (uint64_t)((uint32_t)(dsoff[dl[di]] * 16) >> 4);
-                    const uint64_t dBh = dB0 + (uint64_t)((uint32_t)(st * gstage + (size_t)j * g.bstage_bytes) >> 4);
-                    const uint64_t dAl = dAh + (uint64_t)(slab_one >> 4), dBl = dBh + (uint64_t)(B_B >> 4);
-                    const uint32_t td = tmem + (uint32_t)((di % g.nacc) * Np);
-                    for (int ks = 0; ks < Kp / 8; ++ks) {   // hi*hi, hi*lo, lo*hi per K step
+                    const uint64_t dBc = dB0 + (uint64_t)((uint32_t)(st * gstage + (size_t)j * g.bstage_bytes) >> 4);
+                    const uint64_t dAl = dAh + (uint64_t)(slab_one >> 4);
+                    const uint32_t td = tmem + (uint32_t)((di % g.nacc) * 2 * Np);
+                    for (int ks = 0; ks < Kp / 8; ++ks) {   // A_hi.[W_hi|W_lo], then A_lo.W_hi
                         const uint32_t acc = (di >= g.nacc || ks != 0) ? 1u : 0u;
-                        umma_tf32(td, dAh + ks * kA, dBh + ks * kB, idesc, acc);
-                        umma_tf32(td, dAh + ks * kA, dBl + ks * kB, idesc, 1u);
-                        umma_tf32(td, dAl + ks * kA, dBh + ks * kB, idesc, 1u);
+                        umma_tf32(td, dAh + ks * kA, dBc + ks * kB, idesc2, acc);
+                        umma_tf32(td, dAl + ks * kA, dBc + ks * kB, idesc, 1u);
                     }
                 }
                 umma_commit(mb0 + 8u * (S + st));
@@ -607,11 +592,12 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
         float v[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = 0.0f;
-        for (int ai = 0; ai < min(g.nacc, nd); ++ai) {   // sum the accumulators
-            float u[16];
-            tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(ai * Np + c0), u);
+        for (int ai = 0; ai < min(g.nacc, nd); ++ai) {   // sum the accumulators, both halves of each
+            float u[16], w2[16];
+            tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(ai * 2 * Np + c0), u);
+            tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(ai * 2 * Np + Np + c0), w2);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] += u[i];
+            for (int i = 0; i < 16; ++i) v[i] += u[i] + w2[i];
         }
         if (!pin) continue;
 #pragma unroll
@@ -662,8 +648,7 @@ cudaError_t launch_conv_gemm(const Geo& gx, const Geo& gy, const KGeo& kg, const
     cudaMemsetAsync(ga.xhi, 0, nvox * g.Kp * sizeof(float), s);
     cudaMemsetAsync(ga.xlo, 0, nvox * g.Kp * sizeof(float), s);
     cudaMemsetAsync(ga.occ, 0, nvox * sizeof(uint32_t), s);
-    cudaMemsetAsync(ga.bhi, 0, (size_t)g.KV * g.Np * g.Kp * sizeof(float), s);
-    cudaMemsetAsync(ga.blo, 0, (size_t)g.KV * g.Np * g.Kp * sizeof(float), s);
+    cudaMemsetAsync(ga.bhi, 0, (size_t)2 * g.KV * g.Np * g.Kp * sizeof(float), s);
     cudaMemsetAsync(ga.wmask, 0, (size_t)g.KV * g.Np * sizeof(uint32_t), s);
     {
         SPC_PHASE("gemm_densify", s, 1);
@@ -672,7 +657,7 @@ cudaError_t launch_conv_gemm(const Geo& gx, const Geo& gy, const KGeo& kg, const
     }
     {
         SPC_PHASE("gemm_wprep", s, 1);
-        gemm_wprep_kernel<<<32, 256, 0, s>>>(kg, (int)gx.C, g.Kp, g.Np, ga.wkeys, ga.wvals, ga.nw, ga.bhi, ga.blo,
+        gemm_wprep_kernel<<<32, 256, 0, s>>>(kg, (int)gx.C, g.Kp, g.Np, ga.wkeys, ga.wvals, ga.nw, ga.bhi,
                                              ga.wmask);
     }
     {
