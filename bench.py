@@ -183,7 +183,7 @@ def run_ours(args):
     X = spc.SparseMap.from_arrays(x.keys, x.values, x.batch, x.channels, x.dims)
     W = spc.SparseFilter.from_arrays(w.keys, w.values, w.c_in, w.c_out, w.ksize)
     bias_t = torch.from_numpy(bias).cuda()
-    fwd = spc.FwdPlan(X, W, "magnitude", k, args.variant, bias_t)
+    fwd = spc.FwdPlan(X, W, "magnitude", k, args.variant, bias_t, args.samples_per_pass)
     args.resolved_variant = fwd.resolved
     cap = fwd.capacity
     dy_t = torch.from_numpy(grad_values(cap, SEED_BASE + 7 + rank)).cuda()
@@ -291,6 +291,8 @@ def run_ours(args):
                 "global_batch": BATCH,
                 "density": args.density,
                 "fwd_variant": f"{args.variant} -> {args.resolved_variant}",
+                "fwd_samples_per_pass": args.samples_per_pass or "all",
+                "fwd_workspace_gb": round(fwd.ws_bytes / 1e9, 3),
                 "parallelism": f"dp{world}",
                 "l2": "flushed between timed steps (512 MB write); inputs also exceed L2",
             },
@@ -386,7 +388,7 @@ def run_e2e(torch, spc, x, w, bias, k, cap, dy_dev, args, world, dist):
     W = spc.SparseFilter.from_arrays(w.keys, w.values, w.c_in, w.c_out, w.ksize)
     bias_t = torch.from_numpy(bias).cuda()
     Xs = [spc.SparseMap(bk, bv, x.batch, x.channels, x.dims, x.nnz, None) for bk, bv, _ in bufs]
-    fwd = spc.FwdPlan(Xs[0], W, "magnitude", k, args.resolved_variant)
+    fwd = spc.FwdPlan(Xs[0], W, "magnitude", k, args.resolved_variant, None, args.samples_per_pass)
     for bk, bv, bd in bufs:
         bk.copy_(hk)
         bv.copy_(hv)
@@ -530,6 +532,8 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", default="measure", choices=["auto", "scatter", "gemm", "measure"],
                     help="forward accumulate variant (SURVEY §8 a3); 'measure' times both once and keeps the faster")
+    ap.add_argument("--samples-per-pass", type=int, default=None,
+                    help="bounded-memory forward (sparse_conv_fwd_pass, SURVEY §8 f2): samples per pass")
     args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference(args)

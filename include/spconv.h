@@ -146,6 +146,22 @@ spc_status_t sparse_conv_fwd_ex(const spc_map_t* x, const spc_filter_t* w, const
 int spc_conv_fwd_variant(const spc_map_t* x, const spc_filter_t* w, spc_attn_t attn, int64_t k,
                          spc_variant_t variant);
 
+/* Batch-sliced forward (memory). The paper keeps ONE temporary dense buffer and
+ * reuses it across (b, oc) (Table 1 "Sparse Temp" = r^k * 8 bytes, Appendix A
+ * "a temporary buffer, which can be reused in all layers"). sparse_conv_fwd holds the buffer,
+ * candidate and staging lists of every (b, oc) at once (fastest: one launch per stage for the
+ * whole batch); sparse_conv_fwd_pass sizes them for samples_per_pass samples and runs
+ * ceil(batch / samples_per_pass) passes of the scatter pipeline on `stream`, appending each
+ * pass's outputs in key order -- the output is identical (bit for bit) to sparse_conv_fwd's
+ * scatter variant. samples_per_pass: 1..batch, 0 = batch. Workspace from
+ * spc_conv_fwd_query_pass (same samples_per_pass); out_capacity as spc_conv_fwd_query.
+ * Errors: as sparse_conv_fwd; SPC_ERR_UNSUPPORTED when the scatter variant does not fit. */
+spc_status_t spc_conv_fwd_query_pass(const spc_map_t* x, const spc_filter_t* w, spc_attn_t attn, int64_t k,
+                                     int64_t samples_per_pass, int64_t* out_capacity, size_t* workspace_bytes);
+spc_status_t sparse_conv_fwd_pass(const spc_map_t* x, const spc_filter_t* w, const float* bias,
+                                  spc_attn_t attn, int64_t k, int64_t samples_per_pass, spc_map_out_t* y,
+                                  void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
 /* ------------------------------------------------------------------------------------
  * Backward of the convolution, Alg. 2 with the masked rule of Eqs. (3)/(4)
  * (P:121-129): gradients exist only at stored inputs and stored (unpruned) weights.
@@ -226,6 +242,31 @@ spc_status_t sparse_scatter_grad(const int64_t* src_index, const float* dy, int6
  * ------------------------------------------------------------------------------------ */
 spc_status_t sparse_to_dense(const spc_map_t* x, float* dense, cudaStream_t stream);
 spc_status_t sparse_to_dense_bwd(const spc_map_t* x, const float* ddense, float* dvalues, cudaStream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * Memory model (§3, Table 1, §4.1, Appendix A).
+ *
+ * spc_memory_estimate — the paper's theoretical footprint of one layer's result (host only, no
+ *   GPU work): cells = r^ndim,
+ *     dense  = cells * batch * channels * 4                          (fp32 dense tensor)
+ *     sparse = ceil(rho_up * cells) * batch * channels * (index_bits/8 + 4)   (keys + fp32)
+ *     temp   = cells * 8                                  (one reused 64-bit buffer per voxel)
+ *   (reading R15). index_bits 32 or 64. SPC_ERR_UNSUPPORTED for 32-bit indices when
+ *   cells*batch*channels >= 2^32 (Appendix A: "32 bit indices can only be used for resolutions
+ *   r < 256^3 due to buffer overflows"; Table 1 prints "-" there). Outputs in bytes (NULL = skip).
+ *
+ * sparse_keys_narrow / sparse_keys_widen — the "Sparse 32" storage of Table 1: keys32[i] =
+ *   (uint32_t)keys[i] and back, for maps whose key space batch*channels*prod(dims) < 2^32
+ *   (else SPC_ERR_UNSUPPORTED). 8 instead of 12 bytes per stored entry between layers; the
+ *   layer kernels take 64-bit keys. Device arrays of nnz (bound) entries; the device count
+ *   nnz_dev (or nnz) limits the copy. Asynchronous on `stream`.
+ * ------------------------------------------------------------------------------------ */
+spc_status_t spc_memory_estimate(int32_t ndim, int64_t r, int64_t batch, int64_t channels, double rho_up,
+                                 int32_t index_bits, double* dense_bytes, double* sparse_bytes,
+                                 double* temp_bytes);
+spc_status_t sparse_keys_narrow(const spc_map_t* x, uint32_t* keys32, cudaStream_t stream);
+spc_status_t sparse_keys_widen(const uint32_t* keys32, const int64_t* nnz_dev, int64_t nnz, uint64_t* keys,
+                               cudaStream_t stream);
 
 /* ------------------------------------------------------------------------------------
  * Training-loop steps over a sparse filter bank. Elementwise over the STORED

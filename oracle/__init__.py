@@ -18,6 +18,7 @@ from .oracle import (  # noqa: F401
     adagrad_step,
     prune,
     to_dense,
+    memory_estimate,
     ATTN_NONE,
     ATTN_MAGNITUDE,
     ATTN_RAW,

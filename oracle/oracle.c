@@ -537,3 +537,25 @@ int ora_to_dense(int ndim, const int64_t* dims, int64_t batch, int64_t channels,
     }
     return 0;
 }
+
+/* ----------------------------------------------------------- memory model
+ * Table 1 and Appendix A / Fig. 7: theoretical memory of a layer's
+ * result for resolution r (spatial rank k), minibatch b, c output channels, upper bound rho_up.
+ *   dense  : one fp32 per grid cell             r^k * b * c * 4      ("Dense convolutions
+ *            require only a single output tensor")
+ *   sparse : indices and data of the <= rho_up * r^k entries per channel,
+ *            ceil(rho_up * r^k) * b * c * (index_bits / 8 + 4)         ("tensors for indices and
+ *            data"; 64- or 32-bit indices and "32 bit floating point" data)
+ *   temp   : the temporary buffer "which can be reused in all layers", one 64-bit entry
+ *            per grid cell, r^k * 8 (reading R15: fits every "Sparse Temp" entry of Table 1)
+ * Returns -1 for 32-bit indices when r^k * b * c >= 2^32 ("32 bit indices can only be used for
+ * resolutions r < 256^3 due to buffer overflows"; Table 1 prints "-" at 256^3). */
+int ora_memory_estimate(int k, int64_t r, int64_t b, int64_t c, double rho_up, int index_bits, double* out3) {
+    double cells = 1.0;
+    for (int d = 0; d < k; ++d) cells *= (double)r;
+    if (index_bits == 32 && cells * (double)b * (double)c >= 4294967296.0) return -1;
+    out3[0] = cells * (double)b * (double)c * 4.0;
+    out3[1] = ceil(rho_up * cells) * (double)b * (double)c * (double)(index_bits / 8 + 4);
+    out3[2] = cells * 8.0;
+    return 0;
+}

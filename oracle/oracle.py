@@ -56,6 +56,8 @@ def _load():
         _lib.ora_prune.restype = C.c_int64
         _lib.ora_to_dense.argtypes = [C.c_int, P, I64, I64, I64, P, P, P]
         _lib.ora_to_dense.restype = C.c_int
+        _lib.ora_memory_estimate.argtypes = [C.c_int, I64, I64, I64, C.c_double, C.c_int, P]
+        _lib.ora_memory_estimate.restype = C.c_int
         for f in ("ora_conv_fwd", "ora_conv_bwd", "ora_topk", "ora_relu", "ora_maxpool",
                   "ora_scatter_grad", "ora_decode_key", "ora_get_update_id"):
             getattr(_lib, f).restype = C.c_int
@@ -246,3 +248,14 @@ def to_dense(x):
     if rc != 0:
         raise OracleError(f"ora_to_dense rc={rc}")
     return out
+
+
+# ------------------------------------------------------------------ memory model (f2)
+def memory_estimate(k: int, r: int, b: int, c: int, rho_up: float, index_bits: int = 64):
+    """Table 1 / Fig. 7: {"dense", "sparse", "temp"} bytes, or None for
+    32-bit indices past 2^32 cells (the paper's overflow caveat)."""
+    out = np.zeros(3, np.float64)
+    rc = _load().ora_memory_estimate(int(k), int(r), int(b), int(c), float(rho_up), int(index_bits), _p(out))
+    if rc < 0:
+        return None
+    return {"dense": float(out[0]), "sparse": float(out[1]), "temp": float(out[2])}

@@ -28,6 +28,9 @@ from .ops import (  # noqa: F401
     filter_prune,
     sparse_to_dense,
     sparse_to_dense_bwd,
+    memory_estimate,
+    keys_narrow,
+    keys_widen,
     kernel_launches,
     profile_enable,
     profile_reset,

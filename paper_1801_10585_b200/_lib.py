@@ -29,6 +29,8 @@ EXPORTS = [
     "sparse_scatter_grad",
     "sparse_to_dense", "sparse_to_dense_bwd",
     "sparse_adagrad_step", "spc_prune_query", "sparse_filter_prune",
+    "spc_conv_fwd_query_pass", "sparse_conv_fwd_pass",
+    "spc_memory_estimate", "sparse_keys_narrow", "sparse_keys_widen",
     "spc_kernel_launches", "spc_profile_enable", "spc_profile_reset", "spc_profile_read",
 ]
 
@@ -103,6 +105,12 @@ def load(path: str = LIB_PATH):
         "sparse_to_dense": ([pM, P, P], C.c_int),
         "sparse_to_dense_bwd": ([pM, P, P, P], C.c_int),
         "sparse_filter_prune": ([P, P, P, P, I64, C.c_double, P, P, P, P, P, P, C.c_size_t, P], C.c_int),
+        "spc_conv_fwd_query_pass": ([pM, pF, C.c_int, I64, I64, pi64, sz], C.c_int),
+        "sparse_conv_fwd_pass": ([pM, pF, P, C.c_int, I64, I64, pO, P, C.c_size_t, P], C.c_int),
+        "spc_memory_estimate": ([C.c_int32, I64, I64, I64, C.c_double, C.c_int32, C.POINTER(C.c_double),
+                                 C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
+        "sparse_keys_narrow": ([pM, P, P], C.c_int),
+        "sparse_keys_widen": ([P, P, I64, P, P], C.c_int),
         "spc_kernel_launches": ([], C.c_int64),
         "spc_profile_enable": ([C.c_int], C.c_int),
         "spc_profile_reset": ([], C.c_int),

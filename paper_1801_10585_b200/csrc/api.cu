@@ -5,6 +5,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <algorithm>
+#include <cmath>
 
 using namespace spc;
 
@@ -487,6 +488,81 @@ spc_status_t sparse_conv_fwd(const spc_map_t* x, const spc_filter_t* w, const fl
     return sparse_conv_fwd_ex(x, w, bias, attn, k, SPC_VARIANT_AUTO, y, workspace, workspace_bytes, s);
 }
 
+// Batch-sliced forward: the per-(b, oc) workspace -- the pre-attention buffer
+// (P:90), candidate and staging lists -- is sized for samples_per_pass samples and reused by
+// ceil(batch / samples_per_pass) passes of the scatter pipeline; the outputs of each pass are
+// appended in key order (samples are independent in Alg. 1).
+spc_status_t spc_conv_fwd_query_pass(const spc_map_t* x, const spc_filter_t* w, spc_attn_t attn, int64_t k,
+                                     int64_t samples_per_pass, int64_t* out_capacity, size_t* workspace_bytes) {
+    Geo gx, gy;
+    KGeo kg;
+    FwdTile t;
+    GemmPlan gp;
+    int64_t cap;
+    int use_gemm;
+    SPC_TRY(fwd_plan(x, w, attn, k, SPC_VARIANT_SCATTER, &gx, &gy, &kg, &t, &gp, &cap, &use_gemm));
+    if (samples_per_pass < 0) return SPC_ERR_INVALID_ARG;
+    Geo gyp = gy;
+    gyp.B = samples_per_pass == 0 ? gy.B : std::min<int64_t>(samples_per_pass, gy.B);
+    Carver m(nullptr);
+    carve_fwd(m, gx, gyp, kg, t, w, attn, nullptr);
+    if (out_capacity) *out_capacity = cap;
+    if (workspace_bytes) *workspace_bytes = m.used;
+    return SPC_OK;
+}
+
+spc_status_t sparse_conv_fwd_pass(const spc_map_t* x, const spc_filter_t* w, const float* bias, spc_attn_t attn,
+                                  int64_t k, int64_t samples_per_pass, spc_map_out_t* y, void* workspace,
+                                  size_t workspace_bytes, cudaStream_t s) {
+    Geo gx, gy;
+    KGeo kg;
+    FwdTile t;
+    GemmPlan gp;
+    int64_t cap;
+    int use_gemm;
+    SPC_TRY(fwd_plan(x, w, attn, k, SPC_VARIANT_SCATTER, &gx, &gy, &kg, &t, &gp, &cap, &use_gemm));
+    if (samples_per_pass < 0) return SPC_ERR_INVALID_ARG;
+    SPC_TRY(check_out(y, cap));
+    const int64_t spp = samples_per_pass == 0 ? std::max<int64_t>(gy.B, 1) : std::min<int64_t>(samples_per_pass, std::max<int64_t>(gy.B, 1));
+    Geo gyp = gy;
+    gyp.B = spp;
+    Carver m(nullptr);
+    carve_fwd(m, gx, gyp, kg, t, w, attn, nullptr);
+    if (!workspace || workspace_bytes < m.used) return SPC_ERR_WORKSPACE;
+    Carver c(workspace);
+    FwdWs ws = carve_fwd(c, gx, gyp, kg, t, w, attn, nullptr);
+    if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
+    SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
+    SPC_TRY(cu(launch_filter_table_fwd(kg, (int)w->c_in, (int)w->c_out, w->keys, w->values, w->nnz, ws.meta2,
+                                       ws.val2, ws.off2, ws.scratch2, s)));
+    FwdArgs a = ws.a;
+    a.xkeys = x->keys;
+    a.x_nnz_dev = x->nnz_dev;
+    a.x_nnz = x->nnz;
+    a.xvals = x->values;
+    a.xrow = ws.xrow;
+    a.meta2 = ws.meta2;
+    a.val2 = ws.val2;
+    a.off2 = ws.off2;
+    a.bias = bias;
+    a.attn = attn;
+    a.k = attn == SPC_ATTN_NONE ? gy.V : k;
+    a.out_keys = y->keys;
+    a.out_vals = y->values;
+    a.out_nnz = y->nnz_dev;
+    if (gy.B == 0) return cu(cudaMemsetAsync(y->nnz_dev, 0, sizeof(int64_t), s));
+    for (int64_t b0 = 0; b0 < gy.B; b0 += spp) {
+        Geo gyl = gy;
+        gyl.B = std::min<int64_t>(spp, gy.B - b0);
+        a.b0 = b0;
+        a.seg0 = b0 * gy.C;
+        a.nseg = gyl.B * gy.C;
+        a.out_append = b0 > 0;
+        SPC_TRY(cu(launch_conv_fwd_pipeline(gx, gyl, kg, t, a, s)));
+    }
+    return SPC_OK;
+}
+
 spc_status_t spc_conv_bwd_query(const spc_map_t* x, const spc_filter_t* w, const spc_map_t* y,
                                 size_t* workspace_bytes) {
     Geo gx, gy;
@@ -657,4 +733,43 @@ spc_status_t sparse_to_dense_bwd(const spc_map_t* x, const float* ddense, float*
     SPC_TRY(check_map(x, false));
     if (!ddense || (x->nnz > 0 && !dvalues)) return SPC_ERR_INVALID_ARG;
     return cu(launch_gather_dense(x->keys, x->nnz_dev, x->nnz, ddense, dvalues, s));
+}
+
+// ------------------------------------------------------------------ memory model (f2)
+extern "C" spc_status_t spc_memory_estimate(int32_t ndim, int64_t r, int64_t batch, int64_t channels, double rho_up,
+                                            int32_t index_bits, double* dense_bytes, double* sparse_bytes,
+                                            double* temp_bytes) {
+    if (ndim < 1 || ndim > SPC_MAX_NDIM || r < 1 || batch < 1 || channels < 1 || !(rho_up > 0.0 && rho_up <= 1.0) ||
+        (index_bits != 32 && index_bits != 64))
+        return SPC_ERR_INVALID_ARG;
+    double cells = 1.0;   // r^k (exact in double up to 2^53)
+    for (int d = 0; d < ndim; ++d) cells *= (double)r;
+    const double space = cells * (double)batch * (double)channels;
+    if (index_bits == 32 && space >= 4294967296.0) return SPC_ERR_UNSUPPORTED;   // App. A
+    if (dense_bytes) *dense_bytes = space * 4.0;
+    if (sparse_bytes) *sparse_bytes = std::ceil(rho_up * cells) * (double)batch * (double)channels * (index_bits / 8 + 4);
+    if (temp_bytes) *temp_bytes = cells * 8.0;
+    return SPC_OK;
+}
+
+// ------------------------------------------------------------------ 32-bit key storage (f2)
+namespace {
+bool fits32(const spc_map_t* x) {
+    double space = (double)x->batch * (double)x->channels;
+    for (int d = 0; d < x->ndim; ++d) space *= (double)x->dims[d];
+    return space < 4294967296.0;
+}
+}  // namespace
+
+extern "C" spc_status_t sparse_keys_narrow(const spc_map_t* x, uint32_t* keys32, cudaStream_t s) {
+    SPC_TRY(check_map(x, false));
+    if (!fits32(x)) return SPC_ERR_UNSUPPORTED;
+    if (x->nnz > 0 && !keys32) return SPC_ERR_INVALID_ARG;
+    return cu(launch_keys_narrow(x->keys, x->nnz_dev, x->nnz, keys32, s));
+}
+
+extern "C" spc_status_t sparse_keys_widen(const uint32_t* keys32, const int64_t* nnz_dev, int64_t nnz, uint64_t* keys,
+                                          cudaStream_t s) {
+    if (nnz < 0 || (nnz > 0 && (!keys32 || !keys))) return SPC_ERR_INVALID_ARG;
+    return cu(launch_keys_widen(keys32, nnz_dev, nnz, keys, s));
 }

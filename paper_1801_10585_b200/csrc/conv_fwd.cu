@@ -285,7 +285,8 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     const int64_t tile = blockIdx.x;                 // (b, x, ty) flattened
     const int ty = (int)(tile % t.nty);
     const int x = (int)((tile / t.nty) % gy.X);
-    const int64_t b = tile / ((int64_t)t.nty * gy.X);
+    const int64_t bl = tile / ((int64_t)t.nty * gy.X);   // sample within this pass
+    const int64_t b = a.b0 + bl;                        // global sample (input rows)
     const int oc0 = blockIdx.y * t.ocg;
     const int nocl = min(t.ocg, c_out - oc0);
     const int y0 = ty * t.TY, ye = min(y0 + t.TY, gy.Y);
@@ -449,7 +450,7 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     __syncthreads();
     for (int ocl = 0; ocl < nocl; ++ocl) {
         const int oc = oc0 + ocl;
-        const int64_t s = b * c_out + oc;
+        const int64_t s = bl * c_out + oc;
         const float bv = a.bias ? __ldg(&a.bias[oc]) : 0.0f;
         const float* S = acc + ocl * SL + 2 * kg.hy * ZR + t.cz;
         uint32_t cnt = 0;
@@ -527,10 +528,11 @@ __global__ void fwd_find_kernel(FwdArgs a, int64_t nseg) {
     }
 }
 
-// exclusive scan of a per-segment u64 array (single block); total -> *total
-__global__ void seg_scan_u64_kernel(const uint64_t* in, uint64_t* out, int64_t n, int64_t* total) {
+// exclusive scan of a per-segment u64 array (single block); total -> *total. add_base: the scan
+// starts at the value *total holds on entry (appending passes), and *total grows by the sum.
+__global__ void seg_scan_u64_kernel(const uint64_t* in, uint64_t* out, int64_t n, int64_t* total, int add_base = 0) {
     __shared__ uint64_t sm[33];
-    uint64_t carry = 0;
+    uint64_t carry = add_base ? (uint64_t)*total : 0;   // read by all before the first barrier
     for (int64_t base = 0; base < n; base += blockDim.x) {
         const int64_t i = base + threadIdx.x;
         const uint64_t v = i < n ? in[i] : 0;
@@ -822,7 +824,7 @@ __global__ void __launch_bounds__(32 * kWriteWarps) fwd_write_kernel(FwdArgs a, 
     if (n == 0) return;
     const uint2* in = a.stg + a.chunk_stg[it];
     uint64_t out = a.seg_off[s] + a.tile_off[it];
-    const uint64_t kb = (uint64_t)s * (uint64_t)V;
+    const uint64_t kb = ((uint64_t)a.seg0 + (uint64_t)s) * (uint64_t)V;
     // composite(score, p) = (score << 32 | ~p) >= kstar, as two 32-bit compares
     const uint32_t ks = (uint32_t)(st.kstar >> 32), kp = (uint32_t)st.kstar;
     for (uint32_t i0 = 0; i0 < n; i0 += 32) {
@@ -844,7 +846,7 @@ __global__ void __launch_bounds__(32 * kWriteWarps) fwd_write_kernel(FwdArgs a, 
 cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& kg, const FwdTile& t,
                                      const FwdArgs& a, cudaStream_t s, const GemmPlan* gp, const GemmArgs* ga) {
     const int64_t nseg = gy.B * gy.C;
-    if (nseg == 0) return cudaMemsetAsync(a.out_nnz, 0, sizeof(int64_t), s);
+    if (nseg == 0) return a.out_append ? cudaSuccess : cudaMemsetAsync(a.out_nnz, 0, sizeof(int64_t), s);
     if (!gp) {
         cudaError_t e = t.rec_smem
             ? cudaFuncSetAttribute(conv_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem)
@@ -892,7 +894,7 @@ cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& k
     }
     // kept per segment goes to cand_cnt (reused as scratch), then segment offsets
     { SPC_PHASE("fwd_chunk_scan", s, 1); fwd_chunk_scan_kernel<<<(unsigned)nseg, 256, 0, s>>>(a, a.cand_cnt); }
-    { SPC_PHASE("seg_scan", s, 1); seg_scan_u64_kernel<<<1, 1024, 0, s>>>(a.cand_cnt, a.seg_off, nseg, a.out_nnz); }
+    { SPC_PHASE("seg_scan", s, 1); seg_scan_u64_kernel<<<1, 1024, 0, s>>>(a.cand_cnt, a.seg_off, nseg, a.out_nnz, a.out_append); }
     { SPC_PHASE("fwd_write", s, 1); fwd_write_kernel<<<(unsigned)((nseg * a.nchunk + kWriteWarps - 1) / kWriteWarps), 32 * kWriteWarps, 0, s>>>(a, gy.V); }
     return cudaGetLastError();
 }

@@ -336,4 +336,32 @@ cudaError_t launch_gather_dense(const uint64_t* keys, const int64_t* nnz_dev, in
     return cudaGetLastError();
 }
 
+// 32-bit key storage (Table 1 "Sparse 32"): the low word of every key; valid
+// because the caller checked batch*channels*V < 2^32. Elementwise HBM streams.
+__global__ void keys_narrow_kernel(const uint64_t* __restrict__ k, const int64_t* nnz_dev, int64_t bound,
+                                   uint32_t* __restrict__ o) {
+    const int64_t n = load_n(nnz_dev, bound);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        o[i] = (uint32_t)__ldcs(&k[i]);
+}
+__global__ void keys_widen_kernel(const uint32_t* __restrict__ k, const int64_t* nnz_dev, int64_t bound,
+                                  uint64_t* __restrict__ o) {
+    const int64_t n = load_n(nnz_dev, bound);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        o[i] = (uint64_t)__ldcs(&k[i]);
+}
+
+cudaError_t launch_keys_narrow(const uint64_t* keys, const int64_t* nnz_dev, int64_t bound, uint32_t* out, cudaStream_t s) {
+    if (bound == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)std::min<int64_t>((bound + 255) / 256, 148 * 16);
+    { SPC_PHASE("keys_narrow", s, 1); keys_narrow_kernel<<<grid, 256, 0, s>>>(keys, nnz_dev, bound, out); }
+    return cudaGetLastError();
+}
+cudaError_t launch_keys_widen(const uint32_t* keys, const int64_t* nnz_dev, int64_t bound, uint64_t* out, cudaStream_t s) {
+    if (bound == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)std::min<int64_t>((bound + 255) / 256, 148 * 16);
+    { SPC_PHASE("keys_widen", s, 1); keys_widen_kernel<<<grid, 256, 0, s>>>(keys, nnz_dev, bound, out); }
+    return cudaGetLastError();
+}
+
 }  // namespace spc

@@ -159,6 +159,11 @@ struct FwdArgs {
     uint64_t* out_keys;
     float* out_vals;
     int64_t* out_nnz;
+    // batch-sliced passes (sparse_conv_fwd_pass): this pass covers samples b0 .. b0 + gy.B - 1;
+    // segment s of the pass is global segment b0 * c_out + s; out_append: the pass's outputs go
+    // after the *out_nnz entries already written (and *out_nnz grows by them)
+    int64_t b0, seg0;
+    int out_append;
 };
 // Variant G of the forward accumulate (conv_gemm.cu): tcgen05 TF32 (3xTF32) implicit GEMM over
 // filter offsets, writing the same dense pre-attention buffer as the scatter kernel.
@@ -294,6 +299,8 @@ cudaError_t launch_to_dense(const uint64_t* keys, const float* vals, const int64
 cudaError_t launch_gather_dense(const uint64_t* keys, const int64_t* nnz_dev, int64_t bound, const float* ddense,
                                 float* dvals, cudaStream_t s);
 
+cudaError_t launch_keys_narrow(const uint64_t* keys, const int64_t* nnz_dev, int64_t bound, uint32_t* out, cudaStream_t s);
+cudaError_t launch_keys_widen(const uint32_t* keys, const int64_t* nnz_dev, int64_t bound, uint64_t* out, cudaStream_t s);
 // Validation (SPC_VALIDATE=1): flag = 1 if keys are not strictly increasing or out of range.
 cudaError_t launch_validate(const uint64_t* keys, const int64_t* nnz_dev, int64_t nbound, uint64_t limit,
                             int* flag, cudaStream_t s);

@@ -156,22 +156,32 @@ class FwdPlan:
     variant is picked per layer from measurement")."""
 
     def __init__(self, x: SparseMap, w: SparseFilter, attn: str = "magnitude", k: int = 0, variant: str = "auto",
-                 bias: Optional[torch.Tensor] = None):
+                 bias: Optional[torch.Tensor] = None, samples_per_pass: Optional[int] = None):
         lib = load()
         self.attn = ATTN[attn]
         self.k = int(k)
-        if variant == "measure":
-            variant = select_variant(x, w, bias, attn, k)
-        self.variant = VARIANT[variant]
         cap = C.c_int64()
         ws = C.c_size_t()
         xs, fs = x.c_struct(), w.c_struct()
-        check("spc_conv_fwd_query_ex", lib.spc_conv_fwd_query_ex(C.byref(xs), C.byref(fs), self.attn, self.k,
-                                                                 self.variant, C.byref(cap), C.byref(ws)))
-        self.resolved = {1: "scatter", 2: "gemm"}.get(
-            lib.spc_conv_fwd_variant(C.byref(xs), C.byref(fs), self.attn, self.k, self.variant), "?")
+        self.spp = samples_per_pass
+        if samples_per_pass is not None:
+            # batch-sliced scatter forward (spc_conv_fwd_query_pass): workspace for spp samples
+            check("spc_conv_fwd_query_pass", lib.spc_conv_fwd_query_pass(C.byref(xs), C.byref(fs), self.attn, self.k,
+                                                                         int(samples_per_pass), C.byref(cap),
+                                                                         C.byref(ws)))
+            self.variant = VARIANT["scatter"]
+            self.resolved = "scatter"
+        else:
+            if variant == "measure":
+                variant = select_variant(x, w, bias, attn, k)
+            self.variant = VARIANT[variant]
+            check("spc_conv_fwd_query_ex", lib.spc_conv_fwd_query_ex(C.byref(xs), C.byref(fs), self.attn, self.k,
+                                                                     self.variant, C.byref(cap), C.byref(ws)))
+            self.resolved = {1: "scatter", 2: "gemm"}.get(
+                lib.spc_conv_fwd_variant(C.byref(xs), C.byref(fs), self.attn, self.k, self.variant), "?")
         dev = x.values.device
         self.capacity = int(cap.value)
+        self.ws_bytes = int(ws.value)
         self.ws = _workspace(ws.value, dev)
         self.keys, self.vals, self.nnz, self.out = _out(self.capacity, dev)
         self.c_out = w.c_out
@@ -180,9 +190,14 @@ class FwdPlan:
     def __call__(self, x: SparseMap, w: SparseFilter, bias: Optional[torch.Tensor] = None,
                  stream: Optional[torch.cuda.Stream] = None) -> SparseMap:
         xs, fs = x.c_struct(), w.c_struct()
-        rc = load().sparse_conv_fwd_ex(C.byref(xs), C.byref(fs), _ptr(bias), self.attn, self.k, self.variant,
-                                       C.byref(self.out), _ptr(self.ws), self.ws.numel(), _stream(stream))
-        check("sparse_conv_fwd_ex", rc)
+        if self.spp is not None:
+            rc = load().sparse_conv_fwd_pass(C.byref(xs), C.byref(fs), _ptr(bias), self.attn, self.k, int(self.spp),
+                                             C.byref(self.out), _ptr(self.ws), self.ws.numel(), _stream(stream))
+            check("sparse_conv_fwd_pass", rc)
+        else:
+            rc = load().sparse_conv_fwd_ex(C.byref(xs), C.byref(fs), _ptr(bias), self.attn, self.k, self.variant,
+                                           C.byref(self.out), _ptr(self.ws), self.ws.numel(), _stream(stream))
+            check("sparse_conv_fwd_ex", rc)
         return SparseMap(self.keys, self.vals, self.batch, self.c_out, self.dims, self.capacity, self.nnz)
 
 
@@ -224,10 +239,11 @@ def select_variant(x: SparseMap, w: SparseFilter, bias=None, attn: str = "magnit
 
 
 def sparse_conv_fwd(x: SparseMap, w: SparseFilter, bias: Optional[torch.Tensor] = None, attn: str = "magnitude",
-                    k: int = 0, stream=None, variant: str = "auto") -> SparseMap:
+                    k: int = 0, stream=None, variant: str = "auto", samples_per_pass: Optional[int] = None) -> SparseMap:
     """Alg. 1 (P:51-90). attn in {"none", "magnitude", "raw"}; k entries kept per (b, oc);
-    variant in {"auto", "scatter", "gemm", "measure"} (FwdPlan)."""
-    return FwdPlan(x, w, attn, k, variant, bias)(x, w, bias, stream)
+    variant in {"auto", "scatter", "gemm", "measure"} (FwdPlan); samples_per_pass bounds the
+    workspace to that many samples' buffers (sparse_conv_fwd_pass, scatter variant)."""
+    return FwdPlan(x, w, attn, k, variant, bias, samples_per_pass)(x, w, bias, stream)
 
 
 class BwdPlan:
@@ -431,3 +447,29 @@ def sparse_to_dense_bwd(x: SparseMap, ddense: torch.Tensor, stream=None) -> torc
     check("sparse_to_dense_bwd", load().sparse_to_dense_bwd(C.byref(xs), _ptr(ddense.contiguous()), _ptr(dv),
                                                             _stream(stream)))
     return dv[:x.nnz_bound]
+
+
+# ------------------------------------------------------------------ memory model
+def memory_estimate(ndim: int, r: int, batch: int, channels: int, rho_up: float, index_bits: int = 64) -> dict:
+    """Table 1 / Fig. 7 theoretical bytes (spc_memory_estimate): dense, sparse, temp."""
+    d, sp, t = C.c_double(), C.c_double(), C.c_double()
+    check("spc_memory_estimate", load().spc_memory_estimate(int(ndim), int(r), int(batch), int(channels),
+                                                            float(rho_up), int(index_bits), C.byref(d),
+                                                            C.byref(sp), C.byref(t)))
+    return {"dense": d.value, "sparse": sp.value, "temp": t.value}
+
+
+def keys_narrow(x: SparseMap, stream=None) -> torch.Tensor:
+    """Table 1 "Sparse 32" storage: int32 tensor holding the low 32 bits of every key."""
+    out = torch.empty(max(x.nnz_bound, 1), dtype=torch.int32, device=x.keys.device)
+    xs = x.c_struct()
+    check("sparse_keys_narrow", load().sparse_keys_narrow(C.byref(xs), _ptr(out), _stream(stream)))
+    return out[:x.nnz_bound]
+
+
+def keys_widen(keys32: torch.Tensor, nnz_bound: int, nnz_dev: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Inverse of keys_narrow: int64 keys (zero-extended)."""
+    out = torch.empty(max(nnz_bound, 1), dtype=torch.int64, device=keys32.device)
+    check("sparse_keys_widen", load().sparse_keys_widen(_ptr(keys32), _ptr(nnz_dev), int(nnz_bound), _ptr(out),
+                                                        _stream(stream)))
+    return out[:nnz_bound]

@@ -167,3 +167,44 @@ def test_training_and_bridge_argument_checks():
                                    None) == 1
     m = _map(2, 1, 1, (4, 4), 3)
     assert lib.sparse_to_dense(C.byref(m), None, None) == 1
+
+
+# ------------------------------------------------------------------ memory model / passes (f2)
+def test_memory_estimate_matches_oracle():
+    import oracle as ora
+    for k, r, b, c, rho, bits in [(3, 32, 32, 8, 1 / 32, 64), (3, 256, 32, 8, 1 / 256, 64), (3, 128, 32, 8, 1 / 128, 32),
+                                  (2, 28, 256, 8, 0.15, 64), (1, 1000, 3, 5, 0.37, 32), (3, 512, 32, 8, 1 / 512, 64)]:
+        got = spc.memory_estimate(k, r, b, c, rho, bits)
+        want = ora.memory_estimate(k, r, b, c, rho, bits)
+        assert got == want, (k, r, b, c, rho, bits)
+
+
+def test_memory_estimate_errors():
+    lib = spc.load()
+    d = C.c_double()
+    assert lib.spc_memory_estimate(3, 256, 32, 8, 1 / 256, 32, C.byref(d), None, None) == 6   # 2^32 cells
+    assert lib.spc_memory_estimate(3, 256, 32, 8, 1 / 256, 16, C.byref(d), None, None) == 1
+    assert lib.spc_memory_estimate(3, 0, 32, 8, 0.1, 64, None, None, None) == 1
+    assert lib.spc_memory_estimate(3, 8, 1, 1, 0.0, 64, None, None, None) == 1
+    assert lib.spc_memory_estimate(4, 8, 1, 1, 0.5, 64, None, None, None) == 1
+
+
+def test_fwd_pass_workspace_shrinks_with_samples_per_pass():
+    """The per-(b, oc) buffers scale with samples_per_pass (C4: 64 samples -> 1)."""
+    lib = spc.load()
+    m, f = _c4_structs()
+    cap, ws_all, ws_one, ws_full = C.c_int64(), C.c_size_t(), C.c_size_t(), C.c_size_t()
+    assert lib.spc_conv_fwd_query_pass(C.byref(m), C.byref(f), 1, 104857, 0, C.byref(cap), C.byref(ws_all)) == 0
+    assert lib.spc_conv_fwd_query_pass(C.byref(m), C.byref(f), 1, 104857, 1, C.byref(cap), C.byref(ws_one)) == 0
+    assert lib.spc_conv_fwd_query_ex(C.byref(m), C.byref(f), 1, 104857, 1, None, C.byref(ws_full)) == 0
+    assert ws_all.value == ws_full.value
+    assert ws_one.value * 40 < ws_all.value
+    assert cap.value == 64 * 8 * 104857
+    assert lib.spc_conv_fwd_query_pass(C.byref(m), C.byref(f), 1, 104857, -1, C.byref(cap), C.byref(ws_one)) == 1
+
+
+def test_keys_narrow_rejects_large_key_space():
+    lib = spc.load()
+    m, _ = _c4_structs()
+    m.batch, m.channels = 256, 256   # 2^21 * 2^16 = 2^37 keys
+    assert lib.sparse_keys_narrow(C.byref(m), C.c_void_p(64), None) == 6

@@ -528,3 +528,47 @@ def test_to_dense_pins():
                                        padding=1).numpy()
     sup = yd != 0
     np.testing.assert_allclose(yd[sup], dense[sup], rtol=1e-6, atol=1e-6)
+
+
+# ------------------------------------------------------------------ memory model
+def _table1():
+    with open(os.path.join(os.path.dirname(__file__), "golden", "table1_memory.json")) as f:
+        return json.load(f)
+
+
+def test_memory_estimate_table1():
+    """Every cell of Table 1 within one unit of its printed last digit (the paper
+    rounds inconsistently: dense 32^3 = 0.0336 GB is printed 0.04, temp 128^3 = 0.0168 as 0.016)."""
+    t = _table1()
+    for r in (32, 64, 128, 256):
+        m64 = ora.memory_estimate(t["ndim"], r, t["batch"], t["channels"], 1.0 / r, 64)
+        m32 = ora.memory_estimate(t["ndim"], r, t["batch"], t["channels"], 1.0 / r, 32)
+        got = {"dense": m64["dense"], "sparse64": m64["sparse"], "temp": m64["temp"],
+               "sparse32": None if m32 is None else m32["sparse"]}
+        for row, vals in t["rows"].items():
+            want = vals[str(r)]
+            if want is None:
+                assert got[row] is None, (row, r)
+                continue
+            unit = t["printed_unit"][row][str(r)]
+            assert abs(got[row] / 1e9 - want) <= unit + 1e-12, (row, r, got[row] / 1e9, want)
+
+
+def test_memory_estimate_paper_statements():
+    """P:45 (3x at 100 %, break-even 33 %, 97 % less at 1 %) and P:315 (170x at 512^3)."""
+    st = _table1()["statements"]
+    full = ora.memory_estimate(3, 64, 1, 1, 1.0, 64)
+    assert full["sparse"] / full["dense"] == st["dense_vs_sparse64_at_full_density"]["value"]
+    # break-even: sparse == dense at rho = 4 / 12
+    be = st["break_even_density"]["value"]
+    m = ora.memory_estimate(1, 3 * 2 ** 20, 1, 1, be, 64)
+    assert abs(m["sparse"] / m["dense"] - 1.0) < 1e-6
+    one = ora.memory_estimate(3, 100, 1, 1, 0.01, 64)
+    assert abs((1.0 - one["sparse"] / one["dense"]) - st["saving_at_1pct"]["value"]) < 1e-12
+    m512 = ora.memory_estimate(3, 512, 32, 8, 1.0 / 512, 64)
+    assert int(m512["dense"] / m512["sparse"]) == st["ratio_at_512"]["value"]
+    # 32-bit indices: exactly the cells < 2^32 (P:315), 8 of 12 bytes per entry
+    assert ora.memory_estimate(3, 256, 32, 8, 1 / 256, 32) is None
+    assert ora.memory_estimate(3, 256, 32, 7, 1 / 256, 32) is not None
+    a, b = ora.memory_estimate(3, 128, 32, 8, 1 / 128, 32), ora.memory_estimate(3, 128, 32, 8, 1 / 128, 64)
+    assert a["sparse"] * 12 == b["sparse"] * 8 and a["dense"] == b["dense"] and a["temp"] == b["temp"]

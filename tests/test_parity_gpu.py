@@ -567,3 +567,77 @@ def test_sparse_to_dense_and_backward(cuda_lib):
         g = torch.randn_like(d)
         dv = spc.sparse_to_dense_bwd(X, g)
         np.testing.assert_array_equal(host(dv), host(g).reshape(-1)[x.keys.astype(np.int64)])
+
+
+# ------------------------------------------------------------------ batch-sliced forward (f2)
+PASS_CASES = [
+    # name, dims, batch, c_in, c_out, ksize, rho_d, rho_f, samples_per_pass
+    ("1d_b5_spp2", (37,), 5, 2, 3, (3,), 0.2, 0.7, 2),
+    ("2d_b3_spp1", (13, 17), 3, 3, 5, (5, 3), 0.1, 0.8, 1),
+    ("3d_tiles_b3_spp2", (24, 20, 40), 3, 8, 8, (3, 3, 3), 0.03, 0.5, 2),
+    ("3d_wide_oc_b4_spp3", (10, 12, 14), 4, 2, 40, (3, 3, 3), 0.05, 0.3, 3),
+    ("3d_b2_spp_all", (9, 7, 11), 2, 3, 4, (3, 3, 3), 0.08, 0.5, 0),
+]
+
+
+@pytest.mark.parametrize("case", PASS_CASES, ids=lambda c: c[0])
+@pytest.mark.parametrize("attn", ["none", "magnitude", "raw"])
+def test_fwd_pass_matches_oracle_and_full(cuda_lib, case, attn):
+    """sparse_conv_fwd_pass (bounded workspace, ragged last pass): dyadic values bit-exact vs the
+    oracle, and identical (keys and value bits) to the one-shot scatter forward."""
+    spc = cuda_lib
+    _, dims, B, ci, co, ks, rd, rf, spp = case
+    x = uniform_map(B, ci, dims, rd, 1500 + B, values="dyadic")
+    w = sparse_filter(ci, co, ks, rf, 1501, values="dyadic")
+    bias = bias_vector(co, 1502, values="dyadic")
+    V = int(np.prod(dims))
+    k = max(1, V // 20)
+    ok_, ov, _, _ = ora.conv_fwd(x, w, bias, attn=ATTN_ORA[attn], k=k)
+    bt = torch.from_numpy(bias).cuda()
+    y = spc.sparse_conv_fwd(dev_map(spc, x), dev_filter(spc, w), bt, attn, k, samples_per_pass=spp)
+    pk, pv = (host(t) for t in y.trimmed())
+    np.testing.assert_array_equal(pk.view(np.uint64), ok_)
+    np.testing.assert_array_equal(pv, ov)
+    xc = uniform_map(B, ci, dims, rd, 1600 + B)
+    wc = sparse_filter(ci, co, ks, rf, 1601)
+    full = spc.sparse_conv_fwd(dev_map(spc, xc), dev_filter(spc, wc), bt, attn, k, variant="scatter")
+    part = spc.sparse_conv_fwd(dev_map(spc, xc), dev_filter(spc, wc), bt, attn, k, samples_per_pass=spp)
+    fk, fv = (host(t) for t in full.trimmed())
+    qk, qv = (host(t) for t in part.trimmed())
+    np.testing.assert_array_equal(qk, fk)
+    np.testing.assert_array_equal(qv.view(np.uint32), fv.view(np.uint32))
+
+
+def test_fwd_pass_device_nnz_and_empty(cuda_lib):
+    """Chained input (device nnz word, larger bound) and an all-empty batch through the passes."""
+    spc = cuda_lib
+    x = uniform_map(3, 2, (9, 10, 11), 0.1, 7, values="dyadic")
+    w = sparse_filter(2, 3, (3, 3, 3), 0.5, 7, values="dyadic")
+    n = x.keys.size
+    keys = torch.zeros(n + 50, dtype=torch.int64, device="cuda")
+    vals = torch.zeros(n + 50, dtype=torch.float32, device="cuda")
+    keys[:n] = torch.from_numpy(x.keys.view(np.int64)).cuda()
+    vals[:n] = torch.from_numpy(x.values).cuda()
+    xm = spc.SparseMap(keys, vals, x.batch, x.channels, x.dims, n + 50,
+                       torch.tensor([n], dtype=torch.int64, device="cuda"))
+    y = spc.sparse_conv_fwd(xm, dev_filter(spc, w), None, "magnitude", 40, samples_per_pass=1)
+    ok_, ov, _, _ = ora.conv_fwd(x, w, None, attn=ora.ATTN_MAGNITUDE, k=40)
+    gk, gv = (host(t) for t in y.trimmed())
+    np.testing.assert_array_equal(gk.view(np.uint64), ok_)
+    np.testing.assert_array_equal(gv, ov)
+    e = COO(3, 2, (5, 6), np.zeros(0, np.uint64), np.zeros(0, np.float32))
+    y = spc.sparse_conv_fwd(dev_map(spc, e), dev_filter(spc, sparse_filter(2, 3, (3, 3), 0.5, 3)), None,
+                            "magnitude", 4, samples_per_pass=2)
+    assert y.nnz() == 0
+
+
+def test_keys_narrow_widen_roundtrip(cuda_lib):
+    """Table 1 "Sparse 32" storage: the low words of the keys and back, bit-exact."""
+    spc = cuda_lib
+    x = uniform_map(4, 3, (24, 20, 40), 0.05, 9)
+    m = dev_map(spc, x)
+    k32 = spc.keys_narrow(m)
+    assert k32.dtype == torch.int32 and k32.numel() == x.keys.size
+    np.testing.assert_array_equal(host(k32).view(np.uint32), x.keys.astype(np.uint32))
+    back = spc.keys_widen(k32, m.nnz_bound)
+    np.testing.assert_array_equal(host_keys(back), x.keys)
