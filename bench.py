@@ -320,8 +320,10 @@ def run_ours(args):
 
 
 def roofline_for(name, ph, ny, nnz_x, nnz_w, B_local, fwd_macs, bwd_macs, pk, src, clocks):
-    """Roofline of the dominant kernel; algorithmic work per launch."""
-    t = ph["ms_per_step"] / max(ph["launches_per_step"], 1) * 1e-3
+    """Roofline of the dominant kernel: algorithmic work per launch over the
+    average launch duration = the step's work over the kernel's time per step (the batch-sliced
+    forward launches the kernel once per pass, each on 1/passes of the work)."""
+    t = ph["ms_per_step"] * 1e-3
     V = RES ** 3
     nseg = B_local * C_OUT
     hbm = float(pk.get("hbm_gbs", 6650.0))
@@ -338,14 +340,14 @@ def roofline_for(name, ph, ny, nnz_x, nnz_w, B_local, fwd_macs, bwd_macs, pk, sr
                 "peak": round(lsu_fwd, 3), "frac": round(fwd_macs / t / 1e12 / lsu_fwd, 4),
                 "traffic": ncu_traffic(name),
                 "peak_source": f"derived: shared-memory RMW rate 148 SM x 128 B/clk / 8 B per MAC x {sm_mhz:.0f} MHz",
-                "algorithmic": f"{fwd_macs} MACs per launch (Eq. (1) pairs)"}
+                "algorithmic": f"{fwd_macs} MACs per step (Eq. (1) pairs) in {ph['launches_per_step']:g} launch(es)"}
     if name == "conv_bwd":
         lsu_bwd = 148 * 32 * sm_mhz * 1e6 / 1e12   # pair visits/s: one 4-byte G load each
         return {"kernel": name, "bound": "alu", "achieved": round(fwd_macs / t / 1e12, 4), "unit": "Tpair/s",
                 "peak": round(lsu_bwd, 3), "frac": round(fwd_macs / t / 1e12 / lsu_bwd, 4),
                 "traffic": ncu_traffic(name),
                 "peak_source": f"derived: one 4-byte shared gradient load per (entry, weight) pair, 148 SM x 32 lanes/clk x {sm_mhz:.0f} MHz",
-                "algorithmic": f"{fwd_macs} (entry, weight) pairs visited per launch ({bwd_macs} MACs on kept outputs)"}
+                "algorithmic": f"{fwd_macs} (entry, weight) pairs visited per step ({bwd_macs} MACs on kept outputs) in {ph['launches_per_step']:g} launch(es)"}
     per_launch_bytes = {
         "fwd_classify": 4 * nseg * V,
         "fwd_write": 4 * nseg * V + 12 * ny,
@@ -359,7 +361,7 @@ def roofline_for(name, ph, ny, nnz_x, nnz_w, B_local, fwd_macs, bwd_macs, pk, sr
     return {"kernel": name, "bound": "hbm", "achieved": round(gbs, 1), "unit": "GB/s", "peak": hbm,
             "frac": round(gbs / hbm, 4), "traffic": ncu_traffic(name),
             "peak_source": f"{src} (MEASURED_PEAKS.json hbm_gbs)",
-            "algorithmic": f"{per_launch_bytes} bytes per launch"}
+            "algorithmic": f"{per_launch_bytes} bytes per step in {ph['launches_per_step']:g} launch(es)"}
 
 
 def ncu_traffic(kernel):

@@ -865,15 +865,17 @@ cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& k
         cudaError_t eg = launch_conv_gemm(gx, gy, kg, *gp, *ga, a, s);
         if (eg != cudaSuccess) return eg;
     } else {
-        cudaMemsetAsync(a.guard, 0, sizeof(int), s);
-        {
-            SPC_PHASE("value_guard", s, 1);
-            value_guard_kernel<<<148 * 4, 256, 0, s>>>(a.xvals, a.x_nnz_dev, a.x_nnz, a.guard);
-        }
-        {
-            SPC_PHASE("fwd_rounds", s, 1);
-            fwd_rounds_kernel<<<(unsigned)t.n_ocg, 256, 0, s>>>(kg, (int)gx.C, (int)gy.C, t, a.meta2, a.val2, a.off2,
-                                                              a.rnd, a.roff, a.guard);
+        if (!a.out_append) {   // later passes of sparse_conv_fwd_pass reuse the guard and the rounds
+            cudaMemsetAsync(a.guard, 0, sizeof(int), s);
+            {
+                SPC_PHASE("value_guard", s, 1);
+                value_guard_kernel<<<148 * 4, 256, 0, s>>>(a.xvals, a.x_nnz_dev, a.x_nnz, a.guard);
+            }
+            {
+                SPC_PHASE("fwd_rounds", s, 1);
+                fwd_rounds_kernel<<<(unsigned)t.n_ocg, 256, 0, s>>>(kg, (int)gx.C, (int)gy.C, t, a.meta2, a.val2,
+                                                                  a.off2, a.rnd, a.roff, a.guard);
+            }
         }
         {
             SPC_PHASE("conv_fwd", s, 1);
