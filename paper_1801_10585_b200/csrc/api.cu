@@ -306,25 +306,14 @@ spc_status_t conv_bwd_impl(const spc_map_t* x, const spc_filter_t* w, const spc_
 // -------------------------------------------------------------------- selection ws
 struct TopkWs {
     uint32_t* xrow;
-    SelState* st;
-    uint32_t* hist;
-    ChunkRec* rec;
     uint64_t* seg_off;
     int* flag;
 };
 
-int64_t topk_nchunk(const Geo& g, int64_t nnz) {
-    const int64_t maxseg = std::min<int64_t>(g.V, nnz);
-    return std::max<int64_t>(1, (maxseg + kSelChunk - 1) / kSelChunk);
-}
-
-TopkWs carve_topk(Carver& c, const Geo& g, int64_t nnz) {
+TopkWs carve_topk(Carver& c, const Geo& g, int64_t) {
     TopkWs ws{};
     const int64_t nseg = g.B * g.C;
     ws.xrow = c.take<uint32_t>((size_t)(g.B * g.C * g.R + 1));
-    ws.st = c.take<SelState>((size_t)nseg);
-    ws.hist = c.take<uint32_t>((size_t)nseg * kSelBins);
-    ws.rec = c.take<ChunkRec>((size_t)(nseg * topk_nchunk(g, nnz)));
     ws.seg_off = c.take<uint64_t>((size_t)nseg + 1);
     ws.flag = c.take<int>(1);
     return ws;
@@ -618,17 +607,8 @@ spc_status_t attention_topk(const spc_map_t* x, spc_attn_t attn, int64_t k, spc_
     TopkWs ws = carve_topk(c, g, x->nnz);
     if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
     SPC_TRY(cu(launch_row_index(g, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
-    SelSrc src{};
-    src.kind = 1;
-    src.attn = attn;
-    src.nseg = g.B * g.C;
-    src.V = g.V;
-    src.nchunk = topk_nchunk(g, x->nnz);
-    src.keys = x->keys;
-    src.vals = x->values;
-    src.row_ptr = ws.xrow;
-    src.R = g.R;
-    return cu(launch_select(src, k, ws.st, ws.hist, ws.rec, ws.seg_off, y->keys, y->values, src_index, y->nnz_dev, s));
+    return cu(launch_topk(x->keys, x->values, ws.xrow, g.R, g.B * g.C, attn, k, ws.seg_off, y->keys, y->values,
+                          src_index, y->nnz_dev, s));
 }
 
 spc_status_t spc_relu_query(const spc_map_t* x, int64_t* out_capacity, size_t* workspace_bytes) {

@@ -222,41 +222,12 @@ cudaError_t launch_dbias(const Geo& gy, const uint32_t* yrow, const float* dy, d
 cudaError_t launch_f64_to_f32(const double* a, float* b, int64_t n, cudaStream_t s);
 
 // ---------------------------------------------------------------- selection (attention)
-struct SelState {
-    uint32_t prefix;   // known high bits of the threshold score T
-    uint32_t pmask;    // which bits of prefix are known
-    int64_t need;      // entries with score == T to keep (after the last pass)
-    int64_t kept;      // min(k, n) for the segment
-    int32_t keep_all;  // 1: keep every present entry (n <= k or no attention)
-    int32_t pad;
-};
-struct ChunkRec {
-    uint32_t gt, eq;          // entries with score > T / == T in the chunk
-    uint64_t out_off;         // output offset of the chunk within its segment
-    uint64_t tie_before;      // entries == T in earlier chunks of the segment
-};
-constexpr int kSelChunk = 4096;   // elements per chunk (256 threads x 16)
-constexpr int kSelBins = 2048;    // 11-bit digits
-
-// Source of a selection: dense pre-attention buffer (kind 0) or compact COO (kind 1).
-struct SelSrc {
-    int kind;
-    int attn;
-    int64_t nseg;
-    int64_t V;
-    int64_t nchunk;             // chunks per segment (grid.x)
-    // dense
-    const float* pre;           // [nseg*V]
-    const unsigned long long* seg_count;  // support counts per segment (dense)
-    // compact
-    const uint64_t* keys;
-    const float* vals;
-    const uint32_t* row_ptr;    // segment s starts at row_ptr[s*R]
-    int64_t R;
-};
-cudaError_t launch_select(const SelSrc& src, int64_t k, SelState* st, uint32_t* hist, ChunkRec* rec,
-                          uint64_t* seg_off, uint64_t* out_keys, float* out_vals, int64_t* out_src,
-                          int64_t* out_nnz, cudaStream_t s);
+constexpr int kSelBins = 2048;    // 11-bit score digits
+// Standalone attention over a COO map (select.cu): segment s = entries row_ptr[s*R] ..
+// row_ptr[(s+1)*R]; workspace seg_off [nseg].
+cudaError_t launch_topk(const uint64_t* keys, const float* vals, const uint32_t* row_ptr, int64_t R, int64_t nseg,
+                        int attn, int64_t k, uint64_t* seg_off, uint64_t* out_keys, float* out_vals, int64_t* out_src,
+                        int64_t* out_nnz, cudaStream_t s);
 
 // --------------------------------------------------------------------- relu / pool / misc
 cudaError_t launch_relu(const uint64_t* keys, const float* vals, const int64_t* nnz_dev, int64_t nbound,
@@ -267,7 +238,9 @@ struct PoolPlan {
     int PX, PY, PZ;       // pooled dims
     int zchunk;           // pooled z positions per work item
     int nzc;              // z chunks per pooled row
-    int64_t items;        // B*C*PX*PY*nzc
+    int64_t items;        // work items: B*C*PX*PY*nzc (row form) or the tiles (tile form)
+    int tiled;            // tile form: one CTA per (b, c, pooled plane, band of nyb pooled rows)
+    int nyb, nyt;         // pooled rows per tile, tiles per pooled plane
 };
 PoolPlan plan_pool(const Geo& g, int sx, int sy, int sz);
 cudaError_t launch_maxpool(const Geo& g, const PoolPlan& p, const uint64_t* keys, const float* vals,

@@ -345,11 +345,17 @@ def test_relu_parity(cuda_lib):
         np.testing.assert_array_equal(host(src[:yk.shape[0]]), osrc)
 
 
-@pytest.mark.parametrize("dims,stride", [((28, 28), (2, 2)), ((7, 9), (2, 3)), ((16, 16, 16), (2, 2, 2)),
-                                         ((5, 7, 1100), (2, 3, 2)), ((30,), (4,))])
-def test_maxpool_parity(cuda_lib, dims, stride):
+@pytest.mark.parametrize("dims,stride,density", [
+    ((28, 28), (2, 2), 0.3), ((7, 9), (2, 3), 0.3), ((16, 16, 16), (2, 2, 2), 0.3),
+    ((5, 7, 1100), (2, 3, 2), 0.3), ((30,), (4,), 0.3),
+    ((3, 9000), (1, 2), 0.3),                 # PZ > 4096: row form
+    ((5, 21, 3000), (2, 2, 2), 0.1),          # tile form, several bands per plane, ragged band
+    ((9, 11, 13), (3, 1, 4), 0.9),            # dense, ragged windows in every dim
+    ((33, 32, 31), (2, 2, 2), 0.05),          # C4-like density
+])
+def test_maxpool_parity(cuda_lib, dims, stride, density):
     spc = cuda_lib
-    x = uniform_map(2, 3, dims, 0.3, 61, values="dyadic")   # exact ties exercise the argmax rule
+    x = uniform_map(2, 3, dims, density, 61, values="dyadic")   # exact ties exercise the argmax rule
     ok_, ov, oarg = ora.maxpool(x, stride)
     y, arg = spc.sparse_maxpool(dev_map(spc, x), stride)
     yk, yv = y.trimmed()
@@ -641,3 +647,25 @@ def test_keys_narrow_widen_roundtrip(cuda_lib):
     np.testing.assert_array_equal(host(k32).view(np.uint32), x.keys.astype(np.uint32))
     back = spc.keys_widen(k32, m.nnz_bound)
     np.testing.assert_array_equal(host_keys(back), x.keys)
+
+
+@pytest.mark.parametrize("attn", ["magnitude", "raw"])
+def test_topk_ties_across_tiles_and_mixed_segments(cuda_lib, attn):
+    """All-equal magnitudes (one tie class spanning several 8192-entry tiles: the tie quota is
+    carried across tiles in key order), +0/-0 and sign ties, segments below / above k, empty ones."""
+    spc = cuda_lib
+    x = uniform_map(3, 2, (40, 40, 16), 0.5, 45)
+    rng = np.random.default_rng(45)
+    vals = np.where(rng.random(x.nnz) < 0.5, 1.0, -1.0).astype(np.float32)
+    vals[rng.random(x.nnz) < 0.05] = 0.0
+    vals[rng.random(x.nnz) < 0.05] = -0.0
+    seg = (x.keys // np.uint64(40 * 40 * 16)).astype(np.int64)
+    keep = (seg != 2) & ~((seg == 4) & (rng.random(x.nnz) < 0.995))   # segment 2 empty, segment 4 tiny
+    xs = COO(x.batch, x.channels, x.dims, x.keys[keep], vals[keep])
+    for k in (1, 37, 9000, 12000):
+        ok_, ov, osrc = ora.topk(xs, ATTN_ORA[attn], k)
+        y, src = spc.attention_topk(dev_map(spc, xs), attn, k)
+        yk, yv = y.trimmed()
+        np.testing.assert_array_equal(host_keys(yk), ok_)
+        np.testing.assert_array_equal(host(yv).view(np.uint32), ov.view(np.uint32))
+        np.testing.assert_array_equal(host(src[:yk.shape[0]]), osrc)
