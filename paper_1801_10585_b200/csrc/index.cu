@@ -11,7 +11,9 @@ namespace spc {
 // row_ptr[r] = first entry whose key >= r*Z, for r in [0, total_rows]. Each thread takes 8
 // consecutive entries and fills, for each, the gap of rows between its predecessor's row and its
 // own; long empty stretches are filled by the whole warp so they do not serialise on one thread.
-// key / Z by a 64-bit multiply-high with a host-computed reciprocal and one exact correction.
+// key / Z by a multiply-high with a host-computed reciprocal and one exact correction; 32-bit
+// arithmetic throughout when the key space fits (batch*channels*V <= 2^32, the "Sparse 32"
+// condition of Table 1), 64-bit otherwise.
 constexpr int kRiItems = 8;
 
 __device__ __forceinline__ int64_t row_of(uint64_t key, uint64_t Z, uint64_t magic) {
@@ -19,20 +21,26 @@ __device__ __forceinline__ int64_t row_of(uint64_t key, uint64_t Z, uint64_t mag
     if ((q + 1) * Z <= key) ++q;
     return (int64_t)q;
 }
+__device__ __forceinline__ int32_t row_of(uint32_t key, uint32_t Z, uint32_t magic) {
+    uint32_t q = __umulhi(key, magic);     // floor(key / Z) or one less
+    if ((uint64_t)(q + 1) * Z <= key) ++q;
+    return (int32_t)q;
+}
 
-__global__ void __launch_bounds__(256) row_index_kernel(uint64_t Z, uint64_t magic, const uint64_t* __restrict__ keys,
+template <typename K, typename I>   // key word, row / entry index type
+__global__ void __launch_bounds__(256) row_index_kernel(K Z, K magic, const uint64_t* __restrict__ keys,
                                                         const int64_t* nnz_dev, int64_t nbound,
-                                                        uint32_t* __restrict__ row_ptr, int64_t total_rows) {
-    const int64_t n = load_n(nnz_dev, nbound);
-    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRiItems;
+                                                        uint32_t* __restrict__ row_ptr, I total_rows) {
+    const I n = (I)load_n(nnz_dev, nbound);
+    const I i0 = ((I)blockIdx.x * (I)blockDim.x + (I)threadIdx.x) * kRiItems;
     const int lane = threadIdx.x & 31;
-    int64_t prev = (i0 == 0 || i0 > n) ? -1 : row_of(keys[i0 - 1], Z, magic);
+    I prev = (i0 == 0 || i0 > n) ? (I)-1 : (I)row_of((K)keys[i0 - 1], Z, magic);
 #pragma unroll
     for (int u = 0; u < kRiItems; ++u) {
-        const int64_t i = i0 + u;
-        int64_t lo = 0, hi = -1;
+        const I i = i0 + u;
+        I lo = 0, hi = -1;
         if (i < n) {
-            const int64_t r = row_of(keys[i], Z, magic);
+            const I r = (I)row_of((K)keys[i], Z, magic);
             lo = prev + 1;
             hi = r < total_rows ? r : total_rows;
             prev = r;
@@ -42,15 +50,15 @@ __global__ void __launch_bounds__(256) row_index_kernel(uint64_t Z, uint64_t mag
         }
         const bool longgap = hi - lo >= 16;
         if (!longgap)
-            for (int64_t r = lo; r <= hi; ++r) row_ptr[r] = (uint32_t)i;
+            for (I r = lo; r <= hi; ++r) row_ptr[r] = (uint32_t)i;
         unsigned m = __ballot_sync(kFull, longgap);
         while (m) {
             const int src = __ffs(m) - 1;
             m &= m - 1;
-            const int64_t l = __shfl_sync(kFull, lo, src);
-            const int64_t h = __shfl_sync(kFull, hi, src);
-            const int64_t v = __shfl_sync(kFull, i, src);
-            for (int64_t r = l + lane; r <= h; r += 32) row_ptr[r] = (uint32_t)v;
+            const I l = __shfl_sync(kFull, lo, src);
+            const I h = __shfl_sync(kFull, hi, src);
+            const I v = __shfl_sync(kFull, i, src);
+            for (I r = l + lane; r <= h; r += 32) row_ptr[r] = (uint32_t)v;
         }
     }
 }
@@ -61,9 +69,19 @@ cudaError_t launch_row_index(const Geo& g, const uint64_t* keys, const int64_t* 
     const int64_t threads = (nbound + 1 + kRiItems - 1) / kRiItems;
     const int bs = 256;
     const int64_t grid = (threads + bs - 1) / bs;
-    const uint64_t Z = (uint64_t)g.Z;
-    const uint64_t magic = Z == 1 ? ~0ull : ~0ull / Z;   // floor((2^64 - 1) / Z)
-    { SPC_PHASE("row_index", s, 1); row_index_kernel<<<(unsigned)grid, bs, 0, s>>>(Z, magic, keys, nnz_dev, nbound, row_ptr, total_rows); }
+    const double space = (double)g.B * (double)g.C * (double)g.V;
+    SPC_PHASE("row_index", s, 1);
+    if (space <= 4294967296.0 && nbound < (1ll << 30) && total_rows < (1ll << 30)) {
+        const uint32_t Z = (uint32_t)g.Z;
+        const uint32_t magic = Z == 1 ? ~0u : ~0u / Z;
+        row_index_kernel<uint32_t, int32_t><<<(unsigned)grid, bs, 0, s>>>(Z, magic, keys, nnz_dev, nbound, row_ptr,
+                                                                            (int32_t)total_rows);
+    } else {
+        const uint64_t Z = (uint64_t)g.Z;
+        const uint64_t magic = Z == 1 ? ~0ull : ~0ull / Z;   // floor((2^64 - 1) / Z)
+        row_index_kernel<uint64_t, int64_t><<<(unsigned)grid, bs, 0, s>>>(Z, magic, keys, nnz_dev, nbound, row_ptr,
+                                                                            total_rows);
+    }
     return cudaGetLastError();
 }
 

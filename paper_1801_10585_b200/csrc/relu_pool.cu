@@ -41,20 +41,29 @@ __global__ void __launch_bounds__(kReluThreads) relu_write_kernel(const uint64_t
     if (base >= n) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t w0 = base + (int64_t)warp * (32 * kReluItems);
+    const uint64_t pos0 = off[blockIdx.x];   // in flight with the value loads
     float v[kReluItems];
+#pragma unroll
+    for (int u = 0; u < kReluItems; ++u) {
+        const int64_t i = w0 + 32 * u + lane;
+        v[u] = i < n ? vals[i] : 0.0f;
+    }
+    // keys of the kept entries are loaded before the block-wide scan so that their latency
+    // overlaps it
+    uint64_t k[kReluItems];
     unsigned m[kReluItems];
     uint32_t c = 0;
 #pragma unroll
     for (int u = 0; u < kReluItems; ++u) {
         const int64_t i = w0 + 32 * u + lane;
-        v[u] = i < n ? vals[i] : 0.0f;
+        k[u] = v[u] > 0.0f ? keys[i] : 0ull;
         m[u] = __ballot_sync(kFull, v[u] > 0.0f);
         c += (uint32_t)__popc(m[u]);
     }
     __shared__ uint32_t wc[kReluThreads / 32];
     if (lane == 0) wc[warp] = c;
     __syncthreads();
-    uint64_t pos = off[blockIdx.x];
+    uint64_t pos = pos0;
     for (int q = 0; q < warp; ++q) pos += wc[q];
     const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
@@ -62,7 +71,7 @@ __global__ void __launch_bounds__(kReluThreads) relu_write_kernel(const uint64_t
         if (v[u] > 0.0f) {
             const int64_t i = w0 + 32 * u + lane;
             const uint64_t o = pos + (uint32_t)__popc(m[u] & lt);
-            ok[o] = keys[i];
+            ok[o] = k[u];
             ov[o] = v[u];
             if (osrc) osrc[o] = i;
         }
