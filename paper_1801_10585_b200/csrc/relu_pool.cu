@@ -126,10 +126,19 @@ PoolPlan plan_pool(const Geo& g, int sx, int sy, int sz) {
         if ((uint64_t)p.nyb * sy * (uint64_t)g.Z < (1ull << 31)) {
             p.tiled = 1;
             p.nyt = (p.PY + p.nyb - 1) / p.nyb;
+            p.mZ = ~0u / (uint32_t)g.Z;
+            p.msy = ~0u / (uint32_t)sy;
+            p.msz = ~0u / (uint32_t)sz;
             p.items = g.B * g.C * (int64_t)p.PX * p.nyt;
         }
     }
     return p;
+}
+
+// x / d for x < 2^31 with m = floor((2^32 - 1) / d): the multiply-high is exact or one short
+__device__ __forceinline__ uint32_t udiv(uint32_t x, uint32_t d, uint32_t m) {
+    uint32_t q = __umulhi(x, m);
+    return (q + 1) * d <= x ? q + 1 : q;
 }
 
 template <bool WRITE>
@@ -157,21 +166,40 @@ pool_tile_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, const flo
     __syncthreads();
     const int ya = py0 * p.sy, yb = min((py0 + npy) * p.sy, g.Y);
     const uint32_t Z = (uint32_t)g.Z;
-    // pass 1: max per cluster on an order-preserving u32 (occupancy only when counting)
-    for (int dx = 0; dx < p.sx; ++dx) {
-        const int x = px * p.sx + dx;
-        if (x >= g.X) break;
-        const int64_t row0 = (seg * g.X + x) * (int64_t)g.Y + ya;
-        const uint32_t e0 = row_ptr[row0], e1 = row_ptr[row0 + (yb - ya)];
-        const uint64_t kb = (uint64_t)row0 * Z;
-        for (uint32_t e = e0 + tid; e < e1; e += kTileThreads) {
-            const uint32_t rel = (uint32_t)(keys[e] - kb);
-            const uint32_t yy = rel / Z, zz = rel - yy * Z;
-            const int cell = (int)(yy / (uint32_t)p.sy) * p.PZ + (int)(zz / (uint32_t)p.sz);
-            if (WRITE) atomicMax(&best[cell], orderable(vals[e]));
-            else best[cell] = 1u;
+    // f(cell, entry, value) over the member entries: the sx key runs, four loads in flight per thread
+    auto for_members = [&](auto f) {
+        for (int dx = 0; dx < p.sx; ++dx) {
+            const int x = px * p.sx + dx;
+            if (x >= g.X) break;
+            const int64_t row0 = (seg * g.X + x) * (int64_t)g.Y + ya;
+            const uint32_t e0 = row_ptr[row0], e1 = row_ptr[row0 + (yb - ya)];
+            const uint64_t kb = (uint64_t)row0 * Z;
+            for (uint32_t e = e0 + tid; e < e1; e += 4 * kTileThreads) {
+                uint64_t kk[4];
+                float vv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t ee = e + (uint32_t)u * kTileThreads;
+                    kk[u] = ee < e1 ? keys[ee] : kb;
+                    vv[u] = (WRITE && ee < e1) ? vals[ee] : 0.0f;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t ee = e + (uint32_t)u * kTileThreads;
+                    if (ee < e1) {
+                        const uint32_t rel = (uint32_t)(kk[u] - kb);
+                        const uint32_t yy = udiv(rel, Z, p.mZ), zz = rel - yy * Z;
+                        f((int)udiv(yy, (uint32_t)p.sy, p.msy) * p.PZ + (int)udiv(zz, (uint32_t)p.sz, p.msz), ee, vv[u]);
+                    }
+                }
+            }
         }
-    }
+    };
+    // pass 1: max per cluster on an order-preserving u32 (occupancy only when counting)
+    for_members([&](int cell, uint32_t, float v) {
+        if (WRITE) atomicMax(&best[cell], orderable(v));
+        else best[cell] = 1u;
+    });
     __syncthreads();
     if (!WRITE) {
         uint32_t c = 0;
@@ -183,19 +211,9 @@ pool_tile_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, const flo
         return;
     }
     // pass 2 (the runs are L1/L2-resident now): smallest entry index among the maxima
-    for (int dx = 0; dx < p.sx; ++dx) {
-        const int x = px * p.sx + dx;
-        if (x >= g.X) break;
-        const int64_t row0 = (seg * g.X + x) * (int64_t)g.Y + ya;
-        const uint32_t e0 = row_ptr[row0], e1 = row_ptr[row0 + (yb - ya)];
-        const uint64_t kb = (uint64_t)row0 * Z;
-        for (uint32_t e = e0 + tid; e < e1; e += kTileThreads) {
-            const uint32_t rel = (uint32_t)(keys[e] - kb);
-            const uint32_t yy = rel / Z, zz = rel - yy * Z;
-            const int cell = (int)(yy / (uint32_t)p.sy) * p.PZ + (int)(zz / (uint32_t)p.sz);
-            if (orderable(vals[e]) == best[cell]) atomicMin(&arg[cell], e);
-        }
-    }
+    for_members([&](int cell, uint32_t e, float v) {
+        if (orderable(v) == best[cell]) atomicMin(&arg[cell], e);
+    });
     __syncthreads();
     // ordered compaction of the occupied clusters (cell order = (j, warp, lane)): one ballot per
     // j, a scan of the 16 x 8 (j, warp) counts, then the (cell, arg) pairs are staged in place

@@ -4,10 +4,10 @@
 // serves attention_topk.
 //
 // One CTA per segment. Exact radix select on the order-preserving u32 score: up to three digit
-// passes (11, 11, 10 bits) over the segment's values find the threshold T and the number `need`
-// of entries with score == T that are kept; the first pass streams the values from HBM and
-// leaves them in L2 for the later ones (148 x 2 resident segments of a few hundred KB). A final
-// pass compacts in key order -- score > T, or == T while fewer than `need` earlier ties were
+// passes (11, 11, 10 bits) find the threshold T and the number `need` of entries with score == T
+// that are kept. The first digit is counted over the segment's values; when its threshold bucket
+// holds at most 8192 entries their scores are gathered into shared memory and the other digits
+// run there (else over the values again, mostly L2 hits). A final pass compacts in key order -- score > T, or == T while fewer than `need` earlier ties were
 // kept -- with coalesced loads and stores (one ballot per 32 entries, warp totals scanned across
 // the block). Output offsets per segment are known before the select: min(n_s, k).
 #include "spc_internal.cuh"
@@ -19,6 +19,7 @@ constexpr int kTkThreads = 512;
 constexpr int kTkWarps = kTkThreads / 32;
 constexpr int kTkG = 16;                                // groups of 32 entries per warp and tile
 constexpr uint32_t kTkTile = (uint32_t)kTkThreads * kTkG;
+constexpr uint32_t kTkCand = 8192;                      // bucket scores kept in shared memory (32 KB)
 
 // seg_off[s] = sum over earlier segments of kept(s') with kept = n_s if n_s <= k else k
 __global__ void topk_offsets_kernel(const uint32_t* __restrict__ row_ptr, int64_t R, int64_t nseg, int64_t k,
@@ -48,59 +49,99 @@ topk_seg_kernel(const uint64_t* __restrict__ keys, const float* __restrict__ val
     __shared__ uint32_t sm[33];
     __shared__ uint32_t wt[kTkWarps + 1], wk[kTkWarps + 1];
     __shared__ uint32_t sh_bin, sh_need, sh_cnt;
+    __shared__ uint32_t cand[kTkCand];   // scores of the threshold bucket after the first digit
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t s = blockIdx.x;
     const uint32_t lo = row_ptr[s * R], hi = row_ptr[(s + 1) * R];
     const bool keep_all = (uint64_t)(hi - lo) <= (uint64_t)k;
     uint32_t T = 0, pmask = 0, need = 0;
+    // one radix-select step over a histogram h of nb bins: the bin holding the need-th largest
+    auto find_bin = [&](uint32_t nb) {
+        const int per = (int)nb / kTkThreads;   // bins nb-1-per*t .. nb-per*(t+1) for thread t
+        uint32_t own = 0;
+        for (int q = 0; q < per; ++q) own += h[nb - 1 - per * tid - q];
+        uint32_t tot;
+        const uint32_t before = block_excl_scan(own, sm, &tot);
+        if (before < need && before + own >= need) {
+            uint32_t cum = before;
+            for (int q = 0; q < per; ++q) {
+                const uint32_t bin = nb - 1 - per * tid - q, hb = h[bin];
+                if (cum + hb >= need) {
+                    sh_bin = bin;
+                    sh_need = need - cum;
+                    sh_cnt = hb;
+                    break;
+                }
+                cum += hb;
+            }
+        }
+        __syncthreads();
+    };
     if (!keep_all) {
         need = (uint32_t)k;
+        bool in_smem = false;
+        uint32_t ncand = 0;
 #pragma unroll 1
         for (int pass = 0; pass < 3; ++pass) {
             const int sh = pass == 0 ? 21 : (pass == 1 ? 10 : 0);
             const uint32_t nb = pass == 2 ? 1024u : 2048u;
             for (int i = tid; i < kSelBins; i += kTkThreads) h[i] = 0u;
             __syncthreads();
-            // histogram of the next digit among the entries that match the known prefix
-            for (uint32_t i0 = lo + tid; i0 < hi; i0 += 8u * kTkThreads) {
-                uint32_t b[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const uint32_t i = i0 + (uint32_t)u * kTkThreads;
-                    b[u] = i < hi ? __float_as_uint(vals[i]) : 0u;
+            if (in_smem) {   // the candidates of the threshold bucket (pass >= 1)
+                for (uint32_t i = tid; i < ncand; i += kTkThreads) {
+                    const uint32_t sc = cand[i];
+                    if ((sc & pmask) == T) atomicAdd(&h[(sc >> sh) & (nb - 1u)], 1u);
                 }
+            } else {         // the segment's values in global memory
+                for (uint32_t i0 = lo + tid; i0 < hi; i0 += 8u * kTkThreads) {
+                    uint32_t b[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const uint32_t sc = score_bits(b[u], attn);
-                    if (i0 + (uint32_t)u * kTkThreads < hi && (sc & pmask) == T)
-                        atomicAdd(&h[(sc >> sh) & (nb - 1u)], 1u);
-                }
-            }
-            __syncthreads();
-            // bins from the top: thread t owns bins nb-1-per*t .. nb-per*(t+1)
-            const int per = (int)nb / kTkThreads;
-            uint32_t own = 0;
-            for (int q = 0; q < per; ++q) own += h[nb - 1 - per * tid - q];
-            uint32_t tot;
-            const uint32_t before = block_excl_scan(own, sm, &tot);
-            if (before < need && before + own >= need) {
-                uint32_t cum = before;
-                for (int q = 0; q < per; ++q) {
-                    const uint32_t bin = nb - 1 - per * tid - q, hb = h[bin];
-                    if (cum + hb >= need) {
-                        sh_bin = bin;
-                        sh_need = need - cum;
-                        sh_cnt = hb;
-                        break;
+                    for (int u = 0; u < 8; ++u) {
+                        const uint32_t i = i0 + (uint32_t)u * kTkThreads;
+                        b[u] = i < hi ? __float_as_uint(vals[i]) : 0u;
                     }
-                    cum += hb;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const uint32_t sc = score_bits(b[u], attn);
+                        if (i0 + (uint32_t)u * kTkThreads < hi && (sc & pmask) == T)
+                            atomicAdd(&h[(sc >> sh) & (nb - 1u)], 1u);
+                    }
                 }
             }
             __syncthreads();
+            find_bin(nb);
             T |= sh_bin << sh;
             pmask |= (nb - 1u) << sh;
             need = sh_need;
             if (sh_cnt == need) break;   // the whole bucket is kept: no tie split below it
+            if (pass == 0 && sh_cnt <= kTkCand) {
+                // gather the bucket's scores into shared memory; the later digits run there
+                if (tid == 0) sh_cnt = 0;
+                __syncthreads();
+                // warp-uniform trip count (the ballots below need every lane)
+                for (uint32_t w0 = lo + (uint32_t)(tid - lane); w0 < hi; w0 += 8u * kTkThreads) {
+                    const uint32_t i0 = w0 + (uint32_t)lane;
+                    uint32_t b[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const uint32_t i = i0 + (uint32_t)u * kTkThreads;
+                        b[u] = i < hi ? __float_as_uint(vals[i]) : 0u;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const uint32_t sc = score_bits(b[u], attn);
+                        const bool c = i0 + (uint32_t)u * kTkThreads < hi && (sc & pmask) == T;
+                        const unsigned mk = __ballot_sync(kFull, c);
+                        uint32_t slot = 0;
+                        if (lane == 0 && mk) slot = atomicAdd(&sh_cnt, (uint32_t)__popc(mk));
+                        slot = __shfl_sync(kFull, slot, 0);
+                        if (c) cand[slot + __popc(mk & ((1u << lane) - 1u))] = sc;
+                    }
+                }
+                __syncthreads();
+                ncand = sh_cnt;
+                in_smem = true;
+            }
         }
     }
     // ordered compaction
@@ -117,11 +158,19 @@ topk_seg_kernel(const uint64_t* __restrict__ keys, const float* __restrict__ val
 #pragma unroll
         for (int g = 0; g < kTkG; ++g) {
             const uint32_t i = w0 + 32u * g + lane;
+            bits[g] = i < hi ? __float_as_uint(vals[i]) : 0u;
+        }
+        // keys of the entries that may be kept are in flight during the scans below
+        uint64_t kk[kTkG];
+#pragma unroll
+        for (int g = 0; g < kTkG; ++g) {
+            const uint32_t i = w0 + 32u * g + lane;
             const bool in = i < hi;
-            bits[g] = in ? __float_as_uint(vals[i]) : 0u;
             const uint32_t sc = score_bits(bits[g], attn) & pmask;
-            kb[g] = __ballot_sync(kFull, in && (keep_all || sc > T));
-            tb[g] = __ballot_sync(kFull, in && !keep_all && sc == T);
+            const bool keep = in && (keep_all || sc > T), tie = in && !keep_all && sc == T;
+            kk[g] = (keep || tie) ? keys[i] : 0ull;
+            kb[g] = __ballot_sync(kFull, keep);
+            tb[g] = __ballot_sync(kFull, tie);
             ntie += (uint32_t)__popc(tb[g]);
         }
         if (!keep_all) {   // block-uniform: rank the ties in key order, keep the first `need`
@@ -162,7 +211,7 @@ topk_seg_kernel(const uint64_t* __restrict__ keys, const float* __restrict__ val
             if ((kb[g] >> lane) & 1u) {
                 const uint32_t i = w0 + 32u * g + lane;
                 const uint64_t o = pos + (uint32_t)__popc(kb[g] & lt);
-                ok[o] = keys[i];
+                ok[o] = kk[g];
                 ov[o] = __uint_as_float(bits[g]);
                 if (osrc) osrc[o] = (int64_t)i;
             }

@@ -241,6 +241,7 @@ struct PoolPlan {
     int64_t items;        // work items: B*C*PX*PY*nzc (row form) or the tiles (tile form)
     int tiled;            // tile form: one CTA per (b, c, pooled plane, band of nyb pooled rows)
     int nyb, nyt;         // pooled rows per tile, tiles per pooled plane
+    uint32_t mZ, msy, msz;  // floor((2^32 - 1) / d) for d = Z, sy, sz (division by multiply-high)
 };
 PoolPlan plan_pool(const Geo& g, int sx, int sy, int sz);
 cudaError_t launch_maxpool(const Geo& g, const PoolPlan& p, const uint64_t* keys, const float* vals,
