@@ -141,121 +141,127 @@ __device__ __forceinline__ uint32_t udiv(uint32_t x, uint32_t d, uint32_t m) {
     return (q + 1) * d <= x ? q + 1 : q;
 }
 
-template <bool WRITE>
-__global__ void __launch_bounds__(kTileThreads)
-pool_tile_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, const float* __restrict__ vals,
-                 const uint32_t* __restrict__ row_ptr, uint32_t* __restrict__ item_cnt,
-                 const uint64_t* __restrict__ item_off, uint64_t* __restrict__ ok, float* __restrict__ ov,
-                 int64_t* __restrict__ oarg) {
-    __shared__ uint32_t best[kTileCells];
-    __shared__ uint32_t arg[kTileCells];
-    __shared__ uint32_t wcnt[kTileJ * 8 + 1];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t tile = blockIdx.x;
-    const int yt = (int)(tile % p.nyt);
-    const int64_t r = tile / p.nyt;
-    const int px = (int)(r % p.PX);
-    const int64_t seg = r / p.PX;
-    const int py0 = yt * p.nyb, npy = min(p.nyb, p.PY - py0);
-    const int ncell = npy * p.PZ;
-#pragma unroll
-    for (int j = 0; j < kTileJ; ++j) {
-        best[tid + kTileThreads * j] = 0u;
-        if (WRITE) arg[tid + kTileThreads * j] = 0xffffffffu;
-    }
-    __syncthreads();
-    const int ya = py0 * p.sy, yb = min((py0 + npy) * p.sy, g.Y);
+// member entries of a tile: the sx key runs, four loads in flight per thread;
+// f(cell, entry, value) for each (value loaded only when LOADV)
+template <bool LOADV, typename F>
+__device__ __forceinline__ void pool_tile_members(const Geo& g, const PoolPlan& p, const uint64_t* __restrict__ keys,
+                                                  const float* __restrict__ vals,
+                                                  const uint32_t* __restrict__ row_ptr, int64_t seg, int px, int ya,
+                                                  int yb, F f) {
     const uint32_t Z = (uint32_t)g.Z;
-    // f(cell, entry, value) over the member entries: the sx key runs, four loads in flight per thread
-    auto for_members = [&](auto f) {
-        for (int dx = 0; dx < p.sx; ++dx) {
-            const int x = px * p.sx + dx;
-            if (x >= g.X) break;
-            const int64_t row0 = (seg * g.X + x) * (int64_t)g.Y + ya;
-            const uint32_t e0 = row_ptr[row0], e1 = row_ptr[row0 + (yb - ya)];
-            const uint64_t kb = (uint64_t)row0 * Z;
-            for (uint32_t e = e0 + tid; e < e1; e += 4 * kTileThreads) {
-                uint64_t kk[4];
-                float vv[4];
+    for (int dx = 0; dx < p.sx; ++dx) {
+        const int x = px * p.sx + dx;
+        if (x >= g.X) break;
+        const int64_t row0 = (seg * g.X + x) * (int64_t)g.Y + ya;
+        const uint32_t e0 = row_ptr[row0], e1 = row_ptr[row0 + (yb - ya)];
+        const uint64_t kb = (uint64_t)row0 * Z;
+        for (uint32_t e = e0 + threadIdx.x; e < e1; e += 4 * kTileThreads) {
+            uint64_t kk[4];
+            float vv[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const uint32_t ee = e + (uint32_t)u * kTileThreads;
-                    kk[u] = ee < e1 ? keys[ee] : kb;
-                    vv[u] = (WRITE && ee < e1) ? vals[ee] : 0.0f;
-                }
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t ee = e + (uint32_t)u * kTileThreads;
+                kk[u] = ee < e1 ? keys[ee] : kb;
+                vv[u] = (LOADV && ee < e1) ? vals[ee] : 0.0f;
+            }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const uint32_t ee = e + (uint32_t)u * kTileThreads;
-                    if (ee < e1) {
-                        const uint32_t rel = (uint32_t)(kk[u] - kb);
-                        const uint32_t yy = udiv(rel, Z, p.mZ), zz = rel - yy * Z;
-                        f((int)udiv(yy, (uint32_t)p.sy, p.msy) * p.PZ + (int)udiv(zz, (uint32_t)p.sz, p.msz), ee, vv[u]);
-                    }
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t ee = e + (uint32_t)u * kTileThreads;
+                if (ee < e1) {
+                    const uint32_t rel = (uint32_t)(kk[u] - kb);
+                    const uint32_t yy = udiv(rel, Z, p.mZ), zz = rel - yy * Z;
+                    f((int)udiv(yy, (uint32_t)p.sy, p.msy) * p.PZ + (int)udiv(zz, (uint32_t)p.sz, p.msz), ee, vv[u]);
                 }
             }
         }
-    };
-    // pass 1: max per cluster on an order-preserving u32 (occupancy only when counting)
-    for_members([&](int cell, uint32_t, float v) {
-        if (WRITE) atomicMax(&best[cell], orderable(v));
-        else best[cell] = 1u;
+    }
+}
+
+struct PoolTileId {
+    int64_t seg;
+    int px, py0, npy, ya, yb;
+};
+__device__ __forceinline__ PoolTileId pool_tile_id(const Geo& g, const PoolPlan& p, int64_t tile) {
+    PoolTileId t;
+    const int yt = (int)(tile % p.nyt);
+    const int64_t r = tile / p.nyt;
+    t.px = (int)(r % p.PX);
+    t.seg = r / p.PX;
+    t.py0 = yt * p.nyb;
+    t.npy = min(p.nyb, p.PY - t.py0);
+    t.ya = t.py0 * p.sy;
+    t.yb = min((t.py0 + t.npy) * p.sy, g.Y);
+    return t;
+}
+
+// count pass: occupied clusters of the tile (a 4096-bit occupancy mask)
+__global__ void __launch_bounds__(kTileThreads)
+pool_tile_count_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, const uint32_t* __restrict__ row_ptr,
+                       uint32_t* __restrict__ item_cnt) {
+    __shared__ uint32_t occ[kTileCells / 32];
+    __shared__ uint32_t sm[33];
+    const PoolTileId t = pool_tile_id(g, p, blockIdx.x);
+    if (threadIdx.x < kTileCells / 32) occ[threadIdx.x] = 0u;
+    __syncthreads();
+    pool_tile_members<false>(g, p, keys, nullptr, row_ptr, t.seg, t.px, t.ya, t.yb, [&](int cell, uint32_t, float) {
+        atomicOr(&occ[cell >> 5], 1u << (cell & 31));
     });
     __syncthreads();
-    if (!WRITE) {
-        uint32_t c = 0;
+    const uint32_t c = threadIdx.x < kTileCells / 32 ? (uint32_t)__popc(occ[threadIdx.x]) : 0u;
+    const uint32_t tot = block_sum(c, sm);
+    if (threadIdx.x == 0) item_cnt[blockIdx.x] = tot;
+}
+
+// write pass: per cluster the max of (orderable(value) << 32 | ~entry) -- the maximum, ties to
+// the smaller key (reading R8) -- in one 64-bit shared atomic (0 = empty: orderable() is never
+// 0); the occupied clusters are listed in cell order from the occupancy mask (one scan over its
+// 128 words) and written with coalesced stores.
+__global__ void __launch_bounds__(kTileThreads)
+pool_tile_write_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, const float* __restrict__ vals,
+                       const uint32_t* __restrict__ row_ptr, const uint64_t* __restrict__ item_off,
+                       uint64_t* __restrict__ ok, float* __restrict__ ov, int64_t* __restrict__ oarg) {
+    __shared__ __align__(16) unsigned long long best[kTileCells];
+    __shared__ uint32_t occ[kTileCells / 32];
+    __shared__ uint16_t cells[kTileCells];
+    __shared__ uint32_t wsum[4];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const PoolTileId t = pool_tile_id(g, p, blockIdx.x);
+    uint4* b4 = reinterpret_cast<uint4*>(best);
 #pragma unroll
-        for (int j = 0; j < kTileJ; ++j) c += best[tid + kTileThreads * j] != 0u;
-        __shared__ uint32_t sm[33];
-        c = block_sum(c, sm);
-        if (tid == 0) item_cnt[tile] = c;
-        return;
-    }
-    // pass 2 (the runs are L1/L2-resident now): smallest entry index among the maxima
-    for_members([&](int cell, uint32_t e, float v) {
-        if (orderable(v) == best[cell]) atomicMin(&arg[cell], e);
+    for (int j = 0; j < kTileCells / 2 / kTileThreads; ++j) b4[tid + kTileThreads * j] = make_uint4(0u, 0u, 0u, 0u);
+    if (tid < kTileCells / 32) occ[tid] = 0u;
+    __syncthreads();
+    pool_tile_members<true>(g, p, keys, vals, row_ptr, t.seg, t.px, t.ya, t.yb, [&](int cell, uint32_t e, float v) {
+        atomicMax(&best[cell], ((unsigned long long)orderable(v) << 32) | (unsigned long long)(~e));
+        atomicOr(&occ[cell >> 5], 1u << (cell & 31));
     });
     __syncthreads();
-    // ordered compaction of the occupied clusters (cell order = (j, warp, lane)): one ballot per
-    // j, a scan of the 16 x 8 (j, warp) counts, then the (cell, arg) pairs are staged in place
-    // and written with coalesced stores
-    unsigned m[kTileJ];
-    uint32_t av[kTileJ];
-#pragma unroll
-    for (int j = 0; j < kTileJ; ++j) {
-        const int cell = tid + kTileThreads * j;
-        const bool occ = cell < ncell && best[cell] != 0u;
-        m[j] = __ballot_sync(kFull, occ);
-        av[j] = arg[cell];
-        if (lane == 0) wcnt[j * 8 + warp] = (uint32_t)__popc(m[j]);
+    // threads 0..127 own one mask word each: exclusive scan of the popcounts, then the word's
+    // clusters are listed in order
+    uint32_t w = 0, c = 0, pre = 0;
+    if (warp < 4) {
+        w = occ[tid];
+        c = (uint32_t)__popc(w);
+        pre = warp_incl_scan(c) - c;
+        if (lane == 31) wsum[warp] = pre + c;
     }
     __syncthreads();
-    if (warp == 0) {   // exclusive scan of the 128 counts, 4 per lane
-        uint32_t c[4], t = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) { c[q] = wcnt[4 * lane + q]; t += c[q]; }
-        const uint32_t inc = warp_incl_scan(t);
-        uint32_t run = inc - t;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) { wcnt[4 * lane + q] = run; run += c[q]; }
-        if (lane == 31) wcnt[kTileJ * 8] = inc;
-    }
-    __syncthreads();
-    const uint32_t lt = (1u << lane) - 1u;
-#pragma unroll
-    for (int j = 0; j < kTileJ; ++j) {
-        if ((m[j] >> lane) & 1u) {
-            const uint32_t q = wcnt[j * 8 + warp] + (uint32_t)__popc(m[j] & lt);
-            best[q] = (uint32_t)(tid + kTileThreads * j);
-            arg[q] = av[j];
+    const uint32_t tot = wsum[0] + wsum[1] + wsum[2] + wsum[3];
+    if (warp < 4) {
+        for (int q = 0; q < warp; ++q) pre += wsum[q];
+        while (w) {
+            const int bit = __ffs(w) - 1;
+            w &= w - 1;
+            cells[pre++] = (uint16_t)(tid * 32 + bit);
         }
     }
-    const uint32_t tot = wcnt[kTileJ * 8];
     __syncthreads();
-    const uint64_t o0 = item_off[tile];
-    const uint64_t pbase = ((uint64_t)(seg * p.PX + px) * p.PY + py0) * (uint64_t)p.PZ;
+    const uint64_t o0 = item_off[blockIdx.x];
+    const uint64_t pbase = ((uint64_t)(t.seg * p.PX + t.px) * p.PY + t.py0) * (uint64_t)p.PZ;
     for (uint32_t q = tid; q < tot; q += kTileThreads) {
-        const uint32_t a = arg[q];
-        ok[o0 + q] = pbase + best[q];
+        const uint32_t cell = cells[q];
+        const uint32_t a = ~(uint32_t)best[cell];
+        ok[o0 + q] = pbase + cell;
         ov[o0 + q] = vals[a];
         if (oarg) oarg[o0 + q] = a;
     }
@@ -348,10 +354,10 @@ cudaError_t launch_maxpool(const Geo& g, const PoolPlan& p, const uint64_t* keys
     if (p.items == 0) return cudaMemsetAsync(out_nnz, 0, sizeof(int64_t), s);
     if (p.tiled) {
         const unsigned tg = (unsigned)p.items;
-        { SPC_PHASE("pool_count", s, 1); pool_tile_kernel<false><<<tg, kTileThreads, 0, s>>>(g, p, keys, vals, row_ptr, item_cnt, nullptr, nullptr, nullptr, nullptr); }
+        { SPC_PHASE("pool_count", s, 1); pool_tile_count_kernel<<<tg, kTileThreads, 0, s>>>(g, p, keys, row_ptr, item_cnt); }
         cudaError_t e = launch_scan_u32(item_cnt, item_off, p.items, out_nnz, scan_tmp, s);
         if (e != cudaSuccess) return e;
-        { SPC_PHASE("pool_write", s, 1); pool_tile_kernel<true><<<tg, kTileThreads, 0, s>>>(g, p, keys, vals, row_ptr, item_cnt, item_off, out_keys, out_vals, out_arg); }
+        { SPC_PHASE("pool_write", s, 1); pool_tile_write_kernel<<<tg, kTileThreads, 0, s>>>(g, p, keys, vals, row_ptr, item_off, out_keys, out_vals, out_arg); }
         return cudaGetLastError();
     }
     const unsigned grid = (unsigned)((p.items + kPoolWarps - 1) / kPoolWarps);
