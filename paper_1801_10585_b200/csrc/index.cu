@@ -8,9 +8,10 @@
 namespace spc {
 
 // ---------------------------------------------------------------------------- row index
-// row_ptr[r] = first entry whose key >= r*Z, for r in [0, total_rows]. Each thread takes 8
-// consecutive entries and fills, for each, the gap of rows between its predecessor's row and its
-// own; long empty stretches are filled by the whole warp so they do not serialise on one thread.
+// row_ptr[r] = first entry whose key >= r*Z, for r in [0, total_rows]. A block computes the rows
+// of its 2048 entries from coalesced key loads into shared memory; then each entry fills the gap
+// of rows between its predecessor's row and its own (consecutive entries on consecutive lanes);
+// long empty stretches are filled by the whole warp so they do not serialise on one thread.
 // key / Z by a multiply-high with a host-computed reciprocal and one exact correction; 32-bit
 // arithmetic throughout when the key space fits (batch*channels*V <= 2^32, the "Sparse 32"
 // condition of Table 1), 64-bit otherwise.
@@ -31,22 +32,31 @@ template <typename K, typename I>   // key word, row / entry index type
 __global__ void __launch_bounds__(256) row_index_kernel(K Z, K magic, const uint64_t* __restrict__ keys,
                                                         const int64_t* nnz_dev, int64_t nbound,
                                                         uint32_t* __restrict__ row_ptr, I total_rows) {
+    constexpr int kB = 256 * kRiItems;   // entries per block
+    __shared__ I srow[kB + 1];           // srow[1 + t] = row of entry b0 + t; srow[0] = row of b0 - 1
     const I n = (I)load_n(nnz_dev, nbound);
-    const I i0 = ((I)blockIdx.x * (I)blockDim.x + (I)threadIdx.x) * kRiItems;
+    const I b0 = (I)blockIdx.x * kB;
+    if (b0 > n) return;
     const int lane = threadIdx.x & 31;
-    I prev = (i0 == 0 || i0 > n) ? (I)-1 : (I)row_of((K)keys[i0 - 1], Z, magic);
+    // rows of the block's entries, computed from coalesced key loads
 #pragma unroll
-    for (int u = 0; u < kRiItems; ++u) {
-        const I i = i0 + u;
+    for (int q = 0; q < kRiItems; ++q) {
+        const int t = q * 256 + threadIdx.x;
+        const I i = b0 + t;
+        srow[1 + t] = i < n ? (I)row_of((K)keys[i], Z, magic) : total_rows;
+    }
+    if (threadIdx.x == 0) srow[0] = b0 == 0 ? (I)-1 : (I)row_of((K)keys[b0 - 1], Z, magic);
+    __syncthreads();
+    // entry i (and the sentinel i = n) fills the rows between its predecessor's row and its own
+#pragma unroll
+    for (int q = 0; q < kRiItems; ++q) {
+        const int t = q * 256 + threadIdx.x;
+        const I i = b0 + t;
         I lo = 0, hi = -1;
-        if (i < n) {
-            const I r = (I)row_of((K)keys[i], Z, magic);
-            lo = prev + 1;
-            hi = r < total_rows ? r : total_rows;
-            prev = r;
-        } else if (i == n) {
-            lo = prev + 1;
-            hi = total_rows;
+        if (i <= n) {
+            lo = srow[t] + 1;
+            const I r = srow[t + 1];
+            hi = (i < n && r < total_rows) ? r : total_rows;
         }
         const bool longgap = hi - lo >= 16;
         if (!longgap)
@@ -66,9 +76,8 @@ __global__ void __launch_bounds__(256) row_index_kernel(K Z, K magic, const uint
 cudaError_t launch_row_index(const Geo& g, const uint64_t* keys, const int64_t* nnz_dev, int64_t nbound,
                              uint32_t* row_ptr, cudaStream_t s) {
     const int64_t total_rows = g.B * g.C * g.R;
-    const int64_t threads = (nbound + 1 + kRiItems - 1) / kRiItems;
     const int bs = 256;
-    const int64_t grid = (threads + bs - 1) / bs;
+    const int64_t grid = (nbound + 1 + (int64_t)bs * kRiItems - 1) / ((int64_t)bs * kRiItems);
     const double space = (double)g.B * (double)g.C * (double)g.V;
     SPC_PHASE("row_index", s, 1);
     if (space <= 4294967296.0 && nbound < (1ll << 30) && total_rows < (1ll << 30)) {
