@@ -438,8 +438,8 @@ spc_status_t sparse_conv_fwd_ex(const spc_map_t* x, const spc_filter_t* w, const
     Carver c(workspace);
     FwdWs ws = carve_fwd(c, gx, gy, kg, t, w, attn, gpp);
     if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
+    SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));   // both variants
     if (!use_gemm) {
-        SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
         SPC_TRY(cu(launch_filter_table_fwd(kg, (int)w->c_in, (int)w->c_out, w->keys, w->values, w->nnz, ws.meta2,
                                            ws.val2, ws.off2, ws.scratch2, s)));
     }
@@ -467,6 +467,7 @@ spc_status_t sparse_conv_fwd_ex(const spc_map_t* x, const spc_filter_t* w, const
         g.wkeys = w->keys;
         g.wvals = w->values;
         g.nw = w->nnz;
+        g.xrow = ws.xrow;
         return cu(launch_conv_fwd_pipeline(gx, gy, kg, t, a, s, &gp, &g));
     }
     return cu(launch_conv_fwd_pipeline(gx, gy, kg, t, a, s));

@@ -60,18 +60,26 @@ GemmPlan plan_gemm(const Geo& gx, const Geo& gy, const KGeo& kg) {
     g.NV = g.SX * g.SY * g.SZ;
     g.nty = (gy.Y + kSlabTY - 1) / kSlabTY;
     g.ntz = (gy.Z + kSlabTZ - 1) / kSlabTZ;
-    g.slab_bytes = (size_t)2 * g.NV * g.Kp * 4 + (size_t)g.NV * 4;
-    g.bstage_bytes = (size_t)2 * g.Np * g.Kp * 4;
-    // as many B stages as fit next to the slab (they hide the L2 latency of B_delta, 2..8)
-    {
-        const size_t room = 200 * 1024 > g.slab_bytes + extra ? 200 * 1024 - g.slab_bytes - extra : 0;
-        // every B_delta resident (small filter banks): one load, then all MMAs back to back;
-        // otherwise two stages of `bgroup` offsets each (one handshake per group, not per offset)
-        g.ball = (size_t)g.KV * g.bstage_bytes <= std::min<size_t>(room, 96 * 1024) ? 1 : 0;
+    // K split: the slab holds Kp/2 channels at a time when that lets two CTAs share an SM (the
+    // fill of one tile then overlaps the MMAs of the other); else the whole K in one part
+    auto slab_plan = [&](int parts, size_t budget) {
+        g.kparts = parts;
+        g.Kh = g.Kp / parts;
+        g.slab_bytes = (size_t)2 * g.NV * g.Kh * 4 + (size_t)g.NV * 4;
+        g.bstage_bytes = (size_t)2 * g.Np * g.Kh * 4;
+        const size_t room = budget > g.slab_bytes + extra ? budget - g.slab_bytes - extra : 0;
+        // every B_delta resident (small filter banks, one part): one load, then all MMAs back to
+        // back; otherwise two stages of `bgroup` offsets each (one handshake per group)
+        g.ball = parts == 1 && (size_t)g.KV * g.bstage_bytes <= std::min<size_t>(room, 96 * 1024) ? 1 : 0;
         g.bgroup = (int)std::max<size_t>(1, std::min<size_t>(8, room / (2 * g.bstage_bytes)));
         g.bstages = g.ball ? g.KV : 2;
-    }
-    g.slab_smem = g.slab_bytes + (g.ball ? (size_t)g.KV : (size_t)2 * g.bgroup) * g.bstage_bytes + extra;
+        g.slab_smem = g.slab_bytes + (g.ball ? (size_t)g.KV : (size_t)2 * g.bgroup) * g.bstage_bytes + extra;
+        return g.slab_smem <= budget && room >= 2 * g.bstage_bytes;
+    };
+    const bool split_ok = g.Kp % 16 == 0 && !(getenv("SPC_GEMM_KSPLIT") && getenv("SPC_GEMM_KSPLIT")[0] == '0');
+    if (!(split_ok && slab_plan(2, 112 * 1024) && slab_plan(1, 200 * 1024) && g.slab_smem > 112 * 1024 &&
+          slab_plan(2, 112 * 1024)))
+        slab_plan(1, 200 * 1024);
     // several TMEM accumulators, offsets dealt round-robin: consecutive MMAs do not depend on
     // each other's result (summed in the epilogue)
     g.nacc = std::max(1, std::min(4, 256 / (2 * g.Np)));
@@ -105,6 +113,63 @@ __global__ void gemm_densify_kernel(Geo gx, int Kp, const uint64_t* __restrict__
         xlo[o] = v - hi;
         atomicOr(&occ[b * (uint64_t)gx.V + p], 1u << ic);
     }
+}
+
+// Tiled form: one CTA per (b, x, band of ny rows) builds the band's dense [voxel][Kp] block in
+// shared memory -- channel c's entries of the band are one contiguous run of the row index -- and
+// writes it (and the occupancy masks) with coalesced stores, zeros included (no memset, no
+// scattered 4-byte stores). Channel slots are XOR-swizzled by voxel (Kp a power of two) so the
+// scatter of one channel's entries hits distinct banks.
+__device__ __forceinline__ int dz_slot(int v, int c, int Kp) {
+    return (Kp & (Kp - 1)) == 0 ? v * Kp + (c ^ (v & (Kp - 1))) : v * Kp + c;
+}
+
+__global__ void __launch_bounds__(256) gemm_densify_tile_kernel(Geo gx, int Kp, int ny, const uint64_t* __restrict__ keys,
+                                                                 const float* __restrict__ vals,
+                                                                 const uint32_t* __restrict__ xrow,
+                                                                 float* __restrict__ xhi, float* __restrict__ xlo,
+                                                                 uint32_t* __restrict__ occ) {
+    extern __shared__ __align__(16) float dsm[];
+    const int nyt = (gx.Y + ny - 1) / ny;
+    int64_t t = blockIdx.x;
+    const int yt = (int)(t % nyt); t /= nyt;
+    const int x = (int)(t % gx.X);
+    const int64_t b = t / gx.X;
+    const int y0 = yt * ny, nyr = min(ny, gx.Y - y0);
+    const int Z = gx.Z, TV = nyr * Z, TE = TV * Kp;
+    float* shi = dsm;
+    float* slo = dsm + (size_t)ny * Z * Kp;
+    uint32_t* socc = reinterpret_cast<uint32_t*>(slo + (size_t)ny * Z * Kp);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < TE; i += 256) {
+        shi[i] = 0.0f;
+        slo[i] = 0.0f;
+    }
+    for (int v = tid; v < TV; v += 256) socc[v] = 0u;
+    __syncthreads();
+    for (int c = warp; c < (int)gx.C; c += 8) {
+        const int64_t r0 = ((b * gx.C + c) * gx.X + x) * (int64_t)gx.Y + y0;
+        const uint32_t e0 = xrow[r0], e1 = xrow[r0 + nyr];
+        const uint64_t kb = (uint64_t)r0 * (uint64_t)Z;
+        for (uint32_t e = e0 + lane; e < e1; e += 32) {
+            const int v = (int)(keys[e] - kb);
+            const float val = vals[e];
+            const float hi = __uint_as_float(__float_as_uint(val) & 0xffffe000u);
+            const int o = dz_slot(v, c, Kp);
+            shi[o] = hi;
+            slo[o] = val - hi;
+            atomicOr(&socc[v], 1u << c);
+        }
+    }
+    __syncthreads();
+    const size_t vb = (size_t)b * gx.V + ((size_t)x * gx.Y + y0) * Z;
+    for (int i = tid; i < TE; i += 256) {
+        const int v = i / Kp, c = i - v * Kp;
+        const int o = dz_slot(v, c, Kp);
+        xhi[vb * Kp + i] = shi[o];
+        xlo[vb * Kp + i] = slo[o];
+    }
+    for (int v = tid; v < TV; v += 256) occ[vb + v] = socc[v];
 }
 
 // element offset of (row, k) in the canonical K-major, no-swizzle UMMA layout of an R-row operand:
@@ -401,7 +466,7 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_kernel(Geo gx, Geo gy, KG
 __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo gy, KGeo kg, GemmPlan g, GemmArgs a) {
     extern __shared__ __align__(1024) unsigned char gsm[];
     const int tid = threadIdx.x, warp = tid >> 5;
-    const int Kp = g.Kp, Np = g.Np, KV = g.KV, NV = g.NV, SY = g.SY, SZ = g.SZ;
+    const int Kp = g.Kp, Kh = g.Kh, Np = g.Np, KV = g.KV, NV = g.NV, SY = g.SY, SZ = g.SZ;
     const int c_out = (int)gy.C;
     int64_t t = blockIdx.x;
     const int tz = (int)(t % g.ntz); t /= g.ntz;
@@ -411,8 +476,9 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
     const int y0 = ty * kSlabTY, z0 = tz * kSlabTZ;
     const int S = g.bstages;
     // shared layout: slab hi | slab lo | occ | B stages | wmask | dlist | mbarriers | tmem slot
+    // (the slab holds the Kh channels of one K part)
     const size_t half_plane = (size_t)NV * 16;             // one K half of one K step, all voxels
-    const size_t slab_one = (size_t)NV * Kp * 4;           // hi or lo
+    const size_t slab_one = (size_t)NV * Kh * 4;           // hi or lo
     uint32_t* occs = reinterpret_cast<uint32_t*>(gsm + 2 * slab_one);
     unsigned char* bst = gsm + g.slab_bytes;
     uint32_t* wmask = reinterpret_cast<uint32_t*>(
@@ -424,7 +490,6 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(gsm);
     const uint32_t bbase = sbase + (uint32_t)g.slab_bytes;
     const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(mbar);
-    const size_t B_B = (size_t)Np * Kp * 4;
 
     for (int i = tid; i < KV * Np; i += kGThreads) wmask[i] = a.wmask[i];
     if (warp == 0) {
@@ -449,10 +514,11 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
     const int* duni = dlist + 1 + KV;
     const int* dsoff = dlist + 1 + 2 * KV;
 
-    // ---- stage the neighbourhood (joins cp.async group 0 together with B of the first offset):
-    // one slab row (sx, sy) per warp iteration, lanes over its SZ voxels x 16-byte chunks
-    {
-        const int cpv = Kp / 4, lg = __ffs(cpv) - 1;        // chunks per voxel (power of 2)
+    // ---- stage the neighbourhood's channels of K part `part` (joins the cp.async group of the
+    // first B load): one slab row (sx, sy) per warp iteration, lanes over its SZ voxels x 16-byte
+    // chunks; the occupancy masks with the first part
+    auto fill_slab = [&](int part) {
+        const int cpv = Kh / 4, lg = __ffs(cpv) - 1;        // chunks per voxel (power of 2)
         const int xs0 = x - kg.hx, ys0 = y0 - kg.hy, zs0 = z0 - kg.hz;
         const int lane = tid & 31;
         for (int r = warp; r < g.SX * SY; r += kGThreads / 32) {
@@ -460,7 +526,7 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
             const int qx = xs0 + sx, qy = ys0 + sy;
             const bool rok = qx >= 0 && qx < gx.X && qy >= 0 && qy < gx.Y;
             const size_t rowv = (size_t)b * gx.V + ((size_t)(rok ? qx : 0) * gx.Y + (rok ? qy : 0)) * gx.Z;
-            const size_t rowq = rowv * Kp;
+            const size_t rowq = rowv * Kp + (size_t)part * Kh;
             for (int j = lane; j < SZ * cpv; j += 32) {
                 const int sz = j >> lg, c = j & (cpv - 1);
                 const int qz = zs0 + sz;
@@ -471,21 +537,25 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
                 cp16(sbase + off, a.xhi + q, ok);
                 cp16(sbase + (uint32_t)slab_one + off, a.xlo + q, ok);
             }
-            for (int sz = lane; sz < SZ; sz += 32) {   // occupancy masks, same async group
-                const int qz = zs0 + sz;
-                const bool ok = rok && qz >= 0 && qz < gx.Z;
-                cp4(sbase + (uint32_t)(2 * slab_one) + 4u * (uint32_t)(r * SZ + sz), a.occ + (ok ? rowv + qz : 0), ok);
-            }
+            if (part == 0)
+                for (int sz = lane; sz < SZ; sz += 32) {
+                    const int qz = zs0 + sz;
+                    const bool ok = rok && qz >= 0 && qz < gx.Z;
+                    cp4(sbase + (uint32_t)(2 * slab_one) + 4u * (uint32_t)(r * SZ + sz), a.occ + (ok ? rowv + qz : 0), ok);
+                }
         }
-    }
+    };
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(Np >> 3) << 17) | ((uint32_t)(kGM >> 4) << 24);
     const uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)((2 * Np) >> 3) << 17) | ((uint32_t)(kGM >> 4) << 24);
     const uint32_t lbo_a = (uint32_t)half_plane, sbo_a = (uint32_t)(SZ * 16);
     const uint64_t dA0 = umma_sdesc(sbase, lbo_a, sbo_a), dB0 = umma_sdesc(bbase);
+    const uint64_t kA = (uint64_t)(2 * half_plane >> 4), kB = (uint64_t)(2 * Np * 32 >> 4);
+    const size_t B_part = (size_t)2 * Np * Kh;              // floats of one offset's B for one part
 
     if (nd > 0 && g.ball) {
         // all B_delta resident: one async group (slab + every B), then every MMA back to back and
         // a single commit -- no per-offset synchronisation
+        fill_slab(0);
         for (int j = 0; j < nd; ++j) {
             const uint32_t base = bbase + (uint32_t)(j * g.bstage_bytes);
             const float* bh = a.bhi + (size_t)dl[j] * 2 * Np * Kp;
@@ -498,7 +568,6 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
         __syncthreads();
         if (warp == 0) {   // converged warp: MMAs issued through elect.sync
             tc_fence_after();
-            const uint64_t kA = (uint64_t)(2 * half_plane >> 4), kB = (uint64_t)(2 * Np * 32 >> 4);
             for (int it = 0; it < nd; ++it) {
                 const uint64_t dAh = dA0 + (uint64_t)((uint32_t)(dsoff[dl[it]] * 16) >> 4);
                 const uint64_t dBc = dB0 + (uint64_t)((uint32_t)(it * g.bstage_bytes) >> 4);
@@ -514,55 +583,63 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
         mbar_wait(mb0 + 8u * S, 0u);
         tc_fence_after();
     } else if (nd > 0) {
-        // two stages, each holding the B of GD consecutive offsets: group j+1 streams in while the
-        // MMAs of group j run; group 0 also carries the slab
+        // per K part: two stages, each holding the B of GD consecutive offsets (this part's K
+        // steps of each): group j+1 streams in while the MMAs of group j run; the first group of
+        // a part also carries the part's slab. `gi` counts groups over both parts (stage and
+        // barrier phase).
         const int GD = g.bgroup;
         const int ngrp = (nd + GD - 1) / GD;
         const size_t gstage = (size_t)GD * g.bstage_bytes;
-        auto load_grp = [&](int st, int grp) {
+        auto load_grp = [&](int st, int grp, int part) {
             const uint32_t base = bbase + (uint32_t)(st * gstage);
             for (int j = 0; j < GD && grp * GD + j < nd; ++j) {
                 const int d = dl[grp * GD + j];
-                const float* bh = a.bhi + (size_t)d * 2 * Np * Kp;
+                const float* bh = a.bhi + (size_t)d * 2 * Np * Kp + (size_t)part * B_part;
                 const uint32_t sb = base + (uint32_t)(j * g.bstage_bytes);
-                for (int c = tid; c < 2 * Np * Kp / 4; c += kGThreads) cp16(sb + 16u * c, bh + 4 * c, true);
+                for (int c = tid; c < (int)(B_part / 4); c += kGThreads) cp16(sb + 16u * c, bh + 4 * c, true);
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
-        load_grp(0, 0);
-        const uint64_t kA = (uint64_t)(2 * half_plane >> 4), kB = (uint64_t)(2 * Np * 32 >> 4);
-        for (int it = 0; it < ngrp; ++it) {
-            const int st = it & 1;
-            asm volatile("cp.async.wait_group 0;" ::: "memory");   // this thread's share of group it
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive(mb0 + 8u * st);
-            if (warp == 0) {   // converged warp: MMAs issued through elect.sync
-                mbar_wait(mb0 + 8u * st, (uint32_t)((it >> 1) & 1));
-                tc_fence_after();
-                for (int j = 0; j < GD && it * GD + j < nd; ++j) {
-                    const int di = it * GD + j;
-                    // descriptors differ only in the start-address field (16-byte units)
-                    const uint64_t dAh = dA0 + (uint64_t)((uint32_t)(dsoff[dl[di]] * 16) >> 4);
-                    const uint64_t dBc = dB0 + (uint64_t)((uint32_t)(st * gstage + (size_t)j * g.bstage_bytes) >> 4);
-                    const uint64_t dAl = dAh + (uint64_t)(slab_one >> 4);
-                    const uint32_t td = tmem + (uint32_t)((di % g.nacc) * 2 * Np);
-                    for (int ks = 0; ks < Kp / 8; ++ks) {   // A_hi.[W_hi|W_lo], then A_lo.W_hi
-                        const uint32_t acc = (di >= g.nacc || ks != 0) ? 1u : 0u;
-                        umma_tf32(td, dAh + ks * kA, dBc + ks * kB, idesc2, acc);
-                        umma_tf32(td, dAl + ks * kA, dBc + ks * kB, idesc, 1u);
+        int gi = 0;
+        for (int part = 0; part < g.kparts; ++part) {
+            fill_slab(part);
+            load_grp(gi & 1, 0, part);
+            for (int it = 0; it < ngrp; ++it, ++gi) {
+                const int st = gi & 1;
+                asm volatile("cp.async.wait_group 0;" ::: "memory");   // this thread's share of group gi
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(mb0 + 8u * st);
+                if (warp == 0) {   // converged warp: MMAs issued through elect.sync
+                    mbar_wait(mb0 + 8u * st, (uint32_t)((gi >> 1) & 1));
+                    tc_fence_after();
+                    for (int j = 0; j < GD && it * GD + j < nd; ++j) {
+                        const int di = it * GD + j;
+                        // descriptors differ only in the start-address field (16-byte units)
+                        const uint64_t dAh = dA0 + (uint64_t)((uint32_t)(dsoff[dl[di]] * 16) >> 4);
+                        const uint64_t dBc = dB0 + (uint64_t)((uint32_t)(st * gstage + (size_t)j * g.bstage_bytes) >> 4);
+                        const uint64_t dAl = dAh + (uint64_t)(slab_one >> 4);
+                        const uint32_t td = tmem + (uint32_t)((di % g.nacc) * 2 * Np);
+                        for (int ks = 0; ks < Kh / 8; ++ks) {   // A_hi.[W_hi|W_lo], then A_lo.W_hi
+                            const uint32_t acc = (part > 0 || di >= g.nacc || ks != 0) ? 1u : 0u;
+                            umma_tf32(td, dAh + ks * kA, dBc + ks * kB, idesc2, acc);
+                            umma_tf32(td, dAl + ks * kA, dBc + ks * kB, idesc, 1u);
+                        }
                     }
+                    umma_commit(mb0 + 8u * (S + st));
                 }
-                umma_commit(mb0 + 8u * (S + st));
+                // group gi + 1 into the other stage once the MMAs of group gi - 1 retired
+                if (it + 1 < ngrp) {
+                    if (gi >= 1) mbar_wait(mb0 + 8u * (S + (st ^ 1)), (uint32_t)(((gi - 1) >> 1) & 1));
+                    load_grp(st ^ 1, it + 1, part);
+                }
             }
-            // group it + 1 into the other stage once the MMAs of group it - 1 retired
-            if (it + 1 < ngrp) {
-                if (it >= 1) mbar_wait(mb0 + 8u * (S + (st ^ 1)), (uint32_t)(((it - 1) >> 1) & 1));
-                load_grp(st ^ 1, it + 1);
-            }
+            // every MMA of this part retired: the slab and both stages are free again
+            mbar_wait(mb0 + 8u * (S + ((gi - 1) & 1)), (uint32_t)(((gi - 1) >> 1) & 1));
+            if (gi >= 2) mbar_wait(mb0 + 8u * (S + (gi & 1)), (uint32_t)(((gi - 2) >> 1) & 1));
+            tc_fence_after();
         }
-        mbar_wait(mb0 + 8u * (S + ((ngrp - 1) & 1)), (uint32_t)(((ngrp - 1) >> 1) & 1));
-        tc_fence_after();
     } else {
+        fill_slab(0);
         asm volatile("cp.async.commit_group;" ::: "memory");
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();   // occupancy slab visible
@@ -645,12 +722,23 @@ __global__ void __launch_bounds__(256) pre_hist_kernel(FwdArgs a, int64_t V, int
 cudaError_t launch_conv_gemm(const Geo& gx, const Geo& gy, const KGeo& kg, const GemmPlan& g, const GemmArgs& ga,
                              const FwdArgs& a, cudaStream_t s) {
     const size_t nvox = (size_t)gx.B * gx.V;
-    cudaMemsetAsync(ga.xhi, 0, nvox * g.Kp * sizeof(float), s);
-    cudaMemsetAsync(ga.xlo, 0, nvox * g.Kp * sizeof(float), s);
-    cudaMemsetAsync(ga.occ, 0, nvox * sizeof(uint32_t), s);
     cudaMemsetAsync(ga.bhi, 0, (size_t)2 * g.KV * g.Np * g.Kp * sizeof(float), s);
     cudaMemsetAsync(ga.wmask, 0, (size_t)g.KV * g.Np * sizeof(uint32_t), s);
-    {
+    // tiled densify when a band of rows fits shared memory (bands of up to 256 voxels)
+    const int ny = std::max(1, std::min(gx.Y, 256 / std::max(gx.Z, 1)));
+    const size_t dz_smem = (size_t)ny * gx.Z * g.Kp * 8 + (size_t)ny * gx.Z * 4;
+    if (ga.xrow && dz_smem <= 100 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_densify_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)dz_smem);
+        if (e != cudaSuccess) return e;
+        SPC_PHASE("gemm_densify", s, 1);
+        const int64_t tiles = gx.B * gx.X * (int64_t)((gx.Y + ny - 1) / ny);
+        gemm_densify_tile_kernel<<<(unsigned)tiles, 256, dz_smem, s>>>(gx, g.Kp, ny, ga.xkeys, ga.xvals, ga.xrow, ga.xhi,
+                                                                      ga.xlo, ga.occ);
+    } else {
+        cudaMemsetAsync(ga.xhi, 0, nvox * g.Kp * sizeof(float), s);
+        cudaMemsetAsync(ga.xlo, 0, nvox * g.Kp * sizeof(float), s);
+        cudaMemsetAsync(ga.occ, 0, nvox * sizeof(uint32_t), s);
         SPC_PHASE("gemm_densify", s, 1);
         gemm_densify_kernel<<<148 * 8, 256, 0, s>>>(gx, g.Kp, ga.xkeys, ga.xvals, ga.x_nnz_dev, ga.x_nnz, ga.xhi, ga.xlo,
                                                   ga.occ);

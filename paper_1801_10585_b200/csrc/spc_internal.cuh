@@ -176,6 +176,7 @@ struct GemmPlan {
     size_t stage_bytes, smem;
     // slab form (conv_gemm_slab_kernel): tile 16 rows x 8 z, neighbourhood SX x SY x SZ voxels
     int slab, SX, SY, SZ, NV, nty, ntz, bstages, ball, bgroup, nacc, tcols_slab;
+    int kparts, Kh;    // slab K split: the channels in kparts parts of Kh (2 parts: two CTAs per SM)
     size_t slab_bytes, bstage_bytes, slab_smem;
 };
 struct GemmArgs {
@@ -186,6 +187,7 @@ struct GemmArgs {
     const uint64_t* wkeys;
     const float* wvals;
     int64_t nw;
+    const uint32_t* xrow;   // row index of the input (tiled densify)
     float* xhi;        // [B*V*Kp] dense input, TF32 high part (zero off the support)
     float* xlo;        // [B*V*Kp] low part
     uint32_t* occ;     // [B*V] occupancy mask over ic
