@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
     // first B load): one slab row (sx, sy) per warp iteration, lanes over its SZ voxels x 16-byte
     // chunks; the occupancy masks with the first part
     auto fill_slab = [&](int part) {
-        const int cpv = Kh / 4, lg = __ffs(cpv) - 1;        // chunks per voxel (power of 2)
+        const int cpv = Kh / 4;                              // 16-byte chunks per voxel (2, 4, 6 or 8)
         const int xs0 = x - kg.hx, ys0 = y0 - kg.hy, zs0 = z0 - kg.hz;
         const int lane = tid & 31;
         for (int r = warp; r < g.SX * SY; r += kGThreads / 32) {
@@ -528,7 +528,7 @@ __global__ void __launch_bounds__(kGThreads) conv_gemm_slab_kernel(Geo gx, Geo g
             const size_t rowv = (size_t)b * gx.V + ((size_t)(rok ? qx : 0) * gx.Y + (rok ? qy : 0)) * gx.Z;
             const size_t rowq = rowv * Kp + (size_t)part * Kh;
             for (int j = lane; j < SZ * cpv; j += 32) {
-                const int sz = j >> lg, c = j & (cpv - 1);
+                const int sz = j / cpv, c = j - sz * cpv;
                 const int qz = zs0 + sz;
                 const bool ok = rok && qz >= 0 && qz < gx.Z;
                 const size_t q = ok ? rowq + (size_t)qz * Kp + 4 * c : 0;

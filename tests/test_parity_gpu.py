@@ -106,6 +106,9 @@ GEMM_CASES = FWD_CASES + [
     ("c5_like_5pct", (10, 12, 32), 2, 32, 32, (3, 3, 3), 0.05, 1.0),
     ("c5_like_30pct", (6, 8, 32), 1, 32, 32, (3, 3, 3), 0.3, 1.0),
     ("c3_like_32_64", (8, 8, 24), 1, 32, 64, (3, 3, 3), 0.1, 0.6),
+    ("ksplit_16ch", (9, 37, 20), 2, 16, 24, (3, 3, 3), 0.15, 0.7),      # Kp 16: two K parts; ragged bands
+    ("kp24_noswizzle", (7, 9, 30), 1, 20, 8, (3, 3, 3), 0.2, 0.5),      # Kp 24: one part, plain slots
+    ("long_z_densify_fallback", (2, 3, 4000), 1, 3, 4, (3, 3, 3), 0.05, 0.6),   # band > smem: scatter densify
 ]
 
 
