@@ -95,13 +95,25 @@ cudaError_t launch_row_index(const Geo& g, const uint64_t* keys, const int64_t* 
 }
 
 // ------------------------------------------------------------------------- filter table
-__device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t n, uint64_t v) {
-    int64_t lo = 0, hi = n;
-    while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
-        if (a[mid] < v) lo = mid + 1; else hi = mid;
+// Runs of a grouping of the key-sorted filter entries whose groups are contiguous in key order:
+// run_start[q] / run_len[q] for q < nq (0 / 0 for empty groups). One block; entry j opens its
+// group's run when its predecessor is in another group and closes it likewise.
+template <typename G>
+__device__ __forceinline__ void filter_runs(int64_t nw, int nq, G grp, int* __restrict__ run_start,
+                                            int* __restrict__ run_len) {
+    for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+        run_start[q] = 0;
+        run_len[q] = 0;
     }
-    return lo;
+    __syncthreads();
+    for (int64_t j = threadIdx.x; j < nw; j += blockDim.x) {
+        const int q = grp(j);
+        if (j == 0 || grp(j - 1) != q) run_start[q] = (int)j;
+        if (j + 1 == nw || grp(j + 1) != q) run_len[q] = (int)j + 1;   // the run's end for now
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nq; q += blockDim.x) run_len[q] -= run_start[q];
+    __syncthreads();
 }
 
 // One block. Re-lays the (oc, ic, delta)-sorted filter into ic-major order (ic, oc, delta) so
@@ -113,13 +125,10 @@ __global__ void filter_table_kernel(KGeo kg, int c_in, int c_out, const uint64_t
                                     int* __restrict__ run_len) {
     __shared__ int sm[33];
     const int npairs = c_in * c_out;
-    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
-        const int64_t lo = lower_bound_u64(wk, nw, (uint64_t)p * (uint64_t)kg.KV);
-        const int64_t hi = lower_bound_u64(wk, nw, (uint64_t)(p + 1) * (uint64_t)kg.KV);
-        run_start[p] = (int)lo;
-        run_len[p] = (int)(hi - lo);
-    }
-    __syncthreads();
+    // runs of (oc, ic) = p in the key-sorted filter, from the boundaries between neighbours
+    // (no dependent searches: every entry is looked at once)
+    auto grp = [&](int64_t j) { return (int)(wk[j] / (uint64_t)kg.KV); };
+    filter_runs(nw, npairs, grp, run_start, run_len);
     int carry = 0;
     for (int base = 0; base < npairs; base += blockDim.x) {
         const int q = base + threadIdx.x;          // ic-major: q = ic*c_out + oc
@@ -171,16 +180,14 @@ __global__ void filter_table_fwd_kernel(KGeo kg, int c_in, int c_out, const uint
     __shared__ int sm[33];
     const int KXY = kg.kx * kg.ky;
     const int nq = c_in * KXY * c_out;   // q = (ic*KXY + dxdy)*c_out + oc
-    for (int q = threadIdx.x; q < nq; q += blockDim.x) {
-        const int oc = q % c_out, rest = q / c_out;
-        const int dxdy = rest % KXY, ic = rest / KXY;
-        const uint64_t k0 = ((uint64_t)oc * c_in + ic) * (uint64_t)kg.KV + (uint64_t)dxdy * kg.kz;
-        const int64_t lo = lower_bound_u64(wk, nw, k0);
-        const int64_t hi = lower_bound_u64(wk, nw, k0 + (uint64_t)kg.kz);
-        run_start[q] = (int)lo;
-        run_len[q] = (int)(hi - lo);
-    }
-    __syncthreads();
+    auto grp = [&](int64_t j) {   // q of entry j: key = ((oc*c_in + ic)*KV + dxdy*kz + dz)
+        const uint64_t k = wk[j];
+        const uint64_t pq = k / (uint64_t)kg.KV;
+        const int oc = (int)(pq / (uint64_t)c_in), ic = (int)(pq - (uint64_t)oc * c_in);
+        const int dxdy = (int)((k - pq * (uint64_t)kg.KV) / (uint64_t)kg.kz);
+        return (ic * KXY + dxdy) * c_out + oc;
+    };
+    filter_runs(nw, nq, grp, run_start, run_len);
     int carry = 0;
     for (int base = 0; base < nq; base += blockDim.x) {
         const int q = base + threadIdx.x;
@@ -247,7 +254,7 @@ __global__ void scan_sums_kernel(uint64_t* sums, int64_t nb, int64_t* total) {
 }
 
 __global__ void scan_down_kernel(const uint32_t* __restrict__ in, int64_t n, const uint64_t* __restrict__ sums,
-                                 uint64_t* __restrict__ out) {
+                                 uint64_t* __restrict__ out, int64_t* __restrict__ total = nullptr) {
     __shared__ uint64_t sm[33];
     const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
     uint32_t v[kScanItems];
@@ -259,7 +266,8 @@ __global__ void scan_down_kernel(const uint32_t* __restrict__ in, int64_t n, con
         acc += v[t];
     }
     uint64_t tot;
-    uint64_t ex = block_excl_scan(acc, sm, &tot) + sums[blockIdx.x];
+    uint64_t ex = block_excl_scan(acc, sm, &tot) + (sums ? sums[blockIdx.x] : 0ull);
+    if (total && threadIdx.x == 0) *total = (int64_t)tot;   // single-tile form
 #pragma unroll
     for (int t = 0; t < kScanItems; ++t) {
         const int64_t i = base + t;
@@ -271,6 +279,11 @@ __global__ void scan_down_kernel(const uint32_t* __restrict__ in, int64_t n, con
 cudaError_t launch_scan_u32(const uint32_t* in, uint64_t* out, int64_t n, int64_t* total, uint64_t* tmp,
                             cudaStream_t s) {
     const int64_t nb = (n + kScanTile - 1) / kScanTile;
+    if (nb == 1) {   // one tile: a single launch (latency-bound small layers)
+        SPC_PHASE("scan_down", s, 1);
+        scan_down_kernel<<<1, kScanBlock, 0, s>>>(in, n, nullptr, out, total);
+        return cudaGetLastError();
+    }
     if (nb > 0) { SPC_PHASE("scan_reduce", s, 1); scan_reduce_kernel<<<(unsigned)nb, kScanBlock, 0, s>>>(in, n, tmp); }
     { SPC_PHASE("scan_sums", s, 1); scan_sums_kernel<<<1, 1024, 0, s>>>(tmp, nb, total); }
     if (nb > 0) { SPC_PHASE("scan_down", s, 1); scan_down_kernel<<<(unsigned)nb, kScanBlock, 0, s>>>(in, n, tmp, out); }

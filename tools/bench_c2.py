@@ -113,10 +113,18 @@ def main():
         g.replay()
     torch.cuda.synchronize()
     graph_us = timed(g.replay, args.steps)
+    # per-phase device time of one eager step (CUDA-event brackets of the library, outside the timing)
+    spc.profile_reset()
+    spc.profile_enable(True)
+    step()
+    torch.cuda.synchronize()
+    spc.profile_enable(False)
+    phases = {k: [round(v[0] * 1e3, 1), v[1]] for k, v in sorted(spc.profile_read().items(), key=lambda kv: -kv[1][0])}
     print(json.dumps({"config": "C2: MNIST-like 28x28, batch %d, 3 x [conv3x3+attn(15%%)->ReLU->pool2], 1-8-16-32, "
                       "fwd+bwd" % args.batch, "eager_us_per_step": round(eager_us, 1),
                       "graph_us_per_step": round(graph_us, 1), "kernels_per_step": kernels,
-                      "fwd_macs_per_step": macs, "fwd_gmac_s_graph": round(macs / graph_us / 1e3, 2)}))
+                      "fwd_macs_per_step": macs, "fwd_gmac_s_graph": round(macs / graph_us / 1e3, 2),
+                      "phases_us_eager": phases}))
 
 
 if __name__ == "__main__":
