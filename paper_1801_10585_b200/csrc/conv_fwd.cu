@@ -442,17 +442,23 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     // histogram of the top score digit are accumulated for the attention threshold.
     const int nyr = ye - y0;
     const bool do_hist = a.attn != SPC_ATTN_NONE;
-    const uint32_t hist_s = (uint32_t)__cvta_generic_to_shared(hist);
-    uint4* hist4 = reinterpret_cast<uint4*>(hist);
     constexpr int kHist4 = (kSelBins + 32) / 4;      // bins + one dummy bin per lane
+    // Two histogram buffers alternate between output channels -- A in the staging area, B in the
+    // accumulator slice of the first channel once that is consumed -- so a channel's histogram is
+    // flushed while the next channel's rows are being binned: one barrier per channel.
+    const bool dbuf = do_hist && nocl > 1 && SL >= 4 * kHist4;
+    uint4* histA = reinterpret_cast<uint4*>(hist);
+    uint4* histB = reinterpret_cast<uint4*>(acc);
     if (do_hist)
-        for (int i = threadIdx.x; i < kHist4; i += blockDim.x) hist4[i] = make_uint4(0u, 0u, 0u, 0u);
+        for (int i = threadIdx.x; i < kHist4; i += blockDim.x) histA[i] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
     for (int ocl = 0; ocl < nocl; ++ocl) {
         const int oc = oc0 + ocl;
         const int64_t s = bl * c_out + oc;
         const float bv = a.bias ? __ldg(&a.bias[oc]) : 0.0f;
         const float* S = acc + ocl * SL + 2 * kg.hy * ZR + t.cz;
+        uint4* hist4 = (dbuf && (ocl & 1)) ? histB : histA;
+        const uint32_t hist_s = (uint32_t)__cvta_generic_to_shared(hist4);
         uint32_t cnt = 0;
         float* P = a.pre + s * gy.V + ((int64_t)x * gy.Y + y0) * Z;
         if (a.attn == SPC_ATTN_MAGNITUDE)
@@ -463,6 +469,10 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
             epi_rows<SPC_ATTN_NONE>(S, P, bv, nyr, Z, ZR, hist_s, cnt, marker);
         if (do_hist) {   // merge the tile histogram (support size = its total) and clear it
             __syncthreads();
+            if (dbuf && ocl == 0) {   // slice 0 is consumed: it becomes buffer B
+                for (int i = threadIdx.x; i < kHist4; i += blockDim.x) histB[i] = make_uint4(0u, 0u, 0u, 0u);
+                __syncthreads();
+            }
             uint32_t* gh = a.hist + s * kSelBins;
             for (int i = threadIdx.x; i < kHist4; i += blockDim.x) {
                 const uint4 h = hist4[i];
@@ -480,7 +490,8 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
         }
         cnt = warp_sum(cnt);
         if (lane == 0 && cnt) atomicAdd(&a.seg_count[s], (unsigned long long)cnt);
-        if (do_hist) __syncthreads();
+        // single buffer: the next channel may bin only after everyone's flush
+        if (do_hist && !dbuf) __syncthreads();
     }
 }
 
