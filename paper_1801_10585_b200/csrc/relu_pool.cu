@@ -104,13 +104,12 @@ constexpr int kPoolThreads = 256;
 constexpr int kPoolWarps = kPoolThreads / 32;
 constexpr int kPoolZChunk = 512;
 
-// Tile form (the usual case, PZ <= 4096 and a band's key span < 2^32): the inputs of the pooled
+// Tile form (the usual case, PZ <= 4096 and a band's key span < 2^31): the inputs of the pooled
 // rows py0 .. py0+nyb-1 of one pooled plane are sx contiguous key runs (one per input plane x,
 // rows py0*sy .. (py0+nyb)*sy - 1), so one CTA streams them with coalesced loads into a
 // shared-memory tile of nyb x PZ clusters and writes the occupied clusters in pooled-key order.
 constexpr int kTileThreads = 256;
 constexpr int kTileCells = 4096;
-constexpr int kTileJ = kTileCells / kTileThreads;   // 16 clusters per thread, cell = tid + 256 j
 
 PoolPlan plan_pool(const Geo& g, int sx, int sy, int sz) {
     PoolPlan p{};
