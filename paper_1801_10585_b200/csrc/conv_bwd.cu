@@ -163,8 +163,22 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
         const int x0 = (tile % t.ntx) * t.TX, y0 = (tile / t.ntx) * t.TY;
         const int xe = min(x0 + t.TX, gx.X), ye = min(y0 + t.TY, gx.Y);
         __syncthreads();
+        // entry ranges: per (ic, x) the stored entries of rows y0..ye-1 are contiguous (loaded
+        // first: their latency overlaps the gradient fill below)
+        for (int q = threadIdx.x; q < c_in * t.TX; q += blockDim.x) {
+            const int ic = q / t.TX, xi = q - (q / t.TX) * t.TX;
+            uint32_t lo = 0, hi = 0;
+            if (x0 + xi < xe) {
+                const int64_t r0 = ((b * c_in + ic) * gx.X + x0 + xi) * (int64_t)gx.Y + y0;
+                lo = xrow[r0];
+                hi = xrow[r0 + (ye - y0)];
+            }
+            rng[2 * q] = lo;
+            rng[2 * q + 1] = hi;
+        }
         // "initialize dense buffer with gradients(b, oc)", tile + halo, this oc group:
-        // per (oc, halo x-row) the kept outputs of the halo y-range are one contiguous key run
+        // per (oc, halo x-row) the kept outputs of the halo y-range are one contiguous key run;
+        // four entries per lane in flight
         const int hylo = max(0, y0 - kg.hy), hyhi = min(gy.Y, y0 + t.TY + kg.hy);
         const float invZ = 1.0f / (float)gy.Z;
         const float invHX = 1.0f / (float)HX;
@@ -177,25 +191,25 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
             const uint32_t e0 = yrow[row], e1 = yrow[row + (hyhi - hylo)];
             const uint64_t rowbase = (uint64_t)row * (uint64_t)gy.Z;
             const int gbase = (ocl * HXY + hxr * HY + (hylo - (y0 - kg.hy))) * ZR + kg.hz;
-            for (uint32_t e = e0 + lane; e < e1; e += 32) {
-                const uint32_t L = (uint32_t)(ykeys[e] - rowbase);
-                uint32_t yr = __float2uint_rz(__uint2float_rz(L) * invZ);
-                if (yr * (uint32_t)gy.Z > L) --yr;
-                if ((yr + 1) * (uint32_t)gy.Z <= L) ++yr;
-                G[gbase + (int)yr * ZR + (int)(L - yr * (uint32_t)gy.Z)] = dy[e];
+            for (uint32_t e = e0 + lane; e < e1; e += 128) {
+                uint64_t kk[4];
+                float dv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t eu = e + 32u * u;
+                    kk[u] = eu < e1 ? ykeys[eu] : rowbase;
+                    dv[u] = eu < e1 ? dy[eu] : 0.0f;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (e + 32u * u >= e1) break;
+                    const uint32_t L = (uint32_t)(kk[u] - rowbase);
+                    uint32_t yr = __float2uint_rz(__uint2float_rz(L) * invZ);
+                    if (yr * (uint32_t)gy.Z > L) --yr;
+                    if ((yr + 1) * (uint32_t)gy.Z <= L) ++yr;
+                    G[gbase + (int)yr * ZR + (int)(L - yr * (uint32_t)gy.Z)] = dv[u];
+                }
             }
-        }
-        // entry ranges: per (ic, x) the stored entries of rows y0..ye-1 are contiguous
-        for (int q = threadIdx.x; q < c_in * t.TX; q += blockDim.x) {
-            const int ic = q / t.TX, xi = q - (q / t.TX) * t.TX;
-            uint32_t lo = 0, hi = 0;
-            if (x0 + xi < xe) {
-                const int64_t r0 = ((b * c_in + ic) * gx.X + x0 + xi) * (int64_t)gx.Y + y0;
-                lo = xrow[r0];
-                hi = xrow[r0 + (ye - y0)];
-            }
-            rng[2 * q] = lo;
-            rng[2 * q + 1] = hi;
         }
         __syncthreads();
         if (warp == 0) {   // chunks per ic (32 entries each), exclusive prefix over ic
