@@ -229,30 +229,43 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
         }
         __syncthreads();
         const int nchunks = cpre[c_in];
-        for (int f = warp; f < nchunks; f += nwarps) {
+        // chunk f -> (ic, entry of this lane) from the shared ranges, and the entry's key and value
+        // loads issued; the next chunk's loads are in flight while this chunk's blocks run
+        struct Loc { int ic, xi; int64_t e; uint64_t key; float v; };
+        auto locate = [&](int f, Loc& c) {
             int ic = 0;
             while (cpre[ic + 1] <= f) ++ic;
             const int s = ((f - cpre[ic]) << 5) + lane;
-            // locate the entry: walk the TX ranges of this ic
-            int eb = eb_safe;
-            float v = 0.0f;
-            int64_t e = -1;
-            {
-                int pre = 0;
-                for (int xi = 0; xi < t.TX; ++xi) {
-                    const uint32_t lo = rng[2 * (ic * t.TX + xi)], hi = rng[2 * (ic * t.TX + xi) + 1];
-                    const int n = (int)(hi - lo);
-                    if (s >= pre && s < pre + n) {
-                        e = (int64_t)lo + (s - pre);
-                        const int64_t r0 = ((b * c_in + ic) * gx.X + x0 + xi) * (int64_t)gx.Y + y0;
-                        const uint32_t L = (uint32_t)(xkeys[e] - (uint64_t)r0 * (uint64_t)gx.Z);
-                        const uint32_t yl = L / (uint32_t)gx.Z;
-                        const int z = (int)(L - yl * (uint32_t)gx.Z);
-                        eb = ((xi + kg.hx) * HY + (int)yl + kg.hy) * ZR + z + kg.hz;
-                        v = xvals[e];
-                    }
-                    pre += n;
+            c.ic = ic;
+            c.xi = -1;
+            c.e = -1;
+            int pre = 0;
+            for (int xi = 0; xi < t.TX; ++xi) {
+                const uint32_t lo = rng[2 * (ic * t.TX + xi)], hi = rng[2 * (ic * t.TX + xi) + 1];
+                const int n = (int)(hi - lo);
+                if (s >= pre && s < pre + n) {
+                    c.e = (int64_t)lo + (s - pre);
+                    c.xi = xi;
                 }
+                pre += n;
+            }
+            c.key = c.e >= 0 ? xkeys[c.e] : 0ull;
+            c.v = c.e >= 0 ? xvals[c.e] : 0.0f;
+        };
+        Loc cur{}, nxt{};
+        if (warp < nchunks) locate(warp, cur);
+        for (int f = warp; f < nchunks; f += nwarps) {
+            if (f + nwarps < nchunks) locate(f + nwarps, nxt);
+            const int ic = cur.ic;
+            const int64_t e = cur.e;
+            int eb = eb_safe;
+            const float v = cur.v;
+            if (e >= 0) {
+                const int64_t r0 = ((b * c_in + ic) * gx.X + x0 + cur.xi) * (int64_t)gx.Y + y0;
+                const uint32_t L = (uint32_t)(cur.key - (uint64_t)r0 * (uint64_t)gx.Z);
+                const uint32_t yl = L / (uint32_t)gx.Z;
+                const int z = (int)(L - yl * (uint32_t)gx.Z);
+                eb = ((cur.xi + kg.hx) * HY + (int)yl + kg.hy) * ZR + z + kg.hz;
             }
             __syncwarp();
             st_eb[lane] = eb * (int)sizeof(float);   // byte offsets into G
@@ -285,6 +298,7 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
                 else atomicAdd(&dx[e], dxa);
             }
             __syncwarp();
+            cur = nxt;
         }
         __syncthreads();
         // zero G for the next item: one vectorized sweep of the slab (a few hundred warp
