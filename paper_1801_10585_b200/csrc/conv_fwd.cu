@@ -384,23 +384,59 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
         // ---- stage the chunk: (byte position in a channel slice, value); one warp per item,
         // coalesced reads of the item's key run; in the single-chunk case the same warp writes
         // the item's work descriptors
-        for (int pk = warp; pk < PK; pk += kFwdWarps) {
-            const int s0 = max(ioff[pk], f0), s1 = min(ioff[pk + 1], f1);
-            const uint32_t eb = iglob[pk] - (uint32_t)ioff[pk], rb = ibase[pk];
-            for (int f = s0 + lane; f < s1; f += 32) {
-                const uint32_t e = eb + (uint32_t)f;
-                const uint32_t L = xk32[2 * (size_t)e] - rb;   // < 2^32: offset within the run
-                const uint32_t yrel = div_small(L, (uint32_t)Z, invZ);
-                const uint32_t z = L - yrel * (uint32_t)Z;
-                spos[f - f0] = ((yrel + (uint32_t)arow0) * (uint32_t)ZR + z + (uint32_t)t.cz) * 4u;
-                sval[f - f0] = a.xvals[e];
+        // The warp's items (pk = warp, warp + 8, ...) are one concatenated list of entries; lane
+        // l takes positions l, l + 32, ... in batches of 8, all key / value loads of a batch in
+        // flight before any is used.
+        {
+            int wtot = 0;
+            for (int pk = warp; pk < PK; pk += kFwdWarps)
+                wtot += max(0, min(ioff[pk + 1], f1) - max(ioff[pk], f0));
+            constexpr int kJ = 8;
+            for (int base = 0; base < wtot; base += 32 * kJ) {
+                uint32_t kw[kJ], rbj[kJ];
+                float vj[kJ];
+                int dj[kJ];
+#pragma unroll
+                for (int j = 0; j < kJ; ++j) {
+                    const int pos = base + 32 * j + lane;
+                    dj[j] = -1;
+                    kw[j] = 0u;
+                    rbj[j] = 0u;
+                    vj[j] = 0.0f;
+                    if (pos < wtot) {
+                        int pk = warp, cum = 0;
+                        for (;; pk += kFwdWarps) {   // the item holding list position pos
+                            const int len = max(0, min(ioff[pk + 1], f1) - max(ioff[pk], f0));
+                            if (pos < cum + len) break;
+                            cum += len;
+                        }
+                        const int f = max(ioff[pk], f0) + (pos - cum);
+                        const uint32_t e = iglob[pk] - (uint32_t)ioff[pk] + (uint32_t)f;
+                        kw[j] = xk32[2 * (size_t)e];
+                        vj[j] = a.xvals[e];
+                        rbj[j] = ibase[pk];
+                        dj[j] = f - f0;
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < kJ; ++j) {
+                    if (dj[j] < 0) continue;
+                    const uint32_t L = kw[j] - rbj[j];   // < 2^32: offset within the run
+                    const uint32_t yrel = div_small(L, (uint32_t)Z, invZ);
+                    const uint32_t z = L - yrel * (uint32_t)Z;
+                    spos[dj[j]] = ((yrel + (uint32_t)arow0) * (uint32_t)ZR + z + (uint32_t)t.cz) * 4u;
+                    sval[dj[j]] = vj[j];
+                }
             }
-            if (single)
+        }
+        if (single)
+            for (int pk = warp; pk < PK; pk += kFwdWarps) {
+                const int s0 = max(ioff[pk], f0), s1 = min(ioff[pk + 1], f1);
                 for (int gi = lane; 64 * gi < s1 - s0; gi += 32) {
                     const int st = s0 + 64 * gi;
                     work[wpre[pk] + gi] = (uint32_t)st | ((uint32_t)min(64, s1 - st) << 12) | ((uint32_t)pk << 19);
                 }
-        }
+            }
         __syncthreads();
         if (!single) {
             if (warp == 0) {   // work list of the chunk: groups of <= 64 entries of one item
