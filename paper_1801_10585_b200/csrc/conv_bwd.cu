@@ -182,32 +182,49 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
         const int hylo = max(0, y0 - kg.hy), hyhi = min(gy.Y, y0 + t.TY + kg.hy);
         const float invZ = 1.0f / (float)gy.Z;
         const float invHX = 1.0f / (float)HX;
-        for (int r = warp; r < nocl * HX; r += nwarps) {
-            int ocl = __float2int_rz(((float)r + 0.5f) * invHX);   // r / HX (small integers)
-            const int hxr = r - ocl * HX;
-            const int xs = x0 - kg.hx + hxr;
-            if (xs < 0 || xs >= gy.X || hylo >= hyhi) continue;
-            const int64_t row = ((b * c_out + oc0 + ocl) * gy.X + xs) * (int64_t)gy.Y + hylo;
-            const uint32_t e0 = yrow[row], e1 = yrow[row + (hyhi - hylo)];
-            const uint64_t rowbase = (uint64_t)row * (uint64_t)gy.Z;
-            const int gbase = (ocl * HXY + hxr * HY + (hylo - (y0 - kg.hy))) * ZR + kg.hz;
-            for (uint32_t e = e0 + lane; e < e1; e += 128) {
-                uint64_t kk[4];
-                float dv[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const uint32_t eu = e + 32u * u;
-                    kk[u] = eu < e1 ? ykeys[eu] : rowbase;
-                    dv[u] = eu < e1 ? dy[eu] : 0.0f;
+        // the warp's rows r = warp + k * nwarps: lane k loads row k's bounds (one latency for all)
+        for (int r0 = warp; r0 < nocl * HX; r0 += 32 * nwarps) {
+            uint32_t be0 = 0, be1 = 0;
+            {
+                const int r = r0 + lane * nwarps;
+                if (r < nocl * HX) {
+                    const int ocl = __float2int_rz(((float)r + 0.5f) * invHX);   // r / HX (small integers)
+                    const int xs = x0 - kg.hx + (r - ocl * HX);
+                    if (xs >= 0 && xs < gy.X && hylo < hyhi) {
+                        const int64_t row = ((b * c_out + oc0 + ocl) * gy.X + xs) * (int64_t)gy.Y + hylo;
+                        be0 = yrow[row];
+                        be1 = yrow[row + (hyhi - hylo)];
+                    }
                 }
+            }
+            for (int k = 0; k < 32 && r0 + k * nwarps < nocl * HX; ++k) {
+                const int r = r0 + k * nwarps;
+                const uint32_t e0 = __shfl_sync(kFull, be0, k), e1 = __shfl_sync(kFull, be1, k);
+                if (e0 >= e1) continue;
+                const int ocl = __float2int_rz(((float)r + 0.5f) * invHX);
+                const int hxr = r - ocl * HX;
+                const int xs = x0 - kg.hx + hxr;
+                const int64_t row = ((b * c_out + oc0 + ocl) * gy.X + xs) * (int64_t)gy.Y + hylo;
+                const uint64_t rowbase = (uint64_t)row * (uint64_t)gy.Z;
+                const int gbase = (ocl * HXY + hxr * HY + (hylo - (y0 - kg.hy))) * ZR + kg.hz;
+                for (uint32_t e = e0 + lane; e < e1; e += 128) {
+                    uint64_t kk[4];
+                    float dv[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (e + 32u * u >= e1) break;
-                    const uint32_t L = (uint32_t)(kk[u] - rowbase);
-                    uint32_t yr = __float2uint_rz(__uint2float_rz(L) * invZ);
-                    if (yr * (uint32_t)gy.Z > L) --yr;
-                    if ((yr + 1) * (uint32_t)gy.Z <= L) ++yr;
-                    G[gbase + (int)yr * ZR + (int)(L - yr * (uint32_t)gy.Z)] = dv[u];
+                    for (int u = 0; u < 4; ++u) {
+                        const uint32_t eu = e + 32u * u;
+                        kk[u] = eu < e1 ? ykeys[eu] : rowbase;
+                        dv[u] = eu < e1 ? dy[eu] : 0.0f;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (e + 32u * u >= e1) break;
+                        const uint32_t L = (uint32_t)(kk[u] - rowbase);
+                        uint32_t yr = __float2uint_rz(__uint2float_rz(L) * invZ);
+                        if (yr * (uint32_t)gy.Z > L) --yr;
+                        if ((yr + 1) * (uint32_t)gy.Z <= L) ++yr;
+                        G[gbase + (int)yr * ZR + (int)(L - yr * (uint32_t)gy.Z)] = dv[u];
+                    }
                 }
             }
         }
