@@ -42,21 +42,20 @@ __global__ void __launch_bounds__(kReluThreads) relu_write_kernel(const uint64_t
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t w0 = base + (int64_t)warp * (32 * kReluItems);
     const uint64_t pos0 = off[blockIdx.x];   // in flight with the value loads
+    // values and keys in one round trip (the keys' sectors are fetched anyway at these kept
+    // fractions), in flight during the block-wide scan
     float v[kReluItems];
+    uint64_t k[kReluItems];
 #pragma unroll
     for (int u = 0; u < kReluItems; ++u) {
         const int64_t i = w0 + 32 * u + lane;
         v[u] = i < n ? vals[i] : 0.0f;
+        k[u] = i < n ? keys[i] : 0ull;
     }
-    // keys of the kept entries are loaded before the block-wide scan so that their latency
-    // overlaps it
-    uint64_t k[kReluItems];
     unsigned m[kReluItems];
     uint32_t c = 0;
 #pragma unroll
     for (int u = 0; u < kReluItems; ++u) {
-        const int64_t i = w0 + 32 * u + lane;
-        k[u] = v[u] > 0.0f ? keys[i] : 0ull;
         m[u] = __ballot_sync(kFull, v[u] > 0.0f);
         c += (uint32_t)__popc(m[u]);
     }

@@ -17,7 +17,7 @@ namespace spc {
 
 constexpr int kTkThreads = 512;
 constexpr int kTkWarps = kTkThreads / 32;
-constexpr int kTkG = 16;                                // groups of 32 entries per warp and tile
+constexpr int kTkG = 8;                                 // groups of 32 entries per warp and tile
 constexpr uint32_t kTkTile = (uint32_t)kTkThreads * kTkG;
 constexpr uint32_t kTkCand = 8192;                      // bucket scores kept in shared memory (32 KB)
 
@@ -155,20 +155,21 @@ topk_seg_kernel(const uint64_t* __restrict__ keys, const float* __restrict__ val
         uint32_t bits[kTkG];
         unsigned kb[kTkG], tb[kTkG];
         uint32_t ntie = 0;
+        // values and keys together (one round trip; the keys' sectors are fetched anyway at
+        // these kept fractions)
+        uint64_t kk[kTkG];
 #pragma unroll
         for (int g = 0; g < kTkG; ++g) {
             const uint32_t i = w0 + 32u * g + lane;
             bits[g] = i < hi ? __float_as_uint(vals[i]) : 0u;
+            kk[g] = i < hi ? keys[i] : 0ull;
         }
-        // keys of the entries that may be kept are in flight during the scans below
-        uint64_t kk[kTkG];
 #pragma unroll
         for (int g = 0; g < kTkG; ++g) {
             const uint32_t i = w0 + 32u * g + lane;
             const bool in = i < hi;
             const uint32_t sc = score_bits(bits[g], attn) & pmask;
             const bool keep = in && (keep_all || sc > T), tie = in && !keep_all && sc == T;
-            kk[g] = (keep || tie) ? keys[i] : 0ull;
             kb[g] = __ballot_sync(kFull, keep);
             tb[g] = __ballot_sync(kFull, tie);
             ntie += (uint32_t)__popc(tb[g]);
