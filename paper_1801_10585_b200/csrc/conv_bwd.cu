@@ -177,8 +177,7 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
             rng[2 * q + 1] = hi;
         }
         // "initialize dense buffer with gradients(b, oc)", tile + halo, this oc group:
-        // per (oc, halo x-row) the kept outputs of the halo y-range are one contiguous key run;
-        // four entries per lane in flight
+        // per (oc, halo x-row) the kept outputs of the halo y-range are one contiguous key run
         const int hylo = max(0, y0 - kg.hy), hyhi = min(gy.Y, y0 + t.TY + kg.hy);
         const float invZ = 1.0f / (float)gy.Z;
         const float invHX = 1.0f / (float)HX;
@@ -197,36 +196,53 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
                     }
                 }
             }
-            for (int k = 0; k < 32 && r0 + k * nwarps < nocl * HX; ++k) {
-                const int r = r0 + k * nwarps;
-                const uint32_t e0 = __shfl_sync(kFull, be0, k), e1 = __shfl_sync(kFull, be1, k);
-                if (e0 >= e1) continue;
-                const int ocl = __float2int_rz(((float)r + 0.5f) * invHX);
-                const int hxr = r - ocl * HX;
-                const int xs = x0 - kg.hx + hxr;
-                const int64_t row = ((b * c_out + oc0 + ocl) * gy.X + xs) * (int64_t)gy.Y + hylo;
-                const uint64_t rowbase = (uint64_t)row * (uint64_t)gy.Z;
-                const int gbase = (ocl * HXY + hxr * HY + (hylo - (y0 - kg.hy))) * ZR + kg.hz;
-                for (uint32_t e = e0 + lane; e < e1; e += 128) {
-                    uint64_t kk[4];
-                    float dv[4];
+            // the rows' entries as one list (row k owns positions cum_k .. cum_k + len_k - 1), eight
+            // positions per lane in flight per batch; row starts in the warp's scratch words
+            const uint32_t len = be1 - be0;
+            const uint32_t incl = warp_incl_scan(len);
+            const uint32_t wtot = __shfl_sync(kFull, incl, 31);
+            __syncwarp();
+            st_eb[lane] = (int)(incl - len);   // cum_k
+            st_eb[32 + lane] = (int)be0;       // e0_k
+            __syncwarp();
+            const int nrows = min(32, (nocl * HX - r0 + nwarps - 1) / nwarps);
+            for (uint32_t base = 0; base < wtot; base += 256) {
+                uint64_t kk[8];
+                float dv[8];
+                int rk[8];
+                uint32_t pe[8];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const uint32_t eu = e + 32u * u;
-                        kk[u] = eu < e1 ? ykeys[eu] : rowbase;
-                        dv[u] = eu < e1 ? dy[eu] : 0.0f;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        if (e + 32u * u >= e1) break;
-                        const uint32_t L = (uint32_t)(kk[u] - rowbase);
-                        uint32_t yr = __float2uint_rz(__uint2float_rz(L) * invZ);
-                        if (yr * (uint32_t)gy.Z > L) --yr;
-                        if ((yr + 1) * (uint32_t)gy.Z <= L) ++yr;
-                        G[gbase + (int)yr * ZR + (int)(L - yr * (uint32_t)gy.Z)] = dv[u];
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t pos = base + 32u * j + (uint32_t)lane;
+                    rk[j] = -1;
+                    kk[j] = 0ull;
+                    dv[j] = 0.0f;
+                    if (pos < wtot) {
+                        int k = 0;
+                        while (k + 1 < nrows && (uint32_t)st_eb[k + 1] <= pos) ++k;
+                        const uint32_t e = (uint32_t)st_eb[32 + k] + (pos - (uint32_t)st_eb[k]);
+                        kk[j] = ykeys[e];
+                        dv[j] = dy[e];
+                        rk[j] = k;
                     }
                 }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (rk[j] < 0) continue;
+                    const int r = r0 + rk[j] * nwarps;
+                    const int ocl = __float2int_rz(((float)r + 0.5f) * invHX);
+                    const int hxr = r - ocl * HX;
+                    const int xs = x0 - kg.hx + hxr;
+                    const int64_t row = ((b * c_out + oc0 + ocl) * gy.X + xs) * (int64_t)gy.Y + hylo;
+                    const int gbase = (ocl * HXY + hxr * HY + (hylo - (y0 - kg.hy))) * ZR + kg.hz;
+                    const uint32_t L = (uint32_t)(kk[j] - (uint64_t)row * (uint64_t)gy.Z);
+                    uint32_t yr = __float2uint_rz(__uint2float_rz(L) * invZ);
+                    if (yr * (uint32_t)gy.Z > L) --yr;
+                    if ((yr + 1) * (uint32_t)gy.Z <= L) ++yr;
+                    G[gbase + (int)yr * ZR + (int)(L - yr * (uint32_t)gy.Z)] = dv[j];
+                }
             }
+            __syncwarp();
         }
         __syncthreads();
         if (warp == 0) {   // chunks per ic (32 entries each), exclusive prefix over ic
