@@ -256,6 +256,8 @@ BWD_CASES = [
     ("3d_tiles", (20, 24, 36), 2, 8, 8, (3, 3, 3), 0.03, 0.5),
     ("3d_wide_oc", (8, 9, 10), 1, 2, 40, (3, 3, 3), 0.06, 0.4),
     ("1d_k5", (50,), 3, 2, 2, (5,), 0.2, 0.8),
+    ("3d_wide_ic", (6, 7, 9), 1, 40, 3, (3, 3, 3), 0.05, 0.3),    # c_in > 32: shared chunk prefix
+    ("c5_like", (8, 10, 24), 1, 32, 32, (3, 3, 3), 0.2, 1.0),     # 32 channels, many chunks per ic
 ]
 
 
