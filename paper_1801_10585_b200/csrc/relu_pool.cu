@@ -258,9 +258,13 @@ pool_tile_write_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, con
     const uint64_t pbase = ((uint64_t)(t.seg * p.PX + t.px) * p.PY + t.py0) * (uint64_t)p.PZ;
     for (uint32_t q = tid; q < tot; q += kTileThreads) {
         const uint32_t cell = cells[q];
-        const uint32_t a = ~(uint32_t)best[cell];
+        const unsigned long long bst = best[cell];
+        const uint32_t a = ~(uint32_t)bst;
+        // the maximum's value from its order-preserving code; +-0 (the code cannot tell them
+        // apart) from the entry itself
+        const float mv = from_orderable((uint32_t)(bst >> 32));
         ok[o0 + q] = pbase + cell;
-        ov[o0 + q] = vals[a];
+        ov[o0 + q] = mv != 0.0f ? mv : vals[a];
         if (oarg) oarg[o0 + q] = a;
     }
 }
