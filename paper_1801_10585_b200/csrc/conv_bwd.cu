@@ -286,9 +286,13 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
             c.v = c.e >= 0 ? xvals[c.e] : 0.0f;
         };
         Loc cur{}, nxt{};
-        if (warp < nchunks) locate(warp, cur);
-        for (int f = warp; f < nchunks; f += nwarps) {
-            if (f + nwarps < nchunks) locate(f + nwarps, nxt);
+        // warp w takes a contiguous run of chunks (mostly one input channel): concurrent warps
+        // then mostly update different dw words
+        const int per = (nchunks + nwarps - 1) / nwarps;
+        const int fb = min(nchunks, warp * per), fe = min(nchunks, fb + per);
+        if (fb < fe) locate(fb, cur);
+        for (int f = fb; f < fe; ++f) {
+            if (f + 1 < fe) locate(f + 1, nxt);
             const int ic = cur.ic;
             const int64_t e = cur.e;
             int eb = eb_safe;
