@@ -874,19 +874,26 @@ __global__ void __launch_bounds__(32 * kWriteWarps) fwd_write_kernel(FwdArgs a, 
     const uint64_t kb = ((uint64_t)a.seg0 + (uint64_t)s) * (uint64_t)V;
     // composite(score, p) = (score << 32 | ~p) >= kstar, as two 32-bit compares
     const uint32_t ks = (uint32_t)(st.kstar >> 32), kp = (uint32_t)st.kstar;
-    for (uint32_t i0 = 0; i0 < n; i0 += 32) {
-        const uint32_t i = i0 + lane;
-        const bool ok = i < n;
-        const uint2 e = ok ? in[i] : make_uint2(0u, kAbsent);
-        const uint32_t sc = score_bits(e.y, a.attn);
-        const bool keep = ok && (st.keep_all || sc > ks || (sc == ks && ~e.x >= kp));
-        const unsigned m = __ballot_sync(kFull, keep);
-        if (keep) {
-            const uint64_t q = out + __popc(m & ((1u << lane) - 1u));
-            a.out_keys[q] = kb + e.x;
-            a.out_vals[q] = __uint_as_float(e.y);
+    for (uint32_t i0 = 0; i0 < n; i0 += 128) {   // four groups of 32 loaded before any is used
+        uint2 e[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            const uint32_t i = i0 + 32u * g + lane;
+            e[g] = i < n ? in[i] : make_uint2(0u, kAbsent);
         }
-        out += __popc(m);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            const bool ok = i0 + 32u * g + lane < n;
+            const uint32_t sc = score_bits(e[g].y, a.attn);
+            const bool keep = ok && (st.keep_all || sc > ks || (sc == ks && ~e[g].x >= kp));
+            const unsigned m = __ballot_sync(kFull, keep);
+            if (keep) {
+                const uint64_t q = out + __popc(m & ((1u << lane) - 1u));
+                a.out_keys[q] = kb + e[g].x;
+                a.out_vals[q] = __uint_as_float(e[g].y);
+            }
+            out += __popc(m);
+        }
     }
 }
 
