@@ -15,7 +15,7 @@
 
 namespace spc {
 
-constexpr int kTkThreads = 512;
+constexpr int kTkThreads = 256;
 constexpr int kTkWarps = kTkThreads / 32;
 constexpr int kTkG = 8;                                 // groups of 32 entries per warp and tile
 constexpr uint32_t kTkTile = (uint32_t)kTkThreads * kTkG;
@@ -41,7 +41,7 @@ __global__ void topk_offsets_kernel(const uint32_t* __restrict__ row_ptr, int64_
     if (threadIdx.x == 0) *total = (int64_t)carry;
 }
 
-__global__ void __launch_bounds__(kTkThreads, 2)
+__global__ void __launch_bounds__(kTkThreads, 4)
 topk_seg_kernel(const uint64_t* __restrict__ keys, const float* __restrict__ vals, const uint32_t* __restrict__ row_ptr,
                 int64_t R, int attn, int64_t k, const uint64_t* __restrict__ seg_off, uint64_t* __restrict__ ok,
                 float* __restrict__ ov, int64_t* __restrict__ osrc) {
