@@ -832,8 +832,15 @@ __global__ void __launch_bounds__(kResThreads) fwd_resolve_kernel(FwdArgs a) {
         st.kstar = kstar;
         a.seg[s] = st;
     }
+    // selected candidates per chunk; a chunk's candidates sit together in the list (classify
+    // appends them as one run), so the lanes of a warp aggregate their counts per chunk first
+    const int lane = threadIdx.x & 31;
+    uint32_t* tsel = a.tile_sel + s * a.nchunk;
     for_cands(c, n, [&](uint2 e) {
-        if (composite(score_bits(e.y, a.attn), e.x) >= kstar) atomicAdd(&a.tile_sel[s * a.nchunk + e.x / kChunk], 1u);
+        const bool sel = composite(score_bits(e.y, a.attn), e.x) >= kstar;
+        const uint32_t ch = sel ? e.x / kChunk : 0xffffffffu;
+        const unsigned grp = __match_any_sync(__activemask(), ch);
+        if (sel && lane == __ffs(grp) - 1) atomicAdd(&tsel[ch], (uint32_t)__popc(grp));
     });
 }
 
