@@ -516,10 +516,11 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
                     hist4[i] = make_uint4(0u, 0u, 0u, 0u);
                     if (4 * i < kSelBins) {
                         cnt += h.x + h.y + h.z + h.w;
-                        if (h.x) atomicAdd(gh + 4 * i, h.x);
-                        if (h.y) atomicAdd(gh + 4 * i + 1, h.y);
-                        if (h.z) atomicAdd(gh + 4 * i + 2, h.z);
-                        if (h.w) atomicAdd(gh + 4 * i + 3, h.w);
+                        // two adjacent bins per 64-bit atomic (a bin's total is at most V < 2^32,
+                        // so the low word never carries into the high one)
+                        unsigned long long* g2 = reinterpret_cast<unsigned long long*>(gh + 4 * i);
+                        if (h.x | h.y) atomicAdd(g2, (unsigned long long)h.x | ((unsigned long long)h.y << 32));
+                        if (h.z | h.w) atomicAdd(g2 + 1, (unsigned long long)h.z | ((unsigned long long)h.w << 32));
                     }
                 }
             }
