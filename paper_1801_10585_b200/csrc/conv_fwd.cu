@@ -765,8 +765,12 @@ __global__ void __launch_bounds__(kResThreads) fwd_resolve_kernel(FwdArgs a) {
             st.kstar = kstar;
             a.seg[s] = st;
         }
-        for (uint32_t i = threadIdx.x; i < (uint32_t)n; i += blockDim.x)
-            if (sc[i] >= kstar) atomicAdd(&a.tile_sel[s * a.nchunk + (uint32_t)(~sc[i]) / kChunk], 1u);
+        for (uint32_t i = threadIdx.x; i < (uint32_t)n; i += blockDim.x) {   // aggregated per chunk in the warp
+            const bool sel = sc[i] >= kstar;
+            const uint32_t ch = sel ? (uint32_t)(~sc[i]) / kChunk : 0xffffffffu;
+            const unsigned grp = __match_any_sync(__activemask(), ch);
+            if (sel && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&a.tile_sel[s * a.nchunk + ch], (uint32_t)__popc(grp));
+        }
         return;
     }
     bool in_smem = false;
