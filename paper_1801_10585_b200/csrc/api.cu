@@ -438,7 +438,13 @@ spc_status_t sparse_conv_fwd_ex(const spc_map_t* x, const spc_filter_t* w, const
     Carver c(workspace);
     FwdWs ws = carve_fwd(c, gx, gy, kg, t, w, attn, gpp);
     if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
-    SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));   // both variants
+    if (!use_gemm) {   // row index with the value guard fused (the scatter kernel reads the guard)
+        SPC_TRY(cu(cudaMemsetAsync(ws.a.guard, 0, sizeof(int), s)));
+        SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s, x->values, ws.a.guard)));
+        ws.a.guard_done = 1;
+    } else {
+        SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
+    }
     if (!use_gemm) {
         SPC_TRY(cu(launch_filter_table_fwd(kg, (int)w->c_in, (int)w->c_out, w->keys, w->values, w->nnz, ws.meta2,
                                            ws.val2, ws.off2, ws.scratch2, s)));
@@ -522,7 +528,9 @@ spc_status_t sparse_conv_fwd_pass(const spc_map_t* x, const spc_filter_t* w, con
     Carver c(workspace);
     FwdWs ws = carve_fwd(c, gx, gyp, kg, t, w, attn, nullptr);
     if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
-    SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
+    SPC_TRY(cu(cudaMemsetAsync(ws.a.guard, 0, sizeof(int), s)));
+    SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s, x->values, ws.a.guard)));
+    ws.a.guard_done = 1;
     SPC_TRY(cu(launch_filter_table_fwd(kg, (int)w->c_in, (int)w->c_out, w->keys, w->values, w->nnz, ws.meta2,
                                        ws.val2, ws.off2, ws.scratch2, s)));
     FwdArgs a = ws.a;

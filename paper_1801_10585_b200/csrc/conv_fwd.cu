@@ -932,8 +932,8 @@ cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& k
         if (eg != cudaSuccess) return eg;
     } else {
         if (!a.out_append) {   // later passes of sparse_conv_fwd_pass reuse the guard and the rounds
-            cudaMemsetAsync(a.guard, 0, sizeof(int), s);
-            {
+            if (!a.guard_done) {
+                cudaMemsetAsync(a.guard, 0, sizeof(int), s);
                 SPC_PHASE("value_guard", s, 1);
                 value_guard_kernel<<<148 * 4, 256, 0, s>>>(a.xvals, a.x_nnz_dev, a.x_nnz, a.guard);
             }

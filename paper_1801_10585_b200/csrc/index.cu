@@ -31,7 +31,8 @@ __device__ __forceinline__ int32_t row_of(uint32_t key, uint32_t Z, uint32_t mag
 template <typename K, typename I>   // key word, row / entry index type
 __global__ void __launch_bounds__(256) row_index_kernel(K Z, K magic, const uint64_t* __restrict__ keys,
                                                         const int64_t* nnz_dev, int64_t nbound,
-                                                        uint32_t* __restrict__ row_ptr, I total_rows) {
+                                                        uint32_t* __restrict__ row_ptr, I total_rows,
+                                                        const float* __restrict__ vals, int* __restrict__ guard) {
     constexpr int kB = 256 * kRiItems;   // entries per block
     __shared__ I srow[kB + 1];           // srow[1 + t] = row of entry b0 + t; srow[0] = row of b0 - 1
     const I n = (I)load_n(nnz_dev, nbound);
@@ -39,14 +40,19 @@ __global__ void __launch_bounds__(256) row_index_kernel(K Z, K magic, const uint
     if (b0 > n) return;
     const int lane = threadIdx.x & 31;
     // rows of the block's entries, computed from coalesced key loads
+    bool tiny = false;   // the forward's value guard (value_guard_kernel), fused when vals != null
 #pragma unroll
     for (int q = 0; q < kRiItems; ++q) {
         const int t = q * 256 + threadIdx.x;
         const I i = b0 + t;
         srow[1 + t] = i < n ? (I)row_of((K)keys[i], Z, magic) : total_rows;
+        if (vals && i < n) {
+            const float v = vals[i];
+            tiny |= !(fabsf(v) >= 0x1p-50f) && !isnan(v);
+        }
     }
     if (threadIdx.x == 0) srow[0] = b0 == 0 ? (I)-1 : (I)row_of((K)keys[b0 - 1], Z, magic);
-    __syncthreads();
+    if (__syncthreads_or(tiny) && threadIdx.x == 0) *guard = 1;
     // entry i (and the sentinel i = n) fills the rows between its predecessor's row and its own
 #pragma unroll
     for (int q = 0; q < kRiItems; ++q) {
@@ -74,7 +80,7 @@ __global__ void __launch_bounds__(256) row_index_kernel(K Z, K magic, const uint
 }
 
 cudaError_t launch_row_index(const Geo& g, const uint64_t* keys, const int64_t* nnz_dev, int64_t nbound,
-                             uint32_t* row_ptr, cudaStream_t s) {
+                             uint32_t* row_ptr, cudaStream_t s, const float* vals, int* guard) {
     const int64_t total_rows = g.B * g.C * g.R;
     const int bs = 256;
     const int64_t grid = (nbound + 1 + (int64_t)bs * kRiItems - 1) / ((int64_t)bs * kRiItems);
@@ -84,12 +90,12 @@ cudaError_t launch_row_index(const Geo& g, const uint64_t* keys, const int64_t* 
         const uint32_t Z = (uint32_t)g.Z;
         const uint32_t magic = Z == 1 ? ~0u : ~0u / Z;
         row_index_kernel<uint32_t, int32_t><<<(unsigned)grid, bs, 0, s>>>(Z, magic, keys, nnz_dev, nbound, row_ptr,
-                                                                            (int32_t)total_rows);
+                                                                            (int32_t)total_rows, vals, guard);
     } else {
         const uint64_t Z = (uint64_t)g.Z;
         const uint64_t magic = Z == 1 ? ~0ull : ~0ull / Z;   // floor((2^64 - 1) / Z)
         row_index_kernel<uint64_t, int64_t><<<(unsigned)grid, bs, 0, s>>>(Z, magic, keys, nnz_dev, nbound, row_ptr,
-                                                                            total_rows);
+                                                                            total_rows, vals, guard);
     }
     return cudaGetLastError();
 }

@@ -85,9 +85,10 @@ struct PhaseScope {
 
 // ------------------------------------------------------------------ launchers (host)
 // Row index: row_ptr[r] = first entry with key >= r*Z, r in [0, B*C*R]; workspace
-// (B*C*R + 1) uint32 words. Requires nnz < 2^32.
+// (B*C*R + 1) uint32 words. Requires nnz < 2^32. With vals / guard: also the forward's value
+// guard (*guard = 1 when some stored |x| < 2^-50; *guard must be zeroed before).
 cudaError_t launch_row_index(const Geo& g, const uint64_t* keys, const int64_t* nnz_dev, int64_t nnz_bound,
-                             uint32_t* row_ptr, cudaStream_t s);
+                             uint32_t* row_ptr, cudaStream_t s, const float* vals = nullptr, int* guard = nullptr);
 
 // Filter table in ic-major order. meta[j] = {oc, packed offset}; val[j]; off[ic*(c_out+1)+oc]
 // = first table entry of (ic, oc) (off[ic*(c_out+1)+c_out] = end); src[j] = original filter
@@ -164,6 +165,7 @@ struct FwdArgs {
     // after the *out_nnz entries already written (and *out_nnz grows by them)
     int64_t b0, seg0;
     int out_append;
+    int guard_done;   // the value guard ran with the row index (launch_row_index with vals)
 };
 // Variant G of the forward accumulate (conv_gemm.cu): tcgen05 TF32 (3xTF32) implicit GEMM over
 // filter offsets, writing the same dense pre-attention buffer as the scatter kernel.

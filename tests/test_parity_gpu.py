@@ -674,3 +674,24 @@ def test_topk_ties_across_tiles_and_mixed_segments(cuda_lib, attn):
         np.testing.assert_array_equal(host_keys(yk), ok_)
         np.testing.assert_array_equal(host(yv).view(np.uint32), ov.view(np.uint32))
         np.testing.assert_array_equal(host(src[:yk.shape[0]]), osrc)
+
+
+def test_fwd_tiny_values_keep_structural_support(cuda_lib):
+    """Inputs below 2^-50 (products underflow to +-0 in fp32): the forward switches to the
+    NaN-marker accumulation (value guard, fused with the row index) so every reached voxel stays
+    in the support (reading R3); values compare as numbers (0 == -0)."""
+    spc = cuda_lib
+    x = uniform_map(2, 3, (9, 10, 11), 0.15, 91)
+    w = sparse_filter(3, 4, (3, 3, 3), 0.6, 91)
+    vals = x.values.copy()
+    vals[::3] *= np.float32(1e-30)          # a third of the inputs tiny: products underflow
+    xt = COO(x.batch, x.channels, x.dims, x.keys, vals)
+    fk, fv, fa, _ = ora.conv_fwd(xt, w, None, with_abs=True)
+    gk, gv, _ = run_fwd(spc, xt, w, None, "none", 0)
+    np.testing.assert_array_equal(gk, fk)
+    assert_values_close(gv, fv, fa)
+    for variant in ("scatter",):
+        y = spc.sparse_conv_fwd(dev_map(spc, xt), dev_filter(spc, w), None, "none", 0, variant=variant,
+                                samples_per_pass=1)
+        pk, pv = (host(t) for t in y.trimmed())
+        np.testing.assert_array_equal(pk.view(np.uint64), fk)
