@@ -289,9 +289,9 @@ spc_status_t conv_bwd_impl(const spc_map_t* x, const spc_filter_t* w, const spc_
     if (dbias) {
         SPC_TRY(cu(cudaMemsetAsync(ws.db_acc, 0, sizeof(double) * (size_t)w->c_out, s)));
         SPC_TRY(cu(launch_dbias(gy, ws.yrow, dy, ws.db_acc, s)));
-        SPC_TRY(cu(launch_f64_to_f32(ws.db_acc, dbias, w->c_out, s)));
     }
-    if (!want_dx && !want_dw) return SPC_OK;
+    const int64_t nb = dbias ? w->c_out : 0;   // dbias rounded with dw (one launch)
+    if (!want_dx && !want_dw) return cu(launch_f64_to_f32_2(ws.db_acc, dbias, nb, nullptr, nullptr, 0, s));
     SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
     SPC_TRY(cu(launch_filter_table(kg, (int)w->c_in, (int)w->c_out, w->keys, w->values, w->nnz, ws.f.meta, ws.f.val,
                                    ws.f.off, ws.f.src, ws.f.scratch, s)));
@@ -299,8 +299,7 @@ spc_status_t conv_bwd_impl(const spc_map_t* x, const spc_filter_t* w, const spc_
     if (want_dw && w->nnz > 0) SPC_TRY(cu(cudaMemsetAsync(ws.dw_acc, 0, sizeof(double) * (size_t)w->nnz, s)));
     SPC_TRY(cu(launch_conv_bwd(gx, gy, kg, t, x->keys, x->values, ws.xrow, y->keys, dy, ws.yrow, ws.f.meta, ws.f.val,
                                ws.f.off, ws.f.src, dx, ws.dw_acc, want_dx, want_dw, s)));
-    if (want_dw) SPC_TRY(cu(launch_f64_to_f32(ws.dw_acc, dw, w->nnz, s)));
-    return SPC_OK;
+    return cu(launch_f64_to_f32_2(ws.db_acc, dbias, nb, ws.dw_acc, dw, want_dw ? w->nnz : 0, s));
 }
 
 // -------------------------------------------------------------------- selection ws

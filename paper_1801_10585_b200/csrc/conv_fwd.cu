@@ -595,6 +595,26 @@ __global__ void seg_scan_u64_kernel(const uint64_t* in, uint64_t* out, int64_t n
     }
 }
 
+// two independent segment scans in one launch (candidate and staging offsets)
+__global__ void seg_scan2_u64_kernel(const uint64_t* in, uint64_t* out, const uint64_t* in2, uint64_t* out2, int64_t n) {
+    __shared__ uint64_t sm[33];
+    for (int pass = 0; pass < 2; ++pass) {
+        const uint64_t* src = pass ? in2 : in;
+        uint64_t* dst = pass ? out2 : out;
+        if (!src) continue;   // block-uniform
+        uint64_t carry = 0;
+        for (int64_t base = 0; base < n; base += blockDim.x) {
+            const int64_t i = base + threadIdx.x;
+            const uint64_t v = i < n ? src[i] : 0;
+            uint64_t t;
+            const uint64_t ex = block_excl_scan(v, sm, &t);
+            if (i < n) dst[i] = carry + ex;
+            carry += t;
+        }
+        if (threadIdx.x == 0) dst[n] = carry;
+    }
+}
+
 constexpr int kChunkThreads = 256;
 constexpr int kChunkItems = 16;
 constexpr int kChunk = kChunkThreads * kChunkItems;   // voxels per chunk of a (b, oc) buffer
@@ -951,9 +971,9 @@ cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& k
     }
     { SPC_PHASE("fwd_find", s, 1); fwd_find_kernel<<<(unsigned)nseg, 256, 0, s>>>(a, nseg); }
     {
-        SPC_PHASE("seg_scan", s, a.attn != SPC_ATTN_NONE ? 2 : 1);
-        if (a.attn != SPC_ATTN_NONE) seg_scan_u64_kernel<<<1, 1024, 0, s>>>(a.cand_cnt, a.cand_off, nseg, nullptr);
-        seg_scan_u64_kernel<<<1, 1024, 0, s>>>(a.stg_cnt, a.stg_off, nseg, nullptr);
+        SPC_PHASE("seg_scan", s, 1);
+        seg_scan2_u64_kernel<<<1, 1024, 0, s>>>(a.attn != SPC_ATTN_NONE ? a.cand_cnt : nullptr, a.cand_off, a.stg_cnt,
+                                               a.stg_off, nseg);
     }
     { SPC_PHASE("fwd_classify", s, 1); fwd_classify_kernel<<<sgrid, kChunkThreads, 0, s>>>(a, gy.V); }
     if (a.attn != SPC_ATTN_NONE) {

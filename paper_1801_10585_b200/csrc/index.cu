@@ -318,6 +318,24 @@ __global__ void f64_to_f32_kernel(const double* __restrict__ a, float* __restric
         b[i] = (float)a[i];
 }
 
+// two ranges in one launch (the backward's dw and dbias)
+__global__ void f64_to_f32_2_kernel(const double* __restrict__ a, float* __restrict__ b, int64_t n,
+                                    const double* __restrict__ a2, float* __restrict__ b2, int64_t n2) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n + n2; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < n) b[i] = (float)a[i];
+        else b2[i - n] = (float)a2[i - n];
+    }
+}
+
+cudaError_t launch_f64_to_f32_2(const double* a, float* b, int64_t n, const double* a2, float* b2, int64_t n2,
+                                cudaStream_t s) {
+    if (n + n2 <= 0) return cudaSuccess;
+    int64_t grid = (n + n2 + 255) / 256;
+    if (grid > 1184) grid = 1184;
+    { SPC_PHASE("f64_to_f32", s, 1); f64_to_f32_2_kernel<<<(unsigned)grid, 256, 0, s>>>(a, b, n, a2, b2, n2); }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_f64_to_f32(const double* a, float* b, int64_t n, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     int64_t grid = (n + 255) / 256;

@@ -224,6 +224,8 @@ cudaError_t launch_conv_bwd(const Geo& gx, const Geo& gy, const KGeo& kg, const 
                             float* dx, double* dw_acc, bool want_dx, bool want_dw, cudaStream_t s);
 cudaError_t launch_dbias(const Geo& gy, const uint32_t* yrow, const float* dy, double* db_acc, cudaStream_t s);
 cudaError_t launch_f64_to_f32(const double* a, float* b, int64_t n, cudaStream_t s);
+cudaError_t launch_f64_to_f32_2(const double* a, float* b, int64_t n, const double* a2, float* b2, int64_t n2,
+                                cudaStream_t s);
 
 // ---------------------------------------------------------------- selection (attention)
 constexpr int kSelBins = 2048;    // 11-bit score digits
