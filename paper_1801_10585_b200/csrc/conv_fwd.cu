@@ -392,6 +392,7 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
             for (int pk = warp; pk < PK; pk += kFwdWarps)
                 wtot += max(0, min(ioff[pk + 1], f1) - max(ioff[pk], f0));
             constexpr int kJ = 8;
+            int cpk = warp, ccum = 0;   // this lane's item cursor: its positions only increase
             for (int base = 0; base < wtot; base += 32 * kJ) {
                 uint32_t kw[kJ], rbj[kJ];
                 float vj[kJ];
@@ -404,12 +405,12 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
                     rbj[j] = 0u;
                     vj[j] = 0.0f;
                     if (pos < wtot) {
-                        int pk = warp, cum = 0;
-                        for (;; pk += kFwdWarps) {   // the item holding list position pos
-                            const int len = max(0, min(ioff[pk + 1], f1) - max(ioff[pk], f0));
-                            if (pos < cum + len) break;
-                            cum += len;
+                        for (;; cpk += kFwdWarps) {   // advance to the item holding list position pos
+                            const int len = max(0, min(ioff[cpk + 1], f1) - max(ioff[cpk], f0));
+                            if (pos < ccum + len) break;
+                            ccum += len;
                         }
+                        const int pk = cpk, cum = ccum;
                         const int f = max(ioff[pk], f0) + (pos - cum);
                         const uint32_t e = iglob[pk] - (uint32_t)ioff[pk] + (uint32_t)f;
                         kw[j] = xk32[2 * (size_t)e];
