@@ -180,6 +180,7 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
         // per (oc, halo x-row) the kept outputs of the halo y-range are one contiguous key run
         const int hylo = max(0, y0 - kg.hy), hyhi = min(gy.Y, y0 + t.TY + kg.hy);
         const float invZ = 1.0f / (float)gy.Z;
+        const float invXZ = 1.0f / (float)gx.Z;
         const float invHX = 1.0f / (float)HX;
         // the warp's rows r = warp + k * nwarps: lane k loads row k's bounds (one latency for all)
         for (int r0 = warp; r0 < nocl * HX; r0 += 32 * nwarps) {
@@ -300,7 +301,7 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
             if (e >= 0) {
                 const int64_t r0 = ((b * c_in + ic) * gx.X + x0 + cur.xi) * (int64_t)gx.Y + y0;
                 const uint32_t L = (uint32_t)(cur.key - (uint64_t)r0 * (uint64_t)gx.Z);
-                const uint32_t yl = L / (uint32_t)gx.Z;
+                const uint32_t yl = div_small(L, (uint32_t)gx.Z, invXZ);   // L < TY * Z
                 const int z = (int)(L - yl * (uint32_t)gx.Z);
                 eb = ((cur.xi + kg.hx) * HY + (int)yl + kg.hy) * ZR + z + kg.hz;
             }

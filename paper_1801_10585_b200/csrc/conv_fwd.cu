@@ -145,14 +145,6 @@ __global__ void fwd_rounds_kernel(KGeo kg, int c_in, int c_out, FwdTile t, const
     if (threadIdx.x == 0) RO[NQ] = carry;
 }
 
-// fast y = L / Z for L < 2^24 (float reciprocal + one correction each way)
-__device__ __forceinline__ uint32_t div_small(uint32_t L, uint32_t Z, float invZ) {
-    uint32_t q = __float2uint_rz(__uint2float_rz(L) * invZ);
-    if (q * Z > L) --q;
-    if ((q + 1) * Z <= L) ++q;
-    return q;
-}
-
 __device__ __forceinline__ uint64_t composite(uint32_t sc, uint32_t p) {
     return ((uint64_t)sc << 32) | (uint64_t)(0xffffffffu - p);
 }

@@ -61,6 +61,14 @@ __device__ __forceinline__ float from_orderable(uint32_t o) {
     return __uint_as_float(b);
 }
 
+// fast y = L / Z for L < 2^24 (float reciprocal + one correction each way)
+__device__ __forceinline__ uint32_t div_small(uint32_t L, uint32_t Z, float invZ) {
+    uint32_t q = __float2uint_rz(__uint2float_rz(L) * invZ);
+    if (q * Z > L) --q;
+    if ((q + 1) * Z <= L) ++q;
+    return q;
+}
+
 __device__ __forceinline__ int64_t load_n(const int64_t* nnz_dev, int64_t bound) {
     if (!nnz_dev) return bound;
     int64_t n = *nnz_dev;
