@@ -203,25 +203,44 @@ FwdWs carve_fwd(Carver& c, const Geo& gx, const Geo& gy, const KGeo& kg, const F
     ws.scratch2 = c.take<int>((size_t)2 * w->c_in * KXY * w->c_out);
     FwdArgs& a = ws.a;
     a.seg_count = c.take<unsigned long long>((size_t)nseg);
-    a.hist = c.take<uint32_t>((size_t)nseg * kSelBins);
     a.seg = c.take<FwdSeg>((size_t)nseg);
-    a.nchunk = (gy.V + 4095) / 4096;
     a.nseg = nseg;
-    a.pre = c.take<float>((size_t)(nseg * gy.V));
-    a.tile_def = c.take<uint32_t>((size_t)(nseg * a.nchunk));
-    a.tile_sel = c.take<uint32_t>((size_t)(nseg * a.nchunk));
-    a.tile_off = c.take<uint64_t>((size_t)(nseg * a.nchunk));
-    a.cand_off = c.take<uint64_t>((size_t)nseg + 1);
+    a.seg_off = c.take<uint64_t>((size_t)nseg + 1);
     a.cand_cnt = c.take<uint64_t>((size_t)nseg + 1);
     a.cand_cur = c.take<unsigned long long>((size_t)nseg);
-    a.cand = c.take<uint2>(attn == SPC_ATTN_NONE ? 1 : (size_t)(nseg * gy.V));
-    a.seg_off = c.take<uint64_t>((size_t)nseg + 1);
-    a.stg = c.take<uint2>((size_t)(nseg * gy.V));
-    a.stg_cnt = c.take<uint64_t>((size_t)nseg + 1);
-    a.stg_off = c.take<uint64_t>((size_t)nseg + 1);
-    a.stg_cur = c.take<unsigned long long>((size_t)nseg);
-    a.chunk_stg = c.take<uint64_t>((size_t)(nseg * a.nchunk));
-    a.chunk_ge = c.take<uint32_t>((size_t)(nseg * a.nchunk));
+    a.seg_stride = (int)gy.C;
+    if (gp) {   // variant G: the dense pre-attention buffer and the classify / resolve lists
+        a.hist = c.take<uint32_t>((size_t)nseg * kSelBins);
+        a.nchunk = (gy.V + 4095) / 4096;
+        a.pre = c.take<float>((size_t)(nseg * gy.V));
+        a.tile_def = c.take<uint32_t>((size_t)(nseg * a.nchunk));
+        a.tile_sel = c.take<uint32_t>((size_t)(nseg * a.nchunk));
+        a.tile_off = c.take<uint64_t>((size_t)(nseg * a.nchunk));
+        a.cand_off = c.take<uint64_t>((size_t)nseg + 1);
+        a.cand = c.take<uint2>(attn == SPC_ATTN_NONE ? 1 : (size_t)(nseg * gy.V));
+        a.stg = c.take<uint2>((size_t)(nseg * gy.V));
+        a.stg_cnt = c.take<uint64_t>((size_t)nseg + 1);
+        a.stg_off = c.take<uint64_t>((size_t)nseg + 1);
+        a.stg_cur = c.take<unsigned long long>((size_t)nseg);
+        a.chunk_stg = c.take<uint64_t>((size_t)(nseg * a.nchunk));
+        a.chunk_ge = c.take<uint32_t>((size_t)(nseg * a.nchunk));
+    } else {    // variant S, streamed: candidate runs (8 B per voxel and output channel) + tiles
+        plan_fwd_sampling(gy, t, attn, &a);
+        const size_t nt = (size_t)nseg * (size_t)a.ntile;
+        if (a.nsamp > 0) a.hist = c.take<uint32_t>((size_t)nseg * kSelBins);
+        a.tlow = c.take<uint32_t>((size_t)nseg);
+        a.cmax = c.take<uint32_t>((size_t)nseg);
+        a.fail = c.take<int>((size_t)nseg);
+        a.bflag = c.take<int>((size_t)std::max<int64_t>(gy.B, 1));
+        a.redo_b = c.take<int>((size_t)std::max<int64_t>(gy.B, 1));
+        a.redo_n = c.take<int>(1);
+        a.cpos = c.take<uint32_t>((size_t)(nseg * gy.V));
+        a.cval = c.take<float>((size_t)(nseg * gy.V));
+        a.tcnt = c.take<uint32_t>(nt);
+        a.tile_def = c.take<uint32_t>(nt);
+        a.tile_sel = c.take<uint32_t>(nt);
+        a.tile_off = c.take<uint64_t>(nt);
+    }
     const size_t PK = (size_t)w->c_in * kg.kx;
     a.rnd = c.take<int2>((size_t)t.n_ocg * t.nwg_max + 1);
     a.roff = c.take<int>((size_t)t.n_ocg * (t.ocg * PK + 1));
@@ -475,7 +494,7 @@ spc_status_t sparse_conv_fwd_ex(const spc_map_t* x, const spc_filter_t* w, const
         g.xrow = ws.xrow;
         return cu(launch_conv_fwd_pipeline(gx, gy, kg, t, a, s, &gp, &g));
     }
-    return cu(launch_conv_fwd_pipeline(gx, gy, kg, t, a, s));
+    return cu(launch_conv_fwd_stream(gx, gy, kg, t, a, s));
 }
 
 spc_status_t sparse_conv_fwd(const spc_map_t* x, const spc_filter_t* w, const float* bias, spc_attn_t attn, int64_t k,
@@ -555,7 +574,7 @@ spc_status_t sparse_conv_fwd_pass(const spc_map_t* x, const spc_filter_t* w, con
         a.seg0 = b0 * gy.C;
         a.nseg = gyl.B * gy.C;
         a.out_append = b0 > 0;
-        SPC_TRY(cu(launch_conv_fwd_pipeline(gx, gyl, kg, t, a, s)));
+        SPC_TRY(cu(launch_conv_fwd_stream(gx, gyl, kg, t, a, s)));
     }
     return SPC_OK;
 }

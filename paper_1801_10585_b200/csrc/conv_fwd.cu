@@ -149,13 +149,13 @@ __device__ __forceinline__ uint64_t composite(uint32_t sc, uint32_t p) {
     return ((uint64_t)sc << 32) | (uint64_t)(0xffffffffu - p);
 }
 
-// Epilogue rows of one output channel: bias on the support, streaming store of the slice,
-// support count and (with attention) the score-digit histogram. Branch-free: lanes off the
-// support increment a private dummy bin past the histogram instead of branching around the
+// Sampled-pass epilogue rows of one output channel: bias on the support, support count and
+// the score-digit histogram (the responses themselves are not stored). Branch-free: lanes off
+// the support increment a private dummy bin past the histogram instead of branching around the
 // atomic.
 template <int MODE>
-__device__ __forceinline__ void epi_rows(const float* S, float* P, float bv, int nyr, int Z, int ZR, uint32_t hist_s,
-                                         uint32_t& cnt, uint32_t marker) {
+__device__ __forceinline__ void epi_hist_rows(const float* S, float bv, int nyr, int Z, int ZR, uint32_t hist_s,
+                                              uint32_t marker) {
     const bool vec = (Z & 3) == 0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t dummy = hist_s + (uint32_t)(kSelBins + lane) * 4u;
@@ -173,22 +173,73 @@ __device__ __forceinline__ void epi_rows(const float* S, float* P, float bv, int
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const bool pres = __float_as_uint(v[u]) != marker;
-                v[u] = pres ? v[u] + bv : __uint_as_float(kAbsent);
-                if (MODE == SPC_ATTN_NONE) cnt += pres ? 1u : 0u;   // else: the histogram total
-                if (MODE != SPC_ATTN_NONE) {
-                    const uint32_t addr = pres ? hist_s + ((score_bits(__float_as_uint(v[u]), MODE) >> 21) << 2) : dummy;
-                    asm volatile("red.shared.add.u32 [%0], 1;" :: "r"(addr) : "memory");
-                }
-            }
-            if (vec) {
-                __stcs(reinterpret_cast<float4*>(P + (int64_t)r * Z + z0), make_float4(v[0], v[1], v[2], v[3]));
-            } else {
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (z0 + u < Z) __stcs(P + (int64_t)r * Z + z0 + u, v[u]);
+                const uint32_t addr =
+                    pres ? hist_s + ((score_bits(__float_as_uint(v[u] + bv), MODE) >> 21) << 2) : dummy;
+                asm volatile("red.shared.add.u32 [%0], 1;" :: "r"(addr) : "memory");
             }
         }
     }
+}
+
+// Candidate epilogue of one output channel (warp = channel, no block barrier): "get non-zero
+// entries" (structural support R3), "add bias", and every support entry whose score
+// reaches the segment's threshold tlow is appended in key order to the tile's candidate run.
+// Row by row, 128 voxels per step: lane l holds z = z0 + l + 32u (u = 0..3), so each of the four
+// 32-voxel groups is one ballot. Candidates are ranked into a per-warp shared-memory buffer
+// (branch-free: non-candidates store to a private dummy slot) that is flushed to the run with
+// coalesced stores. Returns the run length, the support size and the largest candidate score.
+constexpr int kCandBuf = 160;   // per-warp buffer entries (+ 32 dummy slots), in the staging area
+template <int MODE>
+__device__ __forceinline__ void epi_cand(const float* S, int nyr, int Z, int ZR, float bv, uint32_t tlow,
+                                         uint32_t marker, uint32_t pbase, uint32_t* __restrict__ cpos,
+                                         float* __restrict__ cval, uint32_t* bufp, float* bufv, uint32_t& n_out,
+                                         uint32_t& sup_out, uint32_t& max_out) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t dummy = kCandBuf + (uint32_t)lane;
+    uint32_t nb = 0, nf = 0, sup = 0, mx = 0;   // buffered, flushed
+    for (int r = 0; r < nyr; ++r) {
+        const float* row = S + r * ZR;
+        const uint32_t prow = pbase + (uint32_t)(r * Z);
+        for (int z0 = 0; z0 < Z; z0 += 128) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int z = z0 + 32 * u + lane;
+                const float raw = z < Z ? row[z] : __uint_as_float(marker);
+                const bool pres = __float_as_uint(raw) != marker;
+                const float val = raw + bv;
+                const uint32_t sc = MODE == SPC_ATTN_NONE ? 0u : score_bits(__float_as_uint(val), MODE);
+                const bool c = pres && sc >= tlow;
+                sup += pres ? 1u : 0u;
+                mx = c ? max(mx, sc) : mx;
+                const uint32_t bal = __ballot_sync(kFull, c);
+                const uint32_t slot = c ? nb + (uint32_t)__popc(bal & lt) : dummy;
+                bufp[slot] = prow + (uint32_t)z;
+                bufv[slot] = val;
+                nb += (uint32_t)__popc(bal);
+            }
+            if (nb > kCandBuf - 128) {   // flush: coalesced copy of the buffer to the run
+                __syncwarp();
+                for (uint32_t i = lane; i < nb; i += 32) {
+                    cpos[nf + i] = bufp[i];
+                    cval[nf + i] = bufv[i];
+                }
+                nf += nb;
+                nb = 0;
+                __syncwarp();
+            }
+        }
+    }
+    __syncwarp();
+    for (uint32_t i = lane; i < nb; i += 32) {
+        cpos[nf + i] = bufp[i];
+        cval[nf + i] = bufv[i];
+    }
+    n_out = nf + nb;
+    sup_out = warp_sum(sup);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, d));
+    max_out = mx;
 }
 
 // "add val*fval to buffer at uid" on the shared accumulator; the first update of a voxel
@@ -219,41 +270,71 @@ __device__ __forceinline__ float upd(float old, float v, float w) {
 // positions, so the 64 targets of a round are distinct; rounds are separated by __syncwarp (a
 // later round may read what an earlier one wrote). Idle lanes address a safe interior word
 // (every round offset keeps it inside the slice) and do not store.
+// One work descriptor as a warp needs it: its round range and the lane's two entries.
+struct FwdDesc {
+    int r0, r1;          // rounds (records) of (oc, item)
+    uint32_t aA, aB;     // accumulator byte addresses of the lane's entries (safe word when idle)
+    float vA, vB;
+    int n;               // entries of the descriptor (<= 64)
+};
+
+__device__ __forceinline__ FwdDesc load_desc(uint32_t wdsc, int lane, uint32_t accs, uint32_t safe,
+                                             const int* roffw, const uint32_t* spos, const float* sval) {
+    FwdDesc d;
+    const int item = (int)(wdsc >> 19);
+    d.r0 = roffw[item];
+    d.r1 = roffw[item + 1];
+    const int s = (int)(wdsc & 0xfffu);
+    d.n = (int)((wdsc >> 12) & 0x7fu);
+    const bool okA = lane < d.n, okB = lane + 32 < d.n;
+    d.aA = accs + (okA ? spos[s + lane] : safe);
+    d.vA = okA ? sval[s + lane] : 0.0f;
+    d.aB = accs + (okB ? spos[s + 32 + lane] : safe);
+    d.vB = okB ? sval[s + 32 + lane] : 0.0f;
+    return d;
+}
+
+// The accumulate loop of one warp (output channel slice fixed by the round records): every
+// work item (ic, input plane) of the staged chunk against the item's rounds {byte offset,
+// weight}, read from shared memory by broadcast. Entries go 64 at a time, two per lane, so that
+// two independent read-modify-writes are in flight per round. Entries of one item have distinct
+// positions, so the 64 targets of a round are distinct; rounds are separated by __syncwarp (a
+// later round may read what an earlier one wrote). Idle lanes address a safe interior word
+// (every round offset keeps it inside the slice) and do not store. The next descriptor's
+// dependent shared loads (descriptor -> round range, entries) are issued before the current
+// descriptor's rounds run.
 template <bool NEG0>
 __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, uint32_t safe, const uint32_t* work,
                                           const int* roffw, const int2* rec, const uint32_t* spos,
                                           const float* sval) {
+    if (nwork <= 0) return;
+    FwdDesc nx = load_desc(work[0], lane, accs, safe, roffw, spos, sval);
 #pragma unroll 1
     for (int g = 0; g < nwork; ++g) {
-        const uint32_t wdsc = work[g];                 // {chunk-relative start, count <= 64, item}
-        const int2 rr = make_int2(roffw[wdsc >> 19], roffw[(wdsc >> 19) + 1]);
-        if (rr.x == rr.y) continue;
-        const int s = (int)(wdsc & 0xfffu), n = (int)((wdsc >> 12) & 0x7fu);
-        const bool okA = lane < n, okB = lane + 32 < n;
-        const uint32_t aA = accs + (okA ? spos[s + lane] : safe);
-        const float vA = okA ? sval[s + lane] : 0.0f;
-        if (n > 32) {
-            const uint32_t aB = accs + (okB ? spos[s + 32 + lane] : safe);
-            const float vB = okB ? sval[s + 32 + lane] : 0.0f;
-            int2 q = rec[rr.x];
+        const FwdDesc d = nx;
+        if (g + 1 < nwork) nx = load_desc(work[g + 1], lane, accs, safe, roffw, spos, sval);
+        if (d.r0 == d.r1) continue;
+        const bool okA = lane < d.n, okB = lane + 32 < d.n;
+        if (d.n > 32) {
+            int2 q = rec[d.r0];
 #pragma unroll 2
-            for (int r = rr.x; r < rr.y; ++r) {
+            for (int r = d.r0; r < d.r1; ++r) {
                 const int2 qn = rec[r + 1];   // next record in flight during this round (rec has a spare slot)
-                const uint32_t qa = aA + (uint32_t)q.x, qb = aB + (uint32_t)q.x;
+                const uint32_t qa = d.aA + (uint32_t)q.x, qb = d.aB + (uint32_t)q.x;
                 const float w = __int_as_float(q.y);
                 const float oa = lds_u(qa), ob = lds_u(qb);
-                sts_p(qa, upd<NEG0>(oa, vA, w), okA);
-                sts_p(qb, upd<NEG0>(ob, vB, w), okB);
+                sts_p(qa, upd<NEG0>(oa, d.vA, w), okA);
+                sts_p(qb, upd<NEG0>(ob, d.vB, w), okB);
                 __syncwarp();
                 q = qn;
             }
         } else {
-            int2 q = rec[rr.x];
+            int2 q = rec[d.r0];
 #pragma unroll 2
-            for (int r = rr.x; r < rr.y; ++r) {
+            for (int r = d.r0; r < d.r1; ++r) {
                 const int2 qn = rec[r + 1];
-                const uint32_t qa = aA + (uint32_t)q.x;
-                sts_p(qa, upd<NEG0>(lds_u(qa), vA, __int_as_float(q.y)), okA);
+                const uint32_t qa = d.aA + (uint32_t)q.x;
+                sts_p(qa, upd<NEG0>(lds_u(qa), d.vA, __int_as_float(q.y)), okA);
                 __syncwarp();
                 q = qn;
             }
@@ -268,16 +349,19 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
 // plus halo, are contiguous key runs (row index); they are staged once per CTA as (byte position,
 // value) and shared by all warps. Warp w owns output channel oc0 + w: no two warps write the
 // same word, no atomics, and a fixed order makes the result deterministic.
-template <bool REC_SMEM>
-__global__ void __launch_bounds__(kFwdThreads, 2)
-conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
+// EPI: kEpiSample -- the sampled pass (score histogram only); kEpiCand -- the main pass
+// (candidate runs); kEpiRedo -- the main pass again, for the queued samples only, with every
+// support entry of a failed segment as a candidate.
+constexpr int kEpiSample = 1, kEpiCand = 2, kEpiRedo = 3;
+
+template <bool REC_SMEM, int EPI>
+__device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGeo& kg, const FwdTile& t,
+                                         const FwdArgs& a, int64_t bl, int tin) {
     extern __shared__ __align__(16) float smf[];
     const int c_in = (int)gx.C, c_out = (int)gy.C;
     const int Z = gy.Z, ZR = t.ZR;
-    const int64_t tile = blockIdx.x;                 // (b, x, ty) flattened
-    const int ty = (int)(tile % t.nty);
-    const int x = (int)((tile / t.nty) % gy.X);
-    const int64_t bl = tile / ((int64_t)t.nty * gy.X);   // sample within this pass
+    const int ty = tin % t.nty;
+    const int x = tin / t.nty;
     const int64_t b = a.b0 + bl;                        // global sample (input rows)
     const int oc0 = blockIdx.y * t.ocg;
     const int nocl = min(t.ocg, c_out - oc0);
@@ -373,42 +457,34 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     const bool single = total <= kStageCap;          // the usual case: one chunk, descriptors known
     for (int f0 = 0; f0 < total; f0 += kStageCap) {
         const int f1 = min(total, f0 + kStageCap);
-        // ---- stage the chunk: (byte position in a channel slice, value); one warp per item,
-        // coalesced reads of the item's key run; in the single-chunk case the same warp writes
-        // the item's work descriptors
-        // The warp's items (pk = warp, warp + 8, ...) are one concatenated list of entries; lane
-        // l takes positions l, l + 32, ... in batches of 8, all key / value loads of a batch in
+        // ---- stage the chunk: (byte position in a channel slice, value). The items' key runs
+        // are one concatenated list; thread i takes list positions i, i + 256, ... (item by a
+        // binary search over the item offsets), all key / value loads of a batch of eight in
         // flight before any is used.
         {
-            int wtot = 0;
-            for (int pk = warp; pk < PK; pk += kFwdWarps)
-                wtot += max(0, min(ioff[pk + 1], f1) - max(ioff[pk], f0));
             constexpr int kJ = 8;
-            int cpk = warp, ccum = 0;   // this lane's item cursor: its positions only increase
-            for (int base = 0; base < wtot; base += 32 * kJ) {
+            for (int base = f0 + (int)threadIdx.x; base < f1; base += kFwdThreads * kJ) {
                 uint32_t kw[kJ], rbj[kJ];
                 float vj[kJ];
                 int dj[kJ];
 #pragma unroll
                 for (int j = 0; j < kJ; ++j) {
-                    const int pos = base + 32 * j + lane;
+                    const int pos = base + kFwdThreads * j;
                     dj[j] = -1;
                     kw[j] = 0u;
                     rbj[j] = 0u;
                     vj[j] = 0.0f;
-                    if (pos < wtot) {
-                        for (;; cpk += kFwdWarps) {   // advance to the item holding list position pos
-                            const int len = max(0, min(ioff[cpk + 1], f1) - max(ioff[cpk], f0));
-                            if (pos < ccum + len) break;
-                            ccum += len;
+                    if (pos < f1) {
+                        int lo = 0, hi = PK;   // last item q with ioff[q] <= pos
+                        while (hi - lo > 1) {
+                            const int mid = (lo + hi) >> 1;
+                            if (ioff[mid] <= pos) lo = mid; else hi = mid;
                         }
-                        const int pk = cpk, cum = ccum;
-                        const int f = max(ioff[pk], f0) + (pos - cum);
-                        const uint32_t e = iglob[pk] - (uint32_t)ioff[pk] + (uint32_t)f;
+                        const uint32_t e = iglob[lo] + (uint32_t)(pos - ioff[lo]);
                         kw[j] = xk32[2 * (size_t)e];
                         vj[j] = a.xvals[e];
-                        rbj[j] = ibase[pk];
-                        dj[j] = f - f0;
+                        rbj[j] = ibase[lo];
+                        dj[j] = pos - f0;
                     }
                 }
 #pragma unroll
@@ -422,10 +498,10 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
                 }
             }
         }
-        if (single)
-            for (int pk = warp; pk < PK; pk += kFwdWarps) {
-                const int s0 = max(ioff[pk], f0), s1 = min(ioff[pk + 1], f1);
-                for (int gi = lane; 64 * gi < s1 - s0; gi += 32) {
+        if (single)   // work descriptors of item q by thread q
+            for (int pk = threadIdx.x; pk < PK; pk += kFwdThreads) {
+                const int s0 = ioff[pk], s1 = ioff[pk + 1];
+                for (int gi = 0; 64 * gi < s1 - s0; ++gi) {
                     const int st = s0 + 64 * gi;
                     work[wpre[pk] + gi] = (uint32_t)st | ((uint32_t)min(64, s1 - st) << 12) | ((uint32_t)pk << 19);
                 }
@@ -465,21 +541,49 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     }
 
     // ------------------------------------------------------------------------ epilogue
-    // "get non-zero entries" and "add bias to non-zero entries": the tile's slice
-    // of the pre-attention responses goes to the (b, oc) buffers -- the paper's temporary dense
-    // buffer, absent marker where there is no support -- while the support size and a
-    // histogram of the top score digit are accumulated for the attention threshold.
     const int nyr = ye - y0;
-    const bool do_hist = a.attn != SPC_ATTN_NONE;
+    if (EPI != kEpiSample) {
+        // "get non-zero entries" / "add bias" / candidates for "select k largest"
+        // (P:80): warp w reads only its own channel's slice, so no barrier is needed
+        if (warp >= nocl) return;
+        const int oc = oc0 + warp;
+        const int64_t s = bl * c_out + oc;
+        if (EPI == kEpiRedo && !a.fail[s]) return;
+        const float bv = a.bias ? __ldg(&a.bias[oc]) : 0.0f;
+        const float* S = acc + warp * SL + 2 * kg.hy * ZR + t.cz;
+        const uint32_t tl = EPI == kEpiRedo ? 0u : a.tlow[s];
+        const uint32_t pbase = (uint32_t)(((int64_t)x * gy.Y + y0) * Z);
+        uint32_t* cp = a.cpos + s * gy.V + pbase;
+        float* cv = a.cval + s * gy.V + pbase;
+        uint32_t n, sup, mx;
+        static_assert(kFwdWarps * (kCandBuf + 32) <= kStageCap, "candidate buffers live in the staging area");
+        uint32_t* bp = spos + warp * (kCandBuf + 32);
+        float* bvv = sval + warp * (kCandBuf + 32);
+        if (a.attn == SPC_ATTN_MAGNITUDE)
+            epi_cand<SPC_ATTN_MAGNITUDE>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, bvv, n, sup, mx);
+        else if (a.attn == SPC_ATTN_RAW)
+            epi_cand<SPC_ATTN_RAW>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, bvv, n, sup, mx);
+        else
+            epi_cand<SPC_ATTN_NONE>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, bvv, n, sup, mx);
+        if (lane == 0) {
+            a.tcnt[s * a.ntile + tin] = n;
+            if (n) {
+                atomicAdd(&a.cand_cur[s], (unsigned long long)n);
+                atomicMax(&a.cmax[s], mx);
+            }
+            if (EPI == kEpiCand && sup) atomicAdd(&a.seg_count[s], (unsigned long long)sup);
+        }
+        return;
+    }
+    // sampled pass: the tile's score histogram per output channel, merged into the segment's
+    // (support size = its total). Two histogram buffers alternate between output channels -- A in
+    // the staging area, B in the accumulator slice of the first channel once that is consumed --
+    // so a channel's histogram is flushed while the next channel's rows are being binned.
     constexpr int kHist4 = (kSelBins + 32) / 4;      // bins + one dummy bin per lane
-    // Two histogram buffers alternate between output channels -- A in the staging area, B in the
-    // accumulator slice of the first channel once that is consumed -- so a channel's histogram is
-    // flushed while the next channel's rows are being binned: one barrier per channel.
-    const bool dbuf = do_hist && nocl > 1 && SL >= 4 * kHist4;
+    const bool dbuf = nocl > 1 && SL >= 4 * kHist4;
     uint4* histA = reinterpret_cast<uint4*>(hist);
     uint4* histB = reinterpret_cast<uint4*>(acc);
-    if (do_hist)
-        for (int i = threadIdx.x; i < kHist4; i += blockDim.x) histA[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = threadIdx.x; i < kHist4; i += blockDim.x) histA[i] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
     for (int ocl = 0; ocl < nocl; ++ocl) {
         const int oc = oc0 + ocl;
@@ -488,40 +592,56 @@ conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
         const float* S = acc + ocl * SL + 2 * kg.hy * ZR + t.cz;
         uint4* hist4 = (dbuf && (ocl & 1)) ? histB : histA;
         const uint32_t hist_s = (uint32_t)__cvta_generic_to_shared(hist4);
-        uint32_t cnt = 0;
-        float* P = a.pre + s * gy.V + ((int64_t)x * gy.Y + y0) * Z;
-        if (a.attn == SPC_ATTN_MAGNITUDE)
-            epi_rows<SPC_ATTN_MAGNITUDE>(S, P, bv, nyr, Z, ZR, hist_s, cnt, marker);
-        else if (a.attn == SPC_ATTN_RAW)
-            epi_rows<SPC_ATTN_RAW>(S, P, bv, nyr, Z, ZR, hist_s, cnt, marker);
-        else
-            epi_rows<SPC_ATTN_NONE>(S, P, bv, nyr, Z, ZR, hist_s, cnt, marker);
-        if (do_hist) {   // merge the tile histogram (support size = its total) and clear it
+        if (a.attn == SPC_ATTN_RAW) epi_hist_rows<SPC_ATTN_RAW>(S, bv, nyr, Z, ZR, hist_s, marker);
+        else epi_hist_rows<SPC_ATTN_MAGNITUDE>(S, bv, nyr, Z, ZR, hist_s, marker);
+        __syncthreads();
+        if (dbuf && ocl == 0) {   // slice 0 is consumed: it becomes buffer B
+            for (int i = threadIdx.x; i < kHist4; i += blockDim.x) histB[i] = make_uint4(0u, 0u, 0u, 0u);
             __syncthreads();
-            if (dbuf && ocl == 0) {   // slice 0 is consumed: it becomes buffer B
-                for (int i = threadIdx.x; i < kHist4; i += blockDim.x) histB[i] = make_uint4(0u, 0u, 0u, 0u);
-                __syncthreads();
-            }
-            uint32_t* gh = a.hist + s * kSelBins;
-            for (int i = threadIdx.x; i < kHist4; i += blockDim.x) {
-                const uint4 h = hist4[i];
-                if (h.x | h.y | h.z | h.w) {
-                    hist4[i] = make_uint4(0u, 0u, 0u, 0u);
-                    if (4 * i < kSelBins) {
-                        cnt += h.x + h.y + h.z + h.w;
-                        // two adjacent bins per 64-bit atomic (a bin's total is at most V < 2^32,
-                        // so the low word never carries into the high one)
-                        unsigned long long* g2 = reinterpret_cast<unsigned long long*>(gh + 4 * i);
-                        if (h.x | h.y) atomicAdd(g2, (unsigned long long)h.x | ((unsigned long long)h.y << 32));
-                        if (h.z | h.w) atomicAdd(g2 + 1, (unsigned long long)h.z | ((unsigned long long)h.w << 32));
-                    }
+        }
+        uint32_t* gh = a.hist + s * kSelBins;
+        for (int i = threadIdx.x; i < kHist4; i += blockDim.x) {
+            const uint4 h = hist4[i];
+            if (h.x | h.y | h.z | h.w) {
+                hist4[i] = make_uint4(0u, 0u, 0u, 0u);
+                if (4 * i < kSelBins) {
+                    // two adjacent bins per 64-bit atomic (a bin's total is at most V < 2^32, so
+                    // the low word never carries into the high one)
+                    unsigned long long* g2 = reinterpret_cast<unsigned long long*>(gh + 4 * i);
+                    if (h.x | h.y) atomicAdd(g2, (unsigned long long)h.x | ((unsigned long long)h.y << 32));
+                    if (h.z | h.w) atomicAdd(g2 + 1, (unsigned long long)h.z | ((unsigned long long)h.w << 32));
                 }
             }
         }
-        cnt = warp_sum(cnt);
-        if (lane == 0 && cnt) atomicAdd(&a.seg_count[s], (unsigned long long)cnt);
-        // single buffer: the next channel may bin only after everyone's flush
-        if (do_hist && !dbuf) __syncthreads();
+        if (!dbuf) __syncthreads();   // single buffer: the next channel bins only after the flush
+    }
+}
+
+// One CTA = one tile (b, x, band, output-channel group): main pass (EPI = kEpiCand), grid
+// (B * ntile, n_ocg).
+template <bool REC_SMEM>
+__global__ void __launch_bounds__(kFwdThreads, 2) conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
+    const int64_t tile = blockIdx.x;
+    fwd_tile<REC_SMEM, kEpiCand>(gx, gy, kg, t, a, tile / a.ntile, (int)(tile % a.ntile));
+}
+
+// Sampled pass: grid (B * nsamp, n_ocg); tile j of a segment's sample = j*sp_period + sp_off.
+template <bool REC_SMEM>
+__global__ void __launch_bounds__(kFwdThreads, 2) conv_fwd_sample_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t,
+                                                                         FwdArgs a) {
+    const int64_t j = blockIdx.x;
+    fwd_tile<REC_SMEM, kEpiSample>(gx, gy, kg, t, a, j / a.nsamp, (int)(j % a.nsamp) * a.sp_period + a.sp_off);
+}
+
+// Redo pass: grid (ntile, n_ocg); block t recomputes tile t of every queued sample (normally
+// none: the block exits at once).
+template <bool REC_SMEM>
+__global__ void __launch_bounds__(kFwdThreads, 2) conv_fwd_redo_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t,
+                                                                       FwdArgs a) {
+    const int nq = *a.redo_n;
+    for (int i = 0; i < nq; ++i) {
+        fwd_tile<REC_SMEM, kEpiRedo>(gx, gy, kg, t, a, a.redo_b[i], (int)blockIdx.x);
+        __syncthreads();
     }
 }
 
@@ -922,45 +1042,118 @@ __global__ void __launch_bounds__(32 * kWriteWarps) fwd_write_kernel(FwdArgs a, 
     }
 }
 
+cudaError_t launch_seg_scan_u64(const uint64_t* in, uint64_t* out, int64_t n, int64_t* total, int add_base,
+                                cudaStream_t s) {
+    SPC_PHASE("seg_scan", s, 1);
+    seg_scan_u64_kernel<<<1, 1024, 0, s>>>(in, out, n, total, add_base);
+    return cudaGetLastError();
+}
+
+void plan_fwd_sampling(const Geo& gy, const FwdTile& t, int attn, FwdArgs* a) {
+    a->ntile = (int)(gy.X * t.nty);
+    // every sp_period-th tile of a segment (period prime to the band count, so that the sampled
+    // tiles cycle through the bands); no sampling for small segments or without attention
+    int P = 31;
+    if (t.nty % P == 0) P = 37;
+    a->sp_period = P;
+    a->sp_off = P / 2;
+    a->nsamp = (attn != SPC_ATTN_NONE && a->ntile >= 2 * P) ? (a->ntile - a->sp_off + P - 1) / P : 0;
+}
+
+template <bool REC>
+static cudaError_t set_fwd_smem(size_t smem) {
+    cudaError_t e = cudaFuncSetAttribute(conv_fwd_kernel<REC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(conv_fwd_sample_kernel<REC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(conv_fwd_redo_kernel<REC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return e;
+}
+
+template <bool REC>
+static void launch_fwd_passes(const Geo& gx, const Geo& gy, const KGeo& kg, const FwdTile& t, const FwdArgs& a,
+                              int which, cudaStream_t s) {
+    if (which == 0) {
+        const dim3 grid((unsigned)(gy.B * a.nsamp), (unsigned)t.n_ocg);
+        SPC_PHASE("conv_fwd_sample", s, 1);
+        conv_fwd_sample_kernel<REC><<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a);
+    } else if (which == 1) {
+        const dim3 grid((unsigned)(gy.B * a.ntile), (unsigned)t.n_ocg);
+        SPC_PHASE("conv_fwd", s, 1);
+        conv_fwd_kernel<REC><<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a);
+    } else {
+        const dim3 grid((unsigned)a.ntile, (unsigned)t.n_ocg);
+        SPC_PHASE("conv_fwd_redo", s, 1);
+        conv_fwd_redo_kernel<REC><<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a);
+    }
+}
+
+cudaError_t launch_conv_fwd_stream(const Geo& gx, const Geo& gy, const KGeo& kg, const FwdTile& t,
+                                   const FwdArgs& a, cudaStream_t s) {
+    const int64_t nseg = gy.B * gy.C;
+    if (nseg == 0) return a.out_append ? cudaSuccess : cudaMemsetAsync(a.out_nnz, 0, sizeof(int64_t), s);
+    cudaError_t e = t.rec_smem ? set_fwd_smem<true>(t.smem) : set_fwd_smem<false>(t.smem);
+    if (e != cudaSuccess) return e;
+    const size_t segb = sizeof(uint64_t) * (size_t)nseg;
+    cudaMemsetAsync(a.seg_count, 0, segb, s);
+    cudaMemsetAsync(a.cand_cur, 0, segb, s);
+    cudaMemsetAsync(a.cmax, 0, sizeof(uint32_t) * (size_t)nseg, s);
+    cudaMemsetAsync(a.fail, 0, sizeof(int) * (size_t)nseg, s);
+    cudaMemsetAsync(a.bflag, 0, sizeof(int) * (size_t)gy.B, s);
+    cudaMemsetAsync(a.redo_n, 0, sizeof(int), s);
+    cudaMemsetAsync(a.tile_sel, 0, sizeof(uint32_t) * (size_t)(nseg * a.ntile), s);
+    if (!a.out_append) {   // later passes of sparse_conv_fwd_pass reuse the guard and the rounds
+        if (!a.guard_done) {
+            cudaMemsetAsync(a.guard, 0, sizeof(int), s);
+            SPC_PHASE("value_guard", s, 1);
+            value_guard_kernel<<<148 * 4, 256, 0, s>>>(a.xvals, a.x_nnz_dev, a.x_nnz, a.guard);
+        }
+        SPC_PHASE("fwd_rounds", s, 1);
+        fwd_rounds_kernel<<<(unsigned)t.n_ocg, 256, 0, s>>>(kg, (int)gx.C, (int)gy.C, t, a.meta2, a.val2, a.off2,
+                                                          a.rnd, a.roff, a.guard);
+    }
+    auto passes = [&](int which) {
+        if (t.rec_smem) launch_fwd_passes<true>(gx, gy, kg, t, a, which, s);
+        else launch_fwd_passes<false>(gx, gy, kg, t, a, which, s);
+    };
+    if (a.nsamp > 0) {
+        cudaMemsetAsync(a.hist, 0, sizeof(uint32_t) * kSelBins * (size_t)nseg, s);
+        passes(0);
+        e = launch_stream_find(a, s);
+        if (e != cudaSuccess) return e;
+    } else {
+        cudaMemsetAsync(a.tlow, 0, sizeof(uint32_t) * (size_t)nseg, s);
+    }
+    // test hook: a threshold above every score, so that every non-empty segment takes the redo
+    // path (tests/test_parity_gpu.py::test_fwd_forced_redo)
+    if (const char* f = getenv("SPC_FWD_FORCE_REDO"))
+        if (f[0] == '1') cudaMemsetAsync(a.tlow, 0xff, sizeof(uint32_t) * (size_t)nseg, s);
+    passes(1);
+    e = launch_stream_resolve(gy, t, a, 0, s);
+    if (e != cudaSuccess) return e;
+    passes(2);
+    e = launch_stream_resolve(gy, t, a, 1, s);
+    if (e != cudaSuccess) return e;
+    e = launch_stream_tail(gy, t, a, s);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& kg, const FwdTile& t,
                                      const FwdArgs& a, cudaStream_t s, const GemmPlan* gp, const GemmArgs* ga) {
     const int64_t nseg = gy.B * gy.C;
     if (nseg == 0) return a.out_append ? cudaSuccess : cudaMemsetAsync(a.out_nnz, 0, sizeof(int64_t), s);
-    if (!gp) {
-        cudaError_t e = t.rec_smem
-            ? cudaFuncSetAttribute(conv_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem)
-            : cudaFuncSetAttribute(conv_fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem);
-        if (e != cudaSuccess) return e;
-    }
+    if (!gp || !ga) return cudaErrorInvalidValue;   // variant S runs launch_conv_fwd_stream
     const size_t segb = sizeof(uint64_t) * (size_t)nseg;
     cudaMemsetAsync(a.seg_count, 0, segb, s);
     cudaMemsetAsync(a.cand_cur, 0, segb, s);
     cudaMemsetAsync(a.stg_cur, 0, segb, s);
     cudaMemsetAsync(a.tile_sel, 0, sizeof(uint32_t) * (size_t)(nseg * a.nchunk), s);
     if (a.attn != SPC_ATTN_NONE) cudaMemsetAsync(a.hist, 0, sizeof(uint32_t) * kSelBins * (size_t)nseg, s);
-    const dim3 grid((unsigned)(gy.B * gy.X * t.nty), (unsigned)t.n_ocg);
     const unsigned sgrid = (unsigned)(nseg * a.nchunk);
-    if (gp) {
+    {
         cudaError_t eg = launch_conv_gemm(gx, gy, kg, *gp, *ga, a, s);
         if (eg != cudaSuccess) return eg;
-    } else {
-        if (!a.out_append) {   // later passes of sparse_conv_fwd_pass reuse the guard and the rounds
-            if (!a.guard_done) {
-                cudaMemsetAsync(a.guard, 0, sizeof(int), s);
-                SPC_PHASE("value_guard", s, 1);
-                value_guard_kernel<<<148 * 4, 256, 0, s>>>(a.xvals, a.x_nnz_dev, a.x_nnz, a.guard);
-            }
-            {
-                SPC_PHASE("fwd_rounds", s, 1);
-                fwd_rounds_kernel<<<(unsigned)t.n_ocg, 256, 0, s>>>(kg, (int)gx.C, (int)gy.C, t, a.meta2, a.val2,
-                                                                  a.off2, a.rnd, a.roff, a.guard);
-            }
-        }
-        {
-            SPC_PHASE("conv_fwd", s, 1);
-            if (t.rec_smem) conv_fwd_kernel<true><<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a);
-            else conv_fwd_kernel<false><<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a);
-        }
     }
     { SPC_PHASE("fwd_find", s, 1); fwd_find_kernel<<<(unsigned)nseg, 256, 0, s>>>(a, nseg); }
     {

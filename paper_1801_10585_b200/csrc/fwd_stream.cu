@@ -1,0 +1,411 @@
+// Streamed forward (variant S): the per-segment stages around the convolution passes of
+// conv_fwd.cu. Alg. 1 keeps one dense buffer per (b, oc) and selects the k largest responses
+// from it ("select k largest responses" P:80, Alabi et al. P:104). Here the dense
+// responses never reach HBM:
+//   sampled pass (conv_fwd_sample_kernel): score histograms of every sp_period-th tile;
+//   find (this file):      per segment a threshold tlow whose estimated rank is a little above k;
+//   main pass (conv_fwd_kernel): every support entry with score >= tlow ("candidates") is
+//                          appended in key order to its tile's run;
+//   resolve (this file):   the exact k-th largest composite key (score, ~p) among the candidates
+//                          (reading R7: ties -> smaller key); a segment whose candidates cannot
+//                          contain it (the sample missed) is queued for the redo pass, which
+//                          recomputes its tiles with every support entry as a candidate;
+//   tile scan + write:     ordered compaction of the kept candidates ("compress ids ...
+//                          write").
+// The result is exactly the selection of the dense-buffer algorithm: the candidates are a
+// superset of the kept set whenever resolve accepts them.
+#include "spc_internal.cuh"
+#include "block_scan.cuh"
+
+#include <cmath>
+
+namespace spc {
+
+__device__ __forceinline__ uint64_t comp_key(uint32_t sc, uint32_t p) {
+    return ((uint64_t)sc << 32) | (uint64_t)(0xffffffffu - p);
+}
+
+// first voxel (within the segment) of tile t = x*nty + ty
+__device__ __forceinline__ uint32_t tile_base(int t, int nty, int TY, int Y, int Z) {
+    const int x = t / nty, ty = t - x * nty;
+    return (uint32_t)(((int64_t)x * Y + (int64_t)ty * TY) * Z);
+}
+
+struct StreamGeo {
+    int nty, TY, Y, Z;
+    int64_t V;
+};
+
+// ------------------------------------------------------------------------------------ find
+// tlow from the sampled histogram (bins = score >> 21). The sampled tiles are a fraction f of
+// the segment; the threshold is placed where the sampled count above it reaches
+// want = 1.08 k f + 4 sqrt(k f) + 8 (binomial margin of several sigma), interpolating inside the
+// crossing bin. Segments whose estimated support is close to k (or whose sample is too small)
+// take every support entry as a candidate (tlow = 0).
+__global__ void stream_find_kernel(FwdArgs a, double f) {
+    const int64_t s = blockIdx.x;
+    __shared__ uint64_t sm[33];
+    const uint32_t* h = a.hist + s * kSelBins;
+    constexpr int per = kSelBins / 256;
+    uint64_t local = 0;
+    for (int q = 0; q < per; ++q) local += h[kSelBins - 1 - threadIdx.x * per - q];
+    uint64_t tot;
+    const uint64_t before = block_excl_scan(local, sm, &tot);
+    const double k = (double)a.k;
+    const double r = k * f;
+    const double want = 1.08 * r + 4.0 * sqrt(r) + 8.0;
+    const bool all = tot == 0 || (double)tot / f <= 1.1 * k + 64.0 || (double)tot < want;
+    if (all) {
+        if (threadIdx.x == 0) a.tlow[s] = 0u;
+        return;
+    }
+    if ((double)before < want && (double)(before + local) >= want) {
+        double cum = (double)before;
+        for (int q = 0; q < per; ++q) {
+            const int bin = kSelBins - 1 - threadIdx.x * per - q;
+            const double hb = (double)h[bin];
+            if (cum + hb >= want) {
+                const double frac = (want - cum) / hb;   // share of the bin needed, from its top
+                const double off = (1.0 - frac) * (double)(1u << 21);
+                a.tlow[s] = ((uint32_t)bin << 21) + (uint32_t)fmax(0.0, floor(off));
+                return;
+            }
+            cum += hb;
+        }
+    }
+}
+
+// --------------------------------------------------------------------------------- resolve
+constexpr int kSRThreads = 512;
+constexpr int kSRWarps = kSRThreads / 32;
+constexpr int kSRCap = 4096;   // candidates of the threshold bucket collected in shared memory
+
+// Visit every candidate of segment s: f(t, i, value bits, global index); one warp per tile run,
+// the runs' lengths loaded 32 at a time, four entries per lane in flight.
+template <typename F>
+__device__ __forceinline__ void for_candidates(const FwdArgs& a, int64_t s, F f) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t* tc = a.tcnt + s * a.ntile;
+    for (int t0 = warp * 32; t0 < a.ntile; t0 += kSRWarps * 32) {
+        const uint32_t mycnt = t0 + lane < a.ntile ? tc[t0 + lane] : 0u;
+        unsigned any = __ballot_sync(kFull, mycnt != 0u);
+        while (any) {
+            const int j = __ffs(any) - 1;
+            any &= any - 1;
+            const int t = t0 + j;
+            const uint32_t n = __shfl_sync(kFull, mycnt, j);
+            f.run(t, n);
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t tile_of(uint32_t p, const StreamGeo& g) {
+    const uint32_t yz = (uint32_t)g.Y * (uint32_t)g.Z;
+    const uint32_t x = p / yz;
+    const uint32_t y = (p - x * yz) / (uint32_t)g.Z;
+    return x * (uint32_t)g.nty + y / (uint32_t)g.TY;
+}
+
+// need-th largest (1-based) of n distinct u64 keys in shared memory: radix select with 8-bit
+// digits from the top (all threads of the block call it)
+__device__ uint64_t smem_select(const uint64_t* keys, uint32_t n, uint32_t need, uint32_t* h256, uint64_t* sh) {
+    uint64_t prefix = 0, mask = 0;
+    for (int pass = 0; pass < 8; ++pass) {
+        const int shf = 56 - 8 * pass;
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) h256[i] = 0;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+            const uint64_t k = keys[i];
+            if ((k & mask) == prefix) atomicAdd(&h256[(uint32_t)(k >> shf) & 255u], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t cum = 0;
+            int bin = 255;
+            for (; bin > 0; --bin) {
+                if (cum + h256[bin] >= need) break;
+                cum += h256[bin];
+            }
+            sh[0] = prefix | ((uint64_t)bin << shf);
+            sh[1] = (uint64_t)(need - cum);
+        }
+        __syncthreads();
+        prefix = sh[0];
+        need = (uint32_t)sh[1];
+        mask |= 255ull << shf;
+        __syncthreads();
+    }
+    return prefix;
+}
+
+// pass 0: every segment; pass 1: only segments the redo pass recomputed
+__global__ void __launch_bounds__(kSRThreads) stream_resolve_kernel(FwdArgs a, StreamGeo g, int pass) {
+    const int64_t s = blockIdx.x;
+    if (pass == 1 && !a.fail[s]) return;
+    const uint64_t n = a.cand_cur[s];
+    const uint64_t sup = a.seg_count[s];
+    const uint64_t k = (uint64_t)a.k;
+    const bool keep_all = a.attn == SPC_ATTN_NONE || sup <= k;
+    const bool fail = keep_all ? (n != sup) : (n < k);
+    if (fail) {
+        if (pass == 0 && threadIdx.x == 0) {
+            // the sampled threshold was too high: recompute this segment with tlow = 0
+            a.fail[s] = 1;
+            a.cand_cur[s] = 0;
+            a.cmax[s] = 0;
+            const int b = (int)(s / (int64_t)a.seg_stride);
+            if (atomicExch(&a.bflag[b], 1) == 0) a.redo_b[atomicAdd(a.redo_n, 1)] = b;
+        }
+        return;   // (pass 1 cannot fail: with tlow = 0 the candidates are the whole support)
+    }
+    if (keep_all) {
+        if (threadIdx.x == 0) {
+            FwdSeg st{};
+            st.keep_all = 1;
+            a.seg[s] = st;
+        }
+        return;
+    }
+    __shared__ uint32_t h[kSelBins];
+    __shared__ uint64_t keys[kSRCap];
+    __shared__ uint64_t sh[4];
+    __shared__ uint32_t sh_n;
+    const uint32_t tl = a.tlow[s];
+    const uint32_t mxr = a.cmax[s] - tl;
+    const int sh1 = max(0, 32 - __clz(mxr) - 11);   // (score - tl) >> sh1 < 2048
+    const int attn = a.attn;
+    const float* cval = a.cval + s * g.V;
+    const uint32_t* cpos = a.cpos + s * g.V;
+    const int lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) h[i] = 0;
+    if (threadIdx.x == 0) sh_n = 0;
+    __syncthreads();
+    // ---- histogram of the candidates' score digit
+    struct HistF {
+        const float* cv; uint32_t* h; uint32_t tl; int sh1, attn, lane; const StreamGeo* g;
+        __device__ void run(int t, uint32_t n) const {
+            const float* v = cv + tile_base(t, g->nty, g->TY, g->Y, g->Z);
+            for (uint32_t i0 = lane; i0 < n; i0 += 128) {   // four loads in flight per lane
+                uint32_t vb[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) vb[q] = i0 + 32u * q < n ? __float_as_uint(v[i0 + 32u * q]) : 0u;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (i0 + 32u * q < n) atomicAdd(&h[(score_bits(vb[q], attn) - tl) >> sh1], 1u);
+            }
+        }
+    } hf{cval, h, tl, sh1, attn, lane, &g};
+    for_candidates(a, s, hf);
+    __syncthreads();
+    // ---- bucket of the k-th from the top
+    if (threadIdx.x < 32) {
+        constexpr int per = kSelBins / 32;
+        uint32_t own = 0;
+        for (int q = 0; q < per; ++q) own += h[kSelBins - 1 - per * lane - q];
+        const uint32_t incl = warp_incl_scan(own);
+        const uint64_t before = incl - own;
+        if (own && before < k && before + own >= k) {
+            uint64_t cum = before;
+            for (int q = 0; q < per; ++q) {
+                const int bin = kSelBins - 1 - per * lane - q;
+                if (cum + h[bin] >= k) {
+                    sh[0] = (uint64_t)bin;
+                    sh[1] = k - cum;       // need within the bucket
+                    sh[2] = h[bin];
+                    break;
+                }
+                cum += h[bin];
+            }
+        }
+    }
+    __syncthreads();
+    const uint32_t B = (uint32_t)sh[0];
+    uint64_t need = sh[1];
+    uint64_t bcnt = sh[2];
+    // Within the bucket, the order is that of K' = ((score - lo) << 32) | ~p (lo = the bucket's
+    // lowest score): a key of W = sh1 + 32 bits. Narrow it with 11-bit digits over the HBM list
+    // until the survivors fit shared memory (usually no narrowing at all).
+    const uint32_t lo = tl + (B << sh1);
+    uint64_t pre = 0;   // survivors: (K' >> pos) == pre
+    int pos = sh1 + 32;
+    auto kprime = [&](uint32_t sc, uint32_t p) -> uint64_t {
+        return ((uint64_t)(sc - lo) << 32) | (uint64_t)(0xffffffffu - p);
+    };
+    while (bcnt > (uint64_t)kSRCap) {
+        const int d = min(11, pos);
+        pos -= d;
+        const uint32_t nb = 1u << d;
+        for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) h[i] = 0;
+        __syncthreads();
+        struct NarrowF {
+            const float* cv; const uint32_t* cp; uint32_t* h; uint32_t tl, lo; uint32_t B; int sh1, attn, lane, pos, d;
+            uint64_t pre; const StreamGeo* g;
+            __device__ void run(int t, uint32_t n) const {
+                const uint32_t b0 = tile_base(t, g->nty, g->TY, g->Y, g->Z);
+                for (uint32_t i = lane; i < n; i += 32) {
+                    const uint32_t sc = score_bits(__float_as_uint(cv[b0 + i]), attn);
+                    if (((sc - tl) >> sh1) != B) continue;
+                    const uint64_t kp = ((uint64_t)(sc - lo) << 32) | (uint64_t)(0xffffffffu - cp[b0 + i]);
+                    if ((kp >> (pos + d)) == pre) atomicAdd(&h[(uint32_t)(kp >> pos) & ((1u << d) - 1u)], 1u);
+                }
+            }
+        } nf{cval, cpos, h, tl, lo, B, sh1, attn, lane, pos, d, pre, &g};
+        for_candidates(a, s, nf);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t cum = 0;
+            int bin = (int)nb - 1;
+            for (; bin > 0; --bin) {
+                if (cum + h[bin] >= need) break;
+                cum += h[bin];
+            }
+            sh[0] = (pre << d) | (uint64_t)bin;
+            sh[1] = need - cum;
+            sh[2] = h[bin];
+        }
+        __syncthreads();
+        pre = sh[0];
+        need = sh[1];
+        bcnt = sh[2];
+        __syncthreads();
+    }
+    // ---- collect the survivors; per tile run count the entries ranked above them ("definite")
+    struct CollectF {
+        const float* cv; const uint32_t* cp; uint64_t* keys; uint32_t* sh_n; uint32_t* tdef;
+        uint32_t tl, lo, B; int sh1, attn, lane, pos; uint64_t pre; const StreamGeo* g;
+        __device__ void run(int t, uint32_t n) const {
+            const uint32_t b0 = tile_base(t, g->nty, g->TY, g->Y, g->Z);
+            uint32_t def = 0;
+            for (uint32_t i0 = lane; i0 < n; i0 += 128) {   // four loads in flight per lane
+                uint32_t vb[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) vb[q] = i0 + 32u * q < n ? __float_as_uint(cv[b0 + i0 + 32u * q]) : 0u;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t i = i0 + 32u * q;
+                    if (i >= n) continue;
+                    const uint32_t sc = score_bits(vb[q], attn);
+                    const uint32_t dg = (sc - tl) >> sh1;
+                    if (dg > B) { ++def; continue; }
+                    if (dg < B) continue;
+                    const uint32_t p = cp[b0 + i];
+                    const uint64_t kp = ((uint64_t)(sc - lo) << 32) | (uint64_t)(0xffffffffu - p);
+                    const uint64_t top = kp >> pos;
+                    if (top > pre) ++def;
+                    else if (top == pre) keys[atomicAdd(sh_n, 1u)] = kp;
+                }
+            }
+            def = warp_sum(def);
+            if (lane == 0) tdef[t] = def;
+        }
+    } cf{cval, cpos, keys, &sh_n, a.tile_def + s * a.ntile, tl, lo, B, sh1, attn, lane, pos, pre, &g};
+    // runs without candidates keep tile_def = 0 (zeroed with tile_sel before the pass)
+    for_candidates(a, s, cf);
+    __syncthreads();
+    const uint32_t ns = sh_n;
+    const uint64_t kps = smem_select(keys, ns, (uint32_t)need, h, sh);
+    // kept iff K' >= kps among the survivors; per tile run the selected survivors
+    uint32_t* tsel = a.tile_sel + s * a.ntile;
+    for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) {
+        const uint64_t kp = keys[i];
+        if (kp >= kps) atomicAdd(&tsel[tile_of(0xffffffffu - (uint32_t)kp, g)], 1u);
+    }
+    if (threadIdx.x == 0) {
+        FwdSeg st{};
+        st.keep_all = 0;
+        st.kstar = ((uint64_t)(lo + (uint32_t)(kps >> 32)) << 32) | (kps & 0xffffffffull);
+        a.seg[s] = st;
+    }
+}
+
+// ------------------------------------------------------------------------- tile scan / write
+// per segment: kept entries per tile run -> exclusive offsets; segment total -> kept[s]
+__global__ void stream_tile_scan_kernel(FwdArgs a, uint64_t* kept) {
+    const int64_t s = blockIdx.x;
+    __shared__ uint64_t sm[33];
+    const bool all = a.seg[s].keep_all != 0;
+    uint64_t carry = 0;
+    for (int64_t base = 0; base < a.ntile; base += blockDim.x) {
+        const int64_t t = base + threadIdx.x;
+        uint64_t v = 0;
+        if (t < a.ntile) {
+            const int64_t it = s * a.ntile + t;
+            const uint32_t c = a.tcnt[it];
+            v = (all || c == 0) ? (uint64_t)c : (uint64_t)a.tile_def[it] + a.tile_sel[it];
+        }
+        uint64_t tot;
+        const uint64_t ex = block_excl_scan(v, sm, &tot);
+        if (t < a.ntile) a.tile_off[s * a.ntile + t] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) kept[s] = carry;
+}
+
+// one warp per tile run: keep iff composite(score, p) >= kstar (every candidate when keep-all),
+// ordered compaction ("compress ids from kD to 1D, write as sparse output")
+constexpr int kSWWarps = 8;
+__global__ void __launch_bounds__(32 * kSWWarps) stream_write_kernel(FwdArgs a, StreamGeo g) {
+    const int lane = threadIdx.x & 31;
+    const int64_t it = (int64_t)blockIdx.x * kSWWarps + (threadIdx.x >> 5);
+    if (it >= a.nseg * a.ntile) return;
+    const uint32_t n = a.tcnt[it];
+    if (n == 0) return;
+    const int64_t s = it / a.ntile;
+    const int t = (int)(it - s * a.ntile);
+    const FwdSeg st = a.seg[s];
+    const uint32_t b0 = tile_base(t, g.nty, g.TY, g.Y, g.Z);
+    const uint32_t* ip = a.cpos + s * g.V + b0;
+    const float* iv = a.cval + s * g.V + b0;
+    uint64_t out = a.seg_off[s] + a.tile_off[it];
+    const uint64_t kb = ((uint64_t)a.seg0 + (uint64_t)s) * (uint64_t)g.V;
+    const uint32_t ks = (uint32_t)(st.kstar >> 32), kp = (uint32_t)st.kstar;
+    for (uint32_t i0 = 0; i0 < n; i0 += 128) {   // four groups of 32 loaded before any is used
+        uint32_t pp[4], vb[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t i = i0 + 32u * q + lane;
+            pp[q] = i < n ? ip[i] : 0u;
+            vb[q] = i < n ? __float_as_uint(iv[i]) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const bool ok = i0 + 32u * q + lane < n;
+            const uint32_t sc = score_bits(vb[q], a.attn);
+            const bool keep = ok && (st.keep_all || sc > ks || (sc == ks && 0xffffffffu - pp[q] >= kp));
+            const unsigned m = __ballot_sync(kFull, keep);
+            if (keep) {
+                const uint64_t o = out + __popc(m & ((1u << lane) - 1u));
+                a.out_keys[o] = kb + pp[q];
+                a.out_vals[o] = __uint_as_float(vb[q]);
+            }
+            out += __popc(m);
+        }
+    }
+}
+
+cudaError_t launch_stream_find(const FwdArgs& a, cudaStream_t s) {
+    const double f = (double)a.nsamp / (double)a.ntile;
+    SPC_PHASE("fwd_find", s, 1);
+    stream_find_kernel<<<(unsigned)a.nseg, 256, 0, s>>>(a, f);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stream_resolve(const Geo& gy, const FwdTile& t, const FwdArgs& a, int pass, cudaStream_t s) {
+    const StreamGeo g{t.nty, t.TY, gy.Y, gy.Z, gy.V};
+    SPC_PHASE(pass == 0 ? "fwd_resolve" : "fwd_resolve_redo", s, 1);
+    stream_resolve_kernel<<<(unsigned)a.nseg, kSRThreads, 0, s>>>(a, g, pass);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stream_tail(const Geo& gy, const FwdTile& t, const FwdArgs& a, cudaStream_t s) {
+    const StreamGeo g{t.nty, t.TY, gy.Y, gy.Z, gy.V};
+    { SPC_PHASE("fwd_tile_scan", s, 1); stream_tile_scan_kernel<<<(unsigned)a.nseg, 256, 0, s>>>(a, a.cand_cnt); }
+    cudaError_t e = launch_seg_scan_u64(a.cand_cnt, a.seg_off, a.nseg, a.out_nnz, a.out_append, s);
+    if (e != cudaSuccess) return e;
+    const int64_t runs = a.nseg * a.ntile;
+    SPC_PHASE("fwd_write", s, 1);
+    stream_write_kernel<<<(unsigned)((runs + kSWWarps - 1) / kSWWarps), 32 * kSWWarps, 0, s>>>(a, g);
+    return cudaGetLastError();
+}
+
+}  // namespace spc

@@ -13,9 +13,10 @@
 
 namespace spc {
 
-// Absent marker for the dense pre-attention buffer: a NaN pattern. Finite inputs never
-// produce it (NaN/Inf inputs are outside the contract).
-constexpr uint32_t kAbsent = 0x7fffffffu;
+// Absent marker of the pre-attention accumulators: a signalling-NaN pattern. GPU arithmetic
+// only ever produces the canonical quiet NaN 0x7fffffff, so a NaN that arises from the data
+// (NaN/Inf inputs, inf - inf) stays a value and propagates instead of being read as "absent".
+constexpr uint32_t kAbsent = 0x7fbfffffu;
 constexpr uint32_t kNegZero = 0x80000000u;   // accumulator marker of the -0 mode (conv_fwd)
 
 // Geometry of a feature map with its spatial dims padded to rank 3 (leading 1s):
@@ -174,6 +175,25 @@ struct FwdArgs {
     int64_t b0, seg0;
     int out_append;
     int guard_done;   // the value guard ran with the row index (launch_row_index with vals)
+    // ---- streamed forward (variant S, launch_conv_fwd_stream): the pre-attention responses
+    // never leave the SM. A sampled pass estimates a per-segment score threshold tlow; the main
+    // pass appends every support entry with score >= tlow (the candidates, a superset of the k
+    // kept ones) to the segment's run for the tile, in key order; an exact selection over the
+    // candidates and an ordered write follow. Tile t of a segment = x*nty + ty; its run starts at
+    // the tile's first voxel (x*Y + ty*TY)*Z of the segment's candidate region (it holds at most
+    // the tile's voxels).
+    int ntile;                       // tiles per segment (X * nty)
+    int nsamp, sp_period, sp_off;    // sampled tiles per segment: t = j*sp_period + sp_off
+    uint32_t* tlow;                  // [nseg] candidate score threshold (0: every support entry)
+    uint32_t* cmax;                  // [nseg] largest candidate score
+    uint32_t* cpos;                  // [nseg * V] candidate spatial index p
+    float* cval;                     // [nseg * V] candidate value (bias added)
+    uint32_t* tcnt;                  // [nseg * ntile] candidates of each tile run
+    int* fail;                       // [nseg] 1: the candidates missed the k-th score (redo pass)
+    int* bflag;                      // [B] sample queued for the redo pass
+    int* redo_b;                     // [B] queued samples
+    int* redo_n;                     // number of queued samples
+    int seg_stride;                  // c_out (segment s belongs to sample s / c_out of the pass)
 };
 // Variant G of the forward accumulate (conv_gemm.cu): tcgen05 TF32 (3xTF32) implicit GEMM over
 // filter offsets, writing the same dense pre-attention buffer as the scatter kernel.
@@ -212,8 +232,24 @@ GemmPlan plan_gemm(const Geo& gx, const Geo& gy, const KGeo& kg);
 cudaError_t launch_conv_gemm(const Geo& gx, const Geo& gy, const KGeo& kg, const GemmPlan& g, const GemmArgs& ga,
                              const FwdArgs& a, cudaStream_t s);
 
-// Forward pipeline: the accumulate stage (scatter variant S, or variant G when `gemm` is given)
-// followed by the shared attention/selection stage.
+// Streamed forward (variant S, no dense buffer): sampled threshold pass, candidate pass, exact
+// selection over the candidates (with a redo pass for segments whose sample missed), ordered
+// write. FwdArgs' streamed fields must be carved (a.pre / stg / cand are unused).
+cudaError_t launch_conv_fwd_stream(const Geo& gx, const Geo& gy, const KGeo& kg, const FwdTile& t,
+                                   const FwdArgs& a, cudaStream_t s);
+// sampling plan of the streamed forward (sets a->ntile / nsamp / sp_period / sp_off)
+void plan_fwd_sampling(const Geo& gy, const FwdTile& t, int attn, FwdArgs* a);
+// per-segment stages of the streamed forward (fwd_stream.cu)
+cudaError_t launch_stream_find(const FwdArgs& a, cudaStream_t s);
+cudaError_t launch_stream_resolve(const Geo& gy, const FwdTile& t, const FwdArgs& a, int pass, cudaStream_t s);
+cudaError_t launch_stream_tail(const Geo& gy, const FwdTile& t, const FwdArgs& a, cudaStream_t s);
+// exclusive scan of a per-segment u64 array (one block); total -> *total; add_base: start at
+// *total (appending passes of the batch-sliced forward)
+cudaError_t launch_seg_scan_u64(const uint64_t* in, uint64_t* out, int64_t n, int64_t* total, int add_base,
+                                cudaStream_t s);
+
+// Dense-buffer pipeline (variant G): the accumulate stage writes the dense pre-attention buffer
+// that the classify / resolve / write stages read.
 cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& kg, const FwdTile& t,
                                      const FwdArgs& a, cudaStream_t s, const GemmPlan* gp = nullptr,
                                      const GemmArgs* ga = nullptr);

@@ -208,6 +208,56 @@ def test_fwd_binary_surface_ties(cuda_lib):
         np.testing.assert_array_equal(gv, ov)
 
 
+# Segments large enough for the streamed forward's sampled threshold (>= 34 tiles per segment):
+# the candidates (score >= the sampled tlow) must contain the exact top-k; ragged Z (not a
+# multiple of 4) takes the scalar epilogue; 12 output channels = two channel groups.
+SAMPLED_CASES = [
+    ("3d_sampled", (40, 96, 64), 1, 4, 4, (3, 3, 3), 0.03, 0.5),
+    ("3d_sampled_ragged_z", (45, 70, 37), 1, 3, 8, (3, 3, 3), 0.04, 0.5),
+    ("3d_sampled_two_groups", (36, 64, 32), 2, 3, 12, (3, 3, 3), 0.05, 0.5),
+]
+
+
+@pytest.mark.parametrize("case", SAMPLED_CASES, ids=lambda c: c[0])
+@pytest.mark.parametrize("attn", ["magnitude", "raw"])
+@pytest.mark.parametrize("values", ["dyadic", "continuous"])
+def test_fwd_sampled_threshold(cuda_lib, case, attn, values):
+    spc = cuda_lib
+    _, dims, B, ci, co, ks, rd, rf = case
+    x = uniform_map(B, ci, dims, rd, 4100, values=values)
+    w = sparse_filter(ci, co, ks, rf, 4101, values=values)
+    bias = bias_vector(co, 4102, values=values)
+    V = int(np.prod(dims))
+    k = V // 20
+    ok_, ov, _, _ = ora.conv_fwd(x, w, bias, attn=ATTN_ORA[attn], k=k)
+    gk, gv, _ = run_fwd(spc, x, w, bias, attn, k)
+    if values == "dyadic":
+        np.testing.assert_array_equal(gk, ok_)
+        np.testing.assert_array_equal(gv, ov)
+    else:
+        fk, fv, fa, _ = ora.conv_fwd(x, w, bias, with_abs=True)
+        assert_topk_sets_match(gk, gv, ok_, ov, fk, fv, fa, V, k, attn)
+
+
+@pytest.mark.parametrize("attn", ["magnitude", "raw", "none"])
+def test_fwd_forced_redo(cuda_lib, monkeypatch, attn):
+    """Every segment's sampled threshold forced above all scores (SPC_FWD_FORCE_REDO=1): the
+    resolve stage must detect that the candidates miss the k-th response and the redo pass must
+    recompute those segments with every support entry as a candidate -- same exact result."""
+    spc = cuda_lib
+    monkeypatch.setenv("SPC_FWD_FORCE_REDO", "1")
+    for dims, B, ci, co in [((40, 96, 64), 2, 3, 4), ((9, 7, 11), 3, 2, 5), ((28, 28), 4, 1, 8)]:
+        x = uniform_map(B, ci, dims, 0.05, 4200, values="dyadic")
+        w = sparse_filter(ci, co, (3,) * len(dims), 0.6, 4201, values="dyadic")
+        bias = bias_vector(co, 4202, values="dyadic")
+        V = int(np.prod(dims))
+        k = max(1, V // 20)
+        ok_, ov, _, _ = ora.conv_fwd(x, w, bias, attn=ATTN_ORA[attn], k=k)
+        gk, gv, _ = run_fwd(spc, x, w, bias, attn, k)
+        np.testing.assert_array_equal(gk, ok_)
+        np.testing.assert_array_equal(gv, ov)
+
+
 def test_fwd_empty_and_degenerate(cuda_lib):
     spc = cuda_lib
     x = COO(2, 2, (5, 6), np.zeros(0, np.uint64), np.zeros(0, np.float32))
