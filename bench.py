@@ -4,15 +4,19 @@
 Workload (N=1): 3D 128^3 grid, batch 64, 8 -> 8 channels, 3x3x3 filters pruned to 50%
 (rho_f = 0.5), input density rho_d per (b, c) (default 2%; --density), attention with
 rho_up = 5% (k = floor(0.05 * 128^3) = 104857 per (b, oc), magnitude variant). One step =
-sparse_conv_fwd (Alg. 1 with attention) + sparse_conv_bwd (Alg. 2: dx, dw, dbias) [+ NCCL
-all-reduce of dw||dbias when N > 1]. With N GPUs the global batch of 64 is sharded (strong
-scaling, BASELINE "batch 64 sharded on 1/2/4/8 GPUs").
+sparse_conv_fwd (Alg. 1 with attention) + sparse_conv_bwd_f64 (Alg. 2: dx and the fp64 dw /
+dbias partials) + the SUM all-reduce of dw||dbias across ranks (NCCL, N > 1) and its single
+rounding. The all-reduce of step i runs on a side stream and overlaps step i+1's forward (its
+rounding is enqueued after that forward). With N GPUs the global batch of 64 is sharded
+(strong scaling, BASELINE "batch 64 sharded on 1/2/4/8 GPUs"); `--gpus N` launched as one
+process re-executes itself under torch.distributed.run with N ranks (NCCL, NCCL_DEBUG=INFO).
+The headline line is rho_d = 2 %; `density_sweep` adds the north-star range 1 % and 5 %.
 
 Metric: effective GMAC/s = algorithmic MACs / time, where fwd MACs are the in-bounds
 (input, weight) pairs (Eq. (1) first term) and bwd MACs are 2 x the pairs landing on
 kept outputs (dx and dw). HBM GB/s is reported alongside from compulsory bytes.
 
-  python bench.py [--gpus N --steps K --warmup W] [--density 0.02] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--density 0.02] [--sweep 0.01,0.05] [--impl reference]
 """
 from __future__ import annotations
 
@@ -159,6 +163,125 @@ def algorithmic_macs(torch, X, W, y_keys_list, B_local, V):
 
 
 # ----------------------------------------------------------------------- our arm
+class Step:
+    """One training step of the C4 layer on this rank's shard: forward (attention), backward with
+    the fp64 dw / dbias partials, the all-reduce of step i started on a side stream and finished
+    (waited + rounded) after step i+1's forward has been enqueued; two partial buffers alternate."""
+
+    def __init__(self, torch, spc, X, W, bias_t, k, variant, spp, world, dy_t):
+        self.torch, self.spc = torch, spc
+        self.fwd = spc.FwdPlan(X, W, "magnitude", k, variant, bias_t, spp)
+        self.resolved = self.fwd.resolved
+        self.cap = self.fwd.capacity
+        Y0 = self.fwd(X, W, bias_t)
+        self.bwd = spc.BwdPlan(X, W, Y0)
+        self.dx = torch.empty(max(X.nnz_bound, 1), device="cuda")
+        self.dw = torch.empty(W.keys.numel(), device="cuda")
+        self.db = torch.empty(C_OUT, device="cuda")
+        side = torch.cuda.Stream() if world > 1 else None
+        self.ar = [spc.dp.GradAllReduce(W.keys.numel(), C_OUT, "cuda", stream=side) for _ in range(2)]
+        self.i = 0
+        self.pending = None
+        self.dy = dy_t
+
+    def __call__(self, X, W, bias_t, dy=None):
+        Y = self.fwd(X, W, bias_t)
+        if self.pending is not None:           # previous step's all-reduce overlapped this forward
+            self.pending.finish(self.dw, self.db)
+        ar = self.ar[self.i & 1]
+        self.bwd.f64(X, W, Y, self.dy if dy is None else dy, self.dx, ar.dw64, ar.db64)
+        ar.start()
+        self.pending = ar
+        self.i += 1
+        return Y
+
+    def drain(self):
+        if self.pending is not None:
+            self.pending.finish(self.dw, self.db)
+            self.pending = None
+
+
+def measure(args, torch, spc, density, rank, world, local, steps, warmup, clocks=True):
+    """Inputs of this rank's shard at `density`, warm-up, the algorithmic work of one step, then
+    `steps` timed steps (CUDA events per step on the launching stream; a 512 MB write flushes L2
+    between steps, outside the timed intervals)."""
+    import torch.distributed as dist
+
+    B_local = BATCH // world
+    b0 = rank * B_local
+    V = RES ** 3
+    cfg = c4_inputs(density, args.values, batch=B_local, b0=b0)
+    x, w, bias, k = cfg["x"], cfg["w"], cfg["bias"], cfg["k"]
+    X = spc.SparseMap.from_arrays(x.keys, x.values, x.batch, x.channels, x.dims)
+    W = spc.SparseFilter.from_arrays(w.keys, w.values, w.c_in, w.c_out, w.ksize)
+    bias_t = torch.from_numpy(bias).cuda()
+    probe = spc.FwdPlan(X, W, "magnitude", k, args.variant, bias_t, args.samples_per_pass)
+    variant = probe.resolved
+    cap = probe.capacity
+    del probe
+    dy_t = torch.from_numpy(grad_values(cap, SEED_BASE + 7 + rank)).cuda()
+    step = Step(torch, spc, X, W, bias_t, k, variant, args.samples_per_pass, world, dy_t)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # 512 MB > L2
+
+    for _ in range(warmup):
+        step(X, W, bias_t)
+    step.drain()
+    torch.cuda.synchronize()
+    # algorithmic work of one step (measurement plumbing, outside the timed region)
+    Y = step(X, W, bias_t)
+    step.drain()
+    torch.cuda.synchronize()
+    ny = int(Y.nnz_dev.item())
+    fwd_macs, bwd_macs = algorithmic_macs(torch, X, W, Y.keys[:ny], B_local, V)
+    nnz_x, nnz_w = x.nnz, w.nnz
+    fwd_bytes = 12 * nnz_x + 12 * nnz_w + 4 * C_OUT + 12 * ny
+    bwd_bytes = 12 * nnz_x + 4 * nnz_x + 12 * ny + 16 * nnz_w
+    launches0 = spc.kernel_launches()
+    step(X, W, bias_t)
+    step.drain()
+    torch.cuda.synchronize()
+    launches_per_step = spc.kernel_launches() - launches0
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local) if clocks else None
+    if clk:
+        clk.__enter__()
+    for i in range(steps):
+        flush.zero_()
+        evs[i][0].record()
+        step(X, W, bias_t)
+        if i == steps - 1:
+            step.drain()                         # the last all-reduce + rounding belong to the run
+        evs[i][1].record()
+    torch.cuda.synchronize()
+    if clk:
+        clk.__exit__()
+    if world > 1:
+        dist.barrier()
+    per_step = [a.elapsed_time(b) for a, b in evs]
+    t_ms = float(sum(per_step))
+    if world > 1:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+        tot = torch.tensor([fwd_macs + bwd_macs, fwd_bytes + bwd_bytes, fwd_macs, bwd_macs, ny, nnz_x],
+                           dtype=torch.float64, device="cuda")
+        dist.all_reduce(tot)
+        macs_all, bytes_all = float(tot[0].item()), float(tot[1].item())
+    else:
+        macs_all, bytes_all = float(fwd_macs + bwd_macs), float(fwd_bytes + bwd_bytes)
+    ms_per_step = t_ms / steps
+    return dict(cfg=cfg, x=x, w=w, X=X, W=W, bias_t=bias_t, k=k, Y=Y, step=step, flush=flush, variant=variant,
+                cap=cap, dy_t=dy_t, B_local=B_local, fwd_macs=fwd_macs, bwd_macs=bwd_macs, ny=ny, nnz_x=nnz_x,
+                nnz_w=nnz_w, fwd_bytes=fwd_bytes, bwd_bytes=bwd_bytes, macs_all=macs_all, bytes_all=bytes_all,
+                ms_per_step=ms_per_step, per_step=per_step, launches_per_step=launches_per_step,
+                clocks=clk.summary() if clk else None,
+                value=macs_all / (ms_per_step * 1e-3) / 1e9, hbm_gbs=bytes_all / (ms_per_step * 1e-3) / 1e9)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -168,90 +291,25 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus and world > 1:
+    if world != args.gpus:
         raise SystemExit(f"WORLD_SIZE={world} but --gpus {args.gpus}")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     spc.load()
     assert BATCH % world == 0
-    B_local = BATCH // world
-    b0 = rank * B_local
-    V = RES ** 3
-    cfg = c4_inputs(args.density, args.values, batch=B_local, b0=b0)
-    x, w, bias, k = cfg["x"], cfg["w"], cfg["bias"], cfg["k"]
-    X = spc.SparseMap.from_arrays(x.keys, x.values, x.batch, x.channels, x.dims)
-    W = spc.SparseFilter.from_arrays(w.keys, w.values, w.c_in, w.c_out, w.ksize)
-    bias_t = torch.from_numpy(bias).cuda()
-    fwd = spc.FwdPlan(X, W, "magnitude", k, args.variant, bias_t, args.samples_per_pass)
-    args.resolved_variant = fwd.resolved
-    cap = fwd.capacity
-    dy_t = torch.from_numpy(grad_values(cap, SEED_BASE + 7 + rank)).cuda()
-    Y0 = fwd(X, W, bias_t)
-    bwd = spc.BwdPlan(X, W, Y0)
-    dx_t = torch.empty(max(X.nnz_bound, 1), device="cuda")
-    dw_t = torch.empty(W.keys.numel(), device="cuda")
-    db_t = torch.empty(C_OUT, device="cuda")
-    allreduce = spc.dp.GradAllReduce(W.keys.numel(), C_OUT, "cuda")   # SUM of dw||dbias (R13)
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # 512 MB > L2
-
-    def step():
-        Y = fwd(X, W, bias_t)
-        bwd(X, W, Y, dy_t, dx_t, dw_t, db_t)
-        allreduce(dw_t, db_t)               # no-op on one GPU
-        return Y
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    # algorithmic work of one step (measurement plumbing, outside the timed region)
-    Y = step()
-    torch.cuda.synchronize()
-    ny = int(Y.nnz_dev.item())
-    fwd_macs, bwd_macs = algorithmic_macs(torch, X, W, Y.keys[:ny], B_local, V)
-    nnz_x, nnz_w = x.nnz, w.nnz
-    fwd_bytes = 12 * nnz_x + 12 * nnz_w + 4 * C_OUT + 12 * ny
-    bwd_bytes = 12 * nnz_x + 4 * nnz_x + 12 * ny + 16 * nnz_w
-    launches0 = spc.kernel_launches()
-    step()
-    torch.cuda.synchronize()
-    launches_per_step = spc.kernel_launches() - launches0
-
-    # ---- timed region: K steps, L2 flushed between steps (not timed), CUDA events
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            flush.zero_()
-            evs[i][0].record()
-            step()
-            evs[i][1].record()
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    per_step = [a.elapsed_time(b) for a, b in evs]
-    t_ms = float(sum(per_step))
-    if world > 1:
-        tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
-        tot = torch.tensor([fwd_macs + bwd_macs, fwd_bytes + bwd_bytes], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tot)
-        macs_all, bytes_all = float(tot[0].item()), float(tot[1].item())
-    else:
-        macs_all, bytes_all = float(fwd_macs + bwd_macs), float(fwd_bytes + bwd_bytes)
-    ms_per_step = t_ms / args.steps
-    value = macs_all / (ms_per_step * 1e-3) / 1e9
+    m = measure(args, torch, spc, args.density, rank, world, local, args.steps, args.warmup)
+    args.resolved_variant = m["variant"]
 
     # ---- per-kernel durations (CUDA events the library records on its stream)
+    step, X, W, bias_t = m["step"], m["X"], m["W"], m["bias_t"]
     spc.profile_reset()
     spc.profile_enable(True)
     nprof = max(1, min(3, args.steps))
     for _ in range(nprof):
-        flush.zero_()
-        step()
+        m["flush"].zero_()
+        step(X, W, bias_t)
+        step.drain()
     torch.cuda.synchronize()
     prof = spc.profile_read()
     spc.profile_enable(False)
@@ -259,58 +317,81 @@ def run_ours(args):
     step_sum = sum(p["ms_per_step"] for p in phases.values()) or 1.0
     top = max(phases, key=lambda n: phases[n]["ms_per_step"])
     pk, src = peaks()
-    roof = roofline_for(top, phases[top], ny, nnz_x, nnz_w, B_local, fwd_macs, bwd_macs, pk, src, clk.summary())
-    roof["share_of_step"] = phases[top]["ms_per_step"] / step_sum
+    roof = roofline_for(top, phases[top], m, pk, src)
+    roof["share_of_step"] = round(phases[top]["ms_per_step"] / step_sum, 4)
+    kernel_roofs = {n: roofline_for(n, phases[n], m, pk, src) for n in ("conv_fwd", "conv_bwd", "fwd_write", "row_index")
+                    if n in phases}
 
     # ---- end to end through the C-ABI with host buffers (pinned), copies inside the region
-    e2e = run_e2e(torch, spc, x, w, bias, k, cap, dy_t, args, world, dist if world > 1 else None)
+    e2e = run_e2e(torch, spc, m, args, world, dist if world > 1 else None)
+
+    # ---- the north-star density range (1 % / 5 %) in the same run
+    sweep = []
+    for d in args.sweep:
+        if abs(d - args.density) < 1e-12:
+            continue
+        md = measure(args, torch, spc, d, rank, world, local, max(1, args.steps // 2), min(args.warmup, 3),
+                     clocks=False)
+        sweep.append({"density": d, "value": round(md["value"], 3), "unit": "GMAC/s",
+                      "ms_per_step": round(md["ms_per_step"], 4), "hbm_gbs": round(md["hbm_gbs"], 2),
+                      "hbm_frac_of_peak": round(md["hbm_gbs"] / float(pk.get("hbm_gbs", 6650.0)), 4),
+                      "work_per_step": {"fwd_macs": md["fwd_macs"], "bwd_macs": md["bwd_macs"], "nnz_x": md["nnz_x"],
+                                        "nnz_y": md["ny"], "compulsory_bytes": md["fwd_bytes"] + md["bwd_bytes"]},
+                      "steps": max(1, args.steps // 2)})
+        del md
+        torch.cuda.empty_cache()
 
     result = None
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            cpu = cpu_baseline(cfg, fwd_macs, bwd_macs, Y, x)
-        e2e_value = (macs_all / (e2e["ms_per_step"] * 1e-3) / 1e9) if e2e else None
+            cpu = cpu_baseline(m["cfg"], args.cpu_samples)
+        e2e_value = (m["macs_all"] / (e2e["ms_per_step"] * 1e-3) / 1e9) if e2e else None
         result = {
             "metric": "sparse conv fwd+bwd effective GMAC/s (C4 128^3, rho_up 5%)",
-            "value": round(value, 3),
+            "value": round(m["value"], 3),
             "unit": "GMAC/s",
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
-            "ms_per_step": round(ms_per_step, 4),
+            "ms_per_step": round(m["ms_per_step"], 4),
             "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None,
             "dtype": "f32",
             "data": f"synthetic ({args.values} values, uniform positions, seeded)",
             "config": {
-                "workload": f"C4: 3D {RES}^3, batch {BATCH} (sharded {B_local}/GPU), {C_IN}->{C_OUT} ch, 3x3x3, "
+                "workload": f"C4: 3D {RES}^3, batch {BATCH} (sharded {m['B_local']}/GPU), {C_IN}->{C_OUT} ch, 3x3x3, "
                             f"rho_f {RHO_F}, rho_d {args.density}, rho_up {RHO_UP} (k={K_SEL}), magnitude attention, "
-                            f"fwd + bwd(dx,dw,dbias)",
+                            f"fwd + bwd(dx,dw,dbias) + dw||dbias all-reduce",
                 "global_batch": BATCH,
                 "density": args.density,
                 "fwd_variant": f"{args.variant} -> {args.resolved_variant}",
                 "fwd_samples_per_pass": args.samples_per_pass or "all",
-                "fwd_workspace_gb": round(fwd.ws_bytes / 1e9, 3),
+                "fwd_workspace_gb": round(step.fwd.ws_bytes / 1e9, 3),
                 "parallelism": f"dp{world}",
                 "l2": "flushed between timed steps (512 MB write); inputs also exceed L2",
             },
-            "hbm_gbs": round(bytes_all / (ms_per_step * 1e-3) / 1e9, 2),
-            "work_per_step": {"fwd_macs": fwd_macs, "bwd_macs": bwd_macs, "nnz_x": nnz_x, "nnz_w": nnz_w,
-                              "nnz_y": ny, "compulsory_bytes": fwd_bytes + bwd_bytes},
-            "per_step_ms": [round(t, 4) for t in per_step],
+            "hbm_gbs": round(m["hbm_gbs"], 2),
+            "hbm_frac_of_peak": round(m["hbm_gbs"] / float(pk.get("hbm_gbs", 6650.0)), 4),
+            "work_per_step": {"fwd_macs": m["fwd_macs"], "bwd_macs": m["bwd_macs"], "nnz_x": m["nnz_x"],
+                              "nnz_w": m["nnz_w"], "nnz_y": m["ny"],
+                              "compulsory_bytes": m["fwd_bytes"] + m["bwd_bytes"],
+                              "fwd_bytes": m["fwd_bytes"], "bwd_bytes": m["bwd_bytes"]},
+            "per_step_ms": [round(t, 4) for t in m["per_step"]],
             "kernels": {n: {"ms": round(p["ms_per_step"], 4), "n": p["launches_per_step"],
                             "share": round(p["ms_per_step"] / step_sum, 4)} for n, p in
                         sorted(phases.items(), key=lambda kv: -kv[1]["ms_per_step"])},
             "roofline": roof,
+            "kernel_rooflines": kernel_roofs,
+            "density_sweep": sweep,
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 3) if e2e_value else None, "unit": "GMAC/s",
                     "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
                     "ms_per_step": round(e2e["ms_per_step"], 4)} if e2e else None,
-            "gpu_launches": int(launches_per_step * args.steps),
-            "gpu_launches_per_step": int(launches_per_step),
-            "clocks": clk.summary(),
+            "gpu_launches": int(m["launches_per_step"] * args.steps),
+            "gpu_launches_per_step": int(m["launches_per_step"]),
+            "clocks": m["clocks"],
         }
         print(json.dumps(result), flush=True)
     if world > 1:
@@ -319,53 +400,41 @@ def run_ours(args):
     return result
 
 
-def roofline_for(name, ph, ny, nnz_x, nnz_w, B_local, fwd_macs, bwd_macs, pk, src, clocks):
-    """Roofline of the dominant kernel: algorithmic work per launch over the
-    average launch duration = the step's work over the kernel's time per step (the batch-sliced
-    forward launches the kernel once per pass, each on 1/passes of the work)."""
+# Algorithmic bytes per launch (SURVEY §8(d) "Algorithmic bytes per unit of work", 64-bit keys):
+# the forward's kernels are charged the whole forward's compulsory traffic (12 B per input, 12 B
+# per weight, 4 B per bias, 12 B per output), the backward's the backward's.
+def roofline_for(name, ph, m, pk, src):
     t = ph["ms_per_step"] * 1e-3
-    V = RES ** 3
-    nseg = B_local * C_OUT
     hbm = float(pk.get("hbm_gbs", 6650.0))
     sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
-    # The scatter convolutions are bound by shared-memory read-modify-writes, not by FFMA issue:
-    # every MAC of Alg. 1 (fwd) reads and writes one 4-byte accumulator word (8 B through the
-    # 128 B/clk/SM shared-memory crossbar, B300_MICROARCH "LDS/STS"), so the peak is 16 MAC/clk/SM.
-    # The backward reads one 4-byte gradient word per (entry, weight) pair it visits (every pair
-    # is visited; 2 MACs are algorithmic only on kept outputs): 32 pair visits/clk/SM on the same
-    # crossbar. DESIGN.md section 7 derives both.
-    lsu_fwd = 148 * 16 * sm_mhz * 1e6 / 1e12
-    if name == "conv_fwd":
-        return {"kernel": name, "bound": "alu", "achieved": round(fwd_macs / t / 1e12, 4), "unit": "TMAC/s",
-                "peak": round(lsu_fwd, 3), "frac": round(fwd_macs / t / 1e12 / lsu_fwd, 4),
-                "traffic": ncu_traffic(name),
-                "peak_source": f"derived: shared-memory RMW rate 148 SM x 128 B/clk / 8 B per MAC x {sm_mhz:.0f} MHz",
-                "algorithmic": f"{fwd_macs} MACs per step (Eq. (1) pairs) in {ph['launches_per_step']:g} launch(es)"}
-    if name == "conv_bwd":
-        lsu_bwd = 148 * 32 * sm_mhz * 1e6 / 1e12   # pair visits/s: one 4-byte G load each
-        return {"kernel": name, "bound": "alu", "achieved": round(fwd_macs / t / 1e12, 4), "unit": "Tpair/s",
-                "peak": round(lsu_bwd, 3), "frac": round(fwd_macs / t / 1e12 / lsu_bwd, 4),
-                "traffic": ncu_traffic(name),
-                "peak_source": f"derived: one 4-byte shared gradient load per (entry, weight) pair, 148 SM x 32 lanes/clk x {sm_mhz:.0f} MHz",
-                "algorithmic": f"{fwd_macs} (entry, weight) pairs visited per step ({bwd_macs} MACs on kept outputs) in {ph['launches_per_step']:g} launch(es)"}
-    per_launch_bytes = {
-        "fwd_classify": 4 * nseg * V,
-        "fwd_write": 4 * nseg * V + 12 * ny,
-        "row_index": 8 * nnz_x + 4 * (B_local * C_IN * RES * RES + 1),
-        "dbias": 12 * ny,
+    nrows = m["B_local"] * C_IN * RES * RES
+    per = {
+        "conv_fwd": (m["fwd_bytes"], "fwd: 12 B/input + 12 B/weight + 4 B/bias + 12 B/output (SURVEY 8d)"),
+        "conv_bwd": (m["bwd_bytes"], "bwd: 12 B/input + 4 B/dx + 12 B/kept output + 16 B/weight (SURVEY 8d)"),
+        "fwd_write": (12 * m["ny"], "12 B per kept output written"),
+        "row_index": (8 * m["nnz_x"] + 4 * (nrows + 1), "8 B per key read + 4 B per row pointer"),
     }.get(name)
-    if per_launch_bytes is None:
+    if per is None:
         return {"kernel": name, "bound": "unknown", "achieved": None, "peak": None, "unit": None, "frac": None,
                 "traffic": None}
-    gbs = per_launch_bytes / t / 1e9
-    return {"kernel": name, "bound": "hbm", "achieved": round(gbs, 1), "unit": "GB/s", "peak": hbm,
-            "frac": round(gbs / hbm, 4), "traffic": ncu_traffic(name),
-            "peak_source": f"{src} (MEASURED_PEAKS.json hbm_gbs)",
-            "algorithmic": f"{per_launch_bytes} bytes per step in {ph['launches_per_step']:g} launch(es)"}
+    nbytes, what = per
+    gbs = nbytes / t / 1e9
+    out = {"kernel": name, "bound": "hbm", "achieved": round(gbs, 1), "unit": "GB/s", "peak": hbm,
+           "frac": round(gbs / hbm, 4), "traffic": ncu_traffic(name),
+           "peak_source": f"{src} (MEASURED_PEAKS.json hbm_gbs)",
+           "algorithmic": f"{nbytes} bytes per launch ({what}), {ph['launches_per_step']:g} launch(es) per step",
+           "ms": round(ph["ms_per_step"], 4)}
+    if name in ("conv_fwd", "conv_bwd"):
+        macs = m["fwd_macs"] if name == "conv_fwd" else m["bwd_macs"]
+        ffma = 148 * 128 * sm_mhz * 1e6 / 1e12   # TMAC/s: 148 SM x 128 FP32 lanes x clock
+        out["alu"] = {"achieved_tmacs": round(macs / t / 1e12, 4), "ffma_peak_tmacs": round(ffma, 2),
+                      "frac": round(macs / t / 1e12 / ffma, 4),
+                      "note": "secondary: Eq. (1) MACs over the FP32 FMA peak (derived from unit counts)"}
+    return out
 
 
 def ncu_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture, or None."""
+    """DRAM bytes per launch of `kernel` from the newest committed ncu --set full capture, or None."""
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_traffic.json")), reverse=True):
         try:
             d = json.load(open(path))
@@ -376,34 +445,28 @@ def ncu_traffic(kernel):
     return None
 
 
-def run_e2e(torch, spc, x, w, bias, k, cap, dy_dev, args, world, dist):
+def run_e2e(torch, spc, m, args, world, dist):
     """Same step through the public API with HOST inputs: every step's inputs (x keys/values, dy)
     are copied H2D from pinned memory inside the timed region and its result (dw, dbias, output
     nnz) is read back D2H. Like a data loader, the upload of step i+1 runs on a copy stream into
     the second of two device input buffers while step i computes (the buffer is reused only after
     the step that read it has finished)."""
+    x, w, k, bias_t = m["x"], m["w"], m["k"], m["bias_t"]
     hk = torch.from_numpy(x.keys.view(np.int64)).pin_memory()
     hv = torch.from_numpy(x.values).pin_memory()
-    hdy = dy_dev.cpu().pin_memory()
+    hdy = m["dy_t"].cpu().pin_memory()
     bufs = [(torch.empty_like(hk, device="cuda"), torch.empty_like(hv, device="cuda"),
              torch.empty_like(hdy, device="cuda")) for _ in range(2)]
-    W = spc.SparseFilter.from_arrays(w.keys, w.values, w.c_in, w.c_out, w.ksize)
-    bias_t = torch.from_numpy(bias).cuda()
+    W = m["W"]
     Xs = [spc.SparseMap(bk, bv, x.batch, x.channels, x.dims, x.nnz, None) for bk, bv, _ in bufs]
-    fwd = spc.FwdPlan(Xs[0], W, "magnitude", k, args.resolved_variant, None, args.samples_per_pass)
     for bk, bv, bd in bufs:
         bk.copy_(hk)
         bv.copy_(hv)
         bd.copy_(hdy)
-    Y0 = fwd(Xs[0], W, bias_t)
-    bwd = spc.BwdPlan(Xs[0], W, Y0)
-    dx = torch.empty(max(x.nnz, 1), device="cuda")
-    dw = torch.empty(W.keys.numel(), device="cuda")
-    db = torch.empty(C_OUT, device="cuda")
+    step = Step(torch, spc, Xs[0], W, bias_t, k, args.resolved_variant, args.samples_per_pass, world, bufs[0][2])
     out_dw = torch.empty(W.keys.numel()).pin_memory()
     out_db = torch.empty(C_OUT).pin_memory()
     out_n = torch.empty(1, dtype=torch.int64).pin_memory()
-    allreduce = spc.dp.GradAllReduce(W.keys.numel(), C_OUT, "cuda")
     comp = torch.cuda.current_stream()
     copy = torch.cuda.Stream()
     loaded = [torch.cuda.Event(), torch.cuda.Event()]
@@ -419,17 +482,17 @@ def run_e2e(torch, spc, x, w, bias, k, cap, dy_dev, args, world, dist):
             bd.copy_(hdy, non_blocking=True)
             loaded[j].record(copy)
 
-    def step(i, last):
+    def one(i, last):
         j = i % 2
         if not last:
             upload(i + 1)
         comp.wait_event(loaded[j])
-        Y = fwd(Xs[j], W, bias_t)
-        bwd(Xs[j], W, Y, bufs[j][2], dx, dw, db)
+        Y = step(Xs[j], W, bias_t, bufs[j][2])
         consumed[j].record(comp)
-        allreduce(dw, db)
-        out_dw.copy_(dw, non_blocking=True)
-        out_db.copy_(db, non_blocking=True)
+        if last:
+            step.drain()
+        out_dw.copy_(step.dw, non_blocking=True)
+        out_db.copy_(step.db, non_blocking=True)
         out_n.copy_(Y.nnz_dev, non_blocking=True)
 
     def run(n):
@@ -437,7 +500,7 @@ def run_e2e(torch, spc, x, w, bias, k, cap, dy_dev, args, world, dist):
             e.record(comp)
         upload(0)
         for i in range(n):
-            step(i, i == n - 1)
+            one(i, i == n - 1)
 
     run(max(1, args.warmup))
     torch.cuda.synchronize()
@@ -459,19 +522,56 @@ def run_e2e(torch, spc, x, w, bias, k, cap, dy_dev, args, world, dist):
 
 
 # --------------------------------------------------------------------- CPU baseline
-def cpu_baseline(cfg, fwd_macs_total, bwd_macs_total, Y, x):
-    """The oracle (oracle/, plain C, fp64, single thread) on one sample of the same workload."""
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+_CPU_CFG = None   # (x, w, bias, k) inherited by the forked oracle workers (no pickling of the map)
+
+
+def _oracle_sample(b):
+    """fwd+bwd of sample b by the oracle (one worker process of the all-cores leg)."""
     import oracle as ora
 
-    xs = select_samples(x, [0])
+    x, w, bias, k = _CPU_CFG
+    xs = select_samples(x, [b])
     t0 = time.perf_counter()
-    yk, yv, _, macs = ora.conv_fwd(xs, cfg["w"], cfg["bias"], attn=ora.ATTN_MAGNITUDE, k=cfg["k"])
-    dy = grad_values(yk.shape[0], SEED_BASE + 99)
-    *_, kept_pairs = ora.conv_bwd(xs, cfg["w"], yk, dy, return_pairs=True)
-    dt = time.perf_counter() - t0
-    bwd = 2 * kept_pairs
-    return {"value": round((macs + bwd) / dt / 1e9, 4), "unit": "GMAC/s", "cores": 1, "kind": "oracle",
-            "sample": f"1 of {BATCH} samples (b=0), fwd+bwd, {dt:.1f} s", "seconds": round(dt, 2)}
+    yk, _, _, macs = ora.conv_fwd(xs, w, bias, attn=ora.ATTN_MAGNITUDE, k=k)
+    dy = grad_values(yk.shape[0], SEED_BASE + 99 + b)
+    *_, kept_pairs = ora.conv_bwd(xs, w, yk, dy, return_pairs=True)
+    return macs + 2 * kept_pairs, time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, nsamples):
+    """The oracle (oracle/, plain C, fp64, single-threaded code) on a bounded sample of the same
+    workload: one sample on 1 core, then `nsamples` samples on all the host's cores (one forked
+    worker process per sample). Reported baseline only."""
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+
+    global _CPU_CFG
+    _CPU_CFG = (cfg["x"], cfg["w"], cfg["bias"], cfg["k"])
+    macs1, dt1 = _oracle_sample(0)
+    ncpu = os.cpu_count() or 1
+    ns = max(1, min(nsamples, cfg["x"].batch))
+    nw = min(ncpu, ns)
+    t0 = time.perf_counter()
+    with ProcessPoolExecutor(max_workers=nw, mp_context=mp.get_context("fork")) as ex:
+        res = list(ex.map(_oracle_sample, range(ns)))
+    dtn = time.perf_counter() - t0
+    macsn = sum(r[0] for r in res)
+    return {"value": round(macsn / dtn / 1e9, 4), "unit": "GMAC/s", "cores": nw, "kind": "oracle",
+            "sample": f"{ns} of {BATCH} samples, fwd+bwd, one worker process per sample on {nw} of {ncpu} cores, "
+                      f"{dtn:.1f} s wall",
+            "cpu_model": _cpu_model(), "nproc": ncpu,
+            "single_core": {"value": round(macs1 / dt1 / 1e9, 4), "unit": "GMAC/s", "cores": 1,
+                            "sample": f"1 of {BATCH} samples (b=0), fwd+bwd, {dt1:.1f} s"}}
 
 
 # ------------------------------------------------------------------- reference arm
@@ -523,23 +623,89 @@ def run_reference(args):
     return res
 
 
+def _spawn(args, argv):
+    """`--gpus N` started as one process: re-execute under torch.distributed.run with N ranks on
+    this node (rendezvous on 127.0.0.1), NCCL with its communicator log."""
+    import subprocess
+    import socket
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+    return subprocess.call(cmd, env=env)
+
+
 def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--density", type=float, default=0.02)
+    ap.add_argument("--sweep", type=lambda s: [float(v) for v in s.split(",") if v], default=[0.01, 0.05],
+                    help="extra densities measured in the same run (north-star range), '' for none")
     ap.add_argument("--values", default="continuous", choices=["continuous", "dyadic"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-samples", type=int, default=16, help="samples of the all-cores oracle leg")
     ap.add_argument("--variant", default="measure", choices=["auto", "scatter", "gemm", "measure"],
                     help="forward accumulate variant (SURVEY §8 a3); 'measure' times both once and keeps the faster")
+    ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing only, gloo on CPU (tests)")
     ap.add_argument("--samples-per-pass", type=int, default=None,
                     help="bounded-memory forward (sparse_conv_fwd_pass, SURVEY §8 f2): samples per pass")
     args = ap.parse_args(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(_spawn(args, argv))
     if args.impl == "reference":
         return run_reference(args)
+    if args.dry_run:
+        return run_dry(args)
     return run_ours(args)
+
+
+def run_dry(args):
+    """--dry-run: the multi-rank plumbing of run_ours without a GPU (gloo): rank / world from the
+    launcher, the batch shard of each rank, the fp64 SUM all-reduce + single rounding of a
+    dw||dbias buffer (dp.GradAllReduce) and the max-over-ranks timing; rank 0 prints one line.
+    Covered by tests/test_bench_spawn.py (world size 2 on CPU)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1801_10585_b200 import dp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"WORLD_SIZE={world} but --gpus {args.gpus}")
+    if world > 1:
+        dist.init_process_group("gloo")
+    b0, b1 = dp.shard_range(BATCH, world, rank)
+    nw = 864
+    ar = dp.GradAllReduce(nw, C_OUT, "cpu")
+    ar.dw64.copy_(torch.arange(nw, dtype=torch.float64) * (rank + 1) / 64.0)
+    ar.db64.fill_(float(b1 - b0))
+    dw, db = torch.empty(nw), torch.empty(C_OUT)
+    ar(dw, db)
+    want = torch.arange(nw, dtype=torch.float64) * (world * (world + 1) / 2) / 64.0
+    t = dp.max_over_ranks(float(rank), "cpu")
+    shards = [None] * world
+    if world > 1:
+        dist.all_gather_object(shards, (b0, b1))
+    else:
+        shards = [(b0, b1)]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "shards": shards,
+                          "allreduce_ok": bool(torch.equal(dw, want.to(torch.float32))) and float(db[0]) == BATCH,
+                          "max_over_ranks": t}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -187,6 +187,21 @@ spc_status_t sparse_conv_bwd_weight(const spc_map_t* x, const spc_filter_t* w, c
                                     const float* dy, float* dw, float* dbias,
                                     void* workspace, size_t workspace_bytes, cudaStream_t stream);
 
+/* sparse_conv_bwd_f64 -- the data-parallel form of sparse_conv_bwd (SURVEY §8 a11 / e): dx as in
+ * sparse_conv_bwd (fp32; NULL to skip), dw64 / dbias64 = the UNROUNDED fp64 accumulators of this
+ * call (device [w->nnz] / [c_out] doubles, overwritten; dbias64 may be NULL). Alg. 2 sums
+ * bp_filter over the batch: each rank computes the fp64 partial of its sample shard, the
+ * partials are summed across ranks (NCCL all-reduce, SUM -- reading R13) and spc_round_f64 rounds
+ * the sum once, so the sharded dw equals the single-GPU dw bit for bit whenever the fp64 sums
+ * are exact (and to 1 ulp otherwise). Workspace from spc_conv_bwd_query. Errors: as
+ * sparse_conv_bwd; SPC_ERR_INVALID_ARG when dw64 is NULL. */
+spc_status_t sparse_conv_bwd_f64(const spc_map_t* x, const spc_filter_t* w, const spc_map_t* y,
+                                 const float* dy, float* dx, double* dw64, double* dbias64,
+                                 void* workspace, size_t workspace_bytes, cudaStream_t stream);
+/* spc_round_f64 -- out[i] = (float)in[i], round to nearest even, i < n (device pointers);
+ * the single rounding of the reduced fp64 gradients (R12). */
+spc_status_t spc_round_f64(const double* in, float* out, int64_t n, cudaStream_t stream);
+
 /* ------------------------------------------------------------------------------------
  * attention_topk — the attention filter as a standalone layer: per (b, c)
  * segment of x keep min(k, n_seg) entries with the largest score (|v| for MAGNITUDE, v for

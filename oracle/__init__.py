@@ -7,6 +7,7 @@ from .oracle import (  # noqa: F401
     build,
     conv_fwd,
     conv_bwd,
+    conv_bwd64,
     topk,
     relu,
     maxpool,

@@ -270,13 +270,15 @@ done:
  * dbias[oc] = sum of dy over the kept outputs of channel oc (bias is added on the support only).
  * dx_abs / dw_abs (optional): sums of |terms| for the tolerance rule.
  */
-int ora_conv_bwd(int ndim, const int64_t* dims, int64_t batch, int64_t c_in, int64_t c_out,
-                 const int64_t* ksize,
-                 int64_t nx, const uint64_t* xk, const float* xv,
-                 int64_t nw, const uint64_t* wk, const float* wv,
-                 int64_t ny, const uint64_t* yk, const float* dy,
-                 float* dx, float* dw, float* dbias,
-                 double* dx_abs, double* dw_abs, int64_t* kept_pairs_out) {
+/* dw64 / db64 (optional): the fp64 sums before the final rounding -- the data-parallel tests
+ * add these per-shard partials (Alg. 2 sums bp_filter over b; reading R13) and round once. */
+int ora_conv_bwd64(int ndim, const int64_t* dims, int64_t batch, int64_t c_in, int64_t c_out,
+                   const int64_t* ksize,
+                   int64_t nx, const uint64_t* xk, const float* xv,
+                   int64_t nw, const uint64_t* wk, const float* wv,
+                   int64_t ny, const uint64_t* yk, const float* dy,
+                   float* dx, float* dw, float* dbias,
+                   double* dx_abs, double* dw_abs, int64_t* kept_pairs_out, double* dw64, double* db64) {
     if (ndim < 1 || ndim > ORA_MAXDIM || batch < 0 || c_in < 1 || c_out < 1) return -1;
     for (int d = 0; d < ndim; ++d) if (dims[d] < 1 || ksize[d] < 1 || ksize[d] % 2 == 0) return -1;
     if (check_sorted(nx, xk) || check_sorted(nw, wk) || check_sorted(ny, yk)) return -2;
@@ -316,6 +318,7 @@ int ora_conv_bwd(int ndim, const int64_t* dims, int64_t batch, int64_t c_in, int
         for (int64_t b = 0; b < batch; ++b)
             for (int64_t t = yoff[b * c_out + oc]; t < yoff[b * c_out + oc + 1]; ++t) db += (double)dy[t];
         if (dbias) dbias[oc] = (float)db;
+        if (db64) db64[oc] = db;
     }
     for (int64_t b = 0; b < batch; ++b) {
         for (int64_t oc = 0; oc < c_out; ++oc) {
@@ -343,12 +346,27 @@ int ora_conv_bwd(int ndim, const int64_t* dims, int64_t batch, int64_t c_in, int
         }
     }
     for (int64_t i = 0; i < nx; ++i) { dx[i] = (float)bpd[i]; if (dx_abs) dx_abs[i] = bpd_abs[i]; }
-    for (int64_t j = 0; j < nw; ++j) { dw[j] = (float)bpf[j]; if (dw_abs) dw_abs[j] = bpf_abs[j]; }
+    for (int64_t j = 0; j < nw; ++j) {
+        dw[j] = (float)bpf[j];
+        if (dw_abs) dw_abs[j] = bpf_abs[j];
+        if (dw64) dw64[j] = bpf[j];
+    }
     if (kept_pairs_out) *kept_pairs_out = kept_pairs;
 done:
     free(xp); free(wp); free(xoff); free(woff); free(yoff); free(G); free(K);
     free(bpd); free(bpf); free(bpd_abs); free(bpf_abs);
     return rc;
+}
+
+int ora_conv_bwd(int ndim, const int64_t* dims, int64_t batch, int64_t c_in, int64_t c_out,
+                 const int64_t* ksize,
+                 int64_t nx, const uint64_t* xk, const float* xv,
+                 int64_t nw, const uint64_t* wk, const float* wv,
+                 int64_t ny, const uint64_t* yk, const float* dy,
+                 float* dx, float* dw, float* dbias,
+                 double* dx_abs, double* dw_abs, int64_t* kept_pairs_out) {
+    return ora_conv_bwd64(ndim, dims, batch, c_in, c_out, ksize, nx, xk, xv, nw, wk, wv, ny, yk, dy, dx, dw, dbias,
+                          dx_abs, dw_abs, kept_pairs_out, NULL, NULL);
 }
 
 /* ------------------------------------------------- attention as a standalone layer */

@@ -40,6 +40,8 @@ def _load():
                                       I64, P, P, P, P, P]
         _lib.ora_conv_bwd.argtypes = [C.c_int, P, I64, I64, I64, P, I64, P, P, I64, P, P, I64, P, P,
                                       P, P, P, P, P, P]
+        _lib.ora_conv_bwd64.argtypes = [C.c_int, P, I64, I64, I64, P, I64, P, P, I64, P, P, I64, P, P,
+                                        P, P, P, P, P, P, P, P]
         _lib.ora_topk.argtypes = [C.c_int, P, I64, I64, I64, P, P, C.c_int, I64, I64, P, P, P, P]
         _lib.ora_relu.argtypes = [I64, P, P, P, P, P, P]
         _lib.ora_maxpool.argtypes = [C.c_int, P, I64, I64, P, I64, P, P, I64, P, P, P, P]
@@ -58,7 +60,7 @@ def _load():
         _lib.ora_to_dense.restype = C.c_int
         _lib.ora_memory_estimate.argtypes = [C.c_int, I64, I64, I64, C.c_double, C.c_int, P]
         _lib.ora_memory_estimate.restype = C.c_int
-        for f in ("ora_conv_fwd", "ora_conv_bwd", "ora_topk", "ora_relu", "ora_maxpool",
+        for f in ("ora_conv_fwd", "ora_conv_bwd", "ora_conv_bwd64", "ora_topk", "ora_relu", "ora_maxpool",
                   "ora_scatter_grad", "ora_decode_key", "ora_get_update_id"):
             getattr(_lib, f).restype = C.c_int
     return _lib
@@ -148,6 +150,29 @@ def conv_bwd(x, w, y_keys, dy, with_abs: bool = False, return_pairs: bool = Fals
     out = (dx[:x.nnz], dw[:w.nnz], db,
            dxa[:x.nnz] if with_abs else None, dwa[:w.nnz] if with_abs else None)
     return out + (int(pairs[0]),) if return_pairs else out
+
+
+def conv_bwd64(x, w, y_keys, dy, with_abs: bool = False):
+    """Alg. 2 with the fp64 sums of dw / dbias before their rounding (per-shard partials for the
+    data-parallel tests). Returns (dx, dw64, db64, dx_abs, dw_abs)."""
+    dims = _i64(x.dims)
+    ks = _i64(w.ksize)
+    xk, xv, wk, wv = _u64(x.keys), _f32(x.values), _u64(w.keys), _f32(w.values)
+    yk, g = _u64(y_keys), _f32(dy)
+    dx = np.zeros(max(1, x.nnz), np.float32)
+    dw = np.zeros(max(1, w.nnz), np.float32)
+    db = np.zeros(w.c_out, np.float32)
+    dw64 = np.zeros(max(1, w.nnz), np.float64)
+    db64 = np.zeros(w.c_out, np.float64)
+    dxa = np.zeros(max(1, x.nnz), np.float64) if with_abs else None
+    dwa = np.zeros(max(1, w.nnz), np.float64) if with_abs else None
+    pairs = np.zeros(1, np.int64)
+    rc = _load().ora_conv_bwd64(x.ndim, _p(dims), x.batch, w.c_in, w.c_out, _p(ks),
+                                x.nnz, _p(xk), _p(xv), w.nnz, _p(wk), _p(wv), yk.shape[0], _p(yk), _p(g),
+                                _p(dx), _p(dw), _p(db), _p(dxa), _p(dwa), _p(pairs), _p(dw64), _p(db64))
+    _check(rc, "ora_conv_bwd64")
+    return (dx[:x.nnz], dw64[:w.nnz], db64,
+            dxa[:x.nnz] if with_abs else None, dwa[:w.nnz] if with_abs else None)
 
 
 def topk(x, attn: int, k: int):

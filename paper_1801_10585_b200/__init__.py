@@ -18,6 +18,7 @@ from .ops import (  # noqa: F401
     sparse_conv_bwd,
     sparse_conv_bwd_input,
     sparse_conv_bwd_weight,
+    round_f64,
     attention_topk,
     sparse_relu,
     sparse_maxpool,

@@ -23,6 +23,7 @@ EXPORTS = [
     "spc_conv_fwd_query", "sparse_conv_fwd",
     "spc_conv_fwd_query_ex", "sparse_conv_fwd_ex", "spc_conv_fwd_variant",
     "spc_conv_bwd_query", "sparse_conv_bwd", "sparse_conv_bwd_input", "sparse_conv_bwd_weight",
+    "sparse_conv_bwd_f64", "spc_round_f64",
     "spc_topk_query", "attention_topk",
     "spc_relu_query", "sparse_relu",
     "spc_maxpool_query", "sparse_maxpool",
@@ -92,6 +93,8 @@ def load(path: str = LIB_PATH):
         "sparse_conv_bwd": ([pM, pF, pM, P, P, P, P, P, C.c_size_t, P], C.c_int),
         "sparse_conv_bwd_input": ([pM, pF, pM, P, P, P, C.c_size_t, P], C.c_int),
         "sparse_conv_bwd_weight": ([pM, pF, pM, P, P, P, P, C.c_size_t, P], C.c_int),
+        "sparse_conv_bwd_f64": ([pM, pF, pM, P, P, P, P, P, C.c_size_t, P], C.c_int),
+        "spc_round_f64": ([P, P, I64, P], C.c_int),
         "spc_topk_query": ([pM, C.c_int, I64, pi64, sz], C.c_int),
         "attention_topk": ([pM, C.c_int, I64, pO, P, P, C.c_size_t, P], C.c_int),
         "spc_relu_query": ([pM, pi64, sz], C.c_int),

@@ -285,15 +285,18 @@ BwdWs carve_bwd(Carver& c, const Geo& gx, const Geo& gy, const spc_filter_t* w) 
     return ws;
 }
 
+// dw64 / db64 (optional): accumulate into the caller's fp64 buffers and do not round (the
+// data-parallel form); otherwise the workspace accumulators are rounded into dw / dbias.
 spc_status_t conv_bwd_impl(const spc_map_t* x, const spc_filter_t* w, const spc_map_t* y, const float* dy, float* dx,
-                           float* dw, float* dbias, void* workspace, size_t ws_bytes, cudaStream_t s) {
+                           float* dw, float* dbias, void* workspace, size_t ws_bytes, cudaStream_t s,
+                           double* dw64 = nullptr, double* db64 = nullptr) {
     Geo gx, gy;
     KGeo kg;
     BwdTile t;
     SPC_TRY(bwd_plan(x, w, y, &gx, &gy, &kg, &t));
-    const bool want_dx = dx != nullptr, want_dw = dw != nullptr;
+    const bool want_dx = dx != nullptr, want_dw = dw != nullptr || dw64 != nullptr;
     if (y->nnz > 0 && !dy) return SPC_ERR_INVALID_ARG;
-    if (!want_dx && !want_dw && !dbias) return SPC_OK;
+    if (!want_dx && !want_dw && !dbias && !db64) return SPC_OK;
     if (want_dx && x->nnz > 0 && !dx) return SPC_ERR_INVALID_ARG;
     Carver m(nullptr);
     carve_bwd(m, gx, gy, w);
@@ -304,13 +307,15 @@ spc_status_t conv_bwd_impl(const spc_map_t* x, const spc_filter_t* w, const spc_
         SPC_TRY(maybe_validate(x, ws.flag, s));
         SPC_TRY(maybe_validate(y, ws.flag, s));
     }
+    if (dw64) ws.dw_acc = dw64;
+    if (db64) ws.db_acc = db64;
     SPC_TRY(cu(launch_row_index(gy, y->keys, y->nnz_dev, y->nnz, ws.yrow, s)));
-    if (dbias) {
+    if (dbias || db64) {
         SPC_TRY(cu(cudaMemsetAsync(ws.db_acc, 0, sizeof(double) * (size_t)w->c_out, s)));
         SPC_TRY(cu(launch_dbias(gy, ws.yrow, dy, ws.db_acc, s)));
     }
-    const int64_t nb = dbias ? w->c_out : 0;   // dbias rounded with dw (one launch)
-    if (!want_dx && !want_dw) return cu(launch_f64_to_f32_2(ws.db_acc, dbias, nb, nullptr, nullptr, 0, s));
+    const int64_t nb = (dbias && !db64) ? w->c_out : 0;   // dbias rounded with dw (one launch)
+    if (!want_dx && !want_dw) return nb ? cu(launch_f64_to_f32_2(ws.db_acc, dbias, nb, nullptr, nullptr, 0, s)) : SPC_OK;
     SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
     SPC_TRY(cu(launch_filter_table(kg, (int)w->c_in, (int)w->c_out, w->keys, w->values, w->nnz, ws.f.meta, ws.f.val,
                                    ws.f.off, ws.f.src, ws.f.scratch, s)));
@@ -318,7 +323,9 @@ spc_status_t conv_bwd_impl(const spc_map_t* x, const spc_filter_t* w, const spc_
     if (want_dw && w->nnz > 0) SPC_TRY(cu(cudaMemsetAsync(ws.dw_acc, 0, sizeof(double) * (size_t)w->nnz, s)));
     SPC_TRY(cu(launch_conv_bwd(gx, gy, kg, t, x->keys, x->values, ws.xrow, y->keys, dy, ws.yrow, ws.f.meta, ws.f.val,
                                ws.f.off, ws.f.src, dx, ws.dw_acc, want_dx, want_dw, s)));
-    return cu(launch_f64_to_f32_2(ws.db_acc, dbias, nb, ws.dw_acc, dw, want_dw ? w->nnz : 0, s));
+    const int64_t nw = (want_dw && !dw64) ? w->nnz : 0;
+    if (nb == 0 && nw == 0) return cu(cudaGetLastError());
+    return cu(launch_f64_to_f32_2(ws.db_acc, dbias, nb, ws.dw_acc, dw, nw, s));
 }
 
 // -------------------------------------------------------------------- selection ws
@@ -607,6 +614,19 @@ spc_status_t sparse_conv_bwd_weight(const spc_map_t* x, const spc_filter_t* w, c
                                     float* dw, float* dbias, void* workspace, size_t workspace_bytes, cudaStream_t s) {
     if (!dw) return SPC_ERR_INVALID_ARG;
     return conv_bwd_impl(x, w, y, dy, nullptr, dw, dbias, workspace, workspace_bytes, s);
+}
+
+spc_status_t sparse_conv_bwd_f64(const spc_map_t* x, const spc_filter_t* w, const spc_map_t* y, const float* dy,
+                                 float* dx, double* dw64, double* dbias64, void* workspace, size_t workspace_bytes,
+                                 cudaStream_t s) {
+    if (!dw64) return SPC_ERR_INVALID_ARG;
+    return conv_bwd_impl(x, w, y, dy, dx, nullptr, nullptr, workspace, workspace_bytes, s, dw64, dbias64);
+}
+
+spc_status_t spc_round_f64(const double* in, float* out, int64_t n, cudaStream_t s) {
+    if (n < 0 || (n > 0 && (!in || !out))) return SPC_ERR_INVALID_ARG;
+    if (n == 0) return SPC_OK;
+    return cu(launch_f64_to_f32(in, out, n, s));
 }
 
 spc_status_t spc_topk_query(const spc_map_t* x, spc_attn_t attn, int64_t k, int64_t* out_capacity,

@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(kSRThreads) stream_resolve_kernel(FwdArgs a, S
         if (pass == 0 && threadIdx.x == 0) {
             // the sampled threshold was too high: recompute this segment with tlow = 0
             a.fail[s] = 1;
+            a.tlow[s] = 0;       // the redo pass keeps every support entry
             a.cand_cur[s] = 0;
             a.cmax[s] = 0;
             const int b = (int)(s / (int64_t)a.seg_stride);

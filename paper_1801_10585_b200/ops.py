@@ -258,6 +258,10 @@ class BwdPlan:
         xs, fs, ys = x.c_struct(), w.c_struct(), y.c_struct()
         lib = load()
         st = _stream(stream)
+        if dbias is not None and dw is None:
+            # dbias is produced with the weight gradient (sparse_conv_bwd / _weight); a scratch dw
+            # keeps every requested output initialised
+            dw = torch.empty(max(w.keys.numel(), 1), dtype=torch.float32, device=dbias.device)
         if dx is not None and dw is not None:
             rc = lib.sparse_conv_bwd(C.byref(xs), C.byref(fs), C.byref(ys), _ptr(dy), _ptr(dx), _ptr(dw), _ptr(dbias),
                                      _ptr(self.ws), self.ws.numel(), st)
@@ -273,6 +277,24 @@ class BwdPlan:
         return dx, dw, dbias
 
 
+    def f64(self, x, w, y, dy, dx=None, dw64=None, dbias64=None, stream=None):
+        """Data-parallel form (sparse_conv_bwd_f64): dx (fp32, optional) and the unrounded fp64
+        accumulators of dw / dbias of this call (shard), to be summed across ranks and rounded
+        once (dp.GradAllReduce)."""
+        xs, fs, ys = x.c_struct(), w.c_struct(), y.c_struct()
+        check("sparse_conv_bwd_f64", load().sparse_conv_bwd_f64(
+            C.byref(xs), C.byref(fs), C.byref(ys), _ptr(dy), _ptr(dx), _ptr(dw64), _ptr(dbias64), _ptr(self.ws),
+            self.ws.numel(), _stream(stream)))
+        return dx, dw64, dbias64
+
+
+def round_f64(src: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+    """out = (float32) src, one rounding (spc_round_f64)."""
+    n = int(src.numel())
+    check("spc_round_f64", load().spc_round_f64(_ptr(src), _ptr(out), n, _stream(stream)))
+    return out
+
+
 def sparse_conv_bwd(x: SparseMap, w: SparseFilter, y: SparseMap, dy: torch.Tensor, need_dx=True, need_dw=True,
                     need_dbias=True, stream=None):
     """Alg. 2 (P:137-171), Eqs. (3)/(4). Returns (dx [nnz_x], dw [nnz_w], dbias [c_out])."""
@@ -281,7 +303,7 @@ def sparse_conv_bwd(x: SparseMap, w: SparseFilter, y: SparseMap, dy: torch.Tenso
     dw = torch.empty(max(w.keys.numel(), 1), dtype=torch.float32, device=dev) if need_dw else None
     db = torch.empty(w.c_out, dtype=torch.float32, device=dev) if need_dbias else None
     BwdPlan(x, w, y)(x, w, y, dy, dx, dw, db, stream)
-    return (dx[:x.nnz_bound] if dx is not None else None, dw[:w.keys.numel()] if dw is not None else None, db)
+    return (dx[:x.nnz_bound] if dx is not None else None, dw[:w.keys.numel()] if need_dw else None, db)
 
 
 def sparse_conv_bwd_input(x, w, y, dy, stream=None):

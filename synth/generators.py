@@ -86,6 +86,9 @@ def _draw_values(rng: np.random.Generator, n: int, mode: str) -> np.ndarray:
     if mode == "dyadic4":
         j = rng.integers(1, 5, size=n) * rng.choice(np.array([-1, 1]), size=n)
         return (j.astype(np.float32) / np.float32(4.0)).astype(np.float32)
+    if mode == "signed_zero":   # max-pool tie cases: +0 / -0 / negatives / positives (R8)
+        pool = np.array([-1.0, -0.5, -0.0, 0.0, 0.5], np.float32)
+        return pool[rng.integers(0, 5, size=n)].astype(np.float32)
     if mode == "positive":
         return rng.uniform(0.05, 1.0, size=n).astype(np.float32)
     raise ValueError(f"unknown value mode {mode!r}")

@@ -419,6 +419,22 @@ def test_maxpool_parity(cuda_lib, dims, stride, density):
     np.testing.assert_array_equal(host(arg[:yk.shape[0]]), oarg)
 
 
+@pytest.mark.parametrize("dims,stride", [((16, 16, 16), (2, 2, 2)), ((9, 11, 13), (3, 1, 4)), ((28, 28), (2, 2))])
+def test_maxpool_signed_zero_ties(cuda_lib, dims, stride):
+    """Members drawn from {-1, -0.5, -0, +0, +0.5} at high density: +0 and -0 compare equal
+    (reading R8: max over stored entries, ties -> smaller input key), so the maximum's value and
+    its argmax come from the first member of a cluster's tied zeros (the +0 / -0 branch)."""
+    spc = cuda_lib
+    x = uniform_map(2, 3, dims, 0.8, 62, values="signed_zero")
+    ok_, ov, oarg = ora.maxpool(x, stride)
+    y, arg = spc.sparse_maxpool(dev_map(spc, x), stride)
+    yk, yv = y.trimmed()
+    np.testing.assert_array_equal(host_keys(yk), ok_)
+    np.testing.assert_array_equal(host(yv).view(np.uint32), ov.view(np.uint32))   # the sign of zero too
+    np.testing.assert_array_equal(host(arg[:yk.shape[0]]), oarg)
+    assert np.any(ov == 0) and np.any(np.signbit(ov[ov == 0]))   # the -0 branch was exercised
+
+
 def test_scatter_grad_parity(cuda_lib):
     spc = cuda_lib
     x = uniform_map(2, 3, (9, 9), 0.4, 71)
@@ -540,6 +556,54 @@ def test_c4_full_size_sampled(cuda_lib):
         odx, _, _, _, _ = ora.conv_bwd(xs, w, ok_, dy[lo:hi])
         xlo, xhi = np.searchsorted(x.keys, np.uint64(b) * span), np.searchsorted(x.keys, np.uint64(b + 1) * span)
         np.testing.assert_array_equal(gdx[xlo:xhi], odx)
+
+
+@pytest.mark.slow
+def test_c4_full_size_continuous_all_samples(cuda_lib):
+    """BASELINE configs[3] at full size (128^3, b = 64, 8 -> 8, rho_d 2 %, rho_f 0.5, rho_up 5 %)
+    in continuous values, every sample: the oracle runs per sample in worker processes.
+    Forward: per (b, oc) equal kept counts, values within the tolerance rule on the common keys,
+    and every key in the symmetric difference within the tolerance of the segment's k-th score.
+    Backward with the oracle's kept outputs and dy: dx at all 21.5 M inputs and dw / dbias over
+    all 64 samples -- the high-contention fp64 reduction -- within the tolerance
+    rule (oracle: fp64 per-sample partials added in sample order, rounded once)."""
+    spc = cuda_lib
+    import bench
+    from tests._oracle_pool import per_sample_oracle
+
+    cfg = bench.c4_inputs(density=0.02, values="continuous")
+    x, w, bias, k = cfg["x"], cfg["w"], cfg["bias"], cfg["k"]
+    o = per_sample_oracle(x, w, bias, ora.ATTN_MAGNITUDE, k, SEED_BASE + 11)
+    X, W = dev_map(spc, x), dev_filter(spc, w)
+    y = spc.sparse_conv_fwd(X, W, torch.from_numpy(bias).cuda(), "magnitude", k)
+    yk, yv = y.trimmed()
+    gk, gv = host_keys(yk), host(yv)
+    V = 128 ** 3
+    nseg = 64 * 8
+    ok_, ov, oa = o["yk"], o["yv"], o["ya"]
+    gseg, oseg = (gk // np.uint64(V)).astype(np.int64), (ok_ // np.uint64(V)).astype(np.int64)
+    np.testing.assert_array_equal(np.bincount(gseg, minlength=nseg), np.bincount(oseg, minlength=nseg))
+    common, gi, oi = np.intersect1d(gk, ok_, assume_unique=True, return_indices=True)
+    assert_values_close(gv[gi], ov[oi], oa[oi], "forward values")
+    # k-th score per segment on both sides; swapped keys must sit at the threshold
+    tol_abs = 2 * (1e-5 + 1e-6 * 108 * 1.0 + 1e-6 * 0.1)   # |y| <= ~1 here; A <= 108 |x||w| + |b|
+    t_o = np.full(nseg, np.inf)
+    np.minimum.at(t_o, oseg, np.abs(ov.astype(np.float64)))
+    t_g = np.full(nseg, np.inf)
+    np.minimum.at(t_g, gseg, np.abs(gv.astype(np.float64)))
+    full = np.bincount(oseg, minlength=nseg) == k
+    assert np.all(np.abs(t_o[full] - t_g[full]) <= tol_abs)
+    only_g = np.setdiff1d(np.arange(gk.shape[0]), gi, assume_unique=True)
+    only_o = np.setdiff1d(np.arange(ok_.shape[0]), oi, assume_unique=True)
+    assert only_g.shape == only_o.shape
+    assert np.all(np.abs(np.abs(gv[only_g]) - t_o[gseg[only_g]]) <= tol_abs)
+    assert np.all(np.abs(np.abs(ov[only_o]) - t_g[oseg[only_o]]) <= tol_abs)
+    # backward on the oracle's kept set
+    Yo = spc.SparseMap.from_arrays(ok_, ov, 64, 8, (128,) * 3)
+    gdx, gdw, gdb = spc.sparse_conv_bwd(X, W, Yo, torch.from_numpy(o["dy"]).cuda())
+    assert_values_close(host(gdx), o["dx"], o["dxa"], "dx (all samples)")
+    assert_values_close(host(gdw), o["dw64"].astype(np.float32), o["dwa"], "dw (all 64 samples)")
+    assert_values_close(host(gdb), o["db64"].astype(np.float32), np.full(8, np.abs(o["dy"]).sum()), "dbias")
 
 
 @pytest.mark.slow
