@@ -27,7 +27,8 @@
  *   - Sizes: an input map's exact nnz is *nnz_dev when nnz_dev != NULL (a device int64; `nnz`
  *     is then an upper bound used for grid sizing), else `nnz`. Outputs write their exact
  *     count to *nnz_dev (device) so chained layers never need a host sync.
- *   - Spatial rank 1..3 (SPC_MAX_NDIM); odd kernel sizes; prod(ksize) <= 1024.
+ *   - Spatial rank 1..4 (SPC_MAX_NDIM; "generic n-dimensional tensors"); odd kernel sizes;
+ *     prod(ksize) <= 1024. The tensor-core accumulate variant (SPC_VARIANT_GEMM) is rank <= 3.
  *   - Convolution is cross-correlation with SAME zero padding and stride 1 (readings R1, R2).
  *   - Workspace: query the byte count with the matching *_query function, pass a device
  *     buffer of at least that many bytes (256-byte aligned).
@@ -35,8 +36,8 @@
  * Errors
  *   Host-checkable problems (NULL pointers, ndim out of range, even ksize, c_in mismatch,
  *   k < 1 with attention on, capacity or workspace too small) return synchronously with
- *   nothing enqueued. With the environment variable SPC_VALIDATE=1 every input map is also
- *   checked on the device (strictly increasing, in range); that check synchronises the
+ *   nothing enqueued. With the environment variable SPC_VALIDATE=1 every input map (and the
+ *   filter keys) is also checked on the device (strictly increasing, in range); that check synchronises the
  *   stream and returns SPC_ERR_UNSORTED on failure. Without it, unsorted or duplicate keys
  *   give unspecified values but every write stays within the output capacity. CUDA launch
  *   failures return SPC_ERR_CUDA.
@@ -54,7 +55,7 @@ extern "C" {
 
 typedef struct CUstream_st* cudaStream_t;
 
-#define SPC_MAX_NDIM 3
+#define SPC_MAX_NDIM 4
 
 typedef enum {
     SPC_OK = 0,
@@ -76,7 +77,7 @@ typedef enum {
 
 /* Input sparse feature map. */
 typedef struct {
-    int32_t ndim;                  /* spatial rank k of Eq. (1), 1..3                    */
+    int32_t ndim;                  /* spatial rank k of Eq. (1), 1..4                    */
     int64_t batch;                 /* b                                                  */
     int64_t channels;              /* c                                                  */
     int64_t dims[SPC_MAX_NDIM];    /* s_d per spatial dim (first = most significant)     */

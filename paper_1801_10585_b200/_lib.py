@@ -7,7 +7,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libspconv.so")
 
-MAX_NDIM = 3
+MAX_NDIM = 4
 
 STATUS = {
     0: "SPC_OK", 1: "SPC_ERR_INVALID_ARG", 2: "SPC_ERR_SHAPE", 3: "SPC_ERR_CAPACITY",

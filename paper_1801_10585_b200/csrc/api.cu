@@ -49,15 +49,16 @@ spc_status_t check_map(const spc_map_t* m, bool need_values = true) {
 
 Geo geo_of(const spc_map_t* m, int64_t channels) {
     Geo g{};
-    int64_t d[3] = {1, 1, 1};
-    for (int i = 0; i < m->ndim; ++i) d[3 - m->ndim + i] = m->dims[i];
+    int64_t d[4] = {1, 1, 1, 1};
+    for (int i = 0; i < m->ndim; ++i) d[4 - m->ndim + i] = m->dims[i];
     g.B = m->batch;
     g.C = channels;
-    g.X = (int)d[0];
-    g.Y = (int)d[1];
-    g.Z = (int)d[2];
-    g.V = d[0] * d[1] * d[2];
-    g.R = d[0] * d[1];
+    g.W = (int)d[0];
+    g.X = (int)d[1];
+    g.Y = (int)d[2];
+    g.Z = (int)d[3];
+    g.V = d[0] * d[1] * d[2] * d[3];
+    g.R = d[0] * d[1] * d[2];
     return g;
 }
 
@@ -66,18 +67,19 @@ spc_status_t check_filter(const spc_filter_t* w, const spc_map_t* x, KGeo* kg) {
     if (w->ndim != x->ndim) return SPC_ERR_SHAPE;
     if (w->c_in != x->channels || w->c_out < 1 || w->nnz < 0) return SPC_ERR_SHAPE;
     if (w->c_in * w->c_out > (1ll << 28)) return SPC_ERR_UNSUPPORTED;
-    int64_t k[3] = {1, 1, 1};
+    int64_t k[4] = {1, 1, 1, 1};
     int64_t kv = 1;
     for (int i = 0; i < w->ndim; ++i) {
         if (w->ksize[i] < 1 || w->ksize[i] % 2 == 0) return SPC_ERR_SHAPE;
-        k[3 - w->ndim + i] = w->ksize[i];
+        k[4 - w->ndim + i] = w->ksize[i];
         kv *= w->ksize[i];
     }
     if (kv > 1024) return SPC_ERR_UNSUPPORTED;
+    if (w->ndim == 4 && w->c_out >= (1 << 21)) return SPC_ERR_UNSUPPORTED;   // meta packing (pack_oc_ow)
     if (w->nnz > w->c_in * w->c_out * kv) return SPC_ERR_SHAPE;
     if (w->nnz > 0 && (!w->keys || !w->values)) return SPC_ERR_INVALID_ARG;
-    kg->kx = (int)k[0]; kg->ky = (int)k[1]; kg->kz = (int)k[2];
-    kg->hx = kg->kx / 2; kg->hy = kg->ky / 2; kg->hz = kg->kz / 2;
+    kg->kw = (int)k[0]; kg->kx = (int)k[1]; kg->ky = (int)k[2]; kg->kz = (int)k[3];
+    kg->hw = kg->kw / 2; kg->hx = kg->kx / 2; kg->hy = kg->ky / 2; kg->hz = kg->kz / 2;
     kg->KV = (int)kv;
     return SPC_OK;
 }
@@ -101,11 +103,26 @@ spc_status_t cu(cudaError_t e) { return e == cudaSuccess ? SPC_OK : SPC_ERR_CUDA
 // SPC_VALIDATE=1: device check of sortedness and range; synchronises the stream.
 spc_status_t maybe_validate(const spc_map_t* m, int* flag, cudaStream_t s) {
     if (!flag) return SPC_OK;
-    const uint64_t limit = (uint64_t)m->batch * (uint64_t)m->channels *
-                           (uint64_t)(m->ndim >= 1 ? m->dims[0] : 1) * (uint64_t)(m->ndim >= 2 ? m->dims[1] : 1) *
-                           (uint64_t)(m->ndim >= 3 ? m->dims[2] : 1);
+    uint64_t limit = (uint64_t)m->batch * (uint64_t)m->channels;
+    for (int d = 0; d < m->ndim; ++d) limit *= (uint64_t)m->dims[d];
     SPC_TRY(cu(cudaMemsetAsync(flag, 0, sizeof(int), s)));
     SPC_TRY(cu(launch_validate(m->keys, m->nnz_dev, m->nnz, limit, flag, s)));
+    int h = 0;
+    SPC_TRY(cu(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s)));
+    SPC_TRY(cu(cudaStreamSynchronize(s)));
+    return h ? SPC_ERR_UNSORTED : SPC_OK;
+}
+
+// SPC_VALIDATE=1: the filter keys too -- strictly increasing, below c_out*c_in*prod(ksize)
+// (an unsorted, duplicated or out-of-range filter would otherwise index the filter tables out of
+// bounds). Synchronises the stream.
+spc_status_t maybe_validate_filter(const spc_filter_t* w, int* flag, cudaStream_t s) {
+    if (!flag || w->nnz == 0) return SPC_OK;
+    uint64_t kv = 1;
+    for (int d = 0; d < w->ndim; ++d) kv *= (uint64_t)w->ksize[d];
+    const uint64_t limit = (uint64_t)w->c_out * (uint64_t)w->c_in * kv;
+    SPC_TRY(cu(cudaMemsetAsync(flag, 0, sizeof(int), s)));
+    SPC_TRY(cu(launch_validate(w->keys, nullptr, w->nnz, limit, flag, s)));
     int h = 0;
     SPC_TRY(cu(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s)));
     SPC_TRY(cu(cudaStreamSynchronize(s)));
@@ -195,7 +212,7 @@ FwdWs carve_fwd(Carver& c, const Geo& gx, const Geo& gy, const KGeo& kg, const F
         ws.g.dinfo = c.take<int>((size_t)3 * gp->KV + 1);
     }
     const int64_t nseg = gy.B * gy.C;
-    const size_t KXY = (size_t)kg.kx * kg.ky;
+    const size_t KXY = (size_t)kg.kw * kg.kx * kg.ky;
     ws.xrow = c.take<uint32_t>((size_t)(gx.B * gx.C * gx.R + 1));
     ws.meta2 = c.take<int2>((size_t)w->nnz);
     ws.val2 = c.take<float>((size_t)w->nnz);
@@ -241,7 +258,7 @@ FwdWs carve_fwd(Carver& c, const Geo& gx, const Geo& gy, const KGeo& kg, const F
         a.tile_sel = c.take<uint32_t>(nt);
         a.tile_off = c.take<uint64_t>(nt);
     }
-    const size_t PK = (size_t)w->c_in * kg.kx;
+    const size_t PK = (size_t)w->c_in * kg.kw * kg.kx;
     a.rnd = c.take<int2>((size_t)t.n_ocg * t.nwg_max + 1);
     a.roff = c.take<int>((size_t)t.n_ocg * (t.ocg * PK + 1));
     a.guard = c.take<int>(1);
@@ -306,6 +323,7 @@ spc_status_t conv_bwd_impl(const spc_map_t* x, const spc_filter_t* w, const spc_
     if (validate_env()) {
         SPC_TRY(maybe_validate(x, ws.flag, s));
         SPC_TRY(maybe_validate(y, ws.flag, s));
+        SPC_TRY(maybe_validate_filter(w, ws.flag, s));
     }
     if (dw64) ws.dw_acc = dw64;
     if (db64) ws.db_acc = db64;
@@ -383,13 +401,13 @@ PoolWs carve_pool(Carver& c, const Geo& g, const PoolPlan& p) {
 spc_status_t pool_plan(const spc_map_t* x, const int64_t* stride, Geo* g, PoolPlan* p) {
     SPC_TRY(check_map(x));
     if (!stride) return SPC_ERR_INVALID_ARG;
-    int64_t s3[3] = {1, 1, 1};
+    int64_t s4[4] = {1, 1, 1, 1};
     for (int i = 0; i < x->ndim; ++i) {
         if (stride[i] < 1 || stride[i] > (1 << 20)) return SPC_ERR_SHAPE;
-        s3[3 - x->ndim + i] = stride[i];
+        s4[4 - x->ndim + i] = stride[i];
     }
     *g = geo_of(x, x->channels);
-    *p = plan_pool(*g, (int)s3[0], (int)s3[1], (int)s3[2]);
+    *p = plan_pool(*g, (int)s4[0], (int)s4[1], (int)s4[2], (int)s4[3]);
     return SPC_OK;
 }
 
@@ -462,7 +480,10 @@ spc_status_t sparse_conv_fwd_ex(const spc_map_t* x, const spc_filter_t* w, const
     if (!workspace || workspace_bytes < m.used) return SPC_ERR_WORKSPACE;
     Carver c(workspace);
     FwdWs ws = carve_fwd(c, gx, gy, kg, t, w, attn, gpp);
-    if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
+    if (validate_env()) {
+        SPC_TRY(maybe_validate(x, ws.flag, s));
+        SPC_TRY(maybe_validate_filter(w, ws.flag, s));
+    }
     if (!use_gemm) {   // row index with the value guard fused (the scatter kernel reads the guard)
         SPC_TRY(cu(cudaMemsetAsync(ws.a.guard, 0, sizeof(int), s)));
         SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s, x->values, ws.a.guard)));
@@ -552,7 +573,10 @@ spc_status_t sparse_conv_fwd_pass(const spc_map_t* x, const spc_filter_t* w, con
     if (!workspace || workspace_bytes < m.used) return SPC_ERR_WORKSPACE;
     Carver c(workspace);
     FwdWs ws = carve_fwd(c, gx, gyp, kg, t, w, attn, nullptr);
-    if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
+    if (validate_env()) {
+        SPC_TRY(maybe_validate(x, ws.flag, s));
+        SPC_TRY(maybe_validate_filter(w, ws.flag, s));
+    }
     SPC_TRY(cu(cudaMemsetAsync(ws.a.guard, 0, sizeof(int), s)));
     SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s, x->values, ws.a.guard)));
     ws.a.guard_done = 1;

@@ -28,7 +28,7 @@ static int bwd_ctas_per_sm() {
 }
 
 static size_t bwd_smem(const KGeo& kg, int c_in, int TX, int TY, int ZR, int ocg, int64_t nwg, int threads) {
-    const size_t g = (size_t)ocg * (TX + 2 * kg.hx) * (TY + 2 * kg.hy) * ZR * sizeof(float);
+    const size_t g = (size_t)ocg * (1 + 2 * kg.hw) * (TX + 2 * kg.hx) * (TY + 2 * kg.hy) * ZR * sizeof(float);
     const size_t w = (size_t)nwg * (sizeof(int) + sizeof(float) + sizeof(double));
     const size_t idx = (size_t)(c_in + 1) * sizeof(int) * 2 + (size_t)c_in * TX * 2 * sizeof(uint32_t);
     const size_t stage = (size_t)(threads / 32) * 32 * (sizeof(int) + sizeof(float));
@@ -69,7 +69,7 @@ BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int nw_total) {
         t.nwg_max = (int)nwg;
         t.smem = bwd_smem(kg, c_in, bx, by, ZR, ocg, nwg, threads);
         t.threads = threads;
-        const int64_t items = gx.B * (int64_t)t.ntx * t.nty;
+        const int64_t items = gx.B * gx.W * (int64_t)t.ntx * t.nty;
         int64_t grid = (148 * cps + t.n_ocg - 1) / t.n_ocg;
         grid = std::max<int64_t>(1, std::min<int64_t>(grid, items));
         t.grid = (int)grid;
@@ -105,10 +105,13 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
     const int c_in = (int)gx.C, c_out = (int)gy.C;
     const int oc0 = blockIdx.y * t.ocg;
     const int nocl = min(t.ocg, c_out - oc0);
-    const int HX = t.TX + 2 * kg.hx, HY = t.TY + 2 * kg.hy;
+    // G slab of one output-channel slice: HW w-planes x HX x-rows x HY y-rows x ZR (rank-4 maps:
+    // the tile is one w-plane, its halo the 2*hw neighbouring planes; HW = 1 for rank <= 3)
+    const int HW = 1 + 2 * kg.hw, HX = t.TX + 2 * kg.hx, HY = t.TY + 2 * kg.hy;
     const int ZR = gx.Z + 2 * kg.hz;
     const int HXY = HX * HY;
-    const int gsize = t.ocg * HXY * ZR;
+    const int slice = HW * HXY * ZR;
+    const int gsize = t.ocg * slice;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
 
     // ---- shared layout: G | dwp | wdel | wv | lbase | cpre | rng | stage
@@ -148,18 +151,21 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
         for (int j = threadIdx.x; j < n; j += blockDim.x) {
             const int2 m = wmeta[t0 + j];
             // g at uid = id - (fid - centre): G index = ebase - wdel
-            wdel[lbase[ic] + j] = (off_x(m.y) * HY + off_y(m.y)) * ZR + off_z(m.y) - (m.x - oc0) * HXY * ZR;
+            wdel[lbase[ic] + j] = ((meta_ow(m.x) * HX + off_x(m.y)) * HY + off_y(m.y)) * ZR + off_z(m.y) -
+                                  (meta_oc(m.x) - oc0) * slice;
             wv[lbase[ic] + j] = wval[t0 + j];
         }
     }
     for (int i = threadIdx.x; i < nwg; i += blockDim.x) dwp[i] = 0.0;
     for (int i = threadIdx.x; i < gsize; i += blockDim.x) G[i] = 0.0f;
-    const int eb_safe = (kg.hx * HY + kg.hy) * ZR + kg.hz;   // an in-range G index for idle lanes
+    const int eb_safe = ((kg.hw * HX + kg.hx) * HY + kg.hy) * ZR + kg.hz;   // an in-range G index for idle lanes
 
-    const int64_t items = gx.B * (int64_t)t.ntx * t.nty;
+    const int64_t items = gx.B * gx.W * (int64_t)t.ntx * t.nty;
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-        const int64_t b = item / ((int64_t)t.ntx * t.nty);
-        const int tile = (int)(item - b * (int64_t)t.ntx * t.nty);
+        const int64_t bw = item / ((int64_t)t.ntx * t.nty);   // (b, w-plane)
+        const int64_t b = bw / gx.W;
+        const int wp = (int)(bw - b * gx.W);
+        const int tile = (int)(item - bw * (int64_t)t.ntx * t.nty);
         const int x0 = (tile % t.ntx) * t.TX, y0 = (tile / t.ntx) * t.TY;
         const int xe = min(x0 + t.TX, gx.X), ye = min(y0 + t.TY, gx.Y);
         __syncthreads();
@@ -169,7 +175,7 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
             const int ic = q / t.TX, xi = q - (q / t.TX) * t.TX;
             uint32_t lo = 0, hi = 0;
             if (x0 + xi < xe) {
-                const int64_t r0 = ((b * c_in + ic) * gx.X + x0 + xi) * (int64_t)gx.Y + y0;
+                const int64_t r0 = (((b * c_in + ic) * gx.W + wp) * gx.X + x0 + xi) * (int64_t)gx.Y + y0;
                 lo = xrow[r0];
                 hi = xrow[r0 + (ye - y0)];
             }
@@ -181,17 +187,25 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
         const int hylo = max(0, y0 - kg.hy), hyhi = min(gy.Y, y0 + t.TY + kg.hy);
         const float invZ = 1.0f / (float)gy.Z;
         const float invXZ = 1.0f / (float)gx.Z;
-        const float invHX = 1.0f / (float)HX;
+        const int HWX = HW * HX;
+        // halo row r = (ocl, hw-plane, hx-row) -> its first y-row in the output map (or -1)
+        auto halo_row = [&](int r, int& gbase) -> int64_t {
+            const int ocl = r / HWX, hr = r - ocl * HWX;
+            const int hwi = hr / HX, hxr = hr - hwi * HX;
+            const int ws = wp - kg.hw + hwi, xs = x0 - kg.hx + hxr;
+            gbase = (((ocl * HW + hwi) * HX + hxr) * HY + (hylo - (y0 - kg.hy))) * ZR + kg.hz;
+            if (ws < 0 || ws >= gy.W || xs < 0 || xs >= gy.X || hylo >= hyhi) return -1;
+            return (((b * c_out + oc0 + ocl) * gy.W + ws) * gy.X + xs) * (int64_t)gy.Y + hylo;
+        };
         // the warp's rows r = warp + k * nwarps: lane k loads row k's bounds (one latency for all)
-        for (int r0 = warp; r0 < nocl * HX; r0 += 32 * nwarps) {
+        for (int r0 = warp; r0 < nocl * HWX; r0 += 32 * nwarps) {
             uint32_t be0 = 0, be1 = 0;
             {
                 const int r = r0 + lane * nwarps;
-                if (r < nocl * HX) {
-                    const int ocl = __float2int_rz(((float)r + 0.5f) * invHX);   // r / HX (small integers)
-                    const int xs = x0 - kg.hx + (r - ocl * HX);
-                    if (xs >= 0 && xs < gy.X && hylo < hyhi) {
-                        const int64_t row = ((b * c_out + oc0 + ocl) * gy.X + xs) * (int64_t)gy.Y + hylo;
+                if (r < nocl * HWX) {
+                    int gb;
+                    const int64_t row = halo_row(r, gb);
+                    if (row >= 0) {
                         be0 = yrow[row];
                         be1 = yrow[row + (hyhi - hylo)];
                     }
@@ -206,7 +220,7 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
             st_eb[lane] = (int)(incl - len);   // cum_k
             st_eb[32 + lane] = (int)be0;       // e0_k
             __syncwarp();
-            const int nrows = min(32, (nocl * HX - r0 + nwarps - 1) / nwarps);
+            const int nrows = min(32, (nocl * HWX - r0 + nwarps - 1) / nwarps);
             for (uint32_t base = 0; base < wtot; base += 256) {
                 uint64_t kk[8];
                 float dv[8];
@@ -231,11 +245,8 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
                 for (int j = 0; j < 8; ++j) {
                     if (rk[j] < 0) continue;
                     const int r = r0 + rk[j] * nwarps;
-                    const int ocl = __float2int_rz(((float)r + 0.5f) * invHX);
-                    const int hxr = r - ocl * HX;
-                    const int xs = x0 - kg.hx + hxr;
-                    const int64_t row = ((b * c_out + oc0 + ocl) * gy.X + xs) * (int64_t)gy.Y + hylo;
-                    const int gbase = (ocl * HXY + hxr * HY + (hylo - (y0 - kg.hy))) * ZR + kg.hz;
+                    int gbase;
+                    const int64_t row = halo_row(r, gbase);
                     const uint32_t L = (uint32_t)(kk[j] - (uint64_t)row * (uint64_t)gy.Z);
                     uint32_t yr = __float2uint_rz(__uint2float_rz(L) * invZ);
                     if (yr * (uint32_t)gy.Z > L) --yr;
@@ -299,11 +310,11 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
             int eb = eb_safe;
             const float v = cur.v;
             if (e >= 0) {
-                const int64_t r0 = ((b * c_in + ic) * gx.X + x0 + cur.xi) * (int64_t)gx.Y + y0;
+                const int64_t r0 = (((b * c_in + ic) * gx.W + wp) * gx.X + x0 + cur.xi) * (int64_t)gx.Y + y0;
                 const uint32_t L = (uint32_t)(cur.key - (uint64_t)r0 * (uint64_t)gx.Z);
                 const uint32_t yl = div_small(L, (uint32_t)gx.Z, invXZ);   // L < TY * Z
                 const int z = (int)(L - yl * (uint32_t)gx.Z);
-                eb = ((cur.xi + kg.hx) * HY + (int)yl + kg.hy) * ZR + z + kg.hz;
+                eb = ((kg.hw * HX + cur.xi + kg.hx) * HY + (int)yl + kg.hy) * ZR + z + kg.hz;
             }
             __syncwarp();
             st_eb[lane] = eb * (int)sizeof(float);   // byte offsets into G

@@ -53,7 +53,7 @@ FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_
     FwdTile t{};
     const int cz = ((kg.hz + 3) / 4) * 4;                         // column of z = 0 (16-byte aligned rows)
     const int ZR = (int)r4((size_t)cz + gy.Z + kg.hz);
-    const int PK = c_in * kg.kx;
+    const int PK = c_in * kg.kw * kg.kx;   // items (ic, input plane offset (dw, dx))
     auto nwg = [&](int ocg) { return std::min<int64_t>(nw_total, (int64_t)ocg * c_in * kg.KV); };
     // round records live in shared memory when small; large filter banks (e.g. 32 x 32 x 27) are
     // read through L1 instead of being copied into every CTA
@@ -115,12 +115,13 @@ __global__ void fwd_rounds_kernel(KGeo kg, int c_in, int c_out, FwdTile t, const
     for (int q0 = 0; q0 < NQ; q0 += blockDim.x) {
         const int q = q0 + threadIdx.x;            // q = ocl*PK + pk
         const int ocl = q / PK, pk = q - (q / PK) * PK;
-        const int ic = pk / kg.kx, dx = pk - (pk / kg.kx) * kg.kx;
+        const int KWX = kg.kw * kg.kx;                 // plane offsets (dw, dx) per input channel
+        const int ic = pk / KWX, dx = pk - (pk / KWX) * KWX;
         const int oc = oc0 + ocl;
         int n = 0;
         if (q < NQ && ocl < nocl)
             for (int dy = 0; dy < kg.ky; ++dy) {
-                const int g = (ic * kg.kx + dx) * kg.ky + dy;
+                const int g = (ic * KWX + dx) * kg.ky + dy;
                 n += off2[g * (c_out + 1) + oc + 1] - off2[g * (c_out + 1) + oc];
             }
         int all;
@@ -130,7 +131,7 @@ __global__ void fwd_rounds_kernel(KGeo kg, int c_in, int c_out, FwdTile t, const
             RO[q] = f;
             if (ocl < nocl)
                 for (int dy = 0; dy < kg.ky; ++dy) {
-                    const int g = (ic * kg.kx + dx) * kg.ky + dy;
+                    const int g = (ic * KWX + dx) * kg.ky + dy;
                     const int lo = off2[g * (c_out + 1) + oc], hi = off2[g * (c_out + 1) + oc + 1];
                     for (int j = lo; j < hi; ++j) {
                         const float wv = val2[j];
@@ -184,40 +185,60 @@ __device__ __forceinline__ void epi_hist_rows(const float* S, float bv, int nyr,
 // Candidate epilogue of one output channel (warp = channel, no block barrier): "get non-zero
 // entries" (structural support R3), "add bias", and every support entry whose score
 // reaches the segment's threshold tlow is appended in key order to the tile's candidate run.
-// Row by row, 128 voxels per step: lane l holds z = z0 + l + 32u (u = 0..3), so each of the four
-// 32-voxel groups is one ballot. Candidates are ranked into a per-warp shared-memory buffer
-// (branch-free: non-candidates store to a private dummy slot) that is flushed to the run with
-// coalesced stores. Returns the run length, the support size and the largest candidate score.
-constexpr int kCandBuf = 160;   // per-warp buffer entries (+ 32 dummy slots), in the staging area
+// Row by row, 128 voxels per step: lane l holds z = z0 + 4l .. z0 + 4l + 3 (one 16-byte load when
+// Z % 4 == 0), one warp scan of the per-lane candidate counts ranks them, and only the lanes
+// holding candidates (about 6 % of the voxels) run the store loop -- into a per-warp shared-memory
+// buffer that is flushed to the run with coalesced stores. Returns the run length, the support
+// size and the largest candidate score.
+constexpr int kCandBuf = 160;   // per-warp buffer entries, in the staging area
 template <int MODE>
 __device__ __forceinline__ void epi_cand(const float* S, int nyr, int Z, int ZR, float bv, uint32_t tlow,
                                          uint32_t marker, uint32_t pbase, uint32_t* __restrict__ cpos,
                                          float* __restrict__ cval, uint32_t* bufp, float* bufv, uint32_t& n_out,
                                          uint32_t& sup_out, uint32_t& max_out) {
     const int lane = threadIdx.x & 31;
-    const uint32_t lt = (1u << lane) - 1u;
-    const uint32_t dummy = kCandBuf + (uint32_t)lane;
+    const bool vec = (Z & 3) == 0;
     uint32_t nb = 0, nf = 0, sup = 0, mx = 0;   // buffered, flushed
     for (int r = 0; r < nyr; ++r) {
         const float* row = S + r * ZR;
         const uint32_t prow = pbase + (uint32_t)(r * Z);
         for (int z0 = 0; z0 < Z; z0 += 128) {
+            const int z = z0 + 4 * lane;
+            float v[4];
+            if (vec) {
+                if (z < Z) {
+                    const float4 q = *reinterpret_cast<const float4*>(row + z);
+                    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) v[u] = __uint_as_float(marker);
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = z + u < Z ? row[z + u] : __uint_as_float(marker);
+            }
+            uint32_t f = 0;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int z = z0 + 32 * u + lane;
-                const float raw = z < Z ? row[z] : __uint_as_float(marker);
-                const bool pres = __float_as_uint(raw) != marker;
-                const float val = raw + bv;
-                const uint32_t sc = MODE == SPC_ATTN_NONE ? 0u : score_bits(__float_as_uint(val), MODE);
+                const bool pres = __float_as_uint(v[u]) != marker;
+                v[u] += bv;
+                const uint32_t sc = MODE == SPC_ATTN_NONE ? 0u : score_bits(__float_as_uint(v[u]), MODE);
                 const bool c = pres && sc >= tlow;
+                f |= (uint32_t)c << u;
                 sup += pres ? 1u : 0u;
                 mx = c ? max(mx, sc) : mx;
-                const uint32_t bal = __ballot_sync(kFull, c);
-                const uint32_t slot = c ? nb + (uint32_t)__popc(bal & lt) : dummy;
-                bufp[slot] = prow + (uint32_t)z;
-                bufv[slot] = val;
-                nb += (uint32_t)__popc(bal);
             }
+            const uint32_t cnt = (uint32_t)__popc(f);
+            const uint32_t incl = warp_incl_scan(cnt);
+            uint32_t o = nb + incl - cnt;
+            while (f) {   // the lane's candidates, in z order
+                const int u = __ffs(f) - 1;
+                f &= f - 1;
+                bufp[o] = prow + (uint32_t)(z + u);
+                bufv[o] = v[u];
+                ++o;
+            }
+            nb += __shfl_sync(kFull, incl, 31);
             if (nb > kCandBuf - 128) {   // flush: coalesced copy of the buffer to the run
                 __syncwarp();
                 for (uint32_t i = lane; i < nb; i += 32) {
@@ -226,11 +247,10 @@ __device__ __forceinline__ void epi_cand(const float* S, int nyr, int Z, int ZR,
                 }
                 nf += nb;
                 nb = 0;
-                __syncwarp();
             }
+            __syncwarp();
         }
     }
-    __syncwarp();
     for (uint32_t i = lane; i < nb; i += 32) {
         cpos[nf + i] = bufp[i];
         cval[nf + i] = bufv[i];
@@ -361,7 +381,8 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
     const int c_in = (int)gx.C, c_out = (int)gy.C;
     const int Z = gy.Z, ZR = t.ZR;
     const int ty = tin % t.nty;
-    const int x = tin / t.nty;
+    const int P = tin / t.nty;                       // output plane (w, x): P = w*X + x
+    const int x = P % gy.X, wpl = P / gy.X;
     const int64_t b = a.b0 + bl;                        // global sample (input rows)
     const int oc0 = blockIdx.y * t.ocg;
     const int nocl = min(t.ocg, c_out - oc0);
@@ -409,9 +430,11 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
     auto item_bounds = [&](int q, uint32_t& e0, uint32_t& n, uint32_t& rb) {
         e0 = n = rb = 0u;
         if (q >= PK) return;
-        const int ic = q / kg.kx, xs = x + (q - ic * kg.kx) - kg.hx;
-        if (xs >= 0 && xs < gx.X) {
-            const int64_t row = ((b * c_in + ic) * gx.X + xs) * (int64_t)gx.Y + ylo;
+        const int KWX = kg.kw * kg.kx;
+        const int ic = q / KWX, it = q - ic * KWX;
+        const int ws = wpl + it / kg.kx - kg.hw, xs = x + it % kg.kx - kg.hx;   // input plane (w, x)
+        if (ws >= 0 && ws < gx.W && xs >= 0 && xs < gx.X) {
+            const int64_t row = (((b * c_in + ic) * gx.W + ws) * gx.X + xs) * (int64_t)gx.Y + ylo;
             e0 = a.xrow[row];
             n = a.xrow[row + (yhi - ylo)] - e0;
             rb = (uint32_t)((uint64_t)row * (uint64_t)Z);   // low word of the row's first key
@@ -552,13 +575,13 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
         const float bv = a.bias ? __ldg(&a.bias[oc]) : 0.0f;
         const float* S = acc + warp * SL + 2 * kg.hy * ZR + t.cz;
         const uint32_t tl = EPI == kEpiRedo ? 0u : a.tlow[s];
-        const uint32_t pbase = (uint32_t)(((int64_t)x * gy.Y + y0) * Z);
+        const uint32_t pbase = (uint32_t)(((int64_t)P * gy.Y + y0) * Z);
         uint32_t* cp = a.cpos + s * gy.V + pbase;
         float* cv = a.cval + s * gy.V + pbase;
         uint32_t n, sup, mx;
-        static_assert(kFwdWarps * (kCandBuf + 32) <= kStageCap, "candidate buffers live in the staging area");
-        uint32_t* bp = spos + warp * (kCandBuf + 32);
-        float* bvv = sval + warp * (kCandBuf + 32);
+        static_assert(kFwdWarps * kCandBuf <= kStageCap, "candidate buffers live in the staging area");
+        uint32_t* bp = spos + warp * kCandBuf;
+        float* bvv = sval + warp * kCandBuf;
         if (a.attn == SPC_ATTN_MAGNITUDE)
             epi_cand<SPC_ATTN_MAGNITUDE>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, bvv, n, sup, mx);
         else if (a.attn == SPC_ATTN_RAW)
@@ -1050,7 +1073,7 @@ cudaError_t launch_seg_scan_u64(const uint64_t* in, uint64_t* out, int64_t n, in
 }
 
 void plan_fwd_sampling(const Geo& gy, const FwdTile& t, int attn, FwdArgs* a) {
-    a->ntile = (int)(gy.X * t.nty);
+    a->ntile = (int)((int64_t)gy.W * gy.X * t.nty);
     // every sp_period-th tile of a segment: the largest prime <= 31 that leaves at least 8 sampled
     // tiles and does not divide the band count (so that the sampled tiles cycle through the
     // bands); no sampling for small segments or without attention

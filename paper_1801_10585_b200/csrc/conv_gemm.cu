@@ -39,6 +39,7 @@ GemmPlan plan_gemm(const Geo& gx, const Geo& gy, const KGeo& kg) {
     const int c_in = (int)gx.C, c_out = (int)gy.C;
     if (c_in < 1 || c_in > 32 || c_out < 1 || c_out > 64) return g;   // masks are u32 over ic; N <= 64
     if (gx.B * gx.C >= (1ll << 32)) return g;                          // 32-bit segment ids in densify
+    if (gx.W != 1 || kg.kw != 1) return g;                               // rank <= 3 only (variant S covers rank 4)
     g.Kp = (c_in + 7) & ~7;
     g.Np = (c_out + 15) & ~15;
     g.KV = kg.KV;

@@ -114,11 +114,14 @@ __device__ __forceinline__ void filter_runs(int64_t nw, int nq, G grp, int* __re
     __syncthreads();
     for (int64_t j = threadIdx.x; j < nw; j += blockDim.x) {
         const int q = grp(j);
+        if (q < 0 || q >= nq) continue;   // out-of-range filter key (rejected under SPC_VALIDATE)
         if (j == 0 || grp(j - 1) != q) run_start[q] = (int)j;
         if (j + 1 == nw || grp(j + 1) != q) run_len[q] = (int)j + 1;   // the run's end for now
     }
     __syncthreads();
-    for (int q = threadIdx.x; q < nq; q += blockDim.x) run_len[q] -= run_start[q];
+    // (unsorted or duplicated keys break the runs: clamped so that no write leaves the tables)
+    for (int q = threadIdx.x; q < nq; q += blockDim.x)
+        run_len[q] = max(0, min(run_len[q] - run_start[q], (int)nw - run_start[q]));
     __syncthreads();
 }
 
@@ -157,12 +160,15 @@ __global__ void filter_table_kernel(KGeo kg, int c_in, int c_out, const uint64_t
         const uint64_t key = wk[j];
         const int p = (int)(key / (uint64_t)kg.KV);
         const int dlin = (int)(key - (uint64_t)p * (uint64_t)kg.KV);
+        if (p >= c_in * c_out) continue;   // out-of-range key (rejected under SPC_VALIDATE)
         const int oc = p / c_in, ic = p - (p / c_in) * c_in;
         const int dst = off[ic * (c_out + 1) + oc] + (int)(j - run_start[p]);
+        if (dst < 0 || dst >= nw) continue;
         const int dz = dlin % kg.kz;
         const int dy = (dlin / kg.kz) % kg.ky;
-        const int dx = dlin / (kg.kz * kg.ky);
-        meta[dst] = make_int2(oc, pack_off(dx - kg.hx, dy - kg.hy, dz - kg.hz));
+        const int dx = (dlin / (kg.kz * kg.ky)) % kg.kx;
+        const int dw = dlin / (kg.kz * kg.ky * kg.kx);
+        meta[dst] = make_int2(pack_oc_ow(oc, dw - kg.hw), pack_off(dx - kg.hx, dy - kg.hy, dz - kg.hz));
         val[dst] = wv[j];
         src[dst] = (int)j;
     }
@@ -184,7 +190,7 @@ __global__ void filter_table_fwd_kernel(KGeo kg, int c_in, int c_out, const uint
                                         float* __restrict__ val2, int* __restrict__ off2, int* __restrict__ run_start,
                                         int* __restrict__ run_len) {
     __shared__ int sm[33];
-    const int KXY = kg.kx * kg.ky;
+    const int KXY = kg.kw * kg.kx * kg.ky;
     const int nq = c_in * KXY * c_out;   // q = (ic*KXY + dxdy)*c_out + oc
     auto grp = [&](int64_t j) {   // q of entry j: key = ((oc*c_in + ic)*KV + dxdy*kz + dz)
         const uint64_t k = wk[j];
@@ -210,7 +216,7 @@ __global__ void filter_table_fwd_kernel(KGeo kg, int c_in, int c_out, const uint
     for (int q = threadIdx.x; q < nq; q += blockDim.x) {
         const int oc = q % c_out, g = q / c_out;
         const int dst = off2[g * (c_out + 1) + oc];
-        for (int i = 0; i < run_len[q]; ++i) {
+        for (int i = 0; i < run_len[q] && dst + i < nw; ++i) {
             const int j = run_start[q] + i;
             const int dz = (int)(wk[j] % (uint64_t)kg.kz);
             meta2[dst + i] = make_int2(oc, dz - kg.hz);
@@ -221,7 +227,7 @@ __global__ void filter_table_fwd_kernel(KGeo kg, int c_in, int c_out, const uint
 
 cudaError_t launch_filter_table_fwd(const KGeo& kg, int c_in, int c_out, const uint64_t* wkeys, const float* wvals,
                                     int64_t nw, int2* meta2, float* val2, int* off2, int* scratch, cudaStream_t s) {
-    const size_t nq = (size_t)c_in * kg.kx * kg.ky * c_out;
+    const size_t nq = (size_t)c_in * kg.kw * kg.kx * kg.ky * c_out;
     { SPC_PHASE("filter_table", s, 1); filter_table_fwd_kernel<<<1, 1024, 0, s>>>(kg, c_in, c_out, wkeys, wvals, nw, meta2, val2, off2, scratch, scratch + nq); }
     return cudaGetLastError();
 }

@@ -110,15 +110,16 @@ constexpr int kPoolZChunk = 512;
 constexpr int kTileThreads = 256;
 constexpr int kTileCells = 4096;
 
-PoolPlan plan_pool(const Geo& g, int sx, int sy, int sz) {
+PoolPlan plan_pool(const Geo& g, int sw, int sx, int sy, int sz) {
     PoolPlan p{};
-    p.sx = sx; p.sy = sy; p.sz = sz;
+    p.sw = sw; p.sx = sx; p.sy = sy; p.sz = sz;
+    p.PW = (g.W + sw - 1) / sw;
     p.PX = (g.X + sx - 1) / sx;
     p.PY = (g.Y + sy - 1) / sy;
     p.PZ = (g.Z + sz - 1) / sz;
     p.zchunk = p.PZ < kPoolZChunk ? p.PZ : kPoolZChunk;
     p.nzc = (p.PZ + p.zchunk - 1) / p.zchunk;
-    p.items = g.B * g.C * (int64_t)p.PX * p.PY * p.nzc;
+    p.items = g.B * g.C * (int64_t)p.PW * p.PX * p.PY * p.nzc;
     if (p.PZ <= kTileCells) {
         p.nyb = std::max(1, std::min(p.PY, kTileCells / p.PZ));
         if ((uint64_t)p.nyb * sy * (uint64_t)g.Z < (1ull << 31)) {
@@ -127,7 +128,7 @@ PoolPlan plan_pool(const Geo& g, int sx, int sy, int sz) {
             p.mZ = ~0u / (uint32_t)g.Z;
             p.msy = ~0u / (uint32_t)sy;
             p.msz = ~0u / (uint32_t)sz;
-            p.items = g.B * g.C * (int64_t)p.PX * p.nyt;
+            p.items = g.B * g.C * (int64_t)p.PW * p.PX * p.nyt;
         }
     }
     return p;
@@ -144,13 +145,13 @@ __device__ __forceinline__ uint32_t udiv(uint32_t x, uint32_t d, uint32_t m) {
 template <bool LOADV, typename F>
 __device__ __forceinline__ void pool_tile_members(const Geo& g, const PoolPlan& p, const uint64_t* __restrict__ keys,
                                                   const float* __restrict__ vals,
-                                                  const uint32_t* __restrict__ row_ptr, int64_t seg, int px, int ya,
-                                                  int yb, F f) {
+                                                  const uint32_t* __restrict__ row_ptr, int64_t seg, int pw, int px,
+                                                  int ya, int yb, F f) {
     const uint32_t Z = (uint32_t)g.Z;
-    for (int dx = 0; dx < p.sx; ++dx) {
-        const int x = px * p.sx + dx;
-        if (x >= g.X) break;
-        const int64_t row0 = (seg * g.X + x) * (int64_t)g.Y + ya;
+    for (int dwx = 0; dwx < p.sw * p.sx; ++dwx) {   // input planes (w, x) of the pooled plane
+        const int w = pw * p.sw + dwx / p.sx, x = px * p.sx + dwx % p.sx;
+        if (w >= g.W || x >= g.X) continue;
+        const int64_t row0 = ((seg * g.W + w) * g.X + x) * (int64_t)g.Y + ya;
         const uint32_t e0 = row_ptr[row0], e1 = row_ptr[row0 + (yb - ya)];
         const uint64_t kb = (uint64_t)row0 * Z;
         for (uint32_t e = e0 + threadIdx.x; e < e1; e += 4 * kTileThreads) {
@@ -177,14 +178,16 @@ __device__ __forceinline__ void pool_tile_members(const Geo& g, const PoolPlan& 
 
 struct PoolTileId {
     int64_t seg;
-    int px, py0, npy, ya, yb;
+    int pw, px, py0, npy, ya, yb;
 };
 __device__ __forceinline__ PoolTileId pool_tile_id(const Geo& g, const PoolPlan& p, int64_t tile) {
     PoolTileId t;
     const int yt = (int)(tile % p.nyt);
-    const int64_t r = tile / p.nyt;
+    int64_t r = tile / p.nyt;
     t.px = (int)(r % p.PX);
-    t.seg = r / p.PX;
+    r /= p.PX;
+    t.pw = (int)(r % p.PW);
+    t.seg = r / p.PW;
     t.py0 = yt * p.nyb;
     t.npy = min(p.nyb, p.PY - t.py0);
     t.ya = t.py0 * p.sy;
@@ -201,7 +204,7 @@ pool_tile_count_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, con
     const PoolTileId t = pool_tile_id(g, p, blockIdx.x);
     if (threadIdx.x < kTileCells / 32) occ[threadIdx.x] = 0u;
     __syncthreads();
-    pool_tile_members<false>(g, p, keys, nullptr, row_ptr, t.seg, t.px, t.ya, t.yb, [&](int cell, uint32_t, float) {
+    pool_tile_members<false>(g, p, keys, nullptr, row_ptr, t.seg, t.pw, t.px, t.ya, t.yb, [&](int cell, uint32_t, float) {
         atomicOr(&occ[cell >> 5], 1u << (cell & 31));
     });
     __syncthreads();
@@ -229,7 +232,7 @@ pool_tile_write_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, con
     for (int j = 0; j < kTileCells / 2 / kTileThreads; ++j) b4[tid + kTileThreads * j] = make_uint4(0u, 0u, 0u, 0u);
     if (tid < kTileCells / 32) occ[tid] = 0u;
     __syncthreads();
-    pool_tile_members<true>(g, p, keys, vals, row_ptr, t.seg, t.px, t.ya, t.yb, [&](int cell, uint32_t e, float v) {
+    pool_tile_members<true>(g, p, keys, vals, row_ptr, t.seg, t.pw, t.px, t.ya, t.yb, [&](int cell, uint32_t e, float v) {
         atomicMax(&best[cell], ((unsigned long long)orderable(v) << 32) | (unsigned long long)(~e));
         atomicOr(&occ[cell >> 5], 1u << (cell & 31));
     });
@@ -255,7 +258,7 @@ pool_tile_write_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, con
     }
     __syncthreads();
     const uint64_t o0 = item_off[blockIdx.x];
-    const uint64_t pbase = ((uint64_t)(t.seg * p.PX + t.px) * p.PY + t.py0) * (uint64_t)p.PZ;
+    const uint64_t pbase = ((uint64_t)((t.seg * p.PW + t.pw) * p.PX + t.px) * p.PY + t.py0) * (uint64_t)p.PZ;
     for (uint32_t q = tid; q < tot; q += kTileThreads) {
         const uint32_t cell = cells[q];
         const unsigned long long bst = best[cell];
@@ -287,7 +290,9 @@ pool_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, const float* _
     const int py = (int)(r % p.PY);
     r /= p.PY;
     const int px = (int)(r % p.PX);
-    const int64_t seg = r / p.PX;
+    r /= p.PX;
+    const int pw = (int)(r % p.PW);
+    const int64_t seg = r / p.PW;
     const int z0 = zc * p.zchunk;
     const int nz = min(p.zchunk, p.PZ - z0);
     for (int i = lane; i < nz; i += 32) {
@@ -295,12 +300,14 @@ pool_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, const float* _
         arg[i] = 0xffffffffu;
     }
     __syncwarp();
+    const int wa = pw * p.sw, wb = min(wa + p.sw, g.W);
     const int xa = px * p.sx, xb = min(xa + p.sx, g.X);
     const int ya = py * p.sy, yb = min(ya + p.sy, g.Y);
     // pass 1: max per cluster (or occupancy only when counting)
-    for (int x = xa; x < xb; ++x) {
+    for (int wx = 0; wx < (wb - wa) * (xb - xa); ++wx) {
+        const int w = wa + wx / (xb - xa), x = xa + wx % (xb - xa);
         for (int y = ya; y < yb; ++y) {
-            const int64_t row = (seg * g.X + x) * (int64_t)g.Y + y;
+            const int64_t row = ((seg * g.W + w) * g.X + x) * (int64_t)g.Y + y;
             const uint32_t e0 = row_ptr[row], e1 = row_ptr[row + 1];
             const uint64_t rowbase = (uint64_t)row * (uint64_t)g.Z;
             for (uint32_t e = e0 + lane; e < e1; e += 32) {
@@ -320,9 +327,10 @@ pool_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, const float* _
         return;
     }
     // pass 2: smallest entry index among the maxima (argmax, ties -> smaller key)
-    for (int x = xa; x < xb; ++x) {
+    for (int wx = 0; wx < (wb - wa) * (xb - xa); ++wx) {
+        const int w = wa + wx / (xb - xa), x = xa + wx % (xb - xa);
         for (int y = ya; y < yb; ++y) {
-            const int64_t row = (seg * g.X + x) * (int64_t)g.Y + y;
+            const int64_t row = ((seg * g.W + w) * g.X + x) * (int64_t)g.Y + y;
             const uint32_t e0 = row_ptr[row], e1 = row_ptr[row + 1];
             const uint64_t rowbase = (uint64_t)row * (uint64_t)g.Z;
             for (uint32_t e = e0 + lane; e < e1; e += 32) {
@@ -334,7 +342,7 @@ pool_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, const float* _
     }
     __syncwarp();
     uint64_t pos = item_off[item];
-    const uint64_t pbase = ((uint64_t)(seg * p.PX + px) * p.PY + py) * (uint64_t)p.PZ + z0;
+    const uint64_t pbase = ((uint64_t)((seg * p.PW + pw) * p.PX + px) * p.PY + py) * (uint64_t)p.PZ + z0;
     for (int i0 = 0; i0 < nz; i0 += 32) {
         const int i = i0 + lane;
         const bool occ = i < nz && best[i] != 0u;

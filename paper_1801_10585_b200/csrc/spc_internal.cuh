@@ -19,22 +19,29 @@ namespace spc {
 constexpr uint32_t kAbsent = 0x7fbfffffu;
 constexpr uint32_t kNegZero = 0x80000000u;   // accumulator marker of the -0 mode (conv_fwd)
 
-// Geometry of a feature map with its spatial dims padded to rank 3 (leading 1s):
-// key = seg*V + (x*Y + y)*Z + z, seg = b*C + c. A "row" is (seg, x, y): the Z consecutive
-// keys of the last spatial dimension.
+// Geometry of a feature map with its spatial dims padded to rank 4 (leading 1s):
+// key = seg*V + ((w*X + x)*Y + y)*Z + z, seg = b*C + c. A "row" is (seg, w, x, y): the Z
+// consecutive keys of the last spatial dimension; a "plane" is (w, x): P = w*X + x, so that rank
+// <= 3 maps (W = 1) and rank-4 maps share one row / plane layout.
 struct Geo {
     int64_t B, C;
-    int X, Y, Z;
-    int64_t V;   // X*Y*Z
-    int64_t R;   // rows per segment = X*Y
+    int W, X, Y, Z;
+    int64_t V;   // W*X*Y*Z
+    int64_t R;   // rows per segment = W*X*Y
 };
 
-// Filter geometry padded to rank 3; h = ksize/2 (centre).
+// Filter geometry padded to rank 4; h = ksize/2 (centre).
 struct KGeo {
-    int kx, ky, kz;
-    int hx, hy, hz;
+    int kw, kx, ky, kz;
+    int hw, hx, hy, hz;
     int KV;
 };
+
+// Filter table meta.x of the backward: the output channel (low 21 bits) and the w-offset
+// ow + 512 (bits 21..30); meta.y: pack_off(ox, oy, oz).
+__host__ __device__ inline int pack_oc_ow(int oc, int ow) { return oc | ((ow + 512) << 21); }
+__device__ __forceinline__ int meta_oc(int m) { return m & 0x1fffff; }
+__device__ __forceinline__ int meta_ow(int m) { return ((m >> 21) & 1023) - 512; }
 
 // Packed signed offset o = delta - centre per dim, 10 bits each (|o| < 512).
 __host__ __device__ inline int pack_off(int ox, int oy, int oz) {
@@ -284,8 +291,8 @@ cudaError_t launch_relu(const uint64_t* keys, const float* vals, const int64_t* 
                         uint32_t* chunk_cnt, uint64_t* chunk_off, uint64_t* scan_tmp,
                         uint64_t* out_keys, float* out_vals, int64_t* out_src, int64_t* out_nnz, cudaStream_t s);
 struct PoolPlan {
-    int sx, sy, sz;
-    int PX, PY, PZ;       // pooled dims
+    int sw, sx, sy, sz;
+    int PW, PX, PY, PZ;   // pooled dims
     int zchunk;           // pooled z positions per work item
     int nzc;              // z chunks per pooled row
     int64_t items;        // work items: B*C*PX*PY*nzc (row form) or the tiles (tile form)
@@ -293,7 +300,7 @@ struct PoolPlan {
     int nyb, nyt;         // pooled rows per tile, tiles per pooled plane
     uint32_t mZ, msy, msz;  // floor((2^32 - 1) / d) for d = Z, sy, sz (division by multiply-high)
 };
-PoolPlan plan_pool(const Geo& g, int sx, int sy, int sz);
+PoolPlan plan_pool(const Geo& g, int sw, int sx, int sy, int sz);
 cudaError_t launch_maxpool(const Geo& g, const PoolPlan& p, const uint64_t* keys, const float* vals,
                            const uint32_t* row_ptr, uint32_t* item_cnt, uint64_t* item_off, uint64_t* scan_tmp,
                            uint64_t* out_keys, float* out_vals, int64_t* out_arg, int64_t* out_nnz, cudaStream_t s);

@@ -70,7 +70,7 @@ def test_fwd_query_capacity_is_the_density_bound():
     rc, cap, ws = _query(m, f)
     assert rc == 0
     assert cap == 64 * 8 * 104857        # b * c_out * min(k, V): the rho_up guarantee
-    assert ws > 64 * 8 * 128 ** 3 * 4    # dense pre-attention buffer
+    assert ws > 64 * 8 * 128 ** 3 * 8    # candidate runs: 8 B per voxel and output channel
     rc, cap, _ = _query(m, f, attn=0)
     assert rc == 0 and cap == 64 * 8 * 128 ** 3
 
@@ -78,7 +78,8 @@ def test_fwd_query_capacity_is_the_density_bound():
 @pytest.mark.parametrize("mut,code", [
     (lambda m, f: setattr(f, "c_in", 4), 2),                 # c_in mismatch -> SPC_ERR_SHAPE
     (lambda m, f: f.ksize.__setitem__(0, 2), 2),             # even kernel -> SPC_ERR_SHAPE
-    (lambda m, f: setattr(m, "ndim", 4), 6),                 # rank 4 -> SPC_ERR_UNSUPPORTED
+    (lambda m, f: setattr(m, "ndim", 5), 6),                 # rank 5 -> SPC_ERR_UNSUPPORTED
+    (lambda m, f: setattr(m, "ndim", 4), 2),                 # rank 4 map, rank 3 filter -> SPC_ERR_SHAPE
     (lambda m, f: setattr(m, "keys", None), 1),              # NULL keys -> SPC_ERR_INVALID_ARG
     (lambda m, f: setattr(m, "channels", 0), 2),
 ])
@@ -186,7 +187,8 @@ def test_memory_estimate_errors():
     assert lib.spc_memory_estimate(3, 256, 32, 8, 1 / 256, 16, C.byref(d), None, None) == 1
     assert lib.spc_memory_estimate(3, 0, 32, 8, 0.1, 64, None, None, None) == 1
     assert lib.spc_memory_estimate(3, 8, 1, 1, 0.0, 64, None, None, None) == 1
-    assert lib.spc_memory_estimate(4, 8, 1, 1, 0.5, 64, None, None, None) == 1
+    assert lib.spc_memory_estimate(5, 8, 1, 1, 0.5, 64, None, None, None) == 1
+    assert lib.spc_memory_estimate(4, 8, 1, 1, 0.5, 64, None, None, None) == 0   # rank 4
 
 
 def test_fwd_pass_workspace_shrinks_with_samples_per_pass():

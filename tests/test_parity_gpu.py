@@ -100,6 +100,88 @@ def test_fwd_continuous_tolerance(cuda_lib, case, attn):
     assert_values_close(gv[gi], ov[oi], fa[idx])
 
 
+# ------------------------------------------------------------ rank 4 ("generic n-dimensional")
+RANK4_CASES = [
+    # name, dims, batch, c_in, c_out, ksize, rho_d, rho_f
+    ("4d_small", (5, 6, 7, 9), 2, 3, 4, (3, 3, 3, 3), 0.05, 0.4),
+    ("4d_k3133", (4, 5, 6, 8), 1, 2, 5, (3, 1, 3, 3), 0.1, 0.6),
+    ("4d_k5w", (7, 4, 4, 12), 2, 2, 3, (5, 3, 1, 3), 0.08, 0.5),
+    ("4d_sampled", (12, 16, 20, 32), 1, 2, 3, (3, 3, 3, 3), 0.02, 0.3),   # sampled threshold (>= 184 tiles)
+]
+
+
+@pytest.mark.parametrize("case", RANK4_CASES, ids=lambda c: c[0])
+@pytest.mark.parametrize("attn", ["none", "magnitude", "raw"])
+@pytest.mark.parametrize("values", ["dyadic", "continuous"])
+def test_fwd_rank4(cuda_lib, case, attn, values):
+    spc = cuda_lib
+    _, dims, B, ci, co, ks, rd, rf = case
+    x = uniform_map(B, ci, dims, rd, 4400, values=values)
+    w = sparse_filter(ci, co, ks, rf, 4401, values=values)
+    bias = bias_vector(co, 4402, values=values)
+    V = int(np.prod(dims))
+    k = max(1, V // 20)
+    gk, gv, _ = run_fwd(spc, x, w, bias, attn, k, variant="auto")
+    if values == "dyadic":
+        ok_, ov, _, _ = ora.conv_fwd(x, w, bias, attn=ATTN_ORA[attn], k=k)
+        np.testing.assert_array_equal(gk, ok_)
+        np.testing.assert_array_equal(gv, ov)
+        return
+    fk, fv, fa, _ = ora.conv_fwd(x, w, bias, with_abs=True)
+    if attn == "none":
+        np.testing.assert_array_equal(gk, fk)
+        assert_values_close(gv, fv, fa)
+        return
+    ok_, ov, _, _ = ora.conv_fwd(x, w, bias, attn=ATTN_ORA[attn], k=k)
+    assert_topk_sets_match(gk, gv, ok_, ov, fk, fv, fa, V, k, attn)
+
+
+@pytest.mark.parametrize("case", RANK4_CASES[:3], ids=lambda c: c[0])
+@pytest.mark.parametrize("values", ["dyadic", "continuous"])
+def test_bwd_rank4(cuda_lib, case, values):
+    spc = cuda_lib
+    _, dims, B, ci, co, ks, rd, rf = case
+    x = uniform_map(B, ci, dims, rd, 4500, values=values)
+    w = sparse_filter(ci, co, ks, rf, 4501, values=values)
+    bias = bias_vector(co, 4502, values=values)
+    V = int(np.prod(dims))
+    yk, yv, _, _ = ora.conv_fwd(x, w, bias, attn=ora.ATTN_MAGNITUDE, k=max(1, V // 10))
+    dy = grad_values(yk.shape[0], 4503, values=values)
+    dx, dw, db, dxa, dwa = ora.conv_bwd(x, w, yk, dy, with_abs=True)
+    Y = spc.SparseMap.from_arrays(yk, yv, B, co, dims)
+    gdx, gdw, gdb = (host(t) for t in spc.sparse_conv_bwd(dev_map(spc, x), dev_filter(spc, w), Y,
+                                                           torch.from_numpy(dy).cuda()))
+    if values == "dyadic":
+        np.testing.assert_array_equal(gdx, dx)
+        np.testing.assert_array_equal(gdw, dw)
+        np.testing.assert_array_equal(gdb, db)
+    else:
+        assert_values_close(gdx, dx, dxa, "dx")
+        assert_values_close(gdw, dw, dwa, "dw")
+
+
+@pytest.mark.parametrize("dims,stride", [((6, 8, 8, 10), (2, 2, 2, 2)), ((5, 7, 4, 9), (3, 1, 2, 4)),
+                                         ((3, 2, 3, 9000), (1, 2, 1, 2))])   # last: PZ 4500 > 4096, the row form
+def test_maxpool_relu_topk_rank4(cuda_lib, dims, stride):
+    spc = cuda_lib
+    x = uniform_map(2, 3, dims, 0.3, 4600, values="dyadic")
+    ok_, ov, oarg = ora.maxpool(x, stride)
+    y, arg = spc.sparse_maxpool(dev_map(spc, x), stride)
+    yk, yv = y.trimmed()
+    np.testing.assert_array_equal(host_keys(yk), ok_)
+    np.testing.assert_array_equal(host(yv), ov)
+    np.testing.assert_array_equal(host(arg[:yk.shape[0]]), oarg)
+    rk, rv, rsrc = ora.relu(x)
+    y, src = spc.sparse_relu(dev_map(spc, x))
+    np.testing.assert_array_equal(host_keys(y.trimmed()[0]), rk)
+    k = 17
+    tk, tv, tsrc = ora.topk(x, ora.ATTN_MAGNITUDE, k)
+    y, src = spc.attention_topk(dev_map(spc, x), "magnitude", k)
+    yk, yv = y.trimmed()
+    np.testing.assert_array_equal(host_keys(yk), tk)
+    np.testing.assert_array_equal(host(yv), tv)
+
+
 # ---------------------------------------------------------------- variant G (tcgen05, 3xTF32)
 GEMM_CASES = FWD_CASES + [
     # C5-like: 32 -> 32 channels, dense filter, several densities (SURVEY §8 d, C5)
@@ -521,6 +603,30 @@ def test_validate_env_detects_unsorted(cuda_lib, monkeypatch):
         spc.sparse_relu(dev_map(spc, bad))
     assert e.value.code == 5
     spc.sparse_relu(dev_map(spc, x))   # sorted input passes validation
+
+
+def test_validate_env_detects_bad_filter(cuda_lib, monkeypatch):
+    """SPC_VALIDATE=1 also checks the filter keys: an out-of-range or unsorted filter
+    is rejected before any table is built; without validation the tables stay in bounds."""
+    spc = cuda_lib
+    from paper_1801_10585_b200._lib import SpconvError
+
+    x = uniform_map(1, 2, (6, 6), 0.5, 3)
+    w = sparse_filter(2, 3, (3, 3), 0.5, 3)
+    X = dev_map(spc, x)
+    bad_range = Filter(2, 3, (3, 3), np.append(w.keys[:-1], np.uint64(2 * 3 * 9 + 5)), w.values)
+    swapped = w.keys.copy()
+    swapped[[0, 1]] = swapped[[1, 0]]
+    bad_order = Filter(2, 3, (3, 3), swapped, w.values)
+    monkeypatch.setenv("SPC_VALIDATE", "1")
+    for bad in (bad_range, bad_order):
+        with pytest.raises(SpconvError) as e:
+            spc.sparse_conv_fwd(X, dev_filter(spc, bad), None, "magnitude", 5)
+        assert e.value.code == 5
+    spc.sparse_conv_fwd(X, dev_filter(spc, w), None, "magnitude", 5)   # a valid filter passes
+    monkeypatch.delenv("SPC_VALIDATE")
+    spc.sparse_conv_fwd(X, dev_filter(spc, bad_range), None, "magnitude", 5)   # no fault, result unspecified
+    torch.cuda.synchronize()
 
 
 # ------------------------------------------------------------- full size (bench config)
