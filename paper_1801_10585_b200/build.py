@@ -40,19 +40,24 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, debug: bool = False) -> str:
-    """debug=True builds libspconv_debug.so with -DSPC_DEBUG (device-side bounds reports)."""
-    lib = LIB if not debug else os.path.join(HERE, "libspconv_debug.so")
-    if not force and not debug and not needs_build():
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, debug: bool = False,
+          variant: str = "", defines=()) -> str:
+    """debug=True builds libspconv_debug.so with -DSPC_DEBUG (device-side bounds reports);
+    variant="name" with defines=("SPC_X", ...) builds libspconv_name.so (A/B experiments, loaded
+    with SPC_LIB=...)."""
+    if debug:
+        variant, defines = "debug", tuple(defines) + ("SPC_DEBUG",)
+    lib = LIB if not variant else os.path.join(HERE, f"libspconv_{variant}.so")
+    if not force and not variant and not needs_build():
         return LIB
     objs = []
-    bdir = os.path.join(HERE, "build" if not debug else "build_debug")
+    bdir = os.path.join(HERE, "build" if not variant else f"build_{variant}")
     os.makedirs(bdir, exist_ok=True)
     procs = []
     for src in sources():
         obj = os.path.join(bdir, os.path.basename(src)[:-3] + ".o")
         cmd = [_nvcc(), "-c", src, "-o", obj] + NVCC_FLAGS + (["-Xptxas", "-v"] if ptxas_v else []) + \
-              (["-DSPC_DEBUG"] if debug else [])
+              [f"-D{d}" for d in defines]
         if verbose:
             print(" ".join(cmd), flush=True)
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -74,5 +79,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, deb
 
 
 if __name__ == "__main__":
+    defs = [a[2:] for a in sys.argv if a.startswith("-D")]
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), "")
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, ptxas_v="--ptxas" in sys.argv,
-                debug="--debug" in sys.argv))
+                debug="--debug" in sys.argv, variant=var, defines=defs))

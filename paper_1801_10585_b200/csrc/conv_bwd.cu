@@ -31,7 +31,7 @@ static size_t bwd_smem(const KGeo& kg, int c_in, int TX, int TY, int ZR, int ocg
     const size_t g = (size_t)ocg * (1 + 2 * kg.hw) * (TX + 2 * kg.hx) * (TY + 2 * kg.hy) * ZR * sizeof(float);
     const size_t w = (size_t)nwg * (sizeof(int) + sizeof(float) + sizeof(double));
     const size_t idx = (size_t)(c_in + 1) * sizeof(int) * 2 + (size_t)c_in * TX * 2 * sizeof(uint32_t);
-    const size_t stage = (size_t)(threads / 32) * 32 * (sizeof(int) + sizeof(float));
+    const size_t stage = (size_t)(threads / 32) * 32 * 4 * sizeof(int);   // per warp: 4 x 32 words
     return g + w + idx + stage + 256;
 }
 
@@ -131,8 +131,10 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
     p += (size_t)c_in * t.TX * 2 * sizeof(uint32_t);
     // align from the __shared__ base with integer offsets (keeps the shared address space)
     p = smraw + ((size_t)(p - smraw + 15) & ~(size_t)15);
-    int* st_eb = reinterpret_cast<int*>(p) + warp * 64;   // per warp: 32 ebase + 32 values
+    int* st_eb = reinterpret_cast<int*>(p) + warp * 128;   // per warp: 32 ebase + 32 values (+ 64 fill words)
     float* st_v = reinterpret_cast<float*>(st_eb + 32);
+    int* st_gb = st_eb + 64;                               // G fill: per halo row its G base ...
+    uint32_t* st_rz = reinterpret_cast<uint32_t*>(st_eb + 96);   // ... and the low word of its first key
 
     // ---- one-time setup: group weights with their G-offsets, zero G and dw partials
     if (threadIdx.x == 0) {
@@ -200,14 +202,16 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
         // the warp's rows r = warp + k * nwarps: lane k loads row k's bounds (one latency for all)
         for (int r0 = warp; r0 < nocl * HWX; r0 += 32 * nwarps) {
             uint32_t be0 = 0, be1 = 0;
+            int gb = 0;
+            uint32_t rz = 0;
             {
                 const int r = r0 + lane * nwarps;
                 if (r < nocl * HWX) {
-                    int gb;
                     const int64_t row = halo_row(r, gb);
                     if (row >= 0) {
                         be0 = yrow[row];
                         be1 = yrow[row + (hyhi - hylo)];
+                        rz = (uint32_t)((uint64_t)row * (uint64_t)gy.Z);
                     }
                 }
             }
@@ -219,6 +223,8 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
             __syncwarp();
             st_eb[lane] = (int)(incl - len);   // cum_k
             st_eb[32 + lane] = (int)be0;       // e0_k
+            st_gb[lane] = gb;
+            st_rz[lane] = rz;
             __syncwarp();
             const int nrows = min(32, (nocl * HWX - r0 + nwarps - 1) / nwarps);
             for (uint32_t base = 0; base < wtot; base += 256) {
@@ -244,10 +250,8 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     if (rk[j] < 0) continue;
-                    const int r = r0 + rk[j] * nwarps;
-                    int gbase;
-                    const int64_t row = halo_row(r, gbase);
-                    const uint32_t L = (uint32_t)(kk[j] - (uint64_t)row * (uint64_t)gy.Z);
+                    const int gbase = st_gb[rk[j]];
+                    const uint32_t L = (uint32_t)kk[j] - st_rz[rk[j]];   // offset in the halo rows (mod 2^32)
                     uint32_t yr = __float2uint_rz(__uint2float_rz(L) * invZ);
                     if (yr * (uint32_t)gy.Z > L) --yr;
                     if ((yr + 1) * (uint32_t)gy.Z <= L) ++yr;

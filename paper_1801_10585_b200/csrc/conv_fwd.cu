@@ -185,60 +185,54 @@ __device__ __forceinline__ void epi_hist_rows(const float* S, float bv, int nyr,
 // Candidate epilogue of one output channel (warp = channel, no block barrier): "get non-zero
 // entries" (structural support R3), "add bias", and every support entry whose score
 // reaches the segment's threshold tlow is appended in key order to the tile's candidate run.
-// Row by row, 128 voxels per step: lane l holds z = z0 + 4l .. z0 + 4l + 3 (one 16-byte load when
-// Z % 4 == 0), one warp scan of the per-lane candidate counts ranks them, and only the lanes
-// holding candidates (about 6 % of the voxels) run the store loop -- into a per-warp shared-memory
-// buffer that is flushed to the run with coalesced stores. Returns the run length, the support
-// size and the largest candidate score.
-constexpr int kCandBuf = 160;   // per-warp buffer entries, in the staging area
+// Row by row, 128 voxels per step: lane l holds z = z0 + l + 32u (u = 0..3), so each of the four
+// 32-voxel groups is one ballot. Candidates are ranked into a per-warp shared-memory buffer
+// (branch-free: non-candidates store to a private dummy slot) that is flushed to the run with
+// coalesced stores. Returns the run length, the support size and the largest candidate score.
+constexpr int kCandBuf = 160;   // per-warp buffer entries (+ 32 dummy slots), in the staging area
 template <int MODE>
 __device__ __forceinline__ void epi_cand(const float* S, int nyr, int Z, int ZR, float bv, uint32_t tlow,
                                          uint32_t marker, uint32_t pbase, uint32_t* __restrict__ cpos,
                                          float* __restrict__ cval, uint32_t* bufp, float* bufv, uint32_t& n_out,
                                          uint32_t& sup_out, uint32_t& max_out) {
     const int lane = threadIdx.x & 31;
-    const bool vec = (Z & 3) == 0;
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t dummy = kCandBuf + (uint32_t)lane;
     uint32_t nb = 0, nf = 0, sup = 0, mx = 0;   // buffered, flushed
-    for (int r = 0; r < nyr; ++r) {
-        const float* row = S + r * ZR;
-        const uint32_t prow = pbase + (uint32_t)(r * Z);
-        for (int z0 = 0; z0 < Z; z0 += 128) {
-            const int z = z0 + 4 * lane;
-            float v[4];
-            if (vec) {
-                if (z < Z) {
-                    const float4 q = *reinterpret_cast<const float4*>(row + z);
-                    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
-                } else {
+    // 128-voxel slots in key order (row, z0); two slots per step, their eight loads issued first
+    const int nz0 = (Z + 127) >> 7, nslot = nyr * nz0;
+    for (int s0 = 0; s0 < nslot; s0 += 2) {
+        float raw[8];
+        uint32_t pz[8];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) v[u] = __uint_as_float(marker);
-                }
-            } else {
-#pragma unroll
-                for (int u = 0; u < 4; ++u) v[u] = z + u < Z ? row[z + u] : __uint_as_float(marker);
-            }
-            uint32_t f = 0;
+        for (int h = 0; h < 2; ++h) {
+            const int sl = s0 + h;
+            const int r = sl / nz0, z0 = (sl - r * nz0) << 7;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const bool pres = __float_as_uint(v[u]) != marker;
-                v[u] += bv;
-                const uint32_t sc = MODE == SPC_ATTN_NONE ? 0u : score_bits(__float_as_uint(v[u]), MODE);
+                const int z = z0 + 32 * u + lane;
+                const bool in = sl < nslot && z < Z;
+                raw[4 * h + u] = in ? S[r * ZR + z] : __uint_as_float(marker);
+                pz[4 * h + u] = pbase + (uint32_t)(r * Z + z);
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int q = 4 * h + u;
+                const bool pres = __float_as_uint(raw[q]) != marker;
+                const float val = raw[q] + bv;
+                const uint32_t sc = MODE == SPC_ATTN_NONE ? 0u : score_bits(__float_as_uint(val), MODE);
                 const bool c = pres && sc >= tlow;
-                f |= (uint32_t)c << u;
                 sup += pres ? 1u : 0u;
                 mx = c ? max(mx, sc) : mx;
+                const uint32_t bal = __ballot_sync(kFull, c);
+                const uint32_t slot = c ? nb + (uint32_t)__popc(bal & lt) : dummy;
+                bufp[slot] = pz[q];
+                bufv[slot] = val;
+                nb += (uint32_t)__popc(bal);
             }
-            const uint32_t cnt = (uint32_t)__popc(f);
-            const uint32_t incl = warp_incl_scan(cnt);
-            uint32_t o = nb + incl - cnt;
-            while (f) {   // the lane's candidates, in z order
-                const int u = __ffs(f) - 1;
-                f &= f - 1;
-                bufp[o] = prow + (uint32_t)(z + u);
-                bufv[o] = v[u];
-                ++o;
-            }
-            nb += __shfl_sync(kFull, incl, 31);
             if (nb > kCandBuf - 128) {   // flush: coalesced copy of the buffer to the run
                 __syncwarp();
                 for (uint32_t i = lane; i < nb; i += 32) {
@@ -247,10 +241,11 @@ __device__ __forceinline__ void epi_cand(const float* S, int nyr, int Z, int ZR,
                 }
                 nf += nb;
                 nb = 0;
+                __syncwarp();
             }
-            __syncwarp();
         }
     }
+    __syncwarp();
     for (uint32_t i = lane; i < nb; i += 32) {
         cpos[nf + i] = bufp[i];
         cval[nf + i] = bufv[i];
@@ -261,6 +256,7 @@ __device__ __forceinline__ void epi_cand(const float* S, int nyr, int Z, int ZR,
     for (int d = 16; d > 0; d >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, d));
     max_out = mx;
 }
+
 
 // "add val*fval to buffer at uid" on the shared accumulator; the first update of a voxel
 // replaces the absent marker (structural support, reading R3)
@@ -345,7 +341,9 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
                 const float oa = lds_u(qa), ob = lds_u(qb);
                 sts_p(qa, upd<NEG0>(oa, d.vA, w), okA);
                 sts_p(qb, upd<NEG0>(ob, d.vB, w), okB);
+#ifndef SPC_NO_SYNCWARP
                 __syncwarp();
+#endif
                 q = qn;
             }
         } else {
@@ -355,7 +353,9 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
                 const int2 qn = rec[r + 1];
                 const uint32_t qa = d.aA + (uint32_t)q.x;
                 sts_p(qa, upd<NEG0>(lds_u(qa), d.vA, __int_as_float(q.y)), okA);
+#ifndef SPC_NO_SYNCWARP
                 __syncwarp();
+#endif
                 q = qn;
             }
         }
@@ -579,9 +579,10 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
         uint32_t* cp = a.cpos + s * gy.V + pbase;
         float* cv = a.cval + s * gy.V + pbase;
         uint32_t n, sup, mx;
-        static_assert(kFwdWarps * kCandBuf <= kStageCap, "candidate buffers live in the staging area");
-        uint32_t* bp = spos + warp * kCandBuf;
-        float* bvv = sval + warp * kCandBuf;
+        constexpr int kBufStride = kCandBuf + 32;
+        static_assert(kFwdWarps * kBufStride <= kStageCap, "candidate buffers live in the staging area");
+        uint32_t* bp = spos + warp * kBufStride;
+        float* bvv = sval + warp * kBufStride;
         if (a.attn == SPC_ATTN_MAGNITUDE)
             epi_cand<SPC_ATTN_MAGNITUDE>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, bvv, n, sup, mx);
         else if (a.attn == SPC_ATTN_RAW)
