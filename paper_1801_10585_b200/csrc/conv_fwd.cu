@@ -267,6 +267,14 @@ __device__ __forceinline__ float lds_u(uint32_t addr) {
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
     return v;
 }
+// predicated load: idle lanes do not touch shared memory (no benign read/write overlap with an
+// active lane's target, so racecheck stays silent)
+__device__ __forceinline__ float lds_p(uint32_t addr, bool p) {
+    float v = 0.0f;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.f32 %0, [%1];\n\t}"
+                 : "+f"(v) : "r"(addr), "r"((int)p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void sts_p(uint32_t addr, float v, bool p) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.f32 [%0], %1;\n\t}"
                  :: "r"(addr), "f"(v), "r"((int)p) : "memory");
@@ -338,7 +346,7 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
                 const int2 qn = rec[r + 1];   // next record in flight during this round (rec has a spare slot)
                 const uint32_t qa = d.aA + (uint32_t)q.x, qb = d.aB + (uint32_t)q.x;
                 const float w = __int_as_float(q.y);
-                const float oa = lds_u(qa), ob = lds_u(qb);
+                const float oa = lds_p(qa, okA), ob = lds_p(qb, okB);
                 sts_p(qa, upd<NEG0>(oa, d.vA, w), okA);
                 sts_p(qb, upd<NEG0>(ob, d.vB, w), okB);
 #ifndef SPC_NO_SYNCWARP
@@ -352,7 +360,7 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
             for (int r = d.r0; r < d.r1; ++r) {
                 const int2 qn = rec[r + 1];
                 const uint32_t qa = d.aA + (uint32_t)q.x;
-                sts_p(qa, upd<NEG0>(lds_u(qa), d.vA, __int_as_float(q.y)), okA);
+                sts_p(qa, upd<NEG0>(lds_p(qa, okA), d.vA, __int_as_float(q.y)), okA);
 #ifndef SPC_NO_SYNCWARP
                 __syncwarp();
 #endif

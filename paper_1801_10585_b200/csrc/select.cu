@@ -113,9 +113,11 @@ topk_seg_kernel(const uint64_t* __restrict__ keys, const float* __restrict__ val
             T |= sh_bin << sh;
             pmask |= (nb - 1u) << sh;
             need = sh_need;
-            if (sh_cnt == need) break;   // the whole bucket is kept: no tie split below it
-            if (pass == 0 && sh_cnt <= kTkCand) {
+            const uint32_t bcnt = sh_cnt;
+            if (bcnt == need) break;   // the whole bucket is kept: no tie split below it
+            if (pass == 0 && bcnt <= kTkCand) {
                 // gather the bucket's scores into shared memory; the later digits run there
+                __syncthreads();   // every thread has read sh_cnt before it is reused as the cursor
                 if (tid == 0) sh_cnt = 0;
                 __syncthreads();
                 // warp-uniform trip count (the ballots below need every lane)
