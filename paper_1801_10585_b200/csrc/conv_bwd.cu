@@ -239,8 +239,11 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
                     kk[j] = 0ull;
                     dv[j] = 0.0f;
                     if (pos < wtot) {
-                        int k = 0;
-                        while (k + 1 < nrows && (uint32_t)st_eb[k + 1] <= pos) ++k;
+                        int k = 0, hi = nrows;   // last row k with cum_k <= pos (binary search)
+                        while (hi - k > 1) {
+                            const int mid = (k + hi) >> 1;
+                            if ((uint32_t)st_eb[mid] <= pos) k = mid; else hi = mid;
+                        }
                         const uint32_t e = (uint32_t)st_eb[32 + k] + (pos - (uint32_t)st_eb[k]);
                         kk[j] = ykeys[e];
                         dv[j] = dy[e];

@@ -275,6 +275,9 @@ __device__ __forceinline__ float lds_p(uint32_t addr, bool p) {
                  : "+f"(v) : "r"(addr), "r"((int)p) : "memory");
     return v;
 }
+__device__ __forceinline__ void sts_u(uint32_t addr, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" :: "r"(addr), "f"(v) : "memory");
+}
 __device__ __forceinline__ void sts_p(uint32_t addr, float v, bool p) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.f32 [%0], %1;\n\t}"
                  :: "r"(addr), "f"(v), "r"((int)p) : "memory");
@@ -346,9 +349,11 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
                 const int2 qn = rec[r + 1];   // next record in flight during this round (rec has a spare slot)
                 const uint32_t qa = d.aA + (uint32_t)q.x, qb = d.aB + (uint32_t)q.x;
                 const float w = __int_as_float(q.y);
-                const float oa = lds_p(qa, okA), ob = lds_p(qb, okB);
-                sts_p(qa, upd<NEG0>(oa, d.vA, w), okA);
-                sts_p(qb, upd<NEG0>(ob, d.vB, w), okB);
+                float oa = 0.0f, ob = 0.0f;   // idle lanes do not touch shared memory (racecheck-clean)
+                if (okA) oa = lds_u(qa);
+                if (okB) ob = lds_u(qb);
+                if (okA) sts_u(qa, upd<NEG0>(oa, d.vA, w));
+                if (okB) sts_u(qb, upd<NEG0>(ob, d.vB, w));
 #ifndef SPC_NO_SYNCWARP
                 __syncwarp();
 #endif
@@ -360,7 +365,7 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
             for (int r = d.r0; r < d.r1; ++r) {
                 const int2 qn = rec[r + 1];
                 const uint32_t qa = d.aA + (uint32_t)q.x;
-                sts_p(qa, upd<NEG0>(lds_p(qa, okA), d.vA, __int_as_float(q.y)), okA);
+                if (okA) sts_u(qa, upd<NEG0>(lds_u(qa), d.vA, __int_as_float(q.y)));
 #ifndef SPC_NO_SYNCWARP
                 __syncwarp();
 #endif
