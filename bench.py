@@ -34,7 +34,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from synth import uniform_map, sparse_filter, bias_vector, grad_values, select_samples, SEED_BASE  # noqa: E402
+from synth import (uniform_map, sparse_filter, bias_vector, grad_values, select_samples, surface_occupancy,  # noqa: E402
+                   SEED_BASE)
 
 RES = 128
 BATCH = 64
@@ -657,6 +658,8 @@ def main(argv=None):
     ap.add_argument("--variant", default="measure", choices=["auto", "scatter", "gemm", "measure"],
                     help="forward accumulate variant (SURVEY §8 a3); 'measure' times both once and keeps the faster")
     ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing only, gloo on CPU (tests)")
+    ap.add_argument("--config", default="c4", choices=["c4", "c3"],
+                    help="c4 = BASELINE configs[3] (headline), c3 = configs[2] (point-cloud two-layer step)")
     ap.add_argument("--samples-per-pass", type=int, default=None,
                     help="bounded-memory forward (sparse_conv_fwd_pass, SURVEY §8 f2): samples per pass")
     args = ap.parse_args(argv)
@@ -666,7 +669,158 @@ def main(argv=None):
         return run_reference(args)
     if args.dry_run:
         return run_dry(args)
+    if args.config == "c3":
+        return run_c3(args)
     return run_ours(args)
+
+
+# ---------------------------------------------------------------------- C3 (configs[2])
+C3_RES, C3_BATCH, C3_OCC = 64, 32, 0.02
+C3_K = int(C3_OCC * C3_RES ** 3)          # 5242: reading rho_up = rho_d (P:208 protocol rho = rho_up)
+
+
+def c3_inputs(batch=C3_BATCH, b0=0):
+    x = surface_occupancy(batch, C3_RES, C3_OCC, SEED_BASE * 1000 + 300, b0=b0)
+    w1 = sparse_filter(1, 32, (3, 3, 3), 1.0, SEED_BASE + 31)
+    w2 = sparse_filter(32, 64, (3, 3, 3), 1.0, SEED_BASE + 32)
+    return dict(x=x, w1=w1, w2=w2, b1=bias_vector(32, SEED_BASE + 31), b2=bias_vector(64, SEED_BASE + 32))
+
+
+def run_c3(args):
+    """BASELINE configs[2]: 3D point-cloud occupancy 64^3 at 2 % (binary values), batch 32, conv 1->32
+    (attention, k = 5242) -> ReLU -> conv 32->64 (attention), forward + backward (dw / dbias of both
+    layers, dx of the second, the ReLU backward scatter) [+ the dw||dbias all-reduce per layer].
+    Metric as for C4: (Eq. (1) MACs of both layers + 2 x the pairs on kept outputs) / time."""
+    import torch
+    import torch.distributed as dist
+    import torch.nn.functional as F
+
+    import paper_1801_10585_b200 as spc
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"WORLD_SIZE={world} but --gpus {args.gpus}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    spc.load()
+    assert C3_BATCH % world == 0
+    B = C3_BATCH // world
+    cfg = c3_inputs(B, rank * B)
+    x, w1, w2 = cfg["x"], cfg["w1"], cfg["w2"]
+    X = spc.SparseMap.from_arrays(x.keys, x.values, x.batch, x.channels, x.dims)
+    W1 = spc.SparseFilter.from_arrays(w1.keys, w1.values, 1, 32, (3, 3, 3))
+    W2 = spc.SparseFilter.from_arrays(w2.keys, w2.values, 32, 64, (3, 3, 3))
+    b1, b2 = torch.from_numpy(cfg["b1"]).cuda(), torch.from_numpy(cfg["b2"]).cuda()
+    f1 = spc.FwdPlan(X, W1, "magnitude", C3_K, args.variant, b1)
+    Y1 = f1(X, W1, b1)
+    R1, src1 = spc.sparse_relu(Y1)
+    f2 = spc.FwdPlan(R1, W2, "magnitude", C3_K, args.variant, b2)
+    Y2 = f2(R1, W2, b2)
+    g1, g2 = spc.BwdPlan(X, W1, Y1), spc.BwdPlan(R1, W2, Y2)
+    dy2 = torch.from_numpy(grad_values(Y2.nnz_bound, SEED_BASE + 33 + rank)).cuda()
+    dR1 = torch.empty(max(R1.nnz_bound, 1), device="cuda")
+    side = torch.cuda.Stream() if world > 1 else None
+    ar1 = spc.dp.GradAllReduce(w1.nnz, 32, "cuda", stream=side)
+    ar2 = spc.dp.GradAllReduce(w2.nnz, 64, "cuda", stream=side)
+    dw1, db1 = torch.empty(w1.nnz, device="cuda"), torch.empty(32, device="cuda")
+    dw2, db2 = torch.empty(w2.nnz, device="cuda"), torch.empty(64, device="cuda")
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    state = {}
+
+    def step():
+        Y1 = f1(X, W1, b1)
+        R1, src1 = spc.sparse_relu(Y1)
+        Y2 = f2(R1, W2, b2)
+        g2.f64(R1, W2, Y2, dy2, dR1, ar2.dw64, ar2.db64)
+        ar2.start()                               # layer 2's exchange overlaps layer 1's backward
+        dY1 = spc.sparse_scatter_grad(src1, dR1, R1.nnz_bound, Y1.nnz_bound, R1.nnz_dev)
+        g1.f64(X, W1, Y1, dY1, None, ar1.dw64, ar1.db64)
+        ar1.start()
+        ar2.finish(dw2, db2)
+        ar1.finish(dw1, db1)
+        state.update(Y1=Y1, R1=R1, Y2=Y2)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # algorithmic work (measurement plumbing): Eq. (1) pairs per layer from mask correlations
+    V = C3_RES ** 3
+
+    def pairs(inp, ch_in, w, ch_out, ykeys):
+        wm = torch.zeros(ch_out * ch_in * 27, device="cuda")
+        wm[w.keys.long()] = 1.0
+        wm = wm.view(ch_out, ch_in, 3, 3, 3)
+        keys = inp.keys[:inp.nnz()]
+        fwd, kept = 0, 0
+        for s0 in range(0, B, 4):
+            nb = min(4, B - s0)
+            lo, hi = s0 * ch_in * V, (s0 + nb) * ch_in * V
+            m = torch.zeros(nb * ch_in * V, device="cuda")
+            m[keys[(keys >= lo) & (keys < hi)] - lo] = 1.0
+            cnt = F.conv3d(m.view(nb, ch_in, C3_RES, C3_RES, C3_RES), wm, padding=1)
+            fwd += int(cnt.double().sum().item())
+            ylo, yhi = s0 * ch_out * V, (s0 + nb) * ch_out * V
+            kept += int(cnt.reshape(-1)[ykeys[(ykeys >= ylo) & (ykeys < yhi)] - ylo].double().sum().item())
+        return fwd, 2 * kept
+
+    torch.backends.cudnn.allow_tf32 = False
+    step()
+    torch.cuda.synchronize()
+    Y1, R1, Y2 = state["Y1"], state["R1"], state["Y2"]
+    fm1, bm1 = pairs(X, 1, W1, 32, Y1.keys[:Y1.nnz()])
+    fm2, bm2 = pairs(R1, 32, W2, 64, Y2.keys[:Y2.nnz()])
+    macs = fm1 + bm1 + fm2 + bm2
+    l0 = spc.kernel_launches()
+    step()
+    torch.cuda.synchronize()
+    lps = spc.kernel_launches() - l0
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record()
+            step()
+            evs[i][1].record()
+        torch.cuda.synchronize()
+    t_ms = sum(a.elapsed_time(b) for a, b in evs)
+    macs_all = float(macs)
+    if world > 1:
+        t = torch.tensor([t_ms, macs], dtype=torch.float64, device="cuda")
+        tmax = t[:1].clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:])
+        t_ms, macs_all = float(tmax.item()), float(t[1].item())
+    ms = t_ms / args.steps
+    spc.profile_reset()
+    spc.profile_enable(True)
+    step()
+    torch.cuda.synchronize()
+    prof = spc.profile_read()
+    spc.profile_enable(False)
+    if rank == 0:
+        res = {"metric": "sparse conv fwd+bwd effective GMAC/s (C3 64^3 surface 2%, 1->32->64)",
+               "value": round(macs_all / (ms * 1e-3) / 1e9, 3), "unit": "GMAC/s", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+               "data": "synthetic (voxelised sphere shells and plane patches, binary values, seeded)",
+               "config": {"workload": f"C3: 3D {C3_RES}^3 occupancy {C3_OCC}, batch {C3_BATCH} (sharded {B}/GPU), "
+                                      f"conv 1->32 (attention k={C3_K}) -> ReLU -> conv 32->64 (attention k={C3_K}), "
+                                      "3x3x3 dense filters, fwd + bwd + dw||dbias all-reduce per layer",
+                          "fwd_variants": f"{args.variant} -> {f1.resolved}, {f2.resolved}",
+                          "parallelism": f"dp{world}", "l2": "flushed between timed steps (512 MB write)"},
+               "work_per_step": {"fwd_macs_l1": fm1, "bwd_macs_l1": bm1, "fwd_macs_l2": fm2, "bwd_macs_l2": bm2,
+                                 "nnz_x": int(x.nnz), "nnz_y1": Y1.nnz(), "nnz_relu": R1.nnz(), "nnz_y2": Y2.nnz()},
+               "kernels": {n: round(v[0], 4) for n, v in sorted(prof.items(), key=lambda kv: -kv[1][0])},
+               "gpu_launches": int(lps * args.steps), "gpu_launches_per_step": int(lps), "clocks": clk.summary()}
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def run_dry(args):

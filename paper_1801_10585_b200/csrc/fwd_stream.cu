@@ -65,9 +65,18 @@ __global__ void stream_find_kernel(FwdArgs a, double f) {
             const int bin = kSelBins - 1 - threadIdx.x * per - q;
             const double hb = (double)h[bin];
             if (cum + hb >= want) {
-                const double frac = (want - cum) / hb;   // share of the bin needed, from its top
-                const double off = (1.0 - frac) * (double)(1u << 21);
-                a.tlow[s] = ((uint32_t)bin << 21) + (uint32_t)fmax(0.0, floor(off));
+                // large samples: interpolate inside the crossing bin; small ones (spatially
+                // correlated surface data, discrete values with exact ties) take the bin's lower
+                // edge, one bin lower below 2000 sampled entries -- a miss costs a redo pass
+                uint32_t t;
+                if ((double)tot >= 20000.0) {
+                    const double frac = (want - cum) / hb;   // share of the bin needed, from its top
+                    t = ((uint32_t)bin << 21) + (uint32_t)fmax(0.0, floor((1.0 - frac) * (double)(1u << 21)));
+                } else {
+                    const int b2 = (double)tot >= 2000.0 ? bin : max(0, bin - 1);
+                    t = (uint32_t)b2 << 21;
+                }
+                a.tlow[s] = t;
                 return;
             }
             cum += hb;
