@@ -434,8 +434,12 @@ def roofline_for(name, ph, m, pk, src):
     return out
 
 
+_NCU_NAME = {"fwd_write": "stream_write", "fwd_resolve": "stream_resolve"}   # library phase -> ncu kernel
+
+
 def ncu_traffic(kernel):
     """DRAM bytes per launch of `kernel` from the newest committed ncu --set full capture, or None."""
+    kernel = _NCU_NAME.get(kernel, kernel)
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_traffic.json")), reverse=True):
         try:
             d = json.load(open(path))
@@ -649,8 +653,8 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--density", type=float, default=0.02)
-    ap.add_argument("--sweep", type=lambda s: [float(v) for v in s.split(",") if v], default=[0.01, 0.05],
-                    help="extra densities measured in the same run (north-star range), '' for none")
+    ap.add_argument("--sweep", type=lambda s: [] if s in ("", "none") else [float(v) for v in s.split(",") if v],
+                    default=[0.01, 0.05], help="extra densities measured in the same run (north-star range), 'none'")
     ap.add_argument("--values", default="continuous", choices=["continuous", "dyadic"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

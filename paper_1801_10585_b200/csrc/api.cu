@@ -171,7 +171,7 @@ double est_gemm_s(const Geo& gx, const GemmPlan& g) {
     const double gather = (2.0 * 128 * g.Kp * 4 + 2.0 * g.Np * g.Kp * 4) / 128.0;
     const double mma = 3.0 * (g.Kp / 8) * (128.0 * g.Np / 256.0);
     const double tiles = (double)gx.B * (double)g.ntile;
-    return tiles * g.KV * std::max(gather, mma) / (148.0 * 1.9e9) + (double)gx.B * gx.V * g.Kp * 16.0 / 3e12;
+    return tiles * g.KV * std::max(gather, mma) / ((double)num_sms() * sm_clock_hz()) + (double)gx.B * gx.V * g.Kp * 16.0 / 3e12;
 }
 
 spc_status_t fwd_plan(const spc_map_t* x, const spc_filter_t* w, spc_attn_t attn, int64_t k, spc_variant_t variant,

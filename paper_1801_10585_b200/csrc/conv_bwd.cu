@@ -70,7 +70,7 @@ BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int nw_total) {
         t.smem = bwd_smem(kg, c_in, bx, by, ZR, ocg, nwg, threads);
         t.threads = threads;
         const int64_t items = gx.B * gx.W * (int64_t)t.ntx * t.nty;
-        int64_t grid = (148 * cps + t.n_ocg - 1) / t.n_ocg;
+        int64_t grid = (num_sms() * cps + t.n_ocg - 1) / t.n_ocg;
         grid = std::max<int64_t>(1, std::min<int64_t>(grid, items));
         t.grid = (int)grid;
         return t;
@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(256) dbias_kernel(Geo gy, const uint32_t* __re
 cudaError_t launch_dbias(const Geo& gy, const uint32_t* yrow, const float* dy, double* db_acc, cudaStream_t s) {
     const int64_t nseg = gy.B * gy.C;
     if (nseg <= 0) return cudaSuccess;
-    const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(64, (4 * 148 + nseg - 1) / nseg));
+    const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(64, (4 * num_sms() + nseg - 1) / nseg));
     { SPC_PHASE("dbias", s, 1); dbias_kernel<<<(unsigned)(nseg * splits), 256, 0, s>>>(gy, yrow, dy, splits, db_acc); }
     return cudaGetLastError();
 }

@@ -1146,7 +1146,7 @@ cudaError_t launch_conv_fwd_stream(const Geo& gx, const Geo& gy, const KGeo& kg,
         if (!a.guard_done) {
             cudaMemsetAsync(a.guard, 0, sizeof(int), s);
             SPC_PHASE("value_guard", s, 1);
-            value_guard_kernel<<<148 * 4, 256, 0, s>>>(a.xvals, a.x_nnz_dev, a.x_nnz, a.guard);
+            value_guard_kernel<<<num_sms() * 4, 256, 0, s>>>(a.xvals, a.x_nnz_dev, a.x_nnz, a.guard);
         }
         SPC_PHASE("fwd_rounds", s, 1);
         fwd_rounds_kernel<<<(unsigned)t.n_ocg, 256, 0, s>>>(kg, (int)gx.C, (int)gy.C, t, a.meta2, a.val2, a.off2,

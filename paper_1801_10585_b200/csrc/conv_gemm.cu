@@ -741,7 +741,7 @@ cudaError_t launch_conv_gemm(const Geo& gx, const Geo& gy, const KGeo& kg, const
         cudaMemsetAsync(ga.xlo, 0, nvox * g.Kp * sizeof(float), s);
         cudaMemsetAsync(ga.occ, 0, nvox * sizeof(uint32_t), s);
         SPC_PHASE("gemm_densify", s, 1);
-        gemm_densify_kernel<<<148 * 8, 256, 0, s>>>(gx, g.Kp, ga.xkeys, ga.xvals, ga.x_nnz_dev, ga.x_nnz, ga.xhi, ga.xlo,
+        gemm_densify_kernel<<<num_sms() * 8, 256, 0, s>>>(gx, g.Kp, ga.xkeys, ga.xvals, ga.x_nnz_dev, ga.x_nnz, ga.xhi, ga.xlo,
                                                   ga.occ);
     }
     {
@@ -771,7 +771,7 @@ cudaError_t launch_conv_gemm(const Geo& gx, const Geo& gy, const KGeo& kg, const
     }
     {
         const int64_t nseg = gy.B * gy.C;
-        const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(256, (4 * 148 + nseg - 1) / nseg));
+        const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(256, (4 * num_sms() + nseg - 1) / nseg));
         SPC_PHASE("pre_hist", s, 1);
         pre_hist_kernel<<<(unsigned)(nseg * splits), 256, 0, s>>>(a, gy.V, splits);
     }

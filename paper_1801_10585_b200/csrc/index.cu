@@ -366,7 +366,7 @@ cudaError_t launch_scatter_grad(const int64_t* src, const float* dy, int64_t n_o
     if (e != cudaSuccess) return e;
     if (n_out_bound <= 0) return cudaSuccess;
     int64_t grid = (n_out_bound + 255) / 256;
-    if (grid > 148 * 16) grid = 148 * 16;
+    if (grid > num_sms() * 16) grid = num_sms() * 16;
     { SPC_PHASE("scatter_grad", s, 1); scatter_grad_kernel<<<(unsigned)grid, 256, 0, s>>>(src, dy, n_out_bound, n_out_dev, dx, n_in); }
     return cudaGetLastError();
 }
@@ -393,7 +393,7 @@ cudaError_t launch_to_dense(const uint64_t* keys, const float* vals, const int64
                             float* dense, int64_t cells, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(dense, 0, (size_t)cells * sizeof(float), s);
     if (e != cudaSuccess || bound == 0) return e;
-    const unsigned grid = (unsigned)std::min<int64_t>((bound + 255) / 256, 148 * 16);
+    const unsigned grid = (unsigned)std::min<int64_t>((bound + 255) / 256, num_sms() * 16);
     { SPC_PHASE("to_dense", s, 1); to_dense_kernel<<<grid, 256, 0, s>>>(keys, vals, nnz_dev, bound, dense); }
     return cudaGetLastError();
 }
@@ -401,7 +401,7 @@ cudaError_t launch_to_dense(const uint64_t* keys, const float* vals, const int64
 cudaError_t launch_gather_dense(const uint64_t* keys, const int64_t* nnz_dev, int64_t bound, const float* ddense,
                                 float* dvals, cudaStream_t s) {
     if (bound == 0) return cudaSuccess;
-    const unsigned grid = (unsigned)std::min<int64_t>((bound + 255) / 256, 148 * 16);
+    const unsigned grid = (unsigned)std::min<int64_t>((bound + 255) / 256, num_sms() * 16);
     { SPC_PHASE("gather_dense", s, 1); gather_dense_kernel<<<grid, 256, 0, s>>>(keys, nnz_dev, bound, ddense, dvals); }
     return cudaGetLastError();
 }
@@ -423,13 +423,13 @@ __global__ void keys_widen_kernel(const uint32_t* __restrict__ k, const int64_t*
 
 cudaError_t launch_keys_narrow(const uint64_t* keys, const int64_t* nnz_dev, int64_t bound, uint32_t* out, cudaStream_t s) {
     if (bound == 0) return cudaSuccess;
-    const unsigned grid = (unsigned)std::min<int64_t>((bound + 255) / 256, 148 * 16);
+    const unsigned grid = (unsigned)std::min<int64_t>((bound + 255) / 256, num_sms() * 16);
     { SPC_PHASE("keys_narrow", s, 1); keys_narrow_kernel<<<grid, 256, 0, s>>>(keys, nnz_dev, bound, out); }
     return cudaGetLastError();
 }
 cudaError_t launch_keys_widen(const uint32_t* keys, const int64_t* nnz_dev, int64_t bound, uint64_t* out, cudaStream_t s) {
     if (bound == 0) return cudaSuccess;
-    const unsigned grid = (unsigned)std::min<int64_t>((bound + 255) / 256, 148 * 16);
+    const unsigned grid = (unsigned)std::min<int64_t>((bound + 255) / 256, num_sms() * 16);
     { SPC_PHASE("keys_widen", s, 1); keys_widen_kernel<<<grid, 256, 0, s>>>(keys, nnz_dev, bound, out); }
     return cudaGetLastError();
 }

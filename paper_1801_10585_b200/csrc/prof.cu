@@ -108,3 +108,38 @@ int spc_profile_read(char* names, size_t names_len, double* ms, int64_t* counts,
 int64_t spc_kernel_launches(void) { return spc::g_launches.load(); }
 
 }  // extern "C"
+
+namespace spc {
+
+namespace {
+constexpr int kMaxDev = 64;
+int g_sms[kMaxDev];
+int g_clk_khz[kMaxDev];
+int cur_dev() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDev) d = 0;
+    return d;
+}
+}  // namespace
+
+int num_sms() {
+    const int d = cur_dev();
+    if (g_sms[d] == 0) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || v <= 0) v = 148;
+        g_sms[d] = v;
+    }
+    return g_sms[d];
+}
+
+double sm_clock_hz() {
+    const int d = cur_dev();
+    if (g_clk_khz[d] == 0) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrClockRate, d) != cudaSuccess || v <= 0) v = 1965000;
+        g_clk_khz[d] = v;
+    }
+    return 1e3 * (double)g_clk_khz[d];
+}
+
+}  // namespace spc

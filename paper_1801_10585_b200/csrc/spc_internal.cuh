@@ -83,6 +83,12 @@ __device__ __forceinline__ int64_t load_n(const int64_t* nnz_dev, int64_t bound)
     return n < bound ? n : bound;
 }
 
+// ------------------------------------------------------------- device properties (prof.cu)
+// SM count and SM clock (kHz) of the current device, queried once per device (grid sizing and
+// the AUTO variant cost model; 148 / 1965000 on B200).
+int num_sms();
+double sm_clock_hz();
+
 // ------------------------------------------------------------- launch accounting (prof.cu)
 void note_launch(int n = 1);
 struct PhaseScope {

@@ -43,7 +43,7 @@ __global__ void adagrad_kernel(float* __restrict__ w, const float* __restrict__ 
 cudaError_t launch_adagrad(float* w, const float* g, float* acc, int64_t n, const int64_t* y_nnz_dev, double y_cells,
                            const DensityReg& reg, bool has_reg, double lr, double eps, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
-    const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 8);
     { SPC_PHASE("adagrad", s, 1); adagrad_kernel<<<grid, 256, 0, s>>>(w, g, acc, n, y_nnz_dev, y_cells, reg, has_reg ? 1 : 0, lr, eps); }
     return cudaGetLastError();
 }

@@ -4,7 +4,7 @@
 cd ${GRAFT_REPO_ROOT:-.}
 mkdir -p gpurun_out
 for L in "$@"; do
-  SPC_LIB=paper_1801_10585_b200/$L.so timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --variant scatter --sweep "" ${BENCH_ARGS} > gpurun_out/ab_$L.log 2>&1
+  SPC_LIB=paper_1801_10585_b200/$L.so timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --variant scatter --sweep none ${BENCH_ARGS} > gpurun_out/ab_$L.log 2>&1
   python - $L <<'PY'
 import json, sys
 for l in open("gpurun_out/ab_" + sys.argv[1] + ".log"):

@@ -79,6 +79,9 @@ def main():
                      "phases_ms": timed_phases(fn) if fn else None})
         print(f"{name:28s} {ms:8.4f} ms {nbytes / 1e9:7.3f} GB {gbs:8.1f} GB/s  {gbs / peak * 100:5.1f} %")
 
+    from bench import ClockSampler
+
+    clk = ClockSampler(0).__enter__()   # SM clock + throttle reasons during all timed runs
     ms, (y, src) = timed(lambda: spc.sparse_relu(X))
     nk = y.nnz()
     report("sparse_relu", ms, 12 * n + 20 * nk, "keys+values read; kept keys+values+src written",
@@ -103,8 +106,10 @@ def main():
     half = spc.SparseMap(keys[:n8], vals[:n8], B // 8, C, (R, R, R), n8, None)
     ms, _ = timed(lambda: spc.sparse_to_dense(half))
     report("sparse_to_dense (8 samples)", ms, 12 * n8 + 4 * (B // 8) * C * V, "keys+values read; dense written")
+    clk.__exit__()
     res = {"workload": f"{R}^3 x batch {B} x {C} ch, density {args.density} per channel, {n} entries, randn values",
-           "peak_hbm_gbs": peak, "iters": args.iters, "l2": "512 MB flush between iterations", "ops": rows}
+           "peak_hbm_gbs": peak, "iters": args.iters, "l2": "512 MB flush between iterations", "ops": rows,
+           "clocks": clk.summary()}
     print(json.dumps(res))
     if args.out:
         with open(args.out, "w") as f:
