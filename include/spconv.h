@@ -85,6 +85,9 @@ typedef struct {
     const int64_t* nnz_dev;        /* device: exact count, or NULL                       */
     const uint64_t* keys;          /* device [nnz], strictly increasing                  */
     const float* values;           /* device [nnz]                                       */
+    int32_t key_bits;              /* 0 or 64: keys are uint64; 32: `keys` points to uint32
+                                      keys ("Sparse 32", Table 1, App. A),
+                                      valid when batch*channels*prod(dims) <= 2^32       */
 } spc_map_t;
 
 /* Output sparse feature map (shape implied by the operation). */
@@ -93,6 +96,7 @@ typedef struct {
     uint64_t* keys;                /* device [capacity]                                   */
     float* values;                 /* device [capacity]                                   */
     int64_t* nnz_dev;              /* device: receives the exact output count             */
+    int32_t key_bits;              /* 0 or 64: uint64 keys; 32: uint32 keys (as spc_map_t) */
 } spc_map_out_t;
 
 /* Sparse filter bank; nnz entries = the unpruned weights (rho_f of Eq. (1)). */

@@ -39,11 +39,12 @@ EXPORTS = [
 class MapT(C.Structure):
     _fields_ = [("ndim", C.c_int32), ("batch", C.c_int64), ("channels", C.c_int64),
                 ("dims", C.c_int64 * MAX_NDIM), ("nnz", C.c_int64), ("nnz_dev", C.c_void_p),
-                ("keys", C.c_void_p), ("values", C.c_void_p)]
+                ("keys", C.c_void_p), ("values", C.c_void_p), ("key_bits", C.c_int32)]
 
 
 class MapOutT(C.Structure):
-    _fields_ = [("capacity", C.c_int64), ("keys", C.c_void_p), ("values", C.c_void_p), ("nnz_dev", C.c_void_p)]
+    _fields_ = [("capacity", C.c_int64), ("keys", C.c_void_p), ("values", C.c_void_p), ("nnz_dev", C.c_void_p),
+                ("key_bits", C.c_int32)]
 
 
 class FilterT(C.Structure):

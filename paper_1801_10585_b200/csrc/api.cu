@@ -44,6 +44,8 @@ spc_status_t check_map(const spc_map_t* m, bool need_values = true) {
     if (total >= 9.2e18) return SPC_ERR_SHAPE;
     if (m->nnz >= (1ll << 32) - 1) return SPC_ERR_UNSUPPORTED;   // 32-bit row index
     if (m->nnz > 0 && (!m->keys || (need_values && !m->values))) return SPC_ERR_INVALID_ARG;
+    if (m->key_bits != 0 && m->key_bits != 32 && m->key_bits != 64) return SPC_ERR_INVALID_ARG;
+    if (m->key_bits == 32 && total > 4294967296.0) return SPC_ERR_UNSUPPORTED;   // keys must fit 32 bits
     return SPC_OK;
 }
 
@@ -84,15 +86,28 @@ spc_status_t check_filter(const spc_filter_t* w, const spc_map_t* x, KGeo* kg) {
     return SPC_OK;
 }
 
-spc_status_t check_out(const spc_map_out_t* y, int64_t need) {
+// space: the output map's batch*channels*prod(dims) (its keys must fit 32 bits when key_bits = 32)
+spc_status_t check_out(const spc_map_out_t* y, int64_t need, double space = 0.0) {
     if (!y) return SPC_ERR_INVALID_ARG;
     if (!y->nnz_dev) return SPC_ERR_INVALID_ARG;
     if (y->capacity < need) return SPC_ERR_CAPACITY;
     if (need > 0 && (!y->keys || !y->values)) return SPC_ERR_INVALID_ARG;
+    if (y->key_bits != 0 && y->key_bits != 32 && y->key_bits != 64) return SPC_ERR_INVALID_ARG;
+    if (y->key_bits == 32 && space > 4294967296.0) return SPC_ERR_UNSUPPORTED;
     return SPC_OK;
 }
 
+double space_of(const spc_map_t* m, int64_t channels) {
+    double v = (double)m->batch * (double)channels;
+    for (int d = 0; d < m->ndim; ++d) v *= (double)m->dims[d];
+    return v;
+}
+
 spc_status_t cu(cudaError_t e) { return e == cudaSuccess ? SPC_OK : SPC_ERR_CUDA; }
+
+// key arrays of either width (spc_map_t::key_bits, Table 1 "Sparse 32")
+Keys kin(const spc_map_t* m) { return Keys(m->keys, m->key_bits == 32); }
+KeysOut kout(const spc_map_out_t* y) { return KeysOut(y->keys, y->key_bits == 32); }
 
 #define SPC_TRY(expr)                          \
     do {                                       \
@@ -106,7 +121,7 @@ spc_status_t maybe_validate(const spc_map_t* m, int* flag, cudaStream_t s) {
     uint64_t limit = (uint64_t)m->batch * (uint64_t)m->channels;
     for (int d = 0; d < m->ndim; ++d) limit *= (uint64_t)m->dims[d];
     SPC_TRY(cu(cudaMemsetAsync(flag, 0, sizeof(int), s)));
-    SPC_TRY(cu(launch_validate(m->keys, m->nnz_dev, m->nnz, limit, flag, s)));
+    SPC_TRY(cu(launch_validate(kin(m), m->nnz_dev, m->nnz, limit, flag, s)));
     int h = 0;
     SPC_TRY(cu(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s)));
     SPC_TRY(cu(cudaStreamSynchronize(s)));
@@ -327,19 +342,19 @@ spc_status_t conv_bwd_impl(const spc_map_t* x, const spc_filter_t* w, const spc_
     }
     if (dw64) ws.dw_acc = dw64;
     if (db64) ws.db_acc = db64;
-    SPC_TRY(cu(launch_row_index(gy, y->keys, y->nnz_dev, y->nnz, ws.yrow, s)));
+    SPC_TRY(cu(launch_row_index(gy, kin(y), y->nnz_dev, y->nnz, ws.yrow, s)));
     if (dbias || db64) {
         SPC_TRY(cu(cudaMemsetAsync(ws.db_acc, 0, sizeof(double) * (size_t)w->c_out, s)));
         SPC_TRY(cu(launch_dbias(gy, ws.yrow, dy, ws.db_acc, s)));
     }
     const int64_t nb = (dbias && !db64) ? w->c_out : 0;   // dbias rounded with dw (one launch)
     if (!want_dx && !want_dw) return nb ? cu(launch_f64_to_f32_2(ws.db_acc, dbias, nb, nullptr, nullptr, 0, s)) : SPC_OK;
-    SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
+    SPC_TRY(cu(launch_row_index(gx, kin(x), x->nnz_dev, x->nnz, ws.xrow, s)));
     SPC_TRY(cu(launch_filter_table(kg, (int)w->c_in, (int)w->c_out, w->keys, w->values, w->nnz, ws.f.meta, ws.f.val,
                                    ws.f.off, ws.f.src, ws.f.scratch, s)));
     if (want_dx && t.n_ocg > 1 && x->nnz > 0) SPC_TRY(cu(cudaMemsetAsync(dx, 0, sizeof(float) * (size_t)x->nnz, s)));
     if (want_dw && w->nnz > 0) SPC_TRY(cu(cudaMemsetAsync(ws.dw_acc, 0, sizeof(double) * (size_t)w->nnz, s)));
-    SPC_TRY(cu(launch_conv_bwd(gx, gy, kg, t, x->keys, x->values, ws.xrow, y->keys, dy, ws.yrow, ws.f.meta, ws.f.val,
+    SPC_TRY(cu(launch_conv_bwd(gx, gy, kg, t, kin(x), x->values, ws.xrow, kin(y), dy, ws.yrow, ws.f.meta, ws.f.val,
                                ws.f.off, ws.f.src, dx, ws.dw_acc, want_dx, want_dw, s)));
     const int64_t nw = (want_dw && !dw64) ? w->nnz : 0;
     if (nb == 0 && nw == 0) return cu(cudaGetLastError());
@@ -473,7 +488,7 @@ spc_status_t sparse_conv_fwd_ex(const spc_map_t* x, const spc_filter_t* w, const
     int64_t cap;
     int use_gemm;
     SPC_TRY(fwd_plan(x, w, attn, k, variant, &gx, &gy, &kg, &t, &gp, &cap, &use_gemm));
-    SPC_TRY(check_out(y, cap));
+    SPC_TRY(check_out(y, cap, space_of(x, w->c_out)));
     const GemmPlan* gpp = use_gemm ? &gp : nullptr;
     Carver m(nullptr);
     carve_fwd(m, gx, gy, kg, t, w, attn, gpp);
@@ -486,17 +501,17 @@ spc_status_t sparse_conv_fwd_ex(const spc_map_t* x, const spc_filter_t* w, const
     }
     if (!use_gemm) {   // row index with the value guard fused (the scatter kernel reads the guard)
         SPC_TRY(cu(cudaMemsetAsync(ws.a.guard, 0, sizeof(int), s)));
-        SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s, x->values, ws.a.guard)));
+        SPC_TRY(cu(launch_row_index(gx, kin(x), x->nnz_dev, x->nnz, ws.xrow, s, x->values, ws.a.guard)));
         ws.a.guard_done = 1;
     } else {
-        SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
+        SPC_TRY(cu(launch_row_index(gx, kin(x), x->nnz_dev, x->nnz, ws.xrow, s)));
     }
     if (!use_gemm) {
         SPC_TRY(cu(launch_filter_table_fwd(kg, (int)w->c_in, (int)w->c_out, w->keys, w->values, w->nnz, ws.meta2,
                                            ws.val2, ws.off2, ws.scratch2, s)));
     }
     FwdArgs a = ws.a;
-    a.xkeys = x->keys;
+    a.xkeys = kin(x);
     a.x_nnz_dev = x->nnz_dev;
     a.x_nnz = x->nnz;
     a.xvals = x->values;
@@ -507,12 +522,12 @@ spc_status_t sparse_conv_fwd_ex(const spc_map_t* x, const spc_filter_t* w, const
     a.bias = bias;
     a.attn = attn;
     a.k = attn == SPC_ATTN_NONE ? gy.V : k;
-    a.out_keys = y->keys;
+    a.out_keys = kout(y);
     a.out_vals = y->values;
     a.out_nnz = y->nnz_dev;
     if (use_gemm) {
         GemmArgs g = ws.g;
-        g.xkeys = x->keys;
+        g.xkeys = kin(x);
         g.xvals = x->values;
         g.x_nnz_dev = x->nnz_dev;
         g.x_nnz = x->nnz;
@@ -564,7 +579,7 @@ spc_status_t sparse_conv_fwd_pass(const spc_map_t* x, const spc_filter_t* w, con
     int use_gemm;
     SPC_TRY(fwd_plan(x, w, attn, k, SPC_VARIANT_SCATTER, &gx, &gy, &kg, &t, &gp, &cap, &use_gemm));
     if (samples_per_pass < 0) return SPC_ERR_INVALID_ARG;
-    SPC_TRY(check_out(y, cap));
+    SPC_TRY(check_out(y, cap, space_of(x, w->c_out)));
     const int64_t spp = samples_per_pass == 0 ? std::max<int64_t>(gy.B, 1) : std::min<int64_t>(samples_per_pass, std::max<int64_t>(gy.B, 1));
     Geo gyp = gy;
     gyp.B = spp;
@@ -578,12 +593,12 @@ spc_status_t sparse_conv_fwd_pass(const spc_map_t* x, const spc_filter_t* w, con
         SPC_TRY(maybe_validate_filter(w, ws.flag, s));
     }
     SPC_TRY(cu(cudaMemsetAsync(ws.a.guard, 0, sizeof(int), s)));
-    SPC_TRY(cu(launch_row_index(gx, x->keys, x->nnz_dev, x->nnz, ws.xrow, s, x->values, ws.a.guard)));
+    SPC_TRY(cu(launch_row_index(gx, kin(x), x->nnz_dev, x->nnz, ws.xrow, s, x->values, ws.a.guard)));
     ws.a.guard_done = 1;
     SPC_TRY(cu(launch_filter_table_fwd(kg, (int)w->c_in, (int)w->c_out, w->keys, w->values, w->nnz, ws.meta2,
                                        ws.val2, ws.off2, ws.scratch2, s)));
     FwdArgs a = ws.a;
-    a.xkeys = x->keys;
+    a.xkeys = kin(x);
     a.x_nnz_dev = x->nnz_dev;
     a.x_nnz = x->nnz;
     a.xvals = x->values;
@@ -594,7 +609,7 @@ spc_status_t sparse_conv_fwd_pass(const spc_map_t* x, const spc_filter_t* w, con
     a.bias = bias;
     a.attn = attn;
     a.k = attn == SPC_ATTN_NONE ? gy.V : k;
-    a.out_keys = y->keys;
+    a.out_keys = kout(y);
     a.out_vals = y->values;
     a.out_nnz = y->nnz_dev;
     if (gy.B == 0) return cu(cudaMemsetAsync(y->nnz_dev, 0, sizeof(int64_t), s));
@@ -671,14 +686,14 @@ spc_status_t attention_topk(const spc_map_t* x, spc_attn_t attn, int64_t k, spc_
     int64_t cap;
     size_t need;
     SPC_TRY(spc_topk_query(x, attn, k, &cap, &need));
-    SPC_TRY(check_out(y, cap));
+    SPC_TRY(check_out(y, cap, space_of(x, x->channels)));
     if (!workspace || workspace_bytes < need) return SPC_ERR_WORKSPACE;
     const Geo g = geo_of(x, x->channels);
     Carver c(workspace);
     TopkWs ws = carve_topk(c, g, x->nnz);
     if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
-    SPC_TRY(cu(launch_row_index(g, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
-    return cu(launch_topk(x->keys, x->values, ws.xrow, g.R, g.B * g.C, attn, k, ws.seg_off, y->keys, y->values,
+    SPC_TRY(cu(launch_row_index(g, kin(x), x->nnz_dev, x->nnz, ws.xrow, s)));
+    return cu(launch_topk(kin(x), x->values, ws.xrow, g.R, g.B * g.C, attn, k, ws.seg_off, kout(y), y->values,
                           src_index, y->nnz_dev, s));
 }
 
@@ -696,12 +711,12 @@ spc_status_t sparse_relu(const spc_map_t* x, spc_map_out_t* y, int64_t* src_inde
     int64_t cap;
     size_t need;
     SPC_TRY(spc_relu_query(x, &cap, &need));
-    SPC_TRY(check_out(y, cap));
+    SPC_TRY(check_out(y, cap, space_of(x, x->channels)));
     if (!workspace || workspace_bytes < need) return SPC_ERR_WORKSPACE;
     Carver c(workspace);
     ReluWs ws = carve_relu(c, x->nnz);
     if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
-    return cu(launch_relu(x->keys, x->values, x->nnz_dev, x->nnz, ws.cnt, ws.off, ws.tmp, y->keys, y->values, src_index,
+    return cu(launch_relu(kin(x), x->values, x->nnz_dev, x->nnz, ws.cnt, ws.off, ws.tmp, kout(y), y->values, src_index,
                           y->nnz_dev, s));
 }
 
@@ -722,15 +737,15 @@ spc_status_t sparse_maxpool(const spc_map_t* x, const int64_t* stride, spc_map_o
     Geo g;
     PoolPlan p;
     SPC_TRY(pool_plan(x, stride, &g, &p));
-    SPC_TRY(check_out(y, x->nnz));
+    SPC_TRY(check_out(y, x->nnz, space_of(x, x->channels)));
     Carver m(nullptr);
     carve_pool(m, g, p);
     if (!workspace || workspace_bytes < m.used) return SPC_ERR_WORKSPACE;
     Carver c(workspace);
     PoolWs ws = carve_pool(c, g, p);
     if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
-    SPC_TRY(cu(launch_row_index(g, x->keys, x->nnz_dev, x->nnz, ws.xrow, s)));
-    return cu(launch_maxpool(g, p, x->keys, x->values, ws.xrow, ws.cnt, ws.off, ws.tmp, y->keys, y->values, argmax,
+    SPC_TRY(cu(launch_row_index(g, kin(x), x->nnz_dev, x->nnz, ws.xrow, s)));
+    return cu(launch_maxpool(g, p, kin(x), x->values, ws.xrow, ws.cnt, ws.off, ws.tmp, kout(y), y->values, argmax,
                              y->nnz_dev, s));
 }
 
@@ -777,13 +792,13 @@ spc_status_t sparse_to_dense(const spc_map_t* x, float* dense, cudaStream_t s) {
     SPC_TRY(check_map(x));
     if (!dense) return SPC_ERR_INVALID_ARG;
     const Geo g = geo_of(x, x->channels);
-    return cu(launch_to_dense(x->keys, x->values, x->nnz_dev, x->nnz, dense, g.B * g.C * g.V, s));
+    return cu(launch_to_dense(kin(x), x->values, x->nnz_dev, x->nnz, dense, g.B * g.C * g.V, s));
 }
 
 spc_status_t sparse_to_dense_bwd(const spc_map_t* x, const float* ddense, float* dvalues, cudaStream_t s) {
     SPC_TRY(check_map(x, false));
     if (!ddense || (x->nnz > 0 && !dvalues)) return SPC_ERR_INVALID_ARG;
-    return cu(launch_gather_dense(x->keys, x->nnz_dev, x->nnz, ddense, dvalues, s));
+    return cu(launch_gather_dense(kin(x), x->nnz_dev, x->nnz, ddense, dvalues, s));
 }
 
 // ------------------------------------------------------------------ memory model (f2)
@@ -814,6 +829,7 @@ bool fits32(const spc_map_t* x) {
 
 extern "C" spc_status_t sparse_keys_narrow(const spc_map_t* x, uint32_t* keys32, cudaStream_t s) {
     SPC_TRY(check_map(x, false));
+    if (x->key_bits == 32) return SPC_ERR_INVALID_ARG;   // already 32-bit
     if (!fits32(x)) return SPC_ERR_UNSUPPORTED;
     if (x->nnz > 0 && !keys32) return SPC_ERR_INVALID_ARG;
     return cu(launch_keys_narrow(x->keys, x->nnz_dev, x->nnz, keys32, s));

@@ -96,9 +96,9 @@ __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
 
 template <bool DX, bool DW, int THREADS>
 __global__ void __launch_bounds__(THREADS, 512 / THREADS)
-conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__ xkeys,
+conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
                 const float* __restrict__ xvals, const uint32_t* __restrict__ xrow,
-                const uint64_t* __restrict__ ykeys, const float* __restrict__ dy, const uint32_t* __restrict__ yrow,
+                Keys ykeys, const float* __restrict__ dy, const uint32_t* __restrict__ yrow,
                 const int2* __restrict__ wmeta, const float* __restrict__ wval, const int* __restrict__ woff,
                 const int* __restrict__ wsrc, float* __restrict__ dx, double* __restrict__ dw_acc) {
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -381,8 +381,8 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, const uint64_t* __restrict__
 
 template <bool DX, bool DW, int THREADS>
 static cudaError_t launch_bwd_tt(const Geo& gx, const Geo& gy, const KGeo& kg, const BwdTile& t,
-                                const uint64_t* xkeys, const float* xvals, const uint32_t* xrow,
-                                const uint64_t* ykeys, const float* dy, const uint32_t* yrow,
+                                Keys xkeys, const float* xvals, const uint32_t* xrow,
+                                Keys ykeys, const float* dy, const uint32_t* yrow,
                                 const int2* wmeta, const float* wval, const int* woff, const int* wsrc,
                                 float* dx, double* dw_acc, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(conv_bwd_kernel<DX, DW, THREADS>,
@@ -396,8 +396,8 @@ static cudaError_t launch_bwd_tt(const Geo& gx, const Geo& gy, const KGeo& kg, c
 
 template <bool DX, bool DW>
 static cudaError_t launch_bwd_t(const Geo& gx, const Geo& gy, const KGeo& kg, const BwdTile& t,
-                                const uint64_t* xkeys, const float* xvals, const uint32_t* xrow,
-                                const uint64_t* ykeys, const float* dy, const uint32_t* yrow,
+                                Keys xkeys, const float* xvals, const uint32_t* xrow,
+                                Keys ykeys, const float* dy, const uint32_t* yrow,
                                 const int2* wmeta, const float* wval, const int* woff, const int* wsrc,
                                 float* dx, double* dw_acc, cudaStream_t s) {
     if (t.threads == 256)
@@ -408,8 +408,8 @@ static cudaError_t launch_bwd_t(const Geo& gx, const Geo& gy, const KGeo& kg, co
 }
 
 cudaError_t launch_conv_bwd(const Geo& gx, const Geo& gy, const KGeo& kg, const BwdTile& t,
-                            const uint64_t* xkeys, const float* xvals, const uint32_t* xrow,
-                            const uint64_t* ykeys, const float* dy, const uint32_t* yrow,
+                            Keys xkeys, const float* xvals, const uint32_t* xrow,
+                            Keys ykeys, const float* dy, const uint32_t* yrow,
                             const int2* wmeta, const float* wval, const int* woff, const int* wsrc,
                             float* dx, double* dw_acc, bool want_dx, bool want_dw, cudaStream_t s) {
     if (gx.B == 0) return cudaSuccess;

@@ -487,7 +487,6 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
     const uint32_t accs = (uint32_t)__cvta_generic_to_shared(acc);
     const uint32_t safe = (uint32_t)(2 * kg.hy * ZR + t.cz) * 4u;   // interior word of slice 0
     const float invZ = 1.0f / (float)Z;
-    const uint32_t* xk32 = reinterpret_cast<const uint32_t*>(a.xkeys);   // little-endian low words
     // accumulator row of input row ylo (input row yi -> row yi - (y0 - 2hy))
     const int arow0 = ylo - y0 + 2 * kg.hy;
     const bool single = total <= kStageCap;          // the usual case: one chunk, descriptors known
@@ -517,7 +516,7 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
                             if (ioff[mid] <= pos) lo = mid; else hi = mid;
                         }
                         const uint32_t e = iglob[lo] + (uint32_t)(pos - ioff[lo]);
-                        kw[j] = xk32[2 * (size_t)e];
+                        kw[j] = a.xkeys.lo(e);   // low word of the key
                         vj[j] = a.xvals[e];
                         rbj[j] = ibase[lo];
                         dj[j] = pos - f0;
@@ -1071,7 +1070,7 @@ __global__ void __launch_bounds__(32 * kWriteWarps) fwd_write_kernel(FwdArgs a, 
             const unsigned m = __ballot_sync(kFull, keep);
             if (keep) {
                 const uint64_t q = out + __popc(m & ((1u << lane) - 1u));
-                a.out_keys[q] = kb + e[g].x;
+                a.out_keys.put(q, kb + e[g].x);
                 a.out_vals[q] = __uint_as_float(e[g].y);
             }
             out += __popc(m);

@@ -93,7 +93,7 @@ GemmPlan plan_gemm(const Geo& gx, const Geo& gy, const KGeo& kg) {
 
 // Dense zero-padded copy of the input, split into TF32 hi/lo halves, plus per-voxel occupancy
 // masks over ic (a stored 0.0 is occupied: structural support, reading R3).
-__global__ void gemm_densify_kernel(Geo gx, int Kp, const uint64_t* __restrict__ keys, const float* __restrict__ vals,
+__global__ void gemm_densify_kernel(Geo gx, int Kp, Keys keys, const float* __restrict__ vals,
                                     const int64_t* nnz_dev, int64_t bound, float* __restrict__ xhi,
                                     float* __restrict__ xlo, uint32_t* __restrict__ occ) {
     const int64_t n = load_n(nnz_dev, bound);
@@ -125,7 +125,7 @@ __device__ __forceinline__ int dz_slot(int v, int c, int Kp) {
     return (Kp & (Kp - 1)) == 0 ? v * Kp + (c ^ (v & (Kp - 1))) : v * Kp + c;
 }
 
-__global__ void __launch_bounds__(256) gemm_densify_tile_kernel(Geo gx, int Kp, int ny, const uint64_t* __restrict__ keys,
+__global__ void __launch_bounds__(256) gemm_densify_tile_kernel(Geo gx, int Kp, int ny, Keys keys,
                                                                  const float* __restrict__ vals,
                                                                  const uint32_t* __restrict__ xrow,
                                                                  float* __restrict__ xhi, float* __restrict__ xlo,

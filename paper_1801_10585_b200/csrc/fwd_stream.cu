@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(32 * kSWWarps) stream_write_kernel(FwdArgs a, 
             const unsigned m = __ballot_sync(kFull, keep);
             if (keep) {
                 const uint64_t o = out + __popc(m & ((1u << lane) - 1u));
-                a.out_keys[o] = kb + pp[q];
+                a.out_keys.put(o, kb + pp[q]);
                 a.out_vals[o] = __uint_as_float(vb[q]);
             }
             out += __popc(m);

@@ -29,7 +29,7 @@ __device__ __forceinline__ int32_t row_of(uint32_t key, uint32_t Z, uint32_t mag
 }
 
 template <typename K, typename I>   // key word, row / entry index type
-__global__ void __launch_bounds__(256) row_index_kernel(K Z, K magic, const uint64_t* __restrict__ keys,
+__global__ void __launch_bounds__(256) row_index_kernel(K Z, K magic, Keys keys,
                                                         const int64_t* nnz_dev, int64_t nbound,
                                                         uint32_t* __restrict__ row_ptr, I total_rows,
                                                         const float* __restrict__ vals, int* __restrict__ guard) {
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(256) row_index_kernel(K Z, K magic, const uint
     }
 }
 
-cudaError_t launch_row_index(const Geo& g, const uint64_t* keys, const int64_t* nnz_dev, int64_t nbound,
+cudaError_t launch_row_index(const Geo& g, Keys keys, const int64_t* nnz_dev, int64_t nbound,
                              uint32_t* row_ptr, cudaStream_t s, const float* vals, int* guard) {
     const int64_t total_rows = g.B * g.C * g.R;
     const int bs = 256;
@@ -303,7 +303,7 @@ cudaError_t launch_scan_u32(const uint32_t* in, uint64_t* out, int64_t n, int64_
 }
 
 // --------------------------------------------------------------------------- validation
-__global__ void validate_kernel(const uint64_t* __restrict__ keys, const int64_t* nnz_dev, int64_t nbound,
+__global__ void validate_kernel(Keys keys, const int64_t* nnz_dev, int64_t nbound,
                                 uint64_t limit, int* flag) {
     const int64_t n = load_n(nnz_dev, nbound);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -312,7 +312,7 @@ __global__ void validate_kernel(const uint64_t* __restrict__ keys, const int64_t
     }
 }
 
-cudaError_t launch_validate(const uint64_t* keys, const int64_t* nnz_dev, int64_t nbound, uint64_t limit,
+cudaError_t launch_validate(Keys keys, const int64_t* nnz_dev, int64_t nbound, uint64_t limit,
                             int* flag, cudaStream_t s) {
     { SPC_PHASE("validate", s, 1); validate_kernel<<<592, 256, 0, s>>>(keys, nnz_dev, nbound, limit, flag); }
     return cudaGetLastError();
@@ -375,21 +375,21 @@ cudaError_t launch_scatter_grad(const int64_t* src, const float* dy, int64_t n_o
 // Table 2 "sparseToDense()": the key layout ((b*C + c)*V + row_major(p)) (reading R11)
 // is the linear index of the dense [B, C, dims] tensor, so the bridge is a zero fill plus a
 // scatter of the stored values; its backward gathers the dense gradient at the stored keys.
-__global__ void to_dense_kernel(const uint64_t* __restrict__ keys, const float* __restrict__ vals,
+__global__ void to_dense_kernel(Keys keys, const float* __restrict__ vals,
                                 const int64_t* nnz_dev, int64_t bound, float* __restrict__ dense) {
     const int64_t n = load_n(nnz_dev, bound);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         dense[keys[i]] = vals[i];
 }
 
-__global__ void gather_dense_kernel(const uint64_t* __restrict__ keys, const int64_t* nnz_dev, int64_t bound,
+__global__ void gather_dense_kernel(Keys keys, const int64_t* nnz_dev, int64_t bound,
                                     const float* __restrict__ ddense, float* __restrict__ dvals) {
     const int64_t n = load_n(nnz_dev, bound);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         dvals[i] = ddense[keys[i]];
 }
 
-cudaError_t launch_to_dense(const uint64_t* keys, const float* vals, const int64_t* nnz_dev, int64_t bound,
+cudaError_t launch_to_dense(Keys keys, const float* vals, const int64_t* nnz_dev, int64_t bound,
                             float* dense, int64_t cells, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(dense, 0, (size_t)cells * sizeof(float), s);
     if (e != cudaSuccess || bound == 0) return e;
@@ -398,7 +398,7 @@ cudaError_t launch_to_dense(const uint64_t* keys, const float* vals, const int64
     return cudaGetLastError();
 }
 
-cudaError_t launch_gather_dense(const uint64_t* keys, const int64_t* nnz_dev, int64_t bound, const float* ddense,
+cudaError_t launch_gather_dense(Keys keys, const int64_t* nnz_dev, int64_t bound, const float* ddense,
                                 float* dvals, cudaStream_t s) {
     if (bound == 0) return cudaSuccess;
     const unsigned grid = (unsigned)std::min<int64_t>((bound + 255) / 256, num_sms() * 16);

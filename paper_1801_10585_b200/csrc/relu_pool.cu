@@ -31,10 +31,10 @@ __global__ void __launch_bounds__(kReluThreads) relu_count_kernel(const float* _
 // Write pass: warp w of a chunk owns its 512 consecutive entries (16 groups of 32, coalesced);
 // one ballot per group gives each kept entry its slot, warp totals are scanned across the block,
 // and keys / values / source indices are stored with consecutive addresses per group.
-__global__ void __launch_bounds__(kReluThreads) relu_write_kernel(const uint64_t* __restrict__ keys,
+__global__ void __launch_bounds__(kReluThreads) relu_write_kernel(Keys keys,
                                                                   const float* __restrict__ vals, const int64_t* nnz_dev,
                                                                   int64_t nbound, const uint64_t* __restrict__ off,
-                                                                  uint64_t* __restrict__ ok, float* __restrict__ ov,
+                                                                  KeysOut ok, float* __restrict__ ov,
                                                                   int64_t* __restrict__ osrc) {
     const int64_t n = load_n(nnz_dev, nbound);
     const int64_t base = (int64_t)blockIdx.x * kReluChunk;
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kReluThreads) relu_write_kernel(const uint64_t
         if (v[u] > 0.0f) {
             const int64_t i = w0 + 32 * u + lane;
             const uint64_t o = pos + (uint32_t)__popc(m[u] & lt);
-            ok[o] = k[u];
+            ok.put(o, k[u]);
             ov[o] = v[u];
             if (osrc) osrc[o] = i;
         }
@@ -78,9 +78,9 @@ __global__ void __launch_bounds__(kReluThreads) relu_write_kernel(const uint64_t
     }
 }
 
-cudaError_t launch_relu(const uint64_t* keys, const float* vals, const int64_t* nnz_dev, int64_t nbound,
+cudaError_t launch_relu(Keys keys, const float* vals, const int64_t* nnz_dev, int64_t nbound,
                         uint32_t* chunk_cnt, uint64_t* chunk_off, uint64_t* scan_tmp,
-                        uint64_t* out_keys, float* out_vals, int64_t* out_src, int64_t* out_nnz, cudaStream_t s) {
+                        KeysOut out_keys, float* out_vals, int64_t* out_src, int64_t* out_nnz, cudaStream_t s) {
     const int64_t nch = (nbound + kReluChunk - 1) / kReluChunk;
     if (nch == 0) return cudaMemsetAsync(out_nnz, 0, sizeof(int64_t), s);
     { SPC_PHASE("relu_count", s, 1); relu_count_kernel<<<(unsigned)nch, kReluThreads, 0, s>>>(vals, nnz_dev, nbound, chunk_cnt); }
@@ -143,7 +143,7 @@ __device__ __forceinline__ uint32_t udiv(uint32_t x, uint32_t d, uint32_t m) {
 // member entries of a tile: the sx key runs, four loads in flight per thread;
 // f(cell, entry, value) for each (value loaded only when LOADV)
 template <bool LOADV, typename F>
-__device__ __forceinline__ void pool_tile_members(const Geo& g, const PoolPlan& p, const uint64_t* __restrict__ keys,
+__device__ __forceinline__ void pool_tile_members(const Geo& g, const PoolPlan& p, Keys keys,
                                                   const float* __restrict__ vals,
                                                   const uint32_t* __restrict__ row_ptr, int64_t seg, int pw, int px,
                                                   int ya, int yb, F f) {
@@ -197,7 +197,7 @@ __device__ __forceinline__ PoolTileId pool_tile_id(const Geo& g, const PoolPlan&
 
 // count pass: occupied clusters of the tile (a 4096-bit occupancy mask)
 __global__ void __launch_bounds__(kTileThreads)
-pool_tile_count_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, const uint32_t* __restrict__ row_ptr,
+pool_tile_count_kernel(Geo g, PoolPlan p, Keys keys, const uint32_t* __restrict__ row_ptr,
                        uint32_t* __restrict__ item_cnt) {
     __shared__ uint32_t occ[kTileCells / 32];
     __shared__ uint32_t sm[33];
@@ -218,9 +218,9 @@ pool_tile_count_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, con
 // 0); the occupied clusters are listed in cell order from the occupancy mask (one scan over its
 // 128 words) and written with coalesced stores.
 __global__ void __launch_bounds__(kTileThreads)
-pool_tile_write_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, const float* __restrict__ vals,
+pool_tile_write_kernel(Geo g, PoolPlan p, Keys keys, const float* __restrict__ vals,
                        const uint32_t* __restrict__ row_ptr, const uint64_t* __restrict__ item_off,
-                       uint64_t* __restrict__ ok, float* __restrict__ ov, int64_t* __restrict__ oarg) {
+                       KeysOut ok, float* __restrict__ ov, int64_t* __restrict__ oarg) {
     __shared__ __align__(16) unsigned long long best[kTileCells];
     __shared__ uint32_t occ[kTileCells / 32];
     __shared__ uint16_t cells[kTileCells];
@@ -266,7 +266,7 @@ pool_tile_write_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, con
         // the maximum's value from its order-preserving code; +-0 (the code cannot tell them
         // apart) from the entry itself
         const float mv = from_orderable((uint32_t)(bst >> 32));
-        ok[o0 + q] = pbase + cell;
+        ok.put(o0 + q, pbase + cell);
         ov[o0 + q] = mv != 0.0f ? mv : vals[a];
         if (oarg) oarg[o0 + q] = a;
     }
@@ -274,9 +274,9 @@ pool_tile_write_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, con
 
 template <bool WRITE>
 __global__ void __launch_bounds__(kPoolThreads)
-pool_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, const float* __restrict__ vals,
+pool_kernel(Geo g, PoolPlan p, Keys keys, const float* __restrict__ vals,
             const uint32_t* __restrict__ row_ptr, uint32_t* __restrict__ item_cnt,
-            const uint64_t* __restrict__ item_off, uint64_t* __restrict__ ok, float* __restrict__ ov,
+            const uint64_t* __restrict__ item_off, KeysOut ok, float* __restrict__ ov,
             int64_t* __restrict__ oarg) {
     __shared__ uint32_t s_best[kPoolWarps][kPoolZChunk];
     __shared__ uint32_t s_arg[kPoolWarps][kPoolZChunk];
@@ -350,7 +350,7 @@ pool_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, const float* _
         if (occ) {
             const uint64_t o = pos + __popc(m & ((1u << lane) - 1u));
             const uint32_t a = arg[i];
-            ok[o] = pbase + i;
+            ok.put(o, pbase + i);
             ov[o] = vals[a];
             if (oarg) oarg[o] = a;
         }
@@ -358,9 +358,9 @@ pool_kernel(Geo g, PoolPlan p, const uint64_t* __restrict__ keys, const float* _
     }
 }
 
-cudaError_t launch_maxpool(const Geo& g, const PoolPlan& p, const uint64_t* keys, const float* vals,
+cudaError_t launch_maxpool(const Geo& g, const PoolPlan& p, Keys keys, const float* vals,
                            const uint32_t* row_ptr, uint32_t* item_cnt, uint64_t* item_off, uint64_t* scan_tmp,
-                           uint64_t* out_keys, float* out_vals, int64_t* out_arg, int64_t* out_nnz, cudaStream_t s) {
+                           KeysOut out_keys, float* out_vals, int64_t* out_arg, int64_t* out_nnz, cudaStream_t s) {
     if (p.items == 0) return cudaMemsetAsync(out_nnz, 0, sizeof(int64_t), s);
     if (p.tiled) {
         const unsigned tg = (unsigned)p.items;

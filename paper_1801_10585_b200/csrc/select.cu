@@ -42,8 +42,8 @@ __global__ void topk_offsets_kernel(const uint32_t* __restrict__ row_ptr, int64_
 }
 
 __global__ void __launch_bounds__(kTkThreads, 4)
-topk_seg_kernel(const uint64_t* __restrict__ keys, const float* __restrict__ vals, const uint32_t* __restrict__ row_ptr,
-                int64_t R, int attn, int64_t k, const uint64_t* __restrict__ seg_off, uint64_t* __restrict__ ok,
+topk_seg_kernel(Keys keys, const float* __restrict__ vals, const uint32_t* __restrict__ row_ptr,
+                int64_t R, int attn, int64_t k, const uint64_t* __restrict__ seg_off, KeysOut ok,
                 float* __restrict__ ov, int64_t* __restrict__ osrc) {
     __shared__ uint32_t h[kSelBins];
     __shared__ uint32_t sm[33];
@@ -214,7 +214,7 @@ topk_seg_kernel(const uint64_t* __restrict__ keys, const float* __restrict__ val
             if ((kb[g] >> lane) & 1u) {
                 const uint32_t i = w0 + 32u * g + lane;
                 const uint64_t o = pos + (uint32_t)__popc(kb[g] & lt);
-                ok[o] = kk[g];
+                ok.put(o, kk[g]);
                 ov[o] = __uint_as_float(bits[g]);
                 if (osrc) osrc[o] = (int64_t)i;
             }
@@ -225,8 +225,8 @@ topk_seg_kernel(const uint64_t* __restrict__ keys, const float* __restrict__ val
     }
 }
 
-cudaError_t launch_topk(const uint64_t* keys, const float* vals, const uint32_t* row_ptr, int64_t R, int64_t nseg,
-                        int attn, int64_t k, uint64_t* seg_off, uint64_t* out_keys, float* out_vals, int64_t* out_src,
+cudaError_t launch_topk(Keys keys, const float* vals, const uint32_t* row_ptr, int64_t R, int64_t nseg,
+                        int attn, int64_t k, uint64_t* seg_off, KeysOut out_keys, float* out_vals, int64_t* out_src,
                         int64_t* out_nnz, cudaStream_t s) {
     if (nseg == 0) return cudaMemsetAsync(out_nnz, 0, sizeof(int64_t), s);
     { SPC_PHASE("topk_offsets", s, 1); topk_offsets_kernel<<<1, 1024, 0, s>>>(row_ptr, R, nseg, k, seg_off, out_nnz); }

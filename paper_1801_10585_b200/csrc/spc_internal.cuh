@@ -19,6 +19,35 @@ namespace spc {
 constexpr uint32_t kAbsent = 0x7fbfffffu;
 constexpr uint32_t kNegZero = 0x80000000u;   // accumulator marker of the -0 mode (conv_fwd)
 
+// Key arrays of either width (spc_map_t::key_bits): 64-bit keys, or the 32-bit "Sparse 32"
+// storage of Table 1 (valid below 2^32 keys). Indexing reads one key as uint64.
+struct Keys {
+    const void* p;
+    int k32;
+    __host__ __device__ Keys() : p(nullptr), k32(0) {}
+    __host__ __device__ Keys(const uint64_t* q) : p(q), k32(0) {}
+    __host__ __device__ Keys(const void* q, int is32) : p(q), k32(is32) {}
+    __device__ __forceinline__ uint64_t operator[](int64_t i) const {
+        return k32 ? (uint64_t)__ldg(static_cast<const uint32_t*>(p) + i) : __ldg(static_cast<const uint64_t*>(p) + i);
+    }
+    // low 32 bits of key i (the whole key in 32-bit storage)
+    __device__ __forceinline__ uint32_t lo(int64_t i) const {
+        return k32 ? __ldg(static_cast<const uint32_t*>(p) + i) : __ldg(static_cast<const uint32_t*>(p) + 2 * i);
+    }
+    __host__ __device__ explicit operator bool() const { return p != nullptr; }
+};
+struct KeysOut {
+    void* p;
+    int k32;
+    __host__ __device__ KeysOut() : p(nullptr), k32(0) {}
+    __host__ __device__ KeysOut(uint64_t* q) : p(q), k32(0) {}
+    __host__ __device__ KeysOut(void* q, int is32) : p(q), k32(is32) {}
+    __device__ __forceinline__ void put(int64_t i, uint64_t v) const {
+        if (k32) static_cast<uint32_t*>(p)[i] = (uint32_t)v;
+        else static_cast<uint64_t*>(p)[i] = v;
+    }
+};
+
 // Geometry of a feature map with its spatial dims padded to rank 4 (leading 1s):
 // key = seg*V + ((w*X + x)*Y + y)*Z + z, seg = b*C + c. A "row" is (seg, w, x, y): the Z
 // consecutive keys of the last spatial dimension; a "plane" is (w, x): P = w*X + x, so that rank
@@ -109,7 +138,7 @@ struct PhaseScope {
 // Row index: row_ptr[r] = first entry with key >= r*Z, r in [0, B*C*R]; workspace
 // (B*C*R + 1) uint32 words. Requires nnz < 2^32. With vals / guard: also the forward's value
 // guard (*guard = 1 when some stored |x| < 2^-50; *guard must be zeroed before).
-cudaError_t launch_row_index(const Geo& g, const uint64_t* keys, const int64_t* nnz_dev, int64_t nnz_bound,
+cudaError_t launch_row_index(const Geo& g, Keys keys, const int64_t* nnz_dev, int64_t nnz_bound,
                              uint32_t* row_ptr, cudaStream_t s, const float* vals = nullptr, int* guard = nullptr);
 
 // Filter table in ic-major order. meta[j] = {oc, packed offset}; val[j]; off[ic*(c_out+1)+oc]
@@ -145,7 +174,7 @@ struct FwdSeg {
     int32_t keep_all;    // 1: keep every support entry
 };
 struct FwdArgs {
-    const uint64_t* xkeys;
+    Keys xkeys;
     const int64_t* x_nnz_dev;        // device-side input count (or null: x_nnz)
     int64_t x_nnz;
     const float* xvals;
@@ -179,7 +208,7 @@ struct FwdArgs {
     uint64_t* chunk_stg;             // [nseg * nchunk] first staged entry of each chunk
     uint32_t* chunk_ge;              // [nseg * nchunk] staged entries of each chunk
     uint64_t* seg_off;               // [nseg + 1] output offsets
-    uint64_t* out_keys;
+    KeysOut out_keys;
     float* out_vals;
     int64_t* out_nnz;
     // batch-sliced passes (sparse_conv_fwd_pass): this pass covers samples b0 .. b0 + gy.B - 1;
@@ -223,7 +252,7 @@ struct GemmPlan {
     size_t slab_bytes, bstage_bytes, slab_smem;
 };
 struct GemmArgs {
-    const uint64_t* xkeys;
+    Keys xkeys;
     const float* xvals;
     const int64_t* x_nnz_dev;
     int64_t x_nnz;
@@ -275,8 +304,8 @@ struct BwdTile {
 };
 BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int n_w_max_group);
 cudaError_t launch_conv_bwd(const Geo& gx, const Geo& gy, const KGeo& kg, const BwdTile& t,
-                            const uint64_t* xkeys, const float* xvals, const uint32_t* xrow,
-                            const uint64_t* ykeys, const float* dy, const uint32_t* yrow,
+                            Keys xkeys, const float* xvals, const uint32_t* xrow,
+                            Keys ykeys, const float* dy, const uint32_t* yrow,
                             const int2* wmeta, const float* wval, const int* woff, const int* wsrc,
                             float* dx, double* dw_acc, bool want_dx, bool want_dw, cudaStream_t s);
 cudaError_t launch_dbias(const Geo& gy, const uint32_t* yrow, const float* dy, double* db_acc, cudaStream_t s);
@@ -288,14 +317,14 @@ cudaError_t launch_f64_to_f32_2(const double* a, float* b, int64_t n, const doub
 constexpr int kSelBins = 2048;    // 11-bit score digits
 // Standalone attention over a COO map (select.cu): segment s = entries row_ptr[s*R] ..
 // row_ptr[(s+1)*R]; workspace seg_off [nseg].
-cudaError_t launch_topk(const uint64_t* keys, const float* vals, const uint32_t* row_ptr, int64_t R, int64_t nseg,
-                        int attn, int64_t k, uint64_t* seg_off, uint64_t* out_keys, float* out_vals, int64_t* out_src,
+cudaError_t launch_topk(Keys keys, const float* vals, const uint32_t* row_ptr, int64_t R, int64_t nseg,
+                        int attn, int64_t k, uint64_t* seg_off, KeysOut out_keys, float* out_vals, int64_t* out_src,
                         int64_t* out_nnz, cudaStream_t s);
 
 // --------------------------------------------------------------------- relu / pool / misc
-cudaError_t launch_relu(const uint64_t* keys, const float* vals, const int64_t* nnz_dev, int64_t nbound,
+cudaError_t launch_relu(Keys keys, const float* vals, const int64_t* nnz_dev, int64_t nbound,
                         uint32_t* chunk_cnt, uint64_t* chunk_off, uint64_t* scan_tmp,
-                        uint64_t* out_keys, float* out_vals, int64_t* out_src, int64_t* out_nnz, cudaStream_t s);
+                        KeysOut out_keys, float* out_vals, int64_t* out_src, int64_t* out_nnz, cudaStream_t s);
 struct PoolPlan {
     int sw, sx, sy, sz;
     int PW, PX, PY, PZ;   // pooled dims
@@ -307,9 +336,9 @@ struct PoolPlan {
     uint32_t mZ, msy, msz;  // floor((2^32 - 1) / d) for d = Z, sy, sz (division by multiply-high)
 };
 PoolPlan plan_pool(const Geo& g, int sw, int sx, int sy, int sz);
-cudaError_t launch_maxpool(const Geo& g, const PoolPlan& p, const uint64_t* keys, const float* vals,
+cudaError_t launch_maxpool(const Geo& g, const PoolPlan& p, Keys keys, const float* vals,
                            const uint32_t* row_ptr, uint32_t* item_cnt, uint64_t* item_off, uint64_t* scan_tmp,
-                           uint64_t* out_keys, float* out_vals, int64_t* out_arg, int64_t* out_nnz, cudaStream_t s);
+                           KeysOut out_keys, float* out_vals, int64_t* out_arg, int64_t* out_nnz, cudaStream_t s);
 cudaError_t launch_scatter_grad(const int64_t* src, const float* dy, int64_t n_out_bound, const int64_t* n_out_dev,
                                 float* dx, int64_t n_in, cudaStream_t s);
 
@@ -331,15 +360,15 @@ cudaError_t launch_prune(const uint64_t* keys, const float* w, const float* acc,
                          uint64_t* ws, cudaStream_t s);
 
 // sparseToDense bridge (index.cu)
-cudaError_t launch_to_dense(const uint64_t* keys, const float* vals, const int64_t* nnz_dev, int64_t bound,
+cudaError_t launch_to_dense(Keys keys, const float* vals, const int64_t* nnz_dev, int64_t bound,
                             float* dense, int64_t cells, cudaStream_t s);
-cudaError_t launch_gather_dense(const uint64_t* keys, const int64_t* nnz_dev, int64_t bound, const float* ddense,
+cudaError_t launch_gather_dense(Keys keys, const int64_t* nnz_dev, int64_t bound, const float* ddense,
                                 float* dvals, cudaStream_t s);
 
 cudaError_t launch_keys_narrow(const uint64_t* keys, const int64_t* nnz_dev, int64_t bound, uint32_t* out, cudaStream_t s);
 cudaError_t launch_keys_widen(const uint32_t* keys, const int64_t* nnz_dev, int64_t bound, uint64_t* out, cudaStream_t s);
 // Validation (SPC_VALIDATE=1): flag = 1 if keys are not strictly increasing or out of range.
-cudaError_t launch_validate(const uint64_t* keys, const int64_t* nnz_dev, int64_t nbound, uint64_t limit,
+cudaError_t launch_validate(Keys keys, const int64_t* nnz_dev, int64_t nbound, uint64_t limit,
                             int* flag, cudaStream_t s);
 
 }  // namespace spc

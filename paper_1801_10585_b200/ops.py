@@ -29,7 +29,7 @@ def _ptr(t: Optional[torch.Tensor]):
 class SparseMap:
     """Device COO feature map: key = ((b*C + c)*V + row_major(p)) (include/spconv.h)."""
 
-    keys: torch.Tensor          # int64 (bit pattern of the uint64 keys), [capacity]
+    keys: torch.Tensor          # int64 (bit pattern of the uint64 keys) or int32 ("Sparse 32"), [capacity]
     values: torch.Tensor        # float32 [capacity]
     batch: int
     channels: int
@@ -72,18 +72,37 @@ class SparseMap:
         m.nnz_dev = None if self.nnz_dev is None else self.nnz_dev.data_ptr()
         m.keys = self.keys.data_ptr() if self.keys.numel() else None
         m.values = self.values.data_ptr() if self.values.numel() else None
+        m.key_bits = self.key_bits
         return m
 
+    @property
+    def key_bits(self) -> int:
+        """32 for int32 key storage (Table 1 "Sparse 32"), else 64."""
+        return 32 if self.keys.dtype == torch.int32 else 64
+
+    def to_key_bits(self, bits: int) -> "SparseMap":
+        """Same map with its keys stored in `bits` (32 / 64) bits (sparse_keys_narrow / _widen)."""
+        if bits == self.key_bits:
+            return self
+        if bits == 32:
+            k = keys_narrow(self)
+        else:
+            k = keys_widen(self.keys[:self.nnz_bound], self.nnz_bound, self.nnz_dev)
+        return SparseMap(k, self.values, self.batch, self.channels, self.dims, self.nnz_bound, self.nnz_dev)
+
     @staticmethod
-    def from_arrays(keys, values, batch: int, channels: int, dims: Sequence[int], device="cuda") -> "SparseMap":
-        """Upload host arrays (numpy uint64 keys / float32 values, or tensors)."""
+    def from_arrays(keys, values, batch: int, channels: int, dims: Sequence[int], device="cuda",
+                    key_bits: int = 64) -> "SparseMap":
+        """Upload host arrays (numpy uint64 keys / float32 values, or tensors); key_bits=32 stores
+        the keys as int32 ("Sparse 32", valid below 2^32 keys)."""
         if not isinstance(keys, torch.Tensor):
             import numpy as np
 
-            keys = torch.from_numpy(np.ascontiguousarray(keys).view(np.int64))
+            keys = np.ascontiguousarray(keys)
+            keys = torch.from_numpy(keys.astype(np.uint32).view(np.int32) if key_bits == 32 else keys.view(np.int64))
         if not isinstance(values, torch.Tensor):
             values = torch.from_numpy(values)
-        k = keys.to(device=device, dtype=torch.int64).contiguous()
+        k = keys.to(device=device, dtype=torch.int32 if key_bits == 32 else torch.int64).contiguous()
         v = values.to(device=device, dtype=torch.float32).contiguous()
         return SparseMap(k, v, int(batch), int(channels), tuple(int(d) for d in dims), int(k.numel()), None)
 
@@ -135,8 +154,8 @@ def _workspace(nbytes: int, device) -> torch.Tensor:
     return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
 
 
-def _out(cap: int, device) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor, MapOutT]:
-    keys = torch.empty(max(cap, 1), dtype=torch.int64, device=device)
+def _out(cap: int, device, key_bits: int = 64) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor, MapOutT]:
+    keys = torch.empty(max(cap, 1), dtype=torch.int32 if key_bits == 32 else torch.int64, device=device)
     vals = torch.empty(max(cap, 1), dtype=torch.float32, device=device)
     nnz = torch.zeros(1, dtype=torch.int64, device=device)
     o = MapOutT()
@@ -144,6 +163,7 @@ def _out(cap: int, device) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor, Ma
     o.keys = keys.data_ptr()
     o.values = vals.data_ptr()
     o.nnz_dev = nnz.data_ptr()
+    o.key_bits = int(key_bits)
     return keys, vals, nnz, o
 
 
@@ -156,7 +176,8 @@ class FwdPlan:
     variant is picked per layer from measurement")."""
 
     def __init__(self, x: SparseMap, w: SparseFilter, attn: str = "magnitude", k: int = 0, variant: str = "auto",
-                 bias: Optional[torch.Tensor] = None, samples_per_pass: Optional[int] = None):
+                 bias: Optional[torch.Tensor] = None, samples_per_pass: Optional[int] = None,
+                 key_bits: Optional[int] = None):
         lib = load()
         self.attn = ATTN[attn]
         self.k = int(k)
@@ -183,7 +204,8 @@ class FwdPlan:
         self.capacity = int(cap.value)
         self.ws_bytes = int(ws.value)
         self.ws = _workspace(ws.value, dev)
-        self.keys, self.vals, self.nnz, self.out = _out(self.capacity, dev)
+        self.key_bits = x.key_bits if key_bits is None else int(key_bits)   # output keys: as the input by default
+        self.keys, self.vals, self.nnz, self.out = _out(self.capacity, dev, self.key_bits)
         self.c_out = w.c_out
         self.batch, self.dims = x.batch, x.dims
 
@@ -239,11 +261,13 @@ def select_variant(x: SparseMap, w: SparseFilter, bias=None, attn: str = "magnit
 
 
 def sparse_conv_fwd(x: SparseMap, w: SparseFilter, bias: Optional[torch.Tensor] = None, attn: str = "magnitude",
-                    k: int = 0, stream=None, variant: str = "auto", samples_per_pass: Optional[int] = None) -> SparseMap:
+                    k: int = 0, stream=None, variant: str = "auto", samples_per_pass: Optional[int] = None,
+                    key_bits: Optional[int] = None) -> SparseMap:
     """Alg. 1 (P:51-90). attn in {"none", "magnitude", "raw"}; k entries kept per (b, oc);
     variant in {"auto", "scatter", "gemm", "measure"} (FwdPlan); samples_per_pass bounds the
-    workspace to that many samples' buffers (sparse_conv_fwd_pass, scatter variant)."""
-    return FwdPlan(x, w, attn, k, variant, bias, samples_per_pass)(x, w, bias, stream)
+    workspace to that many samples' buffers (sparse_conv_fwd_pass, scatter variant); key_bits: the
+    output's key width (default: the input's)."""
+    return FwdPlan(x, w, attn, k, variant, bias, samples_per_pass, key_bits)(x, w, bias, stream)
 
 
 class BwdPlan:
@@ -324,7 +348,7 @@ def attention_topk(x: SparseMap, attn: str, k: int, stream=None) -> Tuple[Sparse
     a = ATTN[attn]
     check("spc_topk_query", lib.spc_topk_query(C.byref(xs), a, int(k), C.byref(cap), C.byref(ws)))
     dev = x.values.device
-    keys, vals, nnz, o = _out(int(cap.value), dev)
+    keys, vals, nnz, o = _out(int(cap.value), dev, x.key_bits)
     src = torch.empty(max(int(cap.value), 1), dtype=torch.int64, device=dev)
     w = _workspace(ws.value, dev)
     check("attention_topk", lib.attention_topk(C.byref(xs), a, int(k), C.byref(o), _ptr(src), _ptr(w), w.numel(),
@@ -340,7 +364,7 @@ def sparse_relu(x: SparseMap, stream=None) -> Tuple[SparseMap, torch.Tensor]:
     xs = x.c_struct()
     check("spc_relu_query", lib.spc_relu_query(C.byref(xs), C.byref(cap), C.byref(ws)))
     dev = x.values.device
-    keys, vals, nnz, o = _out(int(cap.value), dev)
+    keys, vals, nnz, o = _out(int(cap.value), dev, x.key_bits)
     src = torch.empty(max(int(cap.value), 1), dtype=torch.int64, device=dev)
     w = _workspace(ws.value, dev)
     check("sparse_relu", lib.sparse_relu(C.byref(xs), C.byref(o), _ptr(src), _ptr(w), w.numel(), _stream(stream)))
@@ -356,7 +380,7 @@ def sparse_maxpool(x: SparseMap, stride: Sequence[int], stream=None) -> Tuple[Sp
     st = (C.c_int64 * len(stride))(*[int(s) for s in stride])
     check("spc_maxpool_query", lib.spc_maxpool_query(C.byref(xs), C.cast(st, C.c_void_p), C.byref(cap), C.byref(ws)))
     dev = x.values.device
-    keys, vals, nnz, o = _out(int(cap.value), dev)
+    keys, vals, nnz, o = _out(int(cap.value), dev, x.key_bits)
     arg = torch.empty(max(int(cap.value), 1), dtype=torch.int64, device=dev)
     w = _workspace(ws.value, dev)
     check("sparse_maxpool", lib.sparse_maxpool(C.byref(xs), C.cast(st, C.c_void_p), C.byref(o), _ptr(arg), _ptr(w),

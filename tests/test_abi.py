@@ -210,3 +210,14 @@ def test_keys_narrow_rejects_large_key_space():
     m, _ = _c4_structs()
     m.batch, m.channels = 256, 256   # 2^21 * 2^16 = 2^37 keys
     assert lib.sparse_keys_narrow(C.byref(m), C.c_void_p(64), None) == 6
+
+
+def test_32bit_keys_need_a_small_key_space():
+    """key_bits = 32 is accepted only when batch*channels*prod(dims) <= 2^32 (Table 1's "-")."""
+    m, f = _c4_structs()
+    m.key_bits = 32                      # 64 * 8 * 128^3 = 2^30: fits
+    assert _query(m, f)[0] == 0
+    m.dims[0] = m.dims[1] = m.dims[2] = 1024   # 64 * 8 * 2^30 > 2^32
+    assert _query(m, f)[0] == 6
+    m.key_bits = 16
+    assert _query(m, f)[0] == 1

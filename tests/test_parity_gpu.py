@@ -915,3 +915,63 @@ def test_fwd_tiny_values_keep_structural_support(cuda_lib):
                                 samples_per_pass=1)
         pk, pv = (host(t) for t in y.trimmed())
         np.testing.assert_array_equal(pk.view(np.uint64), fk)
+
+
+# --------------------------------------------- 32-bit key storage (Table 1 "Sparse 32")
+def _keys_u64(t):
+    a = host(t)
+    return a.view(np.uint32).astype(np.uint64) if a.dtype == np.int32 else a.view(np.uint64)
+
+
+@pytest.mark.parametrize("case", [FWD_CASES[4], FWD_CASES[7], SAMPLED_CASES[1], RANK4_CASES[0]], ids=lambda c: c[0])
+@pytest.mark.parametrize("attn", ["none", "magnitude"])
+def test_fwd_bwd_32bit_keys(cuda_lib, case, attn):
+    """Input and output maps with uint32 keys (spc_map_t.key_bits = 32): the forward, the
+    backward and the 64 <-> 32-bit conversions give the oracle's result bit for bit."""
+    spc = cuda_lib
+    _, dims, B, ci, co, ks, rd, rf = case
+    x = uniform_map(B, ci, dims, rd, 4700, values="dyadic")
+    w = sparse_filter(ci, co, ks, rf, 4701, values="dyadic")
+    bias = bias_vector(co, 4702, values="dyadic")
+    V = int(np.prod(dims))
+    k = max(1, V // 20)
+    X32 = spc.SparseMap.from_arrays(x.keys, x.values, x.batch, x.channels, x.dims, key_bits=32)
+    assert X32.key_bits == 32
+    Y = spc.sparse_conv_fwd(X32, dev_filter(spc, w), torch.from_numpy(bias).cuda(), attn, k, variant="scatter")
+    assert Y.key_bits == 32
+    yk, yv = Y.trimmed()
+    ok_, ov, _, _ = ora.conv_fwd(x, w, bias, attn=ATTN_ORA[attn], k=k)
+    np.testing.assert_array_equal(_keys_u64(yk), ok_)
+    np.testing.assert_array_equal(host(yv), ov)
+    Y64 = spc.sparse_conv_fwd(X32, dev_filter(spc, w), torch.from_numpy(bias).cuda(), attn, k, variant="scatter",
+                              key_bits=64)
+    np.testing.assert_array_equal(_keys_u64(Y64.trimmed()[0]), ok_)
+    dy = grad_values(ok_.shape[0], 4703, values="dyadic")
+    odx, odw, odb, _, _ = ora.conv_bwd(x, w, ok_, dy)
+    gdx, gdw, gdb = spc.sparse_conv_bwd(X32, dev_filter(spc, w), Y.exact(), torch.from_numpy(dy).cuda())
+    np.testing.assert_array_equal(host(gdx), odx)
+    np.testing.assert_array_equal(host(gdw), odw)
+    np.testing.assert_array_equal(host(gdb), odb)
+
+
+def test_relu_pool_topk_32bit_keys(cuda_lib):
+    spc = cuda_lib
+    x = uniform_map(2, 3, (16, 12, 20), 0.3, 4800, values="dyadic")
+    X32 = spc.SparseMap.from_arrays(x.keys, x.values, x.batch, x.channels, x.dims, key_bits=32)
+    rk, rv, rsrc = ora.relu(x)
+    y, src = spc.sparse_relu(X32)
+    np.testing.assert_array_equal(_keys_u64(y.trimmed()[0]), rk)
+    np.testing.assert_array_equal(host(src[:rk.shape[0]]), rsrc)
+    pk, pv, parg = ora.maxpool(x, (2, 3, 2))
+    y, arg = spc.sparse_maxpool(X32, (2, 3, 2))
+    np.testing.assert_array_equal(_keys_u64(y.trimmed()[0]), pk)
+    np.testing.assert_array_equal(host(y.trimmed()[1]), pv)
+    np.testing.assert_array_equal(host(arg[:pk.shape[0]]), parg)
+    tk, tv, tsrc = ora.topk(x, ora.ATTN_RAW, 23)
+    y, src = spc.attention_topk(X32, "raw", 23)
+    np.testing.assert_array_equal(_keys_u64(y.trimmed()[0]), tk)
+    np.testing.assert_array_equal(host(y.trimmed()[1]), tv)
+    # conversions round-trip, sparse_to_dense reads 32-bit keys too
+    X64 = X32.to_key_bits(64)
+    np.testing.assert_array_equal(_keys_u64(X64.keys), x.keys)
+    np.testing.assert_array_equal(host(spc.sparse_to_dense(X32)), host(spc.sparse_to_dense(X64)))
