@@ -202,7 +202,7 @@ class Step:
             self.pending = None
 
 
-def measure(args, torch, spc, density, rank, world, local, steps, warmup, clocks=True):
+def measure(args, torch, spc, density, rank, world, local, steps, warmup, clocks=True, key_bits=64):
     """Inputs of this rank's shard at `density`, warm-up, the algorithmic work of one step, then
     `steps` timed steps (CUDA events per step on the launching stream; a 512 MB write flushes L2
     between steps, outside the timed intervals)."""
@@ -213,7 +213,7 @@ def measure(args, torch, spc, density, rank, world, local, steps, warmup, clocks
     V = RES ** 3
     cfg = c4_inputs(density, args.values, batch=B_local, b0=b0)
     x, w, bias, k = cfg["x"], cfg["w"], cfg["bias"], cfg["k"]
-    X = spc.SparseMap.from_arrays(x.keys, x.values, x.batch, x.channels, x.dims)
+    X = spc.SparseMap.from_arrays(x.keys, x.values, x.batch, x.channels, x.dims, key_bits=key_bits)
     W = spc.SparseFilter.from_arrays(w.keys, w.values, w.c_in, w.c_out, w.ksize)
     bias_t = torch.from_numpy(bias).cuda()
     probe = spc.FwdPlan(X, W, "magnitude", k, args.variant, bias_t, args.samples_per_pass)
@@ -275,7 +275,7 @@ def measure(args, torch, spc, density, rank, world, local, steps, warmup, clocks
     else:
         macs_all, bytes_all = float(fwd_macs + bwd_macs), float(fwd_bytes + bwd_bytes)
     ms_per_step = t_ms / steps
-    return dict(cfg=cfg, x=x, w=w, X=X, W=W, bias_t=bias_t, k=k, Y=Y, step=step, flush=flush, variant=variant,
+    return dict(cfg=cfg, x=x, w=w, X=X, W=W, key_bits=key_bits, bias_t=bias_t, k=k, Y=Y, step=step, flush=flush, variant=variant,
                 cap=cap, dy_t=dy_t, B_local=B_local, fwd_macs=fwd_macs, bwd_macs=bwd_macs, ny=ny, nnz_x=nnz_x,
                 nnz_w=nnz_w, fwd_bytes=fwd_bytes, bwd_bytes=bwd_bytes, macs_all=macs_all, bytes_all=bytes_all,
                 ms_per_step=ms_per_step, per_step=per_step, launches_per_step=launches_per_step,
@@ -342,6 +342,20 @@ def run_ours(args):
         del md
         torch.cuda.empty_cache()
 
+    # ---- the same step with 32-bit key storage (Table 1 "Sparse 32"): device and end to end
+    k32 = None
+    if not args.no_key32:
+        mk = measure(args, torch, spc, args.density, rank, world, local, max(1, args.steps // 2), min(args.warmup, 3),
+                     clocks=False, key_bits=32)
+        ek = run_e2e(torch, spc, mk, args, world, dist if world > 1 else None)
+        k32 = {"key_bits": 32, "value": round(mk["value"], 3), "unit": "GMAC/s", "ms_per_step": round(mk["ms_per_step"], 4),
+               "e2e": {"value": round(mk["macs_all"] / (ek["ms_per_step"] * 1e-3) / 1e9, 3), "unit": "GMAC/s",
+                       "h2d_bytes_per_step": ek["h2d"], "d2h_bytes_per_step": ek["d2h"],
+                       "ms_per_step": round(ek["ms_per_step"], 4)},
+               "note": "uint32 keys in and out (valid: 64*8*128^3 = 2^30 keys < 2^32); same work, 4 B less per entry"}
+        del mk
+        torch.cuda.empty_cache()
+
     result = None
     if rank == 0:
         cpu = None
@@ -386,6 +400,7 @@ def run_ours(args):
             "roofline": roof,
             "kernel_rooflines": kernel_roofs,
             "density_sweep": sweep,
+            "key_bits_32": k32,
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 3) if e2e_value else None, "unit": "GMAC/s",
                     "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
@@ -457,7 +472,8 @@ def run_e2e(torch, spc, m, args, world, dist):
     the second of two device input buffers while step i computes (the buffer is reused only after
     the step that read it has finished)."""
     x, w, k, bias_t = m["x"], m["w"], m["k"], m["bias_t"]
-    hk = torch.from_numpy(x.keys.view(np.int64)).pin_memory()
+    kb = m.get("key_bits", 64)
+    hk = torch.from_numpy(x.keys.astype(np.uint32).view(np.int32) if kb == 32 else x.keys.view(np.int64)).pin_memory()
     hv = torch.from_numpy(x.values).pin_memory()
     hdy = m["dy_t"].cpu().pin_memory()
     bufs = [(torch.empty_like(hk, device="cuda"), torch.empty_like(hv, device="cuda"),
@@ -522,7 +538,7 @@ def run_e2e(torch, spc, m, args, world, dist):
         tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    return {"ms_per_step": ms, "h2d": int(hk.numel() * 8 + hv.numel() * 4 + hdy.numel() * 4),
+    return {"ms_per_step": ms, "h2d": int(hk.numel() * hk.element_size() + hv.numel() * 4 + hdy.numel() * 4),
             "d2h": int(out_dw.numel() * 4 + out_db.numel() * 4 + 8)}
 
 
@@ -659,6 +675,7 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=16, help="samples of the all-cores oracle leg")
+    ap.add_argument("--no-key32", action="store_true", help="skip the 32-bit-key sub-record")
     ap.add_argument("--variant", default="measure", choices=["auto", "scatter", "gemm", "measure"],
                     help="forward accumulate variant (SURVEY §8 a3); 'measure' times both once and keeps the faster")
     ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing only, gloo on CPU (tests)")

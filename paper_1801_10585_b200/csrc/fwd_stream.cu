@@ -354,6 +354,7 @@ __global__ void stream_tile_scan_kernel(FwdArgs a, uint64_t* kept) {
 // one warp per tile run: keep iff composite(score, p) >= kstar (every candidate when keep-all),
 // ordered compaction ("compress ids from kD to 1D, write as sparse output")
 constexpr int kSWWarps = 8;
+template <bool K32>
 __global__ void __launch_bounds__(32 * kSWWarps) stream_write_kernel(FwdArgs a, StreamGeo g) {
     const int lane = threadIdx.x & 31;
     const int64_t it = (int64_t)blockIdx.x * kSWWarps + (threadIdx.x >> 5);
@@ -385,7 +386,7 @@ __global__ void __launch_bounds__(32 * kSWWarps) stream_write_kernel(FwdArgs a, 
             const unsigned m = __ballot_sync(kFull, keep);
             if (keep) {
                 const uint64_t o = out + __popc(m & ((1u << lane) - 1u));
-                a.out_keys.put(o, kb + pp[q]);
+                a.out_keys.template put_t<K32>(o, kb + pp[q]);
                 a.out_vals[o] = __uint_as_float(vb[q]);
             }
             out += __popc(m);
@@ -414,7 +415,9 @@ cudaError_t launch_stream_tail(const Geo& gy, const FwdTile& t, const FwdArgs& a
     if (e != cudaSuccess) return e;
     const int64_t runs = a.nseg * a.ntile;
     SPC_PHASE("fwd_write", s, 1);
-    stream_write_kernel<<<(unsigned)((runs + kSWWarps - 1) / kSWWarps), 32 * kSWWarps, 0, s>>>(a, g);
+    const unsigned grid = (unsigned)((runs + kSWWarps - 1) / kSWWarps);
+    if (a.out_keys.k32) stream_write_kernel<true><<<grid, 32 * kSWWarps, 0, s>>>(a, g);
+    else stream_write_kernel<false><<<grid, 32 * kSWWarps, 0, s>>>(a, g);
     return cudaGetLastError();
 }
 

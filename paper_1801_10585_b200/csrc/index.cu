@@ -28,7 +28,7 @@ __device__ __forceinline__ int32_t row_of(uint32_t key, uint32_t Z, uint32_t mag
     return (int32_t)q;
 }
 
-template <typename K, typename I>   // key word, row / entry index type
+template <typename K, typename I, bool K32>   // key word, row / entry index type, 32-bit key storage
 __global__ void __launch_bounds__(256) row_index_kernel(K Z, K magic, Keys keys,
                                                         const int64_t* nnz_dev, int64_t nbound,
                                                         uint32_t* __restrict__ row_ptr, I total_rows,
@@ -45,13 +45,13 @@ __global__ void __launch_bounds__(256) row_index_kernel(K Z, K magic, Keys keys,
     for (int q = 0; q < kRiItems; ++q) {
         const int t = q * 256 + threadIdx.x;
         const I i = b0 + t;
-        srow[1 + t] = i < n ? (I)row_of((K)keys[i], Z, magic) : total_rows;
+        srow[1 + t] = i < n ? (I)row_of((K)keys.template at<K32>(i), Z, magic) : total_rows;
         if (vals && i < n) {
             const float v = vals[i];
             tiny |= !(fabsf(v) >= 0x1p-50f) && !isnan(v);
         }
     }
-    if (threadIdx.x == 0) srow[0] = b0 == 0 ? (I)-1 : (I)row_of((K)keys[b0 - 1], Z, magic);
+    if (threadIdx.x == 0) srow[0] = b0 == 0 ? (I)-1 : (I)row_of((K)keys.template at<K32>(b0 - 1), Z, magic);
     if (__syncthreads_or(tiny) && threadIdx.x == 0) *guard = 1;
     // entry i (and the sentinel i = n) fills the rows between its predecessor's row and its own
 #pragma unroll
@@ -89,13 +89,17 @@ cudaError_t launch_row_index(const Geo& g, Keys keys, const int64_t* nnz_dev, in
     if (space <= 4294967296.0 && nbound < (1ll << 30) && total_rows < (1ll << 30)) {
         const uint32_t Z = (uint32_t)g.Z;
         const uint32_t magic = Z == 1 ? ~0u : ~0u / Z;
-        row_index_kernel<uint32_t, int32_t><<<(unsigned)grid, bs, 0, s>>>(Z, magic, keys, nnz_dev, nbound, row_ptr,
-                                                                            (int32_t)total_rows, vals, guard);
+        if (keys.k32)
+            row_index_kernel<uint32_t, int32_t, true><<<(unsigned)grid, bs, 0, s>>>(Z, magic, keys, nnz_dev, nbound,
+                                                                                  row_ptr, (int32_t)total_rows, vals, guard);
+        else
+            row_index_kernel<uint32_t, int32_t, false><<<(unsigned)grid, bs, 0, s>>>(Z, magic, keys, nnz_dev, nbound,
+                                                                                   row_ptr, (int32_t)total_rows, vals, guard);
     } else {
         const uint64_t Z = (uint64_t)g.Z;
         const uint64_t magic = Z == 1 ? ~0ull : ~0ull / Z;   // floor((2^64 - 1) / Z)
-        row_index_kernel<uint64_t, int64_t><<<(unsigned)grid, bs, 0, s>>>(Z, magic, keys, nnz_dev, nbound, row_ptr,
-                                                                            total_rows, vals, guard);
+        row_index_kernel<uint64_t, int64_t, false><<<(unsigned)grid, bs, 0, s>>>(Z, magic, keys, nnz_dev, nbound, row_ptr,
+                                                                                   total_rows, vals, guard);
     }
     return cudaGetLastError();
 }

@@ -30,6 +30,11 @@ struct Keys {
     __device__ __forceinline__ uint64_t operator[](int64_t i) const {
         return k32 ? (uint64_t)__ldg(static_cast<const uint32_t*>(p) + i) : __ldg(static_cast<const uint64_t*>(p) + i);
     }
+    // key width known at compile time (hot kernels are instantiated per width)
+    template <bool K32>
+    __device__ __forceinline__ uint64_t at(int64_t i) const {
+        return K32 ? (uint64_t)__ldg(static_cast<const uint32_t*>(p) + i) : __ldg(static_cast<const uint64_t*>(p) + i);
+    }
     // low 32 bits of key i (the whole key in 32-bit storage)
     __device__ __forceinline__ uint32_t lo(int64_t i) const {
         return k32 ? __ldg(static_cast<const uint32_t*>(p) + i) : __ldg(static_cast<const uint32_t*>(p) + 2 * i);
@@ -44,6 +49,11 @@ struct KeysOut {
     __host__ __device__ KeysOut(void* q, int is32) : p(q), k32(is32) {}
     __device__ __forceinline__ void put(int64_t i, uint64_t v) const {
         if (k32) static_cast<uint32_t*>(p)[i] = (uint32_t)v;
+        else static_cast<uint64_t*>(p)[i] = v;
+    }
+    template <bool K32>
+    __device__ __forceinline__ void put_t(int64_t i, uint64_t v) const {
+        if (K32) static_cast<uint32_t*>(p)[i] = (uint32_t)v;
         else static_cast<uint64_t*>(p)[i] = v;
     }
 };
