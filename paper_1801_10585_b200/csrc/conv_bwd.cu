@@ -333,19 +333,36 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
             float prod[32];
 #pragma unroll
             for (int q = 0; q < 32; ++q) prod[q] = 0.0f;
-            for (int wb = 0; wb < n; wb += 32) {
-                const int j = wb + lane;
-                const bool wok = j < n;
-                const int wd = (wok ? wdel[lb + j] : wdel[lb]) * (int)sizeof(float);
-                const float wl = wok ? wv[lb + j] : 0.0f;
-                float dwl = 0.0f;
+            // four 32-weight blocks per sweep over the 32 staged entries: each entry's staged
+            // (G offset, value) is read once per sweep instead of once per block
+            constexpr int NB = 4;
+            for (int wb = 0; wb < n; wb += 32 * NB) {
+                int wd[NB];
+                float wl[NB], dwl[NB];
+#pragma unroll
+                for (int b = 0; b < NB; ++b) {
+                    const int j = wb + 32 * b + lane;
+                    const bool wok = j < n;
+                    wd[b] = (wok ? wdel[lb + j] : wdel[lb]) * (int)sizeof(float);
+                    wl[b] = wok ? wv[lb + j] : 0.0f;
+                    dwl[b] = 0.0f;
+                }
 #pragma unroll
                 for (int q = 0; q < 32; ++q) {
-                    const float g = *reinterpret_cast<const float*>(Gb + (st_eb[q] - wd));
-                    prod[q] = fmaf(g, wl, prod[q]);         // bp_data contribution
-                    dwl = fmaf(g, st_v[q], dwl);            // bp_filter contribution
+                    const int ebq = st_eb[q];
+                    const float vq = st_v[q];
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) {
+                        const float g = *reinterpret_cast<const float*>(Gb + (ebq - wd[b]));
+                        prod[q] = fmaf(g, wl[b], prod[q]);     // bp_data contribution
+                        dwl[b] = fmaf(g, vq, dwl[b]);          // bp_filter contribution
+                    }
                 }
-                if (DW && wok && dwl != 0.0f) atomicAdd(&dwp[lb + j], (double)dwl);
+#pragma unroll
+                for (int b = 0; b < NB; ++b) {
+                    const int j = wb + 32 * b + lane;
+                    if (DW && j < n && dwl[b] != 0.0f) atomicAdd(&dwp[lb + j], (double)dwl[b]);
+                }
             }
             float dxa = 0.0f;
             if (DX) dxa = reduce_scatter32(prod, lane);   // lane e: sum over this ic's weights
