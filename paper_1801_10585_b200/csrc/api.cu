@@ -371,7 +371,7 @@ struct TopkWs {
 TopkWs carve_topk(Carver& c, const Geo& g, int64_t) {
     TopkWs ws{};
     const int64_t nseg = g.B * g.C;
-    ws.xrow = c.take<uint32_t>((size_t)(g.B * g.C * g.R + 1));
+    ws.xrow = c.take<uint32_t>((size_t)nseg + 1);   // segment bounds only (no row index)
     ws.seg_off = c.take<uint64_t>((size_t)nseg + 1);
     ws.flag = c.take<int>(1);
     return ws;
@@ -405,7 +405,7 @@ struct PoolWs {
 
 PoolWs carve_pool(Carver& c, const Geo& g, const PoolPlan& p) {
     PoolWs ws{};
-    ws.xrow = c.take<uint32_t>((size_t)(g.B * g.C * g.R + 1));
+    ws.xrow = c.take<uint32_t>(pool_bound_words(g, p));   // band bounds (tile form) or row index
     ws.cnt = c.take<uint32_t>((size_t)p.items);
     ws.off = c.take<uint64_t>((size_t)p.items);
     ws.tmp = c.take<uint64_t>(scan_tmp_words(p.items));
@@ -692,8 +692,8 @@ spc_status_t attention_topk(const spc_map_t* x, spc_attn_t attn, int64_t k, spc_
     Carver c(workspace);
     TopkWs ws = carve_topk(c, g, x->nnz);
     if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
-    SPC_TRY(cu(launch_row_index(g, kin(x), x->nnz_dev, x->nnz, ws.xrow, s)));
-    return cu(launch_topk(kin(x), x->values, ws.xrow, g.R, g.B * g.C, attn, k, ws.seg_off, kout(y), y->values,
+    SPC_TRY(cu(launch_seg_bounds(kin(x), x->nnz_dev, x->nnz, g.B * g.C, g.V, ws.xrow, s)));
+    return cu(launch_topk(kin(x), x->values, ws.xrow, 1, g.B * g.C, attn, k, ws.seg_off, kout(y), y->values,
                           src_index, y->nnz_dev, s));
 }
 
@@ -744,8 +744,8 @@ spc_status_t sparse_maxpool(const spc_map_t* x, const int64_t* stride, spc_map_o
     Carver c(workspace);
     PoolWs ws = carve_pool(c, g, p);
     if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
-    SPC_TRY(cu(launch_row_index(g, kin(x), x->nnz_dev, x->nnz, ws.xrow, s)));
-    return cu(launch_maxpool(g, p, kin(x), x->values, ws.xrow, ws.cnt, ws.off, ws.tmp, kout(y), y->values, argmax,
+    if (!p.tiled) SPC_TRY(cu(launch_row_index(g, kin(x), x->nnz_dev, x->nnz, ws.xrow, s)));
+    return cu(launch_maxpool(g, p, kin(x), x->values, x->nnz_dev, x->nnz, ws.xrow, ws.cnt, ws.off, ws.tmp, kout(y), y->values, argmax,
                              y->nnz_dev, s));
 }
 

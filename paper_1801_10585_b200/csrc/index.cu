@@ -7,6 +7,32 @@
 
 namespace spc {
 
+// ------------------------------------------------------------------------ segment bounds
+// seg_ptr[s] = first entry whose key >= s*V, s in [0, nseg]: one binary search per segment (the
+// per-(b, c) bounds of a map without its full row index -- the standalone attention needs only
+// these).
+__global__ void seg_bounds_kernel(Keys keys, const int64_t* nnz_dev, int64_t nbound, int64_t nseg, uint64_t V,
+                                  uint32_t* __restrict__ seg_ptr) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s > nseg) return;
+    const int64_t n = load_n(nnz_dev, nbound);
+    const uint64_t want = (uint64_t)s * V;
+    int64_t lo = 0, hi = n;   // first i with keys[i] >= want
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (keys[mid] < want) lo = mid + 1; else hi = mid;
+    }
+    seg_ptr[s] = (uint32_t)lo;
+}
+
+cudaError_t launch_seg_bounds(Keys keys, const int64_t* nnz_dev, int64_t nbound, int64_t nseg, int64_t V,
+                              uint32_t* seg_ptr, cudaStream_t s) {
+    SPC_PHASE("seg_bounds", s, 1);
+    seg_bounds_kernel<<<(unsigned)((nseg + 1 + 255) / 256), 256, 0, s>>>(keys, nnz_dev, nbound, nseg, (uint64_t)V,
+                                                                          seg_ptr);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------- row index
 // row_ptr[r] = first entry whose key >= r*Z, for r in [0, total_rows]. A block computes the rows
 // of its 2048 entries from coalesced key loads into shared memory; then each entry fills the gap

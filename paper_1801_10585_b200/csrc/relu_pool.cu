@@ -134,6 +134,10 @@ PoolPlan plan_pool(const Geo& g, int sw, int sx, int sy, int sz) {
     return p;
 }
 
+size_t pool_bound_words(const Geo& g, const PoolPlan& p) {
+    return p.tiled ? (size_t)(g.B * g.C * (int64_t)g.W * g.X * (p.nyt + 1)) : (size_t)(g.B * g.C * g.R + 1);
+}
+
 // x / d for x < 2^31 with m = floor((2^32 - 1) / d): the multiply-high is exact or one short
 __device__ __forceinline__ uint32_t udiv(uint32_t x, uint32_t d, uint32_t m) {
     uint32_t q = __umulhi(x, m);
@@ -142,17 +146,40 @@ __device__ __forceinline__ uint32_t udiv(uint32_t x, uint32_t d, uint32_t m) {
 
 // member entries of a tile: the sx key runs, four loads in flight per thread;
 // f(cell, entry, value) for each (value loaded only when LOADV)
+// Band bounds of the tile form: bnd[pl*(nyt+1) + j] = first entry of input plane pl = (seg, w, x)
+// at or after input row j*nyb*sy (one binary search each, all in parallel) -- the tiles need only
+// these, not the map's full row index.
+__global__ void pool_bounds_kernel(Geo g, PoolPlan p, Keys keys, const int64_t* nnz_dev, int64_t nbound,
+                                   uint32_t* __restrict__ bnd) {
+    const int64_t nb = (int64_t)p.nyt + 1;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t npl = g.B * g.C * (int64_t)g.W * g.X;
+    if (i >= npl * nb) return;
+    const int64_t pl = i / nb;
+    const int j = (int)(i - pl * nb);
+    const int64_t y = min((int64_t)j * p.nyb * p.sy, (int64_t)g.Y);
+    const uint64_t want = (uint64_t)(pl * g.Y + y) * (uint64_t)g.Z;
+    const int64_t n = load_n(nnz_dev, nbound);
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (keys[mid] < want) lo = mid + 1; else hi = mid;
+    }
+    bnd[i] = (uint32_t)lo;
+}
+
 template <bool LOADV, typename F>
 __device__ __forceinline__ void pool_tile_members(const Geo& g, const PoolPlan& p, Keys keys,
                                                   const float* __restrict__ vals,
-                                                  const uint32_t* __restrict__ row_ptr, int64_t seg, int pw, int px,
-                                                  int ya, int yb, F f) {
+                                                  const uint32_t* __restrict__ bnd, int64_t seg, int pw, int px,
+                                                  int ya, int yt, F f) {
     const uint32_t Z = (uint32_t)g.Z;
     for (int dwx = 0; dwx < p.sw * p.sx; ++dwx) {   // input planes (w, x) of the pooled plane
         const int w = pw * p.sw + dwx / p.sx, x = px * p.sx + dwx % p.sx;
         if (w >= g.W || x >= g.X) continue;
-        const int64_t row0 = ((seg * g.W + w) * g.X + x) * (int64_t)g.Y + ya;
-        const uint32_t e0 = row_ptr[row0], e1 = row_ptr[row0 + (yb - ya)];
+        const int64_t pl = (seg * g.W + w) * g.X + x;
+        const int64_t row0 = pl * (int64_t)g.Y + ya;
+        const uint32_t e0 = bnd[pl * (p.nyt + 1) + yt], e1 = bnd[pl * (p.nyt + 1) + yt + 1];
         const uint64_t kb = (uint64_t)row0 * Z;
         for (uint32_t e = e0 + threadIdx.x; e < e1; e += 4 * kTileThreads) {
             uint64_t kk[4];
@@ -178,7 +205,7 @@ __device__ __forceinline__ void pool_tile_members(const Geo& g, const PoolPlan& 
 
 struct PoolTileId {
     int64_t seg;
-    int pw, px, py0, npy, ya, yb;
+    int pw, px, py0, npy, ya, yb, yt;
 };
 __device__ __forceinline__ PoolTileId pool_tile_id(const Geo& g, const PoolPlan& p, int64_t tile) {
     PoolTileId t;
@@ -188,6 +215,7 @@ __device__ __forceinline__ PoolTileId pool_tile_id(const Geo& g, const PoolPlan&
     r /= p.PX;
     t.pw = (int)(r % p.PW);
     t.seg = r / p.PW;
+    t.yt = yt;
     t.py0 = yt * p.nyb;
     t.npy = min(p.nyb, p.PY - t.py0);
     t.ya = t.py0 * p.sy;
@@ -204,7 +232,7 @@ pool_tile_count_kernel(Geo g, PoolPlan p, Keys keys, const uint32_t* __restrict_
     const PoolTileId t = pool_tile_id(g, p, blockIdx.x);
     if (threadIdx.x < kTileCells / 32) occ[threadIdx.x] = 0u;
     __syncthreads();
-    pool_tile_members<false>(g, p, keys, nullptr, row_ptr, t.seg, t.pw, t.px, t.ya, t.yb, [&](int cell, uint32_t, float) {
+    pool_tile_members<false>(g, p, keys, nullptr, row_ptr, t.seg, t.pw, t.px, t.ya, t.yt, [&](int cell, uint32_t, float) {
         atomicOr(&occ[cell >> 5], 1u << (cell & 31));
     });
     __syncthreads();
@@ -232,7 +260,7 @@ pool_tile_write_kernel(Geo g, PoolPlan p, Keys keys, const float* __restrict__ v
     for (int j = 0; j < kTileCells / 2 / kTileThreads; ++j) b4[tid + kTileThreads * j] = make_uint4(0u, 0u, 0u, 0u);
     if (tid < kTileCells / 32) occ[tid] = 0u;
     __syncthreads();
-    pool_tile_members<true>(g, p, keys, vals, row_ptr, t.seg, t.pw, t.px, t.ya, t.yb, [&](int cell, uint32_t e, float v) {
+    pool_tile_members<true>(g, p, keys, vals, row_ptr, t.seg, t.pw, t.px, t.ya, t.yt, [&](int cell, uint32_t e, float v) {
         atomicMax(&best[cell], ((unsigned long long)orderable(v) << 32) | (unsigned long long)(~e));
         atomicOr(&occ[cell >> 5], 1u << (cell & 31));
     });
@@ -358,12 +386,18 @@ pool_kernel(Geo g, PoolPlan p, Keys keys, const float* __restrict__ vals,
     }
 }
 
-cudaError_t launch_maxpool(const Geo& g, const PoolPlan& p, Keys keys, const float* vals,
-                           const uint32_t* row_ptr, uint32_t* item_cnt, uint64_t* item_off, uint64_t* scan_tmp,
+cudaError_t launch_maxpool(const Geo& g, const PoolPlan& p, Keys keys, const float* vals, const int64_t* nnz_dev,
+                           int64_t nbound, const uint32_t* row_ptr, uint32_t* item_cnt, uint64_t* item_off, uint64_t* scan_tmp,
                            KeysOut out_keys, float* out_vals, int64_t* out_arg, int64_t* out_nnz, cudaStream_t s) {
     if (p.items == 0) return cudaMemsetAsync(out_nnz, 0, sizeof(int64_t), s);
-    if (p.tiled) {
+    if (p.tiled) {   // row_ptr holds the band bounds (pool_bounds_kernel), not a row index
         const unsigned tg = (unsigned)p.items;
+        {
+            const int64_t nbnd = g.B * g.C * (int64_t)g.W * g.X * (p.nyt + 1);
+            SPC_PHASE("pool_bounds", s, 1);
+            pool_bounds_kernel<<<(unsigned)((nbnd + 255) / 256), 256, 0, s>>>(g, p, keys, nnz_dev, nbound,
+                                                                              const_cast<uint32_t*>(row_ptr));
+        }
         { SPC_PHASE("pool_count", s, 1); pool_tile_count_kernel<<<tg, kTileThreads, 0, s>>>(g, p, keys, row_ptr, item_cnt); }
         cudaError_t e = launch_scan_u32(item_cnt, item_off, p.items, out_nnz, scan_tmp, s);
         if (e != cudaSuccess) return e;

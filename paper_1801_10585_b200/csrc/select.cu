@@ -15,7 +15,10 @@
 
 namespace spc {
 
-constexpr int kTkThreads = 256;
+#ifndef SPC_TK_THREADS
+#define SPC_TK_THREADS 256
+#endif
+constexpr int kTkThreads = SPC_TK_THREADS;
 constexpr int kTkWarps = kTkThreads / 32;
 constexpr int kTkG = 8;                                 // groups of 32 entries per warp and tile
 constexpr uint32_t kTkTile = (uint32_t)kTkThreads * kTkG;
@@ -41,7 +44,7 @@ __global__ void topk_offsets_kernel(const uint32_t* __restrict__ row_ptr, int64_
     if (threadIdx.x == 0) *total = (int64_t)carry;
 }
 
-__global__ void __launch_bounds__(kTkThreads, 4)
+__global__ void __launch_bounds__(kTkThreads, 1024 / kTkThreads)
 topk_seg_kernel(Keys keys, const float* __restrict__ vals, const uint32_t* __restrict__ row_ptr,
                 int64_t R, int attn, int64_t k, const uint64_t* __restrict__ seg_off, KeysOut ok,
                 float* __restrict__ ov, int64_t* __restrict__ osrc) {

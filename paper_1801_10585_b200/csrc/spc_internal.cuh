@@ -151,6 +151,10 @@ struct PhaseScope {
 cudaError_t launch_row_index(const Geo& g, Keys keys, const int64_t* nnz_dev, int64_t nnz_bound,
                              uint32_t* row_ptr, cudaStream_t s, const float* vals = nullptr, int* guard = nullptr);
 
+// Segment bounds: seg_ptr[s] = first entry with key >= s*V, s in [0, nseg] (nseg + 1 words).
+cudaError_t launch_seg_bounds(Keys keys, const int64_t* nnz_dev, int64_t nbound, int64_t nseg, int64_t V,
+                              uint32_t* seg_ptr, cudaStream_t s);
+
 // Filter table in ic-major order. meta[j] = {oc, packed offset}; val[j]; off[ic*(c_out+1)+oc]
 // = first table entry of (ic, oc) (off[ic*(c_out+1)+c_out] = end); src[j] = original filter
 // position of table entry j. scratch: 2*c_in*c_out ints.
@@ -346,8 +350,11 @@ struct PoolPlan {
     uint32_t mZ, msy, msz;  // floor((2^32 - 1) / d) for d = Z, sy, sz (division by multiply-high)
 };
 PoolPlan plan_pool(const Geo& g, int sw, int sx, int sy, int sz);
-cudaError_t launch_maxpool(const Geo& g, const PoolPlan& p, Keys keys, const float* vals,
-                           const uint32_t* row_ptr, uint32_t* item_cnt, uint64_t* item_off, uint64_t* scan_tmp,
+// Tile form (p.tiled): row_ptr is the band-bound workspace (pool_bound_words), filled here;
+// row form: the map's row index (launch_row_index) built by the caller.
+size_t pool_bound_words(const Geo& g, const PoolPlan& p);
+cudaError_t launch_maxpool(const Geo& g, const PoolPlan& p, Keys keys, const float* vals, const int64_t* nnz_dev,
+                           int64_t nbound, const uint32_t* row_ptr, uint32_t* item_cnt, uint64_t* item_off, uint64_t* scan_tmp,
                            KeysOut out_keys, float* out_vals, int64_t* out_arg, int64_t* out_nnz, cudaStream_t s);
 cudaError_t launch_scatter_grad(const int64_t* src, const float* dy, int64_t n_out_bound, const int64_t* n_out_dev,
                                 float* dx, int64_t n_in, cudaStream_t s);
