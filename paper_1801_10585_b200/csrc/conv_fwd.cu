@@ -1087,13 +1087,18 @@ cudaError_t launch_seg_scan_u64(const uint64_t* in, uint64_t* out, int64_t n, in
 
 void plan_fwd_sampling(const Geo& gy, const FwdTile& t, int attn, FwdArgs* a) {
     a->ntile = (int)((int64_t)gy.W * gy.X * t.nty);
-    // every sp_period-th tile of a segment: the largest prime <= 31 that leaves at least 8 sampled
-    // tiles and does not divide the band count (so that the sampled tiles cycle through the
-    // bands); no sampling for small segments or without attention
-    static const int primes[] = {31, 29, 23, 19, 17, 13, 11, 7, 5, 3};
+    // every sp_period-th tile of a segment: for large segments the largest prime in 37..61 that
+    // leaves at least 16 sampled tiles, else the largest prime <= 31 that leaves at least 8 --
+    // never one dividing the band count (the sampled tiles cycle through the bands); no sampling
+    // for small segments or without attention
+    static const int big[] = {61, 59, 53, 47, 43, 41, 37};
+    static const int small[] = {31, 29, 23, 19, 17, 13, 11, 7, 5, 3};
     int P = 0;
-    for (int p : primes)
-        if (a->ntile >= 8 * p && t.nty % p != 0) { P = p; break; }
+    for (int p : big)
+        if (a->ntile >= 16 * p && t.nty % p != 0) { P = p; break; }
+    if (P == 0)
+        for (int p : small)
+            if (a->ntile >= 8 * p && t.nty % p != 0) { P = p; break; }
     a->sp_period = P > 0 ? P : 1;
     a->sp_off = P / 2;
     a->nsamp = (attn != SPC_ATTN_NONE && P > 0) ? (a->ntile - a->sp_off + P - 1) / P : 0;
