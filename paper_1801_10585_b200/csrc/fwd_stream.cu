@@ -187,8 +187,51 @@ __global__ void __launch_bounds__(kSRThreads) stream_resolve_kernel(FwdArgs a, S
     const float* cval = a.cval + s * g.V;
     const uint32_t* cpos = a.cpos + s * g.V;
     const int lane = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) h[i] = 0;
     if (threadIdx.x == 0) sh_n = 0;
+    __syncthreads();
+    if (n <= (uint64_t)kSRCap) {
+        // small candidate sets (MNIST-like layers, small grids): every candidate's composite key
+        // in shared memory in one pass, the k-th largest by ranking (n <= 1024) or radix select
+        struct AllF {
+            const float* cv; const uint32_t* cp; uint64_t* keys; uint32_t* sh_n; uint32_t* tdef; int attn, lane;
+            const StreamGeo* g;
+            __device__ void run(int t, uint32_t n) const {
+                const uint32_t b0 = tile_base(t, g->nty, g->TY, g->Y, g->Z);
+                for (uint32_t i = lane; i < n; i += 32)
+                    keys[atomicAdd(sh_n, 1u)] = comp_key(score_bits(__float_as_uint(cv[b0 + i]), attn), cp[b0 + i]);
+                if (lane == 0) tdef[t] = 0;
+            }
+        } af{cval, cpos, keys, &sh_n, a.tile_def + s * a.ntile, attn, lane, &g};
+        for_candidates(a, s, af);
+        __syncthreads();
+        const uint32_t ns = sh_n;
+        uint64_t kst;
+        if (ns <= 1024u) {
+            if (threadIdx.x == 0) sh[0] = 0;
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) {   // rank = keys above (all distinct)
+                const uint64_t ki = keys[i];
+                uint32_t above = 0;
+                for (uint32_t j = 0; j < ns; ++j) above += keys[j] > ki ? 1u : 0u;
+                if (above == (uint32_t)k - 1u) sh[0] = ki;
+            }
+            __syncthreads();
+            kst = sh[0];
+        } else {
+            kst = smem_select(keys, ns, (uint32_t)k, h, sh);
+        }
+        uint32_t* tsel = a.tile_sel + s * a.ntile;
+        for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x)
+            if (keys[i] >= kst) atomicAdd(&tsel[tile_of(0xffffffffu - (uint32_t)keys[i], g)], 1u);
+        if (threadIdx.x == 0) {
+            FwdSeg st{};
+            st.keep_all = 0;
+            st.kstar = kst;
+            a.seg[s] = st;
+        }
+        return;
+    }
+    for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) h[i] = 0;
     __syncthreads();
     // ---- histogram of the candidates' score digit
     struct HistF {
