@@ -87,25 +87,43 @@ __global__ void stream_find_kernel(FwdArgs a, double f) {
 // --------------------------------------------------------------------------------- resolve
 constexpr int kSRThreads = 512;
 constexpr int kSRWarps = kSRThreads / 32;
-constexpr int kSRCap = 4096;   // candidates of the threshold bucket collected in shared memory
+constexpr int kSRCap = 4096;
+#ifndef SPC_SR_GRANULE
+#define SPC_SR_GRANULE 1
+#endif   // candidates of the threshold bucket collected in shared memory
 
-// Visit every candidate of segment s: f(t, i, value bits, global index); one warp per tile run,
-// the runs' lengths loaded 32 at a time, four entries per lane in flight.
+// Visit every candidate run of segment s: f.run(t, n) by one warp per tile run. Tiles are dealt
+// to the warps in granules of G consecutive tiles (granule q -> warp q % kSRWarps); G = 1 spreads
+// spatially clustered candidates (surfaces, strokes) over all warps (OctNet trunk resolve 1.28 ->
+// 0.42 ms against G = 32; C4 is indifferent).
 template <typename F>
 __device__ __forceinline__ void for_candidates(const FwdArgs& a, int64_t s, F f) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t* tc = a.tcnt + s * a.ntile;
-    for (int t0 = warp * 32; t0 < a.ntile; t0 += kSRWarps * 32) {
-        const uint32_t mycnt = t0 + lane < a.ntile ? tc[t0 + lane] : 0u;
+    constexpr int G = SPC_SR_GRANULE;
+    auto tile_at = [&](int base, int j) { return base + (warp + kSRWarps * (j / G)) * G + (j % G); };
+    for (int base = 0; base < a.ntile; base += kSRWarps * 32) {
+        const int tl = tile_at(base, lane);
+        const uint32_t mycnt = tl < a.ntile ? tc[tl] : 0u;
         unsigned any = __ballot_sync(kFull, mycnt != 0u);
         while (any) {
             const int j = __ffs(any) - 1;
             any &= any - 1;
-            const int t = t0 + j;
             const uint32_t n = __shfl_sync(kFull, mycnt, j);
-            f.run(t, n);
+            f.run(tile_at(base, j), n);
         }
     }
+}
+
+// slot of the calling lane in a shared-memory list: one atomic per warp for the active lanes
+__device__ __forceinline__ uint32_t warp_append(uint32_t* cnt) {
+    const unsigned m = __activemask();
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(cnt, (uint32_t)__popc(m));
+    base = __shfl_sync(m, base, leader);
+    return base + (uint32_t)__popc(m & ((1u << lane) - 1u));
 }
 
 __device__ __forceinline__ uint32_t tile_of(uint32_t p, const StreamGeo& g) {
@@ -113,6 +131,44 @@ __device__ __forceinline__ uint32_t tile_of(uint32_t p, const StreamGeo& g) {
     const uint32_t x = p / yz;
     const uint32_t y = (p - x * yz) / (uint32_t)g.Z;
     return x * (uint32_t)g.nty + y / (uint32_t)g.TY;
+}
+
+// The bin of histogram h[0..nb) holding the need-th largest entry (1 <= need <= total), found by
+// warp 0 (the caller restricts it): 32 stripes of consecutive bins from the top, summed with a
+// lane rotation (no bank conflicts), one warp scan, then the crossing lane walks its stripe.
+// sh[0] = bin, sh[1] = need - (entries above the bin), sh[2] = h[bin].
+__device__ __forceinline__ void warp_find_bin(const uint32_t* h, uint32_t nb, uint64_t need, uint64_t* sh) {
+    const int lane = threadIdx.x & 31;
+    const int per = (int)((nb + 31u) >> 5);
+    uint32_t own = 0;
+    for (int q = 0; q < per; ++q) {
+        const int bin = (int)nb - 1 - per * lane - (q + lane) % per;
+        if (bin >= 0) own += h[bin];
+    }
+    const uint32_t incl = warp_incl_scan(own);
+    const uint64_t before = incl - own;
+    const bool hit = own && before < need && before + own >= need;
+    if (hit) {
+        uint64_t cum = before;
+        for (int q = 0; q < per; ++q) {
+            const int bin = (int)nb - 1 - per * lane - q;
+            if (bin < 0) break;
+            if (cum + h[bin] >= need) {
+                sh[0] = (uint64_t)bin;
+                sh[1] = need - cum;
+                sh[2] = h[bin];
+                break;
+            }
+            cum += h[bin];
+        }
+    }
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    if (!__any_sync(kFull, hit) && lane == 0) {   // unreachable for a valid need: bin 0
+        const uint64_t above = total - h[0];
+        sh[0] = 0;
+        sh[1] = need > above ? need - above : 1;
+        sh[2] = h[0];
+    }
 }
 
 // need-th largest (1-based) of n distinct u64 keys in shared memory: radix select with 8-bit
@@ -128,27 +184,55 @@ __device__ uint64_t smem_select(const uint64_t* keys, uint32_t n, uint32_t need,
             if ((k & mask) == prefix) atomicAdd(&h256[(uint32_t)(k >> shf) & 255u], 1u);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t cum = 0;
-            int bin = 255;
-            for (; bin > 0; --bin) {
-                if (cum + h256[bin] >= need) break;
-                cum += h256[bin];
-            }
-            sh[0] = prefix | ((uint64_t)bin << shf);
-            sh[1] = (uint64_t)(need - cum);
-        }
+        if (threadIdx.x < 32) warp_find_bin(h256, 256u, need, sh);
         __syncthreads();
-        prefix = sh[0];
+        prefix |= sh[0] << shf;
         need = (uint32_t)sh[1];
         mask |= 255ull << shf;
+        const bool single = sh[2] == 1u;   // one key left with this prefix: it is the answer
         __syncthreads();
+        if (single) {
+            for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
+                if ((keys[i] & mask) == prefix) sh[3] = keys[i];
+            __syncthreads();
+            return sh[3];
+        }
+    }
+    return prefix;
+}
+
+// the same select by one warp over its own key list (warp-per-segment resolve)
+__device__ uint64_t warp_select(const uint64_t* keys, uint32_t n, uint32_t need, uint32_t* h256, uint64_t* sh) {
+    const int lane = threadIdx.x & 31;
+    uint64_t prefix = 0, mask = 0;
+    for (int pass = 0; pass < 8; ++pass) {
+        const int shf = 56 - 8 * pass;
+        for (int i = lane; i < 256; i += 32) h256[i] = 0;
+        __syncwarp();
+        for (uint32_t i = lane; i < n; i += 32) {
+            const uint64_t k = keys[i];
+            if ((k & mask) == prefix) atomicAdd(&h256[(uint32_t)(k >> shf) & 255u], 1u);
+        }
+        __syncwarp();
+        warp_find_bin(h256, 256u, need, sh);
+        __syncwarp();
+        prefix |= sh[0] << shf;
+        need = (uint32_t)sh[1];
+        mask |= 255ull << shf;
+        const bool single = sh[2] == 1u;
+        __syncwarp();
+        if (single) {
+            for (uint32_t i = lane; i < n; i += 32)
+                if ((keys[i] & mask) == prefix) sh[3] = keys[i];
+            __syncwarp();
+            return sh[3];
+        }
     }
     return prefix;
 }
 
 // pass 0: every segment; pass 1: only segments the redo pass recomputed
-__global__ void __launch_bounds__(kSRThreads) stream_resolve_kernel(FwdArgs a, StreamGeo g, int pass) {
+__global__ void __launch_bounds__(kSRThreads, 4) stream_resolve_kernel(FwdArgs a, StreamGeo g, int pass) {
     const int64_t s = blockIdx.x;
     if (pass == 1 && !a.fail[s]) return;
     const uint64_t n = a.cand_cur[s];
@@ -191,14 +275,17 @@ __global__ void __launch_bounds__(kSRThreads) stream_resolve_kernel(FwdArgs a, S
     __syncthreads();
     if (n <= (uint64_t)kSRCap) {
         // small candidate sets (MNIST-like layers, small grids): every candidate's composite key
-        // in shared memory in one pass, the k-th largest by ranking (n <= 1024) or radix select
+        // in shared memory in one pass, the k-th largest by ranking (n <= 256) or radix select
         struct AllF {
             const float* cv; const uint32_t* cp; uint64_t* keys; uint32_t* sh_n; uint32_t* tdef; int attn, lane;
             const StreamGeo* g;
             __device__ void run(int t, uint32_t n) const {
                 const uint32_t b0 = tile_base(t, g->nty, g->TY, g->Y, g->Z);
                 for (uint32_t i = lane; i < n; i += 32)
-                    keys[atomicAdd(sh_n, 1u)] = comp_key(score_bits(__float_as_uint(cv[b0 + i]), attn), cp[b0 + i]);
+                    {
+                    const uint64_t key = comp_key(score_bits(__float_as_uint(cv[b0 + i]), attn), cp[b0 + i]);
+                    keys[warp_append(sh_n)] = key;
+                }
                 if (lane == 0) tdef[t] = 0;
             }
         } af{cval, cpos, keys, &sh_n, a.tile_def + s * a.ntile, attn, lane, &g};
@@ -206,7 +293,7 @@ __global__ void __launch_bounds__(kSRThreads) stream_resolve_kernel(FwdArgs a, S
         __syncthreads();
         const uint32_t ns = sh_n;
         uint64_t kst;
-        if (ns <= 1024u) {
+        if (ns <= 256u) {
             if (threadIdx.x == 0) sh[0] = 0;
             __syncthreads();
             for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) {   // rank = keys above (all distinct)
@@ -305,19 +392,9 @@ __global__ void __launch_bounds__(kSRThreads) stream_resolve_kernel(FwdArgs a, S
         } nf{cval, cpos, h, tl, lo, B, sh1, attn, lane, pos, d, pre, &g};
         for_candidates(a, s, nf);
         __syncthreads();
-        if (threadIdx.x == 0) {
-            uint64_t cum = 0;
-            int bin = (int)nb - 1;
-            for (; bin > 0; --bin) {
-                if (cum + h[bin] >= need) break;
-                cum += h[bin];
-            }
-            sh[0] = (pre << d) | (uint64_t)bin;
-            sh[1] = need - cum;
-            sh[2] = h[bin];
-        }
+        if (threadIdx.x < 32) warp_find_bin(h, nb, need, sh);
         __syncthreads();
-        pre = sh[0];
+        pre = (pre << d) | sh[0];
         need = sh[1];
         bcnt = sh[2];
         __syncthreads();
@@ -352,7 +429,7 @@ __global__ void __launch_bounds__(kSRThreads) stream_resolve_kernel(FwdArgs a, S
             if (lane == 0) tdef[t] = def;
         }
     } cf{cval, cpos, keys, &sh_n, a.tile_def + s * a.ntile, tl, lo, B, sh1, attn, lane, pos, pre, &g};
-    // runs without candidates keep tile_def = 0 (zeroed with tile_sel before the pass)
+    // (tile_def is written for every run with candidates; the tile scan reads no other)
     for_candidates(a, s, cf);
     __syncthreads();
     const uint32_t ns = sh_n;
@@ -367,6 +444,85 @@ __global__ void __launch_bounds__(kSRThreads) stream_resolve_kernel(FwdArgs a, S
         FwdSeg st{};
         st.keep_all = 0;
         st.kstar = ((uint64_t)(lo + (uint32_t)(kps >> 32)) << 32) | (kps & 0xffffffffull);
+        a.seg[s] = st;
+    }
+}
+
+// Segments of at most kSmallV voxels (MNIST-like layers, coarse grids): one warp per segment, no
+// block barriers. Every candidate's composite key goes to the warp's shared list (n <= V), the
+// k-th largest by warp_select; same outcome and outputs as stream_resolve_kernel.
+constexpr int kSmallV = 1024;
+constexpr int kSmallWarps = 4;
+
+__global__ void __launch_bounds__(32 * kSmallWarps) stream_resolve_small_kernel(FwdArgs a, StreamGeo g, int pass) {
+    __shared__ uint64_t keys_all[kSmallWarps][kSmallV];
+    __shared__ uint32_t h_all[kSmallWarps][256];
+    __shared__ uint64_t sh_all[kSmallWarps][4];
+    __shared__ uint32_t n_all[kSmallWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t s = (int64_t)blockIdx.x * kSmallWarps + warp;
+    if (s >= a.nseg) return;                       // (warp-uniform, as every return below)
+    if (pass == 1 && !a.fail[s]) return;
+    const uint64_t n = a.cand_cur[s];
+    const uint64_t sup = a.seg_count[s];
+    const uint64_t k = (uint64_t)a.k;
+    const bool keep_all = a.attn == SPC_ATTN_NONE || sup <= k;
+    const bool fail = keep_all ? (n != sup) : (n < k);
+    if (fail) {
+        if (pass == 0 && lane == 0) {
+            a.fail[s] = 1;
+            a.tlow[s] = 0;
+            a.cand_cur[s] = 0;
+            a.cmax[s] = 0;
+            const int b = (int)(s / (int64_t)a.seg_stride);
+            if (atomicExch(&a.bflag[b], 1) == 0) a.redo_b[atomicAdd(a.redo_n, 1)] = b;
+        }
+        return;
+    }
+    if (keep_all) {
+        if (lane == 0) {
+            FwdSeg st{};
+            st.keep_all = 1;
+            a.seg[s] = st;
+        }
+        return;
+    }
+    uint64_t* keys = keys_all[warp];
+    uint32_t* cnt = &n_all[warp];
+    if (lane == 0) *cnt = 0;
+    __syncwarp();
+    const float* cv = a.cval + s * g.V;
+    const uint32_t* cp = a.cpos + s * g.V;
+    const uint32_t* tc = a.tcnt + s * a.ntile;
+    uint32_t* tdef = a.tile_def + s * a.ntile;
+    const int attn = a.attn;
+    for (int t0 = 0; t0 < a.ntile; t0 += 32) {
+        const uint32_t mycnt = t0 + lane < a.ntile ? tc[t0 + lane] : 0u;
+        unsigned any = __ballot_sync(kFull, mycnt != 0u);
+        while (any) {
+            const int j = __ffs(any) - 1;
+            any &= any - 1;
+            const int t = t0 + j;
+            const uint32_t rn = __shfl_sync(kFull, mycnt, j);
+            const uint32_t b0 = tile_base(t, g.nty, g.TY, g.Y, g.Z);
+            for (uint32_t i = lane; i < rn; i += 32) {
+                const uint64_t key = comp_key(score_bits(__float_as_uint(cv[b0 + i]), attn), cp[b0 + i]);
+                const uint32_t slot = warp_append(cnt);
+                if (slot < (uint32_t)kSmallV) keys[slot] = key;
+            }
+            if (lane == 0) tdef[t] = 0;   // every kept entry is counted in tile_sel
+        }
+    }
+    __syncwarp();
+    const uint32_t ns = min(*cnt, (uint32_t)kSmallV);
+    const uint64_t kst = warp_select(keys, ns, (uint32_t)k, h_all[warp], sh_all[warp]);
+    uint32_t* tsel = a.tile_sel + s * a.ntile;
+    for (uint32_t i = lane; i < ns; i += 32)
+        if (keys[i] >= kst) atomicAdd(&tsel[tile_of(0xffffffffu - (uint32_t)keys[i], g)], 1u);
+    if (lane == 0) {
+        FwdSeg st{};
+        st.keep_all = 0;
+        st.kstar = kst;
         a.seg[s] = st;
     }
 }
@@ -447,7 +603,10 @@ cudaError_t launch_stream_find(const FwdArgs& a, cudaStream_t s) {
 cudaError_t launch_stream_resolve(const Geo& gy, const FwdTile& t, const FwdArgs& a, int pass, cudaStream_t s) {
     const StreamGeo g{t.nty, t.TY, gy.Y, gy.Z, gy.V};
     SPC_PHASE(pass == 0 ? "fwd_resolve" : "fwd_resolve_redo", s, 1);
-    stream_resolve_kernel<<<(unsigned)a.nseg, kSRThreads, 0, s>>>(a, g, pass);
+    if (gy.V <= kSmallV)
+        stream_resolve_small_kernel<<<(unsigned)((a.nseg + kSmallWarps - 1) / kSmallWarps), 32 * kSmallWarps, 0, s>>>(a, g, pass);
+    else
+        stream_resolve_kernel<<<(unsigned)a.nseg, kSRThreads, 0, s>>>(a, g, pass);
     return cudaGetLastError();
 }
 

@@ -340,6 +340,24 @@ def test_fwd_forced_redo(cuda_lib, monkeypatch, attn):
         np.testing.assert_array_equal(gv, ov)
 
 
+@pytest.mark.parametrize("dims", [(32, 32), (25, 41), (4, 16, 16)], ids=["V1024", "V1025", "3d_V1024"])
+@pytest.mark.parametrize("attn", ["magnitude", "raw"])
+def test_fwd_resolve_small_segment_boundary(cuda_lib, dims, attn):
+    """Segments of <= 1024 voxels are resolved one warp per segment, larger ones one block per
+    segment: both sides of the boundary, k from 1 to nearly the whole support, dense and sparse
+    inputs -- bit-exact against the oracle."""
+    spc = cuda_lib
+    V = int(np.prod(dims))
+    for rd, k in [(0.3, 1), (0.3, V // 7), (0.05, V // 3), (0.9, V - 3)]:
+        x = uniform_map(3, 2, dims, rd, 4300 + k, values="dyadic")
+        w = sparse_filter(2, 5, (3,) * len(dims), 0.6, 4301, values="dyadic")
+        bias = bias_vector(5, 4302, values="dyadic")
+        ok_, ov, _, _ = ora.conv_fwd(x, w, bias, attn=ATTN_ORA[attn], k=k)
+        gk, gv, _ = run_fwd(spc, x, w, bias, attn, k)
+        np.testing.assert_array_equal(gk, ok_)
+        np.testing.assert_array_equal(gv, ov)
+
+
 def test_fwd_empty_and_degenerate(cuda_lib):
     spc = cuda_lib
     x = COO(2, 2, (5, 6), np.zeros(0, np.uint64), np.zeros(0, np.float32))

@@ -105,11 +105,19 @@ def main():
         gph.replay()
     torch.cuda.synchronize()
     graph = timed(gph.replay, args.steps)
+    # per-phase device time of one eager step (CUDA-event brackets of the library, outside the timing)
+    spc.profile_reset()
+    spc.profile_enable(True)
+    step()
+    torch.cuda.synchronize()
+    spc.profile_enable(False)
+    phases = {k: [round(v[0], 3), v[1]] for k, v in sorted(spc.profile_read().items(), key=lambda kv: -kv[1][0])}
     print(json.dumps({"config": f"OctNet3-{args.res}^3 sparse trunk (Table 2), batch {args.batch}, surface occupancy "
                       f"2%, 9 convs + attention (0.06/0.14/0.33) + ReLU, 2 pools, sparseToDense; fwd+bwd",
                       "eager_ms_per_step": round(eager, 3), "graph_ms_per_step": round(graph, 3),
                       "kernels_per_step": launches[-1], "input_nnz": int(X.nnz_bound), "variant": args.variant,
-                      "choices": sorted(set(spc.ops._MEASURED.values())) if args.variant == "measure" else None}))
+                      "choices": sorted(set(spc.ops._MEASURED.values())) if args.variant == "measure" else None,
+                      "phases_ms_eager": phases}))
 
 
 if __name__ == "__main__":
