@@ -73,6 +73,14 @@ BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int nw_total) {
         int64_t grid = (num_sms() * cps + t.n_ocg - 1) / t.n_ocg;
         grid = std::max<int64_t>(1, std::min<int64_t>(grid, items));
         t.grid = (int)grid;
+        if (items >= ((int64_t)1 << 31)) { t.smem = 0; return t; }   // 32-bit item decode
+        const int HX = bx + 2 * kg.hx, HW = 1 + 2 * kg.hw;
+        t.fd_tiles = make_fastdiv((uint32_t)(t.ntx * t.nty));
+        t.fd_W = make_fastdiv((uint32_t)gx.W);
+        t.fd_ntx = make_fastdiv((uint32_t)t.ntx);
+        t.fd_HWX = make_fastdiv((uint32_t)(HW * HX));
+        t.fd_HX = make_fastdiv((uint32_t)HX);
+        t.fd_TX = make_fastdiv((uint32_t)bx);
         return t;
     }
     t.smem = 0;
@@ -112,7 +120,8 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
     const int HXY = HX * HY;
     const int slice = HW * HXY * ZR;
     const int gsize = t.ocg * slice;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int nwarps = THREADS / 32;
 
     // ---- shared layout: G | dwp | wdel | wv | lbase | cpre | rng | stage
     float* G = reinterpret_cast<float*>(smraw);
@@ -164,17 +173,20 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
 
     const int64_t items = gx.B * gx.W * (int64_t)t.ntx * t.nty;
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-        const int64_t bw = item / ((int64_t)t.ntx * t.nty);   // (b, w-plane)
-        const int64_t b = bw / gx.W;
-        const int wp = (int)(bw - b * gx.W);
-        const int tile = (int)(item - bw * (int64_t)t.ntx * t.nty);
-        const int x0 = (tile % t.ntx) * t.TX, y0 = (tile / t.ntx) * t.TY;
+        // (items < 2^31, plan_bwd_tile): divisions by multiply-high
+        const uint32_t bw = fdiv((uint32_t)item, t.fd_tiles);   // (b, w-plane)
+        const uint32_t bq = fdiv(bw, t.fd_W);
+        const int64_t b = bq;
+        const int wp = (int)(bw - bq * (uint32_t)gx.W);
+        const int tile = (int)((uint32_t)item - bw * (uint32_t)(t.ntx * t.nty));
+        const int tyi = (int)fdiv((uint32_t)tile, t.fd_ntx);
+        const int x0 = (tile - tyi * t.ntx) * t.TX, y0 = tyi * t.TY;
         const int xe = min(x0 + t.TX, gx.X), ye = min(y0 + t.TY, gx.Y);
         __syncthreads();
         // entry ranges: per (ic, x) the stored entries of rows y0..ye-1 are contiguous (loaded
         // first: their latency overlaps the gradient fill below)
         for (int q = threadIdx.x; q < c_in * t.TX; q += blockDim.x) {
-            const int ic = q / t.TX, xi = q - (q / t.TX) * t.TX;
+            const int ic = (int)fdiv((uint32_t)q, t.fd_TX), xi = q - ic * t.TX;
             uint32_t lo = 0, hi = 0;
             if (x0 + xi < xe) {
                 const int64_t r0 = (((b * c_in + ic) * gx.W + wp) * gx.X + x0 + xi) * (int64_t)gx.Y + y0;
@@ -192,8 +204,8 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
         const int HWX = HW * HX;
         // halo row r = (ocl, hw-plane, hx-row) -> its first y-row in the output map (or -1)
         auto halo_row = [&](int r, int& gbase) -> int64_t {
-            const int ocl = r / HWX, hr = r - ocl * HWX;
-            const int hwi = hr / HX, hxr = hr - hwi * HX;
+            const int ocl = (int)fdiv((uint32_t)r, t.fd_HWX), hr = r - ocl * HWX;
+            const int hwi = (int)fdiv((uint32_t)hr, t.fd_HX), hxr = hr - hwi * HX;
             const int ws = wp - kg.hw + hwi, xs = x0 - kg.hx + hxr;
             gbase = (((ocl * HW + hwi) * HX + hxr) * HY + (hylo - (y0 - kg.hy))) * ZR + kg.hz;
             if (ws < 0 || ws >= gy.W || xs < 0 || xs >= gy.X || hylo >= hyhi) return -1;

@@ -201,13 +201,15 @@ __device__ __forceinline__ void epi_cand(const float* S, int nyr, int Z, int ZR,
     uint32_t nb = 0, nf = 0, sup = 0, mx = 0;   // buffered, flushed
     // 128-voxel slots in key order (row, z0); two slots per step, their eight loads issued first
     const int nz0 = (Z + 127) >> 7, nslot = nyr * nz0;
+    int r_s = 0, zi_s = 0;   // (row, 128-voxel column) of slot s0, advanced without divisions
     for (int s0 = 0; s0 < nslot; s0 += 2) {
         float raw[8];
         uint32_t pz[8];
+        int r = r_s, zi = zi_s;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int sl = s0 + h;
-            const int r = sl / nz0, z0 = (sl - r * nz0) << 7;
+            const int z0 = zi << 7;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int z = z0 + 32 * u + lane;
@@ -215,7 +217,10 @@ __device__ __forceinline__ void epi_cand(const float* S, int nyr, int Z, int ZR,
                 raw[4 * h + u] = in ? S[r * ZR + z] : __uint_as_float(marker);
                 pz[4 * h + u] = pbase + (uint32_t)(r * Z + z);
             }
+            if (++zi == nz0) { zi = 0; ++r; }
         }
+        r_s = r;
+        zi_s = zi;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
 #pragma unroll

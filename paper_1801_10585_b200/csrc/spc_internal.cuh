@@ -116,6 +116,27 @@ __device__ __forceinline__ uint32_t div_small(uint32_t L, uint32_t Z, float invZ
     return q;
 }
 
+// n / d for 0 <= n < 2^31 by a multiply-high and a shift (d fixed per launch, set on the host):
+// m = ceil(2^p / d) with p = 31 + ceil(log2 d), quotient = umulhi(n, m) >> (p - 32); d = 1 is
+// m = 0.
+struct FastDiv {
+    uint32_t d, m, s;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f{d, 0u, 0u};
+    if (d > 1) {
+        uint32_t l = 0;
+        while ((1ull << l) < d) ++l;   // ceil(log2 d)
+        const uint32_t p = 31 + l;
+        f.m = (uint32_t)(((1ull << p) + d - 1) / d);
+        f.s = p - 32;
+    }
+    return f;
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+    return f.m ? __umulhi(n, f.m) >> f.s : n;
+}
+
 __device__ __forceinline__ int64_t load_n(const int64_t* nnz_dev, int64_t bound) {
     if (!nnz_dev) return bound;
     int64_t n = *nnz_dev;
@@ -312,6 +333,7 @@ cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& k
 
 struct BwdTile {
     int TX, TY, ocg, ntx, nty, n_ocg, grid;
+    FastDiv fd_tiles, fd_W, fd_ntx, fd_HWX, fd_HX, fd_TX;   // ntx*nty, W, ntx, HW*HX, HX, TX
     int threads;      // CTA size (512: one CTA per SM, 256: two)
     int nwg_max;      // upper bound of stored weights in one output-channel group
     size_t smem;
