@@ -80,6 +80,8 @@ FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_
     t.nwg_max = (int)nwg(ocg);
     t.rec_smem = rec_sm(ocg) ? 1 : 0;
     t.smem = need(ocg, t.TY);
+    t.fd_nty = make_fastdiv((uint32_t)t.nty);
+    t.fd_X = make_fastdiv((uint32_t)gy.X);
     return t;
 }
 
@@ -398,9 +400,9 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
     extern __shared__ __align__(16) float smf[];
     const int c_in = (int)gx.C, c_out = (int)gy.C;
     const int Z = gy.Z, ZR = t.ZR;
-    const int ty = tin % t.nty;
-    const int P = tin / t.nty;                       // output plane (w, x): P = w*X + x
-    const int x = P % gy.X, wpl = P / gy.X;
+    const int P = (int)fdiv((uint32_t)tin, t.fd_nty);   // output plane (w, x): P = w*X + x
+    const int ty = tin - P * t.nty;
+    const int wpl = (int)fdiv((uint32_t)P, t.fd_X), x = P - wpl * gy.X;
     const int64_t b = a.b0 + bl;                        // global sample (input rows)
     const int oc0 = blockIdx.y * t.ocg;
     const int nocl = min(t.ocg, c_out - oc0);
@@ -662,16 +664,16 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
 // (B * ntile, n_ocg).
 template <bool REC_SMEM>
 __global__ void __launch_bounds__(kFwdThreads, 2) conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
-    const int64_t tile = blockIdx.x;
-    fwd_tile<REC_SMEM, kEpiCand>(gx, gy, kg, t, a, tile / a.ntile, (int)(tile % a.ntile));
+    const uint32_t tile = blockIdx.x, bl = fdiv(tile, a.fd_ntile);   // (B * ntile < 2^31)
+    fwd_tile<REC_SMEM, kEpiCand>(gx, gy, kg, t, a, bl, (int)(tile - bl * (uint32_t)a.ntile));
 }
 
 // Sampled pass: grid (B * nsamp, n_ocg); tile j of a segment's sample = j*sp_period + sp_off.
 template <bool REC_SMEM>
 __global__ void __launch_bounds__(kFwdThreads, 2) conv_fwd_sample_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t,
                                                                          FwdArgs a) {
-    const int64_t j = blockIdx.x;
-    fwd_tile<REC_SMEM, kEpiSample>(gx, gy, kg, t, a, j / a.nsamp, (int)(j % a.nsamp) * a.sp_period + a.sp_off);
+    const uint32_t j = blockIdx.x, bl = fdiv(j, a.fd_nsamp);
+    fwd_tile<REC_SMEM, kEpiSample>(gx, gy, kg, t, a, bl, (int)(j - bl * (uint32_t)a.nsamp) * a.sp_period + a.sp_off);
 }
 
 // Redo pass: grid (ntile, n_ocg); block t recomputes tile t of every queued sample (normally
@@ -1107,6 +1109,8 @@ void plan_fwd_sampling(const Geo& gy, const FwdTile& t, int attn, FwdArgs* a) {
     a->sp_period = P > 0 ? P : 1;
     a->sp_off = P / 2;
     a->nsamp = (attn != SPC_ATTN_NONE && P > 0) ? (a->ntile - a->sp_off + P - 1) / P : 0;
+    a->fd_ntile = make_fastdiv((uint32_t)a->ntile);
+    a->fd_nsamp = make_fastdiv((uint32_t)std::max(1, a->nsamp));
 }
 
 template <bool REC>

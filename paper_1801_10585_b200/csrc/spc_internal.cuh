@@ -197,6 +197,7 @@ struct FwdTile {
     int PK;            // work items (ic, input plane) = c_in * kx
     int nwg_max;       // stored weights of one output-channel group (upper bound = round records)
     int rec_smem;      // 1: round records copied to shared memory; 0: read through L1
+    FastDiv fd_nty, fd_X;   // tile index -> (plane, band), plane -> (w, x)
     size_t smem;
 };
 FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_t nw_total);
@@ -261,6 +262,7 @@ struct FwdArgs {
     // the tile's voxels).
     int ntile;                       // tiles per segment (X * nty)
     int nsamp, sp_period, sp_off;    // sampled tiles per segment: t = j*sp_period + sp_off
+    FastDiv fd_ntile, fd_nsamp;      // block index decode of the tile kernels
     uint32_t* tlow;                  // [nseg] candidate score threshold (0: every support entry)
     uint32_t* cmax;                  // [nseg] largest candidate score
     uint32_t* cpos;                  // [nseg * V] candidate spatial index p
