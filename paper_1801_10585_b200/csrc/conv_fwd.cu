@@ -290,6 +290,26 @@ __device__ __forceinline__ void sts_p(uint32_t addr, float v, bool p) {
                  :: "r"(addr), "f"(v), "r"((int)p) : "memory");
 }
 
+// -0 mode RMW of the lane's two entries in one predicated block: loads, fmas and stores under
+// the entries' predicates, no zero-initialised temporaries (the same instructions the C++ form
+// needs, minus the moves and selects the compiler adds around conditional asm outputs)
+__device__ __forceinline__ void rmw2_neg0(uint32_t qa, uint32_t qb, float va, float vb, float w, int oka, int okb) {
+    asm volatile(
+        "{\n\t.reg .pred pa, pb;\n\t.reg .f32 ta, tb;\n\t"
+        "setp.ne.b32 pa, %5, 0;\n\tsetp.ne.b32 pb, %6, 0;\n\t"
+        "@pa ld.shared.f32 ta, [%0];\n\t@pb ld.shared.f32 tb, [%1];\n\t"
+        "@pa fma.rn.f32 ta, %2, %4, ta;\n\t@pb fma.rn.f32 tb, %3, %4, tb;\n\t"
+        "@pa st.shared.f32 [%0], ta;\n\t@pb st.shared.f32 [%1], tb;\n\t}"
+        :: "r"(qa), "r"(qb), "f"(va), "f"(vb), "f"(w), "r"(oka), "r"(okb) : "memory");
+}
+__device__ __forceinline__ void rmw1_neg0(uint32_t qa, float va, float w, int oka) {
+    asm volatile(
+        "{\n\t.reg .pred pa;\n\t.reg .f32 ta;\n\t"
+        "setp.ne.b32 pa, %3, 0;\n\t"
+        "@pa ld.shared.f32 ta, [%0];\n\t@pa fma.rn.f32 ta, %1, %2, ta;\n\t@pa st.shared.f32 [%0], ta;\n\t}"
+        :: "r"(qa), "f"(va), "f"(w), "r"(oka) : "memory");
+}
+
 // (-0 mode: the marker is -0.0, which the first fma replaces by the product itself)
 template <bool NEG0>
 __device__ __forceinline__ float upd(float old, float v, float w) {
@@ -356,11 +376,15 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
                 const int2 qn = rec[r + 1];   // next record in flight during this round (rec has a spare slot)
                 const uint32_t qa = d.aA + (uint32_t)q.x, qb = d.aB + (uint32_t)q.x;
                 const float w = __int_as_float(q.y);
-                float oa = 0.0f, ob = 0.0f;   // idle lanes do not touch shared memory (racecheck-clean)
-                if (okA) oa = lds_u(qa);
-                if (okB) ob = lds_u(qb);
-                if (okA) sts_u(qa, upd<NEG0>(oa, d.vA, w));
-                if (okB) sts_u(qb, upd<NEG0>(ob, d.vB, w));
+                if (NEG0) {
+                    rmw2_neg0(qa, qb, d.vA, d.vB, w, okA, okB);
+                } else {
+                    float oa = 0.0f, ob = 0.0f;   // idle lanes do not touch shared memory (racecheck-clean)
+                    if (okA) oa = lds_u(qa);
+                    if (okB) ob = lds_u(qb);
+                    if (okA) sts_u(qa, upd<NEG0>(oa, d.vA, w));
+                    if (okB) sts_u(qb, upd<NEG0>(ob, d.vB, w));
+                }
 #ifndef SPC_NO_SYNCWARP
                 __syncwarp();
 #endif
@@ -372,7 +396,8 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
             for (int r = d.r0; r < d.r1; ++r) {
                 const int2 qn = rec[r + 1];
                 const uint32_t qa = d.aA + (uint32_t)q.x;
-                if (okA) sts_u(qa, upd<NEG0>(lds_u(qa), d.vA, __int_as_float(q.y)));
+                if (NEG0) rmw1_neg0(qa, d.vA, __int_as_float(q.y), okA);
+                else if (okA) sts_u(qa, upd<NEG0>(lds_u(qa), d.vA, __int_as_float(q.y)));
 #ifndef SPC_NO_SYNCWARP
                 __syncwarp();
 #endif
