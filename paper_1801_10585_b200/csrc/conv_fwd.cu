@@ -192,7 +192,7 @@ __device__ __forceinline__ void epi_hist_rows(const float* S, float bv, int nyr,
 // (branch-free: non-candidates store to a private dummy slot) that is flushed to the run with
 // coalesced stores. Returns the run length, the support size and the largest candidate score.
 constexpr int kCandBuf = 160;   // per-warp buffer entries (+ 32 dummy slots), in the staging area
-template <int MODE>
+template <int MODE, bool FULL>   // FULL: Z is a multiple of 128 (no ragged 128-voxel slot)
 __device__ __forceinline__ void epi_cand(const float* S, int nyr, int Z, int ZR, float bv, uint32_t tlow,
                                          uint32_t marker, uint32_t pbase, uint32_t* __restrict__ cpos,
                                          float* __restrict__ cval, uint32_t* bufp, float* bufv, uint32_t& n_out,
@@ -215,7 +215,7 @@ __device__ __forceinline__ void epi_cand(const float* S, int nyr, int Z, int ZR,
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int z = z0 + 32 * u + lane;
-                const bool in = sl < nslot && z < Z;
+                const bool in = sl < nslot && (FULL || z < Z);
                 raw[4 * h + u] = in ? S[r * ZR + z] : __uint_as_float(marker);
                 pz[4 * h + u] = pbase + (uint32_t)(r * Z + z);
             }
@@ -232,7 +232,8 @@ __device__ __forceinline__ void epi_cand(const float* S, int nyr, int Z, int ZR,
                 const float val = raw[q] + bv;
                 const uint32_t sc = MODE == SPC_ATTN_NONE ? 0u : score_bits(__float_as_uint(val), MODE);
                 const bool c = pres && sc >= tlow;
-                sup += pres ? 1u : 0u;
+                asm("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %1, 0;\n\t@p add.u32 %0, %0, 1;\n\t}"
+                    : "+r"(sup) : "r"((int)pres));
                 mx = c ? max(mx, sc) : mx;
                 const uint32_t bal = __ballot_sync(kFull, c);
                 const uint32_t slot = c ? nb + (uint32_t)__popc(bal & lt) : dummy;
@@ -627,12 +628,16 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
         static_assert(kFwdWarps * kBufStride <= kStageCap, "candidate buffers live in the staging area");
         uint32_t* bp = spos + warp * kBufStride;
         float* bvv = sval + warp * kBufStride;
-        if (a.attn == SPC_ATTN_MAGNITUDE)
-            epi_cand<SPC_ATTN_MAGNITUDE>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, bvv, n, sup, mx);
-        else if (a.attn == SPC_ATTN_RAW)
-            epi_cand<SPC_ATTN_RAW>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, bvv, n, sup, mx);
-        else
-            epi_cand<SPC_ATTN_NONE>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, bvv, n, sup, mx);
+        const bool full = (Z & 127) == 0;
+        if (a.attn == SPC_ATTN_MAGNITUDE) {
+            if (full) epi_cand<SPC_ATTN_MAGNITUDE, true>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, bvv, n, sup, mx);
+            else epi_cand<SPC_ATTN_MAGNITUDE, false>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, bvv, n, sup, mx);
+        } else if (a.attn == SPC_ATTN_RAW) {
+            if (full) epi_cand<SPC_ATTN_RAW, true>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, bvv, n, sup, mx);
+            else epi_cand<SPC_ATTN_RAW, false>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, bvv, n, sup, mx);
+        } else {
+            epi_cand<SPC_ATTN_NONE, false>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, bvv, n, sup, mx);
+        }
         if (lane == 0) {
             a.tcnt[s * a.ntile + tin] = n;
             if (n) {

@@ -57,6 +57,7 @@ FWD_CASES = [
     ("3d_wide_oc", (10, 12, 14), 1, 2, 40, (3, 3, 3), 0.05, 0.3),  # several oc groups
     ("3d_long_z", (3, 3, 700), 2, 2, 3, (3, 3, 3), 0.05, 0.5),
     ("3d_dense", (12, 16, 64), 1, 3, 4, (3, 3, 3), 0.4, 0.5),     # > 32 inputs per warp item
+    ("3d_z128", (5, 9, 128), 2, 3, 4, (3, 3, 3), 0.05, 0.5),      # Z a multiple of 128
 ]
 
 
@@ -297,6 +298,8 @@ SAMPLED_CASES = [
     ("3d_sampled", (40, 96, 64), 1, 4, 4, (3, 3, 3), 0.03, 0.5),
     ("3d_sampled_ragged_z", (45, 70, 37), 1, 3, 8, (3, 3, 3), 0.04, 0.5),
     ("3d_sampled_two_groups", (36, 64, 32), 2, 3, 12, (3, 3, 3), 0.05, 0.5),
+    ("3d_sampled_z128", (24, 40, 128), 1, 3, 5, (3, 3, 3), 0.03, 0.5),   # full 128-voxel epilogue slots
+    ("3d_sampled_z256", (12, 30, 256), 1, 2, 4, (3, 3, 3), 0.03, 0.5),
 ]
 
 
