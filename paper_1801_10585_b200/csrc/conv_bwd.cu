@@ -27,8 +27,26 @@ static int bwd_ctas_per_sm() {
     return (v && v[0] == '2') ? 2 : 1;
 }
 
-static size_t bwd_smem(const KGeo& kg, int c_in, int TX, int TY, int ZR, int ocg, int64_t nwg, int threads) {
-    const size_t g = (size_t)ocg * (1 + 2 * kg.hw) * (TX + 2 * kg.hx) * (TY + 2 * kg.hy) * ZR * sizeof(float);
+// Strides of the G slab (floats): y-row sY, x-row sX, w-plane sW, output-channel slice sOC, each
+// padded to a residue mod 32 that makes the filter offsets dz + dy*sY + dx*sX + dw*sW land in
+// distinct banks (mixed radix kz, kz*ky, kz*ky*kx, ...): the 32 lanes of a G load read one
+// entry's targets under 32 different weights, i.e. 32 different filter offsets.
+struct BwdStrides {
+    int sY, sX, sW, sOC;
+};
+static BwdStrides bwd_strides(const KGeo& kg, int Z, int TX, int TY) {
+    auto pad = [](int v, int r) { return v + ((r - v) % 32 + 32) % 32; };   // >= v, == r mod 32
+    const int HW = 1 + 2 * kg.hw, HX = TX + 2 * kg.hx, HY = TY + 2 * kg.hy;
+    BwdStrides st;
+    st.sY = pad(Z + 2 * kg.hz, kg.kz % 32);
+    st.sX = pad(HY * st.sY, (kg.kz * kg.ky) % 32);
+    st.sW = pad(HX * st.sX, (kg.kz * kg.ky * kg.kx) % 32);
+    st.sOC = pad(HW * st.sW, (kg.kz * kg.ky * kg.kx * kg.kw) % 32);
+    return st;
+}
+
+static size_t bwd_smem(const KGeo& kg, int c_in, int TX, int TY, int Z, int ocg, int64_t nwg, int threads) {
+    const size_t g = (size_t)ocg * bwd_strides(kg, Z, TX, TY).sOC * sizeof(float);
     const size_t w = (size_t)nwg * (sizeof(int) + sizeof(float) + sizeof(double));
     const size_t idx = (size_t)(c_in + 1) * sizeof(int) * 2 + (size_t)c_in * TX * 2 * sizeof(uint32_t);
     const size_t stage = (size_t)(threads / 32) * 32 * 4 * sizeof(int);   // per warp: 4 x 32 words
@@ -38,7 +56,6 @@ static size_t bwd_smem(const KGeo& kg, int c_in, int TX, int TY, int ZR, int ocg
 BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int nw_total) {
     BwdTile t{};
     const int c_in = (int)gx.C;
-    const int ZR = gx.Z + 2 * kg.hz;
     const int cps = bwd_ctas_per_sm();
     const int threads = cps == 2 ? 256 : 512;
     const size_t budget = cps == 2 ? 110 * 1024 : 200 * 1024;
@@ -51,7 +68,7 @@ BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int nw_total) {
             int lo = 1, hi = gx.Y, ty = 0;
             while (lo <= hi) {   // largest ty that fits
                 const int mid = (lo + hi) / 2;
-                if (bwd_smem(kg, c_in, tx, mid, ZR, ocg, nwg, threads) <= budget) { ty = mid; lo = mid + 1; }
+                if (bwd_smem(kg, c_in, tx, mid, gx.Z, ocg, nwg, threads) <= budget) { ty = mid; lo = mid + 1; }
                 else hi = mid - 1;
             }
             if (ty < 1) break;
@@ -67,7 +84,14 @@ BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int nw_total) {
         t.ntx = (gx.X + bx - 1) / bx;
         t.nty = (gx.Y + by - 1) / by;
         t.nwg_max = (int)nwg;
-        t.smem = bwd_smem(kg, c_in, bx, by, ZR, ocg, nwg, threads);
+        t.smem = bwd_smem(kg, c_in, bx, by, gx.Z, ocg, nwg, threads);
+        {
+            const BwdStrides st = bwd_strides(kg, gx.Z, bx, by);
+            t.sY = st.sY;
+            t.sX = st.sX;
+            t.sW = st.sW;
+            t.sOC = st.sOC;
+        }
         t.threads = threads;
         const int64_t items = gx.B * gx.W * (int64_t)t.ntx * t.nty;
         int64_t grid = (num_sms() * cps + t.n_ocg - 1) / t.n_ocg;
@@ -115,11 +139,10 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
     const int nocl = min(t.ocg, c_out - oc0);
     // G slab of one output-channel slice: HW w-planes x HX x-rows x HY y-rows x ZR (rank-4 maps:
     // the tile is one w-plane, its halo the 2*hw neighbouring planes; HW = 1 for rank <= 3)
-    const int HW = 1 + 2 * kg.hw, HX = t.TX + 2 * kg.hx, HY = t.TY + 2 * kg.hy;
-    const int ZR = gx.Z + 2 * kg.hz;
-    const int HXY = HX * HY;
-    const int slice = HW * HXY * ZR;
-    const int gsize = t.ocg * slice;
+    // (strides t.sY / sX / sW / sOC: bwd_strides)
+    const int HW = 1 + 2 * kg.hw, HX = t.TX + 2 * kg.hx;
+    const int sY = t.sY, sX = t.sX, sW = t.sW, sOC = t.sOC;
+    const int gsize = t.ocg * sOC;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int nwarps = THREADS / 32;
 
@@ -162,14 +185,14 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
         for (int j = threadIdx.x; j < n; j += blockDim.x) {
             const int2 m = wmeta[t0 + j];
             // g at uid = id - (fid - centre): G index = ebase - wdel
-            wdel[lbase[ic] + j] = ((meta_ow(m.x) * HX + off_x(m.y)) * HY + off_y(m.y)) * ZR + off_z(m.y) -
-                                  (meta_oc(m.x) - oc0) * slice;
+            wdel[lbase[ic] + j] = meta_ow(m.x) * sW + off_x(m.y) * sX + off_y(m.y) * sY + off_z(m.y) -
+                                  (meta_oc(m.x) - oc0) * sOC;
             wv[lbase[ic] + j] = wval[t0 + j];
         }
     }
     for (int i = threadIdx.x; i < nwg; i += blockDim.x) dwp[i] = 0.0;
     for (int i = threadIdx.x; i < gsize; i += blockDim.x) G[i] = 0.0f;
-    const int eb_safe = ((kg.hw * HX + kg.hx) * HY + kg.hy) * ZR + kg.hz;   // an in-range G index for idle lanes
+    const int eb_safe = kg.hw * sW + kg.hx * sX + kg.hy * sY + kg.hz;   // an in-range G index for idle lanes
 
     const int64_t items = gx.B * gx.W * (int64_t)t.ntx * t.nty;
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
@@ -207,7 +230,7 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
             const int ocl = (int)fdiv((uint32_t)r, t.fd_HWX), hr = r - ocl * HWX;
             const int hwi = (int)fdiv((uint32_t)hr, t.fd_HX), hxr = hr - hwi * HX;
             const int ws = wp - kg.hw + hwi, xs = x0 - kg.hx + hxr;
-            gbase = (((ocl * HW + hwi) * HX + hxr) * HY + (hylo - (y0 - kg.hy))) * ZR + kg.hz;
+            gbase = ocl * sOC + hwi * sW + hxr * sX + (hylo - (y0 - kg.hy)) * sY + kg.hz;
             if (ws < 0 || ws >= gy.W || xs < 0 || xs >= gy.X || hylo >= hyhi) return -1;
             return (((b * c_out + oc0 + ocl) * gy.W + ws) * gy.X + xs) * (int64_t)gy.Y + hylo;
         };
@@ -270,7 +293,7 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
                     uint32_t yr = __float2uint_rz(__uint2float_rz(L) * invZ);
                     if (yr * (uint32_t)gy.Z > L) --yr;
                     if ((yr + 1) * (uint32_t)gy.Z <= L) ++yr;
-                    G[gbase + (int)yr * ZR + (int)(L - yr * (uint32_t)gy.Z)] = dv[j];
+                    G[gbase + (int)yr * sY + (int)(L - yr * (uint32_t)gy.Z)] = dv[j];
                 }
             }
             __syncwarp();
@@ -333,7 +356,7 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
                 const uint32_t L = (uint32_t)(cur.key - (uint64_t)r0 * (uint64_t)gx.Z);
                 const uint32_t yl = div_small(L, (uint32_t)gx.Z, invXZ);   // L < TY * Z
                 const int z = (int)(L - yl * (uint32_t)gx.Z);
-                eb = ((kg.hw * HX + cur.xi + kg.hx) * HY + (int)yl + kg.hy) * ZR + z + kg.hz;
+                eb = kg.hw * sW + (cur.xi + kg.hx) * sX + ((int)yl + kg.hy) * sY + z + kg.hz;
             }
             __syncwarp();
             st_eb[lane] = eb * (int)sizeof(float);   // byte offsets into G
