@@ -255,30 +255,37 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
             const uint32_t len = be1 - be0;
             const uint32_t incl = warp_incl_scan(len);
             const uint32_t wtot = __shfl_sync(kFull, incl, 31);
+            // the non-empty rows, compacted: their starts cum_k are strictly increasing, so the
+            // row of list position pos is (rows starting at or before pos) - 1
+            const unsigned nzm = __ballot_sync(kFull, len != 0u);
+            const int kc = __popc(nzm & ((1u << lane) - 1u));
             __syncwarp();
-            st_eb[lane] = (int)(incl - len);   // cum_k
-            st_eb[32 + lane] = (int)be0;       // e0_k
-            st_gb[lane] = gb;
-            st_rz[lane] = rz;
+            if (len != 0u) {
+                st_eb[kc] = (int)(incl - len);   // cum_k
+                st_eb[32 + kc] = (int)be0;       // e0_k
+                st_gb[kc] = gb;
+                st_rz[kc] = rz;
+            }
             __syncwarp();
-            const int nrows = min(32, (nocl * HWX - r0 + nwarps - 1) / nwarps);
+            const uint32_t mycum = lane < __popc(nzm) ? (uint32_t)st_eb[lane] : 0xffffffffu;
             for (uint32_t base = 0; base < wtot; base += 256) {
                 uint64_t kk[8];
                 float dv[8];
                 int rk[8];
-                uint32_t pe[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const uint32_t pos = base + 32u * j + (uint32_t)lane;
+                    const uint32_t w0 = base + 32u * j;   // window of 32 list positions (warp-uniform)
+                    const uint32_t pos = w0 + (uint32_t)lane;
                     rk[j] = -1;
                     kk[j] = 0ull;
                     dv[j] = 0.0f;
+                    if (w0 >= wtot) continue;
+                    // rows starting at or before w0, plus one bit per row starting inside the window
+                    const int before = __popc(__ballot_sync(kFull, mycum <= w0));
+                    const uint32_t d = mycum - w0;
+                    const uint32_t bits = __reduce_or_sync(kFull, (mycum > w0 && d < 32u) ? (1u << d) : 0u);
+                    const int k = before + __popc(bits & (0xffffffffu >> (31 - lane))) - 1;
                     if (pos < wtot) {
-                        int k = 0, hi = nrows;   // last row k with cum_k <= pos (binary search)
-                        while (hi - k > 1) {
-                            const int mid = (k + hi) >> 1;
-                            if ((uint32_t)st_eb[mid] <= pos) k = mid; else hi = mid;
-                        }
                         const uint32_t e = (uint32_t)st_eb[32 + k] + (pos - (uint32_t)st_eb[k]);
                         kk[j] = ykeys[e];
                         dv[j] = dy[e];
@@ -414,7 +421,8 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
         {
             float4* G4 = reinterpret_cast<float4*>(G);
             const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int i = threadIdx.x; i < (gsize >> 2); i += blockDim.x) G4[i] = z4;
+#pragma unroll 4
+            for (int i = threadIdx.x; i < (gsize >> 2); i += THREADS) G4[i] = z4;
             for (int i = (gsize & ~3) + threadIdx.x; i < gsize; i += blockDim.x) G[i] = 0.0f;
         }
     }
