@@ -82,6 +82,7 @@ FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_
     t.smem = need(ocg, t.TY);
     t.fd_nty = make_fastdiv((uint32_t)t.nty);
     t.fd_X = make_fastdiv((uint32_t)gy.X);
+    t.fd_Z = make_fastdiv((uint32_t)gy.Z);
     return t;
 }
 
@@ -189,18 +190,19 @@ __device__ __forceinline__ void epi_hist_rows(const float* S, float bv, int nyr,
 // reaches the segment's threshold tlow is appended in key order to the tile's candidate run.
 // Row by row, 128 voxels per step: lane l holds z = z0 + l + 32u (u = 0..3), so each of the four
 // 32-voxel groups is one ballot. Candidates are ranked into a per-warp shared-memory buffer
-// (branch-free: non-candidates store to a private dummy slot) that is flushed to the run with
-// coalesced stores. Returns the run length, the support size and the largest candidate score.
-constexpr int kCandBuf = 160;   // per-warp buffer entries (+ 32 dummy slots), in the staging area
+// as (position, value) pairs -- one 8-byte store per candidate, none for the other lanes, so a
+// 32-voxel group costs one shared-memory wavefront when it has candidates -- and the buffer is
+// flushed to the run with coalesced stores. Returns the run length and the largest candidate
+// score.
+constexpr int kCandBuf = 192;   // per-warp buffer entries, in the staging area
 template <int MODE, bool FULL>   // FULL: Z is a multiple of 128 (no ragged 128-voxel slot)
 __device__ __forceinline__ void epi_cand(const float* S, int nyr, int Z, int ZR, float bv, uint32_t tlow,
                                          uint32_t marker, uint32_t pbase, uint32_t* __restrict__ cpos,
-                                         float* __restrict__ cval, uint32_t* bufp, float* bufv, uint32_t& n_out,
-                                         uint32_t& sup_out, uint32_t& max_out) {
+                                         float* __restrict__ cval, uint2* buf, uint32_t& n_out, uint32_t& max_out) {
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
-    const uint32_t dummy = kCandBuf + (uint32_t)lane;
-    uint32_t nb = 0, nf = 0, sup = 0, mx = 0;   // buffered, flushed
+    const uint32_t bufs = (uint32_t)__cvta_generic_to_shared(buf);
+    uint32_t nb = 0, nf = 0, mx = 0;   // buffered, flushed
     // 128-voxel slots in key order (row, z0); two slots per step, their eight loads issued first
     const int nz0 = (Z + 127) >> 7, nslot = nyr * nz0;
     int r_s = 0, zi_s = 0;   // (row, 128-voxel column) of slot s0, advanced without divisions
@@ -232,20 +234,21 @@ __device__ __forceinline__ void epi_cand(const float* S, int nyr, int Z, int ZR,
                 const float val = raw[q] + bv;
                 const uint32_t sc = MODE == SPC_ATTN_NONE ? 0u : score_bits(__float_as_uint(val), MODE);
                 const bool c = pres && sc >= tlow;
-                asm("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %1, 0;\n\t@p add.u32 %0, %0, 1;\n\t}"
-                    : "+r"(sup) : "r"((int)pres));
                 mx = c ? max(mx, sc) : mx;
                 const uint32_t bal = __ballot_sync(kFull, c);
-                const uint32_t slot = c ? nb + (uint32_t)__popc(bal & lt) : dummy;
-                bufp[slot] = pz[q];
-                bufv[slot] = val;
+                {   // predicated 8-byte store (no branch): only candidate lanes write
+                    const uint32_t ad = bufs + 8u * (nb + (uint32_t)__popc(bal & lt));
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t@p st.shared.v2.u32 [%0], {%1, %2};\n\t}"
+                                 :: "r"(ad), "r"(pz[q]), "r"(__float_as_uint(val)), "r"((int)c) : "memory");
+                }
                 nb += (uint32_t)__popc(bal);
             }
             if (nb > kCandBuf - 128) {   // flush: coalesced copy of the buffer to the run
                 __syncwarp();
                 for (uint32_t i = lane; i < nb; i += 32) {
-                    cpos[nf + i] = bufp[i];
-                    cval[nf + i] = bufv[i];
+                    const uint2 e = buf[i];
+                    cpos[nf + i] = e.x;
+                    cval[nf + i] = __uint_as_float(e.y);
                 }
                 nf += nb;
                 nb = 0;
@@ -255,16 +258,15 @@ __device__ __forceinline__ void epi_cand(const float* S, int nyr, int Z, int ZR,
     }
     __syncwarp();
     for (uint32_t i = lane; i < nb; i += 32) {
-        cpos[nf + i] = bufp[i];
-        cval[nf + i] = bufv[i];
+        const uint2 e = buf[i];
+        cpos[nf + i] = e.x;
+        cval[nf + i] = __uint_as_float(e.y);
     }
     n_out = nf + nb;
-    sup_out = warp_sum(sup);
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, d));
     max_out = mx;
 }
-
 
 // "add val*fval to buffer at uid" on the shared accumulator; the first update of a voxel
 // replaces the absent marker (structural support, reading R3)
@@ -597,8 +599,8 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
             }
             __syncthreads();
         }
-        // ---- accumulate (Alg. 1 inner loops)
         const int nwork = single ? wtotal : (int)misc[0];
+        // ---- accumulate (Alg. 1 inner loops)
         if (warp < nocl) {
             if (neg0)
                 fwd_items<true>(nwork, lane, accs, safe, work, roffs + warp * PK, recp, spos, sval);
@@ -623,20 +625,18 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
         const uint32_t pbase = (uint32_t)(((int64_t)P * gy.Y + y0) * Z);
         uint32_t* cp = a.cpos + s * gy.V + pbase;
         float* cv = a.cval + s * gy.V + pbase;
-        uint32_t n, sup, mx;
-        constexpr int kBufStride = kCandBuf + 32;
-        static_assert(kFwdWarps * kBufStride <= kStageCap, "candidate buffers live in the staging area");
-        uint32_t* bp = spos + warp * kBufStride;
-        float* bvv = sval + warp * kBufStride;
+        uint32_t n, mx;
+        static_assert(kFwdWarps * kCandBuf <= kStageCap, "candidate buffers live in the staging area");
+        uint2* bp = reinterpret_cast<uint2*>(spos) + warp * kCandBuf;   // (spos | sval: 8 B per staged entry)
         const bool full = (Z & 127) == 0;
         if (a.attn == SPC_ATTN_MAGNITUDE) {
-            if (full) epi_cand<SPC_ATTN_MAGNITUDE, true>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, bvv, n, sup, mx);
-            else epi_cand<SPC_ATTN_MAGNITUDE, false>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, bvv, n, sup, mx);
+            if (full) epi_cand<SPC_ATTN_MAGNITUDE, true>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, n, mx);
+            else epi_cand<SPC_ATTN_MAGNITUDE, false>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, n, mx);
         } else if (a.attn == SPC_ATTN_RAW) {
-            if (full) epi_cand<SPC_ATTN_RAW, true>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, bvv, n, sup, mx);
-            else epi_cand<SPC_ATTN_RAW, false>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, bvv, n, sup, mx);
+            if (full) epi_cand<SPC_ATTN_RAW, true>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, n, mx);
+            else epi_cand<SPC_ATTN_RAW, false>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, n, mx);
         } else {
-            epi_cand<SPC_ATTN_NONE, false>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, bvv, n, sup, mx);
+            epi_cand<SPC_ATTN_NONE, false>(S, nyr, Z, ZR, bv, tl, marker, pbase, cp, cv, bp, n, mx);
         }
         if (lane == 0) {
             a.tcnt[s * a.ntile + tin] = n;
@@ -644,7 +644,6 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
                 atomicAdd(&a.cand_cur[s], (unsigned long long)n);
                 atomicMax(&a.cmax[s], mx);
             }
-            if (EPI == kEpiCand && sup) atomicAdd(&a.seg_count[s], (unsigned long long)sup);
         }
         return;
     }

@@ -236,10 +236,13 @@ __global__ void __launch_bounds__(kSRThreads, 4) stream_resolve_kernel(FwdArgs a
     const int64_t s = blockIdx.x;
     if (pass == 1 && !a.fail[s]) return;
     const uint64_t n = a.cand_cur[s];
-    const uint64_t sup = a.seg_count[s];
     const uint64_t k = (uint64_t)a.k;
-    const bool keep_all = a.attn == SPC_ATTN_NONE || sup <= k;
-    const bool fail = keep_all ? (n != sup) : (n < k);
+    // With tlow = 0 every support entry is a candidate (n = |S|): keep all when |S| <= k. With
+    // tlow > 0 the candidates hold the k largest iff there are at least k of them; otherwise the
+    // segment is recomputed with tlow = 0 (whatever its support size).
+    const bool tl0 = a.tlow[s] == 0u;
+    const bool fail = !tl0 && (a.attn == SPC_ATTN_NONE || n < k);
+    const bool keep_all = a.attn == SPC_ATTN_NONE || n <= k;   // (tlow = 0: n = |S|)
     if (fail) {
         if (pass == 0 && threadIdx.x == 0) {
             // the sampled threshold was too high: recompute this segment with tlow = 0
@@ -464,10 +467,13 @@ __global__ void __launch_bounds__(32 * kSmallWarps) stream_resolve_small_kernel(
     if (s >= a.nseg) return;                       // (warp-uniform, as every return below)
     if (pass == 1 && !a.fail[s]) return;
     const uint64_t n = a.cand_cur[s];
-    const uint64_t sup = a.seg_count[s];
     const uint64_t k = (uint64_t)a.k;
-    const bool keep_all = a.attn == SPC_ATTN_NONE || sup <= k;
-    const bool fail = keep_all ? (n != sup) : (n < k);
+    // With tlow = 0 every support entry is a candidate (n = |S|): keep all when |S| <= k. With
+    // tlow > 0 the candidates hold the k largest iff there are at least k of them; otherwise the
+    // segment is recomputed with tlow = 0 (whatever its support size).
+    const bool tl0 = a.tlow[s] == 0u;
+    const bool fail = !tl0 && (a.attn == SPC_ATTN_NONE || n < k);
+    const bool keep_all = a.attn == SPC_ATTN_NONE || n <= k;   // (tlow = 0: n = |S|)
     if (fail) {
         if (pass == 0 && lane == 0) {
             a.fail[s] = 1;

@@ -198,6 +198,7 @@ struct FwdTile {
     int nwg_max;       // stored weights of one output-channel group (upper bound = round records)
     int rec_smem;      // 1: round records copied to shared memory; 0: read through L1
     FastDiv fd_nty, fd_X;   // tile index -> (plane, band), plane -> (w, x)
+    FastDiv fd_Z;           // voxel of a band -> (row, z) in the candidate epilogue
     size_t smem;
 };
 FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_t nw_total);
