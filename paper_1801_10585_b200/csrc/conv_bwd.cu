@@ -45,10 +45,11 @@ static BwdStrides bwd_strides(const KGeo& kg, int Z, int TX, int TY) {
     return st;
 }
 
-static size_t bwd_smem(const KGeo& kg, int c_in, int TX, int TY, int Z, int ocg, int64_t nwg, int threads) {
-    const size_t g = (size_t)ocg * bwd_strides(kg, Z, TX, TY).sOC * sizeof(float);
+// ocs: output channels in the G slab (one pass); ocp passes per item cover the CTA's group
+static size_t bwd_smem(const KGeo& kg, int c_in, int TX, int TY, int Z, int ocs, int ocp, int64_t nwg, int threads) {
+    const size_t g = (size_t)ocs * bwd_strides(kg, Z, TX, TY).sOC * sizeof(float);
     const size_t w = (size_t)nwg * (sizeof(int) + sizeof(float) + sizeof(double));
-    const size_t idx = (size_t)(c_in + 1) * sizeof(int) * 2 + (size_t)c_in * TX * 2 * sizeof(uint32_t);
+    const size_t idx = (size_t)(c_in + 1) * sizeof(int) * (1 + ocp) + (size_t)c_in * TX * 2 * sizeof(uint32_t);
     const size_t stage = (size_t)(threads / 32) * 32 * 4 * sizeof(int);   // per warp: 4 x 32 words
     return g + w + idx + stage + 256;
 }
@@ -60,7 +61,18 @@ BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int nw_total) {
     const int threads = cps == 2 ? 256 : 512;
     const size_t budget = cps == 2 ? 110 * 1024 : 200 * 1024;
     int ocg = std::min(c_out, cps == 2 ? 4 : 8);
+    // passes per item (SPC_BWD_OCP): the G slab holds ocg / ocp channels, so the tile can be larger
+    // (less halo re-read per interior voxel, more entry chunks per item to spread over the warps)
+    // at the cost of ocp fills / sweeps per item
+    // Measured: C4 (c_in = 8) 3.12 / 3.69 ms for 1 / 2 passes, the C3 chain (32 -> 64 layer)
+    // 20.3 / 18.3 ms per step: wide inputs have enough entries per chunk row to pay for the
+    // second pass.
+    int ocp_req = c_in >= 16 ? 2 : 1;
+    if (const char* v = getenv("SPC_BWD_OCP")) ocp_req = std::max(1, atoi(v));
     for (; ocg >= 1; ocg = ocg > 1 ? (ocg + 1) / 2 : 0) {
+        int ocp = std::min(ocp_req, ocg);
+        while (ocg % ocp) --ocp;
+        const int ocs = ocg / ocp;
         const int64_t nwg = std::min<int64_t>(nw_total, (int64_t)ocg * c_in * kg.KV);
         double best = -1.0;
         int bx = 0, by = 0;
@@ -68,7 +80,7 @@ BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int nw_total) {
             int lo = 1, hi = gx.Y, ty = 0;
             while (lo <= hi) {   // largest ty that fits
                 const int mid = (lo + hi) / 2;
-                if (bwd_smem(kg, c_in, tx, mid, gx.Z, ocg, nwg, threads) <= budget) { ty = mid; lo = mid + 1; }
+                if (bwd_smem(kg, c_in, tx, mid, gx.Z, ocs, ocp, nwg, threads) <= budget) { ty = mid; lo = mid + 1; }
                 else hi = mid - 1;
             }
             if (ty < 1) break;
@@ -80,11 +92,13 @@ BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int nw_total) {
         t.TX = bx;
         t.TY = by;
         t.ocg = ocg;
+        t.ocp = ocp;
+        t.ocs = ocs;
         t.n_ocg = (c_out + ocg - 1) / ocg;
         t.ntx = (gx.X + bx - 1) / bx;
         t.nty = (gx.Y + by - 1) / by;
         t.nwg_max = (int)nwg;
-        t.smem = bwd_smem(kg, c_in, bx, by, gx.Z, ocg, nwg, threads);
+        t.smem = bwd_smem(kg, c_in, bx, by, gx.Z, ocs, ocp, nwg, threads);
         {
             const BwdStrides st = bwd_strides(kg, gx.Z, bx, by);
             t.sY = st.sY;
@@ -126,6 +140,43 @@ __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
     return v[0];
 }
 
+// Slot order of the n weights of one input channel (one thread): counting sort by the bank
+// residue of the G offset (d & 31), then position i of that order goes to block i % nb, lane
+// i / nb while every block still has room (the last block holds L = n - 32 (nb - 1)), the rest
+// round-robin over the full blocks. f(j, slot, d) for each weight j.
+template <typename D, typename F>
+__device__ __forceinline__ void bwd_weight_slots(int ic, int t0, int n, D gdel, F f) {
+    (void)ic;
+    const int nb = (n + 31) >> 5;
+    if (nb <= 1) {   // one block: any order, no conflicts to spread
+        for (int j = 0; j < n; ++j) f(j, j, gdel(t0, j));
+        return;
+    }
+    const int L = n - 32 * (nb - 1);
+    int cnt[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) cnt[r] = 0;
+    for (int j = 0; j < n; ++j) ++cnt[gdel(t0, j) & 31];
+    int run = 0;
+    for (int r = 0; r < 32; ++r) {
+        const int c = cnt[r];
+        cnt[r] = run;
+        run += c;
+    }
+    for (int j = 0; j < n; ++j) {
+        const int d = gdel(t0, j);
+        const int i = cnt[d & 31]++;
+        int slot;
+        if (i < nb * L) {
+            slot = (i % nb) * 32 + i / nb;
+        } else {
+            const int i2 = i - nb * L;
+            slot = (i2 % (nb - 1)) * 32 + L + i2 / (nb - 1);
+        }
+        f(j, slot, d);
+    }
+}
+
 template <bool DX, bool DW, int THREADS>
 __global__ void __launch_bounds__(THREADS, 512 / THREADS)
 conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
@@ -142,7 +193,8 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
     // (strides t.sY / sX / sW / sOC: bwd_strides)
     const int HW = 1 + 2 * kg.hw, HX = t.TX + 2 * kg.hx;
     const int sY = t.sY, sX = t.sX, sW = t.sW, sOC = t.sOC;
-    const int gsize = t.ocg * sOC;
+    const int gsize = t.ocs * sOC;   // the slab holds the ocs channels of one pass
+    const int ocp = t.ocp, ocs = t.ocs;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int nwarps = THREADS / 32;
 
@@ -155,8 +207,8 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
     p += (size_t)t.nwg_max * sizeof(int);
     float* wv = reinterpret_cast<float*>(p);
     p += (size_t)t.nwg_max * sizeof(float);
-    int* lbase = reinterpret_cast<int*>(p);
-    p += (size_t)(c_in + 1) * sizeof(int);
+    int* lbase = reinterpret_cast<int*>(p);   // [pass][ic]: first slot of (pass, ic); [ocp*(c_in+1)]
+    p += (size_t)(c_in + 1) * ocp * sizeof(int);
     int* cpre = reinterpret_cast<int*>(p);
     p += (size_t)(c_in + 1) * sizeof(int);
     uint32_t* rng = reinterpret_cast<uint32_t*>(p);
@@ -168,27 +220,39 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
     int* st_gb = st_eb + 64;                               // G fill: per halo row its G base ...
     uint32_t* st_rz = reinterpret_cast<uint32_t*>(st_eb + 96);   // ... and the low word of its first key
 
-    // ---- one-time setup: group weights with their G-offsets, zero G and dw partials
+    // ---- one-time setup: group weights with their G-offsets, zero G and dw partials. The
+    // weights of an input channel are walked by lanes in blocks of 32; two lanes of a block whose
+    // G offsets agree mod 32 words read the same bank for every entry. So the weights of each
+    // input channel are ordered by that residue and dealt round-robin to the channel's blocks
+    // (bwd_slot): same-residue weights land in different blocks. dw per weight is unaffected by
+    // the order; dx(e), a sum over the weights, only changes its fp32 summation order.
+    // pass p covers output channels oc0 + p*ocs .. (its weights of input channel ic are the
+    // contiguous range wo(p, ic) .. wo(p + 1, ic) of the filter table)
+    auto wo = [&](int pp, int ic) { return woff[ic * (c_out + 1) + oc0 + min(nocl, pp * ocs)]; };
     if (threadIdx.x == 0) {
         int acc = 0;
-        for (int ic = 0; ic < c_in; ++ic) {
-            lbase[ic] = acc;
-            acc += woff[ic * (c_out + 1) + oc0 + nocl] - woff[ic * (c_out + 1) + oc0];
+        for (int pp = 0; pp < ocp; ++pp) {
+            for (int ic = 0; ic < c_in; ++ic) {
+                lbase[pp * (c_in + 1) + ic] = acc;
+                acc += wo(pp + 1, ic) - wo(pp, ic);
+            }
+            lbase[pp * (c_in + 1) + c_in] = acc;
         }
-        lbase[c_in] = acc;
     }
     __syncthreads();
-    const int nwg = lbase[c_in];
-    for (int ic = 0; ic < c_in; ++ic) {
-        const int t0 = woff[ic * (c_out + 1) + oc0];
-        const int n = lbase[ic + 1] - lbase[ic];
-        for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const int nwg = lbase[(ocp - 1) * (c_in + 1) + c_in];
+    for (int q = threadIdx.x; q < c_in * ocp; q += blockDim.x) {
+        const int pp = q / c_in, ic = q - pp * c_in;
+        const int ocb = oc0 + pp * ocs;   // first channel of the pass: slice 0 of the slab
+        auto gdel = [&](int t0, int j) {   // g at uid = id - (fid - centre): G index = ebase - wdel
             const int2 m = wmeta[t0 + j];
-            // g at uid = id - (fid - centre): G index = ebase - wdel
-            wdel[lbase[ic] + j] = meta_ow(m.x) * sW + off_x(m.y) * sX + off_y(m.y) * sY + off_z(m.y) -
-                                  (meta_oc(m.x) - oc0) * sOC;
-            wv[lbase[ic] + j] = wval[t0 + j];
-        }
+            return meta_ow(m.x) * sW + off_x(m.y) * sX + off_y(m.y) * sY + off_z(m.y) - (meta_oc(m.x) - ocb) * sOC;
+        };
+        const int lb = lbase[pp * (c_in + 1) + ic], t0 = wo(pp, ic);
+        bwd_weight_slots(ic, t0, wo(pp + 1, ic) - t0, gdel, [&](int j, int slot, int d) {
+            wdel[lb + slot] = d;
+            wv[lb + slot] = wval[t0 + j];
+        });
     }
     for (int i = threadIdx.x; i < nwg; i += blockDim.x) dwp[i] = 0.0;
     for (int i = threadIdx.x; i < gsize; i += blockDim.x) G[i] = 0.0f;
@@ -219,6 +283,10 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
             rng[2 * q] = lo;
             rng[2 * q + 1] = hi;
         }
+        int nchunks = 0;
+        for (int pp = 0; pp < ocp; ++pp) {
+        const int ocb = oc0 + pp * ocs, nocp = min(ocs, nocl - pp * ocs);   // channels of this pass
+        if (pp > 0) __syncthreads();   // the previous pass's sweep of G is complete
         // "initialize dense buffer with gradients(b, oc)", tile + halo, this oc group:
         // per (oc, halo x-row) the kept outputs of the halo y-range are one contiguous key run
         const int hylo = max(0, y0 - kg.hy), hyhi = min(gy.Y, y0 + t.TY + kg.hy);
@@ -232,16 +300,16 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
             const int ws = wp - kg.hw + hwi, xs = x0 - kg.hx + hxr;
             gbase = ocl * sOC + hwi * sW + hxr * sX + (hylo - (y0 - kg.hy)) * sY + kg.hz;
             if (ws < 0 || ws >= gy.W || xs < 0 || xs >= gy.X || hylo >= hyhi) return -1;
-            return (((b * c_out + oc0 + ocl) * gy.W + ws) * gy.X + xs) * (int64_t)gy.Y + hylo;
+            return (((b * c_out + ocb + ocl) * gy.W + ws) * gy.X + xs) * (int64_t)gy.Y + hylo;
         };
         // the warp's rows r = warp + k * nwarps: lane k loads row k's bounds (one latency for all)
-        for (int r0 = warp; r0 < nocl * HWX; r0 += 32 * nwarps) {
+        for (int r0 = warp; r0 < nocp * HWX; r0 += 32 * nwarps) {
             uint32_t be0 = 0, be1 = 0;
             int gb = 0;
             uint32_t rz = 0;
             {
                 const int r = r0 + lane * nwarps;
-                if (r < nocl * HWX) {
+                if (r < nocp * HWX) {
                     const int64_t row = halo_row(r, gb);
                     if (row >= 0) {
                         be0 = yrow[row];
@@ -306,6 +374,7 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
             __syncwarp();
         }
         __syncthreads();
+        if (pp == 0) {
         if (warp == 0) {   // chunks per ic (32 entries each), exclusive prefix over ic
             int carry = 0;
             for (int ic0 = 0; ic0 < c_in; ic0 += 32) {
@@ -322,7 +391,8 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
             if (lane == 0) cpre[c_in] = carry;
         }
         __syncthreads();
-        const int nchunks = cpre[c_in];
+        nchunks = cpre[c_in];
+        }
         // chunk f -> (ic, entry of this lane) from the shared ranges, and the entry's key and value
         // loads issued; the next chunk's loads are in flight while this chunk's blocks run
         struct Loc { int ic, xi; int64_t e; uint64_t key; float v; };
@@ -369,8 +439,8 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
             st_eb[lane] = eb * (int)sizeof(float);   // byte offsets into G
             st_v[lane] = v;
             __syncwarp();
-            const int n = lbase[ic + 1] - lbase[ic];
-            const int lb = lbase[ic];
+            const int n = lbase[pp * (c_in + 1) + ic + 1] - lbase[pp * (c_in + 1) + ic];
+            const int lb = lbase[pp * (c_in + 1) + ic];
             const char* Gb = reinterpret_cast<const char*>(G);
             float prod[32];
 #pragma unroll
@@ -409,8 +479,11 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
             float dxa = 0.0f;
             if (DX) dxa = reduce_scatter32(prod, lane);   // lane e: sum over this ic's weights
             if (DX && e >= 0) {
-                if (t.n_ocg == 1) dx[e] = dxa;
-                else atomicAdd(&dx[e], dxa);
+                // the same lane owns entry e in every pass (same chunk split): plain
+                // read-modify-write of its own earlier pass, atomics only across CTAs
+                if (t.n_ocg > 1) atomicAdd(&dx[e], dxa);
+                else if (pp == 0) dx[e] = dxa;
+                else dx[e] += dxa;
             }
             __syncwarp();
             cur = nxt;
@@ -425,16 +498,22 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
             for (int i = threadIdx.x; i < (gsize >> 2); i += THREADS) G4[i] = z4;
             for (int i = (gsize & ~3) + threadIdx.x; i < gsize; i += blockDim.x) G[i] = 0.0f;
         }
+        }   // passes
     }
     __syncthreads();
-    if (DW) {
-        for (int ic = 0; ic < c_in; ++ic) {
-            const int t0 = woff[ic * (c_out + 1) + oc0];
-            const int n = lbase[ic + 1] - lbase[ic];
-            for (int j = threadIdx.x; j < n; j += blockDim.x) {
-                const double v = dwp[lbase[ic] + j];
+    if (DW) {   // the same slot order again: slot -> weight
+        for (int q = threadIdx.x; q < c_in * ocp; q += blockDim.x) {
+            const int pp = q / c_in, ic = q - pp * c_in;
+            const int ocb = oc0 + pp * ocs;
+            auto gdel = [&](int t0, int j) {
+                const int2 m = wmeta[t0 + j];
+                return meta_ow(m.x) * sW + off_x(m.y) * sX + off_y(m.y) * sY + off_z(m.y) - (meta_oc(m.x) - ocb) * sOC;
+            };
+            const int lb = lbase[pp * (c_in + 1) + ic], t0 = wo(pp, ic);
+            bwd_weight_slots(ic, t0, wo(pp + 1, ic) - t0, gdel, [&](int j, int slot, int) {
+                const double v = dwp[lb + slot];
                 if (v != 0.0) atomicAdd(&dw_acc[wsrc[t0 + j]], v);
-            }
+            });
         }
     }
 }

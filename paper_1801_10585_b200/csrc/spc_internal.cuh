@@ -336,6 +336,7 @@ cudaError_t launch_conv_fwd_pipeline(const Geo& gx, const Geo& gy, const KGeo& k
 
 struct BwdTile {
     int TX, TY, ocg, ntx, nty, n_ocg, grid;
+    int ocp, ocs;     // passes per item, output channels per pass (ocg = ocp * ocs)
     FastDiv fd_tiles, fd_W, fd_ntx, fd_HWX, fd_HX, fd_TX;   // ntx*nty, W, ntx, HW*HX, HX, TX
     int sY, sX, sW, sOC;   // G slab strides (floats), bank-spread padding
     int threads;      // CTA size (512: one CTA per SM, 256: two)
