@@ -757,7 +757,7 @@ def run_c3(args):
         Y2 = f2(R1, W2, b2)
         g2.f64(R1, W2, Y2, dy2, dR1, ar2.dw64, ar2.db64)
         ar2.start()                               # layer 2's exchange overlaps layer 1's backward
-        dY1 = spc.sparse_scatter_grad(src1, dR1, R1.nnz_bound, Y1.nnz_bound, R1.nnz_dev)
+        dY1 = spc.sparse_scatter_grad(src1, dR1, R1.nnz_bound, Y1.nnz_bound, R1.nnz_dev, sorted=True)
         g1.f64(X, W1, Y1, dY1, None, ar1.dw64, ar1.db64)
         ar1.start()
         ar2.finish(dw2, db2)

@@ -253,6 +253,16 @@ spc_status_t sparse_scatter_grad(const int64_t* src_index, const float* dy, int6
                                  const int64_t* n_out_dev, float* dx, int64_t n_in,
                                  cudaStream_t stream);
 
+/* sparse_scatter_grad_sorted — the same result when src_index[0..n_out) is strictly increasing
+ *   (ReLU and attention_topk emit their sources in key order; max-pool's argmax is not
+ *   ordered): every dx element is written once (dy at a source, 0 on the gaps), no separate
+ *   zero fill, so the call moves exactly its compulsory bytes. Unsorted or out-of-range input
+ *   gives an unspecified dx; under SPC_VALIDATE=1 it returns SPC_ERR_UNSORTED instead
+ *   (synchronising). */
+spc_status_t sparse_scatter_grad_sorted(const int64_t* src_index, const float* dy, int64_t n_out_bound,
+                                        const int64_t* n_out_dev, float* dx, int64_t n_in,
+                                        cudaStream_t stream);
+
 /* ------------------------------------------------------------------------------------
  * sparse_to_dense — the sparseToDense() bridge of the OctNet3 stacks (Appendix B, Table 2,
  *   P:332): dense[key] = value for every stored entry, 0 elsewhere. dense: device float

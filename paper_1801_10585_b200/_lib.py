@@ -28,6 +28,7 @@ EXPORTS = [
     "spc_relu_query", "sparse_relu",
     "spc_maxpool_query", "sparse_maxpool",
     "sparse_scatter_grad",
+    "sparse_scatter_grad_sorted",
     "sparse_to_dense", "sparse_to_dense_bwd",
     "sparse_adagrad_step", "spc_prune_query", "sparse_filter_prune",
     "spc_conv_fwd_query_pass", "sparse_conv_fwd_pass",
@@ -103,6 +104,7 @@ def load(path: str = LIB_PATH):
         "spc_maxpool_query": ([pM, P, pi64, sz], C.c_int),
         "sparse_maxpool": ([pM, P, pO, P, P, C.c_size_t, P], C.c_int),
         "sparse_scatter_grad": ([P, P, I64, P, P, I64, P], C.c_int),
+        "sparse_scatter_grad_sorted": ([P, P, I64, P, P, I64, P], C.c_int),
         "sparse_adagrad_step": ([P, P, P, I64, P, C.c_double, C.POINTER(DensityRegT), C.c_double, C.c_double, P],
                                 C.c_int),
         "spc_prune_query": ([I64, sz], C.c_int),

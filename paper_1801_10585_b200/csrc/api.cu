@@ -758,6 +758,27 @@ spc_status_t sparse_scatter_grad(const int64_t* src_index, const float* dy, int6
     return cu(launch_scatter_grad(src_index, dy, n_out_bound, n_out_dev, dx, n_in, s));
 }
 
+spc_status_t sparse_scatter_grad_sorted(const int64_t* src_index, const float* dy, int64_t n_out_bound,
+                                        const int64_t* n_out_dev, float* dx, int64_t n_in, cudaStream_t s) {
+    if (n_out_bound < 0 || n_in < 0) return SPC_ERR_SHAPE;
+    if (n_out_bound > 0 && (!src_index || !dy)) return SPC_ERR_INVALID_ARG;
+    if (n_in > 0 && !dx) return SPC_ERR_INVALID_ARG;
+    if (n_in == 0) return SPC_OK;
+    if (validate_env() && n_out_bound > 0) {   // strictly increasing and in range; synchronises
+        int* flag = nullptr;
+        SPC_TRY(cu(cudaMallocAsync(reinterpret_cast<void**>(&flag), sizeof(int), s)));
+        int h = 0;
+        cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), s);
+        if (e == cudaSuccess) e = launch_check_sorted(src_index, n_out_bound, n_out_dev, n_in, flag, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s);
+        cudaFreeAsync(flag, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        SPC_TRY(cu(e));
+        if (h) return SPC_ERR_UNSORTED;
+    }
+    return cu(launch_scatter_grad_sorted(src_index, dy, n_out_bound, n_out_dev, dx, n_in, s));
+}
+
 }  // extern "C"
 
 // ------------------------------------------------------------------ training-loop steps (f1)

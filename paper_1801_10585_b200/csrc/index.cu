@@ -401,6 +401,106 @@ cudaError_t launch_scatter_grad(const int64_t* src, const float* dy, int64_t n_o
     return cudaGetLastError();
 }
 
+// The same for a strictly increasing src (ReLU and attention_topk emit their sources in key
+// order): every dx element is written exactly once, no zero fill first. CTA c owns the sources
+// t in [c*T, (c+1)*T) and the dx range [a, b) from just after its predecessor's last index to its
+// own last index (the CTA holding the end sentinel t = n: to n_in). When the range fits shared
+// memory it is assembled there (zeros, then dy at the sources) and streamed out with 16-byte
+// coalesced stores; otherwise thread t writes dy[t] and zeroes the gap after its predecessor
+// (gaps of 64 or more by the whole warp).
+constexpr int kSgItems = 8;
+constexpr int kSgT = 256 * kSgItems;    // sources per CTA
+constexpr int kSgCap = 8192;            // dx elements assembled in shared memory (32 KB)
+
+__global__ void __launch_bounds__(256) scatter_grad_sorted_kernel(const int64_t* __restrict__ src,
+                                                                  const float* __restrict__ dy, int64_t nbound,
+                                                                  const int64_t* n_dev, float* __restrict__ dx,
+                                                                  int64_t n_in) {
+    __shared__ __align__(16) float buf[kSgCap];
+    const int64_t n = load_n(n_dev, nbound);
+    const int64_t t0 = (int64_t)blockIdx.x * kSgT;
+    if (t0 > n) return;
+    const int64_t t1 = min(t0 + (int64_t)kSgT, n);   // sources [t0, t1); the sentinel when t1 == n
+    const bool last = t0 + kSgT >= n;                   // this CTA covers the tail up to n_in
+    auto clampi = [&](int64_t v) { return v < 0 ? (int64_t)0 : (v > n_in ? n_in : v); };
+    const int64_t a = t0 == 0 ? 0 : clampi(src[t0 - 1] + 1);
+    const int64_t b = last ? n_in : clampi(src[t1 - 1] + 1);
+    const int64_t len = b > a ? b - a : 0;
+    if (len <= kSgCap) {
+        float4* b4 = reinterpret_cast<float4*>(buf);
+        for (int i = threadIdx.x; i < (int)((len + 3) >> 2); i += 256) b4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncthreads();
+        for (int64_t t = t0 + threadIdx.x; t < t1; t += 256) {
+            const int64_t i = src[t] - a;
+            if (i >= 0 && i < len) buf[i] = dy[t];
+        }
+        __syncthreads();
+        // stream [a, b) out: scalar head up to 16-byte alignment, float4 body, scalar tail
+        const int64_t head = min(len, (int64_t)((4 - (a & 3)) & 3));
+        if (threadIdx.x < head) dx[a + threadIdx.x] = buf[threadIdx.x];
+        const int64_t nb4 = (len - head) >> 2;
+        for (int64_t q = threadIdx.x; q < nb4; q += 256) {
+            const int64_t o = head + 4 * q;
+            *reinterpret_cast<float4*>(dx + a + o) = make_float4(buf[o], buf[o + 1], buf[o + 2], buf[o + 3]);
+        }
+        for (int64_t r = head + 4 * nb4 + threadIdx.x; r < len; r += 256) dx[a + r] = buf[r];
+        return;
+    }
+    const int lane = threadIdx.x & 31;
+    // warp-uniform trip count (the long-gap path needs every lane); t = n is the tail sentinel
+    const int64_t tend = last ? n + 1 : t1;
+    for (int64_t w0 = t0 + (threadIdx.x & ~31); w0 < tend; w0 += 256) {
+        const int64_t t = w0 + lane;
+        int64_t lo = 0, hi = 0;   // zero [lo, hi)
+        float v = 0.0f;
+        if (t < tend) {
+            lo = t == 0 ? 0 : clampi(src[t - 1] + 1);
+            hi = t < n ? clampi(src[t]) : n_in;
+            if (hi < lo) hi = lo;
+            if (t < n) v = dy[t];
+        }
+        const bool longgap = hi - lo >= 64;
+        if (!longgap)
+            for (int64_t i = lo; i < hi; ++i) dx[i] = 0.0f;
+        unsigned m = __ballot_sync(kFull, longgap);
+        while (m) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
+            const int64_t l = __shfl_sync(kFull, lo, j), h = __shfl_sync(kFull, hi, j);
+            const int64_t al = (l + 3) & ~(int64_t)3, ah = h & ~(int64_t)3;
+            for (int64_t i = l + lane; i < al; i += 32) dx[i] = 0.0f;
+            for (int64_t q = al + 4 * lane; q < ah; q += 128) *reinterpret_cast<float4*>(dx + q) = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int64_t i = ah + lane; i < h; i += 32) dx[i] = 0.0f;
+        }
+        if (t < n && src[t] >= 0 && src[t] < n_in) dx[src[t]] = v;
+    }
+}
+
+__global__ void check_sorted_kernel(const int64_t* __restrict__ src, int64_t nbound, const int64_t* n_dev,
+                                    int64_t n_in, int* flag) {
+    const int64_t n = load_n(n_dev, nbound);
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = src[t];
+        if (i < 0 || i >= n_in || (t > 0 && src[t - 1] >= i)) atomicOr(flag, 1);
+    }
+}
+
+cudaError_t launch_check_sorted(const int64_t* src, int64_t n_out_bound, const int64_t* n_out_dev, int64_t n_in,
+                                int* flag, cudaStream_t s) {
+    if (n_out_bound <= 0) return cudaSuccess;
+    const int64_t grid = std::min<int64_t>((n_out_bound + 255) / 256, num_sms() * 8);
+    { SPC_PHASE("validate", s, 1); check_sorted_kernel<<<(unsigned)grid, 256, 0, s>>>(src, n_out_bound, n_out_dev, n_in, flag); }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_grad_sorted(const int64_t* src, const float* dy, int64_t n_out_bound,
+                                       const int64_t* n_out_dev, float* dx, int64_t n_in, cudaStream_t s) {
+    // one CTA per kSgT sources plus the tail sentinel
+    const int64_t grid = (n_out_bound + 1 + kSgT - 1) / kSgT;
+    { SPC_PHASE("scatter_grad", s, 1); scatter_grad_sorted_kernel<<<(unsigned)grid, 256, 0, s>>>(src, dy, n_out_bound, n_out_dev, dx, n_in); }
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------- sparseToDense bridge
 // Table 2 "sparseToDense()": the key layout ((b*C + c)*V + row_major(p)) (reading R11)
 // is the linear index of the dense [B, C, dims] tensor, so the bridge is a zero fill plus a

@@ -385,6 +385,10 @@ cudaError_t launch_maxpool(const Geo& g, const PoolPlan& p, Keys keys, const flo
                            KeysOut out_keys, float* out_vals, int64_t* out_arg, int64_t* out_nnz, cudaStream_t s);
 cudaError_t launch_scatter_grad(const int64_t* src, const float* dy, int64_t n_out_bound, const int64_t* n_out_dev,
                                 float* dx, int64_t n_in, cudaStream_t s);
+cudaError_t launch_scatter_grad_sorted(const int64_t* src, const float* dy, int64_t n_out_bound,
+                                       const int64_t* n_out_dev, float* dx, int64_t n_in, cudaStream_t s);
+cudaError_t launch_check_sorted(const int64_t* src, int64_t n_out_bound, const int64_t* n_out_dev, int64_t n_in,
+                                int* flag, cudaStream_t s);
 
 // Device-wide exclusive scan of uint32 counts into uint64 offsets; total -> *total (int64,
 // may be NULL). tmp: scan_tmp_words(n) uint64 words.

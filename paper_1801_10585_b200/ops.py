@@ -390,11 +390,13 @@ def sparse_maxpool(x: SparseMap, stride: Sequence[int], stream=None) -> Tuple[Sp
 
 
 def sparse_scatter_grad(src: torch.Tensor, dy: torch.Tensor, n_out_bound: int, n_in: int,
-                        n_out_dev: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-    """Backward of ReLU / pool / top-k (Eq. (5)): dx[src[t]] = dy[t], zeros elsewhere."""
+                        n_out_dev: Optional[torch.Tensor] = None, stream=None, sorted: bool = False) -> torch.Tensor:
+    """Backward of ReLU / pool / top-k (Eq. (5)): dx[src[t]] = dy[t], zeros elsewhere.
+    sorted=True (src strictly increasing: ReLU, top-k) takes sparse_scatter_grad_sorted."""
     dx = torch.empty(max(n_in, 1), dtype=torch.float32, device=dy.device)
-    check("sparse_scatter_grad", load().sparse_scatter_grad(_ptr(src), _ptr(dy), int(n_out_bound), _ptr(n_out_dev),
-                                                            _ptr(dx), int(n_in), _stream(stream)))
+    fn = "sparse_scatter_grad_sorted" if sorted else "sparse_scatter_grad"
+    check(fn, getattr(load(), fn)(_ptr(src), _ptr(dy), int(n_out_bound), _ptr(n_out_dev), _ptr(dx), int(n_in),
+                                  _stream(stream)))
     return dx[:n_in]
 
 

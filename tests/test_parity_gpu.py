@@ -548,6 +548,31 @@ def test_scatter_grad_parity(cuda_lib):
     np.testing.assert_array_equal(host(got), want)
 
 
+@pytest.mark.parametrize("case", ["relu", "topk", "sparse_tail", "empty", "bound"])
+def test_scatter_grad_sorted_parity(cuda_lib, case):
+    """sparse_scatter_grad_sorted (Eq. (5) with key-ordered sources): bit-exact vs the oracle,
+    including long zero gaps (warp-cooperative fill), an empty source list, and a device count
+    below the bound."""
+    spc = cuda_lib
+    x = uniform_map(2, 3, (17, 19), 0.4, 73)
+    if case in ("relu", "bound"):
+        _, _, src = ora.relu(x)
+    elif case == "topk":
+        _, _, src = ora.topk(x, ora.ATTN_MAGNITUDE, 20)
+    elif case == "sparse_tail":
+        src = np.array([3, 5, 300, 301, x.nnz - 200], dtype=np.int64)
+    else:
+        src = np.zeros(0, dtype=np.int64)
+    dy = grad_values(max(src.shape[0], 1), 73)[:src.shape[0]]
+    n_use = src.shape[0] if case != "bound" else src.shape[0] // 2
+    want = ora.scatter_grad(src[:n_use], dy[:n_use], x.nnz)
+    s_dev = torch.from_numpy(np.concatenate([src, np.zeros(1, np.int64)])).cuda()
+    d_dev = torch.from_numpy(np.concatenate([dy, np.zeros(1, np.float32)])).cuda()
+    n_dev = torch.tensor([n_use], dtype=torch.int64, device="cuda") if case == "bound" else None
+    got = spc.sparse_scatter_grad(s_dev, d_dev, src.shape[0], x.nnz, n_out_dev=n_dev, sorted=True)
+    np.testing.assert_array_equal(host(got), want)
+
+
 def test_chain_c2_like_device_nnz(cuda_lib):
     """BASELINE configs[1] shape (smaller batch): 3 x [conv+attention -> ReLU -> maxpool2],
     1->8->16->32, chained on the device with no host sync between layers. Dyadic values on

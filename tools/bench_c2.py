@@ -61,7 +61,7 @@ def main():
         for i in reversed(range(3)):
             xin, y, r, rsrc, p, parg = acts[i]
             dr = spc.sparse_scatter_grad(parg, dp, p.nnz_bound, r.nnz_bound, p.nnz_dev)
-            dyv = spc.sparse_scatter_grad(rsrc, dr, r.nnz_bound, y.nnz_bound, r.nnz_dev)
+            dyv = spc.sparse_scatter_grad(rsrc, dr, r.nnz_bound, y.nnz_bound, r.nnz_dev, sorted=True)
             dx, dw, db = spc.sparse_conv_bwd(xin, Wd[i], y, dyv, need_dx=i > 0)
             grads.append((dw, db))
             dp = dx

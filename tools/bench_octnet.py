@@ -74,7 +74,7 @@ def main():
         for xin, W, y, r, rsrc, p, parg in reversed(tape):
             if p is not None:
                 dcur = spc.sparse_scatter_grad(parg, dcur, p.nnz_bound, r.nnz_bound, p.nnz_dev)
-            dy = spc.sparse_scatter_grad(rsrc, dcur, r.nnz_bound, y.nnz_bound, r.nnz_dev)
+            dy = spc.sparse_scatter_grad(rsrc, dcur, r.nnz_bound, y.nnz_bound, r.nnz_dev, sorted=True)
             dx, dw, db = spc.sparse_conv_bwd(xin, W, y, dy, need_dx=xin is not X)
             dcur = dx
         launches.append(spc.kernel_launches() - n0)

@@ -98,6 +98,8 @@ def main():
     dy = torch.randn(max(nk, 1), device="cuda", generator=g)
     ms, _ = timed(lambda: spc.sparse_scatter_grad(src, dy, nk, n))
     report("sparse_scatter_grad (relu)", ms, 12 * nk + 4 * n, "src+dy read; dx written (zeros included)")
+    ms, _ = timed(lambda: spc.sparse_scatter_grad(src, dy, nk, n, sorted=True))
+    report("sparse_scatter_grad_sorted (relu)", ms, 12 * nk + 4 * n, "src+dy read; dx written once (zeros included)")
     ms, k32 = timed(lambda: spc.keys_narrow(X))
     report("keys_narrow", ms, 12 * n, "8 B read + 4 B written per key")
     ms, _ = timed(lambda: spc.keys_widen(k32, n))

@@ -47,6 +47,8 @@ def main():
         r, src = spc.sparse_relu(Y)
         spc.sparse_scatter_grad(src, torch.ones(max(r.nnz_bound, 1), device="cuda"), r.nnz_bound, Y.nnz_bound,
                                 r.nnz_dev)
+        spc.sparse_scatter_grad(src, torch.ones(max(r.nnz_bound, 1), device="cuda"), r.nnz_bound, Y.nnz_bound,
+                                r.nnz_dev, sorted=True)
         spc.sparse_maxpool(Y, (2,) * len(dims))
         spc.attention_topk(Y, "raw", max(1, k // 3))
     torch.cuda.synchronize()
