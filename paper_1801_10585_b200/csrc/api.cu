@@ -364,15 +364,25 @@ spc_status_t conv_bwd_impl(const spc_map_t* x, const spc_filter_t* w, const spc_
 // -------------------------------------------------------------------- selection ws
 struct TopkWs {
     uint32_t* xrow;
-    uint64_t* seg_off;
+    TopkBufs b;
     int* flag;
 };
 
-TopkWs carve_topk(Carver& c, const Geo& g, int64_t) {
+TopkWs carve_topk(Carver& c, const Geo& g, int64_t nnz) {
     TopkWs ws{};
     const int64_t nseg = g.B * g.C;
+    const size_t tiles = topk_tiles_bound(nnz, nseg);
     ws.xrow = c.take<uint32_t>((size_t)nseg + 1);   // segment bounds only (no row index)
-    ws.seg_off = c.take<uint64_t>((size_t)nseg + 1);
+    ws.b.seg_off = c.take<uint64_t>((size_t)nseg + 1);
+    ws.b.tile_start = c.take<uint32_t>((size_t)nseg + 1);
+    ws.b.hist = c.take<uint32_t>((size_t)nseg * kSelBins);
+    ws.b.seg = reinterpret_cast<TkSeg*>(c.take<uint64_t>((size_t)nseg * (topk_seg_bytes() / 8)));
+    ws.b.cand_cnt = c.take<uint32_t>((size_t)nseg);
+    ws.b.cand = c.take<uint64_t>((size_t)std::max<int64_t>(nnz, 1));
+    ws.b.tile_seg = c.take<uint32_t>(tiles);
+    ws.b.tile_def = c.take<uint32_t>(tiles);
+    ws.b.tile_sel = c.take<uint32_t>(tiles);
+    ws.b.tile_off = c.take<uint64_t>(tiles);
     ws.flag = c.take<int>(1);
     return ws;
 }
@@ -693,7 +703,7 @@ spc_status_t attention_topk(const spc_map_t* x, spc_attn_t attn, int64_t k, spc_
     TopkWs ws = carve_topk(c, g, x->nnz);
     if (validate_env()) SPC_TRY(maybe_validate(x, ws.flag, s));
     SPC_TRY(cu(launch_seg_bounds(kin(x), x->nnz_dev, x->nnz, g.B * g.C, g.V, ws.xrow, s)));
-    return cu(launch_topk(kin(x), x->values, ws.xrow, 1, g.B * g.C, attn, k, ws.seg_off, kout(y), y->values,
+    return cu(launch_topk(kin(x), x->values, ws.xrow, g.B * g.C, x->nnz, attn, k, ws.b, kout(y), y->values,
                           src_index, y->nnz_dev, s));
 }
 

@@ -1,242 +1,428 @@
 // Attention as a standalone layer: per (b, c) segment of a COO map keep the k
 // entries with the largest score (|y| for variant (ii), y for variant (i)); ties go to the
-// smaller key (reading R7). The fused forward has its own pipeline (conv_fwd.cu); this one
-// serves attention_topk.
+// smaller key (reading R7). The fused forward has its own pipeline (conv_fwd.cu, fwd_stream.cu);
+// this one serves attention_topk.
 //
-// One CTA per segment. Exact radix select on the order-preserving u32 score: up to three digit
-// passes (11, 11, 10 bits) find the threshold T and the number `need` of entries with score == T
-// that are kept. The first digit is counted over the segment's values; when its threshold bucket
-// holds at most 8192 entries their scores are gathered into shared memory and the other digits
-// run there (else over the values again, mostly L2 hits). A final pass compacts in key order -- score > T, or == T while fewer than `need` earlier ties were
-// kept -- with coalesced loads and stores (one ballot per 32 entries, warp totals scanned across
-// the block). Output offsets per segment are known before the select: min(n_s, k).
+// Streamed over tiles of kTkTile entries (a tile never spans two segments), so every pass runs
+// on the whole GPU whatever the number and size of the segments:
+//   plan:    per segment its kept count min(n, k) -> output offsets, and its first tile;
+//   hist:    per tile an 11-bit histogram of the top score digit, added to the segment's;
+//   find:    per segment the digit B1 holding the k-th largest score; the whole bucket is kept
+//            when it holds exactly the entries still needed (mode 1), else it is resolved
+//            exactly (mode 2); segments with n <= k keep everything (mode 0);
+//   collect: per tile the entries above B1 are counted, those in B1 (mode 2) appended to the
+//            segment's candidate list as composite keys (score << 32 | ~local index);
+//   select:  per segment the need-th largest candidate (radix select) -> kstar; per tile the
+//            selected candidates are counted and the segment's tiles get their output offsets;
+//   write:   per tile an ordered compaction of the kept entries (keys, values, sources).
+// The values are read three times (hist, collect, write) and the keys once.
 #include "spc_internal.cuh"
 #include "block_scan.cuh"
 
+#include <algorithm>
+
 namespace spc {
 
-#ifndef SPC_TK_THREADS
-#define SPC_TK_THREADS 256
-#endif
-constexpr int kTkThreads = SPC_TK_THREADS;
-constexpr int kTkWarps = kTkThreads / 32;
-constexpr int kTkG = 8;                                 // groups of 32 entries per warp and tile
-constexpr uint32_t kTkTile = (uint32_t)kTkThreads * kTkG;
-constexpr uint32_t kTkCand = 8192;                      // bucket scores kept in shared memory (32 KB)
+constexpr int kTkTile = 4096;                         // entries per tile
+constexpr int kTkThreads = 256;
+constexpr int kTkItems = kTkTile / kTkThreads;        // 16 entries per thread
+constexpr uint32_t kTkSmemCand = 12288;               // candidates selected in shared memory (96 KB, dynamic)
 
-// seg_off[s] = sum over earlier segments of kept(s') with kept = n_s if n_s <= k else k
-__global__ void topk_offsets_kernel(const uint32_t* __restrict__ row_ptr, int64_t R, int64_t nseg, int64_t k,
-                                    uint64_t* __restrict__ seg_off, int64_t* __restrict__ total) {
+struct TkSeg {
+    uint64_t kstar;    // mode 2: keep composite >= kstar within bucket b1
+    uint32_t b1;       // threshold digit (score >> 21)
+    uint32_t mode;     // 0 keep all, 1 keep digit >= b1, 2 keep digit > b1 or composite >= kstar
+    uint32_t need;     // mode 2: entries to take from bucket b1
+    uint32_t pad;
+};
+
+size_t topk_tiles_bound(int64_t nnz, int64_t nseg) { return (size_t)(nnz / kTkTile + nseg + 1); }
+size_t topk_seg_bytes() { return sizeof(TkSeg); }
+
+__device__ __forceinline__ uint64_t tk_comp(uint32_t sc, uint32_t local) {
+    return ((uint64_t)sc << 32) | (uint64_t)(0xffffffffu - local);
+}
+
+// tile -> segment map (one dependent load for a tile kernel instead of a binary search)
+__global__ void topk_tile_map_kernel(const uint32_t* __restrict__ tile_start, int64_t nseg,
+                                     uint32_t* __restrict__ tile_seg) {
+    for (int64_t s = blockIdx.x; s < nseg; s += gridDim.x)
+        for (uint32_t t = tile_start[s] + threadIdx.x; t < tile_start[s + 1]; t += blockDim.x) tile_seg[t] = (uint32_t)s;
+}
+
+// seg_off[s] = sum over earlier segments of min(n_s', k); tile_start[s] = sum of ceil(n_s' / tile)
+__global__ void topk_plan_kernel(const uint32_t* __restrict__ seg_lo, int64_t nseg, int64_t k,
+                                 uint64_t* __restrict__ seg_off, uint32_t* __restrict__ tile_start,
+                                 int64_t* __restrict__ total) {
     __shared__ uint64_t sm[33];
-    uint64_t carry = 0;
+    uint64_t carry = 0, tcarry = 0;
     for (int64_t base = 0; base < nseg; base += blockDim.x) {
         const int64_t s = base + threadIdx.x;
-        uint64_t v = 0;
+        uint64_t v = 0, nt = 0;
         if (s < nseg) {
-            const uint64_t n = (uint64_t)(row_ptr[(s + 1) * R] - row_ptr[s * R]);
+            const uint64_t n = (uint64_t)(seg_lo[s + 1] - seg_lo[s]);
             v = n <= (uint64_t)k ? n : (uint64_t)k;
+            nt = (n + kTkTile - 1) / kTkTile;
         }
         uint64_t t;
-        const uint64_t ex = block_excl_scan(v, sm, &t);
-        if (s < nseg) seg_off[s] = carry + ex;
-        carry += t;
+        const uint64_t packed = (v << 24) | nt;   // (kept < 2^32 per call, tiles < 2^24)
+        const uint64_t ex = block_excl_scan(packed, sm, &t);
+        if (s < nseg) {
+            seg_off[s] = carry + (ex >> 24);
+            tile_start[s] = (uint32_t)(tcarry + (ex & 0xffffffull));
+        }
+        carry += t >> 24;
+        tcarry += t & 0xffffffull;
+        __syncthreads();
     }
-    if (threadIdx.x == 0) *total = (int64_t)carry;
+    if (threadIdx.x == 0) {
+        *total = (int64_t)carry;
+        tile_start[nseg] = (uint32_t)tcarry;
+    }
 }
 
-__global__ void __launch_bounds__(kTkThreads, 1024 / kTkThreads)
-topk_seg_kernel(Keys keys, const float* __restrict__ vals, const uint32_t* __restrict__ row_ptr,
-                int64_t R, int attn, int64_t k, const uint64_t* __restrict__ seg_off, KeysOut ok,
-                float* __restrict__ ov, int64_t* __restrict__ osrc) {
+struct TkTile {
+    int64_t s;
+    uint32_t lo, hi;   // entries [lo, hi) of the tile
+    uint32_t seg0;     // first entry of the segment
+    bool ok;
+};
+__device__ __forceinline__ TkTile tk_tile(const uint32_t* seg_lo, const uint32_t* tile_start, const uint32_t* tile_seg,
+                                          int64_t nseg, uint32_t t) {
+    TkTile r{};
+    r.ok = t < __ldg(&tile_start[nseg]);
+    if (!r.ok) return r;
+    r.s = __ldg(&tile_seg[t]);
+    r.seg0 = __ldg(&seg_lo[r.s]);
+    r.lo = r.seg0 + (t - __ldg(&tile_start[r.s])) * (uint32_t)kTkTile;
+    r.hi = min(r.lo + (uint32_t)kTkTile, __ldg(&seg_lo[r.s + 1]));
+    return r;
+}
+
+__global__ void __launch_bounds__(kTkThreads) topk_hist_kernel(const float* __restrict__ vals,
+                                                               const uint32_t* __restrict__ seg_lo,
+                                                               const uint32_t* __restrict__ tile_start,
+                                                               const uint32_t* __restrict__ tile_seg, int64_t nseg,
+                                                               int attn, int64_t k, uint32_t* __restrict__ hist) {
     __shared__ uint32_t h[kSelBins];
+    const TkTile tl = tk_tile(seg_lo, tile_start, tile_seg, nseg, blockIdx.x);
+    if (!tl.ok) return;
+    if ((int64_t)(__ldg(&seg_lo[tl.s + 1]) - tl.seg0) <= k) return;   // keep-all segment
+    for (int i = threadIdx.x; i < kSelBins; i += kTkThreads) h[i] = 0u;
+    uint32_t b[kTkItems];
+#pragma unroll
+    for (int u = 0; u < kTkItems; ++u) {
+        const uint32_t i = tl.lo + (uint32_t)(u * kTkThreads) + threadIdx.x;
+        b[u] = i < tl.hi ? __float_as_uint(__ldg(&vals[i])) : 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kTkItems; ++u) {
+        const uint32_t i = tl.lo + (uint32_t)(u * kTkThreads) + threadIdx.x;
+        if (i < tl.hi) atomicAdd(&h[score_bits(b[u], attn) >> 21], 1u);
+    }
+    __syncthreads();
+    uint32_t* gh = hist + tl.s * kSelBins;
+    for (int i = threadIdx.x; i < kSelBins; i += kTkThreads)
+        if (h[i]) atomicAdd(&gh[i], h[i]);
+}
+
+__global__ void topk_find_kernel(const uint32_t* __restrict__ seg_lo, int64_t k, const uint32_t* __restrict__ hist,
+                                 TkSeg* __restrict__ seg, uint32_t* __restrict__ cand_cnt) {
     __shared__ uint32_t sm[33];
-    __shared__ uint32_t wt[kTkWarps + 1], wk[kTkWarps + 1];
-    __shared__ uint32_t sh_bin, sh_need, sh_cnt;
-    __shared__ uint32_t cand[kTkCand];   // scores of the threshold bucket after the first digit
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t s = blockIdx.x;
-    const uint32_t lo = row_ptr[s * R], hi = row_ptr[(s + 1) * R];
-    const bool keep_all = (uint64_t)(hi - lo) <= (uint64_t)k;
-    uint32_t T = 0, pmask = 0, need = 0;
-    // one radix-select step over a histogram h of nb bins: the bin holding the need-th largest
-    auto find_bin = [&](uint32_t nb) {
-        const int per = (int)nb / kTkThreads;   // bins nb-1-per*t .. nb-per*(t+1) for thread t
+    const uint64_t n = (uint64_t)(seg_lo[s + 1] - seg_lo[s]);
+    if (n <= (uint64_t)k) {
+        if (threadIdx.x == 0) {
+            TkSeg st{};
+            st.mode = 0;
+            seg[s] = st;
+            cand_cnt[s] = 0;
+        }
+        return;
+    }
+    const uint32_t* h = hist + s * kSelBins;
+    constexpr int per = kSelBins / 256;   // blockDim 256: bins from the top, per thread a stripe
+    uint32_t own = 0;
+    for (int q = 0; q < per; ++q) own += h[kSelBins - 1 - threadIdx.x * per - q];
+    uint32_t tot;
+    const uint32_t before = block_excl_scan(own, sm, &tot);
+    if (before < (uint32_t)k && before + own >= (uint32_t)k) {
+        uint32_t cum = before;
+        for (int q = 0; q < per; ++q) {
+            const int bin = kSelBins - 1 - threadIdx.x * per - q;
+            if (cum + h[bin] >= (uint32_t)k) {
+                TkSeg st{};
+                st.b1 = (uint32_t)bin;
+                st.need = (uint32_t)k - cum;
+                st.mode = st.need == h[bin] ? 1u : 2u;
+                seg[s] = st;
+                cand_cnt[s] = 0;
+                break;
+            }
+            cum += h[bin];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kTkThreads) topk_collect_kernel(const float* __restrict__ vals,
+                                                                  const uint32_t* __restrict__ seg_lo,
+                                                                  const uint32_t* __restrict__ tile_start,
+                                                                  const uint32_t* __restrict__ tile_seg,
+                                                                  int64_t nseg, int attn, const TkSeg* __restrict__ seg,
+                                                                  uint64_t* __restrict__ cand,
+                                                                  uint32_t* __restrict__ cand_cnt,
+                                                                  uint32_t* __restrict__ tile_def) {
+    __shared__ uint32_t sm[33];
+    const TkTile tl = tk_tile(seg_lo, tile_start, tile_seg, nseg, blockIdx.x);
+    if (!tl.ok) return;
+    const TkSeg st = seg[tl.s];
+    if (st.mode == 0) {
+        if (threadIdx.x == 0) tile_def[blockIdx.x] = tl.hi - tl.lo;
+        return;
+    }
+    uint32_t b[kTkItems];
+#pragma unroll
+    for (int u = 0; u < kTkItems; ++u) {
+        const uint32_t i = tl.lo + (uint32_t)(u * kTkThreads) + threadIdx.x;
+        b[u] = i < tl.hi ? __float_as_uint(__ldg(&vals[i])) : 0u;
+    }
+    // count first, one atomic per tile for the tile's slots in the segment's candidate list
+    // (the list is unordered: the select does not care), then write
+    uint32_t def = 0, nc = 0, cm = 0;
+#pragma unroll
+    for (int u = 0; u < kTkItems; ++u) {
+        const uint32_t i = tl.lo + (uint32_t)(u * kTkThreads) + threadIdx.x;
+        const bool in = i < tl.hi;
+        const uint32_t d = score_bits(b[u], attn) >> 21;
+        def += (in && (d > st.b1 || (st.mode == 1u && d == st.b1))) ? 1u : 0u;
+        const bool c = in && st.mode == 2u && d == st.b1;
+        cm |= (c ? 1u : 0u) << u;
+        nc += c ? 1u : 0u;
+    }
+    __shared__ uint32_t sh_base;
+    uint32_t ctot;
+    const uint32_t cex = block_excl_scan(nc, sm, &ctot);
+    if (threadIdx.x == 0 && ctot) sh_base = atomicAdd(&cand_cnt[tl.s], ctot);
+    __syncthreads();
+    if (cm) {
+        uint64_t* cs = cand + tl.seg0 + sh_base + cex;   // the segment's candidates (at most its size)
+#pragma unroll
+        for (int u = 0; u < kTkItems; ++u)
+            if ((cm >> u) & 1u) {
+                const uint32_t i = tl.lo + (uint32_t)(u * kTkThreads) + threadIdx.x;
+                *cs++ = tk_comp(score_bits(b[u], attn), i - tl.seg0);
+            }
+    }
+    def = block_sum(def, sm);
+    if (threadIdx.x == 0) tile_def[blockIdx.x] = def;
+}
+
+// one radix-select step: the bin of h[0..256) holding the need-th largest (whole block calls;
+// sh[0] = bin, sh[1] = need within it, sh[2] = its count)
+__device__ __forceinline__ void tk_find_bin256(const uint32_t* h, uint32_t need, uint32_t* sh) {
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
         uint32_t own = 0;
-        for (int q = 0; q < per; ++q) own += h[nb - 1 - per * tid - q];
-        uint32_t tot;
-        const uint32_t before = block_excl_scan(own, sm, &tot);
-        if (before < need && before + own >= need) {
+        for (int q = 0; q < 8; ++q) own += h[255 - 8 * lane - q];
+        const uint32_t incl = warp_incl_scan(own);
+        const uint32_t before = incl - own;
+        if (own && before < need && before + own >= need) {
             uint32_t cum = before;
-            for (int q = 0; q < per; ++q) {
-                const uint32_t bin = nb - 1 - per * tid - q, hb = h[bin];
-                if (cum + hb >= need) {
-                    sh_bin = bin;
-                    sh_need = need - cum;
-                    sh_cnt = hb;
+            for (int q = 0; q < 8; ++q) {
+                const int bin = 255 - 8 * lane - q;
+                if (cum + h[bin] >= need) {
+                    sh[0] = (uint32_t)bin;
+                    sh[1] = need - cum;
+                    sh[2] = h[bin];
                     break;
                 }
-                cum += hb;
-            }
-        }
-        __syncthreads();
-    };
-    if (!keep_all) {
-        need = (uint32_t)k;
-        bool in_smem = false;
-        uint32_t ncand = 0;
-#pragma unroll 1
-        for (int pass = 0; pass < 3; ++pass) {
-            const int sh = pass == 0 ? 21 : (pass == 1 ? 10 : 0);
-            const uint32_t nb = pass == 2 ? 1024u : 2048u;
-            for (int i = tid; i < kSelBins; i += kTkThreads) h[i] = 0u;
-            __syncthreads();
-            if (in_smem) {   // the candidates of the threshold bucket (pass >= 1)
-                for (uint32_t i = tid; i < ncand; i += kTkThreads) {
-                    const uint32_t sc = cand[i];
-                    if ((sc & pmask) == T) atomicAdd(&h[(sc >> sh) & (nb - 1u)], 1u);
-                }
-            } else {         // the segment's values in global memory
-                for (uint32_t i0 = lo + tid; i0 < hi; i0 += 8u * kTkThreads) {
-                    uint32_t b[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const uint32_t i = i0 + (uint32_t)u * kTkThreads;
-                        b[u] = i < hi ? __float_as_uint(vals[i]) : 0u;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const uint32_t sc = score_bits(b[u], attn);
-                        if (i0 + (uint32_t)u * kTkThreads < hi && (sc & pmask) == T)
-                            atomicAdd(&h[(sc >> sh) & (nb - 1u)], 1u);
-                    }
-                }
-            }
-            __syncthreads();
-            find_bin(nb);
-            T |= sh_bin << sh;
-            pmask |= (nb - 1u) << sh;
-            need = sh_need;
-            const uint32_t bcnt = sh_cnt;
-            if (bcnt == need) break;   // the whole bucket is kept: no tie split below it
-            if (pass == 0 && bcnt <= kTkCand) {
-                // gather the bucket's scores into shared memory; the later digits run there
-                __syncthreads();   // every thread has read sh_cnt before it is reused as the cursor
-                if (tid == 0) sh_cnt = 0;
-                __syncthreads();
-                // warp-uniform trip count (the ballots below need every lane)
-                for (uint32_t w0 = lo + (uint32_t)(tid - lane); w0 < hi; w0 += 8u * kTkThreads) {
-                    const uint32_t i0 = w0 + (uint32_t)lane;
-                    uint32_t b[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const uint32_t i = i0 + (uint32_t)u * kTkThreads;
-                        b[u] = i < hi ? __float_as_uint(vals[i]) : 0u;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const uint32_t sc = score_bits(b[u], attn);
-                        const bool c = i0 + (uint32_t)u * kTkThreads < hi && (sc & pmask) == T;
-                        const unsigned mk = __ballot_sync(kFull, c);
-                        uint32_t slot = 0;
-                        if (lane == 0 && mk) slot = atomicAdd(&sh_cnt, (uint32_t)__popc(mk));
-                        slot = __shfl_sync(kFull, slot, 0);
-                        if (c) cand[slot + __popc(mk & ((1u << lane) - 1u))] = sc;
-                    }
-                }
-                __syncthreads();
-                ncand = sh_cnt;
-                in_smem = true;
+                cum += h[bin];
             }
         }
     }
-    // ordered compaction
-    const uint64_t obase = seg_off[s];
-    uint32_t tie_carry = 0;
-    uint64_t out_carry = 0;
-    const unsigned lt = (1u << lane) - 1u;
-#pragma unroll 1
-    for (uint32_t t0 = lo; t0 < hi; t0 += kTkTile) {
-        const uint32_t w0 = t0 + (uint32_t)warp * (32u * kTkG);
-        uint32_t bits[kTkG];
-        unsigned kb[kTkG], tb[kTkG];
-        uint32_t ntie = 0;
-        // values and keys together (one round trip; the keys' sectors are fetched anyway at
-        // these kept fractions)
-        uint64_t kk[kTkG];
-#pragma unroll
-        for (int g = 0; g < kTkG; ++g) {
-            const uint32_t i = w0 + 32u * g + lane;
-            bits[g] = i < hi ? __float_as_uint(vals[i]) : 0u;
-            kk[g] = i < hi ? keys[i] : 0ull;
-        }
-#pragma unroll
-        for (int g = 0; g < kTkG; ++g) {
-            const uint32_t i = w0 + 32u * g + lane;
-            const bool in = i < hi;
-            const uint32_t sc = score_bits(bits[g], attn) & pmask;
-            const bool keep = in && (keep_all || sc > T), tie = in && !keep_all && sc == T;
-            kb[g] = __ballot_sync(kFull, keep);
-            tb[g] = __ballot_sync(kFull, tie);
-            ntie += (uint32_t)__popc(tb[g]);
-        }
-        if (!keep_all) {   // block-uniform: rank the ties in key order, keep the first `need`
-            if (lane == 0) wt[warp] = ntie;
-            __syncthreads();
-            if (warp == 0) {
-                const uint32_t v = lane < kTkWarps ? wt[lane] : 0u;
-                const uint32_t inc = warp_incl_scan(v);
-                if (lane < kTkWarps) wt[lane] = inc - v;
-                if (lane == 31) wt[kTkWarps] = inc;
-            }
-            __syncthreads();
-            uint32_t r = tie_carry + wt[warp];
-#pragma unroll
-            for (int g = 0; g < kTkG; ++g) {
-                const bool tie = (tb[g] >> lane) & 1u;
-                const bool take = tie && r + (uint32_t)__popc(tb[g] & lt) < need;
-                kb[g] |= __ballot_sync(kFull, take);
-                r += (uint32_t)__popc(tb[g]);
-            }
-            tie_carry += wt[kTkWarps];
-        }
-        uint32_t nk = 0;
-#pragma unroll
-        for (int g = 0; g < kTkG; ++g) nk += (uint32_t)__popc(kb[g]);
-        if (lane == 0) wk[warp] = nk;
+    __syncthreads();
+}
+
+// need-th largest (1-based) of n distinct u64 keys at p (shared or global memory) that agree on
+// every bit from `top` up (the candidates of one score bucket share its 11 top bits): digits of
+// up to 8 bits from bit top - 1 down; stops as soon as one key is left with the prefix
+__device__ uint64_t tk_select(const uint64_t* p, uint32_t n, uint32_t need, int top, uint32_t* h, uint32_t* sh,
+                              uint64_t* shk) {
+    const uint64_t fixed = top >= 64 ? 0ull : ~0ull << top;
+    uint64_t prefix = n ? (p[0] & fixed) : 0ull, mask = fixed;
+    for (int hi = top; hi > 0;) {
+        const int wd = hi < 8 ? hi : 8, shf = hi - wd;
+        hi = shf;
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
         __syncthreads();
-        if (warp == 0) {
-            const uint32_t v = lane < kTkWarps ? wk[lane] : 0u;
-            const uint32_t inc = warp_incl_scan(v);
-            if (lane < kTkWarps) wk[lane] = inc - v;
-            if (lane == 31) wk[kTkWarps] = inc;
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+            const uint64_t kk = p[i];
+            if ((kk & mask) == prefix) atomicAdd(&h[(uint32_t)(kk >> shf) & ((1u << wd) - 1u)], 1u);
         }
         __syncthreads();
-        uint64_t pos = obase + out_carry + wk[warp];
-#pragma unroll
-        for (int g = 0; g < kTkG; ++g) {
-            if ((kb[g] >> lane) & 1u) {
-                const uint32_t i = w0 + 32u * g + lane;
-                const uint64_t o = pos + (uint32_t)__popc(kb[g] & lt);
-                ok.put(o, kk[g]);
-                ov[o] = __uint_as_float(bits[g]);
-                if (osrc) osrc[o] = (int64_t)i;
-            }
-            pos += (uint32_t)__popc(kb[g]);
+        tk_find_bin256(h, need, sh);
+        prefix |= (uint64_t)sh[0] << shf;
+        need = sh[1];
+        mask |= (uint64_t)((1u << wd) - 1u) << shf;
+        const bool single = sh[2] == 1u;
+        __syncthreads();
+        if (single) {
+            for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
+                if ((p[i] & mask) == prefix) *shk = p[i];
+            __syncthreads();
+            return *shk;
         }
-        out_carry += wk[kTkWarps];
-        __syncthreads();   // wt / wk are rewritten by the next tile
+    }
+    return prefix;
+}
+
+// per segment: kstar (mode 2), the selected candidates per tile, then the exclusive output
+// offsets of the segment's tiles
+constexpr int kTkSelThreads = 512;
+__global__ void __launch_bounds__(kTkSelThreads) topk_select_kernel(const uint32_t* __restrict__ seg_lo,
+                                                                    const uint32_t* __restrict__ tile_start,
+                                                                    const uint64_t* __restrict__ seg_off,
+                                                                    TkSeg* __restrict__ seg,
+                                                                    const uint64_t* __restrict__ cand,
+                                                                    const uint32_t* __restrict__ cand_cnt,
+                                                                    const uint32_t* __restrict__ tile_def,
+                                                                    uint32_t* __restrict__ tile_sel,
+                                                                    uint64_t* __restrict__ tile_off) {
+    extern __shared__ __align__(16) uint64_t keys[];   // [kTkSmemCand]
+    __shared__ uint32_t h[256];
+    __shared__ uint32_t sh[4];
+    __shared__ uint64_t shk;
+    __shared__ uint64_t sm[33];
+    const int64_t s = blockIdx.x;
+    TkSeg st = seg[s];
+    const uint32_t t0 = tile_start[s], t1 = tile_start[s + 1];
+    const uint32_t seg0 = seg_lo[s];
+    if (st.mode == 2u) {
+        const uint32_t n = cand_cnt[s];
+        const uint64_t* cs = cand + seg0;
+        uint64_t kst;
+        if (n <= kTkSmemCand) {
+            for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) keys[i] = cs[i];
+            __syncthreads();
+            kst = tk_select(keys, n, st.need, 53, h, sh, &shk);   // (score >> 21 == b1: bits 53.. fixed)
+        } else {
+            kst = tk_select(cs, n, st.need, 53, h, sh, &shk);   // (massive ties: the candidates stay in HBM)
+        }
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+            const uint64_t c = n <= kTkSmemCand ? keys[i] : cs[i];
+            if (c >= kst) atomicAdd(&tile_sel[t0 + (0xffffffffu - (uint32_t)c) / (uint32_t)kTkTile], 1u);
+        }
+        if (threadIdx.x == 0) {
+            st.kstar = kst;
+            seg[s] = st;
+        }
+        __syncthreads();
+    }
+    uint64_t carry = seg_off[s];
+    for (uint32_t base = t0; base < t1; base += blockDim.x) {
+        const uint32_t t = base + threadIdx.x;
+        uint64_t v = 0;
+        if (t < t1) v = (uint64_t)tile_def[t] + (st.mode == 2u ? tile_sel[t] : 0u);
+        uint64_t tot;
+        const uint64_t ex = block_excl_scan(v, sm, &tot);
+        if (t < t1) tile_off[t] = carry + ex;
+        carry += tot;
+        __syncthreads();
     }
 }
 
-cudaError_t launch_topk(Keys keys, const float* vals, const uint32_t* row_ptr, int64_t R, int64_t nseg,
-                        int attn, int64_t k, uint64_t* seg_off, KeysOut out_keys, float* out_vals, int64_t* out_src,
-                        int64_t* out_nnz, cudaStream_t s) {
+// ordered compaction of one tile: 512 threads, warp w owns entries w*256 .. w*256+255 of the
+// tile (8 groups of 32, coalesced), one ballot per group, warp totals scanned across the block
+constexpr int kTkWThreads = 512;
+constexpr int kTkWItems = kTkTile / kTkWThreads;   // 8
+__global__ void __launch_bounds__(kTkWThreads, 2) topk_write_kernel(Keys keys, const float* __restrict__ vals,
+                                                                    const uint32_t* __restrict__ seg_lo,
+                                                                    const uint32_t* __restrict__ tile_start,
+                                                                    const uint32_t* __restrict__ tile_seg, int64_t nseg,
+                                                                    int attn, const TkSeg* __restrict__ seg,
+                                                                    const uint64_t* __restrict__ tile_off, KeysOut ok,
+                                                                    float* __restrict__ ov, int64_t* __restrict__ osrc) {
+    __shared__ uint32_t wc[kTkWThreads / 32];
+    const TkTile tl = tk_tile(seg_lo, tile_start, tile_seg, nseg, blockIdx.x);
+    if (!tl.ok) return;
+    const TkSeg st = seg[tl.s];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t w0 = tl.lo + (uint32_t)warp * (32u * kTkWItems);
+    const uint64_t pos0 = tile_off[blockIdx.x];
+    uint32_t b[kTkWItems];
+    uint64_t kk[kTkWItems];
+#pragma unroll
+    for (int u = 0; u < kTkWItems; ++u) {
+        const uint32_t i = w0 + 32u * u + lane;
+        b[u] = i < tl.hi ? __float_as_uint(__ldg(&vals[i])) : 0u;
+        kk[u] = i < tl.hi ? keys[i] : 0ull;
+    }
+    unsigned m[kTkWItems];
+    uint32_t c = 0;
+#pragma unroll
+    for (int u = 0; u < kTkWItems; ++u) {
+        const uint32_t i = w0 + 32u * u + lane;
+        const uint32_t sc = score_bits(b[u], attn);
+        const uint32_t d = sc >> 21;
+        const bool keep = i < tl.hi && (st.mode == 0u || d > st.b1 || (d == st.b1 && (st.mode == 1u ||
+                                                                                     tk_comp(sc, i - tl.seg0) >= st.kstar)));
+        m[u] = __ballot_sync(kFull, keep);
+        c += (uint32_t)__popc(m[u]);
+    }
+    if (lane == 0) wc[warp] = c;
+    __syncthreads();
+    uint64_t pos = pos0;
+    for (int q = 0; q < warp; ++q) pos += wc[q];
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int u = 0; u < kTkWItems; ++u) {
+        if ((m[u] >> lane) & 1u) {
+            const uint32_t i = w0 + 32u * u + lane;
+            const uint64_t o = pos + (uint32_t)__popc(m[u] & lt);
+            ok.put(o, kk[u]);
+            ov[o] = __uint_as_float(b[u]);
+            if (osrc) osrc[o] = (int64_t)i;
+        }
+        pos += (uint32_t)__popc(m[u]);
+    }
+}
+
+cudaError_t launch_topk(Keys keys, const float* vals, const uint32_t* seg_lo, int64_t nseg, int64_t nnz_bound,
+                        int attn, int64_t k, const TopkBufs& w, KeysOut out_keys, float* out_vals,
+                        int64_t* out_src, int64_t* out_nnz, cudaStream_t s) {
     if (nseg == 0) return cudaMemsetAsync(out_nnz, 0, sizeof(int64_t), s);
-    { SPC_PHASE("topk_offsets", s, 1); topk_offsets_kernel<<<1, 1024, 0, s>>>(row_ptr, R, nseg, k, seg_off, out_nnz); }
+    const unsigned tiles = (unsigned)topk_tiles_bound(nnz_bound, nseg);
+    cudaError_t e = cudaMemsetAsync(w.hist, 0, sizeof(uint32_t) * kSelBins * (size_t)nseg, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(w.tile_sel, 0, sizeof(uint32_t) * (size_t)tiles, s);
+    if (e != cudaSuccess) return e;
+    { SPC_PHASE("topk_plan", s, 1); topk_plan_kernel<<<1, 1024, 0, s>>>(seg_lo, nseg, k, w.seg_off, w.tile_start, out_nnz); }
+    {
+        SPC_PHASE("topk_plan", s, 1);
+        topk_tile_map_kernel<<<(unsigned)std::min<int64_t>(nseg, 4096), 128, 0, s>>>(w.tile_start, nseg, w.tile_seg);
+    }
+    {
+        SPC_PHASE("topk_hist", s, 1);
+        topk_hist_kernel<<<tiles, kTkThreads, 0, s>>>(vals, seg_lo, w.tile_start, w.tile_seg, nseg, attn, k, w.hist);
+    }
+    { SPC_PHASE("topk_find", s, 1); topk_find_kernel<<<(unsigned)nseg, 256, 0, s>>>(seg_lo, k, w.hist, w.seg, w.cand_cnt); }
+    {
+        SPC_PHASE("topk_collect", s, 1);
+        topk_collect_kernel<<<tiles, kTkThreads, 0, s>>>(vals, seg_lo, w.tile_start, w.tile_seg, nseg, attn, w.seg, w.cand,
+                                                         w.cand_cnt, w.tile_def);
+    }
     {
         SPC_PHASE("topk_select", s, 1);
-        topk_seg_kernel<<<(unsigned)nseg, kTkThreads, 0, s>>>(keys, vals, row_ptr, R, attn, k, seg_off, out_keys,
-                                                              out_vals, out_src);
+        const size_t smem = kTkSmemCand * sizeof(uint64_t);
+        cudaError_t ea = cudaFuncSetAttribute(topk_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (ea != cudaSuccess) return ea;
+        topk_select_kernel<<<(unsigned)nseg, kTkSelThreads, smem, s>>>(seg_lo, w.tile_start, w.seg_off, w.seg, w.cand,
+                                                                   w.cand_cnt, w.tile_def, w.tile_sel, w.tile_off);
+    }
+    {
+        SPC_PHASE("topk_write", s, 1);
+        topk_write_kernel<<<tiles, kTkWThreads, 0, s>>>(keys, vals, seg_lo, w.tile_start, w.tile_seg, nseg, attn, w.seg,
+                                                       w.tile_off, out_keys, out_vals, out_src);
     }
     return cudaGetLastError();
 }

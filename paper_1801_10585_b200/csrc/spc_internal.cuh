@@ -358,9 +358,25 @@ cudaError_t launch_f64_to_f32_2(const double* a, float* b, int64_t n, const doub
 constexpr int kSelBins = 2048;    // 11-bit score digits
 // Standalone attention over a COO map (select.cu): segment s = entries row_ptr[s*R] ..
 // row_ptr[(s+1)*R]; workspace seg_off [nseg].
-cudaError_t launch_topk(Keys keys, const float* vals, const uint32_t* row_ptr, int64_t R, int64_t nseg,
-                        int attn, int64_t k, uint64_t* seg_off, KeysOut out_keys, float* out_vals, int64_t* out_src,
-                        int64_t* out_nnz, cudaStream_t s);
+struct TkSeg;
+// workspace of the streamed top-k (select.cu); tiles = topk_tiles_bound(nnz, nseg)
+struct TopkBufs {
+    uint64_t* seg_off;      // [nseg + 1] output offset of each segment
+    uint32_t* tile_start;   // [nseg + 1] first tile of each segment
+    uint32_t* hist;         // [nseg * kSelBins]
+    TkSeg* seg;             // [nseg]
+    uint32_t* cand_cnt;     // [nseg]
+    uint64_t* cand;         // [nnz] candidate composites (segment s at its entry offset)
+    uint32_t* tile_seg;     // [tiles] segment of each tile
+    uint32_t* tile_def;     // [tiles]
+    uint32_t* tile_sel;     // [tiles]
+    uint64_t* tile_off;     // [tiles]
+};
+size_t topk_tiles_bound(int64_t nnz, int64_t nseg);
+size_t topk_seg_bytes();
+cudaError_t launch_topk(Keys keys, const float* vals, const uint32_t* seg_lo, int64_t nseg, int64_t nnz_bound,
+                        int attn, int64_t k, const TopkBufs& w, KeysOut out_keys, float* out_vals,
+                        int64_t* out_src, int64_t* out_nnz, cudaStream_t s);
 
 // --------------------------------------------------------------------- relu / pool / misc
 cudaError_t launch_relu(Keys keys, const float* vals, const int64_t* nnz_dev, int64_t nbound,

@@ -95,6 +95,11 @@ def main():
     nt = t.nnz()
     report(f"attention_topk k={kk}", ms, 12 * n + 20 * nt, "keys+values read; kept keys+values+src written",
            lambda: spc.attention_topk(X, "magnitude", kk))
+    n1 = int(torch.searchsorted(keys, torch.tensor([C * V], device="cuda")).item())   # sample 0 only
+    one = spc.SparseMap(keys[:n1], vals[:n1], 1, C, (R, R, R), n1, None)
+    ms, (t1, _) = timed(lambda: spc.attention_topk(one, "magnitude", kk))
+    report(f"attention_topk k={kk}, 1 sample (8 segments)", ms, 12 * n1 + 20 * t1.nnz(),
+           "keys+values read; kept keys+values+src written", lambda: spc.attention_topk(one, "magnitude", kk))
     dy = torch.randn(max(nk, 1), device="cuda", generator=g)
     ms, _ = timed(lambda: spc.sparse_scatter_grad(src, dy, nk, n))
     report("sparse_scatter_grad (relu)", ms, 12 * nk + 4 * n, "src+dy read; dx written (zeros included)")
