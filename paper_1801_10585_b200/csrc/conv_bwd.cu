@@ -54,21 +54,13 @@ static size_t bwd_smem(const KGeo& kg, int c_in, int TX, int TY, int Z, int ocs,
     return g + w + idx + stage + 256;
 }
 
-BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int nw_total) {
+static BwdTile plan_bwd_tile_ocp(const Geo& gx, const KGeo& kg, int c_out, int nw_total, int ocp_req) {
     BwdTile t{};
     const int c_in = (int)gx.C;
     const int cps = bwd_ctas_per_sm();
     const int threads = cps == 2 ? 256 : 512;
     const size_t budget = cps == 2 ? 110 * 1024 : 200 * 1024;
     int ocg = std::min(c_out, cps == 2 ? 4 : 8);
-    // passes per item (SPC_BWD_OCP): the G slab holds ocg / ocp channels, so the tile can be larger
-    // (less halo re-read per interior voxel, more entry chunks per item to spread over the warps)
-    // at the cost of ocp fills / sweeps per item
-    // Measured: C4 (c_in = 8) 3.12 / 3.69 ms for 1 / 2 passes, the C3 chain (32 -> 64 layer)
-    // 20.3 / 18.3 ms per step: wide inputs have enough entries per chunk row to pay for the
-    // second pass.
-    int ocp_req = c_in >= 16 ? 2 : 1;
-    if (const char* v = getenv("SPC_BWD_OCP")) ocp_req = std::max(1, atoi(v));
     for (; ocg >= 1; ocg = ocg > 1 ? (ocg + 1) / 2 : 0) {
         int ocp = std::min(ocp_req, ocg);
         while (ocg % ocp) --ocp;
@@ -125,6 +117,20 @@ BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int nw_total) {
     return t;
 }
 
+// Passes per item (SPC_BWD_OCP overrides): with ocp passes the G slab holds ocg / ocp channels,
+// so the tile can be larger (less halo re-read per interior voxel, more entry chunks per item to
+// spread over the warps) at the cost of ocp fills / sweeps per item. Two passes are taken for
+// wide inputs (>= 16 channels) when they buy at least 1.5x the tile area. Measured: C4 (8 input
+// channels) 3.12 / 3.69 ms with 1 / 2 passes; the C3 chain (32 -> 64 layer) 20.3 / 18.3 ms per
+// step; C2 (16 -> 32 on 7 x 7 planes: the tile is the whole plane either way) 0.70 / 0.74 ms.
+BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int nw_total) {
+    if (const char* v = getenv("SPC_BWD_OCP")) return plan_bwd_tile_ocp(gx, kg, c_out, nw_total, std::max(1, atoi(v)));
+    const BwdTile t1 = plan_bwd_tile_ocp(gx, kg, c_out, nw_total, 1);
+    if (gx.C < 16 || t1.smem == 0) return t1;
+    const BwdTile t2 = plan_bwd_tile_ocp(gx, kg, c_out, nw_total, 2);
+    return (t2.smem && t2.ocp == 2 && (double)t2.TX * t2.TY >= 1.5 * t1.TX * t1.TY) ? t2 : t1;
+}
+
 // 32 values per lane -> lane L receives the sum over lanes of v[L] (butterfly reduce-scatter).
 __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
 #pragma unroll
@@ -140,40 +146,57 @@ __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
     return v[0];
 }
 
-// Slot order of the n weights of one input channel (one thread): counting sort by the bank
-// residue of the G offset (d & 31), then position i of that order goes to block i % nb, lane
-// i / nb while every block still has room (the last block holds L = n - 32 (nb - 1)), the rest
-// round-robin over the full blocks. f(j, slot, d) for each weight j.
+// Slot order of the n weights of one input channel, computed by one warp (deterministic, so
+// setup and the final dw flush agree): the weights sorted by the bank residue of their G offset
+// (d & 31; ties in weight order), then position i of that order goes to block i % nb, lane i / nb
+// while every block still has room (the last block holds L = n - 32 (nb - 1)), the rest
+// round-robin over the full blocks. f(j, slot, d) for each weight j. cnt: 32 ints of the warp's
+// shared scratch.
 template <typename D, typename F>
-__device__ __forceinline__ void bwd_weight_slots(int ic, int t0, int n, D gdel, F f) {
-    (void)ic;
+__device__ __forceinline__ void bwd_weight_slots(int t0, int n, D gdel, int* cnt, F f) {
+    const int lane = threadIdx.x & 31;
     const int nb = (n + 31) >> 5;
     if (nb <= 1) {   // one block: any order, no conflicts to spread
-        for (int j = 0; j < n; ++j) f(j, j, gdel(t0, j));
+        for (int j = lane; j < n; j += 32) f(j, j, gdel(t0, j));
         return;
     }
     const int L = n - 32 * (nb - 1);
-    int cnt[32];
-#pragma unroll
-    for (int r = 0; r < 32; ++r) cnt[r] = 0;
-    for (int j = 0; j < n; ++j) ++cnt[gdel(t0, j) & 31];
-    int run = 0;
-    for (int r = 0; r < 32; ++r) {
-        const int c = cnt[r];
-        cnt[r] = run;
-        run += c;
+    const uint32_t lt = (1u << lane) - 1u;
+    cnt[lane] = 0;
+    __syncwarp();
+    for (int c0 = 0; c0 < n; c0 += 32) {   // per-residue totals
+        const int j = c0 + lane;
+        const bool ok = j < n;
+        const int r = ok ? (gdel(t0, j) & 31) : 32 + lane;
+        const unsigned m = __match_any_sync(kFull, r);
+        if (ok && (m >> lane) == 1u) cnt[r] += __popc(m);   // the highest lane of the residue group
+        __syncwarp();
     }
-    for (int j = 0; j < n; ++j) {
-        const int d = gdel(t0, j);
-        const int i = cnt[d & 31]++;
-        int slot;
-        if (i < nb * L) {
-            slot = (i % nb) * 32 + i / nb;
-        } else {
-            const int i2 = i - nb * L;
-            slot = (i2 % (nb - 1)) * 32 + L + i2 / (nb - 1);
+    const int c = cnt[lane];
+    const int incl = warp_incl_scan(c);
+    __syncwarp();
+    cnt[lane] = incl - c;   // first position of residue lane
+    __syncwarp();
+    for (int c0 = 0; c0 < n; c0 += 32) {
+        const int j = c0 + lane;
+        const bool ok = j < n;
+        const int d = ok ? gdel(t0, j) : 0;
+        const int r = ok ? (d & 31) : 32 + lane;
+        const unsigned m = __match_any_sync(kFull, r);
+        const int i = ok ? cnt[r] + __popc(m & lt) : 0;
+        __syncwarp();
+        if (ok && (m >> lane) == 1u) cnt[r] += __popc(m);
+        __syncwarp();
+        if (ok) {
+            int slot;
+            if (i < nb * L) {
+                slot = (i % nb) * 32 + i / nb;
+            } else {
+                const int i2 = i - nb * L;
+                slot = (i2 % (nb - 1)) * 32 + L + i2 / (nb - 1);
+            }
+            f(j, slot, d);
         }
-        f(j, slot, d);
     }
 }
 
@@ -241,7 +264,7 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
     }
     __syncthreads();
     const int nwg = lbase[(ocp - 1) * (c_in + 1) + c_in];
-    for (int q = threadIdx.x; q < c_in * ocp; q += blockDim.x) {
+    for (int q = warp; q < c_in * ocp; q += nwarps) {   // one warp per (pass, input channel)
         const int pp = q / c_in, ic = q - pp * c_in;
         const int ocb = oc0 + pp * ocs;   // first channel of the pass: slice 0 of the slab
         auto gdel = [&](int t0, int j) {   // g at uid = id - (fid - centre): G index = ebase - wdel
@@ -249,7 +272,7 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
             return meta_ow(m.x) * sW + off_x(m.y) * sX + off_y(m.y) * sY + off_z(m.y) - (meta_oc(m.x) - ocb) * sOC;
         };
         const int lb = lbase[pp * (c_in + 1) + ic], t0 = wo(pp, ic);
-        bwd_weight_slots(ic, t0, wo(pp + 1, ic) - t0, gdel, [&](int j, int slot, int d) {
+        bwd_weight_slots(t0, wo(pp + 1, ic) - t0, gdel, st_eb, [&](int j, int slot, int d) {
             wdel[lb + slot] = d;
             wv[lb + slot] = wval[t0 + j];
         });
@@ -502,7 +525,7 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
     }
     __syncthreads();
     if (DW) {   // the same slot order again: slot -> weight
-        for (int q = threadIdx.x; q < c_in * ocp; q += blockDim.x) {
+        for (int q = warp; q < c_in * ocp; q += nwarps) {
             const int pp = q / c_in, ic = q - pp * c_in;
             const int ocb = oc0 + pp * ocs;
             auto gdel = [&](int t0, int j) {
@@ -510,7 +533,7 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
                 return meta_ow(m.x) * sW + off_x(m.y) * sX + off_y(m.y) * sY + off_z(m.y) - (meta_oc(m.x) - ocb) * sOC;
             };
             const int lb = lbase[pp * (c_in + 1) + ic], t0 = wo(pp, ic);
-            bwd_weight_slots(ic, t0, wo(pp + 1, ic) - t0, gdel, [&](int j, int slot, int) {
+            bwd_weight_slots(t0, wo(pp + 1, ic) - t0, gdel, st_eb, [&](int j, int slot, int) {
                 const double v = dwp[lb + slot];
                 if (v != 0.0) atomicAdd(&dw_acc[wsrc[t0 + j]], v);
             });
