@@ -120,13 +120,14 @@ static BwdTile plan_bwd_tile_ocp(const Geo& gx, const KGeo& kg, int c_out, int n
 // Passes per item (SPC_BWD_OCP overrides): with ocp passes the G slab holds ocg / ocp channels,
 // so the tile can be larger (less halo re-read per interior voxel, more entry chunks per item to
 // spread over the warps) at the cost of ocp fills / sweeps per item. Two passes are taken for
-// wide inputs (>= 16 channels) when they buy at least 1.5x the tile area. Measured: C4 (8 input
+// wide inputs (>= 32 channels) when they buy at least 1.5x the tile area. Measured: C4 (8 input
 // channels) 3.12 / 3.69 ms with 1 / 2 passes; the C3 chain (32 -> 64 layer) 20.3 / 18.3 ms per
-// step; C2 (16 -> 32 on 7 x 7 planes: the tile is the whole plane either way) 0.70 / 0.74 ms.
+// step; C5 32 -> 32 at 50 % 20.1 -> 13.2 ms; C2 (16 -> 32 on 7 x 7 planes) 0.70 / 0.74 ms; the
+// OctNet3 trunk (16 / 24 input channels) 8.66 / 9.15 ms.
 BwdTile plan_bwd_tile(const Geo& gx, const KGeo& kg, int c_out, int nw_total) {
     if (const char* v = getenv("SPC_BWD_OCP")) return plan_bwd_tile_ocp(gx, kg, c_out, nw_total, std::max(1, atoi(v)));
     const BwdTile t1 = plan_bwd_tile_ocp(gx, kg, c_out, nw_total, 1);
-    if (gx.C < 16 || t1.smem == 0) return t1;
+    if (gx.C < 32 || t1.smem == 0) return t1;
     const BwdTile t2 = plan_bwd_tile_ocp(gx, kg, c_out, nw_total, 2);
     return (t2.smem && t2.ocp == 2 && (double)t2.TX * t2.TY >= 1.5 * t1.TX * t1.TY) ? t2 : t1;
 }
@@ -146,57 +147,80 @@ __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
     return v[0];
 }
 
-// Slot order of the n weights of one input channel, computed by one warp (deterministic, so
-// setup and the final dw flush agree): the weights sorted by the bank residue of their G offset
-// (d & 31; ties in weight order), then position i of that order goes to block i % nb, lane i / nb
-// while every block still has room (the last block holds L = n - 32 (nb - 1)), the rest
-// round-robin over the full blocks. f(j, slot, d) for each weight j. cnt: 32 ints of the warp's
-// shared scratch.
-template <typename D, typename F>
-__device__ __forceinline__ void bwd_weight_slots(int t0, int n, D gdel, int* cnt, F f) {
-    const int lane = threadIdx.x & 31;
-    const int nb = (n + 31) >> 5;
-    if (nb <= 1) {   // one block: any order, no conflicts to spread
-        for (int j = lane; j < n; j += 32) f(j, j, gdel(t0, j));
-        return;
-    }
-    const int L = n - 32 * (nb - 1);
+// Slot order of the weights of one (pass, input channel) range of the backward filter table: the
+// lanes of conv_bwd_kernel walk a range in blocks of 32 weights, and two lanes of a block whose G
+// offsets agree mod 32 words read the same shared-memory bank for every entry. So the range is
+// reordered in place (before conv_bwd_kernel, once per call, one warp per range): weights sorted
+// by the bank residue of their G offset (ties in table order), then position i of that order goes
+// to block i % nb, lane i / nb while every block still has room (the last block holds
+// L = n - 32 (nb - 1)), the rest round-robin over the full blocks. dw per weight is unaffected
+// (each weight keeps its source index); dx(e), a sum over the weights, only changes its fp32
+// summation order. Ranges of more than 256 weights keep the table order.
+__global__ void __launch_bounds__(512) bwd_slot_order_kernel(KGeo kg, BwdTile t, int c_in, int c_out,
+                                                             int2* __restrict__ wmeta, float* __restrict__ wval,
+                                                             int* __restrict__ wsrc, const int* __restrict__ woff) {
+    __shared__ int cnt_all[16][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int* cnt = cnt_all[warp];
+    const int oc0 = blockIdx.x * t.ocg, nocl = min(t.ocg, c_out - oc0);
     const uint32_t lt = (1u << lane) - 1u;
-    cnt[lane] = 0;
-    __syncwarp();
-    for (int c0 = 0; c0 < n; c0 += 32) {   // per-residue totals
-        const int j = c0 + lane;
-        const bool ok = j < n;
-        const int r = ok ? (gdel(t0, j) & 31) : 32 + lane;
-        const unsigned m = __match_any_sync(kFull, r);
-        if (ok && (m >> lane) == 1u) cnt[r] += __popc(m);   // the highest lane of the residue group
-        __syncwarp();
-    }
-    const int c = cnt[lane];
-    const int incl = warp_incl_scan(c);
-    __syncwarp();
-    cnt[lane] = incl - c;   // first position of residue lane
-    __syncwarp();
-    for (int c0 = 0; c0 < n; c0 += 32) {
-        const int j = c0 + lane;
-        const bool ok = j < n;
-        const int d = ok ? gdel(t0, j) : 0;
-        const int r = ok ? (d & 31) : 32 + lane;
-        const unsigned m = __match_any_sync(kFull, r);
-        const int i = ok ? cnt[r] + __popc(m & lt) : 0;
-        __syncwarp();
-        if (ok && (m >> lane) == 1u) cnt[r] += __popc(m);
-        __syncwarp();
-        if (ok) {
-            int slot;
-            if (i < nb * L) {
-                slot = (i % nb) * 32 + i / nb;
-            } else {
-                const int i2 = i - nb * L;
-                slot = (i2 % (nb - 1)) * 32 + L + i2 / (nb - 1);
-            }
-            f(j, slot, d);
+    for (int q = warp; q < c_in * t.ocp; q += 16) {
+        const int pp = q / c_in, ic = q - pp * c_in;
+        const int ocb = oc0 + pp * t.ocs;
+        const int t0 = woff[ic * (c_out + 1) + oc0 + min(nocl, pp * t.ocs)];
+        const int n = woff[ic * (c_out + 1) + oc0 + min(nocl, (pp + 1) * t.ocs)] - t0;
+        if (n <= 32 || n > 256) continue;   // one block (nothing to spread) / too long: table order
+        const int nb = (n + 31) >> 5, L = n - 32 * (nb - 1);
+        int2 mm[8];
+        float vv[8];
+        int ss[8], dd[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const int j = c * 32 + lane;
+            const bool ok = j < n;
+            mm[c] = ok ? wmeta[t0 + j] : make_int2(0, 0);
+            vv[c] = ok ? wval[t0 + j] : 0.0f;
+            ss[c] = ok ? wsrc[t0 + j] : 0;
+            // g at uid = id - (fid - centre): G index = ebase - wdel, as conv_bwd_kernel
+            dd[c] = meta_ow(mm[c].x) * t.sW + off_x(mm[c].y) * t.sX + off_y(mm[c].y) * t.sY + off_z(mm[c].y) -
+                    (meta_oc(mm[c].x) - ocb) * t.sOC;
         }
+        cnt[lane] = 0;
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {   // per-residue totals
+            const bool ok = c * 32 + lane < n;
+            const int r = ok ? (dd[c] & 31) : 32 + lane;
+            const unsigned m = __match_any_sync(kFull, r);
+            if (ok && (m >> lane) == 1u) cnt[r] += __popc(m);   // the highest lane of the residue group
+            __syncwarp();
+        }
+        const int c0 = cnt[lane];
+        const int incl = warp_incl_scan(c0);
+        __syncwarp();
+        cnt[lane] = incl - c0;   // first position of residue lane
+        __syncwarp();
+        int slot[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const bool ok = c * 32 + lane < n;
+            const int r = ok ? (dd[c] & 31) : 32 + lane;
+            const unsigned m = __match_any_sync(kFull, r);
+            const int i = ok ? cnt[r] + __popc(m & lt) : 0;
+            __syncwarp();
+            if (ok && (m >> lane) == 1u) cnt[r] += __popc(m);
+            __syncwarp();
+            slot[c] = i < nb * L ? (i % nb) * 32 + i / nb
+                                 : ((i - nb * L) % (nb - 1)) * 32 + L + (i - nb * L) / (nb - 1);
+        }
+        __syncwarp();   // every lane holds its weights: write them back in slot order
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            if (c * 32 + lane < n) {
+                wmeta[t0 + slot[c]] = mm[c];
+                wval[t0 + slot[c]] = vv[c];
+                wsrc[t0 + slot[c]] = ss[c];
+            }
     }
 }
 
@@ -267,15 +291,13 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
     for (int q = warp; q < c_in * ocp; q += nwarps) {   // one warp per (pass, input channel)
         const int pp = q / c_in, ic = q - pp * c_in;
         const int ocb = oc0 + pp * ocs;   // first channel of the pass: slice 0 of the slab
-        auto gdel = [&](int t0, int j) {   // g at uid = id - (fid - centre): G index = ebase - wdel
+        const int lb = lbase[pp * (c_in + 1) + ic], t0 = wo(pp, ic), n = wo(pp + 1, ic) - t0;
+        for (int j = lane; j < n; j += 32) {   // (the table range is in slot order: bwd_slot_order_kernel)
             const int2 m = wmeta[t0 + j];
-            return meta_ow(m.x) * sW + off_x(m.y) * sX + off_y(m.y) * sY + off_z(m.y) - (meta_oc(m.x) - ocb) * sOC;
-        };
-        const int lb = lbase[pp * (c_in + 1) + ic], t0 = wo(pp, ic);
-        bwd_weight_slots(t0, wo(pp + 1, ic) - t0, gdel, st_eb, [&](int j, int slot, int d) {
-            wdel[lb + slot] = d;
-            wv[lb + slot] = wval[t0 + j];
-        });
+            // g at uid = id - (fid - centre): G index = ebase - wdel
+            wdel[lb + j] = meta_ow(m.x) * sW + off_x(m.y) * sX + off_y(m.y) * sY + off_z(m.y) - (meta_oc(m.x) - ocb) * sOC;
+            wv[lb + j] = wval[t0 + j];
+        }
     }
     for (int i = threadIdx.x; i < nwg; i += blockDim.x) dwp[i] = 0.0;
     for (int i = threadIdx.x; i < gsize; i += blockDim.x) G[i] = 0.0f;
@@ -524,19 +546,14 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
         }   // passes
     }
     __syncthreads();
-    if (DW) {   // the same slot order again: slot -> weight
+    if (DW) {   // slot j of a range is table entry t0 + j
         for (int q = warp; q < c_in * ocp; q += nwarps) {
             const int pp = q / c_in, ic = q - pp * c_in;
-            const int ocb = oc0 + pp * ocs;
-            auto gdel = [&](int t0, int j) {
-                const int2 m = wmeta[t0 + j];
-                return meta_ow(m.x) * sW + off_x(m.y) * sX + off_y(m.y) * sY + off_z(m.y) - (meta_oc(m.x) - ocb) * sOC;
-            };
-            const int lb = lbase[pp * (c_in + 1) + ic], t0 = wo(pp, ic);
-            bwd_weight_slots(t0, wo(pp + 1, ic) - t0, gdel, st_eb, [&](int j, int slot, int) {
-                const double v = dwp[lb + slot];
+            const int lb = lbase[pp * (c_in + 1) + ic], t0 = wo(pp, ic), n = wo(pp + 1, ic) - t0;
+            for (int j = lane; j < n; j += 32) {
+                const double v = dwp[lb + j];
                 if (v != 0.0) atomicAdd(&dw_acc[wsrc[t0 + j]], v);
-            });
+            }
         }
     }
 }
@@ -575,6 +592,11 @@ cudaError_t launch_conv_bwd(const Geo& gx, const Geo& gy, const KGeo& kg, const 
                             const int2* wmeta, const float* wval, const int* woff, const int* wsrc,
                             float* dx, double* dw_acc, bool want_dx, bool want_dw, cudaStream_t s) {
     if (gx.B == 0) return cudaSuccess;
+    {
+        SPC_PHASE("bwd_slot_order", s, 1);
+        bwd_slot_order_kernel<<<(unsigned)t.n_ocg, 512, 0, s>>>(kg, t, (int)gx.C, (int)gy.C, const_cast<int2*>(wmeta),
+                                                                 const_cast<float*>(wval), const_cast<int*>(wsrc), woff);
+    }
     if (want_dx && want_dw)
         return launch_bwd_t<true, true>(gx, gy, kg, t, xkeys, xvals, xrow, ykeys, dy, yrow, wmeta, wval, woff, wsrc,
                                         dx, dw_acc, s);

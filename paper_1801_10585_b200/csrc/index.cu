@@ -408,10 +408,11 @@ cudaError_t launch_scatter_grad(const int64_t* src, const float* dy, int64_t n_o
 // memory it is assembled there (zeros, then dy at the sources) and streamed out with 16-byte
 // coalesced stores; otherwise thread t writes dy[t] and zeroes the gap after its predecessor
 // (gaps of 64 or more by the whole warp).
-constexpr int kSgItems = 8;
-constexpr int kSgT = 256 * kSgItems;    // sources per CTA
+// sources per CTA: T = 256 * items, items in {1, 2, 4, 8} chosen on the host so that small maps
+// still spread over the SMs
 constexpr int kSgCap = 8192;            // dx elements assembled in shared memory (32 KB)
 
+template <int kSgT>
 __global__ void __launch_bounds__(256) scatter_grad_sorted_kernel(const int64_t* __restrict__ src,
                                                                   const float* __restrict__ dy, int64_t nbound,
                                                                   const int64_t* n_dev, float* __restrict__ dx,
@@ -495,9 +496,18 @@ cudaError_t launch_check_sorted(const int64_t* src, int64_t n_out_bound, const i
 
 cudaError_t launch_scatter_grad_sorted(const int64_t* src, const float* dy, int64_t n_out_bound,
                                        const int64_t* n_out_dev, float* dx, int64_t n_in, cudaStream_t s) {
-    // one CTA per kSgT sources plus the tail sentinel
-    const int64_t grid = (n_out_bound + 1 + kSgT - 1) / kSgT;
-    { SPC_PHASE("scatter_grad", s, 1); scatter_grad_sorted_kernel<<<(unsigned)grid, 256, 0, s>>>(src, dy, n_out_bound, n_out_dev, dx, n_in); }
+    // one CTA per T sources plus the tail sentinel; T as large as keeps >= 4 CTAs per SM busy
+    const int64_t want = 4 * (int64_t)num_sms();
+    int items = 8;
+    while (items > 1 && (n_out_bound + 1) / (256 * items) < want) items >>= 1;
+    const unsigned grid = (unsigned)((n_out_bound + 256 * items) / (256 * items));
+    SPC_PHASE("scatter_grad", s, 1);
+    switch (items) {
+        case 8: scatter_grad_sorted_kernel<2048><<<grid, 256, 0, s>>>(src, dy, n_out_bound, n_out_dev, dx, n_in); break;
+        case 4: scatter_grad_sorted_kernel<1024><<<grid, 256, 0, s>>>(src, dy, n_out_bound, n_out_dev, dx, n_in); break;
+        case 2: scatter_grad_sorted_kernel<512><<<grid, 256, 0, s>>>(src, dy, n_out_bound, n_out_dev, dx, n_in); break;
+        default: scatter_grad_sorted_kernel<256><<<grid, 256, 0, s>>>(src, dy, n_out_bound, n_out_dev, dx, n_in); break;
+    }
     return cudaGetLastError();
 }
 
