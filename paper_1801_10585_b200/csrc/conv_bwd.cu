@@ -49,7 +49,11 @@ static BwdStrides bwd_strides(const KGeo& kg, int Z, int TX, int TY) {
 static size_t bwd_smem(const KGeo& kg, int c_in, int TX, int TY, int Z, int ocs, int ocp, int64_t nwg, int threads) {
     const size_t g = (size_t)ocs * bwd_strides(kg, Z, TX, TY).sOC * sizeof(float);
     const size_t w = (size_t)nwg * (sizeof(int) + sizeof(float) + sizeof(double));
-    const size_t idx = (size_t)(c_in + 1) * sizeof(int) * (1 + ocp) + (size_t)c_in * TX * 2 * sizeof(uint32_t);
+    // lbase / cpre, and two buffers each of the entry-range bounds (rng) and the halo-row bounds
+    // of the gradient fill (prefetched one item ahead)
+    const size_t nhalo = (size_t)ocs * ocp * (1 + 2 * kg.hw) * (TX + 2 * kg.hx);
+    const size_t idx = (size_t)(c_in + 1) * sizeof(int) * (1 + ocp) + 2 * (size_t)c_in * TX * 2 * sizeof(uint32_t) +
+                       2 * nhalo * 2 * sizeof(uint32_t);
     const size_t stage = (size_t)(threads / 32) * 32 * 4 * sizeof(int);   // per warp: 4 x 32 words
     return g + w + idx + stage + 256;
 }
@@ -258,8 +262,17 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
     p += (size_t)(c_in + 1) * ocp * sizeof(int);
     int* cpre = reinterpret_cast<int*>(p);
     p += (size_t)(c_in + 1) * sizeof(int);
-    uint32_t* rng = reinterpret_cast<uint32_t*>(p);
+    uint32_t* rbuf[2];   // entry-range bounds per (ic, x-row) of an item, double-buffered
+    rbuf[0] = reinterpret_cast<uint32_t*>(p);
     p += (size_t)c_in * t.TX * 2 * sizeof(uint32_t);
+    rbuf[1] = reinterpret_cast<uint32_t*>(p);
+    p += (size_t)c_in * t.TX * 2 * sizeof(uint32_t);
+    const int nhalo = t.ocg * HW * HX;   // halo rows of the group (all passes)
+    uint32_t* fbuf[2];   // per halo row the kept-output range of its y-rows, double-buffered
+    fbuf[0] = reinterpret_cast<uint32_t*>(p);
+    p += (size_t)nhalo * 2 * sizeof(uint32_t);
+    fbuf[1] = reinterpret_cast<uint32_t*>(p);
+    p += (size_t)nhalo * 2 * sizeof(uint32_t);
     // align from the __shared__ base with integer offsets (keeps the shared address space)
     p = smraw + ((size_t)(p - smraw + 15) & ~(size_t)15);
     int* st_eb = reinterpret_cast<int*>(p) + warp * 128;   // per warp: 32 ebase + 32 values (+ 64 fill words)
@@ -304,49 +317,132 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
     const int eb_safe = kg.hw * sW + kg.hx * sX + kg.hy * sY + kg.hz;   // an in-range G index for idle lanes
 
     const int64_t items = gx.B * gx.W * (int64_t)t.ntx * t.nty;
-    for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-        // (items < 2^31, plan_bwd_tile): divisions by multiply-high
+    const int HWX = HW * HX;
+    const float invZ = 1.0f / (float)gy.Z;
+    const float invXZ = 1.0f / (float)gx.Z;
+    struct ItemGeo { int64_t b; int wp, x0, y0, xe, ye, hylo, hyhi; };
+    auto item_geo = [&](int64_t item) {   // (items < 2^31, plan_bwd_tile): divisions by multiply-high
+        ItemGeo g;
         const uint32_t bw = fdiv((uint32_t)item, t.fd_tiles);   // (b, w-plane)
         const uint32_t bq = fdiv(bw, t.fd_W);
-        const int64_t b = bq;
-        const int wp = (int)(bw - bq * (uint32_t)gx.W);
+        g.b = bq;
+        g.wp = (int)(bw - bq * (uint32_t)gx.W);
         const int tile = (int)((uint32_t)item - bw * (uint32_t)(t.ntx * t.nty));
         const int tyi = (int)fdiv((uint32_t)tile, t.fd_ntx);
-        const int x0 = (tile - tyi * t.ntx) * t.TX, y0 = tyi * t.TY;
-        const int xe = min(x0 + t.TX, gx.X), ye = min(y0 + t.TY, gx.Y);
-        __syncthreads();
-        // entry ranges: per (ic, x) the stored entries of rows y0..ye-1 are contiguous (loaded
-        // first: their latency overlaps the gradient fill below)
-        for (int q = threadIdx.x; q < c_in * t.TX; q += blockDim.x) {
+        g.x0 = (tile - tyi * t.ntx) * t.TX;
+        g.y0 = tyi * t.TY;
+        g.xe = min(g.x0 + t.TX, gx.X);
+        g.ye = min(g.y0 + t.TY, gx.Y);
+        g.hylo = max(0, g.y0 - kg.hy);
+        g.hyhi = min(gy.Y, g.y0 + t.TY + kg.hy);
+        return g;
+    };
+    // halo row r of the group = (ocl, hw-plane, hx-row) -> its first y-row in the output map (or
+    // -1) and its base in the slab (channel slice ocl % ocs of its pass)
+    auto halo_row = [&](const ItemGeo& g, int r, int& gbase) -> int64_t {
+        const int ocl = (int)fdiv((uint32_t)r, t.fd_HWX), hr = r - ocl * HWX;
+        const int hwi = (int)fdiv((uint32_t)hr, t.fd_HX), hxr = hr - hwi * HX;
+        const int ws = g.wp - kg.hw + hwi, xs = g.x0 - kg.hx + hxr;
+        gbase = (ocl % ocs) * sOC + hwi * sW + hxr * sX + (g.hylo - (g.y0 - kg.hy)) * sY + kg.hz;
+        if (ws < 0 || ws >= gy.W || xs < 0 || xs >= gy.X || g.hylo >= g.hyhi || ocl >= nocl) return -1;
+        return (((g.b * c_out + oc0 + ocl) * gy.W + ws) * gy.X + xs) * (int64_t)gy.Y + g.hylo;
+    };
+    // the bounds of an item, fetched with cp.async one item ahead (their latency overlaps the
+    // current item): per (ic, x-row) the stored entries of rows y0..ye-1 (one contiguous run), per
+    // halo row the kept outputs of its halo y-range (one contiguous run)
+    auto cp4 = [](uint32_t* dst, const uint32_t* src) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;"
+                     :: "r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
+    };
+    auto prefetch = [&](int64_t item, uint32_t* rb, uint32_t* fbb) {
+        // (issued by the highest threads: warp 0 goes on with the chunk prefix meanwhile)
+        const int tr = (int)blockDim.x - 1 - (int)threadIdx.x;
+        const ItemGeo g = item_geo(item);
+        for (int q = tr; q < c_in * t.TX; q += blockDim.x) {
             const int ic = (int)fdiv((uint32_t)q, t.fd_TX), xi = q - ic * t.TX;
-            uint32_t lo = 0, hi = 0;
-            if (x0 + xi < xe) {
-                const int64_t r0 = (((b * c_in + ic) * gx.W + wp) * gx.X + x0 + xi) * (int64_t)gx.Y + y0;
-                lo = xrow[r0];
-                hi = xrow[r0 + (ye - y0)];
+            if (g.x0 + xi < g.xe) {
+                const int64_t r0 = (((g.b * c_in + ic) * gx.W + g.wp) * gx.X + g.x0 + xi) * (int64_t)gx.Y + g.y0;
+                cp4(rb + 2 * q, xrow + r0);
+                cp4(rb + 2 * q + 1, xrow + r0 + (g.ye - g.y0));
+            } else {
+                rb[2 * q] = 0u;
+                rb[2 * q + 1] = 0u;
             }
-            rng[2 * q] = lo;
-            rng[2 * q + 1] = hi;
         }
-        int nchunks = 0;
+        for (int r = tr; r < nhalo; r += blockDim.x) {
+            int gb;
+            const int64_t row = halo_row(g, r, gb);
+            if (row >= 0) {
+                cp4(fbb + 2 * r, yrow + row);
+                cp4(fbb + 2 * r + 1, yrow + row + (g.hyhi - g.hylo));
+            } else {
+                fbb[2 * r] = 0u;
+                fbb[2 * r + 1] = 0u;
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int cb = 0;
+    if (blockIdx.x < items) prefetch(blockIdx.x, rbuf[0], fbuf[0]);
+    for (int64_t item = blockIdx.x; item < items; item += gridDim.x, cb ^= 1) {
+        const ItemGeo ig = item_geo(item);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();   // this item's bounds are in; the previous item's sweep of G is complete
+        if (item + gridDim.x < items) prefetch(item + gridDim.x, cb ? rbuf[0] : rbuf[1], cb ? fbuf[0] : fbuf[1]);
+        const uint32_t* rng = cb ? rbuf[1] : rbuf[0];
+        const uint32_t* fbd = cb ? fbuf[1] : fbuf[0];
+        if (warp == 0) {   // chunks per ic (32 entries each), exclusive prefix over ic
+            int carry = 0;
+            for (int ic0 = 0; ic0 < c_in; ic0 += 32) {
+                const int ic = ic0 + lane;
+                int cnt = 0;
+                if (ic < c_in)
+                    for (int xi = 0; xi < t.TX; ++xi)
+                        cnt += (int)(rng[2 * (ic * t.TX + xi) + 1] - rng[2 * (ic * t.TX + xi)]);
+                const int nch = (cnt + 31) >> 5;
+                const int incl = warp_incl_scan(nch);
+                if (ic < c_in) cpre[ic] = carry + incl - nch;
+                carry += __shfl_sync(kFull, incl, 31);
+            }
+            if (lane == 0) cpre[c_in] = carry;
+        }
+        __syncthreads();
+        const int nchunks = cpre[c_in];
+        // chunk f -> (ic, entry of this lane) from the shared ranges, and the entry's key and value
+        // loads issued; the first chunk's loads are in flight during the gradient fill, the next
+        // chunk's while this chunk's blocks run
+        struct Loc { int ic, xi; int64_t e; uint64_t key; float v; };
+        auto locate = [&](int f, Loc& c) {
+            int ic = 0;
+            while (cpre[ic + 1] <= f) ++ic;
+            const int s = ((f - cpre[ic]) << 5) + lane;
+            c.ic = ic;
+            c.xi = -1;
+            c.e = -1;
+            int pre = 0;
+            for (int xi = 0; xi < t.TX; ++xi) {
+                const uint32_t lo = rng[2 * (ic * t.TX + xi)], hi = rng[2 * (ic * t.TX + xi) + 1];
+                const int n = (int)(hi - lo);
+                if (s >= pre && s < pre + n) {
+                    c.e = (int64_t)lo + (s - pre);
+                    c.xi = xi;
+                }
+                pre += n;
+            }
+            c.key = c.e >= 0 ? xkeys[c.e] : 0ull;
+            c.v = c.e >= 0 ? xvals[c.e] : 0.0f;
+        };
+        // warp w takes a contiguous run of chunks (mostly one input channel): concurrent warps
+        // then mostly update different dw words
+        const int per = (nchunks + nwarps - 1) / nwarps;
+        const int fb = min(nchunks, warp * per), fe = min(nchunks, fb + per);
+        Loc first{};
+        if (fb < fe) locate(fb, first);
         for (int pp = 0; pp < ocp; ++pp) {
-        const int ocb = oc0 + pp * ocs, nocp = min(ocs, nocl - pp * ocs);   // channels of this pass
+        const int nocp = min(ocs, nocl - pp * ocs);   // channels of this pass
         if (pp > 0) __syncthreads();   // the previous pass's sweep of G is complete
         // "initialize dense buffer with gradients(b, oc)", tile + halo, this oc group:
         // per (oc, halo x-row) the kept outputs of the halo y-range are one contiguous key run
-        const int hylo = max(0, y0 - kg.hy), hyhi = min(gy.Y, y0 + t.TY + kg.hy);
-        const float invZ = 1.0f / (float)gy.Z;
-        const float invXZ = 1.0f / (float)gx.Z;
-        const int HWX = HW * HX;
-        // halo row r = (ocl, hw-plane, hx-row) -> its first y-row in the output map (or -1)
-        auto halo_row = [&](int r, int& gbase) -> int64_t {
-            const int ocl = (int)fdiv((uint32_t)r, t.fd_HWX), hr = r - ocl * HWX;
-            const int hwi = (int)fdiv((uint32_t)hr, t.fd_HX), hxr = hr - hwi * HX;
-            const int ws = wp - kg.hw + hwi, xs = x0 - kg.hx + hxr;
-            gbase = ocl * sOC + hwi * sW + hxr * sX + (hylo - (y0 - kg.hy)) * sY + kg.hz;
-            if (ws < 0 || ws >= gy.W || xs < 0 || xs >= gy.X || hylo >= hyhi) return -1;
-            return (((b * c_out + ocb + ocl) * gy.W + ws) * gy.X + xs) * (int64_t)gy.Y + hylo;
-        };
         // the warp's rows r = warp + k * nwarps: lane k loads row k's bounds (one latency for all)
         for (int r0 = warp; r0 < nocp * HWX; r0 += 32 * nwarps) {
             uint32_t be0 = 0, be1 = 0;
@@ -355,10 +451,11 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
             {
                 const int r = r0 + lane * nwarps;
                 if (r < nocp * HWX) {
-                    const int64_t row = halo_row(r, gb);
-                    if (row >= 0) {
-                        be0 = yrow[row];
-                        be1 = yrow[row + (hyhi - hylo)];
+                    const int rg = pp * ocs * HWX + r;   // halo row of the group
+                    const int64_t row = halo_row(ig, rg, gb);
+                    if (row >= 0) {   // (bounds prefetched with the item)
+                        be0 = fbd[2 * rg];
+                        be1 = fbd[2 * rg + 1];
                         rz = (uint32_t)((uint64_t)row * (uint64_t)gy.Z);
                     }
                 }
@@ -419,54 +516,9 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
             __syncwarp();
         }
         __syncthreads();
-        if (pp == 0) {
-        if (warp == 0) {   // chunks per ic (32 entries each), exclusive prefix over ic
-            int carry = 0;
-            for (int ic0 = 0; ic0 < c_in; ic0 += 32) {
-                const int ic = ic0 + lane;
-                int cnt = 0;
-                if (ic < c_in)
-                    for (int xi = 0; xi < t.TX; ++xi)
-                        cnt += (int)(rng[2 * (ic * t.TX + xi) + 1] - rng[2 * (ic * t.TX + xi)]);
-                const int nch = (cnt + 31) >> 5;
-                const int incl = warp_incl_scan(nch);
-                if (ic < c_in) cpre[ic] = carry + incl - nch;
-                carry += __shfl_sync(kFull, incl, 31);
-            }
-            if (lane == 0) cpre[c_in] = carry;
-        }
-        __syncthreads();
-        nchunks = cpre[c_in];
-        }
-        // chunk f -> (ic, entry of this lane) from the shared ranges, and the entry's key and value
-        // loads issued; the next chunk's loads are in flight while this chunk's blocks run
-        struct Loc { int ic, xi; int64_t e; uint64_t key; float v; };
-        auto locate = [&](int f, Loc& c) {
-            int ic = 0;
-            while (cpre[ic + 1] <= f) ++ic;
-            const int s = ((f - cpre[ic]) << 5) + lane;
-            c.ic = ic;
-            c.xi = -1;
-            c.e = -1;
-            int pre = 0;
-            for (int xi = 0; xi < t.TX; ++xi) {
-                const uint32_t lo = rng[2 * (ic * t.TX + xi)], hi = rng[2 * (ic * t.TX + xi) + 1];
-                const int n = (int)(hi - lo);
-                if (s >= pre && s < pre + n) {
-                    c.e = (int64_t)lo + (s - pre);
-                    c.xi = xi;
-                }
-                pre += n;
-            }
-            c.key = c.e >= 0 ? xkeys[c.e] : 0ull;
-            c.v = c.e >= 0 ? xvals[c.e] : 0.0f;
-        };
         Loc cur{}, nxt{};
-        // warp w takes a contiguous run of chunks (mostly one input channel): concurrent warps
-        // then mostly update different dw words
-        const int per = (nchunks + nwarps - 1) / nwarps;
-        const int fb = min(nchunks, warp * per), fe = min(nchunks, fb + per);
-        if (fb < fe) locate(fb, cur);
+        if (pp == 0) cur = first;
+        else if (fb < fe) locate(fb, cur);
         for (int f = fb; f < fe; ++f) {
             if (f + 1 < fe) locate(f + 1, nxt);
             const int ic = cur.ic;
@@ -474,7 +526,7 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
             int eb = eb_safe;
             const float v = cur.v;
             if (e >= 0) {
-                const int64_t r0 = (((b * c_in + ic) * gx.W + wp) * gx.X + x0 + cur.xi) * (int64_t)gx.Y + y0;
+                const int64_t r0 = (((ig.b * c_in + ic) * gx.W + ig.wp) * gx.X + ig.x0 + cur.xi) * (int64_t)gx.Y + ig.y0;
                 const uint32_t L = (uint32_t)(cur.key - (uint64_t)r0 * (uint64_t)gx.Z);
                 const uint32_t yl = div_small(L, (uint32_t)gx.Z, invXZ);   // L < TY * Z
                 const int z = (int)(L - yl * (uint32_t)gx.Z);
