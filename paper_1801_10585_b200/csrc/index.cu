@@ -131,43 +131,52 @@ cudaError_t launch_row_index(const Geo& g, Keys keys, const int64_t* nnz_dev, in
 }
 
 // ------------------------------------------------------------------------- filter table
-// Runs of a grouping of the key-sorted filter entries whose groups are contiguous in key order:
-// run_start[q] / run_len[q] for q < nq (0 / 0 for empty groups). One block; entry j opens its
-// group's run when its predecessor is in another group and closes it likewise.
+// Both tables re-lay the key-sorted filter, whose groups (of the target order) are contiguous key
+// runs: (1) grid-wide, entry j opens its group's run when its predecessor is in another group and
+// closes it likewise; (2) one block clamps the runs and scans their lengths into offsets; (3)
+// grid-wide, every entry moves to its slot. K: uint32_t when every filter key is below 2^32
+// (c_out * c_in * prod(ksize), always in practice): the key arithmetic avoids emulated 64-bit
+// divisions.
+template <typename K>
+struct GrpBwd {   // (oc, ic) of a key, ic-major target order q = oc*c_in + ic (run index)
+    KGeo kg;
+    __device__ int operator()(const uint64_t* wk, int64_t j) const { return (int)((K)wk[j] / (K)kg.KV); }
+};
+template <typename K>
+struct GrpFwd {   // q = (ic*KXY + dxdy)*c_out + oc
+    KGeo kg;
+    int c_in, c_out, KXY;
+    __device__ int operator()(const uint64_t* wk, int64_t j) const {
+        const K k = (K)wk[j];
+        const K pq = k / (K)kg.KV;
+        const int oc = (int)(pq / (K)c_in), ic = (int)(pq - (K)oc * (K)c_in);
+        const int dxdy = (int)((k - pq * (K)kg.KV) / (K)kg.kz);
+        return (ic * KXY + dxdy) * c_out + oc;
+    }
+};
+
+// run_start / run_len zeroed by the caller; run_len[q] receives the run's end
 template <typename G>
-__device__ __forceinline__ void filter_runs(int64_t nw, int nq, G grp, int* __restrict__ run_start,
-                                            int* __restrict__ run_len) {
-    for (int q = threadIdx.x; q < nq; q += blockDim.x) {
-        run_start[q] = 0;
-        run_len[q] = 0;
-    }
-    __syncthreads();
-    for (int64_t j = threadIdx.x; j < nw; j += blockDim.x) {
-        const int q = grp(j);
+__global__ void filter_runs_kernel(const uint64_t* __restrict__ wk, int64_t nw, int nq, G grp,
+                                   int* __restrict__ run_start, int* __restrict__ run_len) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nw; j += (int64_t)gridDim.x * blockDim.x) {
+        const int q = grp(wk, j);
         if (q < 0 || q >= nq) continue;   // out-of-range filter key (rejected under SPC_VALIDATE)
-        if (j == 0 || grp(j - 1) != q) run_start[q] = (int)j;
-        if (j + 1 == nw || grp(j + 1) != q) run_len[q] = (int)j + 1;   // the run's end for now
+        if (j == 0 || grp(wk, j - 1) != q) run_start[q] = (int)j;
+        if (j + 1 == nw || grp(wk, j + 1) != q) run_len[q] = (int)j + 1;
     }
-    __syncthreads();
-    // (unsorted or duplicated keys break the runs: clamped so that no write leaves the tables)
-    for (int q = threadIdx.x; q < nq; q += blockDim.x)
-        run_len[q] = max(0, min(run_len[q] - run_start[q], (int)nw - run_start[q]));
-    __syncthreads();
 }
 
-// One block. Re-lays the (oc, ic, delta)-sorted filter into ic-major order (ic, oc, delta) so
-// that a CTA finds "filter(oc, ic)" of Alg. 1 for a group of oc as one contiguous range.
-__global__ void filter_table_kernel(KGeo kg, int c_in, int c_out, const uint64_t* __restrict__ wk,
-                                    const float* __restrict__ wv, int64_t nw, int2* __restrict__ meta,
-                                    float* __restrict__ val, int* __restrict__ off, int* __restrict__ src,
-                                    int* __restrict__ run_start,
-                                    int* __restrict__ run_len) {
+// (unsorted or duplicated keys break the runs: clamped so that no write leaves the tables)
+__device__ __forceinline__ int run_len_of(const int* run_start, const int* run_len, int q, int64_t nw) {
+    return max(0, min(run_len[q] - run_start[q], (int)nw - run_start[q]));
+}
+
+// backward table (ic, oc, delta): off[ic*(c_out+1) + oc] = first entry of (oc, ic)
+__global__ void filter_bwd_offsets_kernel(int c_in, int c_out, int64_t nw, const int* __restrict__ run_start,
+                                          int* __restrict__ run_len, int* __restrict__ off) {
     __shared__ int sm[33];
     const int npairs = c_in * c_out;
-    // runs of (oc, ic) = p in the key-sorted filter, from the boundaries between neighbours
-    // (no dependent searches: every entry is looked at once)
-    auto grp = [&](int64_t j) { return (int)(wk[j] / (uint64_t)kg.KV); };
-    filter_runs(nw, npairs, grp, run_start, run_len);
     int carry = 0;
     for (int base = 0; base < npairs; base += blockDim.x) {
         const int q = base + threadIdx.x;          // ic-major: q = ic*c_out + oc
@@ -175,7 +184,7 @@ __global__ void filter_table_kernel(KGeo kg, int c_in, int c_out, const uint64_t
         if (q < npairs) {
             ic = q / c_out;
             oc = q - ic * c_out;
-            len = run_len[oc * c_in + ic];
+            len = run_len_of(run_start, run_len, oc * c_in + ic, nw);
         }
         int tot;
         const int ex = block_excl_scan(len, sm, &tot);
@@ -185,11 +194,17 @@ __global__ void filter_table_kernel(KGeo kg, int c_in, int c_out, const uint64_t
     __syncthreads();
     for (int ic = threadIdx.x; ic < c_in; ic += blockDim.x)
         off[ic * (c_out + 1) + c_out] = (ic + 1 < c_in) ? off[(ic + 1) * (c_out + 1)] : carry;
-    __syncthreads();
-    for (int64_t j = threadIdx.x; j < nw; j += blockDim.x) {
-        const uint64_t key = wk[j];
-        const int p = (int)(key / (uint64_t)kg.KV);
-        const int dlin = (int)(key - (uint64_t)p * (uint64_t)kg.KV);
+}
+
+template <typename K>
+__global__ void filter_bwd_scatter_kernel(KGeo kg, int c_in, int c_out, const uint64_t* __restrict__ wk,
+                                          const float* __restrict__ wv, int64_t nw, int2* __restrict__ meta,
+                                          float* __restrict__ val, const int* __restrict__ off,
+                                          int* __restrict__ src, const int* __restrict__ run_start) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nw; j += (int64_t)gridDim.x * blockDim.x) {
+        const K key = (K)wk[j];
+        const int p = (int)(key / (K)kg.KV);
+        const int dlin = (int)(key - (K)p * (K)kg.KV);
         if (p >= c_in * c_out) continue;   // out-of-range key (rejected under SPC_VALIDATE)
         const int oc = p / c_in, ic = p - (p / c_in) * c_in;
         const int dst = off[ic * (c_out + 1) + oc] + (int)(j - run_start[p]);
@@ -204,51 +219,65 @@ __global__ void filter_table_kernel(KGeo kg, int c_in, int c_out, const uint64_t
     }
 }
 
+static unsigned table_grid(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 4 * num_sms())); }
+
+// Re-lays the (oc, ic, delta)-sorted filter into ic-major order (ic, oc, delta) so that a CTA
+// finds "filter(oc, ic)" of Alg. 1 for a group of oc as one contiguous range.
 cudaError_t launch_filter_table(const KGeo& kg, int c_in, int c_out, const uint64_t* wkeys, const float* wvals,
                                 int64_t nw, int2* meta, float* val, int* off, int* src, int* scratch, cudaStream_t s) {
-    { SPC_PHASE("filter_table", s, 1); filter_table_kernel<<<1, 1024, 0, s>>>(kg, c_in, c_out, wkeys, wvals, nw, meta, val, off, src, scratch,
-                                           scratch + (size_t)c_in * c_out); }
+    const int npairs = c_in * c_out;
+    int* run_start = scratch;
+    int* run_len = scratch + (size_t)npairs;
+    SPC_PHASE("filter_table", s, 3);
+    cudaError_t e = cudaMemsetAsync(scratch, 0, sizeof(int) * 2 * (size_t)npairs, s);
+    if (e != cudaSuccess) return e;
+    const bool k32 = (double)c_out * c_in * kg.KV <= 4294967295.0;
+    if (k32) filter_runs_kernel<<<table_grid(nw), 256, 0, s>>>(wkeys, nw, npairs, GrpBwd<uint32_t>{kg}, run_start, run_len);
+    else filter_runs_kernel<<<table_grid(nw), 256, 0, s>>>(wkeys, nw, npairs, GrpBwd<uint64_t>{kg}, run_start, run_len);
+    filter_bwd_offsets_kernel<<<1, 1024, 0, s>>>(c_in, c_out, nw, run_start, run_len, off);
+    if (k32)
+        filter_bwd_scatter_kernel<uint32_t><<<table_grid(nw), 256, 0, s>>>(kg, c_in, c_out, wkeys, wvals, nw, meta, val, off,
+                                                                            src, run_start);
+    else
+        filter_bwd_scatter_kernel<uint64_t><<<table_grid(nw), 256, 0, s>>>(kg, c_in, c_out, wkeys, wvals, nw, meta, val, off,
+                                                                            src, run_start);
     return cudaGetLastError();
 }
 
 // Second order of the filter for the forward kernel: (ic, (dx,dy), oc, dz). For a fixed input
 // channel and in-plane offset the weights of a group of output channels are then one
 // contiguous range. meta2[j] = {oc, oz}, off2[(ic*KXY + dxdy)*(c_out+1) + oc] = first entry.
-// scratch: 2 * c_in*KXY*c_out ints. One block.
-__global__ void filter_table_fwd_kernel(KGeo kg, int c_in, int c_out, const uint64_t* __restrict__ wk,
-                                        const float* __restrict__ wv, int64_t nw, int2* __restrict__ meta2,
-                                        float* __restrict__ val2, int* __restrict__ off2, int* __restrict__ run_start,
-                                        int* __restrict__ run_len) {
+// scratch: 2 * c_in*KXY*c_out ints.
+__global__ void filter_fwd_offsets_kernel(int nq, int c_out, int64_t nw, const int* __restrict__ run_start,
+                                          const int* __restrict__ run_len, int* __restrict__ off2) {
     __shared__ int sm[33];
-    const int KXY = kg.kw * kg.kx * kg.ky;
-    const int nq = c_in * KXY * c_out;   // q = (ic*KXY + dxdy)*c_out + oc
-    auto grp = [&](int64_t j) {   // q of entry j: key = ((oc*c_in + ic)*KV + dxdy*kz + dz)
-        const uint64_t k = wk[j];
-        const uint64_t pq = k / (uint64_t)kg.KV;
-        const int oc = (int)(pq / (uint64_t)c_in), ic = (int)(pq - (uint64_t)oc * c_in);
-        const int dxdy = (int)((k - pq * (uint64_t)kg.KV) / (uint64_t)kg.kz);
-        return (ic * KXY + dxdy) * c_out + oc;
-    };
-    filter_runs(nw, nq, grp, run_start, run_len);
+    const int ng = nq / c_out;
     int carry = 0;
     for (int base = 0; base < nq; base += blockDim.x) {
         const int q = base + threadIdx.x;
-        const int len = q < nq ? run_len[q] : 0;
+        const int len = q < nq ? run_len_of(run_start, run_len, q, nw) : 0;
         int tot;
         const int ex = block_excl_scan(len, sm, &tot);
         if (q < nq) off2[(q / c_out) * (c_out + 1) + q % c_out] = carry + ex;
         carry += tot;
     }
     __syncthreads();
-    for (int g = threadIdx.x; g < c_in * KXY; g += blockDim.x)
-        off2[g * (c_out + 1) + c_out] = (g + 1 < c_in * KXY) ? off2[(g + 1) * (c_out + 1)] : carry;
-    __syncthreads();
-    for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+    for (int g = threadIdx.x; g < ng; g += blockDim.x)
+        off2[g * (c_out + 1) + c_out] = (g + 1 < ng) ? off2[(g + 1) * (c_out + 1)] : carry;
+}
+
+template <typename K>
+__global__ void filter_fwd_scatter_kernel(KGeo kg, int nq, int c_out, const uint64_t* __restrict__ wk,
+                                          const float* __restrict__ wv, int64_t nw, int2* __restrict__ meta2,
+                                          float* __restrict__ val2, const int* __restrict__ off2,
+                                          const int* __restrict__ run_start, const int* __restrict__ run_len) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
         const int oc = q % c_out, g = q / c_out;
         const int dst = off2[g * (c_out + 1) + oc];
-        for (int i = 0; i < run_len[q] && dst + i < nw; ++i) {
+        const int n = run_len_of(run_start, run_len, q, nw);
+        for (int i = 0; i < n && dst + i < nw; ++i) {
             const int j = run_start[q] + i;
-            const int dz = (int)(wk[j] % (uint64_t)kg.kz);
+            const int dz = (int)((K)wk[j] % (K)kg.kz);
             meta2[dst + i] = make_int2(oc, dz - kg.hz);
             val2[dst + i] = wv[j];
         }
@@ -257,8 +286,27 @@ __global__ void filter_table_fwd_kernel(KGeo kg, int c_in, int c_out, const uint
 
 cudaError_t launch_filter_table_fwd(const KGeo& kg, int c_in, int c_out, const uint64_t* wkeys, const float* wvals,
                                     int64_t nw, int2* meta2, float* val2, int* off2, int* scratch, cudaStream_t s) {
-    const size_t nq = (size_t)c_in * kg.kw * kg.kx * kg.ky * c_out;
-    { SPC_PHASE("filter_table", s, 1); filter_table_fwd_kernel<<<1, 1024, 0, s>>>(kg, c_in, c_out, wkeys, wvals, nw, meta2, val2, off2, scratch, scratch + nq); }
+    const int KXY = kg.kw * kg.kx * kg.ky;
+    const int nq = c_in * KXY * c_out;
+    int* run_start = scratch;
+    int* run_len = scratch + (size_t)nq;
+    SPC_PHASE("filter_table", s, 3);
+    cudaError_t e = cudaMemsetAsync(scratch, 0, sizeof(int) * 2 * (size_t)nq, s);
+    if (e != cudaSuccess) return e;
+    const bool k32 = (double)c_out * c_in * kg.KV <= 4294967295.0;
+    if (k32)
+        filter_runs_kernel<<<table_grid(nw), 256, 0, s>>>(wkeys, nw, nq, GrpFwd<uint32_t>{kg, c_in, c_out, KXY}, run_start,
+                                                          run_len);
+    else
+        filter_runs_kernel<<<table_grid(nw), 256, 0, s>>>(wkeys, nw, nq, GrpFwd<uint64_t>{kg, c_in, c_out, KXY}, run_start,
+                                                          run_len);
+    filter_fwd_offsets_kernel<<<1, 1024, 0, s>>>(nq, c_out, nw, run_start, run_len, off2);
+    if (k32)
+        filter_fwd_scatter_kernel<uint32_t><<<table_grid(nq), 256, 0, s>>>(kg, nq, c_out, wkeys, wvals, nw, meta2, val2,
+                                                                            off2, run_start, run_len);
+    else
+        filter_fwd_scatter_kernel<uint64_t><<<table_grid(nq), 256, 0, s>>>(kg, nq, c_out, wkeys, wvals, nw, meta2, val2,
+                                                                            off2, run_start, run_len);
     return cudaGetLastError();
 }
 
