@@ -333,14 +333,22 @@ struct FwdDesc {
     uint32_t aA, aB;     // accumulator byte addresses of the lane's entries (safe word when idle)
     float vA, vB;
     int n;               // entries of the descriptor (<= 64)
+    int2 rr;             // REGREC: record r0 + lane (rounds broadcast by shuffles)
 };
 
+// REGREC (round records in global memory, large filter banks): lane j also fetches record
+// r0 + j of the descriptor, so that its rounds read their records with shuffles instead of
+// dependent L1 loads (the descriptor is prefetched one ahead, so the fetch latency is hidden)
+template <bool REGREC>
 __device__ __forceinline__ FwdDesc load_desc(uint32_t wdsc, int lane, uint32_t accs, uint32_t safe,
-                                             const int* roffw, const uint32_t* spos, const float* sval) {
+                                             const int* roffw, const uint32_t* spos, const float* sval,
+                                             const int2* rec) {
     FwdDesc d;
     const int item = (int)(wdsc >> 19);
     d.r0 = roffw[item];
     d.r1 = roffw[item + 1];
+    d.rr = make_int2(0, 0);
+    if (REGREC && lane < d.r1 - d.r0) d.rr = rec[d.r0 + lane];
     const int s = (int)(wdsc & 0xfffu);
     d.n = (int)((wdsc >> 12) & 0x7fu);
     const bool okA = lane < d.n, okB = lane + 32 < d.n;
@@ -360,18 +368,53 @@ __device__ __forceinline__ FwdDesc load_desc(uint32_t wdsc, int lane, uint32_t a
 // (every round offset keeps it inside the slice) and do not store. The next descriptor's
 // dependent shared loads (descriptor -> round range, entries) are issued before the current
 // descriptor's rounds run.
-template <bool NEG0>
+template <bool NEG0, bool REGREC>
 __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, uint32_t safe, const uint32_t* work,
                                           const int* roffw, const int2* rec, const uint32_t* spos,
                                           const float* sval) {
     if (nwork <= 0) return;
-    FwdDesc nx = load_desc(work[0], lane, accs, safe, roffw, spos, sval);
+    FwdDesc nx = load_desc<REGREC>(work[0], lane, accs, safe, roffw, spos, sval, rec);
 #pragma unroll 1
     for (int g = 0; g < nwork; ++g) {
         const FwdDesc d = nx;
-        if (g + 1 < nwork) nx = load_desc(work[g + 1], lane, accs, safe, roffw, spos, sval);
+        if (g + 1 < nwork) nx = load_desc<REGREC>(work[g + 1], lane, accs, safe, roffw, spos, sval, rec);
         if (d.r0 == d.r1) continue;
         const bool okA = lane < d.n, okB = lane + 32 < d.n;
+        if (REGREC && d.r1 - d.r0 <= 32) {   // records in registers, broadcast by shuffles
+            const int nr = d.r1 - d.r0;
+            if (d.n > 32) {
+#pragma unroll 2
+                for (int r = 0; r < nr; ++r) {
+                    const uint32_t off = (uint32_t)__shfl_sync(kFull, d.rr.x, r);
+                    const float w = __int_as_float(__shfl_sync(kFull, d.rr.y, r));
+                    const uint32_t qa = d.aA + off, qb = d.aB + off;
+                    if (NEG0) {
+                        rmw2_neg0(qa, qb, d.vA, d.vB, w, okA, okB);
+                    } else {
+                        float oa = 0.0f, ob = 0.0f;
+                        if (okA) oa = lds_u(qa);
+                        if (okB) ob = lds_u(qb);
+                        if (okA) sts_u(qa, upd<NEG0>(oa, d.vA, w));
+                        if (okB) sts_u(qb, upd<NEG0>(ob, d.vB, w));
+                    }
+#ifndef SPC_NO_SYNCWARP
+                    __syncwarp();
+#endif
+                }
+            } else {
+#pragma unroll 2
+                for (int r = 0; r < nr; ++r) {
+                    const uint32_t qa = d.aA + (uint32_t)__shfl_sync(kFull, d.rr.x, r);
+                    const float w = __int_as_float(__shfl_sync(kFull, d.rr.y, r));
+                    if (NEG0) rmw1_neg0(qa, d.vA, w, okA);
+                    else if (okA) sts_u(qa, upd<NEG0>(lds_u(qa), d.vA, w));
+#ifndef SPC_NO_SYNCWARP
+                    __syncwarp();
+#endif
+                }
+            }
+            continue;
+        }
         if (d.n > 32) {
             int2 q = rec[d.r0];
 #pragma unroll 2
@@ -603,9 +646,9 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
         // ---- accumulate (Alg. 1 inner loops)
         if (warp < nocl) {
             if (neg0)
-                fwd_items<true>(nwork, lane, accs, safe, work, roffs + warp * PK, recp, spos, sval);
+                fwd_items<true, !REC_SMEM>(nwork, lane, accs, safe, work, roffs + warp * PK, recp, spos, sval);
             else
-                fwd_items<false>(nwork, lane, accs, safe, work, roffs + warp * PK, recp, spos, sval);
+                fwd_items<false, !REC_SMEM>(nwork, lane, accs, safe, work, roffs + warp * PK, recp, spos, sval);
         }
         __syncthreads();
     }
