@@ -59,7 +59,9 @@ FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_
     // read through L1 instead of being copied into every CTA
     auto rec_sm = [&](int ocg) { return nwg(ocg) * 8 <= 16 * 1024; };
     auto need = [&](int ocg, int TY) {
-        return fwd_fixed_smem(PK, ocg, rec_sm(ocg) ? nwg(ocg) : 0) + (size_t)ocg * (TY + 4 * kg.hy) * ZR * sizeof(float);
+        // (records in global memory: a 32-record buffer per warp for the current descriptor's)
+        return fwd_fixed_smem(PK, ocg, rec_sm(ocg) ? nwg(ocg) : kFwdWarps * 32) +
+               (size_t)ocg * (TY + 4 * kg.hy) * ZR * sizeof(float);
     };
     if (PK >= (1 << 13)) { t.smem = 0; return t; }                 // work descriptors hold 13-bit items
     int ocg = std::min(c_out, kFwdWarps);
@@ -371,7 +373,7 @@ __device__ __forceinline__ FwdDesc load_desc(uint32_t wdsc, int lane, uint32_t a
 template <bool NEG0, bool REGREC>
 __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, uint32_t safe, const uint32_t* work,
                                           const int* roffw, const int2* rec, const uint32_t* spos,
-                                          const float* sval) {
+                                          const float* sval, int2* wrec) {
     if (nwork <= 0) return;
     FwdDesc nx = load_desc<REGREC>(work[0], lane, accs, safe, roffw, spos, sval, rec);
 #pragma unroll 1
@@ -380,14 +382,18 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
         if (g + 1 < nwork) nx = load_desc<REGREC>(work[g + 1], lane, accs, safe, roffw, spos, sval, rec);
         if (d.r0 == d.r1) continue;
         const bool okA = lane < d.n, okB = lane + 32 < d.n;
-        if (REGREC && d.r1 - d.r0 <= 32) {   // records in registers, broadcast by shuffles
+        if (REGREC && d.r1 - d.r0 <= 32) {
+            // the descriptor's records (fetched with its prefetch) go to the warp's shared buffer
+            // now that they have arrived; the rounds read them by broadcast
             const int nr = d.r1 - d.r0;
+            if (lane < nr) wrec[lane] = d.rr;
+            __syncwarp();
             if (d.n > 32) {
 #pragma unroll 2
                 for (int r = 0; r < nr; ++r) {
-                    const uint32_t off = (uint32_t)__shfl_sync(kFull, d.rr.x, r);
-                    const float w = __int_as_float(__shfl_sync(kFull, d.rr.y, r));
-                    const uint32_t qa = d.aA + off, qb = d.aB + off;
+                    const int2 q = wrec[r];
+                    const uint32_t qa = d.aA + (uint32_t)q.x, qb = d.aB + (uint32_t)q.x;
+                    const float w = __int_as_float(q.y);
                     if (NEG0) {
                         rmw2_neg0(qa, qb, d.vA, d.vB, w, okA, okB);
                     } else {
@@ -404,8 +410,9 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
             } else {
 #pragma unroll 2
                 for (int r = 0; r < nr; ++r) {
-                    const uint32_t qa = d.aA + (uint32_t)__shfl_sync(kFull, d.rr.x, r);
-                    const float w = __int_as_float(__shfl_sync(kFull, d.rr.y, r));
+                    const int2 q = wrec[r];
+                    const uint32_t qa = d.aA + (uint32_t)q.x;
+                    const float w = __int_as_float(q.y);
                     if (NEG0) rmw1_neg0(qa, d.vA, w, okA);
                     else if (okA) sts_u(qa, upd<NEG0>(lds_u(qa), d.vA, w));
 #ifndef SPC_NO_SYNCWARP
@@ -413,6 +420,7 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
 #endif
                 }
             }
+            __syncwarp();   // (the buffer is rewritten by the next descriptor)
             continue;
         }
         if (d.n > 32) {
@@ -646,9 +654,11 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
         // ---- accumulate (Alg. 1 inner loops)
         if (warp < nocl) {
             if (neg0)
-                fwd_items<true, !REC_SMEM>(nwork, lane, accs, safe, work, roffs + warp * PK, recp, spos, sval);
+                fwd_items<true, !REC_SMEM>(nwork, lane, accs, safe, work, roffs + warp * PK, recp, spos, sval,
+                                           rec + warp * 32);
             else
-                fwd_items<false, !REC_SMEM>(nwork, lane, accs, safe, work, roffs + warp * PK, recp, spos, sval);
+                fwd_items<false, !REC_SMEM>(nwork, lane, accs, safe, work, roffs + warp * PK, recp, spos, sval,
+                                            rec + warp * 32);
         }
         __syncthreads();
     }
