@@ -4,7 +4,7 @@
 # Outputs under gpurun_out/r02b_*.
 cd ${GRAFT_REPO_ROOT:-.}
 mkdir -p gpurun_out
-T=r02b
+T=${TAG:-r02b}
 timeout 600 python bench.py > gpurun_out/${T}_bench.log 2>&1; echo "bench rc=$?"
 timeout 600 python bench.py --config c3 > gpurun_out/${T}_c3.log 2>&1; echo "c3 rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled \
