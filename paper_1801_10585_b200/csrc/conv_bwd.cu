@@ -413,8 +413,11 @@ conv_bwd_kernel(Geo gx, Geo gy, KGeo kg, BwdTile t, Keys xkeys,
         // chunk's while this chunk's blocks run
         struct Loc { int ic, xi; int64_t e; uint64_t key; float v; };
         auto locate = [&](int f, Loc& c) {
-            int ic = 0;
-            while (cpre[ic + 1] <= f) ++ic;
+            int ic = 0, hi = c_in;   // the last ic with cpre[ic] <= f (binary search, warp-uniform)
+            while (hi - ic > 1) {
+                const int mid = (ic + hi) >> 1;
+                if (cpre[mid] <= f) ic = mid; else hi = mid;
+            }
             const int s = ((f - cpre[ic]) << 5) + lane;
             c.ic = ic;
             c.xi = -1;
