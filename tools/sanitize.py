@@ -19,13 +19,15 @@ def main():
     from synth import uniform_map, sparse_filter, bias_vector, grad_values
 
     spc.load()
-    cases = [((40, 96, 64), 1, 3, 4, (3, 3, 3)),        # sampled threshold (>= 8 * P tiles)
-             ((9, 7, 11), 2, 3, 5, (3, 3, 3)),          # small, no sampling
-             ((5, 6, 7, 9), 1, 2, 3, (3, 3, 3, 3)),     # rank 4
-             ((28, 28), 2, 1, 8, (3, 3))]
-    for dims, B, ci, co, ks in cases:
+    cases = [((40, 96, 64), 1, 3, 4, (3, 3, 3), 0.6),        # sampled threshold (>= 8 * P tiles)
+             ((9, 7, 11), 2, 3, 5, (3, 3, 3), 0.6),          # small, no sampling
+             ((5, 6, 7, 9), 1, 2, 3, (3, 3, 3, 3), 0.6),     # rank 4
+             ((28, 28), 2, 1, 8, (3, 3), 0.6),
+             ((10, 12, 16), 1, 16, 16, (3, 3, 3), 1.0),      # forward records in global memory
+             ((24, 24, 16), 1, 32, 8, (3, 3, 3), 0.6)]       # backward in two passes per item
+    for dims, B, ci, co, ks, rho_f in cases:
         x = uniform_map(B, ci, dims, 0.05, 7000, values="dyadic")
-        w = sparse_filter(ci, co, ks, 0.6, 7001, values="dyadic")
+        w = sparse_filter(ci, co, ks, rho_f, 7001, values="dyadic")
         bias = torch.from_numpy(bias_vector(co, 7002, values="dyadic")).cuda()
         X = spc.SparseMap.from_arrays(x.keys, x.values, x.batch, x.channels, x.dims)
         W = spc.SparseFilter.from_arrays(w.keys, w.values, w.c_in, w.c_out, w.ksize)
