@@ -7,6 +7,7 @@ device nnz word; nothing here synchronises unless `.nnz()` / `.trimmed()` is cal
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import Optional, Sequence, Tuple
 
@@ -184,6 +185,8 @@ class FwdPlan:
         cap = C.c_int64()
         ws = C.c_size_t()
         xs, fs = x.c_struct(), w.c_struct()
+        if samples_per_pass is None and variant in ("auto", "scatter", "measure"):
+            samples_per_pass = _bounded_pass(lib, xs, fs, self.attn, self.k, x, variant)
         self.spp = samples_per_pass
         if samples_per_pass is not None:
             # batch-sliced scatter forward (spc_conv_fwd_query_pass): workspace for spp samples
@@ -221,6 +224,35 @@ class FwdPlan:
                                            C.byref(self.out), _ptr(self.ws), self.ws.numel(), _stream(stream))
             check("sparse_conv_fwd_ex", rc)
         return SparseMap(self.keys, self.vals, self.batch, self.c_out, self.dims, self.capacity, self.nnz)
+
+
+# Fraction of the free device memory the forward workspace may take before the batch is sliced
+# into passes (sparse_conv_fwd_pass); SPC_FWD_MEM_FRAC overrides.
+_WS_FRAC = float(os.environ.get("SPC_FWD_MEM_FRAC", "0.5"))
+
+
+def _bounded_pass(lib, xs, fs, attn: int, k: int, x: "SparseMap", variant: str) -> Optional[int]:
+    """None when the whole-batch forward's workspace fits _WS_FRAC of the free device memory;
+    else the largest samples-per-pass whose workspace does (at least 1)."""
+    cap, ws = C.c_int64(), C.c_size_t()
+    v = VARIANT["scatter" if variant == "measure" else variant]
+    if lib.spc_conv_fwd_query_ex(C.byref(xs), C.byref(fs), attn, k, v, C.byref(cap), C.byref(ws)) != 0:
+        return None
+    if not torch.cuda.is_available():
+        return None
+    free = torch.cuda.mem_get_info(x.values.device)[0]
+    budget = _WS_FRAC * free
+    if ws.value <= budget or x.batch <= 1:
+        return None
+    lo, hi = 1, int(x.batch) - 1   # largest spp with workspace <= budget
+    while lo < hi:
+        mid = (lo + hi + 1) // 2
+        if lib.spc_conv_fwd_query_pass(C.byref(xs), C.byref(fs), attn, k, mid, C.byref(cap), C.byref(ws)) == 0 \
+                and ws.value <= budget:
+            lo = mid
+        else:
+            hi = mid - 1
+    return lo
 
 
 _MEASURED = {}

@@ -885,6 +885,25 @@ def test_fwd_pass_matches_oracle_and_full(cuda_lib, case, attn):
     np.testing.assert_array_equal(qv.view(np.uint32), fv.view(np.uint32))
 
 
+def test_fwd_default_plan_bounds_workspace(cuda_lib, monkeypatch):
+    """With the workspace budget at ~0 the default plan slices the batch into one-sample passes
+    (ops._bounded_pass) and gives the same keys and value bits as the one-shot forward."""
+    spc = cuda_lib
+    from paper_1801_10585_b200 import ops
+    x = uniform_map(3, 2, (10, 11, 12), 0.1, 77)
+    w = sparse_filter(2, 4, (3, 3, 3), 0.5, 77)
+    bt = torch.from_numpy(bias_vector(4, 77)).cuda()
+    full = spc.sparse_conv_fwd(dev_map(spc, x), dev_filter(spc, w), bt, "magnitude", 60, variant="scatter")
+    monkeypatch.setattr(ops, "_WS_FRAC", 1e-12)
+    plan = ops.FwdPlan(dev_map(spc, x), dev_filter(spc, w), "magnitude", 60, "scatter", bt)
+    assert plan.spp == 1
+    part = plan(dev_map(spc, x), dev_filter(spc, w), bt)
+    fk, fv = (host(t) for t in full.trimmed())
+    qk, qv = (host(t) for t in part.trimmed())
+    np.testing.assert_array_equal(qk, fk)
+    np.testing.assert_array_equal(qv.view(np.uint32), fv.view(np.uint32))
+
+
 def test_fwd_pass_device_nnz_and_empty(cuda_lib):
     """Chained input (device nnz word, larger bound) and an all-empty batch through the passes."""
     spc = cuda_lib
