@@ -446,7 +446,29 @@ def roofline_for(name, ph, m, pk, src):
         out["alu"] = {"achieved_tmacs": round(macs / t / 1e12, 4), "ffma_peak_tmacs": round(ffma, 2),
                       "frac": round(macs / t / 1e12 / ffma, 4),
                       "note": "secondary: Eq. (1) MACs over the FP32 FMA peak (derived from unit counts)"}
+        sp = ncu_shared(name)
+        if sp:
+            sp["floor_wavefronts"] = int(2 * macs / 32)   # 2 words per MAC (read-modify-write), 32 per wavefront
+            out["shared_pipe"] = sp
     return out
+
+
+def ncu_shared(kernel):
+    """The binding resource of the scatter kernels: shared-memory wavefronts per launch and the
+    pipe's busy share (ncu, newest committed capture), and the algorithmic floor of the
+    read-modify-write scatter (2 words per MAC, 32 words per wavefront). Secondary to `frac`."""
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_traffic.json")), reverse=True):
+        try:
+            d = json.load(open(path))
+        except Exception:
+            continue
+        if kernel in d and "shared_wavefronts" in d[kernel]:
+            e = d[kernel]
+            return {"wavefronts": e["shared_wavefronts"], "bank_conflict_wavefronts": e.get("shared_bank_conflicts"),
+                    "pct_of_peak": e.get("shared_pipe_pct_of_peak"),
+                    "source": os.path.relpath(path, ROOT) + ":" + e["report"],
+                    "note": "secondary: the shared-memory pipe the scatter is bound by (ncu --set full)"}
+    return None
 
 
 _NCU_NAME = {"fwd_write": "stream_write", "fwd_resolve": "stream_resolve"}   # library phase -> ncu kernel

@@ -23,12 +23,24 @@ def read(rep):
     kname = vals[h.index("Kernel Name")]
     short = re.sub(r"^void |\(.*$", "", kname).replace("spc::", "")
     short = re.sub(r"<.*>", "", short).replace("_kernel", "")
-    return short, {"dram_bytes_read": get("dram__bytes_read.sum"), "dram_bytes_write": get("dram__bytes_write.sum"),
+    out = {"dram_bytes_read": get("dram__bytes_read.sum"), "dram_bytes_write": get("dram__bytes_write.sum"),
                    "traffic": get("dram__bytes_read.sum") + get("dram__bytes_write.sum"),
                    "duration_ms_ncu": float(vals[h.index("gpu__time_duration.sum")].replace(",", "")) *
                    {"us": 1e-3, "usecond": 1e-3, "ns": 1e-6, "nsecond": 1e-6}.get(
                        units[h.index("gpu__time_duration.sum")], 1.0),
                    "report": rep.split("/")[-1]}
+    # the shared-memory pipe (the binding resource of the scatter kernels): wavefronts per launch
+    # and their share of the pipe's peak over the kernel's elapsed time
+    for name, key in (("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared_wavefronts"),
+                      ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+                       "shared_pipe_pct_of_peak"),
+                      ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "shared_bank_conflicts")):
+        if name in h:
+            try:
+                out[key] = float(vals[h.index(name)].replace(",", ""))
+            except ValueError:
+                pass
+    return short, out
 
 
 if __name__ == "__main__":
