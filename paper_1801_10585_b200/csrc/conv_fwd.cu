@@ -58,17 +58,29 @@ FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_
     // round records live in shared memory when small; large filter banks (e.g. 32 x 32 x 27) are
     // read through L1 instead of being copied into every CTA
     auto rec_sm = [&](int ocg) { return nwg(ocg) * 8 <= 16 * 1024; };
-    auto need = [&](int ocg, int TY) {
+    // accumulator rows per channel: the band plus 2hy margin rows on each side that catch the
+    // updates leaving the band (margin mode), or only the band with those updates predicated off
+    // (pred mode: taller bands in the same shared memory, one compare per update)
+    auto need = [&](int ocg, int TY, bool pred) {
         // (records in global memory: a 32-record buffer per warp for the current descriptor's)
         return fwd_fixed_smem(PK, ocg, rec_sm(ocg) ? nwg(ocg) : kFwdWarps * 32) +
-               (size_t)ocg * (TY + 4 * kg.hy) * ZR * sizeof(float);
+               (size_t)ocg * (TY + (pred ? 0 : 4 * kg.hy)) * ZR * sizeof(float);
     };
     if (PK >= (1 << 13)) { t.smem = 0; return t; }                 // work descriptors hold 13-bit items
     int ocg = std::min(c_out, kFwdWarps);
-    while (ocg > 1 && need(ocg, 1) > kFwdBudget) --ocg;
-    if (need(ocg, 1) > kFwdBudget) { t.smem = 0; return t; }
-    int TYmax = 1;
-    while (TYmax < gy.Y && need(ocg, TYmax + 1) <= kFwdBudget) ++TYmax;
+    while (ocg > 1 && need(ocg, 1, true) > kFwdBudget) --ocg;
+    if (need(ocg, 1, true) > kFwdBudget) { t.smem = 0; return t; }
+    auto tymax = [&](bool pred) {
+        int v = 0;
+        while (v < gy.Y && need(ocg, v + 1, pred) <= kFwdBudget) ++v;
+        return v;
+    };
+    // pred mode only when it saves bands (measured: C4 4.33 -> 4.27 ms with 7 bands instead of
+    // 8; the C3 32 -> 64 layer keeps 2 bands either way and runs 7 % slower predicated)
+    const int tm = tymax(false), tp = tymax(true);
+    bool pred = tm < 1 || (gy.Y + tp - 1) / tp < (gy.Y + tm - 1) / tm;
+    if (const char* e = getenv("SPC_FWD_PRED")) pred = e[0] == '1' || tm < 1;
+    int TYmax = pred ? tp : tm;
     if (const char* e = getenv("SPC_FWD_TY")) TYmax = std::max(1, std::min(TYmax, atoi(e)));
     const int nty = (gy.Y + TYmax - 1) / TYmax;
     t.TY = (gy.Y + nty - 1) / nty;                                   // balanced bands
@@ -77,11 +89,12 @@ FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_
     t.n_ocg = (c_out + ocg - 1) / ocg;
     t.ZR = ZR;
     t.cz = cz;
-    t.RA = t.TY + 4 * kg.hy;
+    t.pred = pred ? 1 : 0;
+    t.RA = t.TY + (pred ? 0 : 4 * kg.hy);
     t.PK = PK;
     t.nwg_max = (int)nwg(ocg);
     t.rec_smem = rec_sm(ocg) ? 1 : 0;
-    t.smem = need(ocg, t.TY);
+    t.smem = need(ocg, t.TY, pred);
     t.fd_nty = make_fastdiv((uint32_t)t.nty);
     t.fd_X = make_fastdiv((uint32_t)gy.X);
     t.fd_Z = make_fastdiv((uint32_t)gy.Z);
@@ -370,10 +383,13 @@ __device__ __forceinline__ FwdDesc load_desc(uint32_t wdsc, int lane, uint32_t a
 // (every round offset keeps it inside the slice) and do not store. The next descriptor's
 // dependent shared loads (descriptor -> round range, entries) are issued before the current
 // descriptor's rounds run.
-template <bool NEG0, bool REGREC>
+template <bool NEG0, bool REGREC, bool PRED>
 __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, uint32_t safe, const uint32_t* work,
                                           const int* roffw, const int2* rec, const uint32_t* spos,
-                                          const float* sval, int2* wrec) {
+                                          const float* sval, int2* wrec, uint32_t slo, uint32_t slen) {
+    // a target outside the warp's band slice [slo, slo + slen) (an update from a halo input row
+    // that leaves the band) is predicated off
+    auto in_band = [&](uint32_t q) { return PRED ? (int)((q - slo) < slen) : 1; };
     if (nwork <= 0) return;
     FwdDesc nx = load_desc<REGREC>(work[0], lane, accs, safe, roffw, spos, sval, rec);
 #pragma unroll 1
@@ -395,13 +411,14 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
                     const uint32_t qa = d.aA + (uint32_t)q.x, qb = d.aB + (uint32_t)q.x;
                     const float w = __int_as_float(q.y);
                     if (NEG0) {
-                        rmw2_neg0(qa, qb, d.vA, d.vB, w, okA, okB);
+                        rmw2_neg0(qa, qb, d.vA, d.vB, w, okA & in_band(qa), okB & in_band(qb));
                     } else {
                         float oa = 0.0f, ob = 0.0f;
-                        if (okA) oa = lds_u(qa);
-                        if (okB) ob = lds_u(qb);
-                        if (okA) sts_u(qa, upd<NEG0>(oa, d.vA, w));
-                        if (okB) sts_u(qb, upd<NEG0>(ob, d.vB, w));
+                        const bool pa = okA && in_band(qa), pb = okB && in_band(qb);
+                        if (pa) oa = lds_u(qa);
+                        if (pb) ob = lds_u(qb);
+                        if (pa) sts_u(qa, upd<NEG0>(oa, d.vA, w));
+                        if (pb) sts_u(qb, upd<NEG0>(ob, d.vB, w));
                     }
 #ifndef SPC_NO_SYNCWARP
                     __syncwarp();
@@ -413,8 +430,8 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
                     const int2 q = wrec[r];
                     const uint32_t qa = d.aA + (uint32_t)q.x;
                     const float w = __int_as_float(q.y);
-                    if (NEG0) rmw1_neg0(qa, d.vA, w, okA);
-                    else if (okA) sts_u(qa, upd<NEG0>(lds_u(qa), d.vA, w));
+                    if (NEG0) rmw1_neg0(qa, d.vA, w, okA & in_band(qa));
+                    else if (okA && in_band(qa)) sts_u(qa, upd<NEG0>(lds_u(qa), d.vA, w));
 #ifndef SPC_NO_SYNCWARP
                     __syncwarp();
 #endif
@@ -431,13 +448,14 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
                 const uint32_t qa = d.aA + (uint32_t)q.x, qb = d.aB + (uint32_t)q.x;
                 const float w = __int_as_float(q.y);
                 if (NEG0) {
-                    rmw2_neg0(qa, qb, d.vA, d.vB, w, okA, okB);
+                    rmw2_neg0(qa, qb, d.vA, d.vB, w, okA & in_band(qa), okB & in_band(qb));
                 } else {
                     float oa = 0.0f, ob = 0.0f;   // idle lanes do not touch shared memory (racecheck-clean)
-                    if (okA) oa = lds_u(qa);
-                    if (okB) ob = lds_u(qb);
-                    if (okA) sts_u(qa, upd<NEG0>(oa, d.vA, w));
-                    if (okB) sts_u(qb, upd<NEG0>(ob, d.vB, w));
+                    const bool pa = okA && in_band(qa), pb = okB && in_band(qb);
+                    if (pa) oa = lds_u(qa);
+                    if (pb) ob = lds_u(qb);
+                    if (pa) sts_u(qa, upd<NEG0>(oa, d.vA, w));
+                    if (pb) sts_u(qb, upd<NEG0>(ob, d.vB, w));
                 }
 #ifndef SPC_NO_SYNCWARP
                 __syncwarp();
@@ -450,8 +468,8 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
             for (int r = d.r0; r < d.r1; ++r) {
                 const int2 qn = rec[r + 1];
                 const uint32_t qa = d.aA + (uint32_t)q.x;
-                if (NEG0) rmw1_neg0(qa, d.vA, __int_as_float(q.y), okA);
-                else if (okA) sts_u(qa, upd<NEG0>(lds_u(qa), d.vA, __int_as_float(q.y)));
+                if (NEG0) rmw1_neg0(qa, d.vA, __int_as_float(q.y), okA & in_band(qa));
+                else if (okA && in_band(qa)) sts_u(qa, upd<NEG0>(lds_u(qa), d.vA, __int_as_float(q.y)));
 #ifndef SPC_NO_SYNCWARP
                 __syncwarp();
 #endif
@@ -473,7 +491,7 @@ __device__ __forceinline__ void fwd_items(int nwork, int lane, uint32_t accs, ui
 // support entry of a failed segment as a candidate.
 constexpr int kEpiSample = 1, kEpiCand = 2, kEpiRedo = 3;
 
-template <bool REC_SMEM, int EPI>
+template <bool REC_SMEM, bool PRED, int EPI>
 __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGeo& kg, const FwdTile& t,
                                          const FwdArgs& a, int64_t bl, int tin) {
     extern __shared__ __align__(16) float smf[];
@@ -571,10 +589,11 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
     __syncthreads();
 
     const uint32_t accs = (uint32_t)__cvta_generic_to_shared(acc);
-    const uint32_t safe = (uint32_t)(2 * kg.hy * ZR + t.cz) * 4u;   // interior word of slice 0
+    const int mrow = PRED ? 0 : 2 * kg.hy;           // margin rows below the band
+    const uint32_t safe = (uint32_t)(mrow * ZR + t.cz) * 4u;   // a word of slice 0 (idle lanes never access it)
     const float invZ = 1.0f / (float)Z;
     // accumulator row of input row ylo (input row yi -> row yi - (y0 - 2hy))
-    const int arow0 = ylo - y0 + 2 * kg.hy;
+    const int arow0 = ylo - y0 + mrow;   // (pred mode: -hy for a halo below, rows below the slice)
     const bool single = total <= kStageCap;          // the usual case: one chunk, descriptors known
     for (int f0 = 0; f0 < total; f0 += kStageCap) {
         const int f1 = min(total, f0 + kStageCap);
@@ -614,7 +633,7 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
                     const uint32_t L = kw[j] - rbj[j];   // < 2^32: offset within the run
                     const uint32_t yrel = div_small(L, (uint32_t)Z, invZ);
                     const uint32_t z = L - yrel * (uint32_t)Z;
-                    spos[dj[j]] = ((yrel + (uint32_t)arow0) * (uint32_t)ZR + z + (uint32_t)t.cz) * 4u;
+                    spos[dj[j]] = (uint32_t)(((int)yrel + arow0) * ZR + (int)z + t.cz) * 4u;   // (mod 2^32)
                     sval[dj[j]] = vj[j];
                 }
             }
@@ -651,14 +670,15 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
             __syncthreads();
         }
         const int nwork = single ? wtotal : (int)misc[0];
+        const uint32_t slo = accs + (uint32_t)(warp * SL) * 4u, slen = (uint32_t)SL * 4u;   // this warp's slice
         // ---- accumulate (Alg. 1 inner loops)
         if (warp < nocl) {
             if (neg0)
-                fwd_items<true, !REC_SMEM>(nwork, lane, accs, safe, work, roffs + warp * PK, recp, spos, sval,
-                                           rec + warp * 32);
+                fwd_items<true, !REC_SMEM, PRED>(nwork, lane, accs, safe, work, roffs + warp * PK, recp, spos, sval,
+                                           rec + warp * 32, slo, slen);
             else
-                fwd_items<false, !REC_SMEM>(nwork, lane, accs, safe, work, roffs + warp * PK, recp, spos, sval,
-                                            rec + warp * 32);
+                fwd_items<false, !REC_SMEM, PRED>(nwork, lane, accs, safe, work, roffs + warp * PK, recp, spos, sval,
+                                            rec + warp * 32, slo, slen);
         }
         __syncthreads();
     }
@@ -673,7 +693,7 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
         const int64_t s = bl * c_out + oc;
         if (EPI == kEpiRedo && !a.fail[s]) return;
         const float bv = a.bias ? __ldg(&a.bias[oc]) : 0.0f;
-        const float* S = acc + warp * SL + 2 * kg.hy * ZR + t.cz;
+        const float* S = acc + warp * SL + mrow * ZR + t.cz;
         const uint32_t tl = EPI == kEpiRedo ? 0u : a.tlow[s];
         const uint32_t pbase = (uint32_t)(((int64_t)P * gy.Y + y0) * Z);
         uint32_t* cp = a.cpos + s * gy.V + pbase;
@@ -714,7 +734,7 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
         const int oc = oc0 + ocl;
         const int64_t s = bl * c_out + oc;
         const float bv = a.bias ? __ldg(&a.bias[oc]) : 0.0f;
-        const float* S = acc + ocl * SL + 2 * kg.hy * ZR + t.cz;
+        const float* S = acc + ocl * SL + mrow * ZR + t.cz;
         uint4* hist4 = (dbuf && (ocl & 1)) ? histB : histA;
         const uint32_t hist_s = (uint32_t)__cvta_generic_to_shared(hist4);
         if (a.attn == SPC_ATTN_RAW) epi_hist_rows<SPC_ATTN_RAW>(S, bv, nyr, Z, ZR, hist_s, marker);
@@ -744,28 +764,28 @@ __device__ __forceinline__ void fwd_tile(const Geo& gx, const Geo& gy, const KGe
 
 // One CTA = one tile (b, x, band, output-channel group): main pass (EPI = kEpiCand), grid
 // (B * ntile, n_ocg).
-template <bool REC_SMEM>
+template <bool REC_SMEM, bool PRED>
 __global__ void __launch_bounds__(kFwdThreads, 2) conv_fwd_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t, FwdArgs a) {
     const uint32_t tile = blockIdx.x, bl = fdiv(tile, a.fd_ntile);   // (B * ntile < 2^31)
-    fwd_tile<REC_SMEM, kEpiCand>(gx, gy, kg, t, a, bl, (int)(tile - bl * (uint32_t)a.ntile));
+    fwd_tile<REC_SMEM, PRED, kEpiCand>(gx, gy, kg, t, a, bl, (int)(tile - bl * (uint32_t)a.ntile));
 }
 
 // Sampled pass: grid (B * nsamp, n_ocg); tile j of a segment's sample = j*sp_period + sp_off.
-template <bool REC_SMEM>
+template <bool REC_SMEM, bool PRED>
 __global__ void __launch_bounds__(kFwdThreads, 2) conv_fwd_sample_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t,
                                                                          FwdArgs a) {
     const uint32_t j = blockIdx.x, bl = fdiv(j, a.fd_nsamp);
-    fwd_tile<REC_SMEM, kEpiSample>(gx, gy, kg, t, a, bl, (int)(j - bl * (uint32_t)a.nsamp) * a.sp_period + a.sp_off);
+    fwd_tile<REC_SMEM, PRED, kEpiSample>(gx, gy, kg, t, a, bl, (int)(j - bl * (uint32_t)a.nsamp) * a.sp_period + a.sp_off);
 }
 
 // Redo pass: grid (ntile, n_ocg); block t recomputes tile t of every queued sample (normally
 // none: the block exits at once).
-template <bool REC_SMEM>
+template <bool REC_SMEM, bool PRED>
 __global__ void __launch_bounds__(kFwdThreads, 2) conv_fwd_redo_kernel(Geo gx, Geo gy, KGeo kg, FwdTile t,
                                                                        FwdArgs a) {
     const int nq = *a.redo_n;
     for (int i = 0; i < nq; ++i) {
-        fwd_tile<REC_SMEM, kEpiRedo>(gx, gy, kg, t, a, a.redo_b[i], (int)blockIdx.x);
+        fwd_tile<REC_SMEM, PRED, kEpiRedo>(gx, gy, kg, t, a, a.redo_b[i], (int)blockIdx.x);
         __syncthreads();
     }
 }
@@ -1195,31 +1215,31 @@ void plan_fwd_sampling(const Geo& gy, const FwdTile& t, int attn, FwdArgs* a) {
     a->fd_nsamp = make_fastdiv((uint32_t)std::max(1, a->nsamp));
 }
 
-template <bool REC>
+template <bool REC, bool PRED>
 static cudaError_t set_fwd_smem(size_t smem) {
-    cudaError_t e = cudaFuncSetAttribute(conv_fwd_kernel<REC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(conv_fwd_kernel<REC, PRED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(conv_fwd_sample_kernel<REC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = cudaFuncSetAttribute(conv_fwd_sample_kernel<REC, PRED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(conv_fwd_redo_kernel<REC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = cudaFuncSetAttribute(conv_fwd_redo_kernel<REC, PRED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return e;
 }
 
-template <bool REC>
+template <bool REC, bool PRED>
 static void launch_fwd_passes(const Geo& gx, const Geo& gy, const KGeo& kg, const FwdTile& t, const FwdArgs& a,
                               int which, cudaStream_t s) {
     if (which == 0) {
         const dim3 grid((unsigned)(gy.B * a.nsamp), (unsigned)t.n_ocg);
         SPC_PHASE("conv_fwd_sample", s, 1);
-        conv_fwd_sample_kernel<REC><<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a);
+        conv_fwd_sample_kernel<REC, PRED><<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a);
     } else if (which == 1) {
         const dim3 grid((unsigned)(gy.B * a.ntile), (unsigned)t.n_ocg);
         SPC_PHASE("conv_fwd", s, 1);
-        conv_fwd_kernel<REC><<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a);
+        conv_fwd_kernel<REC, PRED><<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a);
     } else {
         const dim3 grid((unsigned)a.ntile, (unsigned)t.n_ocg);
         SPC_PHASE("conv_fwd_redo", s, 1);
-        conv_fwd_redo_kernel<REC><<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a);
+        conv_fwd_redo_kernel<REC, PRED><<<grid, kFwdThreads, t.smem, s>>>(gx, gy, kg, t, a);
     }
 }
 
@@ -1227,7 +1247,8 @@ cudaError_t launch_conv_fwd_stream(const Geo& gx, const Geo& gy, const KGeo& kg,
                                    const FwdArgs& a, cudaStream_t s) {
     const int64_t nseg = gy.B * gy.C;
     if (nseg == 0) return a.out_append ? cudaSuccess : cudaMemsetAsync(a.out_nnz, 0, sizeof(int64_t), s);
-    cudaError_t e = t.rec_smem ? set_fwd_smem<true>(t.smem) : set_fwd_smem<false>(t.smem);
+    cudaError_t e = t.rec_smem ? (t.pred ? set_fwd_smem<true, true>(t.smem) : set_fwd_smem<true, false>(t.smem))
+                               : (t.pred ? set_fwd_smem<false, true>(t.smem) : set_fwd_smem<false, false>(t.smem));
     if (e != cudaSuccess) return e;
     const size_t segb = sizeof(uint64_t) * (size_t)nseg;
     cudaMemsetAsync(a.seg_count, 0, segb, s);
@@ -1248,8 +1269,13 @@ cudaError_t launch_conv_fwd_stream(const Geo& gx, const Geo& gy, const KGeo& kg,
                                                           a.rnd, a.roff, a.guard);
     }
     auto passes = [&](int which) {
-        if (t.rec_smem) launch_fwd_passes<true>(gx, gy, kg, t, a, which, s);
-        else launch_fwd_passes<false>(gx, gy, kg, t, a, which, s);
+        if (t.rec_smem) {
+            if (t.pred) launch_fwd_passes<true, true>(gx, gy, kg, t, a, which, s);
+            else launch_fwd_passes<true, false>(gx, gy, kg, t, a, which, s);
+        } else {
+            if (t.pred) launch_fwd_passes<false, true>(gx, gy, kg, t, a, which, s);
+            else launch_fwd_passes<false, false>(gx, gy, kg, t, a, which, s);
+        }
     };
     if (a.nsamp > 0) {
         cudaMemsetAsync(a.hist, 0, sizeof(uint32_t) * kSelBins * (size_t)nseg, s);

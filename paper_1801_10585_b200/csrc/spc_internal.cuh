@@ -193,7 +193,8 @@ struct FwdTile {
     int TY, nty, ocg, n_ocg;
     int ZR;            // accumulator row pitch (floats)
     int cz;            // accumulator column of z = 0 (>= hz, multiple of 4)
-    int RA;            // accumulator rows per output channel: TY + 4*hy (2*hy margin rows each side)
+    int RA;            // accumulator rows per output channel: TY + 4*hy (margin mode) or TY (pred mode)
+    int pred;          // 1: no margin rows, updates leaving the band predicated off
     int PK;            // work items (ic, input plane) = c_in * kx
     int nwg_max;       // stored weights of one output-channel group (upper bound = round records)
     int rec_smem;      // 1: round records copied to shared memory; 0: read through L1
