@@ -78,12 +78,20 @@ GemmPlan plan_gemm(const Geo& gx, const Geo& gy, const KGeo& kg) {
         return g.slab_smem <= budget && room >= 2 * g.bstage_bytes;
     };
     const bool split_ok = g.Kp % 16 == 0 && !(getenv("SPC_GEMM_KSPLIT") && getenv("SPC_GEMM_KSPLIT")[0] == '0');
-    if (!(split_ok && slab_plan(2, 112 * 1024) && slab_plan(1, 200 * 1024) && g.slab_smem > 112 * 1024 &&
-          slab_plan(2, 112 * 1024)))
+    // 32+ input channels: four K parts of Kp/4 in 56 KB (four CTAs per SM, two TMEM accumulators
+    // each: the fills of three tiles overlap the MMAs of the fourth; C5 at 50 %: 2.83 -> 2.61 ms)
+    int parts_env = getenv("SPC_GEMM_PARTS") ? atoi(getenv("SPC_GEMM_PARTS")) : (g.Kp % 32 == 0 ? 4 : 0);
+    if (parts_env > 0 && g.Kp % (8 * parts_env) == 0 &&
+        slab_plan(parts_env, (size_t)(parts_env >= 4 ? 56 : parts_env >= 3 ? 75 : 112) * 1024)) {
+        // (planned)
+    } else if (!(split_ok && slab_plan(2, 112 * 1024) && slab_plan(1, 200 * 1024) && g.slab_smem > 112 * 1024 &&
+                 slab_plan(2, 112 * 1024))) {
         slab_plan(1, 200 * 1024);
+    }
     // several TMEM accumulators, offsets dealt round-robin: consecutive MMAs do not depend on
     // each other's result (summed in the epilogue)
-    g.nacc = std::max(1, std::min(4, 256 / (2 * g.Np)));
+    g.nacc = std::max(1, std::min(g.kparts >= 4 ? 2 : 4, 256 / (2 * g.Np)));   // (TMEM shared by 4 CTAs)
+    if (const char* e = getenv("SPC_GEMM_NACC")) g.nacc = std::max(1, std::min(g.nacc, atoi(e)));
     g.tcols_slab = 32;
     while (g.tcols_slab < g.nacc * 2 * g.Np) g.tcols_slab *= 2;
     g.slab = (g.slab_smem <= 200 * 1024 && g.NV * 16 < (1 << 18) && g.SZ * 16 < (1 << 18)) ? 1 : 0;
