@@ -201,7 +201,8 @@ spc_status_t fwd_plan(const spc_map_t* x, const spc_filter_t* w, spc_attn_t attn
     *gy = geo_of(x, w->c_out);
     const int64_t per = attn != SPC_ATTN_NONE ? std::min<int64_t>(k, gy->V) : gy->V;
     *cap = x->batch * w->c_out * per;
-    *t = plan_fwd_tile(*gy, *kg, (int)w->c_out, (int)w->c_in, w->nnz);
+    const double cells = (double)x->batch * (double)x->channels * (double)gx->V;
+    *t = plan_fwd_tile(*gy, *kg, (int)w->c_out, (int)w->c_in, w->nnz, cells > 0 ? (double)x->nnz / cells : 0.0);
     *gp = plan_gemm(*gx, *gy, *kg);
     const bool s_ok = t->smem != 0, g_ok = gp->ok != 0;
     if (variant == SPC_VARIANT_SCATTER) *use_gemm = 0;

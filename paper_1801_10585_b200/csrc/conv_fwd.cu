@@ -49,7 +49,7 @@ static size_t fwd_fixed_smem(int PK, int ocg, int64_t nwg) {
            8 * ((size_t)ocg * PK + (size_t)nwg + 1) + 64;
 }
 
-FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_t nw_total) {
+FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_t nw_total, double rho_in) {
     FwdTile t{};
     const int cz = ((kg.hz + 3) / 4) * 4;                         // column of z = 0 (16-byte aligned rows)
     const int ZR = (int)r4((size_t)cz + gy.Z + kg.hz);
@@ -75,10 +75,12 @@ FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_
         while (v < gy.Y && need(ocg, v + 1, pred) <= kFwdBudget) ++v;
         return v;
     };
-    // pred mode only when it saves bands (measured: C4 4.33 -> 4.27 ms with 7 bands instead of
-    // 8; the C3 32 -> 64 layer keeps 2 bands either way and runs 7 % slower predicated)
+    // pred mode only when it saves bands and the input is sparse (measured: C4 at 2 % 4.33 ->
+    // 4.28 ms, 7 bands instead of 8; at 5 % the per-update compare costs more than the band
+    // saves, 14.4 -> 14.9 ms per step; the C3 32 -> 64 layer keeps 2 bands either way and runs
+    // 7 % slower predicated). rho_in: input density (upper bound when the count is on the device)
     const int tm = tymax(false), tp = tymax(true);
-    bool pred = tm < 1 || (gy.Y + tp - 1) / tp < (gy.Y + tm - 1) / tm;
+    bool pred = tm < 1 || ((gy.Y + tp - 1) / tp < (gy.Y + tm - 1) / tm && rho_in <= 0.03);
     if (const char* e = getenv("SPC_FWD_PRED")) pred = e[0] == '1' || tm < 1;
     int TYmax = pred ? tp : tm;
     if (const char* e = getenv("SPC_FWD_TY")) TYmax = std::max(1, std::min(TYmax, atoi(e)));

@@ -202,7 +202,7 @@ struct FwdTile {
     FastDiv fd_Z;           // voxel of a band -> (row, z) in the candidate epilogue
     size_t smem;
 };
-FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_t nw_total);
+FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_t nw_total, double rho_in);
 
 // Per-segment selection state of the forward (attention) pipeline.
 struct FwdSeg {
