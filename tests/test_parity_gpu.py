@@ -759,6 +759,63 @@ def test_c4_full_size_continuous_all_samples(cuda_lib):
 
 
 @pytest.mark.slow
+def test_c3_full_size_chain_sampled(cuda_lib):
+    """BASELINE configs[2] at full size in the bench's layer chain: 64^3 surface occupancy 2 %
+    (binary), b = 32, conv 1 -> 32 (attention k = 5242) -> ReLU -> conv 32 -> 64 (attention),
+    then the backward through both layers (ReLU scatter with key-ordered sources). Dyadic weights
+    on coarse grids so that the oracle certifies the forward sums exact in fp32 (any order): two
+    sampled samples recomputed by the oracle from the original input match bit for bit in keys
+    and values of both layers; dx of the 32 -> 64 layer is exact too, dx of the first layer is
+    compared with the tolerance rule."""
+    spc = cuda_lib
+    V = 64 ** 3
+    k = int(0.02 * V)
+    x = surface_occupancy(32, 64, 0.02, SEED_BASE * 1000 + 300)
+    w1 = sparse_filter(1, 32, (3, 3, 3), 1.0, SEED_BASE + 31, values="dyadic", scale=0.25)
+    w2 = sparse_filter(32, 64, (3, 3, 3), 1.0, SEED_BASE + 32, values="dyadic4", scale=0.125)
+    b1, b2 = bias_vector(32, SEED_BASE + 31, values="dyadic"), bias_vector(64, SEED_BASE + 32, values="dyadic")
+    X = dev_map(spc, x)
+    Y1 = spc.sparse_conv_fwd(X, dev_filter(spc, w1), torch.from_numpy(b1).cuda(), "magnitude", k)
+    R1, src1 = spc.sparse_relu(Y1)
+    Y2 = spc.sparse_conv_fwd(R1, dev_filter(spc, w2), torch.from_numpy(b2).cuda(), "magnitude", k)
+    y1k, y1v = (host(t) for t in Y1.trimmed())
+    r1k, r1v = (host(t) for t in R1.trimmed())
+    y2k, y2v = (host(t) for t in Y2.trimmed())
+    y1k, r1k, y2k = y1k.view(np.uint64), r1k.view(np.uint64), y2k.view(np.uint64)
+    dy2 = grad_values(y2k.shape[0], SEED_BASE + 33, values="dyadic")
+    dR1 = spc.sparse_conv_bwd_input(R1, dev_filter(spc, w2), Y2.exact(), torch.from_numpy(dy2).cuda())
+    dY1 = spc.sparse_scatter_grad(src1, dR1, R1.nnz_bound, Y1.nnz_bound, R1.nnz_dev, sorted=True)
+    dX = spc.sparse_conv_bwd_input(X, dev_filter(spc, w1), Y1.exact(), dY1[:y1k.shape[0]])
+    gdr1, gdx = host(dR1), host(dX)
+    sl = lambda keys, b, c: slice(int(np.searchsorted(keys, np.uint64(b * c * V))),
+                                  int(np.searchsorted(keys, np.uint64((b + 1) * c * V))))
+    for b in (0, 19):
+        xs = select_samples(x, [b])
+        o1k, o1v, o1a, _ = ora.conv_fwd(xs, w1, b1, attn=ora.ATTN_MAGNITUDE, k=k, with_abs=True)
+        assert np.all(o1a * 2.0 ** 8 < 2.0 ** 24)   # exactness certificate (grid 2^-8)
+        s1 = sl(y1k, b, 32)
+        np.testing.assert_array_equal(y1k[s1] - np.uint64(b * 32 * V), o1k)
+        np.testing.assert_array_equal(y1v[s1], o1v)
+        ra = COO(1, 32, (64, 64, 64), o1k, o1v)
+        ork, orv, osrc = ora.relu(ra)
+        sr = sl(r1k, b, 32)
+        np.testing.assert_array_equal(r1k[sr] - np.uint64(b * 32 * V), ork)
+        rs = COO(1, 32, (64, 64, 64), ork, orv)
+        o2k, o2v, o2a, _ = ora.conv_fwd(rs, w2, b2, attn=ora.ATTN_MAGNITUDE, k=k, with_abs=True)
+        assert np.all(o2a * 2.0 ** 13 < 2.0 ** 24)   # (grid 2^-13)
+        s2 = sl(y2k, b, 64)
+        np.testing.assert_array_equal(y2k[s2] - np.uint64(b * 64 * V), o2k)
+        np.testing.assert_array_equal(y2v[s2], o2v)
+        odr, _, _, odra, _ = ora.conv_bwd(rs, w2, o2k, dy2[s2], with_abs=True)
+        assert np.all(odra * 2.0 ** 11 < 2.0 ** 24)
+        np.testing.assert_array_equal(gdr1[sr], odr)
+        ody1 = ora.scatter_grad(osrc, odr, o1k.shape[0])
+        odx, _, _, odxa, _ = ora.conv_bwd(xs, w1, o1k, ody1, with_abs=True)
+        sx = sl(x.keys, b, 1)
+        assert_values_close(gdx[sx], odx, odxa, f"first-layer dx, sample {b}")
+
+
+@pytest.mark.slow
 def test_c5_full_size_gemm_sampled(cuda_lib):
     """BASELINE configs[4] at full size for variant G (the tensor-core path the per-layer choice
     takes there): 64^3, b=8, 32->32, rho_d 20%, exact layer. Two sampled samples against the
