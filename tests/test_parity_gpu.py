@@ -573,14 +573,15 @@ def test_scatter_grad_sorted_parity(cuda_lib, case):
     np.testing.assert_array_equal(host(got), want)
 
 
-def test_chain_c2_like_device_nnz(cuda_lib):
-    """BASELINE configs[1] shape (smaller batch): 3 x [conv+attention -> ReLU -> maxpool2],
-    1->8->16->32, chained on the device with no host sync between layers. Dyadic values on
-    coarsening grids; the oracle certifies (sum|terms| * 2^e < 2^24) that blocks 1-2 are
-    exact in fp32 in any order, so they must match bit for bit; block 3 is compared with the
-    tolerance rule."""
+@pytest.mark.parametrize("batch", [16, pytest.param(256, marks=pytest.mark.slow)])
+def test_chain_c2_like_device_nnz(cuda_lib, batch):
+    """BASELINE configs[1] (batch 256: the full size; 16 in the quick suite): 3 x [conv+attention
+    -> ReLU -> maxpool2], 1->8->16->32, chained on the device with no host sync between layers.
+    Dyadic values on coarsening grids; the oracle certifies (sum|terms| * 2^e < 2^24) that blocks
+    1-2 are exact in fp32 in any order, so they must match bit for bit; block 3 is compared with
+    the tolerance rule."""
     spc = cuda_lib
-    x = mnist_like(16, SEED_BASE + 1, values="dyadic")
+    x = mnist_like(batch, SEED_BASE + 1, values="dyadic")
     chans = [1, 8, 16, 32]
     ks = [117, 29, 7]
     ws = [sparse_filter(1, 8, (3, 3), 1.0, 80, values="dyadic", scale=0.25),
