@@ -376,7 +376,7 @@ TopkWs carve_topk(Carver& c, const Geo& g, int64_t nnz) {
     ws.xrow = c.take<uint32_t>((size_t)nseg + 1);   // segment bounds only (no row index)
     ws.b.seg_off = c.take<uint64_t>((size_t)nseg + 1);
     ws.b.tile_start = c.take<uint32_t>((size_t)nseg + 1);
-    ws.b.hist = c.take<uint32_t>((size_t)nseg * kSelBins);
+    ws.b.hist = c.take<uint32_t>((size_t)nseg << topk_bits(nnz, nseg));
     ws.b.seg = reinterpret_cast<TkSeg*>(c.take<uint64_t>((size_t)nseg * (topk_seg_bytes() / 8)));
     ws.b.cand_cnt = c.take<uint32_t>((size_t)nseg);
     ws.b.cand = c.take<uint64_t>((size_t)std::max<int64_t>(nnz, 1));

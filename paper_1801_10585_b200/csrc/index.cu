@@ -11,25 +11,35 @@ namespace spc {
 // seg_ptr[s] = first entry whose key >= s*V, s in [0, nseg]: one binary search per segment (the
 // per-(b, c) bounds of a map without its full row index -- the standalone attention needs only
 // these).
+// One warp per bound: a 32-ary search (32 probes per step, a ballot picks the sub-range), about
+// log32(n) + 1 dependent loads instead of log2(n).
 __global__ void seg_bounds_kernel(Keys keys, const int64_t* nnz_dev, int64_t nbound, int64_t nseg, uint64_t V,
                                   uint32_t* __restrict__ seg_ptr) {
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (s > nseg) return;
     const int64_t n = load_n(nnz_dev, nbound);
     const uint64_t want = (uint64_t)s * V;
-    int64_t lo = 0, hi = n;   // first i with keys[i] >= want
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (keys[mid] < want) lo = mid + 1; else hi = mid;
+    int64_t lo = 0, hi = n;   // first i with keys[i] >= want lies in [lo, hi]
+    while (hi - lo > 32) {
+        const int64_t step = (hi - lo + 31) / 32;
+        const int64_t p = lo + (int64_t)(lane + 1) * step - 1;
+        const bool below = p < hi && keys[p] < want;
+        const int c = __popc(__ballot_sync(0xffffffffu, below));
+        const int64_t nlo = lo + (int64_t)c * step;
+        hi = min(hi, lo + (int64_t)(c + 1) * step - 1);
+        lo = nlo;
     }
-    seg_ptr[s] = (uint32_t)lo;
+    const bool below = lo + lane < hi && keys[lo + lane] < want;
+    const int c = __popc(__ballot_sync(0xffffffffu, below));
+    if (lane == 0) seg_ptr[s] = (uint32_t)(lo + c);
 }
 
 cudaError_t launch_seg_bounds(Keys keys, const int64_t* nnz_dev, int64_t nbound, int64_t nseg, int64_t V,
                               uint32_t* seg_ptr, cudaStream_t s) {
     SPC_PHASE("seg_bounds", s, 1);
-    seg_bounds_kernel<<<(unsigned)((nseg + 1 + 255) / 256), 256, 0, s>>>(keys, nnz_dev, nbound, nseg, (uint64_t)V,
-                                                                          seg_ptr);
+    seg_bounds_kernel<<<(unsigned)((32 * (nseg + 1) + 255) / 256), 256, 0, s>>>(keys, nnz_dev, nbound, nseg,
+                                                                                 (uint64_t)V, seg_ptr);
     return cudaGetLastError();
 }
 

@@ -122,12 +122,16 @@ PoolPlan plan_pool(const Geo& g, int sw, int sx, int sy, int sz) {
     p.items = g.B * g.C * (int64_t)p.PW * p.PX * p.PY * p.nzc;
     if (p.PZ <= kTileCells) {
         p.nyb = std::max(1, std::min(p.PY, kTileCells / p.PZ));
-        if ((uint64_t)p.nyb * sy * (uint64_t)g.Z < (1ull << 31)) {
+        if ((uint64_t)p.nyb * sy * (uint64_t)g.Z < (1ull << 31) && sw * sx <= 64) {   // (kMemPlanes)
             p.tiled = 1;
             p.nyt = (p.PY + p.nyb - 1) / p.nyb;
             p.mZ = ~0u / (uint32_t)g.Z;
             p.msy = ~0u / (uint32_t)sy;
             p.msz = ~0u / (uint32_t)sz;
+            auto lg = [](int64_t d) { int l = 0; while ((1ll << l) < d) ++l; return (1ll << l) == d ? l : -1; };
+            p.lZ = lg(g.Z);
+            p.lsy = lg(sy);
+            p.lsz = lg(sz);
             p.items = g.B * g.C * (int64_t)p.PW * p.PX * p.nyt;
         }
     }
@@ -168,59 +172,100 @@ __global__ void pool_bounds_kernel(Geo g, PoolPlan p, Keys keys, const int64_t* 
     bnd[i] = (uint32_t)lo;
 }
 
-template <bool LOADV, typename F>
-__device__ __forceinline__ void pool_tile_members(const Geo& g, const PoolPlan& p, Keys keys,
-                                                  const float* __restrict__ vals,
-                                                  const uint32_t* __restrict__ bnd, int64_t seg, int pw, int px,
-                                                  int ya, int yt, F f) {
-    const uint32_t Z = (uint32_t)g.Z;
-    for (int dwx = 0; dwx < p.sw * p.sx; ++dwx) {   // input planes (w, x) of the pooled plane
-        const int w = pw * p.sw + dwx / p.sx, x = px * p.sx + dwx % p.sx;
-        if (w >= g.W || x >= g.X) continue;
-        const int64_t pl = (seg * g.W + w) * g.X + x;
-        const int64_t row0 = pl * (int64_t)g.Y + ya;
-        const uint32_t e0 = bnd[pl * (p.nyt + 1) + yt], e1 = bnd[pl * (p.nyt + 1) + yt + 1];
-        const uint64_t kb = (uint64_t)row0 * Z;
-        for (uint32_t e = e0 + threadIdx.x; e < e1; e += 4 * kTileThreads) {
-            uint64_t kk[4];
-            float vv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t ee = e + (uint32_t)u * kTileThreads;
-                kk[u] = ee < e1 ? keys[ee] : kb;
-                vv[u] = (LOADV && ee < e1) ? vals[ee] : 0.0f;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t ee = e + (uint32_t)u * kTileThreads;
-                if (ee < e1) {
-                    const uint32_t rel = (uint32_t)(kk[u] - kb);
-                    const uint32_t yy = udiv(rel, Z, p.mZ), zz = rel - yy * Z;
-                    f((int)udiv(yy, (uint32_t)p.sy, p.msy) * p.PZ + (int)udiv(zz, (uint32_t)p.sz, p.msz), ee, vv[u]);
-                }
-            }
-        }
-    }
-}
-
 struct PoolTileId {
     int64_t seg;
     int pw, px, py0, npy, ya, yb, yt;
 };
 __device__ __forceinline__ PoolTileId pool_tile_id(const Geo& g, const PoolPlan& p, int64_t tile) {
-    PoolTileId t;
-    const int yt = (int)(tile % p.nyt);
-    int64_t r = tile / p.nyt;
-    t.px = (int)(r % p.PX);
-    r /= p.PX;
-    t.pw = (int)(r % p.PW);
-    t.seg = r / p.PW;
-    t.yt = yt;
-    t.py0 = yt * p.nyb;
+    PoolTileId t;   // (tile < 2^31: a grid index; 32-bit divisions)
+    const uint32_t tl = (uint32_t)tile;
+    const uint32_t r0 = tl / (uint32_t)p.nyt, yt = tl - r0 * (uint32_t)p.nyt;
+    const uint32_t r1 = r0 / (uint32_t)p.PX;
+    t.px = (int)(r0 - r1 * (uint32_t)p.PX);
+    const uint32_t r2 = r1 / (uint32_t)p.PW;
+    t.pw = (int)(r1 - r2 * (uint32_t)p.PW);
+    t.seg = (int64_t)r2;
+    t.yt = (int)yt;
+    t.py0 = t.yt * p.nyb;
     t.npy = min(p.nyb, p.PY - t.py0);
     t.ya = t.py0 * p.sy;
     t.yb = min((t.py0 + t.npy) * p.sy, g.Y);
     return t;
+}
+
+
+// Member entries of a tile: the runs of the sw * sx input planes (w, x) (band bounds from
+// pool_bounds_kernel) as one list. pool_tile_runs fills the shared run table (starts, prefix,
+// first keys) and returns the list length; pool_round loads up to kMemU list positions per
+// thread (b0 + u * blockDim.x), all loads in flight before any is used, and gives each its
+// pooled cell (-1: none), entry index and value (loaded only when LOADV).
+constexpr int kMemU = 8;
+constexpr int kMemPlanes = 64;   // (plan_pool's tile-form limit on sw * sx)
+struct PoolRuns {
+    uint32_t rs[kMemPlanes], rp[kMemPlanes + 1];
+    unsigned long long rk[kMemPlanes];
+};
+
+__device__ __forceinline__ uint32_t pool_tile_runs(const Geo& g, const PoolPlan& p, const uint32_t* __restrict__ bnd,
+                                                   const PoolTileId& t, PoolRuns& R) {
+    const int np = p.sw * p.sx;
+    const int tid = threadIdx.x;
+    if (tid < np) {
+        const int w = t.pw * p.sw + tid / p.sx, x = t.px * p.sx + tid % p.sx;
+        uint32_t e0 = 0u, e1 = 0u;
+        unsigned long long kb = 0ull;
+        if (w < g.W && x < g.X) {
+            const int64_t pl = (t.seg * g.W + w) * g.X + x;
+            e0 = bnd[pl * (p.nyt + 1) + t.yt];
+            e1 = bnd[pl * (p.nyt + 1) + t.yt + 1];
+            kb = (unsigned long long)(pl * (int64_t)g.Y + t.ya) * (uint32_t)g.Z;
+        }
+        R.rs[tid] = e0;
+        R.rp[tid + 1] = e1 - e0;
+        R.rk[tid] = kb;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        R.rp[0] = 0u;
+        for (int i = 1; i <= np; ++i) R.rp[i] += R.rp[i - 1];
+    }
+    __syncthreads();
+    return R.rp[np];
+}
+
+template <bool LOADV>
+__device__ __forceinline__ void pool_round(const Geo& g, const PoolPlan& p, Keys keys, const float* __restrict__ vals,
+                                           const PoolRuns& R, uint32_t total, uint32_t b0, int (&cell)[kMemU],
+                                           uint32_t (&ee)[kMemU], float (&vv)[kMemU]) {
+    const uint32_t Z = (uint32_t)g.Z;
+    uint64_t kk[kMemU];
+    int rr[kMemU];
+    int r = 0;   // (a thread's list positions increase with u: the run search continues)
+#pragma unroll
+    for (int u = 0; u < kMemU; ++u) {
+        const uint32_t q = b0 + (uint32_t)u * blockDim.x;
+        rr[u] = -1;
+        kk[u] = 0ull;
+        vv[u] = 0.0f;
+        ee[u] = 0u;
+        if (q < total) {
+            while (R.rp[r + 1] <= q) ++r;
+            rr[u] = r;
+            ee[u] = R.rs[r] + (q - R.rp[r]);
+            kk[u] = keys[ee[u]];
+            if (LOADV) vv[u] = vals[ee[u]];
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kMemU; ++u) {
+        cell[u] = -1;
+        if (rr[u] < 0) continue;
+        const uint32_t rel = (uint32_t)(kk[u] - R.rk[rr[u]]);
+        const uint32_t yy = p.lZ >= 0 ? rel >> p.lZ : udiv(rel, Z, p.mZ), zz = rel - yy * Z;
+        const uint32_t cy = p.lsy >= 0 ? yy >> p.lsy : udiv(yy, (uint32_t)p.sy, p.msy);
+        const uint32_t cz = p.lsz >= 0 ? zz >> p.lsz : udiv(zz, (uint32_t)p.sz, p.msz);
+        cell[u] = (int)cy * p.PZ + (int)cz;
+    }
 }
 
 // count pass: occupied clusters of the tile (a 4096-bit occupancy mask)
@@ -229,44 +274,69 @@ pool_tile_count_kernel(Geo g, PoolPlan p, Keys keys, const uint32_t* __restrict_
                        uint32_t* __restrict__ item_cnt) {
     __shared__ uint32_t occ[kTileCells / 32];
     __shared__ uint32_t sm[33];
+    __shared__ PoolRuns R;
     const PoolTileId t = pool_tile_id(g, p, blockIdx.x);
     if (threadIdx.x < kTileCells / 32) occ[threadIdx.x] = 0u;
-    __syncthreads();
-    pool_tile_members<false>(g, p, keys, nullptr, row_ptr, t.seg, t.pw, t.px, t.ya, t.yt, [&](int cell, uint32_t, float) {
-        atomicOr(&occ[cell >> 5], 1u << (cell & 31));
-    });
+    const uint32_t total = pool_tile_runs(g, p, row_ptr, t, R);
+    for (uint32_t b0 = threadIdx.x; b0 < total; b0 += kMemU * kTileThreads) {
+        int cell[kMemU];
+        uint32_t ee[kMemU];
+        float vv[kMemU];
+        pool_round<false>(g, p, keys, nullptr, R, total, b0, cell, ee, vv);
+#pragma unroll
+        for (int u = 0; u < kMemU; ++u)
+            if (cell[u] >= 0) atomicOr(&occ[cell[u] >> 5], 1u << (cell[u] & 31));
+    }
     __syncthreads();
     const uint32_t c = threadIdx.x < kTileCells / 32 ? (uint32_t)__popc(occ[threadIdx.x]) : 0u;
     const uint32_t tot = block_sum(c, sm);
     if (threadIdx.x == 0) item_cnt[blockIdx.x] = tot;
 }
 
-// write pass: per cluster the max of (orderable(value) << 32 | ~entry) -- the maximum, ties to
-// the smaller key (reading R8) -- in one 64-bit shared atomic (0 = empty: orderable() is never
-// 0); the occupied clusters are listed in cell order from the occupancy mask (one scan over its
-// 128 words) and written with coalesced stores.
-__global__ void __launch_bounds__(kTileThreads)
-pool_tile_write_kernel(Geo g, PoolPlan p, Keys keys, const float* __restrict__ vals,
-                       const uint32_t* __restrict__ row_ptr, const uint64_t* __restrict__ item_off,
-                       KeysOut ok, float* __restrict__ ov, int64_t* __restrict__ oarg) {
-    __shared__ __align__(16) unsigned long long best[kTileCells];
-    __shared__ uint32_t occ[kTileCells / 32];
-    __shared__ uint16_t cells[kTileCells];
-    __shared__ uint32_t wsum[4];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const PoolTileId t = pool_tile_id(g, p, blockIdx.x);
-    uint4* b4 = reinterpret_cast<uint4*>(best);
+// The reduction of a tile into its clusters: the maximum's order-preserving code per cluster by
+// a native 32-bit shared atomicMax, then -- after a barrier -- the smallest entry index among
+// the members that reached it by atomicMin (ties to the smaller key, reading R8). (A single
+// 64-bit max of (code << 32 | ~entry) compiles to a CAS loop on shared memory.) One round of up
+// to kMemU * 256 members keeps them in registers across the barrier; larger tiles reload.
+__device__ __forceinline__ void pool_tile_reduce(const Geo& g, const PoolPlan& p, Keys keys,
+                                                 const float* __restrict__ vals, const PoolRuns& R, uint32_t total,
+                                                 uint32_t* bval, uint32_t* bidx, uint32_t* occ) {
+    int cell[kMemU];
+    uint32_t ee[kMemU];
+    float vv[kMemU];
+    const bool one = total <= (uint32_t)(kMemU * kTileThreads);
+    for (uint32_t b0 = threadIdx.x; b0 < total; b0 += kMemU * kTileThreads) {
+        pool_round<true>(g, p, keys, vals, R, total, b0, cell, ee, vv);
 #pragma unroll
-    for (int j = 0; j < kTileCells / 2 / kTileThreads; ++j) b4[tid + kTileThreads * j] = make_uint4(0u, 0u, 0u, 0u);
-    if (tid < kTileCells / 32) occ[tid] = 0u;
+        for (int u = 0; u < kMemU; ++u)
+            if (cell[u] >= 0) {
+                atomicMax(&bval[cell[u]], orderable(vv[u]));
+                atomicOr(&occ[cell[u] >> 5], 1u << (cell[u] & 31));
+            }
+    }
     __syncthreads();
-    pool_tile_members<true>(g, p, keys, vals, row_ptr, t.seg, t.pw, t.px, t.ya, t.yt, [&](int cell, uint32_t e, float v) {
-        atomicMax(&best[cell], ((unsigned long long)orderable(v) << 32) | (unsigned long long)(~e));
-        atomicOr(&occ[cell >> 5], 1u << (cell & 31));
-    });
+    if (one) {
+        if (threadIdx.x < total) {
+#pragma unroll
+            for (int u = 0; u < kMemU; ++u)
+                if (cell[u] >= 0 && bval[cell[u]] == orderable(vv[u])) atomicMin(&bidx[cell[u]], ee[u]);
+        }
+    } else {
+        for (uint32_t b0 = threadIdx.x; b0 < total; b0 += kMemU * kTileThreads) {
+            pool_round<true>(g, p, keys, vals, R, total, b0, cell, ee, vv);
+#pragma unroll
+            for (int u = 0; u < kMemU; ++u)
+                if (cell[u] >= 0 && bval[cell[u]] == orderable(vv[u])) atomicMin(&bidx[cell[u]], ee[u]);
+        }
+    }
     __syncthreads();
-    // threads 0..127 own one mask word each: exclusive scan of the popcounts, then the word's
-    // clusters are listed in order
+}
+
+// the occupied clusters of the tile in cell order from the occupancy mask (threads 0..127 own
+// one mask word each: exclusive scan of the popcounts, then the word's clusters are listed);
+// returns the tile's cluster count
+__device__ __forceinline__ uint32_t pool_tile_list(const uint32_t* occ, uint16_t* cells, uint32_t* wsum) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint32_t w = 0, c = 0, pre = 0;
     if (warp < 4) {
         w = occ[tid];
@@ -275,7 +345,6 @@ pool_tile_write_kernel(Geo g, PoolPlan p, Keys keys, const float* __restrict__ v
         if (lane == 31) wsum[warp] = pre + c;
     }
     __syncthreads();
-    const uint32_t tot = wsum[0] + wsum[1] + wsum[2] + wsum[3];
     if (warp < 4) {
         for (int q = 0; q < warp; ++q) pre += wsum[q];
         while (w) {
@@ -284,20 +353,56 @@ pool_tile_write_kernel(Geo g, PoolPlan p, Keys keys, const float* __restrict__ v
             cells[pre++] = (uint16_t)(tid * 32 + bit);
         }
     }
-    __syncthreads();
-    const uint64_t o0 = item_off[blockIdx.x];
+    return wsum[0] + wsum[1] + wsum[2] + wsum[3];
+}
+
+// write of the tile's clusters at output offset o0 with coalesced stores: the maximum's value
+// from its order-preserving code; +-0 (the code cannot tell them apart) from the entry itself
+__device__ __forceinline__ void pool_tile_out(const PoolPlan& p, const PoolTileId& t, const float* __restrict__ vals,
+                                              const uint32_t* bval, const uint32_t* bidx, const uint16_t* cells,
+                                              uint32_t tot, uint64_t o0, KeysOut ok, float* __restrict__ ov,
+                                              int64_t* __restrict__ oarg) {
     const uint64_t pbase = ((uint64_t)((t.seg * p.PW + t.pw) * p.PX + t.px) * p.PY + t.py0) * (uint64_t)p.PZ;
-    for (uint32_t q = tid; q < tot; q += kTileThreads) {
+    for (uint32_t q = threadIdx.x; q < tot; q += kTileThreads) {
         const uint32_t cell = cells[q];
-        const unsigned long long bst = best[cell];
-        const uint32_t a = ~(uint32_t)bst;
-        // the maximum's value from its order-preserving code; +-0 (the code cannot tell them
-        // apart) from the entry itself
-        const float mv = from_orderable((uint32_t)(bst >> 32));
+        const uint32_t a = bidx[cell];
+        const float mv = from_orderable(bval[cell]);
         ok.put(o0 + q, pbase + cell);
         ov[o0 + q] = mv != 0.0f ? mv : vals[a];
         if (oarg) oarg[o0 + q] = a;
     }
+}
+
+__device__ __forceinline__ void pool_tile_init(uint32_t* bval, uint32_t* bidx, uint32_t* occ) {
+    const int tid = threadIdx.x;
+    uint4* v4 = reinterpret_cast<uint4*>(bval);
+    uint4* i4 = reinterpret_cast<uint4*>(bidx);
+#pragma unroll
+    for (int j = 0; j < kTileCells / 4 / kTileThreads; ++j) {
+        v4[tid + kTileThreads * j] = make_uint4(0u, 0u, 0u, 0u);
+        i4[tid + kTileThreads * j] = make_uint4(~0u, ~0u, ~0u, ~0u);
+    }
+    if (tid < kTileCells / 32) occ[tid] = 0u;
+}
+
+// write pass (after the count pass and the scan of the tile counts)
+__global__ void __launch_bounds__(kTileThreads)
+pool_tile_write_kernel(Geo g, PoolPlan p, Keys keys, const float* __restrict__ vals,
+                       const uint32_t* __restrict__ row_ptr, const uint64_t* __restrict__ item_off,
+                       KeysOut ok, float* __restrict__ ov, int64_t* __restrict__ oarg) {
+    __shared__ __align__(16) uint32_t bval[kTileCells];
+    __shared__ __align__(16) uint32_t bidx[kTileCells];
+    __shared__ uint32_t occ[kTileCells / 32];
+    __shared__ uint16_t cells[kTileCells];
+    __shared__ uint32_t wsum[4];
+    __shared__ PoolRuns R;
+    const PoolTileId t = pool_tile_id(g, p, blockIdx.x);
+    pool_tile_init(bval, bidx, occ);
+    const uint32_t total = pool_tile_runs(g, p, row_ptr, t, R);
+    pool_tile_reduce(g, p, keys, vals, R, total, bval, bidx, occ);
+    const uint32_t tot = pool_tile_list(occ, cells, wsum);
+    __syncthreads();
+    pool_tile_out(p, t, vals, bval, bidx, cells, tot, item_off[blockIdx.x], ok, ov, oarg);
 }
 
 template <bool WRITE>

@@ -6,7 +6,8 @@
 // Streamed over tiles of kTkTile entries (a tile never spans two segments), so every pass runs
 // on the whole GPU whatever the number and size of the segments:
 //   plan:    per segment its kept count min(n, k) -> output offsets, and its first tile;
-//   hist:    per tile an 11-bit histogram of the top score digit, added to the segment's;
+//   hist:    per tile a histogram of the top score digit (13 bits when the segments are large
+//            enough to amortise 8192 bins, else 11), added to the segment's;
 //   find:    per segment the digit B1 holding the k-th largest score; the whole bucket is kept
 //            when it holds exactly the entries still needed (mode 1), else it is resolved
 //            exactly (mode 2); segments with n <= k keep everything (mode 0);
@@ -30,7 +31,7 @@ constexpr uint32_t kTkSmemCand = 12288;               // candidates selected in 
 
 struct TkSeg {
     uint64_t kstar;    // mode 2: keep composite >= kstar within bucket b1
-    uint32_t b1;       // threshold digit (score >> 21)
+    uint32_t b1;       // threshold digit (score >> (32 - bits))
     uint32_t mode;     // 0 keep all, 1 keep digit >= b1, 2 keep digit > b1 or composite >= kstar
     uint32_t need;     // mode 2: entries to take from bucket b1
     uint32_t pad;
@@ -38,6 +39,10 @@ struct TkSeg {
 
 size_t topk_tiles_bound(int64_t nnz, int64_t nseg) { return (size_t)(nnz / kTkTile + nseg + 1); }
 size_t topk_seg_bytes() { return sizeof(TkSeg); }
+constexpr int kTkMaxBins = 8192;
+// 13-bit first digit (1/16 of the 11-bit bucket: fewer candidates, a shorter select) when the
+// per-segment histograms stay small next to the data (>= 32 Ki entries per segment on average)
+int topk_bits(int64_t nnz, int64_t nseg) { return nseg * (int64_t)kTkMaxBins * 4 <= nnz ? 13 : 11; }
 
 __device__ __forceinline__ uint64_t tk_comp(uint32_t sc, uint32_t local) {
     return ((uint64_t)sc << 32) | (uint64_t)(0xffffffffu - local);
@@ -99,36 +104,76 @@ __device__ __forceinline__ TkTile tk_tile(const uint32_t* seg_lo, const uint32_t
     return r;
 }
 
+// A block takes kTkHistTiles consecutive tiles (the histogram's zeroing and flush amortised over
+// them), flushing into the segment's histogram whenever the segment changes; the next tile's
+// loads are issued before the current one's bins are updated.
+constexpr int kTkHistTiles = 4;
 __global__ void __launch_bounds__(kTkThreads) topk_hist_kernel(const float* __restrict__ vals,
                                                                const uint32_t* __restrict__ seg_lo,
                                                                const uint32_t* __restrict__ tile_start,
                                                                const uint32_t* __restrict__ tile_seg, int64_t nseg,
-                                                               int attn, int64_t k, uint32_t* __restrict__ hist) {
-    __shared__ uint32_t h[kSelBins];
-    const TkTile tl = tk_tile(seg_lo, tile_start, tile_seg, nseg, blockIdx.x);
-    if (!tl.ok) return;
-    if ((int64_t)(__ldg(&seg_lo[tl.s + 1]) - tl.seg0) <= k) return;   // keep-all segment
-    for (int i = threadIdx.x; i < kSelBins; i += kTkThreads) h[i] = 0u;
+                                                               int attn, int64_t k, int bits,
+                                                               uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[kTkMaxBins];
+    const int nb = 1 << bits, sh = 32 - bits;
+    for (int i = threadIdx.x; i < nb; i += kTkThreads) h[i] = 0u;
+    int64_t cur = -1;   // segment whose counts the shared histogram holds
+    auto flush = [&]() {
+        __syncthreads();
+        uint32_t* gh = hist + (cur << bits);
+        for (int i = threadIdx.x; i < nb; i += kTkThreads) {
+            const uint32_t v = h[i];
+            if (v) {
+                atomicAdd(&gh[i], v);
+                h[i] = 0u;
+            }
+        }
+        __syncthreads();
+    };
+    const uint32_t t0 = blockIdx.x * kTkHistTiles;
     uint32_t b[kTkItems];
+    TkTile tl = tk_tile(seg_lo, tile_start, tile_seg, nseg, t0);
+    auto load = [&](const TkTile& q, bool keep_all) {
 #pragma unroll
-    for (int u = 0; u < kTkItems; ++u) {
-        const uint32_t i = tl.lo + (uint32_t)(u * kTkThreads) + threadIdx.x;
-        b[u] = i < tl.hi ? __float_as_uint(__ldg(&vals[i])) : 0u;
-    }
+        for (int u = 0; u < kTkItems; ++u) {
+            const uint32_t i = q.lo + (uint32_t)(u * kTkThreads) + threadIdx.x;
+            b[u] = (!keep_all && i < q.hi) ? __float_as_uint(__ldg(&vals[i])) : 0u;
+        }
+    };
+    bool ka = tl.ok && (int64_t)(__ldg(&seg_lo[tl.s + 1]) - tl.seg0) <= k;   // keep-all segment: no histogram
+    if (tl.ok) load(tl, ka);
     __syncthreads();
+    for (int tt = 0; tt < kTkHistTiles && tl.ok; ++tt) {
+        if (!ka && tl.s != cur) {
+            if (cur >= 0) flush();
+            cur = tl.s;
+        }
+        uint32_t sc[kTkItems];
 #pragma unroll
-    for (int u = 0; u < kTkItems; ++u) {
-        const uint32_t i = tl.lo + (uint32_t)(u * kTkThreads) + threadIdx.x;
-        if (i < tl.hi) atomicAdd(&h[score_bits(b[u], attn) >> 21], 1u);
+        for (int u = 0; u < kTkItems; ++u) sc[u] = score_bits(b[u], attn);
+        const TkTile cu = tl;
+        const bool cka = ka;
+        if (tt + 1 < kTkHistTiles) {   // next tile's loads in flight
+            tl = tk_tile(seg_lo, tile_start, tile_seg, nseg, t0 + tt + 1);
+            ka = tl.ok && (int64_t)(__ldg(&seg_lo[tl.s + 1]) - tl.seg0) <= k;
+            if (tl.ok) load(tl, ka);
+        } else {
+            tl.ok = false;
+        }
+        if (!cka) {
+#pragma unroll
+            for (int u = 0; u < kTkItems; ++u) {
+                const uint32_t i = cu.lo + (uint32_t)(u * kTkThreads) + threadIdx.x;
+                if (i < cu.hi) atomicAdd(&h[sc[u] >> sh], 1u);
+            }
+        }
     }
-    __syncthreads();
-    uint32_t* gh = hist + tl.s * kSelBins;
-    for (int i = threadIdx.x; i < kSelBins; i += kTkThreads)
-        if (h[i]) atomicAdd(&gh[i], h[i]);
+    if (cur >= 0) flush();
 }
 
-__global__ void topk_find_kernel(const uint32_t* __restrict__ seg_lo, int64_t k, const uint32_t* __restrict__ hist,
-                                 TkSeg* __restrict__ seg, uint32_t* __restrict__ cand_cnt) {
+__global__ void topk_find_kernel(const uint32_t* __restrict__ seg_lo, int64_t k, int bits,
+                                 const uint32_t* __restrict__ hist, TkSeg* __restrict__ seg,
+                                 uint32_t* __restrict__ cand_cnt) {
     __shared__ uint32_t sm[33];
     const int64_t s = blockIdx.x;
     const uint64_t n = (uint64_t)(seg_lo[s + 1] - seg_lo[s]);
@@ -141,16 +186,20 @@ __global__ void topk_find_kernel(const uint32_t* __restrict__ seg_lo, int64_t k,
         }
         return;
     }
-    const uint32_t* h = hist + s * kSelBins;
-    constexpr int per = kSelBins / 256;   // blockDim 256: bins from the top, per thread a stripe
+    const int nb = 1 << bits;
+    __shared__ uint32_t h[kTkMaxBins];   // the segment's histogram, staged with coalesced loads
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) h[i] = hist[(s << bits) + i];
+    __syncthreads();
+    const int per = nb / 256;   // blockDim 256: bins from the top, per thread a stripe
     uint32_t own = 0;
-    for (int q = 0; q < per; ++q) own += h[kSelBins - 1 - threadIdx.x * per - q];
+    for (int q = 0; q < per; ++q)   // (rotated start: the 32 lanes' reads hit distinct banks)
+        own += h[nb - 1 - threadIdx.x * per - ((q + (int)threadIdx.x) & (per - 1))];
     uint32_t tot;
     const uint32_t before = block_excl_scan(own, sm, &tot);
     if (before < (uint32_t)k && before + own >= (uint32_t)k) {
         uint32_t cum = before;
         for (int q = 0; q < per; ++q) {
-            const int bin = kSelBins - 1 - threadIdx.x * per - q;
+            const int bin = nb - 1 - threadIdx.x * per - q;
             if (cum + h[bin] >= (uint32_t)k) {
                 TkSeg st{};
                 st.b1 = (uint32_t)bin;
@@ -169,7 +218,8 @@ __global__ void __launch_bounds__(kTkThreads) topk_collect_kernel(const float* _
                                                                   const uint32_t* __restrict__ seg_lo,
                                                                   const uint32_t* __restrict__ tile_start,
                                                                   const uint32_t* __restrict__ tile_seg,
-                                                                  int64_t nseg, int attn, const TkSeg* __restrict__ seg,
+                                                                  int64_t nseg, int attn, int bits,
+                                                                  const TkSeg* __restrict__ seg,
                                                                   uint64_t* __restrict__ cand,
                                                                   uint32_t* __restrict__ cand_cnt,
                                                                   uint32_t* __restrict__ tile_def) {
@@ -189,14 +239,20 @@ __global__ void __launch_bounds__(kTkThreads) topk_collect_kernel(const float* _
     }
     // count first, one atomic per tile for the tile's slots in the segment's candidate list
     // (the list is unordered: the select does not care), then write
+    // kept for sure: score >= ldef (digit above b1, or b1 itself in mode 1); candidates (mode
+    // 2): score - cb < wb (digit b1). Scores are compared directly, no digit extraction.
+    const int sh = 32 - bits;
+    const uint64_t ldef64 = (uint64_t)(st.mode == 1u ? st.b1 : st.b1 + 1u) << sh;
+    const bool none_above = ldef64 > 0xffffffffull;
+    const uint32_t ldef = (uint32_t)ldef64, cb = st.b1 << sh, wb = st.mode == 2u ? 1u << sh : 0u;
+    const uint32_t nin = tl.hi - tl.lo;
     uint32_t def = 0, nc = 0, cm = 0;
 #pragma unroll
     for (int u = 0; u < kTkItems; ++u) {
-        const uint32_t i = tl.lo + (uint32_t)(u * kTkThreads) + threadIdx.x;
-        const bool in = i < tl.hi;
-        const uint32_t d = score_bits(b[u], attn) >> 21;
-        def += (in && (d > st.b1 || (st.mode == 1u && d == st.b1))) ? 1u : 0u;
-        const bool c = in && st.mode == 2u && d == st.b1;
+        const bool in = (uint32_t)(u * kTkThreads) + threadIdx.x < nin;
+        const uint32_t sc = score_bits(b[u], attn);
+        def += (in && sc >= ldef && !none_above) ? 1u : 0u;
+        const bool c = in && (sc - cb) < wb;
         cm |= (c ? 1u : 0u) << u;
         nc += c ? 1u : 0u;
     }
@@ -280,7 +336,7 @@ __device__ uint64_t tk_select(const uint64_t* p, uint32_t n, uint32_t need, int 
 // per segment: kstar (mode 2), the selected candidates per tile, then the exclusive output
 // offsets of the segment's tiles
 constexpr int kTkSelThreads = 512;
-__global__ void __launch_bounds__(kTkSelThreads) topk_select_kernel(const uint32_t* __restrict__ seg_lo,
+__global__ void __launch_bounds__(kTkSelThreads) topk_select_kernel(int bits, const uint32_t* __restrict__ seg_lo,
                                                                     const uint32_t* __restrict__ tile_start,
                                                                     const uint64_t* __restrict__ seg_off,
                                                                     TkSeg* __restrict__ seg,
@@ -305,9 +361,9 @@ __global__ void __launch_bounds__(kTkSelThreads) topk_select_kernel(const uint32
         if (n <= kTkSmemCand) {
             for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) keys[i] = cs[i];
             __syncthreads();
-            kst = tk_select(keys, n, st.need, 53, h, sh, &shk);   // (score >> 21 == b1: bits 53.. fixed)
+            kst = tk_select(keys, n, st.need, 64 - bits, h, sh, &shk);   // (digit == b1: bits 64-bits.. fixed)
         } else {
-            kst = tk_select(cs, n, st.need, 53, h, sh, &shk);   // (massive ties: the candidates stay in HBM)
+            kst = tk_select(cs, n, st.need, 64 - bits, h, sh, &shk);   // (massive ties: the candidates stay in HBM)
         }
         for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
             const uint64_t c = n <= kTkSmemCand ? keys[i] : cs[i];
@@ -340,7 +396,7 @@ __global__ void __launch_bounds__(kTkWThreads, 2) topk_write_kernel(Keys keys, c
                                                                     const uint32_t* __restrict__ seg_lo,
                                                                     const uint32_t* __restrict__ tile_start,
                                                                     const uint32_t* __restrict__ tile_seg, int64_t nseg,
-                                                                    int attn, const TkSeg* __restrict__ seg,
+                                                                    int attn, int bits, const TkSeg* __restrict__ seg,
                                                                     const uint64_t* __restrict__ tile_off, KeysOut ok,
                                                                     float* __restrict__ ov, int64_t* __restrict__ osrc) {
     __shared__ uint32_t wc[kTkWThreads / 32];
@@ -364,7 +420,7 @@ __global__ void __launch_bounds__(kTkWThreads, 2) topk_write_kernel(Keys keys, c
     for (int u = 0; u < kTkWItems; ++u) {
         const uint32_t i = w0 + 32u * u + lane;
         const uint32_t sc = score_bits(b[u], attn);
-        const uint32_t d = sc >> 21;
+        const uint32_t d = sc >> (32 - bits);
         const bool keep = i < tl.hi && (st.mode == 0u || d > st.b1 || (d == st.b1 && (st.mode == 1u ||
                                                                                      tk_comp(sc, i - tl.seg0) >= st.kstar)));
         m[u] = __ballot_sync(kFull, keep);
@@ -393,7 +449,8 @@ cudaError_t launch_topk(Keys keys, const float* vals, const uint32_t* seg_lo, in
                         int64_t* out_src, int64_t* out_nnz, cudaStream_t s) {
     if (nseg == 0) return cudaMemsetAsync(out_nnz, 0, sizeof(int64_t), s);
     const unsigned tiles = (unsigned)topk_tiles_bound(nnz_bound, nseg);
-    cudaError_t e = cudaMemsetAsync(w.hist, 0, sizeof(uint32_t) * kSelBins * (size_t)nseg, s);
+    const int bits = topk_bits(nnz_bound, nseg);
+    cudaError_t e = cudaMemsetAsync(w.hist, 0, sizeof(uint32_t) * ((size_t)nseg << bits), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(w.tile_sel, 0, sizeof(uint32_t) * (size_t)tiles, s);
     if (e != cudaSuccess) return e;
     { SPC_PHASE("topk_plan", s, 1); topk_plan_kernel<<<1, 1024, 0, s>>>(seg_lo, nseg, k, w.seg_off, w.tile_start, out_nnz); }
@@ -403,12 +460,12 @@ cudaError_t launch_topk(Keys keys, const float* vals, const uint32_t* seg_lo, in
     }
     {
         SPC_PHASE("topk_hist", s, 1);
-        topk_hist_kernel<<<tiles, kTkThreads, 0, s>>>(vals, seg_lo, w.tile_start, w.tile_seg, nseg, attn, k, w.hist);
+        topk_hist_kernel<<<(tiles + kTkHistTiles - 1) / kTkHistTiles, kTkThreads, 0, s>>>(vals, seg_lo, w.tile_start, w.tile_seg, nseg, attn, k, bits, w.hist);
     }
-    { SPC_PHASE("topk_find", s, 1); topk_find_kernel<<<(unsigned)nseg, 256, 0, s>>>(seg_lo, k, w.hist, w.seg, w.cand_cnt); }
+    { SPC_PHASE("topk_find", s, 1); topk_find_kernel<<<(unsigned)nseg, 256, 0, s>>>(seg_lo, k, bits, w.hist, w.seg, w.cand_cnt); }
     {
         SPC_PHASE("topk_collect", s, 1);
-        topk_collect_kernel<<<tiles, kTkThreads, 0, s>>>(vals, seg_lo, w.tile_start, w.tile_seg, nseg, attn, w.seg, w.cand,
+        topk_collect_kernel<<<tiles, kTkThreads, 0, s>>>(vals, seg_lo, w.tile_start, w.tile_seg, nseg, attn, bits, w.seg, w.cand,
                                                          w.cand_cnt, w.tile_def);
     }
     {
@@ -416,12 +473,12 @@ cudaError_t launch_topk(Keys keys, const float* vals, const uint32_t* seg_lo, in
         const size_t smem = kTkSmemCand * sizeof(uint64_t);
         cudaError_t ea = cudaFuncSetAttribute(topk_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (ea != cudaSuccess) return ea;
-        topk_select_kernel<<<(unsigned)nseg, kTkSelThreads, smem, s>>>(seg_lo, w.tile_start, w.seg_off, w.seg, w.cand,
+        topk_select_kernel<<<(unsigned)nseg, kTkSelThreads, smem, s>>>(bits, seg_lo, w.tile_start, w.seg_off, w.seg, w.cand,
                                                                    w.cand_cnt, w.tile_def, w.tile_sel, w.tile_off);
     }
     {
         SPC_PHASE("topk_write", s, 1);
-        topk_write_kernel<<<tiles, kTkWThreads, 0, s>>>(keys, vals, seg_lo, w.tile_start, w.tile_seg, nseg, attn, w.seg,
+        topk_write_kernel<<<tiles, kTkWThreads, 0, s>>>(keys, vals, seg_lo, w.tile_start, w.tile_seg, nseg, attn, bits, w.seg,
                                                        w.tile_off, out_keys, out_vals, out_src);
     }
     return cudaGetLastError();

@@ -364,7 +364,7 @@ struct TkSeg;
 struct TopkBufs {
     uint64_t* seg_off;      // [nseg + 1] output offset of each segment
     uint32_t* tile_start;   // [nseg + 1] first tile of each segment
-    uint32_t* hist;         // [nseg * kSelBins]
+    uint32_t* hist;         // [nseg << topk_bits(nnz, nseg)]
     TkSeg* seg;             // [nseg]
     uint32_t* cand_cnt;     // [nseg]
     uint64_t* cand;         // [nnz] candidate composites (segment s at its entry offset)
@@ -375,6 +375,7 @@ struct TopkBufs {
 };
 size_t topk_tiles_bound(int64_t nnz, int64_t nseg);
 size_t topk_seg_bytes();
+int topk_bits(int64_t nnz, int64_t nseg);   // width of the first score digit (11 or 13)
 cudaError_t launch_topk(Keys keys, const float* vals, const uint32_t* seg_lo, int64_t nseg, int64_t nnz_bound,
                         int attn, int64_t k, const TopkBufs& w, KeysOut out_keys, float* out_vals,
                         int64_t* out_src, int64_t* out_nnz, cudaStream_t s);
@@ -392,6 +393,7 @@ struct PoolPlan {
     int tiled;            // tile form: one CTA per (b, c, pooled plane, band of nyb pooled rows)
     int nyb, nyt;         // pooled rows per tile, tiles per pooled plane
     uint32_t mZ, msy, msz;  // floor((2^32 - 1) / d) for d = Z, sy, sz (division by multiply-high)
+    int lZ, lsy, lsz;       // log2 of Z, sy, sz when a power of two (a shift), else -1
 };
 PoolPlan plan_pool(const Geo& g, int sw, int sx, int sy, int sz);
 // Tile form (p.tiled): row_ptr is the band-bound workspace (pool_bound_words), filled here;

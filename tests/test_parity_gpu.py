@@ -491,6 +491,29 @@ def test_topk_large_segments(cuda_lib):
     np.testing.assert_array_equal(host(src[:yk.shape[0]]), osrc)
 
 
+@pytest.mark.parametrize("attn", ["magnitude", "raw"])
+@pytest.mark.parametrize("values", ["continuous", "ties"])
+def test_topk_13bit_digit_segments(cuda_lib, attn, values):
+    """Segments of >= 32 Ki entries take the 13-bit first digit (topk_bits): continuous values
+    with k near half the segment (the bench's shape: the threshold bucket holds thousands of
+    candidates), and massive ties (+-1, +0, -0) where whole buckets straddle k."""
+    spc = cuda_lib
+    x = uniform_map(1, 3, (64, 64, 64), 0.2, 47)    # ~52 k entries per segment
+    if values == "ties":
+        rng = np.random.default_rng(47)
+        vals = np.where(rng.random(x.nnz) < 0.5, 1.0, -1.0).astype(np.float32)
+        vals[rng.random(x.nnz) < 0.1] = 0.0
+        vals[rng.random(x.nnz) < 0.1] = -0.0
+        x = COO(x.batch, x.channels, x.dims, x.keys, vals)
+    for k in (1, 999, 26000, 51000):
+        ok_, ov, osrc = ora.topk(x, ATTN_ORA[attn], k)
+        y, src = spc.attention_topk(dev_map(spc, x), attn, k)
+        yk, yv = y.trimmed()
+        np.testing.assert_array_equal(host_keys(yk), ok_)
+        np.testing.assert_array_equal(host(yv).view(np.uint32), ov.view(np.uint32))
+        np.testing.assert_array_equal(host(src[:yk.shape[0]]), osrc)
+
+
 def test_relu_parity(cuda_lib):
     spc = cuda_lib
     for x in [uniform_map(3, 5, (17, 19), 0.3, 51), uniform_map(1, 1, (10,), 0.0, 1),
