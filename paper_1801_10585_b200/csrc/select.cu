@@ -108,6 +108,7 @@ __device__ __forceinline__ TkTile tk_tile(const uint32_t* seg_lo, const uint32_t
 // them), flushing into the segment's histogram whenever the segment changes; the next tile's
 // loads are issued before the current one's bins are updated.
 constexpr int kTkHistTiles = 4;
+template <int ATTN>
 __global__ void __launch_bounds__(kTkThreads) topk_hist_kernel(const float* __restrict__ vals,
                                                                const uint32_t* __restrict__ seg_lo,
                                                                const uint32_t* __restrict__ tile_start,
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(kTkThreads) topk_hist_kernel(const float* __re
         }
         uint32_t sc[kTkItems];
 #pragma unroll
-        for (int u = 0; u < kTkItems; ++u) sc[u] = score_bits(b[u], attn);
+        for (int u = 0; u < kTkItems; ++u) sc[u] = score_bits(b[u], ATTN);
         const TkTile cu = tl;
         const bool cka = ka;
         if (tt + 1 < kTkHistTiles) {   // next tile's loads in flight
@@ -214,6 +215,7 @@ __global__ void topk_find_kernel(const uint32_t* __restrict__ seg_lo, int64_t k,
     }
 }
 
+template <int ATTN>
 __global__ void __launch_bounds__(kTkThreads) topk_collect_kernel(const float* __restrict__ vals,
                                                                   const uint32_t* __restrict__ seg_lo,
                                                                   const uint32_t* __restrict__ tile_start,
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(kTkThreads) topk_collect_kernel(const float* _
 #pragma unroll
     for (int u = 0; u < kTkItems; ++u) {
         const bool in = (uint32_t)(u * kTkThreads) + threadIdx.x < nin;
-        const uint32_t sc = score_bits(b[u], attn);
+        const uint32_t sc = score_bits(b[u], ATTN);
         def += (in && sc >= ldef && !none_above) ? 1u : 0u;
         const bool c = in && (sc - cb) < wb;
         cm |= (c ? 1u : 0u) << u;
@@ -267,7 +269,7 @@ __global__ void __launch_bounds__(kTkThreads) topk_collect_kernel(const float* _
         for (int u = 0; u < kTkItems; ++u)
             if ((cm >> u) & 1u) {
                 const uint32_t i = tl.lo + (uint32_t)(u * kTkThreads) + threadIdx.x;
-                *cs++ = tk_comp(score_bits(b[u], attn), i - tl.seg0);
+                *cs++ = tk_comp(score_bits(b[u], ATTN), i - tl.seg0);
             }
     }
     def = block_sum(def, sm);
@@ -392,6 +394,7 @@ __global__ void __launch_bounds__(kTkSelThreads) topk_select_kernel(int bits, co
 // tile (8 groups of 32, coalesced), one ballot per group, warp totals scanned across the block
 constexpr int kTkWThreads = 512;
 constexpr int kTkWItems = kTkTile / kTkWThreads;   // 8
+template <int ATTN>
 __global__ void __launch_bounds__(kTkWThreads, 2) topk_write_kernel(Keys keys, const float* __restrict__ vals,
                                                                     const uint32_t* __restrict__ seg_lo,
                                                                     const uint32_t* __restrict__ tile_start,
@@ -419,7 +422,7 @@ __global__ void __launch_bounds__(kTkWThreads, 2) topk_write_kernel(Keys keys, c
 #pragma unroll
     for (int u = 0; u < kTkWItems; ++u) {
         const uint32_t i = w0 + 32u * u + lane;
-        const uint32_t sc = score_bits(b[u], attn);
+        const uint32_t sc = score_bits(b[u], ATTN);
         const uint32_t d = sc >> (32 - bits);
         const bool keep = i < tl.hi && (st.mode == 0u || d > st.b1 || (d == st.b1 && (st.mode == 1u ||
                                                                                      tk_comp(sc, i - tl.seg0) >= st.kstar)));
@@ -460,12 +463,12 @@ cudaError_t launch_topk(Keys keys, const float* vals, const uint32_t* seg_lo, in
     }
     {
         SPC_PHASE("topk_hist", s, 1);
-        topk_hist_kernel<<<(tiles + kTkHistTiles - 1) / kTkHistTiles, kTkThreads, 0, s>>>(vals, seg_lo, w.tile_start, w.tile_seg, nseg, attn, k, bits, w.hist);
+        (attn == SPC_ATTN_RAW ? topk_hist_kernel<SPC_ATTN_RAW> : topk_hist_kernel<SPC_ATTN_MAGNITUDE>)<<<(tiles + kTkHistTiles - 1) / kTkHistTiles, kTkThreads, 0, s>>>(vals, seg_lo, w.tile_start, w.tile_seg, nseg, attn, k, bits, w.hist);
     }
     { SPC_PHASE("topk_find", s, 1); topk_find_kernel<<<(unsigned)nseg, 256, 0, s>>>(seg_lo, k, bits, w.hist, w.seg, w.cand_cnt); }
     {
         SPC_PHASE("topk_collect", s, 1);
-        topk_collect_kernel<<<tiles, kTkThreads, 0, s>>>(vals, seg_lo, w.tile_start, w.tile_seg, nseg, attn, bits, w.seg, w.cand,
+        (attn == SPC_ATTN_RAW ? topk_collect_kernel<SPC_ATTN_RAW> : topk_collect_kernel<SPC_ATTN_MAGNITUDE>)<<<tiles, kTkThreads, 0, s>>>(vals, seg_lo, w.tile_start, w.tile_seg, nseg, attn, bits, w.seg, w.cand,
                                                          w.cand_cnt, w.tile_def);
     }
     {
@@ -478,7 +481,7 @@ cudaError_t launch_topk(Keys keys, const float* vals, const uint32_t* seg_lo, in
     }
     {
         SPC_PHASE("topk_write", s, 1);
-        topk_write_kernel<<<tiles, kTkWThreads, 0, s>>>(keys, vals, seg_lo, w.tile_start, w.tile_seg, nseg, attn, bits, w.seg,
+        (attn == SPC_ATTN_RAW ? topk_write_kernel<SPC_ATTN_RAW> : topk_write_kernel<SPC_ATTN_MAGNITUDE>)<<<tiles, kTkWThreads, 0, s>>>(keys, vals, seg_lo, w.tile_start, w.tile_seg, nseg, attn, bits, w.seg,
                                                        w.tile_off, out_keys, out_vals, out_src);
     }
     return cudaGetLastError();
