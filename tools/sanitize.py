@@ -53,6 +53,11 @@ def main():
                                 r.nnz_dev, sorted=True)
         spc.sparse_maxpool(Y, (2,) * len(dims))
         spc.attention_topk(Y, "raw", max(1, k // 3))
+    # top-k with the 13-bit first digit (segments of >= 32 Ki entries)
+    x = uniform_map(1, 2, (64, 64, 64), 0.2, 7010, values="dyadic")
+    X = spc.SparseMap.from_arrays(x.keys, x.values, x.batch, x.channels, x.dims)
+    spc.attention_topk(X, "magnitude", 20000)
+    spc.attention_topk(X, "raw", 20000)
     torch.cuda.synchronize()
     print("sanitize workload done")
 
