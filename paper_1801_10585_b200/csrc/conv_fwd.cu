@@ -67,6 +67,8 @@ FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_
                (size_t)ocg * (TY + (pred ? 0 : 4 * kg.hy)) * ZR * sizeof(float);
     };
     if (PK >= (1 << 13)) { t.smem = 0; return t; }                 // work descriptors hold 13-bit items
+    size_t kFwdBudget = spc::kFwdBudget;
+    if (const char* e = getenv("SPC_FWD_BUDGET_KB")) kFwdBudget = (size_t)atoi(e) * 1024;
     int ocg = std::min(c_out, kFwdWarps);
     while (ocg > 1 && need(ocg, 1, true) > kFwdBudget) --ocg;
     if (need(ocg, 1, true) > kFwdBudget) { t.smem = 0; return t; }
