@@ -162,7 +162,8 @@ def test_bwd_rank4(cuda_lib, case, values):
 
 
 @pytest.mark.parametrize("dims,stride", [((6, 8, 8, 10), (2, 2, 2, 2)), ((5, 7, 4, 9), (3, 1, 2, 4)),
-                                         ((3, 2, 3, 9000), (1, 2, 1, 2))])   # last: PZ 4500 > 4096, the row form
+                                         ((3, 2, 3, 9000), (1, 2, 1, 2)),    # PZ 4500 > 4096: the row form
+                                         ((16, 18, 4, 6), (8, 9, 1, 2))])    # sw * sx = 72 > 64 planes: row form
 def test_maxpool_relu_topk_rank4(cuda_lib, dims, stride):
     spc = cuda_lib
     x = uniform_map(2, 3, dims, 0.3, 4600, values="dyadic")
