@@ -620,47 +620,41 @@ def cpu_baseline(cfg, nsamples):
 # ------------------------------------------------------------------- reference arm
 def run_reference(args):
     """--impl reference: the oracle as it stands, on this host's cores, on the same config and
-    metric. Each step = fwd+bwd of one (b, oc) pair of the C4 workload (a bounded sample)."""
+    metric. Each step = fwd+bwd of a bounded sample of the C4 batch: one sample per host core, one
+    forked worker process per sample (the oracle itself is single-threaded C); the step's time is
+    the wall time of that parallel map."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    import oracle as ora
-    from synth import Filter
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
 
-    cfg = c4_inputs(args.density, args.values, batch=1)
-    x, w = cfg["x"], cfg["w"]
-    V = RES ** 3
-
-    def one(oc):
-        KV = 27
-        lo, hi = np.searchsorted(w.keys, np.uint64(oc * C_IN * KV)), np.searchsorted(w.keys, np.uint64((oc + 1) * C_IN * KV))
-        wk = w.keys[lo:hi] - np.uint64(oc * C_IN * KV)
-        wo = Filter(C_IN, 1, KS, wk, w.values[lo:hi])
-        t0 = time.perf_counter()
-        yk, yv, _, macs = ora.conv_fwd(x, wo, cfg["bias"][oc:oc + 1], attn=ora.ATTN_MAGNITUDE, k=cfg["k"])
-        dy = grad_values(yk.shape[0], SEED_BASE + 99)
-        *_, kept_pairs = ora.conv_bwd(x, wo, yk, dy, return_pairs=True)
-        dt = time.perf_counter() - t0
-        # bwd MACs: 2 x pairs landing on kept outputs (same definition as our arm)
-        return macs + 2 * kept_pairs, dt, yk
-
-    for i in range(args.warmup):
-        one(i % C_OUT)
+    global _CPU_CFG
+    ncpu = os.cpu_count() or 1
+    nw = max(1, min(ncpu, BATCH))
+    cfg = c4_inputs(args.density, args.values, batch=nw)   # samples 0..nw-1 of the seeded batch
+    _CPU_CFG = (cfg["x"], cfg["w"], cfg["bias"], cfg["k"])
     tot_macs, tot_t = 0.0, 0.0
-    for i in range(args.steps):
-        macs, dt, _ = one(i % C_OUT)
-        tot_macs += macs
-        tot_t += dt
-    value = tot_macs / tot_t / 1e9
+    with ProcessPoolExecutor(max_workers=nw, mp_context=mp.get_context("fork")) as ex:
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            res = list(ex.map(_oracle_sample, range(nw)))
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                tot_macs += sum(r[0] for r in res)
+                tot_t += dt
+    steps = max(1, args.steps)
+    value = tot_macs / tot_t / 1e9 if tot_t > 0 else 0.0
+    sample = f"{nw} of {BATCH} samples per step, fwd+bwd, one worker process per sample on {nw} of {ncpu} cores"
     res = {"impl": "reference", "metric": "sparse conv fwd+bwd effective GMAC/s (C4 128^3, rho_up 5%)",
            "value": round(value, 4), "unit": "GMAC/s", "n_gpus": args.gpus, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": round(tot_t / args.steps * 1e3, 2), "higher_is_better": True,
+           "warmup": args.warmup, "ms_per_step": round(tot_t / steps * 1e3, 2), "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": f"synthetic ({args.values} values, uniform positions, seeded)",
-           "config": {"workload": f"C4 sample: one (b, oc) pair of 3D {RES}^3, {C_IN}->1 ch, 3x3x3, rho_f {RHO_F}, "
-                                  f"rho_d {args.density}, k={K_SEL}, fwd+bwd", "density": args.density},
-           "cpu_baseline": {"value": round(value, 4), "unit": "GMAC/s", "cores": 1, "kind": "oracle",
-                            "sample": "one (b, oc) pair of the C4 batch per step, fwd+bwd"},
+           "config": {"workload": f"C4 sample: {nw} samples of 3D {RES}^3 per step, {C_IN}->{C_OUT} ch, 3x3x3, "
+                                  f"rho_f {RHO_F}, rho_d {args.density}, k={K_SEL}, fwd+bwd", "density": args.density},
+           "cpu_baseline": {"value": round(value, 4), "unit": "GMAC/s", "cores": nw, "kind": "oracle",
+                            "sample": sample, "cpu_model": _cpu_model(), "nproc": ncpu},
            "e2e": {"value": round(value, 4), "unit": "GMAC/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(res), flush=True)
     return res
