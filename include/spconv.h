@@ -264,6 +264,24 @@ spc_status_t sparse_scatter_grad_sorted(const int64_t* src_index, const float* d
                                         cudaStream_t stream);
 
 /* ------------------------------------------------------------------------------------
+ * spc_encode_keys / spc_decode_keys — the key codec of §3 (indices "compressed into
+ *   unique 1D keys and only expanded when needed"; Alg. 1 line 1: "decompress filter and
+ *   data indices from 1D to kD"): key = (b*channels + c)*prod(dims) + row_major(p), the first
+ *   spatial dim most significant (reading R11) -- the keys every op here takes.
+ *   coords: device int64 [n][2 + ndim], rows (b, c, p_0 .. p_{ndim-1}); keys: device uint64 [n];
+ *   dims: host int64 [ndim]. encode: a row with a coordinate outside [0, extent) gets key
+ *   UINT64_MAX and sets *bad_dev = 1; decode: a key >= batch*channels*prod(dims) gets the
+ *   coordinates -1 and sets *bad_dev = 1 (bad_dev: device int written only on such an entry, may
+ *   be NULL). Host-checkable problems (ndim outside 1..4, non-positive extents, key space above
+ *   2^63, null arrays with n > 0, n < 0) return SPC_ERR_INVALID_ARG / SPC_ERR_SHAPE with nothing
+ *   enqueued. Asynchronous on `stream`; caller-owned buffers.
+ * ------------------------------------------------------------------------------------ */
+spc_status_t spc_encode_keys(int32_t ndim, int64_t batch, int64_t channels, const int64_t* dims,
+                             const int64_t* coords, int64_t n, uint64_t* keys, int* bad_dev, cudaStream_t stream);
+spc_status_t spc_decode_keys(int32_t ndim, int64_t batch, int64_t channels, const int64_t* dims,
+                             const uint64_t* keys, int64_t n, int64_t* coords, int* bad_dev, cudaStream_t stream);
+
+/* ------------------------------------------------------------------------------------
  * sparse_to_dense — the sparseToDense() bridge of the OctNet3 stacks (Appendix B, Table 2,
  *   P:332): dense[key] = value for every stored entry, 0 elsewhere. dense: device float
  *   [batch*channels*prod(dims)] in [b][c][dims] order (the key layout makes the key the linear

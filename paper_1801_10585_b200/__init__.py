@@ -29,6 +29,8 @@ from .ops import (  # noqa: F401
     filter_prune,
     sparse_to_dense,
     sparse_to_dense_bwd,
+    encode_keys,
+    decode_keys,
     memory_estimate,
     keys_narrow,
     keys_widen,

@@ -33,6 +33,7 @@ EXPORTS = [
     "sparse_adagrad_step", "spc_prune_query", "sparse_filter_prune",
     "spc_conv_fwd_query_pass", "sparse_conv_fwd_pass",
     "spc_memory_estimate", "sparse_keys_narrow", "sparse_keys_widen",
+    "spc_encode_keys", "spc_decode_keys",
     "spc_kernel_launches", "spc_profile_enable", "spc_profile_reset", "spc_profile_read",
 ]
 
@@ -117,6 +118,8 @@ def load(path: str = LIB_PATH):
                                  C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
         "sparse_keys_narrow": ([pM, P, P], C.c_int),
         "sparse_keys_widen": ([P, P, I64, P, P], C.c_int),
+        "spc_encode_keys": ([C.c_int32, I64, I64, P, P, I64, P, P, P], C.c_int),
+        "spc_decode_keys": ([C.c_int32, I64, I64, P, P, I64, P, P, P], C.c_int),
         "spc_kernel_launches": ([], C.c_int64),
         "spc_profile_enable": ([C.c_int], C.c_int),
         "spc_profile_reset": ([], C.c_int),

@@ -859,6 +859,46 @@ bool fits32(const spc_map_t* x) {
 }
 }  // namespace
 
+// ------------------------------------------------------------------ key codec
+static spc_status_t codec_geo(int32_t ndim, int64_t batch, int64_t channels, const int64_t* dims, int64_t n,
+                              CodecGeo* g) {
+    if (ndim < 1 || ndim > SPC_MAX_NDIM || !dims || n < 0) return SPC_ERR_INVALID_ARG;
+    if (batch <= 0 || channels <= 0) return SPC_ERR_SHAPE;
+    g->nd = ndim;
+    g->B = batch;
+    g->C = channels;
+    double tot = (double)batch * (double)channels;
+    uint64_t V = 1;
+    for (int d = 0; d < ndim; ++d) {
+        if (dims[d] <= 0) return SPC_ERR_SHAPE;
+        g->d[d] = dims[d];
+        tot *= (double)dims[d];
+        if (tot >= 9.2e18) return SPC_ERR_SHAPE;   // key space above 2^63
+        V *= (uint64_t)dims[d];
+    }
+    g->V = V;
+    g->total = (uint64_t)batch * (uint64_t)channels * V;
+    return SPC_OK;
+}
+
+extern "C" spc_status_t spc_encode_keys(int32_t ndim, int64_t batch, int64_t channels, const int64_t* dims,
+                                        const int64_t* coords, int64_t n, uint64_t* keys, int* bad_dev,
+                                        cudaStream_t s) {
+    CodecGeo g{};
+    SPC_TRY(codec_geo(ndim, batch, channels, dims, n, &g));
+    if (n > 0 && (!coords || !keys)) return SPC_ERR_INVALID_ARG;
+    return cu(launch_encode_keys(g, coords, n, keys, bad_dev, s));
+}
+
+extern "C" spc_status_t spc_decode_keys(int32_t ndim, int64_t batch, int64_t channels, const int64_t* dims,
+                                        const uint64_t* keys, int64_t n, int64_t* coords, int* bad_dev,
+                                        cudaStream_t s) {
+    CodecGeo g{};
+    SPC_TRY(codec_geo(ndim, batch, channels, dims, n, &g));
+    if (n > 0 && (!coords || !keys)) return SPC_ERR_INVALID_ARG;
+    return cu(launch_decode_keys(g, keys, n, coords, bad_dev, s));
+}
+
 extern "C" spc_status_t sparse_keys_narrow(const spc_map_t* x, uint32_t* keys32, cudaStream_t s) {
     SPC_TRY(check_map(x, false));
     if (x->key_bits == 32) return SPC_ERR_INVALID_ARG;   // already 32-bit

@@ -619,6 +619,71 @@ __global__ void keys_widen_kernel(const uint32_t* __restrict__ k, const int64_t*
         o[i] = (uint64_t)__ldcs(&k[i]);
 }
 
+// Key codec (reading R11): one thread per entry; the decode divides by the extents
+// from the last (least significant) dimension up, in 32-bit arithmetic when the key space fits.
+__global__ void encode_keys_kernel(CodecGeo g, const int64_t* __restrict__ coords, int64_t n,
+                                   uint64_t* __restrict__ keys, int* __restrict__ bad) {
+    const int w = 2 + g.nd;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t* c = coords + i * w;
+        const int64_t b = c[0], ch = c[1];
+        bool ok = b >= 0 && b < g.B && ch >= 0 && ch < g.C;
+        uint64_t lin = 0;
+        for (int d = 0; d < g.nd; ++d) {
+            const int64_t p = c[2 + d];
+            ok = ok && p >= 0 && p < g.d[d];
+            lin = lin * (uint64_t)g.d[d] + (uint64_t)(p >= 0 ? p : 0);
+        }
+        if (ok) {
+            keys[i] = ((uint64_t)b * (uint64_t)g.C + (uint64_t)ch) * g.V + lin;
+        } else {
+            keys[i] = ~0ull;
+            if (bad) *bad = 1;
+        }
+    }
+}
+
+template <typename U>
+__global__ void decode_keys_kernel(CodecGeo g, const uint64_t* __restrict__ keys, int64_t n,
+                                   int64_t* __restrict__ coords, int* __restrict__ bad) {
+    const int w = 2 + g.nd;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t key = keys[i];
+        int64_t* c = coords + i * w;
+        if (key >= g.total) {
+            for (int d = 0; d < w; ++d) c[d] = -1;
+            if (bad) *bad = 1;
+            continue;
+        }
+        U r = (U)key;
+        for (int d = g.nd - 1; d >= 0; --d) {
+            const U q = r / (U)g.d[d];
+            c[2 + d] = (int64_t)(r - q * (U)g.d[d]);
+            r = q;
+        }
+        const U bb = r / (U)g.C;
+        c[1] = (int64_t)(r - bb * (U)g.C);
+        c[0] = (int64_t)bb;
+    }
+}
+
+cudaError_t launch_encode_keys(const CodecGeo& g, const int64_t* coords, int64_t n, uint64_t* keys, int* bad,
+                               cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 16);
+    { SPC_PHASE("encode_keys", s, 1); encode_keys_kernel<<<grid, 256, 0, s>>>(g, coords, n, keys, bad); }
+    return cudaGetLastError();
+}
+cudaError_t launch_decode_keys(const CodecGeo& g, const uint64_t* keys, int64_t n, int64_t* coords, int* bad,
+                               cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 16);
+    SPC_PHASE("decode_keys", s, 1);
+    if (g.total <= 0xffffffffull) decode_keys_kernel<uint32_t><<<grid, 256, 0, s>>>(g, keys, n, coords, bad);
+    else decode_keys_kernel<uint64_t><<<grid, 256, 0, s>>>(g, keys, n, coords, bad);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_keys_narrow(const uint64_t* keys, const int64_t* nnz_dev, int64_t bound, uint32_t* out, cudaStream_t s) {
     if (bound == 0) return cudaSuccess;
     const unsigned grid = (unsigned)std::min<int64_t>((bound + 255) / 256, num_sms() * 16);

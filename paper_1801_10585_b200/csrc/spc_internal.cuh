@@ -432,6 +432,16 @@ cudaError_t launch_to_dense(Keys keys, const float* vals, const int64_t* nnz_dev
 cudaError_t launch_gather_dense(Keys keys, const int64_t* nnz_dev, int64_t bound, const float* ddense,
                                 float* dvals, cudaStream_t s);
 
+struct CodecGeo {
+    int nd;
+    int64_t B, C;
+    int64_t d[SPC_MAX_NDIM];
+    uint64_t V, total;   // prod(dims), B*C*V
+};
+cudaError_t launch_encode_keys(const CodecGeo& g, const int64_t* coords, int64_t n, uint64_t* keys, int* bad,
+                               cudaStream_t s);
+cudaError_t launch_decode_keys(const CodecGeo& g, const uint64_t* keys, int64_t n, int64_t* coords, int* bad,
+                               cudaStream_t s);
 cudaError_t launch_keys_narrow(const uint64_t* keys, const int64_t* nnz_dev, int64_t bound, uint32_t* out, cudaStream_t s);
 cudaError_t launch_keys_widen(const uint32_t* keys, const int64_t* nnz_dev, int64_t bound, uint64_t* out, cudaStream_t s);
 // Validation (SPC_VALIDATE=1): flag = 1 if keys are not strictly increasing or out of range.

@@ -529,6 +529,42 @@ def sparse_to_dense_bwd(x: SparseMap, ddense: torch.Tensor, stream=None) -> torc
     return dv[:x.nnz_bound]
 
 
+# ------------------------------------------------------------------ key codec
+def _dims_arg(dims):
+    arr = (C.c_int64 * len(dims))(*[int(d) for d in dims])
+    return C.cast(arr, C.c_void_p), arr   # (pointer, owner kept alive by the caller)
+
+
+def encode_keys(coords: torch.Tensor, batch: int, channels: int, dims, stream=None) -> torch.Tensor:
+    """spc_encode_keys: int64 coordinate rows (b, c, p_0..) [n, 2 + ndim] on the device -> uint64
+    keys (as int64) [n]; raises ValueError when a coordinate is out of range."""
+    coords = coords.contiguous()
+    n = coords.shape[0]
+    keys = torch.empty(max(n, 1), dtype=torch.int64, device=coords.device)
+    bad = torch.zeros(1, dtype=torch.int32, device=coords.device)
+    dp, _own = _dims_arg(dims)
+    check("spc_encode_keys", load().spc_encode_keys(len(dims), int(batch), int(channels), dp,
+                                                    _ptr(coords), n, _ptr(keys), _ptr(bad), _stream(stream)))
+    if int(bad.item()):
+        raise ValueError("spc_encode_keys: coordinate out of range")
+    return keys[:n]
+
+
+def decode_keys(keys: torch.Tensor, batch: int, channels: int, dims, stream=None) -> torch.Tensor:
+    """spc_decode_keys: uint64 keys (as int64) [n] -> int64 coordinate rows (b, c, p_0..) [n, 2 + ndim];
+    raises ValueError when a key is outside the key space."""
+    keys = keys.contiguous()
+    n = keys.shape[0]
+    coords = torch.empty((max(n, 1), 2 + len(dims)), dtype=torch.int64, device=keys.device)
+    bad = torch.zeros(1, dtype=torch.int32, device=keys.device)
+    dp, _own = _dims_arg(dims)
+    check("spc_decode_keys", load().spc_decode_keys(len(dims), int(batch), int(channels), dp,
+                                                    _ptr(keys), n, _ptr(coords), _ptr(bad), _stream(stream)))
+    if int(bad.item()):
+        raise ValueError("spc_decode_keys: key outside the key space")
+    return coords[:n]
+
+
 # ------------------------------------------------------------------ memory model (SURVEY §8 f2)
 def memory_estimate(ndim: int, r: int, batch: int, channels: int, rho_up: float, index_bits: int = 64) -> dict:
     """Table 1 / Fig. 7 theoretical bytes (spc_memory_estimate): dense, sparse, temp."""

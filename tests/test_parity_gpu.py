@@ -1009,6 +1009,44 @@ def test_fwd_pass_device_nnz_and_empty(cuda_lib):
     assert y.nnz() == 0
 
 
+@pytest.mark.parametrize("dims", [(37,), (8, 8), (5, 6, 7), (3, 4, 5, 6), (1 << 20, 1 << 20)])
+def test_key_codec_parity(cuda_lib, dims):
+    """spc_encode_keys / spc_decode_keys against the oracle's codec on seeded coordinates (rank
+    1..4; the last case has a key space above 2^32: the 64-bit decode), the SPEC example
+    (shape {b=2, 4x4, c=3}, index (b=1, x=2, y=3, c=0) -> 59), round trips, and the
+    out-of-range flags."""
+    spc = cuda_lib
+    B, Cc = 3, 4
+    rng = np.random.default_rng(5000 + len(dims))
+    n = 2000
+    coords = np.stack([rng.integers(0, B, n), rng.integers(0, Cc, n)] +
+                      [rng.integers(0, d, n) for d in dims], axis=1).astype(np.int64)
+    keys = host(spc.encode_keys(torch.from_numpy(coords).cuda(), B, Cc, dims)).view(np.uint64)
+    want = np.array([ora.encode_key(tuple(r), dims, Cc) for r in coords[:300]], np.uint64)
+    np.testing.assert_array_equal(keys[:300], want)
+    back = host(spc.decode_keys(torch.from_numpy(keys.view(np.int64)).cuda(), B, Cc, dims))
+    np.testing.assert_array_equal(back, coords)
+    for kk in keys[:50]:
+        assert tuple(back[np.nonzero(keys == kk)[0][0]]) == ora.decode_key(int(kk), dims, B, Cc)
+    bad = coords[:3].copy()
+    bad[1, 2] = dims[0]                       # spatial coordinate out of range
+    with pytest.raises(ValueError):
+        spc.encode_keys(torch.from_numpy(bad).cuda(), B, Cc, dims)
+    total = B * Cc * int(np.prod(dims, dtype=object))
+    if total < (1 << 63):
+        with pytest.raises(ValueError):
+            spc.decode_keys(torch.tensor([0, total], dtype=torch.int64).cuda(), B, Cc, dims)
+
+
+def test_key_codec_spec_example(cuda_lib):
+    spc = cuda_lib
+    k = spc.encode_keys(torch.tensor([[1, 0, 2, 3], [0, 0, 0, 0]], dtype=torch.int64).cuda(), 2, 3, (4, 4))
+    assert host(k).tolist() == [59, 0]
+    c = spc.decode_keys(torch.tensor([59], dtype=torch.int64).cuda(), 2, 3, (4, 4))
+    assert host(c).tolist() == [[1, 0, 2, 3]]
+    assert spc.encode_keys(torch.zeros((0, 4), dtype=torch.int64).cuda(), 2, 3, (4, 4)).numel() == 0
+
+
 def test_keys_narrow_widen_roundtrip(cuda_lib):
     """Table 1 "Sparse 32" storage: the low words of the keys and back, bit-exact."""
     spc = cuda_lib

@@ -58,6 +58,10 @@ def main():
     X = spc.SparseMap.from_arrays(x.keys, x.values, x.batch, x.channels, x.dims)
     spc.attention_topk(X, "magnitude", 20000)
     spc.attention_topk(X, "raw", 20000)
+    # key codec
+    co = torch.tensor([[1, 0, 2, 3], [0, 2, 3, 1], [1, 2, 0, 0]], dtype=torch.int64).cuda()
+    kk = spc.encode_keys(co, 2, 3, (4, 4))
+    spc.decode_keys(kk, 2, 3, (4, 4))
     torch.cuda.synchronize()
     print("sanitize workload done")
 
