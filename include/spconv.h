@@ -29,6 +29,10 @@
  *     count to *nnz_dev (device) so chained layers never need a host sync.
  *   - Spatial rank 1..4 (SPC_MAX_NDIM; "generic n-dimensional tensors"); odd kernel sizes;
  *     prod(ksize) <= 1024. The tensor-core accumulate variant (SPC_VARIANT_GEMM) is rank <= 3.
+ *   - Row length (last dimension Z): the scatter forward keeps one band row of Z + 2hz fp32
+ *     columns per output channel on chip (up to ~50 k columns); the backward keeps a gradient
+ *     slab of (1 + 2hw)(TX + 2hx)(TY + 2hy)(Z + 2hz) fp32 words (1D up to ~50 k columns, 2D with
+ *     ky = 3 ~17 k, 3D with 3x3 ~5.5 k). Longer rows return SPC_ERR_UNSUPPORTED.
  *   - Convolution is cross-correlation with SAME zero padding and stride 1 (readings R1, R2).
  *   - Workspace: query the byte count with the matching *_query function, pass a device
  *     buffer of at least that many bytes (256-byte aligned).

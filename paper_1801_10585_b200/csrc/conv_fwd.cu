@@ -37,6 +37,7 @@ namespace spc {
 constexpr int kFwdThreads = 256;
 constexpr int kFwdWarps = kFwdThreads / 32;   // warp w accumulates output channel oc0 + w
 constexpr size_t kFwdBudget = 113 * 1024;     // two CTAs (16 warps) per SM
+constexpr size_t kFwdBudgetMax = 220 * 1024;  // one CTA per SM (very long rows)
 constexpr int kStageCap = 1536;               // staged input entries per chunk (byte position + value)
 static_assert(kStageCap * 8 >= (kSelBins + 32) * 4, "the epilogue histogram (+ 32 dummy bins) reuses the staging area");
 
@@ -71,6 +72,9 @@ FwdTile plan_fwd_tile(const Geo& gy, const KGeo& kg, int c_out, int c_in, int64_
     if (const char* e = getenv("SPC_FWD_BUDGET_KB")) kFwdBudget = (size_t)atoi(e) * 1024;
     int ocg = std::min(c_out, kFwdWarps);
     while (ocg > 1 && need(ocg, 1, true) > kFwdBudget) --ocg;
+    // rows too long for two CTAs per SM (a band row of one channel above ~25 k columns): one CTA
+    // per SM with the whole shared memory (1D signals up to ~50 k columns)
+    if (need(ocg, 1, true) > kFwdBudget) kFwdBudget = kFwdBudgetMax;
     if (need(ocg, 1, true) > kFwdBudget) { t.smem = 0; return t; }
     auto tymax = [&](bool pred) {
         int v = 0;

@@ -362,6 +362,34 @@ def test_fwd_resolve_small_segment_boundary(cuda_lib, dims, attn):
         np.testing.assert_array_equal(gv, ov)
 
 
+@pytest.mark.parametrize("dims,ci", [((40000,), 40), ((2, 30000), 36)])
+def test_fwd_bwd_long_rows(cuda_lib, dims, ci):
+    """Rows longer than the two-CTAs-per-SM accumulator (1D signals, a long last dimension) with
+    more than 32 input channels (no tensor-core variant): the scatter forward takes one CTA per SM
+    with the whole shared memory; forward (attention) and backward bit-exact on dyadic data. The
+    backward's gradient slab holds ky rows of Z + 2hz columns: a 2D map with 30 k-column rows
+    exceeds shared memory and is refused (SPC_ERR_UNSUPPORTED, documented in spconv.h)."""
+    spc = cuda_lib
+    x = uniform_map(2, ci, dims, 0.004, 7100, values="dyadic")
+    w = sparse_filter(ci, 3, (3,) * len(dims), 0.5, 7101, values="dyadic4")
+    bias = bias_vector(3, 7102, values="dyadic")
+    V = int(np.prod(dims))
+    k = V // 30
+    ok_, ov, _, _ = ora.conv_fwd(x, w, bias, attn=ora.ATTN_MAGNITUDE, k=k)
+    gk, gv, y = run_fwd(spc, x, w, bias, "magnitude", k)
+    np.testing.assert_array_equal(gk, ok_)
+    np.testing.assert_array_equal(gv, ov)
+    dy = grad_values(gk.shape[0], 7103, values="dyadic")
+    if len(dims) > 1:
+        with pytest.raises(spc.SpconvError):
+            spc.sparse_conv_bwd(dev_map(spc, x), dev_filter(spc, w), y.exact(), torch.from_numpy(dy).cuda())
+        return
+    gdx, gdw, _ = spc.sparse_conv_bwd(dev_map(spc, x), dev_filter(spc, w), y.exact(), torch.from_numpy(dy).cuda())
+    odx, odw, _, _, _ = ora.conv_bwd(x, w, ok_, dy, with_abs=True)
+    np.testing.assert_array_equal(host(gdx), odx)
+    np.testing.assert_array_equal(host(gdw), odw)
+
+
 def test_fwd_empty_and_degenerate(cuda_lib):
     spc = cuda_lib
     x = COO(2, 2, (5, 6), np.zeros(0, np.uint64), np.zeros(0, np.float32))
