@@ -321,6 +321,74 @@ spc_status_t sparse_keys_widen(const uint32_t* keys32, const int64_t* nnz_dev, i
                                cudaStream_t stream);
 
 /* ------------------------------------------------------------------------------------
+ * Spatial sharding of one sample across ranks (beyond the paper, whose dense
+ * temporary buffer holds a whole (b, oc) grid on one GPU). The FIRST spatial dimension
+ * ("planes", most significant in the key, R11) is cut into contiguous ranges; rank r owns the
+ * outputs of planes [a_r, e_r) and needs the inputs of planes [a_r - h, e_r + h), h = ksize[0]/2
+ * (Eq. (1): an output depends on inputs within the filter's extent). A shard map is an ordinary
+ * map over dims (e_r - a_r, dims[1..]) with the same batch and channels; plane = prod(dims[1..]).
+ * 64-bit keys only (SPC_ERR_UNSUPPORTED otherwise). Asynchronous on `stream`; device arrays.
+ *
+ * spc_slab_gather — for every segment s = b*channels + c (nseg of them), the concatenation over
+ *   sources j = 0..nsrc-1 (nsrc <= 4) of source j's entries of segment s with plane in
+ *   [lo_j, hi_j) (source coordinates), each re-based to plane + shift_j of an output grid of
+ *   `planes_out` planes:  out_key = key + s*(planes_out - planes_j)*plane + shift_j*plane.
+ *   The output is sorted when the sources' shifted ranges are disjoint and increasing in j
+ *   (halo assembly: left halo, own planes, right halo; owned-plane extraction and shard <->
+ *   global re-basing are nsrc = 1). src_index (optional, [capacity]) receives base_j + e for
+ *   source entry e, base_j = n_0 + ... + n_{j-1} (the sources' `n` bounds): the position in the
+ *   concatenated source index space (halo partial gradients are routed with it). Source j's
+ *   count is *nnz_dev when non-NULL, else n. y->capacity >= sum n_j; *y->nnz_dev = exact count.
+ *   Workspace from spc_slab_gather_query (3 words per (segment, source)).
+ *
+ * spc_topk_digit_hist / spc_topk_digit_pick / spc_topk_keep_ge — the attention k-selection of
+ *   P:80-84 (§3.2; variants P:104) over a segment split across ranks, as an exact 8-round
+ *   radix select on the composite c = (score << 32) | ~(uint32)(p + p_base) of reading R7
+ *   (score: |y| for MAGNITUDE, sign-folded y for RAW; p = key mod prod(dims), the shard-local
+ *   position; p_base = a_r*plane makes it the global one, so ties break as on one GPU;
+ *   p + p_base < 2^32 required). Per-segment device state: prefix[nseg] (uint64, zeroed
+ *   before round 1), need[nseg] (int64, = k before round 1; < 0 = settled), hist[nseg*256]
+ *   (uint32, zeroed before each round). For shift = 56, 48, ..., 0:
+ *     digit_hist: hist[s][d] += #{entries of s with (c >> (shift+8)) == (prefix[s] >> (shift+8))
+ *                 and ((c >> shift) & 255) == d}   (all entries when shift = 56)
+ *     (the caller sums hist over ranks: one all-reduce per round)
+ *     digit_pick: the digit d with above(d) < need[s] <= above(d) + hist[s][d] (above = the
+ *                 count of larger digits): prefix[s] |= d << shift, need[s] -= above(d); in
+ *                 round 1 a segment with at most need[s] entries in total keeps all of them
+ *                 (prefix 0, need -1: "keep all if |S| <= k").
+ *   After round shift = 0, prefix[s] is the k-th largest composite of the whole segment (or 0).
+ *   spc_topk_keep_ge writes the entries with c >= thr[seg] in key order (src_index optional:
+ *   their input positions); y->capacity >= x->nnz; workspace from spc_topk_keep_query.
+ *
+ * spc_index_add — out[idx[t]] += v[t], t < n (n = *n_dev if non-NULL, bounded by n_bound);
+ *   idx must be injective (halo partials of dx added into the owner's dx).
+ * ------------------------------------------------------------------------------------ */
+typedef struct {
+    const uint64_t* keys;          /* device [n], sorted                                     */
+    const float* values;           /* device [n]                                             */
+    const int64_t* nnz_dev;        /* device exact count, or NULL (then n)                   */
+    int64_t n;                     /* count, or upper bound when nnz_dev != NULL             */
+    int64_t planes;                /* planes of the source grid                              */
+    int64_t lo, hi;                /* kept planes [lo, hi), source coordinates               */
+    int64_t shift;                 /* output plane = source plane + shift                    */
+} spc_slab_src_t;
+
+spc_status_t spc_slab_gather_query(int64_t nseg, int32_t nsrc, size_t* workspace_bytes);
+spc_status_t spc_slab_gather(const spc_slab_src_t* srcs, int32_t nsrc, int64_t nseg, int64_t plane,
+                             int64_t planes_out, spc_map_out_t* y, int64_t* src_index, void* workspace,
+                             size_t workspace_bytes, cudaStream_t stream);
+spc_status_t spc_topk_digit_hist(const spc_map_t* x, spc_attn_t attn, int64_t p_base, const uint64_t* prefix,
+                                 const int64_t* need, int32_t shift, uint32_t* hist, cudaStream_t stream);
+spc_status_t spc_topk_digit_pick(int64_t nseg, const uint32_t* hist, int32_t shift, uint64_t* prefix,
+                                 int64_t* need, cudaStream_t stream);
+spc_status_t spc_topk_keep_query(const spc_map_t* x, size_t* workspace_bytes);
+spc_status_t spc_topk_keep_ge(const spc_map_t* x, spc_attn_t attn, int64_t p_base, const uint64_t* thr,
+                              spc_map_out_t* y, int64_t* src_index, void* workspace, size_t workspace_bytes,
+                              cudaStream_t stream);
+spc_status_t spc_index_add(const int64_t* idx, const float* v, int64_t n_bound, const int64_t* n_dev,
+                           float* out, cudaStream_t stream);
+
+/* ------------------------------------------------------------------------------------
  * Training-loop steps over a sparse filter bank. Elementwise over the STORED
  * weights only: pruned weights are absent and therefore never move or reappear.
  *

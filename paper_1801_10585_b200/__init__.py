@@ -40,3 +40,4 @@ from .ops import (  # noqa: F401
     profile_read,
 )
 from . import dp  # noqa: F401
+from . import spatial  # noqa: F401

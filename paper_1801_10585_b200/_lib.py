@@ -34,6 +34,8 @@ EXPORTS = [
     "spc_conv_fwd_query_pass", "sparse_conv_fwd_pass",
     "spc_memory_estimate", "sparse_keys_narrow", "sparse_keys_widen",
     "spc_encode_keys", "spc_decode_keys",
+    "spc_slab_gather_query", "spc_slab_gather", "spc_topk_digit_hist", "spc_topk_digit_pick",
+    "spc_topk_keep_query", "spc_topk_keep_ge", "spc_index_add",
     "spc_kernel_launches", "spc_profile_enable", "spc_profile_reset", "spc_profile_read",
 ]
 
@@ -57,6 +59,11 @@ class FilterT(C.Structure):
 class DensityRegT(C.Structure):
     _fields_ = [("lambda_", C.c_double), ("rho_up", C.c_double), ("o", C.c_double), ("b1", C.c_double),
                 ("b2", C.c_double)]
+
+
+class SlabSrcT(C.Structure):
+    _fields_ = [("keys", C.c_void_p), ("values", C.c_void_p), ("nnz_dev", C.c_void_p), ("n", C.c_int64),
+                ("planes", C.c_int64), ("lo", C.c_int64), ("hi", C.c_int64), ("shift", C.c_int64)]
 
 
 class SpconvError(RuntimeError):
@@ -120,6 +127,13 @@ def load(path: str = LIB_PATH):
         "sparse_keys_widen": ([P, P, I64, P, P], C.c_int),
         "spc_encode_keys": ([C.c_int32, I64, I64, P, P, I64, P, P, P], C.c_int),
         "spc_decode_keys": ([C.c_int32, I64, I64, P, P, I64, P, P, P], C.c_int),
+        "spc_slab_gather_query": ([I64, C.c_int32, sz], C.c_int),
+        "spc_slab_gather": ([C.POINTER(SlabSrcT), C.c_int32, I64, I64, I64, pO, P, P, C.c_size_t, P], C.c_int),
+        "spc_topk_digit_hist": ([pM, C.c_int, I64, P, P, C.c_int32, P, P], C.c_int),
+        "spc_topk_digit_pick": ([I64, P, C.c_int32, P, P, P], C.c_int),
+        "spc_topk_keep_query": ([pM, sz], C.c_int),
+        "spc_topk_keep_ge": ([pM, C.c_int, I64, P, pO, P, P, C.c_size_t, P], C.c_int),
+        "spc_index_add": ([P, P, I64, P, P, P], C.c_int),
         "spc_kernel_launches": ([], C.c_int64),
         "spc_profile_enable": ([C.c_int], C.c_int),
         "spc_profile_reset": ([], C.c_int),
