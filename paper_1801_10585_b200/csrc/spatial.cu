@@ -140,14 +140,20 @@ __device__ __forceinline__ uint64_t composite_of(uint64_t key, float v, uint64_t
 
 // Digit histogram: bits [shift, shift + 8) of the composite among the entries whose higher bits
 // equal prefix[seg]'s; segments with need[seg] < 0 are settled and skipped. Blocks take chunks of
-// consecutive entries (a chunk spans few segments: shared bins for up to 4, global otherwise).
+// consecutive entries; a chunk spanning at most 4 segments (the usual case: segments are long)
+// finds an entry's segment by comparing with the chunk's segment bounds (no 64-bit division) and
+// counts in shared bins, aggregated per warp over lanes with the same (segment, digit) -- round 1
+// sees few distinct digits (the exponent byte), so plain atomics would serialise on them.
 constexpr int kHistChunk = 4096;
 __global__ void digit_hist_kernel(const uint64_t* __restrict__ keys, const float* __restrict__ vals,
                                   const int64_t* nnz_dev, int64_t bound, uint64_t V, uint64_t p_base, int attn,
                                   const uint64_t* __restrict__ prefix, const int64_t* __restrict__ need, int shift,
                                   uint32_t* __restrict__ hist) {
     __shared__ uint32_t sh[4 * 256];
+    __shared__ int64_t s_need[4];
+    __shared__ uint64_t s_pre[4];
     const int64_t n = load_n(nnz_dev, bound);
+    const int lane = threadIdx.x & 31;
     for (int64_t c0 = (int64_t)blockIdx.x * kHistChunk; c0 < n; c0 += (int64_t)gridDim.x * kHistChunk) {
         const int64_t c1 = min(c0 + kHistChunk, n);
         const int64_t s0 = (int64_t)(keys[c0] / V);
@@ -155,23 +161,53 @@ __global__ void digit_hist_kernel(const uint64_t* __restrict__ keys, const float
         const bool local = s1 - s0 < 4;
         if (local) {
             for (int t = threadIdx.x; t < 4 * 256; t += blockDim.x) sh[t] = 0;
+            if (threadIdx.x < 4 && s0 + threadIdx.x <= s1) {
+                s_need[threadIdx.x] = need[s0 + threadIdx.x];
+                s_pre[threadIdx.x] = prefix[s0 + threadIdx.x];
+            }
             __syncthreads();
-        }
-        for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-            const uint64_t k = keys[i];
-            const int64_t seg = (int64_t)(k / V);
-            if (need[seg] < 0) continue;
-            const uint64_t c = composite_of(k, vals[i], V, p_base, attn);
-            if (shift < 56 && (c >> (shift + 8)) != (prefix[seg] >> (shift + 8))) continue;
-            const uint32_t d = (uint32_t)(c >> shift) & 255u;
-            if (local) atomicAdd(&sh[(seg - s0) * 256 + d], 1u);
-            else atomicAdd(&hist[seg * 256 + d], 1u);
-        }
-        if (local) {
+            const uint64_t base0 = (uint64_t)s0 * V;
+            // whole warps step together (the aggregation needs converged lanes)
+            for (int64_t i0 = c0 + (threadIdx.x & ~31); i0 < c1; i0 += blockDim.x) {
+                const int64_t i = i0 + lane;
+                int slot = -1;
+                uint32_t d = 0;
+                if (i < c1) {
+                    const uint64_t k = keys[i];
+                    uint64_t rel = k - base0;
+                    int si = 0;
+                    while (rel >= V) {
+                        rel -= V;
+                        ++si;
+                    }
+                    if (s_need[si] >= 0) {
+                        const uint64_t c = ((uint64_t)score_bits(__float_as_uint(vals[i]), attn) << 32) |
+                                           (uint64_t)(~(uint32_t)(rel + p_base));
+                        if (shift >= 56 || (c >> (shift + 8)) == (s_pre[si] >> (shift + 8))) {
+                            d = (uint32_t)(c >> shift) & 255u;
+                            slot = si * 256 + (int)d;
+                        }
+                    }
+                }
+                const unsigned act = __ballot_sync(0xffffffffu, slot >= 0);
+                if (slot >= 0) {
+                    const unsigned same = __match_any_sync(act, slot);
+                    if (lane == __ffs(same) - 1) atomicAdd(&sh[slot], (uint32_t)__popc(same));
+                }
+            }
             __syncthreads();
             for (int t = threadIdx.x; t < (int)(s1 - s0 + 1) * 256; t += blockDim.x)
                 if (sh[t]) atomicAdd(&hist[(s0 + t / 256) * 256 + (t & 255)], sh[t]);
             __syncthreads();
+        } else {
+            for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+                const uint64_t k = keys[i];
+                const int64_t seg = (int64_t)(k / V);
+                if (need[seg] < 0) continue;
+                const uint64_t c = composite_of(k, vals[i], V, p_base, attn);
+                if (shift < 56 && (c >> (shift + 8)) != (prefix[seg] >> (shift + 8))) continue;
+                atomicAdd(&hist[seg * 256 + ((uint32_t)(c >> shift) & 255u)], 1u);
+            }
         }
     }
 }
@@ -206,26 +242,64 @@ __global__ void digit_pick_kernel(int64_t nseg, const uint32_t* __restrict__ his
     // exactly one d satisfies suf[d + 1] < nd <= suf[d]
     if (suf[t + 1] < nd && nd <= suf[t]) {
         prefix[seg] |= (uint64_t)t << shift;
-        need[seg] = nd - suf[t + 1];
+        const int64_t rest = nd - suf[t + 1];
+        // the whole bucket is kept: prefix (lower bits 0) is already an exact threshold
+        need[seg] = rest == suf[t] - suf[t + 1] ? -1 : rest;
     }
 }
 
-// Keep composite >= thr[seg], order preserved: per-tile counts, one-block scan, write.
+// Keep composite >= thr[seg], order preserved: per-tile counts, one-block scan, write. A tile
+// spanning at most 4 segments finds an entry's segment by comparing with the tile's segment
+// bounds (no 64-bit division per entry).
+struct TileSegs {
+    int64_t s0;
+    int span;            // s1 - s0 + 1 when <= 4, else 0 (divide per entry)
+    uint64_t thr[4];
+};
+__device__ __forceinline__ void tile_segs(TileSegs& t, const uint64_t* keys, int64_t c0, int64_t c1, uint64_t V,
+                                          const uint64_t* thr) {
+    if (threadIdx.x == 0) {
+        t.s0 = (int64_t)(keys[c0] / V);
+        const int64_t s1 = (int64_t)(keys[c1 - 1] / V);
+        t.span = s1 - t.s0 < 4 ? (int)(s1 - t.s0 + 1) : 0;
+        for (int j = 0; j < t.span; ++j) t.thr[j] = thr[t.s0 + j];
+    }
+}
+__device__ __forceinline__ bool keep_entry(const TileSegs& t, uint64_t k, float v, uint64_t V, uint64_t p_base,
+                                           int attn, const uint64_t* thr) {
+    uint64_t rel, th;
+    if (t.span) {
+        rel = k - (uint64_t)t.s0 * V;
+        int si = 0;
+        while (rel >= V) {
+            rel -= V;
+            ++si;
+        }
+        th = t.thr[si];
+    } else {
+        const uint64_t seg = k / V;
+        rel = k - seg * V;
+        th = thr[seg];
+    }
+    const uint64_t c = ((uint64_t)score_bits(__float_as_uint(v), attn) << 32) | (uint64_t)(~(uint32_t)(rel + p_base));
+    return c >= th;
+}
+
 constexpr int kKeepTile = 2048;
 __global__ void keep_count_kernel(const uint64_t* __restrict__ keys, const float* __restrict__ vals,
                                   const int64_t* nnz_dev, int64_t bound, uint64_t V, uint64_t p_base, int attn,
                                   const uint64_t* __restrict__ thr, int64_t* __restrict__ tile_cnt, int64_t ntiles) {
     __shared__ int cnt;
+    __shared__ TileSegs ts;
     const int64_t n = load_n(nnz_dev, bound);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        if (threadIdx.x == 0) cnt = 0;
-        __syncthreads();
         const int64_t c0 = tile * kKeepTile, c1 = min(c0 + kKeepTile, n);
+        if (threadIdx.x == 0) cnt = 0;
+        if (c0 < c1) tile_segs(ts, keys, c0, c1, V, thr);
+        __syncthreads();
         int mine = 0;
-        for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-            const uint64_t k = keys[i];
-            mine += composite_of(k, vals[i], V, p_base, attn) >= thr[k / V];
-        }
+        for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x)
+            mine += keep_entry(ts, keys[i], vals[i], V, p_base, attn, thr);
         for (int d = 16; d; d >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, d);
         if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&cnt, mine);
         __syncthreads();
@@ -240,12 +314,14 @@ __global__ void keep_write_kernel(const uint64_t* __restrict__ keys, const float
                                   uint64_t* __restrict__ okeys, float* __restrict__ ovals, int64_t* __restrict__ src_index) {
     __shared__ int warp_cnt[32];
     __shared__ int64_t base;
+    __shared__ TileSegs ts;
     const int64_t n = load_n(nnz_dev, bound);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        if (threadIdx.x == 0) base = tile_off[tile];
-        __syncthreads();
         const int64_t c0 = tile * kKeepTile, c1 = min(c0 + kKeepTile, n);
+        if (threadIdx.x == 0) base = tile_off[tile];
+        if (c0 < c1) tile_segs(ts, keys, c0, c1, V, thr);
+        __syncthreads();
         for (int64_t r0 = c0; r0 < c1; r0 += blockDim.x) {   // rounds of blockDim entries, in order
             const int64_t i = r0 + threadIdx.x;
             bool keep = false;
@@ -254,7 +330,7 @@ __global__ void keep_write_kernel(const uint64_t* __restrict__ keys, const float
             if (i < c1) {
                 k = keys[i];
                 v = vals[i];
-                keep = composite_of(k, v, V, p_base, attn) >= thr[k / V];
+                keep = keep_entry(ts, k, v, V, p_base, attn, thr);
             }
             const unsigned m = __ballot_sync(0xffffffffu, keep);
             if (lane == 0) warp_cnt[wid] = __popc(m);

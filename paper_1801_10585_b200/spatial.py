@@ -255,7 +255,6 @@ class _RankCtx:
     hr: int
     x_ext: SparseMap
     ext_idx: torch.Tensor
-    ext_bases: List[int]
     n_from_left: int
     n_own: int
     n_from_right: int
@@ -268,10 +267,40 @@ class SpatialConv:
     planes across the ranks of `comm`. `planes` = the full grid's first dimension; the filter's
     ksize[0] // 2 halo planes must fit in every rank's range."""
 
-    def __init__(self, comm: Comm, planes: int):
+    def __init__(self, comm: Comm, planes: int, timing: bool = False):
         self.comm = comm
         self.planes = int(planes)
         self.ctx: List[_RankCtx] = []
+        # timing=True: CUDA events around every local rank's share of each phase (on the current
+        # stream); rank_ms() = the GPU time each rank's own work took (with LoopbackComm the
+        # ranks run one after the other, so this is what each GPU would spend computing)
+        self.timing = bool(timing)
+        self._ev: List[List[Tuple[torch.cuda.Event, torch.cuda.Event]]] = [[] for _ in comm.ranks]
+        self.halo_bytes = [0 for _ in comm.ranks]
+
+    def _t(self, j: int):
+        layer = self
+
+        class _Scope:
+            def __enter__(self):
+                if layer.timing:
+                    self.a = torch.cuda.Event(enable_timing=True)
+                    self.a.record()
+
+            def __exit__(self, *exc):
+                if layer.timing:
+                    b = torch.cuda.Event(enable_timing=True)
+                    b.record()
+                    layer._ev[j].append((self.a, b))
+
+        return _Scope()
+
+    def rank_ms(self) -> List[float]:
+        """Per local rank, the summed GPU time of its work since the last call (synchronises)."""
+        torch.cuda.synchronize()
+        out = [sum(a.elapsed_time(b) for a, b in ev) for ev in self._ev]
+        self._ev = [[] for _ in self.comm.ranks]
+        return out
 
     def ranges(self):
         return [plane_range(self.planes, self.comm.world, r) for r in self.comm.ranks]
@@ -286,57 +315,58 @@ class SpatialConv:
         for (a, e) in rng:
             if e - a < max(h, 1):
                 raise ValueError(f"spatial shard of {e - a} planes is thinner than the halo ({h})")
+        # 1. boundary slabs for the neighbours
         to_left, to_right, tl_idx, tr_idx = [], [], [], []
-        for x, r, (a, e) in zip(xs, self.comm.ranks, rng):
-            n = e - a
-            if r > 0 and h > 0:
-                m, i = extract_planes(x, 0, h, src_index=True)
-                m = m.exact()
-                to_left.append([m.keys, m.values])
-                tl_idx.append(i[:m.nnz_bound])
-            else:
-                to_left.append(None)
-                tl_idx.append(None)
-            if r < W - 1 and h > 0:
-                m, i = extract_planes(x, n - h, n, src_index=True)
-                m = m.exact()
-                to_right.append([m.keys, m.values])
-                tr_idx.append(i[:m.nnz_bound])
-            else:
-                to_right.append(None)
-                tr_idx.append(None)
+        for j, (x, r, (a, e)) in enumerate(zip(xs, self.comm.ranks, rng)):
+            with self._t(j):
+                tl, il = self._slab(x, 0, h) if r > 0 and h > 0 else (None, None)
+                tr, ir = self._slab(x, e - a - h, e - a) if r < W - 1 and h > 0 else (None, None)
+            to_left.append(tl)
+            tl_idx.append(il)
+            to_right.append(tr)
+            tr_idx.append(ir)
+            self.halo_bytes[j] += sum(12 * int(t[0].numel()) for t in (tl, tr) if t is not None)
         if h > 0 and W > 1:
             from_left, from_right = self.comm.exchange(to_left, to_right)
         else:
             from_left = from_right = [None] * len(xs)
+        # 2.-4. extended input, convolution, owned planes
         self.ctx = []
         ys = []
-        for j, (x, r, (a, e)) in enumerate(zip(xs, self.comm.ranks, rng)):
+        for j, (x, (a, e)) in enumerate(zip(xs, rng)):
             n = e - a
-            hl = h if from_left[j] is not None else 0
-            hr = h if from_right[j] is not None else 0
-            srcs = []
-            halo = lambda kv: SparseMap(kv[0], kv[1], x.batch, x.channels, (h,) + tuple(x.dims[1:]),
-                                        int(kv[0].numel()), None)
-            if hl:
-                srcs.append((halo(from_left[j]), 0, h, 0))
-            xe = x.exact()
-            srcs.append((xe, 0, n, hl))
-            if hr:
-                srcs.append((halo(from_right[j]), 0, h, hl + n))
-            x_ext, ext_idx, bases = slab_gather(srcs, hl + n + hr, src_index=True)
-            x_ext = x_ext.exact()
-            y_ext = sparse_conv_fwd(x_ext, w, bias, "none", 0)
-            y_own, _ = extract_planes(y_ext, hl, hl + n)
-            self.ctx.append(_RankCtx(a, e, hl, hr, x_ext, ext_idx, bases,
-                                     int(from_left[j][0].numel()) if hl else 0, xe.nnz_bound,
-                                     int(from_right[j][0].numel()) if hr else 0, tl_idx[j], tr_idx[j]))
+            fl, fr = from_left[j], from_right[j]
+            hl = h if fl is not None else 0
+            hr = h if fr is not None else 0
+            halo_dims = (h,) + tuple(x.dims[1:])
+            with self._t(j):
+                xe = x.exact()
+                srcs = []
+                if hl:
+                    srcs.append((SparseMap(fl[0], fl[1], x.batch, x.channels, halo_dims, int(fl[0].numel())), 0, h, 0))
+                srcs.append((xe, 0, n, hl))
+                if hr:
+                    srcs.append((SparseMap(fr[0], fr[1], x.batch, x.channels, halo_dims, int(fr[0].numel())), 0, h,
+                                 hl + n))
+                x_ext, ext_idx, _ = slab_gather(srcs, hl + n + hr, src_index=True)
+                x_ext = x_ext.exact()
+                y_ext = sparse_conv_fwd(x_ext, w, bias, "none", 0)
+                y_own, _ = extract_planes(y_ext, hl, hl + n)
+            self.ctx.append(_RankCtx(a, e, hl, hr, x_ext, ext_idx,
+                                     int(fl[0].numel()) if hl else 0, xe.nnz_bound, int(fr[0].numel()) if hr else 0,
+                                     tl_idx[j], tr_idx[j]))
             ys.append(y_own)
         if attn == "none":
             return ys
         return self._select(ys, attn, k)
 
+    def _slab(self, x: SparseMap, lo: int, hi: int):
+        m, i = extract_planes(x, lo, hi, src_index=True)
+        m = m.exact()
+        return [m.keys, m.values], i[:m.nnz_bound]
+
     def _select(self, ys: List[SparseMap], attn: str, k: int) -> List[SparseMap]:
+        """5. exact k-selection per (b, oc) over all ranks' owned outputs."""
         if k < 1:
             raise ValueError("attention needs k >= 1")
         nseg = ys[0].batch * ys[0].channels
@@ -345,14 +375,27 @@ class SpatialConv:
             plane *= int(d)
         if self.planes * plane > 2 ** 32:
             raise ValueError("the attention composite needs fewer than 2^32 positions per segment")
-        sts = [_select_init(nseg, k, y.values.device) for y in ys]
+        sts = []
+        for j, y in enumerate(ys):
+            with self._t(j):
+                sts.append(_select_init(nseg, k, y.values.device))
         for shift in range(56, -1, -8):
-            for y, st, c in zip(ys, sts, self.ctx):
-                _digit_hist(y, attn, c.a * plane, st, shift)
+            for j, (y, st, c) in enumerate(zip(ys, sts, self.ctx)):
+                with self._t(j):
+                    _digit_hist(y, attn, c.a * plane, st, shift)
             self.comm.allreduce_sum([st.hist for st in sts])
-            for st in sts:
-                _digit_pick(nseg, st, shift)
-        return [keep_ge(y, attn, c.a * plane, st.prefix)[0] for y, st, c in zip(ys, sts, self.ctx)]
+            for j, st in enumerate(sts):
+                with self._t(j):
+                    _digit_pick(nseg, st, shift)
+            # every rank holds the same summed histograms, hence the same settled flags: stop
+            # once every segment's threshold is exact (usually after the score's bytes)
+            if shift and not bool((sts[0].need >= 0).any()):
+                break
+        out = []
+        for j, (y, st, c) in enumerate(zip(ys, sts, self.ctx)):
+            with self._t(j):
+                out.append(keep_ge(y, attn, c.a * plane, st.prefix)[0])
+        return out
 
     def backward(self, xs: List[SparseMap], w: SparseFilter, ys: List[SparseMap], dys: List[torch.Tensor],
                  need_dx: bool = True):
@@ -361,14 +404,16 @@ class SpatialConv:
         nw = int(w.keys.numel())
         dev = xs[0].values.device
         parts, dxe = [], []
-        for x, y, dy, c in zip(xs, ys, dys, self.ctx):
-            ye = place_planes(y.exact(), c.hl, c.x_ext.dims[0])
-            ye = ye.exact()
-            buf = torch.zeros(nw + w.c_out, dtype=torch.float64, device=dev)
-            dx_ext = torch.empty(max(c.x_ext.nnz_bound, 1), dtype=torch.float32, device=dev) if need_dx else None
-            BwdPlan(c.x_ext, w, ye).f64(c.x_ext, w, ye, dy, dx_ext, buf[:nw], buf[nw:])
+        # 6. local backward against the owned kept outputs
+        for j, (y, dy, c) in enumerate(zip(ys, dys, self.ctx)):
+            with self._t(j):
+                ye = place_planes(y.exact(), c.hl, c.x_ext.dims[0]).exact()
+                buf = torch.zeros(nw + w.c_out, dtype=torch.float64, device=dev)
+                dx_ext = torch.empty(max(c.x_ext.nnz_bound, 1), dtype=torch.float32, device=dev) if need_dx else None
+                BwdPlan(c.x_ext, w, ye).f64(c.x_ext, w, ye, dy, dx_ext, buf[:nw], buf[nw:])
             parts.append(buf)
             dxe.append(dx_ext)
+        # 7. dw || dbias over ranks, one rounding
         self.comm.allreduce_sum(parts)
         dw = torch.empty(max(nw, 1), dtype=torch.float32, device=dev)
         db = torch.empty(w.c_out, dtype=torch.float32, device=dev)
@@ -376,26 +421,26 @@ class SpatialConv:
         round_f64(parts[0][nw:], db)
         if not need_dx:
             return [(None, dw[:nw], db) for _ in xs]
-        # route the halo inputs' partials back to their owners
+        # 7. the halo inputs' partials back to their owners
         dcats, to_left, to_right = [], [], []
-        for c, dx_ext in zip(self.ctx, dxe):
+        for j, (c, dx_ext) in enumerate(zip(self.ctx, dxe)):
             ntot = c.n_from_left + c.n_own + c.n_from_right
-            dcat = sparse_scatter_grad(c.ext_idx, dx_ext, c.x_ext.nnz_bound, ntot)
+            with self._t(j):
+                dcat = sparse_scatter_grad(c.ext_idx, dx_ext, c.x_ext.nnz_bound, ntot)
             dcats.append(dcat)
-            b_own = c.n_from_left
             to_left.append([dcat[:c.n_from_left]] if c.hl else None)
-            to_right.append([dcat[b_own + c.n_own:ntot]] if c.hr else None)
-        W = self.comm.world
-        if W > 1 and any(c.hl or c.hr for c in self.ctx):
+            to_right.append([dcat[c.n_from_left + c.n_own:ntot]] if c.hr else None)
+        if self.comm.world > 1 and any(c.hl or c.hr for c in self.ctx):
             from_left, from_right = self.comm.exchange(to_left, to_right)
         else:
             from_left = from_right = [None] * len(xs)
         out = []
         for j, c in enumerate(self.ctx):
-            dx = dcats[j][c.n_from_left:c.n_from_left + c.n_own].clone()
-            if from_left[j] is not None and c.to_left_idx is not None and c.to_left_idx.numel():
-                index_add(c.to_left_idx, from_left[j][0], dx)
-            if from_right[j] is not None and c.to_right_idx is not None and c.to_right_idx.numel():
-                index_add(c.to_right_idx, from_right[j][0], dx)
+            with self._t(j):
+                dx = dcats[j][c.n_from_left:c.n_from_left + c.n_own].clone()
+                if from_left[j] is not None and c.to_left_idx is not None and c.to_left_idx.numel():
+                    index_add(c.to_left_idx, from_left[j][0], dx)
+                if from_right[j] is not None and c.to_right_idx is not None and c.to_right_idx.numel():
+                    index_add(c.to_right_idx, from_right[j][0], dx)
             out.append((dx, dw[:nw], db))
         return out

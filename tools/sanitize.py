@@ -62,6 +62,16 @@ def main():
     co = torch.tensor([[1, 0, 2, 3], [0, 2, 3, 1], [1, 2, 0, 0]], dtype=torch.int64).cuda()
     kk = spc.encode_keys(co, 2, 3, (4, 4))
     spc.decode_keys(kk, 2, 3, (4, 4))
+    # spatial sharding (f4): halo assembly, owned-plane extraction, distributed select, dx routing
+    from paper_1801_10585_b200.spatial import LoopbackComm, SpatialConv, extract_planes
+    x = uniform_map(2, 3, (12, 10, 14), 0.08, 7020, values="dyadic")
+    w = sparse_filter(3, 4, (3, 3, 3), 0.5, 7021, values="dyadic")
+    X = spc.SparseMap.from_arrays(x.keys, x.values, x.batch, x.channels, x.dims)
+    W = spc.SparseFilter.from_arrays(w.keys, w.values, w.c_in, w.c_out, w.ksize)
+    layer = SpatialConv(LoopbackComm(3), 12)
+    xs = [extract_planes(X, a, e)[0].exact() for a, e in layer.ranges()]
+    ys = [y.exact() for y in layer.forward(xs, W, None, "magnitude", 200)]
+    layer.backward(xs, W, ys, [torch.ones(max(y.nnz_bound, 1), device="cuda")[:y.nnz_bound] for y in ys])
     torch.cuda.synchronize()
     print("sanitize workload done")
 
