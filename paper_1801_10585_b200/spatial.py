@@ -181,27 +181,32 @@ class LoopbackComm(Comm):
 
 
 class DistComm(Comm):
-    """One rank per process over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+    """One rank per process over torch.distributed (NCCL on GPUs, gloo in the CPU tests). With a
+    gloo group and device tensors the payloads are staged through host memory (gloo has no
+    device point-to-point): the multi-process tests on a single-GPU box use that."""
 
     def __init__(self, group=None):
         self.group = group
         self.world = dist.get_world_size(group)
         self.ranks = [dist.get_rank(group)]
+        self.host_staging = dist.get_backend(group) == "gloo"
 
     def _p2p(self, sends, recv_shapes):
         """sends: [(peer, tensor)], recv_shapes: [(peer, n, dtype)] -> received tensors."""
-        r = self.ranks[0]
+        stage = self.host_staging
         outs, ops = [], []
-        dev = None
         for peer, n, dt, dv in recv_shapes:
-            t = torch.empty(n, dtype=dt, device=dv)
+            t = torch.empty(n, dtype=dt, device="cpu" if stage else dv)
             outs.append(t)
             ops.append(dist.P2POp(dist.irecv, t, self._g(peer), self.group))
         for peer, t in sends:
-            ops.append(dist.P2POp(dist.isend, t.contiguous(), self._g(peer), self.group))
+            ops.append(dist.P2POp(dist.isend, t.contiguous().cpu() if stage else t.contiguous(), self._g(peer),
+                                  self.group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        if stage:
+            outs = [t.to(dv) for t, (_, _, _, dv) in zip(outs, recv_shapes)]
         return outs
 
     def _g(self, peer: int) -> int:
@@ -243,7 +248,12 @@ class DistComm(Comm):
         return [fl], [fr]
 
     def allreduce_sum(self, ts):
-        dist.all_reduce(ts[0], op=dist.ReduceOp.SUM, group=self.group)
+        if self.host_staging and ts[0].is_cuda:
+            h = ts[0].cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+            ts[0].copy_(h)
+        else:
+            dist.all_reduce(ts[0], op=dist.ReduceOp.SUM, group=self.group)
 
 
 # ------------------------------------------------------------------ the layer

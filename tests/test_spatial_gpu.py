@@ -153,3 +153,68 @@ def test_spatial_empty_shard_and_thin_shard_error(cuda_lib):
     thin = SpatialConv(LoopbackComm(8), dims[0])   # one plane per rank < halo of 2
     with pytest.raises(ValueError):
         thin.forward([extract_planes(X, a, e)[0].exact() for a, e in thin.ranges()], W5, None, "magnitude", 20)
+
+
+def _dist_worker(rank, world, port, q):
+    """One spatial rank per process (gloo with host staging; the kernels of each process run
+    independently on the one GPU): DistComm's real halo exchange and all-reduces."""
+    import os
+
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1801_10585_b200 as spc
+        from paper_1801_10585_b200.spatial import DistComm, SpatialConv, extract_planes
+
+        torch.cuda.set_device(0)
+        spc.load()
+        dims = (12, 10, 14)
+        x = uniform_map(2, 3, dims, 0.08, 7700, values="dyadic")
+        w = sparse_filter(3, 4, (3, 3, 3), 0.5, 7701, values="dyadic")
+        bias = bias_vector(4, 7702, values="dyadic")
+        X = spc.SparseMap.from_arrays(x.keys, x.values, x.batch, x.channels, x.dims)
+        W = spc.SparseFilter.from_arrays(w.keys, w.values, w.c_in, w.c_out, w.ksize)
+        bt = torch.from_numpy(bias).cuda()
+        k = 250
+        Y = spc.sparse_conv_fwd(X, W, bt, "magnitude", k).exact()
+        dy = torch.from_numpy(grad_values(Y.nnz_bound, 7703, values="dyadic")).cuda()
+        dX, dW, dB = spc.sparse_conv_bwd(X, W, Y, dy)
+        layer = SpatialConv(DistComm(), dims[0])
+        (a, e), = layer.ranges()
+        xr = extract_planes(X, a, e)[0].exact()
+        [y] = layer.forward([xr], W, bt, "magnitude", k)
+        y = y.exact()
+        ref, yi = extract_planes(Y, a, e, src_index=True)
+        ref = ref.exact()
+        [(dx, dw, db)] = layer.backward([xr], W, [y], [dy[yi[:ref.nnz_bound]].contiguous()])
+        _, xi = extract_planes(X, a, e, src_index=True)
+        ok = (torch.equal(y.keys, ref.keys) and torch.equal(y.values, ref.values)
+              and torch.equal(dx, dX[xi[:xr.nnz_bound]]) and torch.equal(dw, dW) and torch.equal(db, dB))
+        q.put((rank, bool(ok), int(y.nnz_bound)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_spatial_distcomm_processes(cuda_lib, world):
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dist_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in got), got
