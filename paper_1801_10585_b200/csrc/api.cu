@@ -261,6 +261,9 @@ FwdWs carve_fwd(Carver& c, const Geo& gx, const Geo& gy, const KGeo& kg, const F
         plan_fwd_sampling(gy, t, attn, &a);
         const size_t nt = (size_t)nseg * (size_t)a.ntile;
         if (a.nsamp > 0) a.hist = c.take<uint32_t>((size_t)nseg * kSelBins);
+        // fewer segments than SMs: the resolve's candidate histogram is split over several CTAs
+        // per segment (stream_resolve_hist_kernel) instead of one CTA reading the whole segment
+        if (attn != SPC_ATTN_NONE && nseg < num_sms()) a.rhist = c.take<uint32_t>((size_t)nseg * kSelBins);
         a.tlow = c.take<uint32_t>((size_t)nseg);
         a.cmax = c.take<uint32_t>((size_t)nseg);
         a.fail = c.take<int>((size_t)nseg);

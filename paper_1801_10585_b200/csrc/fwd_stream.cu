@@ -321,9 +321,13 @@ __global__ void __launch_bounds__(kSRThreads, 4) stream_resolve_kernel(FwdArgs a
         }
         return;
     }
+    // ---- histogram of the candidates' score digit (precomputed by stream_resolve_hist_kernel when
+    // the segments are fewer than the SMs)
+    if (a.rhist) {
+        for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) h[i] = a.rhist[s * kSelBins + i];
+    } else {
     for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) h[i] = 0;
     __syncthreads();
-    // ---- histogram of the candidates' score digit
     struct HistF {
         const float* cv; uint32_t* h; uint32_t tl; int sh1, attn, lane; const StreamGeo* g;
         __device__ void run(int t, uint32_t n) const {
@@ -339,6 +343,7 @@ __global__ void __launch_bounds__(kSRThreads, 4) stream_resolve_kernel(FwdArgs a
         }
     } hf{cval, h, tl, sh1, attn, lane, &g};
     for_candidates(a, s, hf);
+    }
     __syncthreads();
     // ---- bucket of the k-th from the top
     if (threadIdx.x < 32) {
@@ -599,6 +604,47 @@ __global__ void __launch_bounds__(32 * kSWWarps) stream_write_kernel(FwdArgs a, 
     }
 }
 
+// The resolve's candidate histogram with gridDim.y CTAs per segment (segments fewer than SMs):
+// the same early outs and digit as stream_resolve_kernel; CTA part takes tiles part, part + P, ...
+// (one warp per tile run), shared bins flushed to a.rhist with atomics.
+__global__ void __launch_bounds__(256) stream_resolve_hist_kernel(FwdArgs a, StreamGeo g, int pass) {
+    const int64_t s = blockIdx.x;
+    if (pass == 1 && !a.fail[s]) return;
+    const uint64_t n = a.cand_cur[s];
+    const uint64_t k = (uint64_t)a.k;
+    const bool tl0 = a.tlow[s] == 0u;
+    const bool fail = !tl0 && (a.attn == SPC_ATTN_NONE || n < k);
+    const bool keep_all = a.attn == SPC_ATTN_NONE || n <= k;
+    if (fail || keep_all || n <= (uint64_t)kSRCap) return;
+    __shared__ uint32_t h[kSelBins];
+    for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const uint32_t tl = a.tlow[s];
+    const uint32_t mxr = a.cmax[s] - tl;
+    const int sh1 = max(0, 32 - __clz(mxr) - 11);
+    const int attn = a.attn;
+    const float* cval = a.cval + s * g.V;
+    const uint32_t* tc = a.tcnt + s * a.ntile;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int P = gridDim.y;
+    for (int t = blockIdx.y + P * warp; t < a.ntile; t += P * nw) {
+        const uint32_t cnt = tc[t];
+        if (!cnt) continue;
+        const float* v = cval + tile_base(t, g.nty, g.TY, g.Y, g.Z);
+        for (uint32_t i0 = lane; i0 < cnt; i0 += 128) {
+            uint32_t vb[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) vb[q] = i0 + 32u * q < cnt ? __float_as_uint(v[i0 + 32u * q]) : 0u;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (i0 + 32u * q < cnt) atomicAdd(&h[(score_bits(vb[q], attn) - tl) >> sh1], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kSelBins; i += blockDim.x)
+        if (h[i]) atomicAdd(&a.rhist[s * kSelBins + i], h[i]);
+}
+
 cudaError_t launch_stream_find(const FwdArgs& a, cudaStream_t s) {
     const double f = (double)a.nsamp / (double)a.ntile;
     SPC_PHASE("fwd_find", s, 1);
@@ -608,7 +654,14 @@ cudaError_t launch_stream_find(const FwdArgs& a, cudaStream_t s) {
 
 cudaError_t launch_stream_resolve(const Geo& gy, const FwdTile& t, const FwdArgs& a, int pass, cudaStream_t s) {
     const StreamGeo g{t.nty, t.TY, gy.Y, gy.Z, gy.V};
-    SPC_PHASE(pass == 0 ? "fwd_resolve" : "fwd_resolve_redo", s, 1);
+    const bool split = a.rhist && gy.V > kSmallV;
+    SPC_PHASE(pass == 0 ? "fwd_resolve" : "fwd_resolve_redo", s, split ? 2 : 1);
+    if (split) {
+        cudaError_t e = cudaMemsetAsync(a.rhist, 0, (size_t)a.nseg * kSelBins * sizeof(uint32_t), s);
+        if (e != cudaSuccess) return e;
+        const int parts = (int)std::max<int64_t>(2, std::min<int64_t>(64, (int64_t)num_sms() * 4 / std::max<int64_t>(a.nseg, 1)));
+        stream_resolve_hist_kernel<<<dim3((unsigned)a.nseg, (unsigned)parts), 256, 0, s>>>(a, g, pass);
+    }
     if (gy.V <= kSmallV)
         stream_resolve_small_kernel<<<(unsigned)((a.nseg + kSmallWarps - 1) / kSmallWarps), 32 * kSmallWarps, 0, s>>>(a, g, pass);
     else

@@ -231,6 +231,8 @@ struct FwdArgs {
     int64_t nseg;                    // (b, oc) segments
     unsigned long long* seg_count;   // [nseg] support size
     uint32_t* hist;                  // [nseg * kSelBins]
+    uint32_t* rhist;                 // [nseg * kSelBins] resolve histogram built by several CTAs per
+                                     // segment (few segments: batch 1 on large grids), or null
     FwdSeg* seg;                     // [nseg]
     uint32_t* tile_def;              // [nseg * nchunk] entries kept outright per chunk
     uint32_t* tile_sel;              // [nseg * nchunk] selected candidates per chunk
