@@ -263,7 +263,12 @@ FwdWs carve_fwd(Carver& c, const Geo& gx, const Geo& gy, const KGeo& kg, const F
         if (a.nsamp > 0) a.hist = c.take<uint32_t>((size_t)nseg * kSelBins);
         // fewer segments than SMs: the resolve's candidate histogram is split over several CTAs
         // per segment (stream_resolve_hist_kernel) instead of one CTA reading the whole segment
-        if (attn != SPC_ATTN_NONE && nseg < num_sms()) a.rhist = c.take<uint32_t>((size_t)nseg * kSelBins);
+        if (attn != SPC_ATTN_NONE && nseg < num_sms()) {
+            a.rhist = c.take<uint32_t>((size_t)nseg * kSelBins);
+            a.rstate = c.take<ResolveState>((size_t)nseg);
+            a.rsurv = c.take<uint64_t>((size_t)nseg * 4096);
+            a.rsurv_n = c.take<uint32_t>((size_t)nseg);
+        }
         a.tlow = c.take<uint32_t>((size_t)nseg);
         a.cmax = c.take<uint32_t>((size_t)nseg);
         a.fail = c.take<int>((size_t)nseg);

@@ -407,6 +407,20 @@ __global__ void __launch_bounds__(kSRThreads, 4) stream_resolve_kernel(FwdArgs a
         bcnt = sh[2];
         __syncthreads();
     }
+    if (a.rhist) {   // split resolve: the collect runs on several CTAs per segment, then the select
+        if (threadIdx.x == 0) {
+            ResolveState r{};
+            r.pre = pre;
+            r.need = need;
+            r.B = B;
+            r.lo = lo;
+            r.pos = pos;
+            r.sh1 = sh1;
+            r.active = 1;
+            a.rstate[s] = r;
+        }
+        return;
+    }
     // ---- collect the survivors; per tile run count the entries ranked above them ("definite")
     struct CollectF {
         const float* cv; const uint32_t* cp; uint64_t* keys; uint32_t* sh_n; uint32_t* tdef;
@@ -645,6 +659,84 @@ __global__ void __launch_bounds__(256) stream_resolve_hist_kernel(FwdArgs a, Str
         if (h[i]) atomicAdd(&a.rhist[s * kSelBins + i], h[i]);
 }
 
+// Split resolve, collect: the survivors of the threshold bucket (K' >> pos == pre) appended to the
+// segment's global list, and per tile run the entries ranked above them (tile_def); CTA part
+// takes tiles part, part + P, ... (one warp per tile run), as stream_resolve_kernel's CollectF.
+__global__ void __launch_bounds__(256) stream_resolve_collect_kernel(FwdArgs a, StreamGeo g) {
+    const int64_t s = blockIdx.x;
+    const ResolveState r = a.rstate[s];
+    if (!r.active) return;
+    const uint32_t tl = a.tlow[s];
+    const int attn = a.attn;
+    const float* cv = a.cval + s * g.V;
+    const uint32_t* cp = a.cpos + s * g.V;
+    const uint32_t* tc = a.tcnt + s * a.ntile;
+    uint32_t* tdef = a.tile_def + s * a.ntile;
+    uint64_t* surv = a.rsurv + s * (int64_t)kSRCap;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int P = gridDim.y;
+    for (int t = blockIdx.y + P * warp; t < a.ntile; t += P * nw) {
+        const uint32_t n = tc[t];
+        if (!n) continue;
+        const uint32_t b0 = tile_base(t, g.nty, g.TY, g.Y, g.Z);
+        uint32_t def = 0;
+        for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            bool put = false;
+            uint64_t kp = 0;
+            if (i < n) {
+                const uint32_t sc = score_bits(__float_as_uint(cv[b0 + i]), attn);
+                const uint32_t dg = (sc - tl) >> r.sh1;
+                if (dg > r.B) {
+                    ++def;
+                } else if (dg == r.B) {
+                    kp = ((uint64_t)(sc - r.lo) << 32) | (uint64_t)(0xffffffffu - cp[b0 + i]);
+                    const uint64_t top = kp >> r.pos;
+                    if (top > r.pre) ++def;
+                    else put = top == r.pre;
+                }
+            }
+            const unsigned m = __ballot_sync(kFull, put);
+            if (m) {
+                uint32_t base = 0;
+                if (lane == __ffs(m) - 1) base = atomicAdd(&a.rsurv_n[s], (uint32_t)__popc(m));
+                base = __shfl_sync(kFull, base, __ffs(m) - 1);
+                if (put) {
+                    const uint32_t o = base + __popc(m & ((1u << lane) - 1u));
+                    if (o < (uint32_t)kSRCap) surv[o] = kp;
+                }
+            }
+        }
+        def = warp_sum(def);
+        if (lane == 0) tdef[t] = def;
+    }
+}
+
+// Split resolve, select: the k-th of the survivors (smem_select), per tile run the selected ones.
+__global__ void __launch_bounds__(kSRThreads) stream_resolve_select_kernel(FwdArgs a, StreamGeo g) {
+    const int64_t s = blockIdx.x;
+    const ResolveState r = a.rstate[s];
+    if (!r.active) return;
+    __shared__ uint32_t h[kSelBins];
+    __shared__ uint64_t keys[kSRCap];
+    __shared__ uint64_t sh[4];
+    const uint32_t ns = min(a.rsurv_n[s], (uint32_t)kSRCap);
+    for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) keys[i] = a.rsurv[s * (int64_t)kSRCap + i];
+    __syncthreads();
+    const uint64_t kps = smem_select(keys, ns, (uint32_t)r.need, h, sh);
+    uint32_t* tsel = a.tile_sel + s * a.ntile;
+    for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) {
+        const uint64_t kp = keys[i];
+        if (kp >= kps) atomicAdd(&tsel[tile_of(0xffffffffu - (uint32_t)kp, g)], 1u);
+    }
+    if (threadIdx.x == 0) {
+        FwdSeg st{};
+        st.keep_all = 0;
+        st.kstar = ((uint64_t)(r.lo + (uint32_t)(kps >> 32)) << 32) | (kps & 0xffffffffull);
+        a.seg[s] = st;
+    }
+}
+
 cudaError_t launch_stream_find(const FwdArgs& a, cudaStream_t s) {
     const double f = (double)a.nsamp / (double)a.ntile;
     SPC_PHASE("fwd_find", s, 1);
@@ -655,12 +747,18 @@ cudaError_t launch_stream_find(const FwdArgs& a, cudaStream_t s) {
 cudaError_t launch_stream_resolve(const Geo& gy, const FwdTile& t, const FwdArgs& a, int pass, cudaStream_t s) {
     const StreamGeo g{t.nty, t.TY, gy.Y, gy.Z, gy.V};
     const bool split = a.rhist && gy.V > kSmallV;
-    SPC_PHASE(pass == 0 ? "fwd_resolve" : "fwd_resolve_redo", s, split ? 2 : 1);
+    SPC_PHASE(pass == 0 ? "fwd_resolve" : "fwd_resolve_redo", s, split ? 4 : 1);
+    const int parts = (int)std::max<int64_t>(2, std::min<int64_t>(64, (int64_t)num_sms() * 4 / std::max<int64_t>(a.nseg, 1)));
     if (split) {
         cudaError_t e = cudaMemsetAsync(a.rhist, 0, (size_t)a.nseg * kSelBins * sizeof(uint32_t), s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(a.rstate, 0, (size_t)a.nseg * sizeof(ResolveState), s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(a.rsurv_n, 0, (size_t)a.nseg * sizeof(uint32_t), s);
         if (e != cudaSuccess) return e;
-        const int parts = (int)std::max<int64_t>(2, std::min<int64_t>(64, (int64_t)num_sms() * 4 / std::max<int64_t>(a.nseg, 1)));
         stream_resolve_hist_kernel<<<dim3((unsigned)a.nseg, (unsigned)parts), 256, 0, s>>>(a, g, pass);
+        stream_resolve_kernel<<<(unsigned)a.nseg, kSRThreads, 0, s>>>(a, g, pass);
+        stream_resolve_collect_kernel<<<dim3((unsigned)a.nseg, (unsigned)parts), 256, 0, s>>>(a, g);
+        stream_resolve_select_kernel<<<(unsigned)a.nseg, kSRThreads, 0, s>>>(a, g);
+        return cudaGetLastError();
     }
     if (gy.V <= kSmallV)
         stream_resolve_small_kernel<<<(unsigned)((a.nseg + kSmallWarps - 1) / kSmallWarps), 32 * kSmallWarps, 0, s>>>(a, g, pass);

@@ -211,6 +211,16 @@ struct FwdSeg {
     uint32_t b1;         // threshold digit (11 bits)
     int32_t keep_all;    // 1: keep every support entry
 };
+// Split resolve (few segments): the bucket / narrowing outcome of a segment, handed from
+// stream_resolve_kernel to the multi-CTA collect and the final select.
+struct ResolveState {
+    uint64_t pre;        // survivors: (K' >> pos) == pre
+    uint64_t need;       // survivors to select
+    uint32_t B, lo;      // threshold digit, its lowest score
+    int32_t pos, sh1;
+    int32_t active;      // 1: collect + select pending
+    int32_t pad;
+};
 struct FwdArgs {
     Keys xkeys;
     const int64_t* x_nnz_dev;        // device-side input count (or null: x_nnz)
@@ -233,6 +243,9 @@ struct FwdArgs {
     uint32_t* hist;                  // [nseg * kSelBins]
     uint32_t* rhist;                 // [nseg * kSelBins] resolve histogram built by several CTAs per
                                      // segment (few segments: batch 1 on large grids), or null
+    ResolveState* rstate;            // [nseg] (split resolve)
+    uint64_t* rsurv;                 // [nseg * 4096] survivors of the threshold bucket (split resolve)
+    uint32_t* rsurv_n;               // [nseg]
     FwdSeg* seg;                     // [nseg]
     uint32_t* tile_def;              // [nseg * nchunk] entries kept outright per chunk
     uint32_t* tile_sel;              // [nseg * nchunk] selected candidates per chunk

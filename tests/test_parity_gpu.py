@@ -1188,3 +1188,26 @@ def test_relu_pool_topk_32bit_keys(cuda_lib):
     X64 = X32.to_key_bits(64)
     np.testing.assert_array_equal(_keys_u64(X64.keys), x.keys)
     np.testing.assert_array_equal(host(spc.sparse_to_dense(X32)), host(spc.sparse_to_dense(X64)))
+
+
+@pytest.mark.parametrize("attn", ["magnitude", "raw"])
+def test_fwd_split_resolve_few_segments(cuda_lib, attn):
+    """Fewer segments than SMs with more than 4096 candidates per segment: the forward's resolve
+    runs split (multi-CTA candidate histogram and collect, then the per-segment select) -- same
+    kept set and values as the oracle's sort (R7)."""
+    import paper_1801_10585_b200 as spc
+
+    dims = (40, 44, 48)
+    x = uniform_map(1, 2, dims, 0.03, 9100, values="dyadic")
+    w = sparse_filter(2, 3, (3, 3, 3), 0.5, 9101, values="dyadic")
+    bias = bias_vector(3, 9102, values="dyadic")
+    k = int(0.06 * np.prod(dims))
+    X = spc.SparseMap.from_arrays(x.keys, x.values, x.batch, x.channels, x.dims)
+    W = spc.SparseFilter.from_arrays(w.keys, w.values, w.c_in, w.c_out, w.ksize)
+    Y = spc.sparse_conv_fwd(X, W, torch.from_numpy(bias).cuda(), attn, k, variant="scatter")
+    yk, yv = Y.trimmed()
+    a = ora.ATTN_MAGNITUDE if attn == "magnitude" else ora.ATTN_RAW
+    ok, ov, _, _ = ora.conv_fwd(x, w, bias, attn=a, k=k)
+    assert ok.shape[0] == 3 * k
+    assert np.array_equal(yk.cpu().numpy().view(np.uint64), ok)
+    assert np.array_equal(yv.cpu().numpy(), ov)
